@@ -1,0 +1,321 @@
+#!/usr/bin/env python
+"""Benchmark of the MAGUS batched replay on B200 (BASELINE.json metric: trace-samples/s and achieved
+HBM GB/s vs peak at 1/2/4/8 GPUs).  Prints ONE JSON line on rank 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+
+A step = one pass of the whole hot path over one batch: the replay kernel,
+the exact fix-up of speculative segments, the per-trace epilogue, the per-policy sums, the NCCL
+allreduce (N > 1) and the argmin, for BASELINE.json config 2 (4,096 traces x 100,000 samples,
+MAGUS default + static max) per GPU -- weak scaling, traces sharded by global id.
+
+`value` is device-timed with CUDA events (inputs resident in HBM, 1.64 GB per GPU >> 126 MB L2, so
+no flush is needed), max over ranks.  `e2e` is the same metric through magus_replay_run_host with
+pinned host buffers: the H2D copy of each step's traces and the D2H read of its results are inside
+the timed region.  `roofline` is the replay kernel's algorithmic HBM bytes (4 B per trace-sample)
+over its CUDA-event duration, against MEASURED_PEAKS.json.  `cpu_baseline` is the oracle (oracle/,
+test infrastructure, never tuned) on the host cores, on a bounded sample of the same workload.
+`--impl reference` times that oracle alone (the reference arm of this tier).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "trace-samples/s"
+UNIT = "samples/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="target CPU work of the oracle baseline")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--preroll-ms", type=float, default=600.0, help="untimed load before the timed region "
+                    "so the clock samples see the GPU under load")
+    return ap.parse_args()
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 50 ms while the GPU is loaded."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.rows, self.proc, self.t = [], None, None
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.t:
+            self.t.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if len(r) >= 8 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit()]
+        reasons = set()
+        for r in self.rows:
+            if len(r) < 8:
+                continue
+            for name, v in zip(["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"], r[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline(cfg, target_s):
+    """The oracle as it stands, on all host cores, over a bounded sample (the first n traces of the
+    workload, full length, all of the config's policies)."""
+    from oracle import oracle as O
+    ns = cfg["n_samples"]
+    pols = [O.Policy(**d) for d in cfg["policies"]]
+    cores = os.cpu_count() or 1
+
+    def timed(n):
+        tr, w = O.gen_traces(O.GenDesc(seed=cfg["seed"], n_traces=n, n_samples=ns, class_mix=cfg["class_mix"]))
+        t0 = time.perf_counter()
+        _, _, used = O.replay_batch(tr, w, pols, n_threads=0)
+        return time.perf_counter() - t0, used
+
+    n0 = min(cfg["n_traces"], cores)
+    t0, _ = timed(n0)
+    n = int(min(cfg["n_traces"], max(n0, n0 * target_s / max(t0, 1e-3))))
+    n = max(1, (n // cores) * cores) if n >= cores else n
+    dt, used = timed(n)
+    return {"value": n * ns / dt, "unit": UNIT, "cores": used, "kind": "oracle",
+            "sample": f"first {n} of {cfg['n_traces']} traces x {ns} samples x {len(pols)} policies "
+                      f"({cfg['name']}), {dt:.1f} s of wall time on {used} threads"}
+
+
+def run_reference(args, cfg):
+    """--impl reference: the oracle (this tier's reference arm) on the host cores; rank 0 only."""
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    ns = cfg["n_samples"]
+    pols = [O.Policy(**d) for d in cfg["policies"]]
+    cores = os.cpu_count() or 1
+    # per-step sample sized so that warmup + steps finish in ~2-3 minutes
+    per_step_s = max(0.5, 150.0 / max(1, args.steps + args.warmup))
+    n = min(cfg["n_traces"], cores)
+    tr, w = O.gen_traces(O.GenDesc(seed=cfg["seed"], n_traces=n, n_samples=ns,
+                                   class_mix=cfg["class_mix"]))
+    t0 = time.perf_counter()
+    O.replay_batch(tr, w, pols)
+    t1 = time.perf_counter() - t0
+    n = int(min(cfg["n_traces"], max(1, n * per_step_s / max(t1, 1e-3))))
+    n = max(1, (n // cores) * cores) if n >= cores else n
+    tr, w = O.gen_traces(O.GenDesc(seed=cfg["seed"], n_traces=n, n_samples=ns, class_mix=cfg["class_mix"]))
+    used = 1
+    for _ in range(args.warmup):
+        _, _, used = O.replay_batch(tr, w, pols)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        _, _, used = O.replay_batch(tr, w, pols)
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * sum(times) / len(times)
+    value = n * ns / (ms / 1e3)
+    sample = f"first {n} of {cfg['n_traces']} traces x {ns} samples x {len(pols)} policies per step ({cfg['name']})"
+    print(json.dumps({"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+                      "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                      "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+                      "config": {"workload": cfg["name"], "n_traces_per_step": n, "n_samples": ns,
+                                 "policies": len(pols)},
+                      "cpu_baseline": {"value": value, "unit": UNIT, "cores": used, "kind": "oracle", "sample": sample},
+                      "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
+          flush=True)
+
+
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+    from paper_2502_03796_b200 import magus as M
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n = cfg.get("per_gpu_traces", cfg["n_traces"])
+    ns = cfg["n_samples"]
+    stride = (n + 3) // 4 * 4
+    offset = rank * n                      # weak scaling: each rank owns its own n traces (global ids)
+    tr = torch.empty((ns, stride), dtype=torch.float32, device=dev)
+    w = torch.empty(n, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    M.gen_traces(cfg["seed"], n, ns, cfg["class_mix"], tr, w, trace_stride=stride, global_trace_offset=offset,
+                 stream=stream)
+    nccl_id = None
+    if world > 1:
+        obj = [M.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    pols = [M.Policy(**d) for d in cfg["policies"]]
+    R = M.Replay(n, ns, pols, M.Model(), trace_stride=stride, global_trace_offset=offset, rank=rank, world=world,
+                 nccl_id=nccl_id, flags=M.F_TIMING)
+    geo = R.geometry()
+    for _ in range(max(3, args.warmup)):
+        R.run(tr, w, stream)
+        R.results()
+    # untimed pre-roll so that clock samples are taken under load, then the timed region
+    sampler = ClockSampler(local)
+    t_end = time.perf_counter() + args.preroll_ms / 1e3
+    while time.perf_counter() < t_end:
+        for _ in range(20):
+            R.run(tr, w, stream)
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        R.run(tr, w, stream)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    tsum = R.timing_summary(args.steps)          # per-kernel CUDA events of the same K runs, same stream
+    res = R.results()
+    ms_t = torch.tensor([ms, tsum["replay_ms"]], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max, replay_ms_max = float(ms_t[0]), float(ms_t[1])
+    total_samples = n * ns * world
+    value = total_samples / (ms_max / 1e3)
+
+    # roofline of the dominant kernel (the replay): 4 algorithmic bytes per trace-sample per launch
+    peak, peak_src = peaks()
+    bytes_per_launch = 4.0 * n * ns
+    achieved = bytes_per_launch / (tsum["replay_ms"] / 1e3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_replay_summary.json")
+    if os.path.exists(prof):
+        try:
+            pj = json.load(open(prof))
+            if pj.get("config") == cfg["name"]:
+                traffic = pj.get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    e2e = None
+    if not args.no_e2e:
+        th = tr.cpu().pin_memory()
+        wh = w.cpu().pin_memory()
+        R.run_host(th, wh, stream)
+        R.results()
+        k_e2e = max(1, min(args.steps, 5))
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        for _ in range(k_e2e):
+            R.run_host(th, wh, stream)
+            R.results()                           # D2H of the step's totals + argmin (synchronising)
+        e2e_ms = 1e3 * (time.perf_counter() - t0) / k_e2e
+        e2e_t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(e2e_t[0])
+        e2e = {"value": total_samples / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms, "steps": k_e2e,
+               "h2d_bytes_per_step": int(th.numel() * 4 + wh.numel() * 4),
+               "d2h_bytes_per_step": int(len(pols) * M.N_TOTALS * 8 + 4 * 4),
+               "path": "magus_replay_run_host + magus_replay_results (pinned host buffers)"}
+        del th, wh
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, args.cpu_seconds)
+
+    n_smax = sum(1 for p in pols if p.kind == M.STATIC_MAX)
+    launches_per_step = geo["launch_groups"] + 1 + (1 if n_smax else 0) + 2
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["name"], "n_traces_per_gpu": n, "n_samples": ns, "policies": len(pols),
+                       "parallelism": f"trace-sharded x{world}" + (", NCCL allreduce of per-policy totals" if world > 1
+                                                                    else ""),
+                       "l2": "inputs 1.64 GB/GPU >> 126 MB L2; no flush needed" if ns * n * 4 > 4e8 else "L2-resident"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": traffic, "kernel": "magus_replay_kernel", "replay_ms": tsum["replay_ms"],
+                         "replay_ms_max_over_ranks": replay_ms_max, "bytes_per_launch": bytes_per_launch,
+                         "peak_source": peak_src},
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "clocks": clocks,
+            "gpu_launches": launches_per_step * args.steps,
+            "kernel_ms": {k: round(v, 5) for k, v in tsum.items()},
+            "segmentation": {"n_segments": res.n_segments, "warmup_ticks": res.warmup_ticks,
+                             "mismatched_segments": res.n_mismatched_segments, "fixup_rounds": res.fixup_rounds,
+                             "geometry": geo},
+            "argmin_policy": res.argmin_policy,
+        }
+        print(json.dumps(out), flush=True)
+    R.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    from paper_2502_03796_b200.configs import CONFIGS
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,217 @@
+/*
+ * include/magus_replay.h -- C ABI of the B200-native MAGUS batched replay.
+ *
+ * MAGUS (arXiv 2502.03796) is a periodic uncore-frequency control loop: read
+ * memory throughput, predict its trend from the first
+ * derivative over a FIFO window (Alg. 1), log whether a change was
+ * requested, detect frequent changes (Alg. 2), force the
+ * maximum uncore level while changes are frequent, otherwise execute the
+ * temporary decision, jumping directly to the bounds.
+ * This library replays that loop for many synthetic throughput traces and
+ * many policy-parameter points at once on a B200 and reports the paper's
+ * metrics (performance loss, package power saving, energy saving, EDP;
+ * P:297-304) against the static-max / Intel-default baselines (P:119-136,
+ * P:282).  The per-tick semantics, including every reading of the paper's
+ * silences, are DESIGN.md sections 2-3.
+ *
+ * Conventions
+ *  - Every call returns magus_status (0 = MAGUS_OK).  On failure
+ *    magus_replay_last_error(handle) (or magus_last_error() for calls without
+ *    a handle) names the problem; for MAGUS_ERR_CONFIG it names the violated
+ *    key.
+ *  - Handles are single-owner and not thread-safe; distinct
+ *    handles may be used concurrently from different threads.
+ *  - Device pointers are borrowed: they must stay valid and unmodified until
+ *    the stream passes the run's completion (magus_replay_results waits for
+ *    it).  The library owns all of its scratch and its NCCL communicator.
+ *  - There is no CPU fallback: without a CUDA device every compute call
+ *    returns MAGUS_ERR_CUDA.
+ *  - Layout of a trace set: fp32, time-major / trace-minor, element (t, j) at
+ *    trace[t * trace_stride + j]; trace_stride >= n_traces, trace_stride % 4
+ *    == 0 and the base 16-byte aligned (TMA 2-D tiles); w[j] fp32 is trace j's
+ *    compute_weight (A18).
+ */
+#ifndef MAGUS_REPLAY_H
+#define MAGUS_REPLAY_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MAGUS_ABI_VERSION 1
+
+typedef enum {
+    MAGUS_OK = 0,
+    MAGUS_ERR_INVALID_ARG = 1,  /* NULL where a pointer is required, negative sizes, bad dump window */
+    MAGUS_ERR_CONFIG = 2,       /* a policy/model invariant is violated; last_error names the key */
+    MAGUS_ERR_ALIGN = 3,        /* trace_stride % 4 != 0 or a trace base not 16-byte aligned */
+    MAGUS_ERR_TRACE = 4,        /* a sample is negative, NaN/Inf or > bw_max (err_trace/err_tick set) */
+    MAGUS_ERR_STATE = 5,        /* results before any run */
+    MAGUS_ERR_OOM = 6,          /* device allocation failed */
+    MAGUS_ERR_CUDA = 7,         /* CUDA runtime/driver error, or no CUDA device */
+    MAGUS_ERR_NCCL = 8          /* NCCL missing or a collective failed */
+} magus_status;
+
+typedef enum {
+    MAGUS_POLICY_MAGUS = 0,       /* Alg. 1 + Alg. 2 + override; starts at f_min */
+    MAGUS_POLICY_STATIC_MAX = 1,  /* uncore pinned at f_max; the savings baseline (DESIGN A21) */
+    MAGUS_POLICY_STATIC_MIN = 2,  /* uncore pinned at f_min */
+    MAGUS_POLICY_TDP_DEFAULT = 3  /* Intel default: lowered only when pkg+DRAM power nears TDP */
+} magus_policy_kind;
+
+/* One policy-parameter point (SPEC GovernorConfig). */
+typedef struct {
+    int32_t kind;                 /* magus_policy_kind */
+    int32_t deriv_ticks;          /* k in [1, 64]: direv_length = k * sample_period_s (DESIGN A2) */
+    double  inc_threshold;        /* GB/s per s, > 0 (A3-A4) */
+    double  dec_threshold;        /* GB/s per s, < 0 */
+    int32_t tune_log_capacity;    /* C in [1, 64]: length of uncore_tune_ls when full (A6) */
+    int32_t _reserved0;
+    double  high_freq_threshold;  /* (0, 1]; the paper's 0.6 */
+    double  tdp_w;                /* TDP_DEFAULT only: > 0 (A24) */
+    double  tdp_margin;           /* TDP_DEFAULT only: (0, 1), default 0.05 */
+} magus_policy;
+
+/* Platform / energy model (SPEC simsys S:316-323; only the two endpoint levels are ever used, A19). */
+typedef struct {
+    double  sample_period_s;      /* Delta > 0, default 0.1 (A1) */
+    double  f_min_ghz, f_max_ghz; /* 0 < f_min < f_max; 0.8 / 2.2 */
+    double  bw_max_gbps;          /* > 0, bandwidth at f_max */
+    int32_t bw_shape;             /* 0 Linear, 1 Saturating */
+    int32_t _reserved0;
+    double  bw_knee;              /* Saturating only, (0, 1] */
+    double  p_pkg_idle_w, p_core_active_w, p_uncore_min_w, p_uncore_max_w; /* >= 0, max >= min */
+    double  p_exponent;           /* >= 1 */
+    double  p_gpu_active_w;       /* >= 0: GPU power while the trace runs */
+    double  dram_w_per_gbps;      /* >= 0: DRAM power proxy, TDP predicate only (A20) */
+} magus_model;
+
+/* desc.flags */
+#define MAGUS_F_PER_TRACE_STATS 0x1u  /* fill magus_results.per_trace */
+#define MAGUS_F_DUMP_WORDS      0x2u  /* per-(trace,policy) 32-tick cmd/tune-flag words from the replay kernel */
+#define MAGUS_F_DUMP_DECISIONS  0x4u  /* per-tick code bytes (DESIGN A27) for a window of traces */
+#define MAGUS_F_TIMING          0x8u  /* record CUDA events around each kernel (magus_replay_kernel_times) */
+
+typedef struct {
+    int32_t n_traces;             /* local traces in this rank's shard, >= 0 */
+    int32_t n_samples;            /* ticks per trace, >= 0 */
+    int64_t trace_stride;         /* floats between consecutive time rows; >= n_traces, % 4 == 0 */
+    int64_t global_trace_offset;  /* global id of local trace 0 (digests are per global id) */
+    int32_t n_policies;           /* >= 1 */
+    int32_t _reserved0;
+    const magus_policy* policies; /* [n_policies], copied at create */
+    magus_model model;
+    int32_t rank, world;          /* world == 1 -> no NCCL; world > 1 needs nccl_unique_id */
+    const void* nccl_unique_id;   /* 128 bytes from magus_nccl_unique_id on rank 0, broadcast by the caller */
+    uint32_t flags;               /* MAGUS_F_* */
+    int32_t dump_first_trace, dump_n_traces;   /* MAGUS_F_DUMP_DECISIONS window (local ids) */
+    int32_t tuning_segments;      /* 0 = automatic time segmentation; else the segment count (tests) */
+    int32_t tuning_warmup;        /* 0 = automatic warm-up ticks; else the warm-up (multiple of 32) */
+} magus_replay_desc;
+
+/* Per-policy totals (fp64), after the cross-rank allreduce. Index with MAGUS_TOT_*. */
+enum {
+    MAGUS_TOT_E = 0, MAGUS_TOT_E_PKG, MAGUS_TOT_T, MAGUS_TOT_EDP, MAGUS_TOT_SLOWDOWN,
+    MAGUS_TOT_ENERGY_SAVING, MAGUS_TOT_EDP_SAVING, MAGUS_TOT_N_HI, MAGUS_TOT_N_THR,
+    MAGUS_TOT_TRANSITIONS, MAGUS_TOT_TUNE_EVENTS, MAGUS_TOT_LOCK_TICKS, MAGUS_TOT_N_TRACES,
+    MAGUS_N_TOTALS
+};
+
+/* One (trace, policy) record; all times in s, energies in J. */
+typedef struct {
+    int64_t  n_hi, n_thr, transitions, tune_events, lock_ticks;
+    double   T, E_pkg, E, EDP, slowdown, energy_saving, edp_saving, pkg_power_saving;
+    uint64_t digest;
+} magus_trace_stats;
+
+/* Caller-owned host arrays; a NULL member is skipped. */
+typedef struct {
+    double*            policy_totals;  /* [n_policies][MAGUS_N_TOTALS] */
+    magus_trace_stats* per_trace;      /* [n_traces][n_policies] (needs MAGUS_F_PER_TRACE_STATS) */
+    uint32_t*          words;          /* [n_policies][n_traces][n_blocks][2] = {w_cmd, w_ev}, n_blocks =
+                                          ceil(n_samples/32) (needs MAGUS_F_DUMP_WORDS) */
+    uint8_t*           decisions;      /* [n_samples][dump_n_traces][n_policies] (needs MAGUS_F_DUMP_DECISIONS) */
+    int32_t  argmin_policy;            /* out: argmin over policies of total EDP, ties -> lowest index (A23) */
+    int32_t  err_trace;                /* out: first local trace with an invalid sample, else -1 */
+    int64_t  err_tick;                 /* out: its first invalid tick, else -1 */
+    int32_t  n_segments;               /* out: time segments per trace used by the run */
+    int32_t  warmup_ticks;             /* out: warm-up ticks per speculative segment */
+    int64_t  n_mismatched_segments;    /* out: speculative segments whose entry state was wrong (re-run) */
+    int32_t  fixup_rounds;             /* out: max rounds of the exact fix-up over all chains */
+    int32_t  _reserved0;
+} magus_results;
+
+/* ---- calls ---------------------------------------------------------------------------- */
+
+typedef struct magus_replay magus_replay_t;
+
+/* Writes 128 bytes (an ncclUniqueId) for world > 1.  MAGUS_ERR_NCCL if NCCL cannot be loaded. */
+magus_status magus_nccl_unique_id(void* out128);
+
+/* Seeded synthetic traces: writes trace[n_samples][trace_stride] (padding
+ * columns zero) and w[n_traces] on the device, stream-ordered.  Counter-based: a trace's bytes depend
+ * only on (seed, global_trace_offset + j, t), so shards and strides never change them. */
+typedef struct {
+    uint64_t seed;
+    int32_t  n_traces, class_mix;       /* 0 cfg2, 1 cfg3/4, 2 cfg5 adversarial, 3 cfg1 concatenated */
+    int64_t  n_samples, trace_stride, global_trace_offset;
+    float    noise_amp, _reserved0;     /* a, default 0.002 */
+    double   bw_max_gbps;               /* clamp bound */
+} magus_gen_desc;
+magus_status magus_gen_traces(const magus_gen_desc* desc, float* d_trace, float* d_w, void* cuda_stream);
+
+/* Validates desc (every invariant of section "magus_policy"/"magus_model"; A17), derives the
+ * exact-equivalent thresholds, allocates device scratch, creates the NCCL communicator when
+ * world > 1 (collective: every rank must call it).  *out is NULL on failure. */
+magus_status magus_replay_create(const magus_replay_desc* desc, magus_replay_t** out);
+
+/* Enqueues the whole replay on cuda_stream (a cudaStream_t; NULL = legacy default stream):
+ * replay kernel, exact fix-up of speculative time segments, per-trace epilogue, per-policy
+ * sums, the cross-rank allreduce (world > 1) and the argmin.  d_trace/d_w are device pointers
+ * in the layout above.  Asynchronous; errors in the trace content surface in results(). */
+magus_status magus_replay_run(magus_replay_t* h, const float* d_trace, const float* d_w, void* cuda_stream);
+
+/* Same, from host buffers (pinned for full speed): copies them into library-owned device memory
+ * on cuda_stream, then runs.  The host buffers may be reused once results() returns. */
+magus_status magus_replay_run_host(magus_replay_t* h, const float* trace, const float* w, void* cuda_stream);
+
+/* Waits for the last run and copies its results into caller-owned host arrays.
+ * Returns MAGUS_ERR_TRACE (with err_trace/err_tick) if a sample was invalid. */
+magus_status magus_replay_results(magus_replay_t* h, magus_results* out);
+
+/* Device milliseconds of the last run's kernels (needs MAGUS_F_TIMING; waits for the run):
+ * out[0] replay kernel, out[1] fix-up + epilogue, out[2] totals + allreduce + argmin, out[3] whole run. */
+magus_status magus_replay_kernel_times(magus_replay_t* h, float out_ms[4]);
+
+/* Same four intervals averaged over the last n_last runs (at most 256 are kept), e.g. the K runs of a
+ * timed benchmark region.  Waits for the last run. */
+magus_status magus_replay_timing_summary(magus_replay_t* h, int32_t n_last, float out_ms[4]);
+
+void         magus_replay_destroy(magus_replay_t* h);
+const char*  magus_replay_last_error(const magus_replay_t* h);
+const char*  magus_last_error(void);   /* errors of calls that have no handle (create, gen, unique id) */
+
+/* Host-only helper (no GPU needed): the exact-equivalent thresholds the kernels compare against,
+ * derived by evaluating the paper's predicates on the host:
+ *   out_d[0] = d*_inc  (max d with fl(d/L) <= inc_threshold:  Alg.1 returns 1  iff d > d*_inc)
+ *   out_d[1] = d*_dec  (min d with fl(d/L) >= dec_threshold:  Alg.1 returns -1 iff d < d*_dec)
+ *   out_d[2] = L = k * sample_period_s,  out_d[3] = P_lo,  out_d[4] = P_hi
+ *   out_f[0] = B_lo, out_f[1] = B_hi,  out_f[2] = a*_lo, out_f[3] = a*_hi (TDP: cmd = f_min iff A >= a*[f])
+ *   out_i[0] = s_min   (min s with fl(s/C) >= high_freq_threshold: Alg.2 true iff popcount >= s_min)  */
+magus_status magus_derive_thresholds(const magus_policy* p, const magus_model* m,
+                                     double out_d[5], float out_f[4], int32_t out_i[1]);
+
+int32_t magus_abi_version(void);
+
+/* Diagnostics: the launch geometry chosen at create: out = {n_segments, segment_len, warmup_ticks,
+ * tile_groups_per_cta, policy_warps_per_group, trace_blocks, policy_blocks, ctas, threads_per_cta,
+ * smem_bytes, lane_policies, launch_groups}. */
+magus_status magus_replay_geometry(const magus_replay_t* h, int32_t out[12]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MAGUS_REPLAY_H */

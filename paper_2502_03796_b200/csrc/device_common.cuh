@@ -1,0 +1,258 @@
+// device_common.cuh -- the per-tick MAGUS recurrence as device code, shared by the replay kernel
+// (4 chains per lane, unrolled) and the fix-up / re-simulation kernels (scalar).
+//
+// One chain = one (trace, policy) recurrence.  Per tick (Alg. 1
+// P:197-222, Alg. 2, S3.2 P:243, S6.1 P:318):
+//   A = min(D, B[f]); thr = A < D                                          (DESIGN A14)
+//   d = (double)A - (double)A_{t-k};   +1 iff d > d*_inc, -1 iff d < d*_dec  (Alg. 1, exact-equivalent
+//                                       thresholds derived on the host from fl(d / (k*Delta)), section 8)
+//   tune flag = signal != 0 pushed into a C-bit shift register               (A7, A12)
+//   lock = log full && popcount(log) >= s_min                                (Alg. 2, s_min from fl(s/C), A8)
+//   cmd = lock ? HI : +1 ? HI : -1 ? LO : f                                   (A9)
+// The hot loop keeps only sufficient statistics for the energy model (section 8): ticks at HI,
+// throttled ticks, the fp64 sum of throttled demand, transitions, tune flags, lock ticks and the
+// 64-bit decision digest (section 5).
+#pragma once
+#include <cstdint>
+
+namespace magus {
+
+enum : int32_t { LANE_MAGUS = 0, LANE_STATIC_MIN = 2, LANE_TDP = 3, LANE_VALIDATE = 4 };
+enum : int32_t { KMAX_GENERIC = 64 };
+
+// one policy as the kernels see it (host-derived, section 8)
+struct DevPolicy {
+    int32_t kind;          // LANE_*
+    int32_t k;             // derivative window in ticks
+    int32_t C;             // tune-log capacity
+    int32_t s_min;         // Alg. 2: lock iff popcount >= s_min (C+1 = never)
+    uint64_t logmask;      // low C bits
+    double dinc, ddec;     // Alg. 1: +1 iff d > dinc, -1 iff d < ddec
+    float astar_lo, astar_hi;   // TDP: cmd = LO iff A >= astar[f]
+    int32_t f0;            // initial level at t = 0 (A10)
+    int32_t guess_f;       // level guessed at a speculative segment start
+    int32_t policy_index;  // index in the user's policy array
+    int32_t _pad;
+};
+
+// run-wide constants and scratch pointers
+struct ReplayParams {
+    int32_t n_traces, n_samples;
+    int32_t n_lane;        // Q lane policies (state / statistics arrays are indexed by lane 0..Q-1)
+    int32_t q_base, nq;    // lanes covered by the current replay launch (all of one chain kind)
+    int32_t n_seg, seg_len, warmup;
+    int32_t n_groups;      // ceil(n_traces / 128)
+    int32_t ng, npw;       // CTA: ng tile groups x npw policy warps (+1 producer warp)
+    int32_t n_tblocks, n_pblocks;
+    int32_t kr;            // ring floats stored per chain state (max k over MAGUS lane policies)
+    int32_t n_blocks;      // ceil(n_samples / 32)
+    float B_lo, B_hi;
+    uint32_t bwbits;       // bit pattern of the largest fp32 <= bw_max
+    int32_t _pad0;
+    int64_t trace_stride;
+    const DevPolicy* pol;  // [n_lane]
+    // chain states, SoA: [e (0 entry, 1 exit)][q][s][j]
+    uint8_t* st_f;
+    uint64_t* st_log;
+    float* st_ring;        // [e][q][s][r < kr][j]
+    // per (q, s, j) statistics of the segment's own ticks
+    uint32_t* s_nhi;
+    uint32_t* s_nthr;
+    uint32_t* s_trans;
+    uint32_t* s_ev;
+    uint32_t* s_lock;
+    uint32_t* s_vmax;
+    double* s_sthr;
+    uint64_t* s_digest;
+    uint32_t* words;       // optional [q][j][n_blocks][2]
+};
+
+__host__ __device__ __forceinline__ int64_t st_idx(const ReplayParams& p, int e, int q, int s, int j) {
+    return ((int64_t)(e * p.n_lane + q) * p.n_seg + s) * p.n_traces + j;
+}
+__host__ __device__ __forceinline__ int64_t ring_idx(const ReplayParams& p, int e, int q, int s, int r, int j) {
+    return (((int64_t)(e * p.n_lane + q) * p.n_seg + s) * p.kr + r) * p.n_traces + j;
+}
+__host__ __device__ __forceinline__ int64_t stat_idx(const ReplayParams& p, int q, int s, int j) {
+    return ((int64_t)q * p.n_seg + s) * p.n_traces + j;
+}
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {   // splitmix64 finaliser
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+static constexpr uint64_t kPhi = 0x9E3779B97F4A7C15ULL;
+
+template <bool LOG64>
+struct LogWord { using T = uint32_t; };
+template <>
+struct LogWord<true> { using T = uint64_t; };
+
+template <bool LOG64>
+__device__ __forceinline__ uint32_t popc_log(typename LogWord<LOG64>::T v) {
+    if constexpr (LOG64) return (uint32_t)__popcll(v);
+    else return (uint32_t)__popc(v);
+}
+
+// Ring of the last k observations, newest first.  K > 0: fp64 registers (k <= 8, unrolled);
+// K == 0: generic runtime k <= 64, fp32 circular buffer in local memory.
+template <int K>
+struct Ring {
+    double v[K];
+    __device__ __forceinline__ double oldest(int) const { return v[K - 1]; }
+    __device__ __forceinline__ void push(double a, int) {
+#pragma unroll
+        for (int i = K - 1; i > 0; --i) v[i] = v[i - 1];
+        v[0] = a;
+    }
+    __device__ __forceinline__ float get(int i, int) const { return (float)v[i]; }      // i = 0 newest
+    // store the k values (newest first) to dst[i * stride]; compile-time indices keep v[] in registers
+    __device__ __forceinline__ void store_all(float* dst, int, int64_t stride) const {
+#pragma unroll
+        for (int i = 0; i < K; ++i) dst[i * stride] = (float)v[i];
+    }
+    __device__ __forceinline__ bool same(const Ring& o, int) const {
+        bool eq = true;
+#pragma unroll
+        for (int i = 0; i < K; ++i) eq = eq && (__double_as_longlong(v[i]) == __double_as_longlong(o.v[i]));
+        return eq;
+    }
+    __device__ __forceinline__ void set_all(const float* src, int, int64_t stride) {
+#pragma unroll
+        for (int i = 0; i < K; ++i) v[i] = (double)src[i * stride];
+    }
+    __device__ __forceinline__ void clear(int) {
+#pragma unroll
+        for (int i = 0; i < K; ++i) v[i] = 0.0;
+    }
+};
+
+template <>
+struct Ring<0> {
+    float v[KMAX_GENERIC];
+    int head;   // index of the newest entry
+    __device__ __forceinline__ double oldest(int k) const {
+        int i = head - (k - 1);
+        if (i < 0) i += k;
+        return (double)v[i];
+    }
+    __device__ __forceinline__ void push(double a, int k) {
+        head = (head + 1 == k) ? 0 : head + 1;
+        v[head] = (float)a;
+    }
+    __device__ __forceinline__ float get(int i, int k) const {
+        int x = head - i;
+        if (x < 0) x += k;
+        return v[x];
+    }
+    __device__ __forceinline__ void store_all(float* dst, int k, int64_t stride) const {
+        for (int i = 0; i < k; ++i) dst[i * stride] = get(i, k);
+    }
+    __device__ __forceinline__ bool same(const Ring& o, int k) const {
+        for (int i = 0; i < k; ++i)
+            if (__float_as_uint(get(i, k)) != __float_as_uint(o.get(i, k))) return false;
+        return true;
+    }
+    __device__ __forceinline__ void set_all(const float* src, int k, int64_t stride) {
+        head = k - 1;   // newest at k-1, oldest at 0
+        for (int i = 0; i < k; ++i) v[k - 1 - i] = src[i * stride];
+    }
+    __device__ __forceinline__ void clear(int k) {
+        head = 0;
+        for (int i = 0; i < k; ++i) v[i] = 0.0f;
+    }
+};
+
+// State of one MAGUS chain between ticks.
+template <int K, bool LOG64>
+struct MagusState {
+    using LogT = typename LogWord<LOG64>::T;
+    uint32_t f;     // level in effect for the next tick (0 LO, 1 HI)
+    LogT evh;       // tune-flag history, newest at bit 0; the log is the low C bits
+    Ring<K> ring;
+};
+
+// Per-tick outputs needed by the accumulators.
+struct TickOut {
+    uint32_t cmd, ev, hf, thr, sig;   // sig: 1 = +1, 2 = -1, 0 = hold / not ready
+};
+
+// One MAGUS tick.  SLOW: the chain is within k + C - 1 ticks of its start, `ready` / `full` say
+// whether Alg. 1 has k+1 samples and whether the log holds C flags (A7, A8); both are uniform
+// across the warp because every chain of a warp starts at the same tick.
+template <int K, bool LOG64, bool SLOW>
+__device__ __forceinline__ TickOut magus_tick(MagusState<K, LOG64>& s, float D, const DevPolicy& pol,
+                                              float B_lo, float B_hi, bool ready, bool full) {
+    TickOut o;
+    const float B = s.f ? B_hi : B_lo;
+    const float A = fminf(D, B);
+    o.thr = D > B;
+    const double Ad = (double)A;
+    const double d = Ad - s.ring.oldest(pol.k);
+    s.ring.push(Ad, pol.k);
+    bool inc = d > pol.dinc;
+    bool dec = d < pol.ddec;
+    if (SLOW && !ready) { inc = false; dec = false; }
+    const uint32_t ev = (inc || dec) ? 1u : 0u;
+    s.evh = (s.evh << 1) | (typename LogWord<LOG64>::T)ev;
+    const uint32_t cnt = popc_log<LOG64>(s.evh & (typename LogWord<LOG64>::T)pol.logmask);
+    bool hf = cnt >= (uint32_t)pol.s_min;
+    if (SLOW && !full) hf = false;
+    const uint32_t cmd = (hf || inc || (s.f && !dec)) ? 1u : 0u;
+    o.cmd = cmd;
+    o.ev = ev;
+    o.hf = hf ? 1u : 0u;
+    o.sig = inc ? 1u : (dec ? 2u : 0u);
+    s.f = cmd;
+    return o;
+}
+
+// Intel default: cmd = LO iff pkg + DRAM power >= (1 - m) TDP, i.e. A >= a*[f] (section 8).
+__device__ __forceinline__ TickOut tdp_tick(uint32_t& f, float D, const DevPolicy& pol, float B_lo, float B_hi) {
+    TickOut o;
+    const float B = f ? B_hi : B_lo;
+    const float A = fminf(D, B);
+    o.thr = D > B;
+    const float as = f ? pol.astar_hi : pol.astar_lo;
+    o.cmd = (A >= as) ? 0u : 1u;
+    o.ev = 0;
+    o.hf = 0;
+    o.sig = 0;
+    f = o.cmd;
+    return o;
+}
+
+// Per-(chain, segment) statistics accumulated over the segment's own ticks.
+struct SegStats {
+    uint32_t nhi, nthr, trans, ev, lock, vmax;
+    double sthr;
+    uint64_t digest;
+    __device__ __forceinline__ void zero() {
+        nhi = nthr = trans = ev = lock = vmax = 0;
+        sthr = 0.0;
+        digest = 0;
+    }
+};
+
+// Fold one 32-tick block [bt0, bt0 + n): `wcmd` holds the block's cmd bits (newest at bit 0, plus the
+// previous tick's cmd above them), `ew` the tune flags (same alignment), fstart the level at bt0.
+__device__ __forceinline__ void fold_block(SegStats& st, uint32_t wcmd, uint32_t ew, uint32_t fstart, int n,
+                                           int64_t block_index, uint32_t* words_out) {
+    const uint32_t mask = (n >= 32) ? 0xFFFFFFFFu : ((1u << n) - 1u);
+    const uint32_t cw = wcmd & mask;
+    const uint32_t lw = ((wcmd >> 1) & (mask >> 1)) | (fstart << (n - 1));   // level in effect per tick
+    const uint32_t evw = ew & mask;
+    st.trans += __popc(cw ^ lw);
+    st.nhi += __popc(lw);
+    st.ev += __popc(evw);
+    const int sh = 32 - n;
+    const uint32_t wc = cw << sh, we = evw << sh;   // tick bt0 + i at bit 31 - i; partial block zero-padded
+    st.digest += mix64((((uint64_t)wc << 32) | (uint64_t)we) ^ ((uint64_t)block_index * kPhi));
+    if (words_out) {
+        words_out[0] = wc;
+        words_out[1] = we;
+    }
+}
+
+}  // namespace magus

@@ -1,0 +1,899 @@
+// magus_replay.cu -- host side of the C ABI (include/magus_replay.h): validation, exact-equivalent
+// threshold derivation, launch geometry, TMA descriptors, kernel launches, NCCL allreduce, results.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/magus_replay.h"
+#include "post_kernels.cuh"
+#include "replay_kernel.cuh"
+
+using namespace magus;
+
+static_assert(sizeof(TraceRec) == sizeof(magus_trace_stats), "TraceRec must mirror magus_trace_stats");
+static_assert(kNTot == MAGUS_N_TOTALS, "totals width");
+
+namespace {
+
+constexpr int kTC = 16;       // ticks per TMA stage (one 8 KB [16 x 128] fp32 tile)
+constexpr int kNStage = 3;    // stages per tile group
+using Smem = ReplaySmem<kTC, kNStage>;
+typedef void (*ReplayKernel)(CUtensorMap, ReplayParams);
+
+// chain kind of a lane policy -> its kernel instantiation (one register allocation per kind)
+int ticker_key(const DevPolicy& q) {
+    if (q.kind == LANE_MAGUS) {
+        const int l64 = q.C > 32 ? 1 : 0;
+        int k = q.k <= 8 ? q.k : 0;
+        if (l64 && (k == 3 || k == 5 || k == 6 || k == 7)) k = 0;
+        return 100 * l64 + k;   // 0..8, 100..108
+    }
+    return 1000 + q.kind;       // TDP, STATIC_MIN, VALIDATE
+}
+
+template <class T>
+ReplayKernel K() { return (ReplayKernel)magus_replay_kernel<T, kTC, kNStage>; }
+
+ReplayKernel replay_kernel_for(int key) {
+    switch (key) {
+        case 0: return K<MagusTicker<0, false>>();
+        case 1: return K<MagusTicker<1, false>>();
+        case 2: return K<MagusTicker<2, false>>();
+        case 3: return K<MagusTicker<3, false>>();
+        case 4: return K<MagusTicker<4, false>>();
+        case 5: return K<MagusTicker<5, false>>();
+        case 6: return K<MagusTicker<6, false>>();
+        case 7: return K<MagusTicker<7, false>>();
+        case 8: return K<MagusTicker<8, false>>();
+        case 100: return K<MagusTicker<0, true>>();
+        case 101: return K<MagusTicker<1, true>>();
+        case 102: return K<MagusTicker<2, true>>();
+        case 104: return K<MagusTicker<4, true>>();
+        case 108: return K<MagusTicker<8, true>>();
+        case 1000 + LANE_TDP: return K<TdpTicker>();
+        case 1000 + LANE_STATIC_MIN: return K<StaticMinTicker<false>>();
+        default: return K<StaticMinTicker<true>>();
+    }
+}
+
+// one replay launch: the lane policies [q_base, q_base + nq) share a chain kind
+struct LaunchGroup {
+    ReplayKernel kernel;
+    int key, q_base, nq, ng, npw, n_tblocks, n_pblocks, n_ctas, threads;
+    size_t smem;
+};
+
+thread_local std::string g_error;
+
+// ------------------------------------------------------------------------------------ NCCL (dlopen)
+struct NcclApi {
+    bool loaded = false;
+    void* handle = nullptr;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+    static NcclApi api;
+    if (!api.loaded) {
+        api.loaded = true;
+        api.handle = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!api.handle) api.handle = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (api.handle) {
+            api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(api.handle, "ncclGetUniqueId");
+            api.CommInitRank = (decltype(api.CommInitRank))dlsym(api.handle, "ncclCommInitRank");
+            api.AllReduce = (decltype(api.AllReduce))dlsym(api.handle, "ncclAllReduce");
+            api.CommDestroy = (decltype(api.CommDestroy))dlsym(api.handle, "ncclCommDestroy");
+            api.GetErrorString = (decltype(api.GetErrorString))dlsym(api.handle, "ncclGetErrorString");
+        }
+    }
+    return api;
+}
+bool nccl_ok() {
+    NcclApi& a = nccl();
+    return a.handle && a.GetUniqueId && a.CommInitRank && a.AllReduce && a.CommDestroy;
+}
+
+// ------------------------------------------------------------------------------------ TMA encode
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+PFN_encodeTiled get_encode() {
+    static PFN_encodeTiled fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_encodeTiled)p;
+        cudaGetLastError();
+    }
+    return fn;
+}
+
+// ------------------------------------------------------------------------------------ exact thresholds
+// Ordered integer keys of doubles / floats: key order == numeric order (with -0 just below +0).
+inline uint64_t dkey(double x) {
+    uint64_t b;
+    std::memcpy(&b, &x, 8);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
+}
+inline double dval(uint64_t k) {
+    uint64_t b = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFULL) : ~k;
+    double x;
+    std::memcpy(&x, &b, 8);
+    return x;
+}
+inline float fval(uint32_t b) {
+    float x;
+    std::memcpy(&x, &b, 4);
+    return x;
+}
+inline uint32_t fbits(float x) {
+    uint32_t b;
+    std::memcpy(&b, &x, 4);
+    return b;
+}
+
+// Alg. 1: +1 iff fl(d / L) > inc.  fl(./L) is monotone, so {d : +1} = {d > d*} with
+// d* = max{d : fl(d/L) <= inc}; found by bisection over the ordered doubles, evaluating the
+// predicate exactly as the oracle writes it.
+double derive_dinc(double L, double inc) {
+    volatile double vL = L, vi = inc;
+    uint64_t lo = dkey(-INFINITY), hi = dkey(INFINITY);   // p(lo) false, p(hi) true
+    while (hi - lo > 1) {
+        const uint64_t mid = lo + (hi - lo) / 2;
+        const double d = dval(mid);
+        if (d / vL > vi) hi = mid;
+        else lo = mid;
+    }
+    return dval(lo);
+}
+// Alg. 1: -1 iff fl(d / L) < dec  <=>  d < d*, d* = min{d : fl(d/L) >= dec}.
+double derive_ddec(double L, double dec) {
+    volatile double vL = L, vd = dec;
+    uint64_t lo = dkey(-INFINITY), hi = dkey(INFINITY);   // q(lo) true, q(hi) false
+    while (hi - lo > 1) {
+        const uint64_t mid = lo + (hi - lo) / 2;
+        const double d = dval(mid);
+        if (d / vL < vd) lo = mid;
+        else hi = mid;
+    }
+    return dval(hi);
+}
+// Alg. 2: true iff fl(s / C) >= thr on a full log; s_min = min such s (C+1 = never).
+int derive_smin(int C, double thr) {
+    for (int s = 0; s <= C; ++s)
+        if ((double)s / (double)C >= thr) return s;
+    return C + 1;
+}
+
+double uncore_power_at(double f, const magus_model& m) {
+    const double x = (f - m.f_min_ghz) / (m.f_max_ghz - m.f_min_ghz);
+    return m.p_uncore_min_w + (m.p_uncore_max_w - m.p_uncore_min_w) * std::pow(x, m.p_exponent);
+}
+double pkg_power_at(double f, const magus_model& m) {
+    return (m.p_pkg_idle_w + m.p_core_active_w) + uncore_power_at(f, m);
+}
+double bandwidth_at(double f, const magus_model& m) {     // SPEC.md:333, operand order DESIGN A26
+    const double ratio = f / m.f_max_ghz;
+    if (m.bw_shape == 0) return m.bw_max_gbps * ratio;
+    const double r = ratio / m.bw_knee;
+    return m.bw_max_gbps * (r < 1.0 ? r : 1.0);
+}
+
+// TDP (A24): cmd = f_min iff fl(P + fl(c*A)) >= fl((1-m)*TDP); monotone in fp32 A >= 0, so
+// it is A >= a*, a* = the smallest such fp32 (+inf if none).
+float derive_astar(double P, const magus_model& m, const magus_policy& p) {
+    volatile double vP = P, vc = m.dram_w_per_gbps;
+    const double bound = (1.0 - p.tdp_margin) * p.tdp_w;
+    auto pred = [&](uint32_t bits) { return (vP + vc * (double)fval(bits)) >= bound; };
+    const uint32_t zero = 0u, inf = 0x7F800000u;
+    if (pred(zero)) return 0.0f;
+    if (!pred(inf)) return INFINITY;
+    uint32_t lo = zero, hi = inf;
+    while (hi - lo > 1) {
+        const uint32_t mid = lo + (hi - lo) / 2;
+        if (pred(mid)) hi = mid;
+        else lo = mid;
+    }
+    return fval(hi);
+}
+
+bool finite(double x) { return std::isfinite(x); }
+
+// ------------------------------------------------------------------------------------ validation
+std::string validate_model(const magus_model& m) {
+    if (!(finite(m.sample_period_s) && m.sample_period_s > 0)) return "sample_period_s must be finite and > 0";
+    if (!(finite(m.f_min_ghz) && m.f_min_ghz > 0)) return "f_min_ghz must be finite and > 0";
+    if (!(finite(m.f_max_ghz) && m.f_max_ghz > m.f_min_ghz)) return "f_max_ghz must be finite and > f_min_ghz";
+    if (!(finite(m.bw_max_gbps) && m.bw_max_gbps > 0)) return "bw_max_gbps must be finite and > 0";
+    if (m.bw_shape != 0 && m.bw_shape != 1) return "bw_shape must be 0 (Linear) or 1 (Saturating)";
+    if (m.bw_shape == 1 && !(m.bw_knee > 0 && m.bw_knee <= 1)) return "bw_knee must be in (0, 1]";
+    const double pw[] = {m.p_pkg_idle_w, m.p_core_active_w, m.p_uncore_min_w, m.p_uncore_max_w, m.p_gpu_active_w,
+                         m.dram_w_per_gbps};
+    const char* names[] = {"p_pkg_idle_w", "p_core_active_w", "p_uncore_min_w", "p_uncore_max_w",
+                           "p_gpu_active_w", "dram_w_per_gbps"};
+    for (int i = 0; i < 6; ++i)
+        if (!(finite(pw[i]) && pw[i] >= 0)) return std::string(names[i]) + " must be finite and >= 0";
+    if (!(m.p_uncore_max_w >= m.p_uncore_min_w)) return "p_uncore_max_w must be >= p_uncore_min_w";
+    if (!(finite(m.p_exponent) && m.p_exponent >= 1)) return "p_exponent must be finite and >= 1";
+    const float blo = (float)bandwidth_at(m.f_min_ghz, m);
+    if (!(blo > 0.0f)) return "bw_max_gbps too small: bandwidth at f_min rounds to 0 in fp32";
+    return "";
+}
+
+std::string validate_policy(const magus_policy& p, int i) {
+    const std::string at = "policies[" + std::to_string(i) + "].";
+    if (p.kind < 0 || p.kind > 3) return at + "kind must be 0..3";
+    if (p.kind == MAGUS_POLICY_MAGUS) {
+        if (p.deriv_ticks < 1 || p.deriv_ticks > KMAX_GENERIC) return at + "deriv_ticks must be in [1, 64]";
+        if (!(finite(p.inc_threshold) && p.inc_threshold > 0)) return at + "inc_threshold must be finite and > 0";
+        if (!(finite(p.dec_threshold) && p.dec_threshold < 0)) return at + "dec_threshold must be finite and < 0";
+        if (p.tune_log_capacity < 1 || p.tune_log_capacity > 64) return at + "tune_log_capacity must be in [1, 64]";
+        if (!(p.high_freq_threshold > 0 && p.high_freq_threshold <= 1))
+            return at + "high_freq_threshold must be in (0, 1]";
+    }
+    if (p.kind == MAGUS_POLICY_TDP_DEFAULT) {
+        if (!(finite(p.tdp_w) && p.tdp_w > 0)) return at + "tdp_w must be finite and > 0";
+        if (!(p.tdp_margin > 0 && p.tdp_margin < 1)) return at + "tdp_margin must be in (0, 1)";
+    }
+    return "";
+}
+
+int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return (v && *v) ? std::atoi(v) : dflt;
+}
+
+}  // namespace
+
+// ============================================================================================ handle
+struct magus_replay {
+    magus_replay_desc desc{};
+    std::vector<magus_policy> pols;
+    std::vector<DevPolicy> lane;        // lane policies (everything but STATIC_MAX; or one validate pseudo)
+    std::vector<int> smax;              // indices of STATIC_MAX policies
+    float B_lo = 0, B_hi = 0;
+    uint32_t bwbits = 0;
+    double P_lo = 0, P_hi = 0;
+    uint64_t digest_all_hi = 0;
+    ReplayParams rp{};
+    EpiParams ep{};
+    std::vector<LaunchGroup> groups;
+    // device memory
+    std::vector<void*> allocs;
+    DevPolicy* d_pol = nullptr;
+    int* d_smax = nullptr;
+    TraceRec* d_rec = nullptr;
+    double* d_totals = nullptr;
+    int* d_argmin = nullptr;
+    unsigned int* d_flag = nullptr;     // [0] invalid flag, [1] fix rounds, [2..3] fix segments (u64)
+    unsigned long long* d_errkey = nullptr;
+    uint8_t* d_codes = nullptr;
+    float* d_trace_own = nullptr;
+    float* d_w_own = nullptr;
+    // last run
+    const float* run_trace = nullptr;
+    cudaStream_t run_stream = nullptr;
+    bool ran = false;
+    CUtensorMap tmap{};
+    const float* tmap_ptr = nullptr;
+    cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};   // ev[4]: the run's completion
+    static constexpr int kTimingRing = 256;
+    std::vector<cudaEvent_t> tev;   // MAGUS_F_TIMING: 4 events per run, ring of kTimingRing runs
+    int64_t n_runs = 0;
+    ncclComm_t comm = nullptr;
+    std::string err;
+};
+
+static magus_status fail(magus_replay_t* h, magus_status s, const std::string& msg) {
+    if (h) h->err = msg;
+    g_error = msg;
+    return s;
+}
+static magus_status cuda_fail(magus_replay_t* h, cudaError_t e, const char* where) {
+    return fail(h, e == cudaErrorMemoryAllocation ? MAGUS_ERR_OOM : MAGUS_ERR_CUDA,
+                std::string(where) + ": " + cudaGetErrorString(e));
+}
+#define CU(h, call)                                          \
+    do {                                                     \
+        cudaError_t e_ = (call);                             \
+        if (e_ != cudaSuccess) return cuda_fail(h, e_, #call); \
+    } while (0)
+
+template <class T>
+static cudaError_t dalloc(magus_replay_t* h, T** p, size_t count) {
+    *p = nullptr;
+    if (count == 0) count = 1;
+    void* v = nullptr;
+    cudaError_t e = cudaMalloc(&v, count * sizeof(T));
+    if (e == cudaSuccess) {
+        h->allocs.push_back(v);
+        *p = (T*)v;
+    }
+    return e;
+}
+
+extern "C" const char* magus_set_global_error(const char* msg) {
+    g_error = msg ? msg : "";
+    return g_error.c_str();
+}
+
+extern "C" int32_t magus_abi_version(void) { return MAGUS_ABI_VERSION; }
+extern "C" const char* magus_last_error(void) { return g_error.c_str(); }
+extern "C" const char* magus_replay_last_error(const magus_replay_t* h) {
+    return h ? h->err.c_str() : g_error.c_str();
+}
+
+extern "C" magus_status magus_derive_thresholds(const magus_policy* p, const magus_model* m, double out_d[5],
+                                                float out_f[4], int32_t out_i[1]) {
+    if (!p || !m || !out_d || !out_f || !out_i) return fail(nullptr, MAGUS_ERR_INVALID_ARG, "NULL argument");
+    std::string e = validate_model(*m);
+    if (e.empty()) e = validate_policy(*p, 0);
+    if (!e.empty()) return fail(nullptr, MAGUS_ERR_CONFIG, e);
+    const double L = (double)(p->kind == MAGUS_POLICY_MAGUS ? p->deriv_ticks : 1) * m->sample_period_s;
+    const double P_lo = pkg_power_at(m->f_min_ghz, *m), P_hi = pkg_power_at(m->f_max_ghz, *m);
+    out_d[0] = p->kind == MAGUS_POLICY_MAGUS ? derive_dinc(L, p->inc_threshold) : 0.0;
+    out_d[1] = p->kind == MAGUS_POLICY_MAGUS ? derive_ddec(L, p->dec_threshold) : 0.0;
+    out_d[2] = L;
+    out_d[3] = P_lo;
+    out_d[4] = P_hi;
+    out_f[0] = (float)bandwidth_at(m->f_min_ghz, *m);
+    out_f[1] = (float)bandwidth_at(m->f_max_ghz, *m);
+    out_f[2] = p->kind == MAGUS_POLICY_TDP_DEFAULT ? derive_astar(P_lo, *m, *p) : INFINITY;
+    out_f[3] = p->kind == MAGUS_POLICY_TDP_DEFAULT ? derive_astar(P_hi, *m, *p) : INFINITY;
+    out_i[0] = p->kind == MAGUS_POLICY_MAGUS ? derive_smin(p->tune_log_capacity, p->high_freq_threshold) : 0;
+    return MAGUS_OK;
+}
+
+extern "C" magus_status magus_nccl_unique_id(void* out128) {
+    if (!out128) return fail(nullptr, MAGUS_ERR_INVALID_ARG, "NULL argument");
+    if (!nccl_ok()) return fail(nullptr, MAGUS_ERR_NCCL, "libnccl.so.2 could not be loaded");
+    ncclUniqueId id;
+    ncclResult_t r = nccl().GetUniqueId(&id);
+    if (r != ncclSuccess) return fail(nullptr, MAGUS_ERR_NCCL, nccl().GetErrorString(r));
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    std::memcpy(out128, &id, 128);
+    return MAGUS_OK;
+}
+
+// ------------------------------------------------------------------------------------ geometry
+// Chooses, per launch group, the CTA shape, and globally the time segmentation:
+// enough independent chains to fill the SMs, whole waves of equal-work CTAs, warm-up W >= k + C - 1
+// (+ margin).
+static void choose_geometry(magus_replay_t* h, int n_sm) {
+    ReplayParams& p = h->rp;
+    const magus_replay_desc& d = h->desc;
+    const int Q = (int)h->lane.size();
+    p.n_lane = Q;
+    p.n_traces = d.n_traces;
+    p.n_samples = d.n_samples;
+    p.trace_stride = d.trace_stride;
+    p.n_groups = (d.n_traces + kTracesPerWarp - 1) / kTracesPerWarp;
+    const int ng_smem = (int)((200 * 1024) / (kNStage * Smem::kTileBytes));
+    h->groups.clear();
+    for (int q = 0; q < Q;) {
+        LaunchGroup g{};
+        g.key = ticker_key(h->lane[q]);
+        g.kernel = replay_kernel_for(g.key);
+        g.q_base = q;
+        while (q < Q && ticker_key(h->lane[q]) == g.key) ++q;
+        g.nq = q - g.q_base;
+        g.npw = std::min(g.nq, kMaxConsumerWarps);
+        g.n_pblocks = (g.nq + g.npw - 1) / g.npw;
+        int ng = std::min(ng_smem, kMaxConsumerWarps / g.npw);
+        ng = std::min(ng, env_int("MAGUS_NG", ng));
+        g.ng = std::max(1, std::min(ng, std::max(1, p.n_groups)));
+        g.n_tblocks = std::max(1, (p.n_groups + g.ng - 1) / g.ng);
+        g.threads = g.ng * g.npw * 32;
+        g.smem = Smem::bytes(g.ng);
+        h->groups.push_back(g);
+    }
+    int kmax = 1, cmax = 1;
+    p.kr = 1;
+    for (const DevPolicy& q : h->lane) {
+        if (q.kind == LANE_MAGUS) {
+            kmax = std::max(kmax, q.k);
+            cmax = std::max(cmax, q.C);
+            p.kr = std::max(p.kr, q.k);
+        }
+    }
+    int W = d.tuning_warmup > 0 ? d.tuning_warmup
+                                : ((kmax + cmax - 1 + 31) / 32) * 32 + env_int("MAGUS_WARMUP_EXTRA", 32);
+    W = ((std::max(W, kmax + cmax - 1) + 31) / 32) * 32;
+    const int N = std::max(1, d.n_samples);
+    int base = 0;   // CTAs per segment over all launch groups
+    for (const LaunchGroup& g : h->groups) base += g.n_tblocks * g.n_pblocks;
+    int S = 1;
+    if (d.tuning_segments > 0) {
+        S = d.tuning_segments;
+    } else {
+        double best = 1e300;
+        const int max_waves = env_int("MAGUS_MAX_WAVES", 4);
+        for (int waves = 1; waves <= max_waves; ++waves) {
+            int s = std::max(1, (n_sm * waves) / base);
+            const int L = (((N + s - 1) / s) + 31) / 32 * 32;
+            if (s > 1 && L < 4 * W) continue;   // segments must dwarf their warm-up
+            s = (N + L - 1) / L;
+            const double cost = std::ceil((double)s * base / n_sm) * (L + (s > 1 ? W : 0));
+            if (cost < best) {
+                best = cost;
+                S = s;
+            }
+        }
+    }
+    int L = (((N + S - 1) / S) + 31) / 32 * 32;
+    if (L < 32) L = 32;
+    S = (N + L - 1) / L;
+    if (S > 1 && L < W) {   // forced segmentation too fine for the warm-up: fall back to fewer segments
+        L = ((W + 31) / 32) * 32;
+        S = (N + L - 1) / L;
+    }
+    p.n_seg = std::max(1, S);
+    p.seg_len = L;
+    p.warmup = p.n_seg > 1 ? W : 0;
+    p.n_blocks = (d.n_samples + 31) / 32;
+    for (LaunchGroup& g : h->groups) g.n_ctas = p.n_seg * g.n_tblocks * g.n_pblocks;
+}
+
+extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus_replay_t** out) {
+    if (out) *out = nullptr;
+    if (!desc || !out) return fail(nullptr, MAGUS_ERR_INVALID_ARG, "magus_replay_create: NULL argument");
+    const magus_replay_desc& d = *desc;
+    if (d.n_traces < 0 || d.n_samples < 0) return fail(nullptr, MAGUS_ERR_INVALID_ARG, "n_traces/n_samples must be >= 0");
+    if (d.n_policies < 1 || !d.policies) return fail(nullptr, MAGUS_ERR_INVALID_ARG, "n_policies must be >= 1 with a policy array");
+    if (d.trace_stride < d.n_traces) return fail(nullptr, MAGUS_ERR_INVALID_ARG, "trace_stride must be >= n_traces");
+    if (d.trace_stride % 4 != 0) return fail(nullptr, MAGUS_ERR_ALIGN, "trace_stride must be a multiple of 4 floats (16 B, TMA)");
+    if (d.world < 1 || d.rank < 0 || d.rank >= d.world) return fail(nullptr, MAGUS_ERR_INVALID_ARG, "need 0 <= rank < world");
+    if (d.world > 1 && !d.nccl_unique_id) return fail(nullptr, MAGUS_ERR_INVALID_ARG, "world > 1 needs nccl_unique_id");
+    if ((d.flags & MAGUS_F_DUMP_DECISIONS) &&
+        (d.dump_first_trace < 0 || d.dump_n_traces < 0 || d.dump_first_trace + d.dump_n_traces > d.n_traces))
+        return fail(nullptr, MAGUS_ERR_INVALID_ARG, "dump window outside [0, n_traces)");
+    if (d.tuning_warmup < 0 || d.tuning_warmup % 32 != 0)
+        return fail(nullptr, MAGUS_ERR_INVALID_ARG, "tuning_warmup must be a multiple of 32");
+    std::string e = validate_model(d.model);
+    if (!e.empty()) return fail(nullptr, MAGUS_ERR_CONFIG, "model." + e);
+    for (int i = 0; i < d.n_policies; ++i) {
+        e = validate_policy(d.policies[i], i);
+        if (!e.empty()) return fail(nullptr, MAGUS_ERR_CONFIG, e);
+    }
+    int dev = 0, n_dev = 0;
+    if (cudaGetDeviceCount(&n_dev) != cudaSuccess || n_dev == 0) {
+        cudaGetLastError();
+        return fail(nullptr, MAGUS_ERR_CUDA, "no CUDA device (there is no CPU fallback)");
+    }
+    cudaGetDevice(&dev);
+    int n_sm = 148;
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+
+    magus_replay_t* h = new magus_replay_t();
+    h->desc = d;
+    h->pols.assign(d.policies, d.policies + d.n_policies);
+    h->desc.policies = nullptr;
+    h->desc.nccl_unique_id = nullptr;
+    const magus_model& m = d.model;
+    h->B_lo = (float)bandwidth_at(m.f_min_ghz, m);
+    h->B_hi = (float)bandwidth_at(m.f_max_ghz, m);
+    float bwf = (float)m.bw_max_gbps;
+    if ((double)bwf > m.bw_max_gbps) bwf = nextafterf(bwf, 0.0f);
+    h->bwbits = fbits(bwf);
+    h->P_lo = pkg_power_at(m.f_min_ghz, m);
+    h->P_hi = pkg_power_at(m.f_max_ghz, m);
+
+    for (int i = 0; i < d.n_policies; ++i) {
+        const magus_policy& p = h->pols[i];
+        if (p.kind == MAGUS_POLICY_STATIC_MAX) {
+            h->smax.push_back(i);
+            continue;
+        }
+        DevPolicy q{};
+        q.policy_index = i;
+        q.k = 1;
+        q.C = 1;
+        q.s_min = 0;
+        q.logmask = 1;
+        q.dinc = INFINITY;
+        q.ddec = -INFINITY;
+        q.astar_lo = q.astar_hi = INFINITY;
+        if (p.kind == MAGUS_POLICY_MAGUS) {
+            q.kind = LANE_MAGUS;
+            q.k = p.deriv_ticks;
+            q.C = p.tune_log_capacity;
+            q.logmask = q.C >= 64 ? ~0ULL : ((1ULL << q.C) - 1ULL);
+            const double L = (double)p.deriv_ticks * m.sample_period_s;
+            q.dinc = derive_dinc(L, p.inc_threshold);
+            q.ddec = derive_ddec(L, p.dec_threshold);
+            q.s_min = derive_smin(q.C, p.high_freq_threshold);
+            q.f0 = 0;
+            q.guess_f = 0;   // speculative segment start
+        } else if (p.kind == MAGUS_POLICY_STATIC_MIN) {
+            q.kind = LANE_STATIC_MIN;
+            q.f0 = q.guess_f = 0;
+        } else {
+            q.kind = LANE_TDP;
+            q.astar_lo = derive_astar(h->P_lo, m, p);
+            q.astar_hi = derive_astar(h->P_hi, m, p);
+            q.f0 = 1;        // the default sits at max
+            q.guess_f = 1;
+        }
+        h->lane.push_back(q);
+    }
+    if (h->lane.empty()) {   // only STATIC_MAX policies: a validate-only lane still scans the samples (A17)
+        DevPolicy q{};
+        q.kind = LANE_VALIDATE;
+        q.k = 1;
+        q.C = 1;
+        q.logmask = 1;
+        q.policy_index = -1;
+        h->lane.push_back(q);
+    }
+    // digest of an all-f_max command stream (STATIC_MAX), DESIGN.md section 5
+    {
+        const int64_t nb = (d.n_samples + 31) / 32;
+        uint64_t dg = 0;
+        for (int64_t b = 0; b < nb; ++b) {
+            const int n = (int)std::min<int64_t>(32, d.n_samples - b * 32);
+            const uint32_t wc = n == 32 ? 0xFFFFFFFFu : (((1u << n) - 1u) << (32 - n));
+            dg += mix64(((uint64_t)wc << 32) ^ ((uint64_t)b * kPhi));
+        }
+        h->digest_all_hi = dg;
+    }
+
+    std::stable_sort(h->lane.begin(), h->lane.end(),
+                     [](const DevPolicy& a, const DevPolicy& b) { return ticker_key(a) < ticker_key(b); });
+    choose_geometry(h, n_sm);
+    ReplayParams& p = h->rp;
+    p.B_lo = h->B_lo;
+    p.B_hi = h->B_hi;
+    p.bwbits = h->bwbits;
+
+    const int Q = p.n_lane, S = p.n_seg;
+    const size_t nst = (size_t)2 * Q * S * std::max(1, d.n_traces);
+    const size_t nstat = (size_t)Q * S * std::max(1, d.n_traces);
+    cudaError_t ce;
+#define ALLOC(ptr, n)                                         \
+    if ((ce = dalloc(h, &(ptr), (n))) != cudaSuccess) {       \
+        magus_status s_ = cuda_fail(h, ce, "cudaMalloc " #ptr); \
+        magus_replay_destroy(h);                              \
+        return s_;                                            \
+    }
+    DevPolicy* dpol;
+    ALLOC(dpol, h->lane.size());
+    h->d_pol = dpol;
+    ALLOC(p.st_f, nst);
+    ALLOC(p.st_log, nst);
+    ALLOC(p.st_ring, nst * p.kr);
+    ALLOC(p.s_nhi, nstat);
+    ALLOC(p.s_nthr, nstat);
+    ALLOC(p.s_trans, nstat);
+    ALLOC(p.s_ev, nstat);
+    ALLOC(p.s_lock, nstat);
+    ALLOC(p.s_vmax, nstat);
+    ALLOC(p.s_sthr, nstat);
+    ALLOC(p.s_digest, nstat);
+    if (d.flags & MAGUS_F_DUMP_WORDS) {
+        ALLOC(p.words, (size_t)Q * std::max(1, d.n_traces) * std::max(1, p.n_blocks) * 2);
+    } else {
+        p.words = nullptr;
+    }
+    ALLOC(h->d_rec, (size_t)std::max(1, d.n_traces) * d.n_policies);
+    ALLOC(h->d_totals, (size_t)d.n_policies * MAGUS_N_TOTALS);
+    ALLOC(h->d_argmin, 1);
+    ALLOC(h->d_flag, 4);
+    ALLOC(h->d_errkey, 1);
+    if (!h->smax.empty()) {
+        ALLOC(h->d_smax, h->smax.size());
+    }
+    if ((d.flags & MAGUS_F_DUMP_DECISIONS) && d.dump_n_traces > 0 && d.n_samples > 0) {
+        ALLOC(h->d_codes, (size_t)d.n_samples * d.dump_n_traces * d.n_policies);
+    }
+#undef ALLOC
+    p.pol = h->d_pol;
+    if ((ce = cudaMemcpy(h->d_pol, h->lane.data(), h->lane.size() * sizeof(DevPolicy), cudaMemcpyHostToDevice)) !=
+        cudaSuccess) {
+        magus_status s = cuda_fail(h, ce, "cudaMemcpy policies");
+        magus_replay_destroy(h);
+        return s;
+    }
+    if (!h->smax.empty())
+        cudaMemcpy(h->d_smax, h->smax.data(), h->smax.size() * sizeof(int), cudaMemcpyHostToDevice);
+
+    EpiParams& ep = h->ep;
+    ep.n_policies = d.n_policies;
+    ep.n_samples = d.n_samples;
+    ep.Delta = m.sample_period_s;
+    ep.P_lo = h->P_lo;
+    ep.P_hi = h->P_hi;
+    ep.P_gpu = m.p_gpu_active_w;
+    ep.B_lo_d = (double)h->B_lo;
+    ep.rec = h->d_rec;
+    ep.flag_invalid = h->d_flag;
+    ep.fix_rounds = (int*)(h->d_flag + 1);
+    ep.fix_segments = (unsigned long long*)(h->d_flag + 2);
+
+    for (int i = 0; i < 5; ++i) cudaEventCreate(&h->ev[i]);
+    if (d.flags & MAGUS_F_TIMING) {
+        h->tev.resize(4 * magus_replay::kTimingRing);
+        for (cudaEvent_t& e : h->tev) cudaEventCreate(&e);
+    }
+    for (const LaunchGroup& g : h->groups) {
+        ce = cudaFuncSetAttribute((const void*)g.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
+        if (ce != cudaSuccess) {
+            magus_status s = cuda_fail(h, ce, "cudaFuncSetAttribute smem");
+            magus_replay_destroy(h);
+            return s;
+        }
+    }
+    if (d.world > 1) {
+        if (!nccl_ok()) {
+            magus_status s = fail(h, MAGUS_ERR_NCCL, "libnccl.so.2 could not be loaded");
+            g_error = h->err;
+            magus_replay_destroy(h);
+            return s;
+        }
+        ncclUniqueId id;
+        std::memcpy(&id, desc->nccl_unique_id, sizeof(id));
+        ncclResult_t r = nccl().CommInitRank(&h->comm, d.world, id, d.rank);
+        if (r != ncclSuccess) {
+            magus_status s = fail(h, MAGUS_ERR_NCCL, std::string("ncclCommInitRank: ") + nccl().GetErrorString(r));
+            h->comm = nullptr;
+            magus_replay_destroy(h);
+            return s;
+        }
+    }
+    *out = h;
+    return MAGUS_OK;
+}
+
+extern "C" void magus_replay_destroy(magus_replay_t* h) {
+    if (!h) return;
+    if (h->ran && h->run_stream) cudaStreamSynchronize(h->run_stream);
+    if (h->comm && nccl_ok()) nccl().CommDestroy(h->comm);
+    for (void* a : h->allocs) cudaFree(a);
+    for (int i = 0; i < 5; ++i)
+        if (h->ev[i]) cudaEventDestroy(h->ev[i]);
+    for (cudaEvent_t e : h->tev) cudaEventDestroy(e);
+    delete h;
+}
+
+static magus_status encode_tmap(magus_replay_t* h, const float* d_trace) {
+    if (h->tmap_ptr == d_trace) return MAGUS_OK;
+    PFN_encodeTiled enc = get_encode();
+    if (!enc) return fail(h, MAGUS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
+    const magus_replay_desc& d = h->desc;
+    cuuint64_t gdim[2] = {(cuuint64_t)d.n_traces, (cuuint64_t)d.n_samples};
+    cuuint64_t gstride[1] = {(cuuint64_t)d.trace_stride * sizeof(float)};
+    cuuint32_t box[2] = {(cuuint32_t)kTracesPerWarp, (cuuint32_t)kTC};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(&h->tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)d_trace, gdim, gstride, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(h, MAGUS_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    h->tmap_ptr = d_trace;
+    return MAGUS_OK;
+}
+
+extern "C" magus_status magus_replay_run(magus_replay_t* h, const float* d_trace, const float* d_w, void* stream) {
+    if (!h) return fail(nullptr, MAGUS_ERR_INVALID_ARG, "NULL handle");
+    const magus_replay_desc& d = h->desc;
+    const bool has_work = d.n_traces > 0 && d.n_samples > 0;
+    if (d.n_traces > 0 && (!d_trace || !d_w)) return fail(h, MAGUS_ERR_INVALID_ARG, "NULL trace or w");
+    if (has_work && ((uintptr_t)d_trace % 16 != 0)) return fail(h, MAGUS_ERR_ALIGN, "trace base must be 16-byte aligned");
+    cudaStream_t s = (cudaStream_t)stream;
+    const bool timing = (d.flags & MAGUS_F_TIMING) != 0;
+    ReplayParams p = h->rp;
+    EpiParams ep = h->ep;
+    ep.w = d_w;
+    if (has_work) {
+        magus_status st = encode_tmap(h, d_trace);
+        if (st != MAGUS_OK) return st;
+    }
+    CU(h, cudaMemsetAsync(h->d_flag, 0, 4 * sizeof(unsigned int), s));
+    cudaEvent_t* tv = timing ? &h->tev[4 * (h->n_runs % magus_replay::kTimingRing)] : nullptr;
+    if (timing) CU(h, cudaEventRecord(tv[0], s));
+    if (has_work) {
+        for (const LaunchGroup& g : h->groups) {
+            ReplayParams pg = p;
+            pg.q_base = g.q_base;
+            pg.nq = g.nq;
+            pg.ng = g.ng;
+            pg.npw = g.npw;
+            pg.n_tblocks = g.n_tblocks;
+            pg.n_pblocks = g.n_pblocks;
+            g.kernel<<<g.n_ctas, g.threads, g.smem, s>>>(h->tmap, pg);
+            CU(h, cudaGetLastError());
+        }
+    } else {
+        const size_t nstat = (size_t)p.n_lane * p.n_seg * std::max(1, d.n_traces);
+        CU(h, cudaMemsetAsync(p.s_nhi, 0, nstat * 4, s));
+        CU(h, cudaMemsetAsync(p.s_nthr, 0, nstat * 4, s));
+        CU(h, cudaMemsetAsync(p.s_trans, 0, nstat * 4, s));
+        CU(h, cudaMemsetAsync(p.s_ev, 0, nstat * 4, s));
+        CU(h, cudaMemsetAsync(p.s_lock, 0, nstat * 4, s));
+        CU(h, cudaMemsetAsync(p.s_vmax, 0, nstat * 4, s));
+        CU(h, cudaMemsetAsync(p.s_sthr, 0, nstat * 8, s));
+        CU(h, cudaMemsetAsync(p.s_digest, 0, nstat * 8, s));
+    }
+    if (timing) CU(h, cudaEventRecord(tv[1], s));
+    if (d.n_traces > 0) {
+        dim3 grid((unsigned)((d.n_traces + 7) / 8), (unsigned)p.n_lane);
+        magus_fixup_epilogue_kernel<<<grid, 256, 0, s>>>(p, ep, d_trace);
+        CU(h, cudaGetLastError());
+        if (!h->smax.empty()) {
+            const int64_t n = (int64_t)d.n_traces * (int64_t)h->smax.size();
+            magus_static_max_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(ep, d.n_traces, h->d_smax,
+                                                                               (int)h->smax.size(), h->digest_all_hi);
+            CU(h, cudaGetLastError());
+        }
+    }
+    if (timing) CU(h, cudaEventRecord(tv[2], s));
+    magus_totals_kernel<<<d.n_policies, kTotThreads, 0, s>>>(h->d_rec, d.n_traces, d.n_policies, h->d_totals);
+    CU(h, cudaGetLastError());
+    if (d.world > 1) {
+        ncclResult_t r = nccl().AllReduce(h->d_totals, h->d_totals, (size_t)d.n_policies * MAGUS_N_TOTALS, ncclFloat64,
+                                          ncclSum, h->comm, s);
+        if (r != ncclSuccess) return fail(h, MAGUS_ERR_NCCL, std::string("ncclAllReduce: ") + nccl().GetErrorString(r));
+    }
+    magus_argmin_kernel<<<1, 32, 0, s>>>(h->d_totals, d.n_policies, h->d_argmin);
+    CU(h, cudaGetLastError());
+    if (timing) CU(h, cudaEventRecord(tv[3], s));
+    if (h->d_codes && has_work) {
+        const int P = d.n_policies;
+        dim3 grid((unsigned)((d.dump_n_traces + 63) / 64), (unsigned)p.n_lane);
+        magus_resim_kernel<<<grid, 64, 0, s>>>(p, d_trace, d.dump_first_trace, d.dump_n_traces, P, h->d_codes);
+        CU(h, cudaGetLastError());
+        const int64_t rows = (int64_t)d.n_samples * d.dump_n_traces;
+        for (int pi : h->smax) {
+            magus_fill_codes_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, s>>>(h->d_codes, rows, P, pi, 0x81);
+            CU(h, cudaGetLastError());
+        }
+    }
+    CU(h, cudaEventRecord(h->ev[4], s));
+    h->run_trace = d_trace;
+    h->run_stream = s;
+    h->ran = true;
+    h->n_runs += 1;
+    return MAGUS_OK;
+}
+
+extern "C" magus_status magus_replay_run_host(magus_replay_t* h, const float* trace, const float* w, void* stream) {
+    if (!h) return fail(nullptr, MAGUS_ERR_INVALID_ARG, "NULL handle");
+    const magus_replay_desc& d = h->desc;
+    if (d.n_traces > 0 && (!trace || !w)) return fail(h, MAGUS_ERR_INVALID_ARG, "NULL trace or w");
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t n_trace = (size_t)d.n_samples * (size_t)d.trace_stride;
+    if (!h->d_trace_own && n_trace > 0) {
+        cudaError_t ce = dalloc(h, &h->d_trace_own, n_trace);
+        if (ce != cudaSuccess) return cuda_fail(h, ce, "cudaMalloc host-run trace buffer");
+    }
+    if (!h->d_w_own) {
+        cudaError_t ce = dalloc(h, &h->d_w_own, (size_t)std::max(1, d.n_traces));
+        if (ce != cudaSuccess) return cuda_fail(h, ce, "cudaMalloc host-run w buffer");
+    }
+    if (n_trace > 0) CU(h, cudaMemcpyAsync(h->d_trace_own, trace, n_trace * sizeof(float), cudaMemcpyHostToDevice, s));
+    if (d.n_traces > 0)
+        CU(h, cudaMemcpyAsync(h->d_w_own, w, (size_t)d.n_traces * sizeof(float), cudaMemcpyHostToDevice, s));
+    return magus_replay_run(h, h->d_trace_own, h->d_w_own, stream);
+}
+
+extern "C" magus_status magus_replay_results(magus_replay_t* h, magus_results* out) {
+    if (!h || !out) return fail(h, MAGUS_ERR_INVALID_ARG, "NULL argument");
+    if (!h->ran) return fail(h, MAGUS_ERR_STATE, "magus_replay_results before any run");
+    const magus_replay_desc& d = h->desc;
+    CU(h, cudaEventSynchronize(h->ev[4]));
+    CU(h, cudaGetLastError());
+    const int P = d.n_policies;
+    if (out->policy_totals)
+        CU(h, cudaMemcpy(out->policy_totals, h->d_totals, (size_t)P * MAGUS_N_TOTALS * sizeof(double),
+                         cudaMemcpyDeviceToHost));
+    int am = 0;
+    CU(h, cudaMemcpy(&am, h->d_argmin, sizeof(int), cudaMemcpyDeviceToHost));
+    out->argmin_policy = am;
+    unsigned int fl[4] = {0, 0, 0, 0};
+    CU(h, cudaMemcpy(fl, h->d_flag, sizeof(fl), cudaMemcpyDeviceToHost));
+    unsigned long long segs = 0;
+    std::memcpy(&segs, &fl[2], 8);
+    out->n_segments = h->rp.n_seg;
+    out->warmup_ticks = h->rp.warmup;
+    out->n_mismatched_segments = (int64_t)segs;
+    out->fixup_rounds = (int32_t)fl[1];
+    if (out->per_trace && (d.flags & MAGUS_F_PER_TRACE_STATS) && d.n_traces > 0)
+        CU(h, cudaMemcpy(out->per_trace, h->d_rec, (size_t)d.n_traces * P * sizeof(TraceRec), cudaMemcpyDeviceToHost));
+    if (out->words && (d.flags & MAGUS_F_DUMP_WORDS) && d.n_traces > 0 && h->rp.n_blocks > 0) {
+        const size_t per_pol = (size_t)d.n_traces * h->rp.n_blocks * 2;
+        for (size_t q = 0; q < h->lane.size(); ++q) {
+            const int pi = h->lane[q].policy_index;
+            if (pi < 0) continue;
+            CU(h, cudaMemcpy(out->words + (size_t)pi * per_pol, h->rp.words + q * per_pol, per_pol * 4,
+                             cudaMemcpyDeviceToHost));
+        }
+        for (int pi : h->smax) {
+            uint32_t* o = out->words + (size_t)pi * per_pol;
+            for (int j = 0; j < d.n_traces; ++j)
+                for (int b = 0; b < h->rp.n_blocks; ++b) {
+                    const int n = std::min(32, d.n_samples - b * 32);
+                    o[((size_t)j * h->rp.n_blocks + b) * 2] = n == 32 ? 0xFFFFFFFFu : (((1u << n) - 1u) << (32 - n));
+                    o[((size_t)j * h->rp.n_blocks + b) * 2 + 1] = 0;
+                }
+        }
+    }
+    if (out->decisions && h->d_codes)
+        CU(h, cudaMemcpy(out->decisions, h->d_codes, (size_t)d.n_samples * d.dump_n_traces * P, cudaMemcpyDeviceToHost));
+    out->err_trace = -1;
+    out->err_tick = -1;
+    if (fl[0]) {
+        unsigned long long key = ~0ULL;
+        CU(h, cudaMemcpy(h->d_errkey, &key, sizeof(key), cudaMemcpyHostToDevice));
+        magus_scan_invalid_kernel<<<(d.n_traces + 127) / 128, 128>>>(h->run_trace, d.n_traces, d.n_samples,
+                                                                     d.trace_stride, h->bwbits, h->d_errkey);
+        CU(h, cudaGetLastError());
+        CU(h, cudaMemcpy(&key, h->d_errkey, sizeof(key), cudaMemcpyDeviceToHost));
+        if (key != ~0ULL) {
+            out->err_trace = (int32_t)(key >> 32);
+            out->err_tick = (int64_t)(key & 0xFFFFFFFFULL);
+            return fail(h, MAGUS_ERR_TRACE,
+                        "invalid sample (negative, NaN/Inf or > bw_max) at trace " + std::to_string(out->err_trace) +
+                            " tick " + std::to_string(out->err_tick));
+        }
+    }
+    return MAGUS_OK;
+}
+
+static magus_status timing_avg(magus_replay_t* h, int n_last, float out_ms[4]) {
+    if (!h || !out_ms) return fail(h, MAGUS_ERR_INVALID_ARG, "NULL argument");
+    if (!h->ran || h->tev.empty()) return fail(h, MAGUS_ERR_STATE, "no timed run (MAGUS_F_TIMING)");
+    CU(h, cudaEventSynchronize(h->ev[4]));
+    const int64_t n = std::min<int64_t>({(int64_t)std::max(1, n_last), h->n_runs, (int64_t)magus_replay::kTimingRing});
+    double acc[4] = {0, 0, 0, 0};
+    for (int64_t r = h->n_runs - n; r < h->n_runs; ++r) {
+        cudaEvent_t* tv = &h->tev[4 * (r % magus_replay::kTimingRing)];
+        float ms;
+        CU(h, cudaEventElapsedTime(&ms, tv[0], tv[1]));
+        acc[0] += ms;
+        CU(h, cudaEventElapsedTime(&ms, tv[1], tv[2]));
+        acc[1] += ms;
+        CU(h, cudaEventElapsedTime(&ms, tv[2], tv[3]));
+        acc[2] += ms;
+        CU(h, cudaEventElapsedTime(&ms, tv[0], tv[3]));
+        acc[3] += ms;
+    }
+    for (int i = 0; i < 4; ++i) out_ms[i] = (float)(acc[i] / (double)n);
+    return MAGUS_OK;
+}
+
+extern "C" magus_status magus_replay_kernel_times(magus_replay_t* h, float out_ms[4]) {
+    return timing_avg(h, 1, out_ms);
+}
+
+extern "C" magus_status magus_replay_timing_summary(magus_replay_t* h, int32_t n_last, float out_ms[4]) {
+    return timing_avg(h, n_last, out_ms);
+}
+
+// Diagnostics: the chosen geometry (first launch group's CTA shape).
+extern "C" magus_status magus_replay_geometry(const magus_replay_t* h, int32_t out[12]) {
+    if (!h || !out) return MAGUS_ERR_INVALID_ARG;
+    const ReplayParams& p = h->rp;
+    int ctas = 0;
+    for (const LaunchGroup& g : h->groups) ctas += g.n_ctas;
+    const LaunchGroup& g0 = h->groups.front();
+    const int32_t v[12] = {p.n_seg, p.seg_len, p.warmup, g0.ng, g0.npw, g0.n_tblocks, g0.n_pblocks, ctas,
+                           g0.threads, (int32_t)g0.smem, p.n_lane, (int32_t)h->groups.size()};
+    std::memcpy(out, v, sizeof(v));
+    return MAGUS_OK;
+}

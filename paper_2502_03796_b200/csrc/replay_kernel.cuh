@@ -1,0 +1,227 @@
+// replay_kernel.cuh -- the hot kernel: batched, time-segmented replay of the MAGUS loop.
+//
+// Work unit of one consumer warp: 128 consecutive traces (a lane owns 4, i.e. one 16-byte float4
+// per time row) x one lane policy x one time segment.  A CTA = ng tile groups x npw policy warps +
+// 1 producer warp.  Each tile group has an NSTAGE-deep ring of [TC ticks x 128 traces] fp32 tiles
+// in shared memory, filled by 2-D TMA (cp.async.bulk.tensor, one elected producer lane) and
+// consumed by the group's policy warps (full / empty mbarriers).  Every trace byte crosses HBM
+// once per launch (plus the W-tick warm-up overlap of speculative segments).
+//
+// Time segmentation: segment s covers ticks [s*L, min((s+1)*L, N)).  s = 0
+// starts from the exact initial state; s >= 1 starts speculatively W ticks early from a guessed
+// state and records the state it reaches at s*L (entry) and at its end (exit).  The fix-up kernel
+// compares each entry with the previous segment's exit and re-runs exactly where they differ.
+#pragma once
+#include <cuda.h>
+#include "device_common.cuh"
+#include "ptx.cuh"
+#include "tickers.cuh"
+
+namespace magus {
+
+constexpr int kTracesPerWarp = 128;   // 32 lanes x 4 traces (one float4 per lane per time row)
+constexpr int kChains = 4;
+constexpr int kMaxConsumerWarps = 8;   // 256 threads: 2 warps per SM sub-partition
+
+template <int TC, int NSTAGE>
+struct ReplaySmem {
+    static constexpr int kTileFloats = TC * kTracesPerWarp;
+    static constexpr int kTileBytes = kTileFloats * 4;
+    __host__ __device__ static size_t bytes(int ng) {
+        return (size_t)ng * NSTAGE * kTileBytes + (size_t)ng * NSTAGE * 2 * sizeof(uint64_t);
+    }
+};
+
+struct SegGeom {
+    int seg_start, seg_end, tau_w, n_stages;
+};
+
+template <int TC>
+__device__ __forceinline__ SegGeom seg_geom(const ReplayParams& p, int seg) {
+    SegGeom g;
+    g.seg_start = seg * p.seg_len;
+    g.seg_end = min(g.seg_start + p.seg_len, p.n_samples);
+    g.tau_w = seg == 0 ? 0 : g.seg_start - p.warmup;
+    g.n_stages = (g.seg_end - g.tau_w + TC - 1) / TC;
+    return g;
+}
+
+// Accumulate one tick of one chain into its segment statistics (counting region only).  The
+// validation maximum (A17) is kept per lane, over its 4 chains.
+__device__ __forceinline__ void acc_tick(SegStats& ss, uint32_t& vmax, const TickOut& o, float D) {
+    ss.nthr += o.thr;
+    ss.lock += o.hf;
+    if (o.thr) ss.sthr += (double)D;
+    vmax = max(vmax, __float_as_uint(D));
+}
+
+// Tile producer of one group: the group's leader lane arms full[slot] and issues the 2-D TMA box
+// {128 traces, TC ticks} at (first trace of the group, tick t0).
+template <int TC>
+__device__ __forceinline__ void issue_stage(const CUtensorMap* tmap, float* tile, uint64_t* full_bar, int x, int t0,
+                                            uint64_t cpol) {
+    ptx::mbar_arrive_expect_tx(full_bar, (uint32_t)(TC * kTracesPerWarp * 4));
+    ptx::tma_load_2d(tile, tmap, full_bar, x, t0, cpol);
+}
+
+template <class T, int TC, int NSTAGE>
+__device__ __forceinline__ void consume(const CUtensorMap* tmap, const ReplayParams& p, const DevPolicy& pol, int q,
+                                        int tgroup, int seg, float* tiles, uint64_t* full, uint64_t* empty, int lane,
+                                        bool producer) {
+    using State = typename T::State;
+    const SegGeom G = seg_geom<TC>(p, seg);
+    const int x = tgroup * kTracesPerWarp;
+    uint64_t cpol = 0;
+    if (producer) {
+        cpol = ptx::policy_evict_first();
+        for (int i = 0; i < NSTAGE && i < G.n_stages; ++i)
+            issue_stage<TC>(tmap, tiles + (size_t)i * TC * kTracesPerWarp, &full[i], x, G.tau_w + i * TC, cpol);
+    }
+    const int j0 = tgroup * kTracesPerWarp + lane * kChains;
+    const float B_lo = p.B_lo, B_hi = p.B_hi;
+    const int k = pol.k, C = pol.C;
+
+    State st[kChains];
+    SegStats ss[kChains];
+    uint32_t wcmd[kChains], fstart[kChains];
+    uint32_t vmax = 0;
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) {
+        T::init(st[c], pol, seg == 0);
+        ss[c].zero();
+        wcmd[c] = 0;
+        fstart[c] = T::level(st[c]);
+    }
+
+    for (int i = 0; i < G.n_stages; ++i) {
+        const int slot = i % NSTAGE;
+        const int t0 = G.tau_w + i * TC;
+        if (t0 == G.seg_start) {
+#pragma unroll
+            for (int c = 0; c < kChains; ++c)
+                if (j0 + c < p.n_traces) T::save(st[c], p, pol, 0, q, seg, j0 + c);
+        }
+        if ((t0 & 31) == 0) {
+#pragma unroll
+            for (int c = 0; c < kChains; ++c) fstart[c] = T::level(st[c]);
+        }
+        ptx::mbar_wait(&full[slot], (uint32_t)((i / NSTAGE) & 1));
+        const float4* rows = reinterpret_cast<const float4*>(tiles + (size_t)slot * TC * kTracesPerWarp) + lane;
+        const bool counting = t0 >= G.seg_start;
+        const int since = t0 - G.tau_w;
+        const bool fast = counting && (!T::kWarmupRules || since >= k + C - 1) && (t0 + TC <= G.seg_end);
+        if (fast) {
+#pragma unroll
+            for (int tt = 0; tt < TC; ++tt) {
+                const float4 d4 = rows[tt * (kTracesPerWarp / 4)];
+                const float d[4] = {d4.x, d4.y, d4.z, d4.w};
+#pragma unroll
+                for (int c = 0; c < kChains; ++c) {
+                    const TickOut o = T::template tick<false>(st[c], d[c], pol, B_lo, B_hi, true, true);
+                    wcmd[c] = (wcmd[c] << 1) | o.cmd;
+                    acc_tick(ss[c], vmax, o, d[c]);
+                }
+            }
+        } else {
+            for (int tt = 0; tt < TC; ++tt) {
+                const int t = t0 + tt;
+                if (t >= G.seg_end) break;
+                const float4 d4 = rows[tt * (kTracesPerWarp / 4)];
+                const float d[4] = {d4.x, d4.y, d4.z, d4.w};
+                const bool ready = (t - G.tau_w) >= k;
+                const bool lfull = (t - G.tau_w) >= k + C - 1;
+#pragma unroll
+                for (int c = 0; c < kChains; ++c) {
+                    const TickOut o = T::template tick<true>(st[c], d[c], pol, B_lo, B_hi, ready, lfull);
+                    wcmd[c] = (wcmd[c] << 1) | o.cmd;
+                    if (counting) acc_tick(ss[c], vmax, o, d[c]);
+                }
+            }
+        }
+        // release the stage; the group's producer lane refills it with stage i + NSTAGE once every
+        // policy warp of the group has released it
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&empty[slot]);
+        if (producer && i + NSTAGE < G.n_stages) {
+            ptx::mbar_wait(&empty[slot], (uint32_t)((i / NSTAGE) & 1));
+            issue_stage<TC>(tmap, tiles + (size_t)slot * TC * kTracesPerWarp, &full[slot], x,
+                            G.tau_w + (i + NSTAGE) * TC, cpol);
+        }
+
+        const int t1 = min(t0 + TC, G.seg_end);
+        if (counting && (((t1 & 31) == 0) || t1 == G.seg_end)) {
+            const int bt0 = (t1 - 1) & ~31;
+            const int n = t1 - bt0;
+            const int64_t b = bt0 >> 5;
+#pragma unroll
+            for (int c = 0; c < kChains; ++c) {
+                uint32_t ew;
+                if constexpr (T::kWarmupRules) ew = (uint32_t)st[c].evh;
+                else ew = 0u;
+                uint32_t* wout = nullptr;
+                if (p.words != nullptr && j0 + c < p.n_traces)
+                    wout = p.words + (((int64_t)q * p.n_traces + (j0 + c)) * p.n_blocks + b) * 2;
+                fold_block(ss[c], wcmd[c], ew, fstart[c], n, b, wout);
+            }
+        }
+    }
+
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) {
+        const int j = j0 + c;
+        if (j >= p.n_traces) continue;
+        T::save(st[c], p, pol, 1, q, seg, j);
+        const int64_t si = stat_idx(p, q, seg, j);
+        p.s_nhi[si] = ss[c].nhi;
+        p.s_nthr[si] = ss[c].nthr;
+        p.s_trans[si] = ss[c].trans;
+        p.s_ev[si] = ss[c].ev;
+        p.s_lock[si] = ss[c].lock;
+        p.s_vmax[si] = vmax;
+        p.s_sthr[si] = ss[c].sthr;
+        p.s_digest[si] = ss[c].digest;
+    }
+}
+
+// One kernel per chain kind T (register allocation is per instantiation): a launch covers the lane
+// policies [p.q_base, p.q_base + p.nq), all of kind T.  CTA = ng tile groups x npw policy warps
+// (<= 8 warps = 2 per SM sub-partition, so up to 255 registers per thread); lane 0 of each group's
+// first warp produces that group's tiles.
+template <class T, int TC, int NSTAGE>
+__global__ void __launch_bounds__(kMaxConsumerWarps * 32, 1)
+    magus_replay_kernel(const __grid_constant__ CUtensorMap tmap, const ReplayParams p) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    using SM = ReplaySmem<TC, NSTAGE>;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    int b = blockIdx.x;
+    const int pblock = b % p.n_pblocks;
+    b /= p.n_pblocks;
+    const int tblock = b % p.n_tblocks;
+    const int seg = b / p.n_tblocks;
+
+    float* tiles = reinterpret_cast<float*>(smem);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)p.ng * NSTAGE * SM::kTileBytes);
+    uint64_t* empty = full + p.ng * NSTAGE;
+    const int npw_active = min(p.npw, p.nq - pblock * p.npw);
+
+    if (threadIdx.x == 0) {
+        ptx::prefetch_tmap(&tmap);
+        for (int i = 0; i < p.ng * NSTAGE; ++i) {
+            ptx::mbar_init(&full[i], 1);
+            ptx::mbar_init(&empty[i], (uint32_t)npw_active);
+        }
+        ptx::fence_mbar_init();
+    }
+    __syncthreads();
+
+    const int g = warp / p.npw, w = warp % p.npw;
+    const int tgroup = tblock * p.ng + g;
+    if (g >= p.ng || tgroup >= p.n_groups || w >= npw_active) return;
+    const int q = p.q_base + pblock * p.npw + w;
+    const DevPolicy pol = p.pol[q];
+    consume<T, TC, NSTAGE>(&tmap, p, pol, q, tgroup, seg, tiles + (size_t)g * NSTAGE * SM::kTileFloats,
+                           &full[g * NSTAGE], &empty[g * NSTAGE], lane, w == 0 && lane == 0);
+}
+
+}  // namespace magus

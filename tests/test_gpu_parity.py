@@ -1,0 +1,257 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.  -m gpu.
+
+Bars (north_star): per-tick cmd / tune-flag bits, counts and 64-bit digests
+bit-exact; T, E, E_pkg, EDP and the savings within 1e-9 relative; generator bytes bit-exact.
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from tests import _parity as PA
+from paper_2502_03796_b200.configs import CONFIGS, pol, sweep64, STATIC_MAX, STATIC_MIN, TDP_DEFAULT
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def M():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    from paper_2502_03796_b200 import magus
+    return magus
+
+
+def gpu_gen(M, seed, n_traces, n_samples, mix, stride=None, offset=0, amp=0.002):
+    stride = stride or ((n_traces + 3) // 4 * 4)
+    tr = torch.empty((n_samples, stride), dtype=torch.float32, device="cuda")
+    w = torch.empty(max(1, n_traces), dtype=torch.float32, device="cuda")
+    M.gen_traces(seed, n_traces, n_samples, mix, tr, w, trace_stride=stride, global_trace_offset=offset,
+                 noise_amp=amp)
+    torch.cuda.synchronize()
+    return tr, w
+
+
+def run_gpu(M, tr, w, policies, n_traces, n_samples, stride, flags=None, segments=0, warmup=0, offset=0,
+            dump=(0, 0), model=None):
+    flags = (M.F_PER_TRACE_STATS | M.F_DUMP_WORDS) if flags is None else flags
+    if dump[1]:
+        flags |= M.F_DUMP_DECISIONS
+    with M.Replay(n_traces, n_samples, PA.gpu_policies(policies), model or M.Model(), trace_stride=stride,
+                  global_trace_offset=offset, flags=flags, dump_first_trace=dump[0], dump_n_traces=dump[1],
+                  tuning_segments=segments, tuning_warmup=warmup) as R:
+        R.run(tr, w)
+        res = R.results()
+        res.geometry = R.geometry()
+    return res
+
+
+def oracle_run(tr_host, w_host, policies, n_traces, model=None):
+    rec, codes, _ = O.replay_batch(tr_host[:, :n_traces], w_host[:n_traces], PA.oracle_policies(policies),
+                                   model or O.Model(), codes=True)
+    return rec, codes
+
+
+# ------------------------------------------------------------------------------------- generator
+
+@pytest.mark.parametrize("mix,n,ns,stride,offset", [(0, 300, 3000, 304, 0), (1, 130, 2100, 132, 7),
+                                                    (2, 77, 4000, 80, 1000), (3, 1, 10000, 4, 0)])
+def test_generator_bytes_match_oracle(M, mix, n, ns, stride, offset):
+    """a11: the CUDA generator writes exactly the oracle generator's bytes (counter-based recipe)."""
+    tr, w = gpu_gen(M, 42 + mix, n, ns, mix, stride, offset)
+    otr, ow = O.gen_traces(O.GenDesc(seed=42 + mix, n_traces=n, n_samples=ns, class_mix=mix, trace_stride=stride,
+                                     global_trace_offset=offset))
+    assert np.array_equal(tr.cpu().numpy().view(np.uint32), otr.view(np.uint32))
+    assert np.array_equal(w.cpu().numpy()[:n].view(np.uint32), ow.view(np.uint32))
+
+
+# ------------------------------------------------------------------------------------- config 1
+
+def test_cfg1_every_tick(M):
+    """cfg 1 (1 trace x 10,000, default policy): every per-tick code byte, every 32-tick cmd/flag word
+    from the replay kernel, and the record, against the oracle."""
+    c = CONFIGS[1]
+    tr, w = gpu_gen(M, c["seed"], 1, c["n_samples"], c["class_mix"], c["stride"])
+    res = run_gpu(M, tr, w, c["policies"], 1, c["n_samples"], c["stride"], dump=(0, 1))
+    rec, codes = oracle_run(tr.cpu().numpy(), w.cpu().numpy(), c["policies"], 1)
+    assert np.array_equal(res.decisions, codes)
+    assert np.array_equal(res.words, PA.pack_words(codes))
+    PA.compare_records(res.per_trace, rec, "cfg1")
+
+
+# ------------------------------------------------------------------------------------- small configs
+
+SMALL = {
+    "cfg2-small": dict(seed=2, n=300, ns=20_000, mix=0, policies=CONFIGS[2]["policies"]),
+    "cfg3-small": dict(seed=3, n=64, ns=4_000, mix=1, policies=CONFIGS[3]["policies"]),
+    "cfg5-small": dict(seed=5, n=257, ns=8_000, mix=2, policies=CONFIGS[5]["policies"]),
+    "mixed-kinds": dict(seed=9, n=131, ns=5_003, mix=1,
+                        policies=[pol(), pol(kind=STATIC_MIN), pol(kind=TDP_DEFAULT, tdp_w=217.0),
+                                  pol(kind=STATIC_MAX), pol(deriv_ticks=3, tune_log_capacity=4,
+                                                            high_freq_threshold=0.75)]),
+}
+
+
+@pytest.mark.parametrize("segments", [0, 1, 7])
+@pytest.mark.parametrize("name", list(SMALL))
+def test_small_configs(M, name, segments):
+    """Several tiles, a ragged trace tail, a ragged final block; automatic, none and forced time
+    segmentation (exercises the speculative segments and the exact fix-up)."""
+    s = SMALL[name]
+    stride = (s["n"] + 3) // 4 * 4
+    tr, w = gpu_gen(M, s["seed"], s["n"], s["ns"], s["mix"], stride)
+    res = run_gpu(M, tr, w, s["policies"], s["n"], s["ns"], stride, segments=segments,
+                  dump=(max(0, s["n"] - 5), 5))
+    rec, codes = oracle_run(tr.cpu().numpy(), w.cpu().numpy(), s["policies"], s["n"])
+    PA.compare_records(res.per_trace, rec, name)
+    assert np.array_equal(res.words, PA.pack_words(codes))
+    assert np.array_equal(res.decisions, codes[:, s["n"] - 5:, :])
+    np.testing.assert_allclose(res.totals, PA.oracle_totals(rec), rtol=1e-9, atol=1e-9)
+    edp = PA.oracle_totals(rec)[:, 3]
+    assert res.totals[res.argmin_policy, 3] <= edp.min() * (1 + 1e-9)
+    if segments == 7:
+        assert res.n_segments == 7
+
+
+@pytest.mark.parametrize("k,C,hf", [(1, 1, 1.0), (2, 10, 0.6), (5, 7, 0.5), (8, 10, 0.4), (9, 10, 0.6),
+                                    (16, 33, 0.6), (33, 64, 0.5), (64, 64, 0.9), (4, 64, 0.3), (7, 40, 0.6),
+                                    (1, 32, 0.6), (3, 33, 0.6)])
+def test_window_and_log_sizes(M, k, C, hf):
+    """Every k in the register-ring specialisations and the generic ring, C up to 64 (64-bit log),
+    with forced segmentation so warm-up lengths scale with k + C."""
+    n, ns = 140, 6000
+    tr, w = gpu_gen(M, 100 + k, n, ns, 1, 140)
+    pols = [pol(deriv_ticks=k, tune_log_capacity=C, high_freq_threshold=hf, inc_threshold=0.5, dec_threshold=-0.5)]
+    res = run_gpu(M, tr, w, pols, n, ns, 140, segments=5)
+    rec, codes = oracle_run(tr.cpu().numpy(), w.cpu().numpy(), pols, n)
+    PA.compare_records(res.per_trace, rec, f"k={k} C={C}")
+    assert np.array_equal(res.words, PA.pack_words(codes))
+
+
+@pytest.mark.parametrize("n,ns", [(1, 1), (1, 31), (3, 33), (5, 32), (128, 64), (129, 95), (4, 1000)])
+def test_tiny_and_ragged(M, n, ns):
+    stride = (n + 3) // 4 * 4
+    tr, w = gpu_gen(M, 7, n, ns, 1, stride)
+    pols = CONFIGS[5]["policies"]
+    res = run_gpu(M, tr, w, pols, n, ns, stride)
+    rec, codes = oracle_run(tr.cpu().numpy(), w.cpu().numpy(), pols, n)
+    PA.compare_records(res.per_trace, rec, f"{n}x{ns}")
+    assert np.array_equal(res.words, PA.pack_words(codes))
+
+
+def test_empty_inputs(M):
+    """n_samples = 0 and n_traces = 0 are valid and give zero totals."""
+    tr = torch.zeros((1, 4), device="cuda")
+    w = torch.zeros(4, device="cuda")
+    res = run_gpu(M, tr, w, CONFIGS[2]["policies"], 3, 0, 4)
+    assert np.all(res.per_trace["T"] == 0) and np.all(res.per_trace["n_hi"] == 0)
+    res = run_gpu(M, tr, w, CONFIGS[2]["policies"], 0, 100, 4)
+    assert np.all(res.totals == 0)
+
+
+def test_handwritten_trace_through_gpu(M):
+    """The hand-derived worked trace ex2 (tests/golden) replayed by the CUDA path in a 4-trace tile."""
+    import json, os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "worked_traces.json")))
+    case = [c for c in g["cases"] if c["name"] == "ex2"][0]
+    D = np.array(case["D"], np.float32)
+    tr = torch.tensor(np.repeat(D[:, None], 4, axis=1)).cuda()
+    w = torch.full((4,), 0.5, device="cuda")
+    res = run_gpu(M, tr, w, [pol(tune_log_capacity=4, high_freq_threshold=0.75)], 4, len(D), 4,
+                  model=M.Model(bw_max_gbps=22.0), dump=(0, 4))
+    levels = "".join("H" if c >> 7 else "L" for c in res.decisions[:, 0, 0])
+    assert levels == case["level"]
+    assert res.per_trace["transitions"][0, 0] == case["transitions"]
+    assert res.per_trace["E"][0, 0] == pytest.approx(case["E"], rel=1e-12)
+    assert res.per_trace["T"][0, 0] == pytest.approx(case["T"], rel=1e-12)
+
+
+def test_invalid_samples_reported(M):
+    """A17: the first invalid (trace, tick) is reported as MAGUS_ERR_TRACE; -0.0 is valid."""
+    n, ns = 300, 2000
+    tr, w = gpu_gen(M, 3, n, ns, 0, 300)
+    tr[100, 200] = -0.0
+    res = run_gpu(M, tr, w, [pol()], n, ns, 300)
+    assert res.status == 0
+    tr[1500, 250] = float("nan")
+    tr[700, 251] = -1.0
+    tr[900, 250] = 25.0
+    with pytest.raises(M.MagusError) as e:
+        run_gpu(M, tr, w, [pol()], n, ns, 300)
+    assert e.value.status == M.ERR_TRACE
+    with M.Replay(n, ns, PA.gpu_policies([pol()]), trace_stride=300) as R:
+        R.run(tr, w)
+        r = R.results(raise_on_trace_error=False)
+    assert (r.err_trace, r.err_tick) == (250, 900)
+
+
+def test_config_errors(M):
+    """invalid configs are rejected at create with the key named."""
+    bad = [pol(deriv_ticks=0), pol(dec_threshold=0.5), pol(inc_threshold=-1.0), pol(tune_log_capacity=65),
+           pol(high_freq_threshold=0.0), pol(kind=TDP_DEFAULT, tdp_margin=1.5), pol(deriv_ticks=65)]
+    for b in bad:
+        with pytest.raises(M.MagusError) as e:
+            M.Replay(4, 10, PA.gpu_policies([b]))
+        assert e.value.status == M.ERR_CONFIG
+    with pytest.raises(M.MagusError) as e:
+        M.Replay(4, 10, PA.gpu_policies([pol()]), M.Model(f_min_ghz=2.5))
+    assert e.value.status == M.ERR_CONFIG and "f_max_ghz" in str(e.value)
+    with pytest.raises(M.MagusError) as e:
+        M.Replay(4, 10, PA.gpu_policies([pol()]), trace_stride=6)
+    assert e.value.status == M.ERR_ALIGN
+
+
+def test_determinism_and_virtual_ranks(M):
+    """K13 on one GPU: two runs are bit-identical; splitting the traces into two shards (global ids)
+    gives the same per-trace records and digests, and the totals agree to 1e-9."""
+    n, ns = 512, 12_000
+    tr, w = gpu_gen(M, 11, n, ns, 1, 512)
+    pols = CONFIGS[5]["policies"]
+    a = run_gpu(M, tr, w, pols, n, ns, 512)
+    b = run_gpu(M, tr, w, pols, n, ns, 512)
+    assert a.per_trace.tobytes() == b.per_trace.tobytes() and np.array_equal(a.totals, b.totals)
+    half = n // 2
+    parts = []
+    for r in range(2):
+        trs, ws = gpu_gen(M, 11, half, ns, 1, half, offset=r * half)
+        parts.append(run_gpu(M, trs, ws, pols, half, ns, half, offset=r * half))
+    joined = np.concatenate([p.per_trace for p in parts])
+    for k in PA.EXACT:
+        assert np.array_equal(joined[k], a.per_trace[k])
+    np.testing.assert_allclose(parts[0].totals[:, :12] + parts[1].totals[:, :12], a.totals[:, :12], rtol=1e-9)
+
+
+def test_host_buffer_path(M):
+    """magus_replay_run_host (the e2e path) gives the same results as the device path."""
+    n, ns = 256, 5000
+    tr, w = gpu_gen(M, 12, n, ns, 0, 256)
+    dev = run_gpu(M, tr, w, CONFIGS[2]["policies"], n, ns, 256)
+    th, wh = tr.cpu().pin_memory(), w.cpu().pin_memory()
+    with M.Replay(n, ns, PA.gpu_policies(CONFIGS[2]["policies"]), trace_stride=256, flags=M.F_PER_TRACE_STATS) as R:
+        R.run_host(th, wh)
+        host = R.results()
+    assert dev.per_trace.tobytes() == host.per_trace.tobytes()
+
+
+# ------------------------------------------------------------------------------------- full size
+
+@pytest.mark.parametrize("cfg", [2, 5, 3])
+def test_full_size_sampled(M, cfg):
+    """BASELINE.json full sizes in the bench's launch configuration (automatic segmentation): the GPU
+    replays every trace; the oracle regenerates a sample of traces one by one (including the ragged
+    last tile) and must match bit-exactly on counts and digests, 1e-9 on energies; totals over all
+    traces are checked against the per-trace records' properties."""
+    c = CONFIGS[cfg]
+    n, ns = c["n_traces"], c["n_samples"]
+    tr, w = gpu_gen(M, c["seed"], n, ns, c["class_mix"], c["stride"])
+    res = run_gpu(M, tr, w, c["policies"], n, ns, c["stride"], flags=M.F_PER_TRACE_STATS)
+    del tr
+    rng = np.random.default_rng(cfg)
+    ids = np.unique(np.r_[rng.choice(n, 24, replace=False), [0, 1, 2, n - 1]])
+    rec, _, _ = O.gen_replay(O.GenDesc(seed=c["seed"], n_traces=n, n_samples=ns, class_mix=c["class_mix"]), ids,
+                             PA.oracle_policies(c["policies"]))
+    PA.compare_records(res.per_trace[ids], rec, f"cfg{cfg}")
+    # totals = fixed-order sums of the records (within 1e-9 of an exactly rounded sum)
+    np.testing.assert_allclose(res.totals, PA.oracle_totals(res.per_trace), rtol=1e-9)
+    print("geometry", res.geometry, "mismatched segments", res.n_mismatched_segments, "rounds", res.fixup_rounds)
