@@ -51,6 +51,7 @@ struct ReplayParams {
     int32_t _pad0;
     int64_t trace_stride;
     const DevPolicy* pol;  // [n_lane]
+    const int32_t* first_low;   // [n_traces] first subsampled tick with D <= B_lo (INT32_MAX if none)
     // chain states, SoA: [e (0 entry, 1 exit)][q][s][j]
     uint8_t* st_f;
     uint64_t* st_log;

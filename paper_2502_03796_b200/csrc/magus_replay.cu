@@ -28,6 +28,7 @@ constexpr int kTC = 16;       // ticks per TMA stage (one 8 KB [16 x 128] fp32 t
 constexpr int kNStage = 3;    // stages per tile group
 using Smem = ReplaySmem<kTC, kNStage>;
 typedef void (*ReplayKernel)(CUtensorMap, ReplayParams);
+typedef void (*RerunKernel)(ReplayParams, EpiParams, FixParams, int, int, int, int, const float*);
 
 // chain kind of a lane policy -> its kernel instantiation (one register allocation per kind)
 int ticker_key(const DevPolicy& q) {
@@ -42,6 +43,20 @@ int ticker_key(const DevPolicy& q) {
 
 template <class T>
 ReplayKernel K() { return (ReplayKernel)magus_replay_kernel<T, kTC, kNStage>; }
+
+// fix-up re-run kernel for a chain kind (nullptr: stateless kinds never mismatch)
+RerunKernel rerun_kernel_for(int key) {
+    switch (key) {
+        case 1: return magus_fix_rerun_kernel<MagusTicker<1, false>>;
+        case 2: return magus_fix_rerun_kernel<MagusTicker<2, false>>;
+        case 4: return magus_fix_rerun_kernel<MagusTicker<4, false>>;
+        case 8: return magus_fix_rerun_kernel<MagusTicker<8, false>>;
+        case 1000 + LANE_TDP: return magus_fix_rerun_kernel<TdpTicker>;
+        case 1000 + LANE_STATIC_MIN: return nullptr;
+        case 1000 + LANE_VALIDATE: return nullptr;
+        default: return key >= 100 ? magus_fix_rerun_kernel<MagusTicker<0, true>> : magus_fix_rerun_kernel<MagusTicker<0, false>>;
+    }
+}
 
 ReplayKernel replay_kernel_for(int key) {
     switch (key) {
@@ -276,13 +291,18 @@ struct magus_replay {
     ReplayParams rp{};
     EpiParams ep{};
     std::vector<LaunchGroup> groups;
+    FixParams fx{};
+    uint32_t* d_wl_count = nullptr;   // [2][G] + cursors [G] + any_unresolved (one allocation)
+    int fix_rounds = 2;
     // device memory
     std::vector<void*> allocs;
     DevPolicy* d_pol = nullptr;
     int* d_smax = nullptr;
     TraceRec* d_rec = nullptr;
     double* d_totals = nullptr;
+    double* d_part = nullptr;         // per-policy chunk partials of the totals
     int* d_argmin = nullptr;
+    int32_t* d_first_low = nullptr;   // [n_traces] speculation aid
     unsigned int* d_flag = nullptr;     // [0] invalid flag, [1] fix rounds, [2..3] fix segments (u64)
     unsigned long long* d_errkey = nullptr;
     uint8_t* d_codes = nullptr;
@@ -424,19 +444,15 @@ static void choose_geometry(magus_replay_t* h, int n_sm) {
     if (d.tuning_segments > 0) {
         S = d.tuning_segments;
     } else {
-        double best = 1e300;
-        const int max_waves = env_int("MAGUS_MAX_WAVES", 4);
-        for (int waves = 1; waves <= max_waves; ++waves) {
-            int s = std::max(1, (n_sm * waves) / base);
-            const int L = (((N + s - 1) / s) + 31) / 32 * 32;
-            if (s > 1 && L < 4 * W) continue;   // segments must dwarf their warm-up
-            s = (N + L - 1) / L;
-            const double cost = std::ceil((double)s * base / n_sm) * (L + (s > 1 ? W : 0));
-            if (cost < best) {
-                best = cost;
-                S = s;
-            }
-        }
+        // enough consumer warps for `target` per SM (each warp holds 4 chains per lane, so one warp per
+        // SM sub-partition already has ILP; more warps hide more latency but need more segments, and
+        // every speculative segment boundary can mismatch)
+        const int target = env_int("MAGUS_TARGET_WARPS_PER_SM", 8);
+        int64_t warps_per_segment = 0;
+        for (const LaunchGroup& g : h->groups) warps_per_segment += (int64_t)p.n_groups * g.nq;
+        S = (int)std::max<int64_t>(1, ((int64_t)n_sm * target) / std::max<int64_t>(1, warps_per_segment));
+        const int L0 = (((N + S - 1) / S) + 31) / 32 * 32;
+        if (S > 1 && L0 < 4 * W) S = std::max(1, N / (4 * W));   // segments must dwarf their warm-up
     }
     int L = (((N + S - 1) / S) + 31) / 32 * 32;
     if (L < 32) L = 32;
@@ -564,7 +580,7 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
     p.bwbits = h->bwbits;
 
     const int Q = p.n_lane, S = p.n_seg;
-    const size_t nst = (size_t)2 * Q * S * std::max(1, d.n_traces);
+    const size_t nst = (size_t)3 * Q * S * std::max(1, d.n_traces);   // entry, exit, staged exit
     const size_t nstat = (size_t)Q * S * std::max(1, d.n_traces);
     cudaError_t ce;
 #define ALLOC(ptr, n)                                         \
@@ -594,7 +610,10 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
     }
     ALLOC(h->d_rec, (size_t)std::max(1, d.n_traces) * d.n_policies);
     ALLOC(h->d_totals, (size_t)d.n_policies * MAGUS_N_TOTALS);
+    ALLOC(h->d_part, (size_t)d.n_policies * MAGUS_N_TOTALS * std::max(1, (d.n_traces + kTotTracesPerBlock - 1) /
+                                                                         kTotTracesPerBlock));
     ALLOC(h->d_argmin, 1);
+    ALLOC(h->d_first_low, (size_t)std::max(1, d.n_traces));
     ALLOC(h->d_flag, 4);
     ALLOC(h->d_errkey, 1);
     if (!h->smax.empty()) {
@@ -603,8 +622,42 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
     if ((d.flags & MAGUS_F_DUMP_DECISIONS) && d.dump_n_traces > 0 && d.n_samples > 0) {
         ALLOC(h->d_codes, (size_t)d.n_samples * d.dump_n_traces * d.n_policies);
     }
+    {   // fix-up worklists
+        const int G = (int)h->groups.size();
+        std::vector<int32_t> grp_of_lane(Q), first(G);
+        std::vector<int64_t> off(G);
+        int64_t total = 0;
+        for (int g = 0; g < G; ++g) {
+            first[g] = h->groups[g].q_base;
+            off[g] = total;
+            for (int q = h->groups[g].q_base; q < h->groups[g].q_base + h->groups[g].nq; ++q) grp_of_lane[q] = g;
+            total += (int64_t)h->groups[g].nq * std::max(0, S - 1) * std::max(1, d.n_traces);
+        }
+        int32_t* d_gol;
+        int32_t* d_first;
+        int64_t* d_off;
+        ALLOC(d_gol, Q);
+        ALLOC(d_first, G);
+        ALLOC(d_off, G);
+        ALLOC(h->fx.wl, (size_t)2 * std::max<int64_t>(1, total));
+        ALLOC(h->d_wl_count, (size_t)3 * G + 1);
+        ALLOC(h->fx.unresolved, (size_t)Q * std::max(1, d.n_traces));
+        cudaMemcpy(d_gol, grp_of_lane.data(), Q * sizeof(int32_t), cudaMemcpyHostToDevice);
+        cudaMemcpy(d_first, first.data(), G * sizeof(int32_t), cudaMemcpyHostToDevice);
+        cudaMemcpy(d_off, off.data(), G * sizeof(int64_t), cudaMemcpyHostToDevice);
+        h->fx.n_fgroups = G;
+        h->fx.cap_total = (int32_t)std::max<int64_t>(1, total);
+        h->fx.grp_of_lane = d_gol;
+        h->fx.grp_first_lane = d_first;
+        h->fx.grp_off = d_off;
+        h->fx.wl_count = h->d_wl_count;
+        h->fx.wl_cursor = h->d_wl_count + 2 * G;
+        h->fx.any_unresolved = h->d_wl_count + 3 * G;
+        h->fix_rounds = std::max(1, env_int("MAGUS_FIX_ROUNDS", 2));
+    }
 #undef ALLOC
     p.pol = h->d_pol;
+    p.first_low = h->d_first_low;
     if ((ce = cudaMemcpy(h->d_pol, h->lane.data(), h->lane.size() * sizeof(DevPolicy), cudaMemcpyHostToDevice)) !=
         cudaSuccess) {
         magus_status s = cuda_fail(h, ce, "cudaMemcpy policies");
@@ -707,6 +760,16 @@ extern "C" magus_status magus_replay_run(magus_replay_t* h, const float* d_trace
     CU(h, cudaMemsetAsync(h->d_flag, 0, 4 * sizeof(unsigned int), s));
     cudaEvent_t* tv = timing ? &h->tev[4 * (h->n_runs % magus_replay::kTimingRing)] : nullptr;
     if (timing) CU(h, cudaEventRecord(tv[0], s));
+    if (has_work && p.n_seg > 1) {
+        // speculation aid: first subsampled low tick of every trace
+        CU(h, cudaMemsetAsync(h->d_first_low, 0x7F, (size_t)d.n_traces * sizeof(int32_t), s));
+        const int sub = 64, per_chunk = 32;
+        const int64_t n_sub = ((int64_t)d.n_samples + sub - 1) / sub;
+        dim3 gfl((unsigned)((d.n_traces + 127) / 128), (unsigned)((n_sub + per_chunk - 1) / per_chunk));
+        magus_first_low_kernel<<<gfl, 128, 0, s>>>(d_trace, d.n_traces, d.n_samples, d.trace_stride, h->B_lo, sub,
+                                                     per_chunk, h->d_first_low);
+        CU(h, cudaGetLastError());
+    }
     if (has_work) {
         for (const LaunchGroup& g : h->groups) {
             ReplayParams pg = p;
@@ -732,8 +795,43 @@ extern "C" magus_status magus_replay_run(magus_replay_t* h, const float* d_trace
     }
     if (timing) CU(h, cudaEventRecord(tv[1], s));
     if (d.n_traces > 0) {
-        dim3 grid((unsigned)((d.n_traces + 7) / 8), (unsigned)p.n_lane);
-        magus_fixup_epilogue_kernel<<<grid, 256, 0, s>>>(p, ep, d_trace);
+        const int G = h->fx.n_fgroups;
+        const FixParams& fx = h->fx;
+        if (has_work && p.n_seg > 1) {
+            // exact fix-up: round 1 checks every segment entry; later rounds only re-check the
+            // successors of segments whose exit changed; a serial walk finishes the rest.
+            CU(h, cudaMemsetAsync(h->d_wl_count, 0, (3 * G + 1) * sizeof(uint32_t), s));
+            CU(h, cudaMemsetAsync(fx.unresolved, 0, (size_t)p.n_lane * d.n_traces, s));
+            dim3 gc((unsigned)((d.n_traces + 255) / 256), (unsigned)(p.n_seg - 1), (unsigned)p.n_lane);
+            magus_fix_check_all_kernel<<<gc, 256, 0, s>>>(p, fx);
+            CU(h, cudaGetLastError());
+            const unsigned rr_blocks = 148 * 4;
+            for (int g = 0; g < G; ++g) {
+                RerunKernel rk = rerun_kernel_for(h->groups[g].key);
+                if (!rk) continue;
+                rk<<<rr_blocks, 256, 0, s>>>(p, ep, fx, g, 0, 1, 1, d_trace);
+                CU(h, cudaGetLastError());
+            }
+            for (int r = 2; r <= h->fix_rounds; ++r) {
+                CU(h, cudaMemsetAsync(fx.wl_count, 0, G * sizeof(uint32_t), s));                 // buf 0
+                magus_fix_check_cand_kernel<<<148, 256, 0, s>>>(p, fx, 1, 0, 0);
+                CU(h, cudaGetLastError());
+                CU(h, cudaMemsetAsync(fx.wl_count + G, 0, 2 * G * sizeof(uint32_t), s));         // buf 1 + cursors
+                for (int g = 0; g < G; ++g) {
+                    RerunKernel rk = rerun_kernel_for(h->groups[g].key);
+                    if (!rk) continue;
+                    rk<<<rr_blocks, 256, 0, s>>>(p, ep, fx, g, 0, 1, r, d_trace);
+                    CU(h, cudaGetLastError());
+                }
+            }
+            magus_fix_check_cand_kernel<<<148, 256, 0, s>>>(p, fx, 1, 0, 1);
+            CU(h, cudaGetLastError());
+            dim3 gs((unsigned)((d.n_traces + 7) / 8), (unsigned)p.n_lane);
+            magus_fix_serial_kernel<<<gs, 256, 0, s>>>(p, ep, fx, d_trace);
+            CU(h, cudaGetLastError());
+        }
+        dim3 ge((unsigned)((d.n_traces + 255) / 256), (unsigned)p.n_lane);
+        magus_epilogue_kernel<<<ge, 256, 0, s>>>(p, ep);
         CU(h, cudaGetLastError());
         if (!h->smax.empty()) {
             const int64_t n = (int64_t)d.n_traces * (int64_t)h->smax.size();
@@ -743,8 +841,14 @@ extern "C" magus_status magus_replay_run(magus_replay_t* h, const float* d_trace
         }
     }
     if (timing) CU(h, cudaEventRecord(tv[2], s));
-    magus_totals_kernel<<<d.n_policies, kTotThreads, 0, s>>>(h->d_rec, d.n_traces, d.n_policies, h->d_totals);
-    CU(h, cudaGetLastError());
+    {
+        const int n_chunks = std::max(1, (d.n_traces + kTotTracesPerBlock - 1) / kTotTracesPerBlock);
+        magus_totals_kernel<<<dim3(d.n_policies, n_chunks), kTotThreads, 0, s>>>(h->d_rec, d.n_traces, d.n_policies,
+                                                                                 h->d_part);
+        CU(h, cudaGetLastError());
+        magus_totals_final_kernel<<<1, 256, 0, s>>>(h->d_part, n_chunks, d.n_policies, d.n_traces, h->d_totals);
+        CU(h, cudaGetLastError());
+    }
     if (d.world > 1) {
         ncclResult_t r = nccl().AllReduce(h->d_totals, h->d_totals, (size_t)d.n_policies * MAGUS_N_TOTALS, ncclFloat64,
                                           ncclSum, h->comm, s);

@@ -1,7 +1,8 @@
 // post_kernels.cuh -- after the replay kernel:
-//   magus_fixup_epilogue_kernel  exact fix-up of speculative time segments (one warp per chain,
-//                                lanes = segments), then the per-trace epilogue (closed-form energy
-//                                model from sufficient statistics)
+//   magus_fix_*_kernel           exact fix-up of speculative time segments: worklist rounds with
+//                                lane-level work stealing, then a serial per-chain fallback
+//   magus_epilogue_kernel        per-trace records (closed-form energy model from sufficient
+//                                statistics)
 //   magus_static_max_kernel      analytic records of STATIC_MAX policies (never throttled, A17/A21)
 //   magus_totals_kernel          per-policy fixed-order sums: thread-strided, warp-shuffle tree, smem
 //   magus_argmin_kernel          argmin over policies of the total EDP (ties -> lowest index, A23)
@@ -64,9 +65,208 @@ __device__ __forceinline__ void finish_record(TraceRec& r, const EpiParams& e, d
     r.digest = digest;
 }
 
-// Re-run segment s of chain (q, j) from the true entry state `tru` next to the speculative one `spec`
-// until they coalesce (checked at 32-tick block ends); returns true if they did.  The statistics
-// delta (true - spec) over the re-run prefix is added to the stored segment statistics.
+// ================================================================================= exact fix-up
+// Segment s >= 1 of chain (q, j) was replayed from a speculative entry E_s.
+// It is exact iff E_s equals the previous segment's true exit X_{s-1}.  Where they differ, the
+// segment is re-run from X_{s-1} next to the speculative trajectory from E_s until the two
+// coalesce (identical state at a 32-tick block end -- from then on they are identical); the
+// statistics delta (true - speculative) over the re-run prefix is added to the segment's stored
+// statistics.  If they never coalesce, the segment's exit changes and segment s+1 is checked
+// again in the next round.  Rounds are worklists processed with lane-level work stealing; a
+// serial per-chain walk finishes whatever is left after the last round.
+
+struct FixParams {
+    int32_t n_fgroups;        // launch groups (one chain kind each)
+    int32_t cap_total;        // items per worklist buffer
+    const int32_t* grp_of_lane;   // [Q]
+    const int32_t* grp_first_lane;   // [n_fgroups] a lane of the group (its DevPolicy gives the kind)
+    const int64_t* grp_off;   // [n_fgroups] offset of the group's region in a worklist buffer
+    uint64_t* wl;             // [2][cap_total] items: q << 48 | s << 32 | j
+    uint32_t* wl_count;       // [2][n_fgroups]
+    uint32_t* wl_cursor;      // [n_fgroups] work-stealing cursors
+    uint8_t* unresolved;      // [Q][n_traces] chains left for the serial walk
+    unsigned int* any_unresolved;
+};
+
+__device__ __forceinline__ uint64_t fix_item(int q, int s, int j) {
+    return ((uint64_t)q << 48) | ((uint64_t)(uint32_t)s << 32) | (uint64_t)(uint32_t)j;
+}
+
+// warp-aggregated append of `item` (lanes with want) to list `buf` of group g
+__device__ __forceinline__ void fix_append(const FixParams& f, int buf, int g, bool want, uint64_t item) {
+    const unsigned m = __ballot_sync(__activemask(), want);
+    if (!want) return;
+    const int leader = __ffs(m) - 1, lane = threadIdx.x & 31;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(&f.wl_count[buf * f.n_fgroups + g], (uint32_t)__popc(m));
+    base = __shfl_sync(m, base, leader);
+    const uint32_t rank = __popc(m & ((1u << lane) - 1u));
+    f.wl[(int64_t)buf * f.cap_total + f.grp_off[g] + base + rank] = item;
+}
+
+template <class T>
+__device__ __forceinline__ bool entry_mismatch(const ReplayParams& p, const DevPolicy& pol, int q, int s, int j) {
+    return !T::stored_equal(p, pol, q, 0, s, 1, s - 1, j);
+}
+
+__device__ __forceinline__ bool entry_mismatch_any(const ReplayParams& p, const DevPolicy& pol, int q, int s, int j) {
+    if (pol.kind == LANE_MAGUS) return entry_mismatch<MagusTicker<0, true>>(p, pol, q, s, j);
+    if (pol.kind == LANE_TDP) return entry_mismatch<TdpTicker>(p, pol, q, s, j);
+    return false;
+}
+
+// copy stored state (e_src, s_src) -> (e_dst, s_dst) for chain (q, j)
+__device__ __forceinline__ void copy_state(const ReplayParams& p, const DevPolicy& pol, int q, int e_src, int s_src,
+                                           int e_dst, int s_dst, int j) {
+    const int64_t a = st_idx(p, e_src, q, s_src, j), b = st_idx(p, e_dst, q, s_dst, j);
+    p.st_f[b] = p.st_f[a];
+    p.st_log[b] = p.st_log[a];
+    if (pol.kind == LANE_MAGUS)
+        for (int r = 0; r < pol.k; ++r)
+            p.st_ring[ring_idx(p, e_dst, q, s_dst, r, j)] = p.st_ring[ring_idx(p, e_src, q, s_src, r, j)];
+}
+
+// Round 1: every (q, s >= 1, j) whose speculative entry differs from the previous exit.
+__global__ void __launch_bounds__(256) magus_fix_check_all_kernel(const ReplayParams p, const FixParams f) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int s = blockIdx.y + 1, q = blockIdx.z;
+    if (j >= p.n_traces) return;
+    const DevPolicy pol = p.pol[q];
+    const bool mism = entry_mismatch_any(p, pol, q, s, j);
+    fix_append(f, 0, f.grp_of_lane[q], mism, fix_item(q, s, j));
+}
+
+// Rounds >= 2: candidates (segments whose predecessor changed its exit in the last round): commit the
+// predecessor's new exit (staged in e = 2) and check the entry again.
+__global__ void __launch_bounds__(256) magus_fix_check_cand_kernel(const ReplayParams p, const FixParams f, int buf_in,
+                                                                   int buf_out, int mark_unresolved) {
+    for (int g = 0; g < f.n_fgroups; ++g) {
+        const uint32_t n = f.wl_count[buf_in * f.n_fgroups + g];
+        for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < ((n + 31u) & ~31u); i += gridDim.x * blockDim.x) {
+            bool mism = false;
+            uint64_t item = 0;
+            if (i < n) {
+                item = f.wl[(int64_t)buf_in * f.cap_total + f.grp_off[g] + i];
+                const int q = (int)(item >> 48), s = (int)((item >> 32) & 0xFFFF), j = (int)(item & 0xFFFFFFFFu);
+                const DevPolicy pol = p.pol[q];
+                copy_state(p, pol, q, 2, s - 1, 1, s - 1, j);
+                mism = entry_mismatch_any(p, pol, q, s, j);
+                if (mism && mark_unresolved) {
+                    f.unresolved[(int64_t)q * p.n_traces + j] = 1;
+                    atomicOr(f.any_unresolved, 1u);
+                }
+            }
+            if (!mark_unresolved) fix_append(f, buf_out, g, mism, item);
+        }
+    }
+}
+
+// Lane-level work stealing over the items of one group; the 32-tick block step stays converged.
+template <class T>
+__device__ void rerun_items(const ReplayParams& p, const EpiParams& e, const FixParams& f, int g, int buf_in,
+                            int buf_out, int round, const float* __restrict__ trace) {
+    using State = typename T::State;
+    const uint32_t n_items = f.wl_count[buf_in * f.n_fgroups + g];
+    State tru, spec;
+    SegStats dt, dp;
+    int q = 0, s = 0, j = 0, t = 0, seg_end = 0;
+    bool active = false;
+    DevPolicy pol = p.pol[f.grp_first_lane[g]];
+    unsigned long long done = 0;
+    bool exhausted = false;
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        // lanes without an item grab the next ones with one warp-aggregated atomic
+        const unsigned need = __ballot_sync(0xffffffffu, !active && !exhausted);
+        if (need) {
+            uint32_t base = 0;
+            const int leader = __ffs(need) - 1;
+            if (lane == leader) base = atomicAdd(&f.wl_cursor[g], (uint32_t)__popc(need));
+            base = __shfl_sync(0xffffffffu, base, leader);
+            const uint32_t idx = base + __popc(need & ((1u << lane) - 1u));
+            if (((need >> lane) & 1u) && idx >= n_items) exhausted = true;
+            if (((need >> lane) & 1u) && idx < n_items) {
+                const uint64_t item = f.wl[(int64_t)buf_in * f.cap_total + f.grp_off[g] + idx];
+                q = (int)(item >> 48);
+                s = (int)((item >> 32) & 0xFFFF);
+                j = (int)(item & 0xFFFFFFFFu);
+                pol = p.pol[q];
+                T::load(tru, p, pol, 1, q, s - 1, j);
+                T::load(spec, p, pol, 0, q, s, j);
+                dt.zero();
+                dp.zero();
+                t = s * p.seg_len;
+                seg_end = min(t + p.seg_len, p.n_samples);
+                active = true;
+            }
+        }
+        if (!__any_sync(0xffffffffu, active)) break;
+        if (active) {
+            const int n = min(32, seg_end - t);
+            float dv[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) dv[i] = (i < n) ? __ldg(trace + (int64_t)(t + i) * p.trace_stride + j) : 0.0f;
+            const uint32_t fst = T::level(tru), fss = T::level(spec);
+            uint32_t wct = 0, wcs = 0;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                if (i < n) {
+                    const TickOut ot = T::template tick<false>(tru, dv[i], pol, p.B_lo, p.B_hi, true, true);
+                    const TickOut os = T::template tick<false>(spec, dv[i], pol, p.B_lo, p.B_hi, true, true);
+                    wct = (wct << 1) | ot.cmd;
+                    wcs = (wcs << 1) | os.cmd;
+                    dt.nthr += ot.thr; dt.lock += ot.hf; if (ot.thr) dt.sthr += (double)dv[i];
+                    dp.nthr += os.thr; dp.lock += os.hf; if (os.thr) dp.sthr += (double)dv[i];
+                }
+            }
+            uint32_t ewt = 0, ews = 0;
+            if constexpr (T::kWarmupRules) {
+                ewt = (uint32_t)tru.evh;
+                ews = (uint32_t)spec.evh;
+            }
+            const int64_t b = t >> 5;
+            uint32_t* wout = p.words ? p.words + (((int64_t)q * p.n_traces + j) * p.n_blocks + b) * 2 : nullptr;
+            fold_block(dt, wct, ewt, fst, n, b, wout);
+            fold_block(dp, wcs, ews, fss, n, b, nullptr);
+            t += n;
+            const bool co = T::equal(tru, spec, pol);
+            if (co || t >= seg_end) {
+                const int64_t si = stat_idx(p, q, s, j);
+                p.s_nhi[si] += dt.nhi - dp.nhi;
+                p.s_nthr[si] += dt.nthr - dp.nthr;
+                p.s_trans[si] += dt.trans - dp.trans;
+                p.s_ev[si] += dt.ev - dp.ev;
+                p.s_lock[si] += dt.lock - dp.lock;
+                p.s_sthr[si] += dt.sthr - dp.sthr;
+                p.s_digest[si] += dt.digest - dp.digest;
+                copy_state(p, pol, q, 1, s - 1, 0, s, j);   // the entry the statistics now belong to
+                if (!co) {                                    // the exit changed: stage it, re-check s+1
+                    if (s + 1 < p.n_seg) T::save(tru, p, pol, 2, q, s, j);
+                    else T::save(tru, p, pol, 1, q, s, j);
+                }
+                ++done;
+                active = false;
+                const bool cand = !co && s + 1 < p.n_seg;
+                if (cand) fix_append(f, buf_out, g, true, fix_item(q, s + 1, j));
+            }
+        }
+    }
+    if (done) {
+        atomicAdd(e.fix_segments, done);
+        atomicMax(e.fix_rounds, round);
+    }
+}
+
+// One instantiation per chain kind (registers are allocated per kind); launched per launch group.
+template <class T>
+__global__ void __launch_bounds__(256) magus_fix_rerun_kernel(const ReplayParams p, const EpiParams e, const FixParams f,
+                                                              int g, int buf_in, int buf_out, int round,
+                                                              const float* __restrict__ trace) {
+    if (f.wl_count[buf_in * f.n_fgroups + g] == 0) return;
+    rerun_items<T>(p, e, f, g, buf_in, buf_out, round, trace);
+}
+
+// ------------------------------------------------------------------ serial walk (fallback, exact)
 template <class T>
 __device__ bool rerun_segment(const ReplayParams& p, const DevPolicy& pol, int q, int s, int j, const float* trace,
                               typename T::State& tru, typename T::State& spec) {
@@ -115,45 +315,78 @@ __device__ bool rerun_segment(const ReplayParams& p, const DevPolicy& pol, int q
     return coalesced;
 }
 
+// One warp per unresolved chain, lanes = segments; rounds until every entry equals the previous exit.
 template <class T>
-__device__ void fixup_and_finish(const ReplayParams& p, const EpiParams& e, const DevPolicy& pol, int q, int j,
-                                 const float* trace, int lane) {
+__device__ void serial_fixup(const ReplayParams& p, const EpiParams& e, const DevPolicy& pol, int q, int j,
+                             const float* trace, int lane) {
     int rounds = 0;
     unsigned long long reruns = 0;
-    if (T::kStateful && p.n_seg > 1) {
-        for (;;) {
-            bool any = false;
-            for (int base = 1; base < p.n_seg; base += 32) {
-                const int s = base + lane;
-                const bool need = s < p.n_seg && !T::stored_equal(p, pol, q, 0, s, 1, s - 1, j);
-                const unsigned m = __ballot_sync(0xffffffffu, need);
-                if (m == 0) continue;
-                any = true;
-                typename T::State tru, spec;
-                if (need) {
-                    T::load(tru, p, pol, 1, q, s - 1, j);
-                    T::load(spec, p, pol, 0, q, s, j);
-                }
-                __syncwarp();
-                if (need) {
-                    const typename T::State entry = tru;   // the entry the corrected statistics belong to
-                    const bool co = rerun_segment<T>(p, pol, q, s, j, trace, tru, spec);
-                    T::save(entry, p, pol, 0, q, s, j);
-                    if (!co) T::save(tru, p, pol, 1, q, s, j);
-                    ++reruns;
-                }
-                __syncwarp();
+    for (;;) {
+        bool any = false;
+        for (int base = 1; base < p.n_seg; base += 32) {
+            const int s = base + lane;
+            const bool need = s < p.n_seg && !T::stored_equal(p, pol, q, 0, s, 1, s - 1, j);
+            const unsigned m = __ballot_sync(0xffffffffu, need);
+            if (m == 0) continue;
+            any = true;
+            typename T::State tru, spec;
+            if (need) {
+                T::load(tru, p, pol, 1, q, s - 1, j);
+                T::load(spec, p, pol, 0, q, s, j);
             }
-            if (!any) break;
-            ++rounds;
+            __syncwarp();
+            if (need) {
+                const typename T::State entry = tru;   // the entry the corrected statistics belong to
+                const bool co = rerun_segment<T>(p, pol, q, s, j, trace, tru, spec);
+                T::save(entry, p, pol, 0, q, s, j);
+                if (!co) T::save(tru, p, pol, 1, q, s, j);
+                ++reruns;
+            }
+            __syncwarp();
         }
+        if (!any) break;
+        ++rounds;
     }
-    // sum the chain's segment statistics: lane-sequential over s = lane, lane+32, ..., then a fixed
-    // xor-shuffle tree (deterministic order)
+    unsigned long long rr = reruns;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) rr += __shfl_xor_sync(0xffffffffu, rr, o);
+    if (lane == 0 && rr) {
+        atomicAdd(e.fix_segments, rr);
+        atomicMax(e.fix_rounds, 100 + rounds);   // >= 100: the serial fallback ran
+    }
+}
+
+__global__ void __launch_bounds__(256) magus_fix_serial_kernel(const ReplayParams p, const EpiParams e, const FixParams f,
+                                                               const float* __restrict__ trace) {
+    if (*f.any_unresolved == 0) return;
+    const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int q = blockIdx.y;
+    if (j >= p.n_traces || !f.unresolved[(int64_t)q * p.n_traces + j]) return;
+    const DevPolicy pol = p.pol[q];
+#define MAGUS_SERIAL(...) serial_fixup<__VA_ARGS__>(p, e, pol, q, j, trace, lane)
+    if (pol.kind == LANE_MAGUS) {
+        if (pol.C <= 32) MAGUS_SERIAL(MagusTicker<0, false>);
+        else MAGUS_SERIAL(MagusTicker<0, true>);
+    } else if (pol.kind == LANE_TDP) {
+        MAGUS_SERIAL(TdpTicker);
+    }
+#undef MAGUS_SERIAL
+}
+
+// ================================================================================= epilogue
+// One thread per (trace, lane policy): the segment statistics summed in segment order, then the
+// closed-form record.
+__global__ void __launch_bounds__(256) magus_epilogue_kernel(const ReplayParams p, const EpiParams e) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int q = blockIdx.y;
+    if (j >= p.n_traces) return;
+    const DevPolicy pol = p.pol[q];
     uint64_t nhi = 0, nthr = 0, trans = 0, ev = 0, lock = 0, dig = 0;
     uint32_t vmax = 0;
     double sthr = 0.0;
-    for (int s = lane; s < p.n_seg; s += 32) {
+#pragma unroll 8
+    for (int s = 0; s < p.n_seg; ++s) {
         const int64_t si = stat_idx(p, q, s, j);
         nhi += p.s_nhi[si];
         nthr += p.s_nthr[si];
@@ -164,71 +397,12 @@ __device__ void fixup_and_finish(const ReplayParams& p, const EpiParams& e, cons
         vmax = max(vmax, p.s_vmax[si]);
         sthr += p.s_sthr[si];
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        nhi += __shfl_xor_sync(0xffffffffu, nhi, o);
-        nthr += __shfl_xor_sync(0xffffffffu, nthr, o);
-        trans += __shfl_xor_sync(0xffffffffu, trans, o);
-        ev += __shfl_xor_sync(0xffffffffu, ev, o);
-        lock += __shfl_xor_sync(0xffffffffu, lock, o);
-        dig += __shfl_xor_sync(0xffffffffu, dig, o);
-        vmax = max(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
-        sthr += __shfl_xor_sync(0xffffffffu, sthr, o);
+    if (pol.policy_index >= 0) {
+        TraceRec& r = e.rec[(int64_t)j * e.n_policies + pol.policy_index];
+        finish_record(r, e, (double)e.w[j], (int64_t)nhi, (int64_t)nthr, (int64_t)trans, (int64_t)ev, (int64_t)lock,
+                      sthr, dig);
     }
-    if (lane == 0) {
-        if (pol.policy_index >= 0) {
-            TraceRec& r = e.rec[(int64_t)j * e.n_policies + pol.policy_index];
-            finish_record(r, e, (double)e.w[j], (int64_t)nhi, (int64_t)nthr, (int64_t)trans, (int64_t)ev,
-                          (int64_t)lock, sthr, dig);
-        }
-        if (vmax > p.bwbits) atomicOr(e.flag_invalid, 1u);
-        if (rounds) atomicMax(e.fix_rounds, rounds);
-    }
-    unsigned long long rr = reruns;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) rr += __shfl_xor_sync(0xffffffffu, rr, o);
-    if (lane == 0 && rr) atomicAdd(e.fix_segments, rr);
-}
-
-__global__ void __launch_bounds__(256) magus_fixup_epilogue_kernel(const ReplayParams p, const EpiParams e,
-                                                                   const float* __restrict__ trace) {
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    const int q = blockIdx.y;
-    const int j = warp;
-    if (j >= p.n_traces) return;
-    const DevPolicy pol = p.pol[q];
-#define MAGUS_FIX(...) fixup_and_finish<__VA_ARGS__>(p, e, pol, q, j, trace, lane)
-    if (pol.kind == LANE_MAGUS) {
-        if (pol.C <= 32) {
-            switch (pol.k) {
-                case 1: MAGUS_FIX(MagusTicker<1, false>); return;
-                case 2: MAGUS_FIX(MagusTicker<2, false>); return;
-                case 3: MAGUS_FIX(MagusTicker<3, false>); return;
-                case 4: MAGUS_FIX(MagusTicker<4, false>); return;
-                case 5: MAGUS_FIX(MagusTicker<5, false>); return;
-                case 6: MAGUS_FIX(MagusTicker<6, false>); return;
-                case 7: MAGUS_FIX(MagusTicker<7, false>); return;
-                case 8: MAGUS_FIX(MagusTicker<8, false>); return;
-                default: MAGUS_FIX(MagusTicker<0, false>); return;
-            }
-        } else {
-            switch (pol.k) {
-                case 1: MAGUS_FIX(MagusTicker<1, true>); return;
-                case 2: MAGUS_FIX(MagusTicker<2, true>); return;
-                case 4: MAGUS_FIX(MagusTicker<4, true>); return;
-                case 8: MAGUS_FIX(MagusTicker<8, true>); return;
-                default: MAGUS_FIX(MagusTicker<0, true>); return;
-            }
-        }
-    } else if (pol.kind == LANE_TDP) {
-        MAGUS_FIX(TdpTicker);
-    } else if (pol.kind == LANE_STATIC_MIN) {
-        MAGUS_FIX(StaticMinTicker<false>);
-    } else {
-        MAGUS_FIX(StaticMinTicker<true>);
-    }
-#undef MAGUS_FIX
+    if (vmax > p.bwbits) atomicOr(e.flag_invalid, 1u);
 }
 
 // STATIC_MAX records: at f_max A = D <= bw_max, never throttled, never a transition or a tune flag.
@@ -242,17 +416,19 @@ __global__ void magus_static_max_kernel(const EpiParams e, int n_traces, const i
 }
 
 constexpr int kTotThreads = 256;
-constexpr int kNTot = 13;   // MAGUS_N_TOTALS
+constexpr int kNTot = 13;              // MAGUS_N_TOTALS
+constexpr int kTotTracesPerBlock = 1024;
 
-// One block per policy: fixed-order sum over traces (thread-strided, then xor-shuffle tree, then the
-// 8 warp partials in order).  Deterministic for a fixed launch configuration.
+// Stage 1: block (p, c) sums traces [c*1024, (c+1)*1024) of policy p in a fixed order (4 per thread
+// sequentially, then an xor-shuffle tree, then the 8 warp partials in order) -> part[p][c].
 __global__ void __launch_bounds__(kTotThreads) magus_totals_kernel(const TraceRec* __restrict__ rec, int n_traces,
-                                                                    int n_policies, double* __restrict__ totals) {
-    const int p = blockIdx.x;
+                                                                    int n_policies, double* __restrict__ part) {
+    const int p = blockIdx.x, c = blockIdx.y;
     double acc[kNTot - 1];
 #pragma unroll
     for (int f = 0; f < kNTot - 1; ++f) acc[f] = 0.0;
-    for (int j = threadIdx.x; j < n_traces; j += kTotThreads) {
+    const int j_end = min(n_traces, (c + 1) * kTotTracesPerBlock);
+    for (int j = c * kTotTracesPerBlock + threadIdx.x; j < j_end; j += kTotThreads) {
         const TraceRec& r = rec[(int64_t)j * n_policies + p];
         acc[0] += r.E;
         acc[1] += r.E_pkg;
@@ -271,18 +447,31 @@ __global__ void __launch_bounds__(kTotThreads) magus_totals_kernel(const TraceRe
     for (int f = 0; f < kNTot - 1; ++f)
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc[f] += __shfl_xor_sync(0xffffffffu, acc[f], o);
-    __shared__ double part[kTotThreads / 32][kNTot - 1];
+    __shared__ double wp[kTotThreads / 32][kNTot - 1];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (lane == 0)
 #pragma unroll
-        for (int f = 0; f < kNTot - 1; ++f) part[warp][f] = acc[f];
+        for (int f = 0; f < kNTot - 1; ++f) wp[warp][f] = acc[f];
     __syncthreads();
     if (threadIdx.x < kNTot - 1) {
-        double s = 0.0;
-        for (int w = 0; w < kTotThreads / 32; ++w) s += part[w][threadIdx.x];
-        totals[p * kNTot + threadIdx.x] = s;
+        double sum = 0.0;
+        for (int w = 0; w < kTotThreads / 32; ++w) sum += wp[w][threadIdx.x];
+        part[((int64_t)p * gridDim.y + c) * (kNTot - 1) + threadIdx.x] = sum;
     }
-    if (threadIdx.x == 0) totals[p * kNTot + kNTot - 1] = (double)n_traces;
+}
+
+// Stage 2 (one block): per policy, the chunk partials in chunk order -> totals[p][13]; then the argmin
+// over policies of the total EDP (ties -> lowest index, A23).  With world > 1 the allreduce runs
+// between this kernel's totals and magus_argmin_kernel.
+__global__ void magus_totals_final_kernel(const double* __restrict__ part, int n_chunks, int n_policies, int n_traces,
+                                          double* __restrict__ totals) {
+    for (int i = threadIdx.x; i < n_policies * (kNTot - 1); i += blockDim.x) {
+        const int p = i / (kNTot - 1), f = i % (kNTot - 1);
+        double sum = 0.0;
+        for (int c = 0; c < n_chunks; ++c) sum += part[((int64_t)p * n_chunks + c) * (kNTot - 1) + f];
+        totals[p * kNTot + f] = sum;
+    }
+    for (int p = threadIdx.x; p < n_policies; p += blockDim.x) totals[p * kNTot + kNTot - 1] = (double)n_traces;
 }
 
 __global__ void magus_argmin_kernel(const double* __restrict__ totals, int n_policies, int* __restrict__ argmin) {
@@ -341,6 +530,24 @@ __global__ void magus_resim_kernel(const ReplayParams p, const float* __restrict
 __global__ void magus_fill_codes_kernel(uint8_t* codes, int64_t n_rows, int P, int pi, uint8_t value) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n_rows) codes[i * P + pi] = value;
+}
+
+// Speculation aid: first_low[j] = the first subsampled tick (stride `sub`) with
+// D <= B_lo, via atomicMin over tick chunks.  Pure performance hint: a wrong guess only costs a re-run.
+__global__ void __launch_bounds__(128) magus_first_low_kernel(const float* __restrict__ trace, int n_traces,
+                                                              int n_samples, int64_t stride, float B_lo, int sub,
+                                                              int per_chunk, int* __restrict__ first_low) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n_traces) return;
+    const int64_t t_begin = (int64_t)blockIdx.y * per_chunk * sub;
+    for (int i = 0; i < per_chunk; ++i) {
+        const int64_t t = t_begin + (int64_t)i * sub;
+        if (t >= n_samples) break;
+        if (__ldg(trace + t * stride + j) <= B_lo) {
+            atomicMin(first_low + j, (int)t);
+            return;
+        }
+    }
 }
 
 // First invalid sample (A17): valid iff bits(D) <= bits(largest fp32 <= bw_max), or D == -0.0.

@@ -101,12 +101,30 @@ __device__ __forceinline__ void consume(const CUtensorMap* tmap, const ReplayPar
             for (int c = 0; c < kChains; ++c)
                 if (j0 + c < p.n_traces) T::save(st[c], p, pol, 0, q, seg, j0 + c);
         }
+        ptx::mbar_wait(&full[slot], (uint32_t)((i / NSTAGE) & 1));
+        const float4* rows = reinterpret_cast<const float4*>(tiles + (size_t)slot * TC * kTracesPerWarp) + lane;
+        if (T::kWarmupRules && i == 0 && seg > 0) {
+            // speculative level at the warm-up start: f_max iff the trace is above
+            // B_lo now and was at or below B_lo before -- a high stretch entered through a rising edge
+            // that Alg. 1 sees even at f_min; a trace never below B_lo is never seen to rise (A14).
+            const float4 d0 = rows[0];
+            const float dd[4] = {d0.x, d0.y, d0.z, d0.w};
+#pragma unroll
+            for (int c = 0; c < kChains; ++c) {
+                const int j = j0 + c;
+                const int fl = j < p.n_traces ? __ldg(p.first_low + j) : 0x7FFFFFFF;
+                T::set_level(st[c], (dd[c] > B_lo && fl < G.tau_w) ? 1u : 0u);
+            }
+            if (t0 == G.seg_start) {   // (no warm-up) re-record the entry with the guessed level
+#pragma unroll
+                for (int c = 0; c < kChains; ++c)
+                    if (j0 + c < p.n_traces) T::save(st[c], p, pol, 0, q, seg, j0 + c);
+            }
+        }
         if ((t0 & 31) == 0) {
 #pragma unroll
             for (int c = 0; c < kChains; ++c) fstart[c] = T::level(st[c]);
         }
-        ptx::mbar_wait(&full[slot], (uint32_t)((i / NSTAGE) & 1));
-        const float4* rows = reinterpret_cast<const float4*>(tiles + (size_t)slot * TC * kTracesPerWarp) + lane;
         const bool counting = t0 >= G.seg_start;
         const int since = t0 - G.tau_w;
         const bool fast = counting && (!T::kWarmupRules || since >= k + C - 1) && (t0 + TC <= G.seg_end);

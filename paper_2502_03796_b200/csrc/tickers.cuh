@@ -24,6 +24,7 @@ struct MagusTicker {
         return magus_tick<K, LOG64, SLOW>(s, D, pol, B_lo, B_hi, ready, full);
     }
     __device__ __forceinline__ static uint32_t level(const State& s) { return s.f; }
+    __device__ __forceinline__ static void set_level(State& s, uint32_t f) { s.f = f; }
     __device__ __forceinline__ static void save(const State& s, const ReplayParams& p, const DevPolicy& pol, int e,
                                                 int q, int seg, int j) {
         const int64_t i = st_idx(p, e, q, seg, j);
@@ -69,6 +70,7 @@ struct TdpTicker {
         return tdp_tick(s.f, D, pol, B_lo, B_hi);
     }
     __device__ __forceinline__ static uint32_t level(const State& s) { return s.f; }
+    __device__ __forceinline__ static void set_level(State& s, uint32_t f) { s.f = f; }
     __device__ __forceinline__ static void save(const State& s, const ReplayParams& p, const DevPolicy&, int e, int q,
                                                 int seg, int j) {
         const int64_t i = st_idx(p, e, q, seg, j);
@@ -105,6 +107,7 @@ struct StaticMinTicker {
         return o;
     }
     __device__ __forceinline__ static uint32_t level(const State&) { return 0; }
+    __device__ __forceinline__ static void set_level(State&, uint32_t) {}
     __device__ __forceinline__ static void save(const State&, const ReplayParams& p, const DevPolicy&, int e, int q,
                                                 int seg, int j) {
         const int64_t i = st_idx(p, e, q, seg, j);
