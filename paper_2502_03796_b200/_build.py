@@ -50,6 +50,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     flags = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2,-ffp-contract=off",
                     "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"), "-I", _nccl_include()]
+    for key in ("MAGUS_TC", "MAGUS_NSTAGE", "MAGUS_MINB"):
+        if os.environ.get(key):
+            flags += [f"-D{key}={int(os.environ[key])}"]
     if os.environ.get("MAGUS_PTXAS_VERBOSE"):
         flags += ["-Xptxas", "-v"]
     for src in SOURCES:

@@ -32,7 +32,7 @@ struct DevPolicy {
     int32_t f0;            // initial level at t = 0 (A10)
     int32_t guess_f;       // level guessed at a speculative segment start
     int32_t policy_index;  // index in the user's policy array
-    int32_t _pad;
+    uint32_t one;          // the constant 1, as data (keeps predicated increments on the FMA pipe)
 };
 
 // run-wide constants and scratch pointers
@@ -63,7 +63,7 @@ struct ReplayParams {
     uint32_t* s_ev;
     uint32_t* s_lock;
     uint32_t* s_vmax;
-    double* s_sthr;
+    double* s_sexc;        // sum over throttled ticks of (D - B_lo), exact in fp64
     uint64_t* s_digest;
     uint32_t* words;       // optional [q][j][n_blocks][2]
 };
@@ -227,11 +227,11 @@ __device__ __forceinline__ TickOut tdp_tick(uint32_t& f, float D, const DevPolic
 // Per-(chain, segment) statistics accumulated over the segment's own ticks.
 struct SegStats {
     uint32_t nhi, nthr, trans, ev, lock, vmax;
-    double sthr;
+    double sexc;
     uint64_t digest;
     __device__ __forceinline__ void zero() {
         nhi = nthr = trans = ev = lock = vmax = 0;
-        sthr = 0.0;
+        sexc = 0.0;
         digest = 0;
     }
 };

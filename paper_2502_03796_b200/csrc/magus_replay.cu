@@ -19,13 +19,20 @@
 
 using namespace magus;
 
+#ifndef MAGUS_TC
+#define MAGUS_TC 8
+#endif
+#ifndef MAGUS_NSTAGE
+#define MAGUS_NSTAGE 3
+#endif
+
 static_assert(sizeof(TraceRec) == sizeof(magus_trace_stats), "TraceRec must mirror magus_trace_stats");
 static_assert(kNTot == MAGUS_N_TOTALS, "totals width");
 
 namespace {
 
-constexpr int kTC = 16;       // ticks per TMA stage (one 8 KB [16 x 128] fp32 tile)
-constexpr int kNStage = 3;    // stages per tile group
+constexpr int kTC = MAGUS_TC;        // ticks per TMA stage ([TC x 128] fp32 tile)
+constexpr int kNStage = MAGUS_NSTAGE;  // stages per tile group
 using Smem = ReplaySmem<kTC, kNStage>;
 typedef void (*ReplayKernel)(CUtensorMap, ReplayParams);
 typedef void (*RerunKernel)(ReplayParams, EpiParams, FixParams, int, int, int, int, const float*);
@@ -406,7 +413,7 @@ static void choose_geometry(magus_replay_t* h, int n_sm) {
     p.n_samples = d.n_samples;
     p.trace_stride = d.trace_stride;
     p.n_groups = (d.n_traces + kTracesPerWarp - 1) / kTracesPerWarp;
-    const int ng_smem = (int)((200 * 1024) / (kNStage * Smem::kTileBytes));
+    const int ng_smem = (int)((100 * 1024) / (kNStage * Smem::kTileBytes));   // 2 CTAs per SM
     h->groups.clear();
     for (int q = 0; q < Q;) {
         LaunchGroup g{};
@@ -447,7 +454,7 @@ static void choose_geometry(magus_replay_t* h, int n_sm) {
         // enough consumer warps for `target` per SM (each warp holds 4 chains per lane, so one warp per
         // SM sub-partition already has ILP; more warps hide more latency but need more segments, and
         // every speculative segment boundary can mismatch)
-        const int target = env_int("MAGUS_TARGET_WARPS_PER_SM", 8);
+        const int target = env_int("MAGUS_TARGET_WARPS_PER_SM", 8 * MAGUS_MINB);
         int64_t warps_per_segment = 0;
         for (const LaunchGroup& g : h->groups) warps_per_segment += (int64_t)p.n_groups * g.nq;
         S = (int)std::max<int64_t>(1, ((int64_t)n_sm * target) / std::max<int64_t>(1, warps_per_segment));
@@ -519,6 +526,7 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
             continue;
         }
         DevPolicy q{};
+        q.one = 1;
         q.policy_index = i;
         q.k = 1;
         q.C = 1;
@@ -552,6 +560,7 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
     }
     if (h->lane.empty()) {   // only STATIC_MAX policies: a validate-only lane still scans the samples (A17)
         DevPolicy q{};
+        q.one = 1;
         q.kind = LANE_VALIDATE;
         q.k = 1;
         q.C = 1;
@@ -601,7 +610,7 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
     ALLOC(p.s_ev, nstat);
     ALLOC(p.s_lock, nstat);
     ALLOC(p.s_vmax, nstat);
-    ALLOC(p.s_sthr, nstat);
+    ALLOC(p.s_sexc, nstat);
     ALLOC(p.s_digest, nstat);
     if (d.flags & MAGUS_F_DUMP_WORDS) {
         ALLOC(p.words, (size_t)Q * std::max(1, d.n_traces) * std::max(1, p.n_blocks) * 2);
@@ -790,7 +799,7 @@ extern "C" magus_status magus_replay_run(magus_replay_t* h, const float* d_trace
         CU(h, cudaMemsetAsync(p.s_ev, 0, nstat * 4, s));
         CU(h, cudaMemsetAsync(p.s_lock, 0, nstat * 4, s));
         CU(h, cudaMemsetAsync(p.s_vmax, 0, nstat * 4, s));
-        CU(h, cudaMemsetAsync(p.s_sthr, 0, nstat * 8, s));
+        CU(h, cudaMemsetAsync(p.s_sexc, 0, nstat * 8, s));
         CU(h, cudaMemsetAsync(p.s_digest, 0, nstat * 8, s));
     }
     if (timing) CU(h, cudaEventRecord(tv[1], s));

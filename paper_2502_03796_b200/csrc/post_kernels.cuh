@@ -34,12 +34,13 @@ struct EpiParams {
 };
 
 // Closed-form energy model of one (trace, policy) from its sufficient statistics (section 8):
-//   T = Delta*((N - n_thr) + w*n_thr) + Delta*(1-w)*S_thr/B_lo
+//   T = Delta*(N + (1-w)*X/B_lo),  X = sum over throttled ticks of (D - B_lo)  (exact in fp64)
 //   E_pkg = P_hi*Delta*n_hi + P_lo*(T - Delta*n_hi),   E = E_pkg + P_gpu*T
 __device__ __forceinline__ void finish_record(TraceRec& r, const EpiParams& e, double w, int64_t n_hi, int64_t n_thr,
-                                              int64_t trans, int64_t ev, int64_t lock, double sthr, uint64_t digest) {
+                                              int64_t trans, int64_t ev, int64_t lock, double sexc, uint64_t digest) {
     const double N = (double)e.n_samples;
-    const double T = e.Delta * ((N - (double)n_thr) + w * (double)n_thr) + e.Delta * (1.0 - w) * sthr / e.B_lo_d;
+    // sum of tau over the ticks: Delta per tick, plus Delta*(1-w)*(D - B_lo)/B_lo per throttled tick
+    const double T = e.Delta * (N + (1.0 - w) * sexc / e.B_lo_d);
     const double T_hi = e.Delta * (double)n_hi;
     const double E_pkg = e.P_hi * T_hi + e.P_lo * (T - T_hi);
     const double E = E_pkg + e.P_gpu * T;
@@ -215,8 +216,8 @@ __device__ void rerun_items(const ReplayParams& p, const EpiParams& e, const Fix
                     const TickOut os = T::template tick<false>(spec, dv[i], pol, p.B_lo, p.B_hi, true, true);
                     wct = (wct << 1) | ot.cmd;
                     wcs = (wcs << 1) | os.cmd;
-                    dt.nthr += ot.thr; dt.lock += ot.hf; if (ot.thr) dt.sthr += (double)dv[i];
-                    dp.nthr += os.thr; dp.lock += os.hf; if (os.thr) dp.sthr += (double)dv[i];
+                    dt.nthr += ot.thr; dt.lock += ot.hf; if (ot.thr) dt.sexc += (double)dv[i] - (double)p.B_lo;
+                    dp.nthr += os.thr; dp.lock += os.hf; if (os.thr) dp.sexc += (double)dv[i] - (double)p.B_lo;
                 }
             }
             uint32_t ewt = 0, ews = 0;
@@ -237,7 +238,7 @@ __device__ void rerun_items(const ReplayParams& p, const EpiParams& e, const Fix
                 p.s_trans[si] += dt.trans - dp.trans;
                 p.s_ev[si] += dt.ev - dp.ev;
                 p.s_lock[si] += dt.lock - dp.lock;
-                p.s_sthr[si] += dt.sthr - dp.sthr;
+                p.s_sexc[si] += dt.sexc - dp.sexc;
                 p.s_digest[si] += dt.digest - dp.digest;
                 copy_state(p, pol, q, 1, s - 1, 0, s, j);   // the entry the statistics now belong to
                 if (!co) {                                    // the exit changed: stage it, re-check s+1
@@ -287,8 +288,8 @@ __device__ bool rerun_segment(const ReplayParams& p, const DevPolicy& pol, int q
             const TickOut os = T::template tick<false>(spec, D, pol, p.B_lo, p.B_hi, true, true);
             wct = (wct << 1) | ot.cmd;
             wcs = (wcs << 1) | os.cmd;
-            dt.nthr += ot.thr; dt.lock += ot.hf; if (ot.thr) dt.sthr += (double)D;
-            dp.nthr += os.thr; dp.lock += os.hf; if (os.thr) dp.sthr += (double)D;
+            dt.nthr += ot.thr; dt.lock += ot.hf; if (ot.thr) dt.sexc += (double)D - (double)p.B_lo;
+            dp.nthr += os.thr; dp.lock += os.hf; if (os.thr) dp.sexc += (double)D - (double)p.B_lo;
         }
         uint32_t ewt = 0, ews = 0;
         if constexpr (T::kWarmupRules) {
@@ -310,7 +311,7 @@ __device__ bool rerun_segment(const ReplayParams& p, const DevPolicy& pol, int q
     p.s_trans[si] += dt.trans - dp.trans;
     p.s_ev[si] += dt.ev - dp.ev;
     p.s_lock[si] += dt.lock - dp.lock;
-    p.s_sthr[si] += dt.sthr - dp.sthr;
+    p.s_sexc[si] += dt.sexc - dp.sexc;
     p.s_digest[si] += dt.digest - dp.digest;
     return coalesced;
 }
@@ -384,7 +385,7 @@ __global__ void __launch_bounds__(256) magus_epilogue_kernel(const ReplayParams 
     const DevPolicy pol = p.pol[q];
     uint64_t nhi = 0, nthr = 0, trans = 0, ev = 0, lock = 0, dig = 0;
     uint32_t vmax = 0;
-    double sthr = 0.0;
+    double sexc = 0.0;
 #pragma unroll 8
     for (int s = 0; s < p.n_seg; ++s) {
         const int64_t si = stat_idx(p, q, s, j);
@@ -395,12 +396,12 @@ __global__ void __launch_bounds__(256) magus_epilogue_kernel(const ReplayParams 
         lock += p.s_lock[si];
         dig += p.s_digest[si];
         vmax = max(vmax, p.s_vmax[si]);
-        sthr += p.s_sthr[si];
+        sexc += p.s_sexc[si];
     }
     if (pol.policy_index >= 0) {
         TraceRec& r = e.rec[(int64_t)j * e.n_policies + pol.policy_index];
         finish_record(r, e, (double)e.w[j], (int64_t)nhi, (int64_t)nthr, (int64_t)trans, (int64_t)ev, (int64_t)lock,
-                      sthr, dig);
+                      sexc, dig);
     }
     if (vmax > p.bwbits) atomicOr(e.flag_invalid, 1u);
 }

@@ -48,10 +48,10 @@ __device__ __forceinline__ SegGeom seg_geom(const ReplayParams& p, int seg) {
 
 // Accumulate one tick of one chain into its segment statistics (counting region only).  The
 // validation maximum (A17) is kept per lane, over its 4 chains.
-__device__ __forceinline__ void acc_tick(SegStats& ss, uint32_t& vmax, const TickOut& o, float D) {
+__device__ __forceinline__ void acc_tick(SegStats& ss, uint32_t& vmax, const TickOut& o, float D, float B_lo) {
     ss.nthr += o.thr;
     ss.lock += o.hf;
-    if (o.thr) ss.sthr += (double)D;
+    if (o.thr) ss.sexc += (double)D - (double)B_lo;   // exact: both fp32 in [B_lo, bw_max] (section 8)
     vmax = max(vmax, __float_as_uint(D));
 }
 
@@ -79,6 +79,7 @@ __device__ __forceinline__ void consume(const CUtensorMap* tmap, const ReplayPar
     }
     const int j0 = tgroup * kTracesPerWarp + lane * kChains;
     const float B_lo = p.B_lo, B_hi = p.B_hi;
+    const double Blo_d = (double)B_lo;
     const int k = pol.k, C = pol.C;
 
     State st[kChains];
@@ -129,15 +130,25 @@ __device__ __forceinline__ void consume(const CUtensorMap* tmap, const ReplayPar
         const int since = t0 - G.tau_w;
         const bool fast = counting && (!T::kWarmupRules || since >= k + C - 1) && (t0 + TC <= G.seg_end);
         if (fast) {
+            uint32_t cnt[kChains];   // ones in each chain's C-window, maintained incrementally in the stage
+#pragma unroll
+            for (int c = 0; c < kChains; ++c) cnt[c] = T::window_count(st[c], pol);
 #pragma unroll
             for (int tt = 0; tt < TC; ++tt) {
                 const float4 d4 = rows[tt * (kTracesPerWarp / 4)];
                 const float d[4] = {d4.x, d4.y, d4.z, d4.w};
+                if constexpr (T::kHasFast4) {
+                    T::fast4(st, d, pol, B_lo, Blo_d, wcmd, ss, vmax, cnt);
+                } else
 #pragma unroll
                 for (int c = 0; c < kChains; ++c) {
-                    const TickOut o = T::template tick<false>(st[c], d[c], pol, B_lo, B_hi, true, true);
-                    wcmd[c] = (wcmd[c] << 1) | o.cmd;
-                    acc_tick(ss[c], vmax, o, d[c]);
+                    if constexpr (T::kHasFast) {
+                        T::fast(st[c], d[c], pol, B_lo, Blo_d, wcmd[c], ss[c], vmax);
+                    } else {
+                        const TickOut o = T::template tick<false>(st[c], d[c], pol, B_lo, B_hi, true, true);
+                        wcmd[c] = (wcmd[c] << 1) | o.cmd;
+                        acc_tick(ss[c], vmax, o, d[c], B_lo);
+                    }
                 }
             }
         } else {
@@ -152,7 +163,7 @@ __device__ __forceinline__ void consume(const CUtensorMap* tmap, const ReplayPar
                 for (int c = 0; c < kChains; ++c) {
                     const TickOut o = T::template tick<true>(st[c], d[c], pol, B_lo, B_hi, ready, lfull);
                     wcmd[c] = (wcmd[c] << 1) | o.cmd;
-                    if (counting) acc_tick(ss[c], vmax, o, d[c]);
+                    if (counting) acc_tick(ss[c], vmax, o, d[c], B_lo);
                 }
             }
         }
@@ -196,7 +207,7 @@ __device__ __forceinline__ void consume(const CUtensorMap* tmap, const ReplayPar
         p.s_ev[si] = ss[c].ev;
         p.s_lock[si] = ss[c].lock;
         p.s_vmax[si] = vmax;
-        p.s_sthr[si] = ss[c].sthr;
+        p.s_sexc[si] = ss[c].sexc;
         p.s_digest[si] = ss[c].digest;
     }
 }
@@ -205,8 +216,11 @@ __device__ __forceinline__ void consume(const CUtensorMap* tmap, const ReplayPar
 // policies [p.q_base, p.q_base + p.nq), all of kind T.  CTA = ng tile groups x npw policy warps
 // (<= 8 warps = 2 per SM sub-partition, so up to 255 registers per thread); lane 0 of each group's
 // first warp produces that group's tiles.
+#ifndef MAGUS_MINB
+#define MAGUS_MINB 2   // CTAs per SM: 2 x 8 warps = 4 warps per SM sub-partition (<= 128 registers)
+#endif
 template <class T, int TC, int NSTAGE>
-__global__ void __launch_bounds__(kMaxConsumerWarps * 32, 1)
+__global__ void __launch_bounds__(kMaxConsumerWarps * 32, MAGUS_MINB)
     magus_replay_kernel(const __grid_constant__ CUtensorMap tmap, const ReplayParams p) {
     extern __shared__ __align__(1024) uint8_t smem[];
     using SM = ReplaySmem<TC, NSTAGE>;
