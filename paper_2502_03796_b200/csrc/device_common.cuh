@@ -171,6 +171,7 @@ struct MagusState {
     using LogT = typename LogWord<LOG64>::T;
     uint32_t f;     // level in effect for the next tick (0 LO, 1 HI)
     LogT evh;       // tune-flag history, newest at bit 0; the log is the low C bits
+    uint32_t cnt;   // ones in the log (derived from evh; carried so the fast path updates it incrementally)
     Ring<K> ring;
 };
 
@@ -198,6 +199,7 @@ __device__ __forceinline__ TickOut magus_tick(MagusState<K, LOG64>& s, float D, 
     const uint32_t ev = (inc || dec) ? 1u : 0u;
     s.evh = (s.evh << 1) | (typename LogWord<LOG64>::T)ev;
     const uint32_t cnt = popc_log<LOG64>(s.evh & (typename LogWord<LOG64>::T)pol.logmask);
+    s.cnt = cnt;
     bool hf = cnt >= (uint32_t)pol.s_min;
     if (SLOW && !full) hf = false;
     const uint32_t cmd = (hf || inc || (s.f && !dec)) ? 1u : 0u;
@@ -235,6 +237,20 @@ struct SegStats {
         digest = 0;
     }
 };
+
+// Full-block fold (n == 32) with the block's hash key b*phi supplied by the caller (kept incrementally).
+__device__ __forceinline__ void fold_full_block(SegStats& st, uint32_t wcmd, uint32_t ew, uint32_t fstart,
+                                                uint64_t bkey, uint32_t* words_out) {
+    const uint32_t lw = (wcmd >> 1) | (fstart << 31);   // level in effect per tick
+    st.trans += __popc(wcmd ^ lw);
+    st.nhi += __popc(lw);
+    st.ev += __popc(ew);
+    st.digest += mix64((((uint64_t)wcmd << 32) | (uint64_t)ew) ^ bkey);
+    if (words_out) {
+        words_out[0] = wcmd;
+        words_out[1] = ew;
+    }
+}
 
 // Fold one 32-tick block [bt0, bt0 + n): `wcmd` holds the block's cmd bits (newest at bit 0, plus the
 // previous tick's cmd above them), `ew` the tune flags (same alignment), fstart the level at bt0.

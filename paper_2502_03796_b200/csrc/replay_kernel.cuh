@@ -69,18 +69,22 @@ __device__ __forceinline__ void consume(const CUtensorMap* tmap, const ReplayPar
                                         int tgroup, int seg, float* tiles, uint64_t* full, uint64_t* empty, int lane,
                                         bool producer) {
     using State = typename T::State;
+    static_assert(32 % TC == 0, "a 32-tick digest block must be whole stages");
     const SegGeom G = seg_geom<TC>(p, seg);
     const int x = tgroup * kTracesPerWarp;
+    constexpr uint32_t kTileBytes = TC * kTracesPerWarp * 4;
+    const uint32_t tile0 = ptx::smem_u32(tiles), full0 = ptx::smem_u32(full), empty0 = ptx::smem_u32(empty);
     uint64_t cpol = 0;
     if (producer) {
         cpol = ptx::policy_evict_first();
         for (int i = 0; i < NSTAGE && i < G.n_stages; ++i)
-            issue_stage<TC>(tmap, tiles + (size_t)i * TC * kTracesPerWarp, &full[i], x, G.tau_w + i * TC, cpol);
+            ptx::tma_load_2d_u32(tile0 + i * kTileBytes, tmap, full0 + 8 * i, x, G.tau_w + i * TC, kTileBytes, cpol);
     }
     const int j0 = tgroup * kTracesPerWarp + lane * kChains;
     const float B_lo = p.B_lo, B_hi = p.B_hi;
     const double Blo_d = (double)B_lo;
     const int k = pol.k, C = pol.C;
+    const int warm_ticks = T::kWarmupRules ? k + C - 1 : 0;   // ticks before Alg. 1/2 are fully defined
 
     State st[kChains];
     SegStats ss[kChains];
@@ -91,108 +95,108 @@ __device__ __forceinline__ void consume(const CUtensorMap* tmap, const ReplayPar
         T::init(st[c], pol, seg == 0);
         ss[c].zero();
         wcmd[c] = 0;
-        fstart[c] = T::level(st[c]);
     }
 
-    for (int i = 0; i < G.n_stages; ++i) {
-        const int slot = i % NSTAGE;
-        const int t0 = G.tau_w + i * TC;
-        if (t0 == G.seg_start) {
-#pragma unroll
-            for (int c = 0; c < kChains; ++c)
-                if (j0 + c < p.n_traces) T::save(st[c], p, pol, 0, q, seg, j0 + c);
-        }
-        ptx::mbar_wait(&full[slot], (uint32_t)((i / NSTAGE) & 1));
-        const float4* rows = reinterpret_cast<const float4*>(tiles + (size_t)slot * TC * kTracesPerWarp) + lane;
-        if (T::kWarmupRules && i == 0 && seg > 0) {
-            // speculative level at the warm-up start: f_max iff the trace is above
-            // B_lo now and was at or below B_lo before -- a high stretch entered through a rising edge
-            // that Alg. 1 sees even at f_min; a trace never below B_lo is never seen to rise (A14).
-            const float4 d0 = rows[0];
-            const float dd[4] = {d0.x, d0.y, d0.z, d0.w};
+    int i = 0;           // stage index
+    int slot = 0;        // i % NSTAGE
+    uint32_t phase = 0;  // (i / NSTAGE) & 1
+    uint64_t bkey = (uint64_t)(G.tau_w >> 5) * kPhi;   // digest key of the current block, b * phi
+    // 32-tick digest blocks; segment starts and warm-up starts are block aligned
+    for (int bt0 = G.tau_w; bt0 < G.seg_end; bt0 += 32) {
+        if (bt0 == G.seg_start) {   // the segment's own ticks start: record the entry, reset the statistics
 #pragma unroll
             for (int c = 0; c < kChains; ++c) {
-                const int j = j0 + c;
-                const int fl = j < p.n_traces ? __ldg(p.first_low + j) : 0x7FFFFFFF;
-                T::set_level(st[c], (dd[c] > B_lo && fl < G.tau_w) ? 1u : 0u);
-            }
-            if (t0 == G.seg_start) {   // (no warm-up) re-record the entry with the guessed level
-#pragma unroll
-                for (int c = 0; c < kChains; ++c)
-                    if (j0 + c < p.n_traces) T::save(st[c], p, pol, 0, q, seg, j0 + c);
+                if (j0 + c < p.n_traces) T::save(st[c], p, pol, 0, q, seg, j0 + c);
+                ss[c].zero();
             }
         }
-        if ((t0 & 31) == 0) {
 #pragma unroll
-            for (int c = 0; c < kChains; ++c) fstart[c] = T::level(st[c]);
-        }
-        const bool counting = t0 >= G.seg_start;
-        const int since = t0 - G.tau_w;
-        const bool fast = counting && (!T::kWarmupRules || since >= k + C - 1) && (t0 + TC <= G.seg_end);
-        if (fast) {
-            uint32_t cnt[kChains];   // ones in each chain's C-window, maintained incrementally in the stage
+        for (int c = 0; c < kChains; ++c) fstart[c] = T::level(st[c]);
+        const bool counting = bt0 >= G.seg_start;
+        for (int sub = 0; sub < 32 / TC && i < G.n_stages; ++sub) {
+            const int t0 = bt0 + sub * TC;
+            ptx::mbar_wait_u32(full0 + 8 * slot, phase);
+            const float4* rows = reinterpret_cast<const float4*>(tiles + (size_t)slot * TC * kTracesPerWarp) + lane;
+            const bool fast = (t0 - G.tau_w >= warm_ticks) && (t0 + TC <= G.seg_end);
+            if (fast) {
 #pragma unroll
-            for (int c = 0; c < kChains; ++c) cnt[c] = T::window_count(st[c], pol);
+                for (int tt = 0; tt < TC; ++tt) {
+                    const float4 d4 = rows[tt * (kTracesPerWarp / 4)];
+                    const float d[4] = {d4.x, d4.y, d4.z, d4.w};
+                    if constexpr (T::kHasFast4) {
+                        T::fast4(st, d, pol, B_lo, Blo_d, wcmd, ss, vmax);
+                    } else
 #pragma unroll
-            for (int tt = 0; tt < TC; ++tt) {
-                const float4 d4 = rows[tt * (kTracesPerWarp / 4)];
-                const float d[4] = {d4.x, d4.y, d4.z, d4.w};
-                if constexpr (T::kHasFast4) {
-                    T::fast4(st, d, pol, B_lo, Blo_d, wcmd, ss, vmax, cnt);
-                } else
+                    for (int c = 0; c < kChains; ++c) {
+                        if constexpr (T::kHasFast) {
+                            T::fast(st[c], d[c], pol, B_lo, Blo_d, wcmd[c], ss[c], vmax);
+                        } else {
+                            const TickOut o = T::template tick<false>(st[c], d[c], pol, B_lo, B_hi, true, true);
+                            wcmd[c] = (wcmd[c] << 1) | o.cmd;
+                            acc_tick(ss[c], vmax, o, d[c], B_lo);
+                        }
+                    }
+                }
+            } else {
+                if (T::kWarmupRules && i == 0 && seg > 0) {
+                    // speculative level at the warm-up start: f_max iff the trace is above
+                    // B_lo now and was at or below B_lo before -- a high stretch entered through a rising edge
+                    // that Alg. 1 sees even at f_min; a trace never below B_lo is never seen to rise (A14).
+                    const float4 d0 = rows[0];
+                    const float dd[4] = {d0.x, d0.y, d0.z, d0.w};
 #pragma unroll
-                for (int c = 0; c < kChains; ++c) {
-                    if constexpr (T::kHasFast) {
-                        T::fast(st[c], d[c], pol, B_lo, Blo_d, wcmd[c], ss[c], vmax);
-                    } else {
-                        const TickOut o = T::template tick<false>(st[c], d[c], pol, B_lo, B_hi, true, true);
+                    for (int c = 0; c < kChains; ++c) {
+                        const int j = j0 + c;
+                        const int fl = j < p.n_traces ? __ldg(p.first_low + j) : 0x7FFFFFFF;
+                        T::set_level(st[c], (dd[c] > B_lo && fl < G.tau_w) ? 1u : 0u);
+                        fstart[c] = T::level(st[c]);
+                    }
+                }
+                for (int tt = 0; tt < TC; ++tt) {
+                    const int t = t0 + tt;
+                    if (t >= G.seg_end) break;
+                    const float4 d4 = rows[tt * (kTracesPerWarp / 4)];
+                    const float d[4] = {d4.x, d4.y, d4.z, d4.w};
+                    const bool ready = (t - G.tau_w) >= k;
+                    const bool lfull = (t - G.tau_w) >= k + C - 1;
+#pragma unroll
+                    for (int c = 0; c < kChains; ++c) {
+                        const TickOut o = T::template tick<true>(st[c], d[c], pol, B_lo, B_hi, ready, lfull);
                         wcmd[c] = (wcmd[c] << 1) | o.cmd;
                         acc_tick(ss[c], vmax, o, d[c], B_lo);
                     }
                 }
             }
-        } else {
-            for (int tt = 0; tt < TC; ++tt) {
-                const int t = t0 + tt;
-                if (t >= G.seg_end) break;
-                const float4 d4 = rows[tt * (kTracesPerWarp / 4)];
-                const float d[4] = {d4.x, d4.y, d4.z, d4.w};
-                const bool ready = (t - G.tau_w) >= k;
-                const bool lfull = (t - G.tau_w) >= k + C - 1;
-#pragma unroll
-                for (int c = 0; c < kChains; ++c) {
-                    const TickOut o = T::template tick<true>(st[c], d[c], pol, B_lo, B_hi, ready, lfull);
-                    wcmd[c] = (wcmd[c] << 1) | o.cmd;
-                    if (counting) acc_tick(ss[c], vmax, o, d[c], B_lo);
-                }
+            // release the stage; the group's producer lane refills it with stage i + NSTAGE once every
+            // policy warp of the group has released it
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive_u32(empty0 + 8 * slot);
+            if (producer && i + NSTAGE < G.n_stages) {
+                ptx::mbar_wait_u32(empty0 + 8 * slot, phase);
+                ptx::tma_load_2d_u32(tile0 + slot * kTileBytes, tmap, full0 + 8 * slot, x,
+                                     G.tau_w + (i + NSTAGE) * TC, kTileBytes, cpol);
+            }
+            ++i;
+            if (++slot == NSTAGE) {
+                slot = 0;
+                phase ^= 1u;
             }
         }
-        // release the stage; the group's producer lane refills it with stage i + NSTAGE once every
-        // policy warp of the group has released it
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&empty[slot]);
-        if (producer && i + NSTAGE < G.n_stages) {
-            ptx::mbar_wait(&empty[slot], (uint32_t)((i / NSTAGE) & 1));
-            issue_stage<TC>(tmap, tiles + (size_t)slot * TC * kTracesPerWarp, &full[slot], x,
-                            G.tau_w + (i + NSTAGE) * TC, cpol);
-        }
-
-        const int t1 = min(t0 + TC, G.seg_end);
-        if (counting && (((t1 & 31) == 0) || t1 == G.seg_end)) {
-            const int bt0 = (t1 - 1) & ~31;
-            const int n = t1 - bt0;
+        if (counting) {
+            const int n = min(32, G.seg_end - bt0);
             const int64_t b = bt0 >> 5;
+            uint32_t* wbase = p.words ? p.words + ((int64_t)q * p.n_traces * p.n_blocks + b) * 2 : nullptr;
 #pragma unroll
             for (int c = 0; c < kChains; ++c) {
                 uint32_t ew;
                 if constexpr (T::kWarmupRules) ew = (uint32_t)st[c].evh;
                 else ew = 0u;
-                uint32_t* wout = nullptr;
-                if (p.words != nullptr && j0 + c < p.n_traces)
-                    wout = p.words + (((int64_t)q * p.n_traces + (j0 + c)) * p.n_blocks + b) * 2;
-                fold_block(ss[c], wcmd[c], ew, fstart[c], n, b, wout);
+                uint32_t* wout = (wbase && j0 + c < p.n_traces) ? wbase + (int64_t)(j0 + c) * p.n_blocks * 2 : nullptr;
+                if (n == 32) fold_full_block(ss[c], wcmd[c], ew, fstart[c], bkey, wout);
+                else fold_block(ss[c], wcmd[c], ew, fstart[c], n, b, wout);
             }
         }
+        bkey += kPhi;
     }
 
 #pragma unroll

@@ -17,6 +17,7 @@ struct MagusTicker {
     __device__ __forceinline__ static void init(State& s, const DevPolicy& pol, bool exact_start) {
         s.f = exact_start ? (uint32_t)pol.f0 : (uint32_t)pol.guess_f;
         s.evh = 0;
+        s.cnt = 0;
         s.ring.clear(pol.k);
     }
     template <bool SLOW>
@@ -31,16 +32,15 @@ struct MagusTicker {
     }
     // The 4 chains of a lane in one interleaved PTX block (tick4_asm.cuh, generated).
     __device__ __forceinline__ static void fast4(State* s, const float* D, const DevPolicy& pol, float B_lo,
-                                                 double Blo_d, uint32_t* wcmd, SegStats* ss, uint32_t& vmax,
-                                                 uint32_t* cnt) {
+                                                 double Blo_d, uint32_t* wcmd, SegStats* ss, uint32_t& vmax) {
         if constexpr (!LOG64) {
             double ad0, ad1, ad2, ad3;
             uint32_t e0 = s[0].evh, e1 = s[1].evh, e2 = s[2].evh, e3 = s[3].evh;
             const uint32_t bitc = 1u << (pol.C - 1), mone = 0xFFFFFFFFu * pol.one;
             MAGUS_TICK4_ASM(s[0].f, s[1].f, s[2].f, s[3].f, ad0, ad1, ad2, ad3, e0, e1, e2, e3, ss[0].sexc, ss[1].sexc,
                             ss[2].sexc, ss[3].sexc, ss[0].lock, ss[1].lock, ss[2].lock, ss[3].lock, ss[0].nthr,
-                            ss[1].nthr, ss[2].nthr, ss[3].nthr, wcmd[0], wcmd[1], wcmd[2], wcmd[3], cnt[0], cnt[1],
-                            cnt[2], cnt[3], vmax, D[0], D[1], D[2], D[3], s[0].ring.oldest(pol.k),
+                            ss[1].nthr, ss[2].nthr, ss[3].nthr, wcmd[0], wcmd[1], wcmd[2], wcmd[3], s[0].cnt, s[1].cnt,
+                            s[2].cnt, s[3].cnt, vmax, D[0], D[1], D[2], D[3], s[0].ring.oldest(pol.k),
                             s[1].ring.oldest(pol.k), s[2].ring.oldest(pol.k), s[3].ring.oldest(pol.k),
                             __float_as_uint(D[0]), __float_as_uint(D[1]), __float_as_uint(D[2]), __float_as_uint(D[3]),
                             B_lo, Blo_d, pol.dinc, pol.ddec, bitc, (uint32_t)pol.s_min, pol.one, mone);
@@ -108,6 +108,7 @@ struct MagusTicker {
             const bool ev = inc || (d < pol.ddec);
             s.evh = (s.evh << 1) | (LogT)(ev ? 1u : 0u);
             const uint32_t cnt = popc_log<LOG64>(s.evh & (LogT)pol.logmask);
+            s.cnt = cnt;
             const bool hf = cnt >= (uint32_t)pol.s_min;
             f = (hf || inc || (!lo && !ev)) ? 1u : 0u;
             wcmd = (wcmd << 1) | f;
@@ -132,6 +133,7 @@ struct MagusTicker {
         const int64_t i = st_idx(p, e, q, seg, j);
         s.f = p.st_f[i];
         s.evh = (LogT)p.st_log[i];
+        s.cnt = popc_log<LOG64>(s.evh & (LogT)pol.logmask);
         s.ring.set_all(p.st_ring + ring_idx(p, e, q, seg, 0, j), pol.k, (int64_t)p.n_traces);
     }
     // exact equality of the two stored states (e0, s0) and (e1, s1): level, log bits, ring values
@@ -160,7 +162,7 @@ struct TdpTicker {
     __device__ __forceinline__ static void fast(State&, float, const DevPolicy&, float, double, uint32_t&, SegStats&,
                                                 uint32_t&) {}
     __device__ __forceinline__ static void fast4(State*, const float*, const DevPolicy&, float, double, uint32_t*,
-                                                 SegStats*, uint32_t&, uint32_t*) {}
+                                                 SegStats*, uint32_t&) {}
     static constexpr bool kStateful = true;
     static constexpr bool kWarmupRules = false;
     __device__ __forceinline__ static void init(State& s, const DevPolicy& pol, bool exact_start) {
@@ -201,7 +203,7 @@ struct StaticMinTicker {
     __device__ __forceinline__ static void fast(State&, float, const DevPolicy&, float, double, uint32_t&, SegStats&,
                                                 uint32_t&) {}
     __device__ __forceinline__ static void fast4(State*, const float*, const DevPolicy&, float, double, uint32_t*,
-                                                 SegStats*, uint32_t&, uint32_t*) {}
+                                                 SegStats*, uint32_t&) {}
     static constexpr bool kStateful = false;
     static constexpr bool kWarmupRules = false;
     __device__ __forceinline__ static void init(State& s, const DevPolicy&, bool) { s.f = 0; }
