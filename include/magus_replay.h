@@ -182,13 +182,14 @@ magus_status magus_replay_run_host(magus_replay_t* h, const float* trace, const 
  * Returns MAGUS_ERR_TRACE (with err_trace/err_tick) if a sample was invalid. */
 magus_status magus_replay_results(magus_replay_t* h, magus_results* out);
 
-/* Device milliseconds of the last run's kernels (needs MAGUS_F_TIMING; waits for the run):
- * out[0] replay kernel, out[1] fix-up + epilogue, out[2] totals + allreduce + argmin, out[3] whole run. */
-magus_status magus_replay_kernel_times(magus_replay_t* h, float out_ms[4]);
+/* Device milliseconds of the last run's kernels (needs MAGUS_F_TIMING; waits for the run), CUDA events
+ * on the run's stream: out[0] replay kernel(s), out[1] fix-up + epilogue, out[2] totals + allreduce +
+ * argmin, out[3] whole run, out[4] speculation pre-pass. */
+magus_status magus_replay_kernel_times(magus_replay_t* h, float out_ms[5]);
 
 /* Same four intervals averaged over the last n_last runs (at most 256 are kept), e.g. the K runs of a
  * timed benchmark region.  Waits for the last run. */
-magus_status magus_replay_timing_summary(magus_replay_t* h, int32_t n_last, float out_ms[4]);
+magus_status magus_replay_timing_summary(magus_replay_t* h, int32_t n_last, float out_ms[5]);
 
 void         magus_replay_destroy(magus_replay_t* h);
 const char*  magus_replay_last_error(const magus_replay_t* h);

@@ -56,15 +56,17 @@ struct ReplayParams {
     uint8_t* st_f;
     uint64_t* st_log;
     float* st_ring;        // [e][q][s][r < kr][j]
-    // per (q, s, j) statistics of the segment's own ticks
-    uint32_t* s_nhi;
-    uint32_t* s_nthr;
-    uint32_t* s_trans;
-    uint32_t* s_ev;
-    uint32_t* s_lock;
-    uint32_t* s_vmax;
-    double* s_sexc;        // sum over throttled ticks of (D - B_lo), exact in fp64
-    uint64_t* s_digest;
+    // per-chain totals [q][j], accumulated with atomics by every segment (and by the fix-up deltas):
+    // integers add modulo 2^32 / 2^64 and the throttling excess is an exact fp64 sum, so the result
+    // does not depend on the order of the additions
+    uint32_t* c_nhi;
+    uint32_t* c_nthr;
+    uint32_t* c_trans;
+    uint32_t* c_ev;
+    uint32_t* c_lock;
+    uint32_t* c_vmax;
+    double* c_sexc;        // sum over throttled ticks of (D - B_lo)
+    unsigned long long* c_digest;
     uint32_t* words;       // optional [q][j][n_blocks][2]
 };
 
@@ -74,8 +76,8 @@ __host__ __device__ __forceinline__ int64_t st_idx(const ReplayParams& p, int e,
 __host__ __device__ __forceinline__ int64_t ring_idx(const ReplayParams& p, int e, int q, int s, int r, int j) {
     return (((int64_t)(e * p.n_lane + q) * p.n_seg + s) * p.kr + r) * p.n_traces + j;
 }
-__host__ __device__ __forceinline__ int64_t stat_idx(const ReplayParams& p, int q, int s, int j) {
-    return ((int64_t)q * p.n_seg + s) * p.n_traces + j;
+__host__ __device__ __forceinline__ int64_t chain_idx(const ReplayParams& p, int q, int j) {
+    return (int64_t)q * p.n_traces + j;
 }
 
 __host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {   // splitmix64 finaliser
@@ -237,6 +239,19 @@ struct SegStats {
         digest = 0;
     }
 };
+
+// Add a segment's statistics (or a fix-up delta) to its chain's totals.
+__device__ __forceinline__ void add_to_chain(const ReplayParams& p, int q, int j, uint32_t nhi, uint32_t nthr,
+                                             uint32_t trans, uint32_t ev, uint32_t lock, double sexc, uint64_t digest) {
+    const int64_t ci = chain_idx(p, q, j);
+    if (nhi) atomicAdd(p.c_nhi + ci, nhi);
+    if (nthr) atomicAdd(p.c_nthr + ci, nthr);
+    if (trans) atomicAdd(p.c_trans + ci, trans);
+    if (ev) atomicAdd(p.c_ev + ci, ev);
+    if (lock) atomicAdd(p.c_lock + ci, lock);
+    if (sexc != 0.0) atomicAdd(p.c_sexc + ci, sexc);
+    if (digest) atomicAdd(p.c_digest + ci, (unsigned long long)digest);
+}
 
 // Full-block fold (n == 32) with the block's hash key b*phi supplied by the caller (kept incrementally).
 __device__ __forceinline__ void fold_full_block(SegStats& st, uint32_t wcmd, uint32_t ew, uint32_t fstart,

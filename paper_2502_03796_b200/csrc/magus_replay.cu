@@ -31,6 +31,7 @@ static_assert(kNTot == MAGUS_N_TOTALS, "totals width");
 
 namespace {
 
+constexpr size_t kChainBytes = 8 + 8 + 6 * 4;   // sexc, digest, nhi, nthr, trans, ev, lock, vmax
 constexpr int kTC = MAGUS_TC;        // ticks per TMA stage ([TC x 128] fp32 tile)
 constexpr int kNStage = MAGUS_NSTAGE;  // stages per tile group
 using Smem = ReplaySmem<kTC, kNStage>;
@@ -310,6 +311,8 @@ struct magus_replay {
     double* d_part = nullptr;         // per-policy chunk partials of the totals
     int* d_argmin = nullptr;
     int32_t* d_first_low = nullptr;   // [n_traces] speculation aid
+    uint8_t* d_chain = nullptr;       // per-chain totals (ReplayParams::c_*)
+    unsigned int* d_finish = nullptr; // totals kernel: last-block counter
     unsigned int* d_flag = nullptr;     // [0] invalid flag, [1] fix rounds, [2..3] fix segments (u64)
     unsigned long long* d_errkey = nullptr;
     uint8_t* d_codes = nullptr;
@@ -590,7 +593,7 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
 
     const int Q = p.n_lane, S = p.n_seg;
     const size_t nst = (size_t)3 * Q * S * std::max(1, d.n_traces);   // entry, exit, staged exit
-    const size_t nstat = (size_t)Q * S * std::max(1, d.n_traces);
+    const size_t nchain = (size_t)Q * std::max(1, d.n_traces);
     cudaError_t ce;
 #define ALLOC(ptr, n)                                         \
     if ((ce = dalloc(h, &(ptr), (n))) != cudaSuccess) {       \
@@ -604,14 +607,15 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
     ALLOC(p.st_f, nst);
     ALLOC(p.st_log, nst);
     ALLOC(p.st_ring, nst * p.kr);
-    ALLOC(p.s_nhi, nstat);
-    ALLOC(p.s_nthr, nstat);
-    ALLOC(p.s_trans, nstat);
-    ALLOC(p.s_ev, nstat);
-    ALLOC(p.s_lock, nstat);
-    ALLOC(p.s_vmax, nstat);
-    ALLOC(p.s_sexc, nstat);
-    ALLOC(p.s_digest, nstat);
+    ALLOC(h->d_chain, nchain * kChainBytes);   // per-chain totals, zeroed by every run
+    p.c_sexc = (double*)h->d_chain;
+    p.c_digest = (unsigned long long*)(h->d_chain + nchain * 8);
+    p.c_nhi = (uint32_t*)(h->d_chain + nchain * 16);
+    p.c_nthr = p.c_nhi + nchain;
+    p.c_trans = p.c_nthr + nchain;
+    p.c_ev = p.c_trans + nchain;
+    p.c_lock = p.c_ev + nchain;
+    p.c_vmax = p.c_lock + nchain;
     if (d.flags & MAGUS_F_DUMP_WORDS) {
         ALLOC(p.words, (size_t)Q * std::max(1, d.n_traces) * std::max(1, p.n_blocks) * 2);
     } else {
@@ -622,6 +626,7 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
     ALLOC(h->d_part, (size_t)d.n_policies * MAGUS_N_TOTALS * std::max(1, (d.n_traces + kTotTracesPerBlock - 1) /
                                                                          kTotTracesPerBlock));
     ALLOC(h->d_argmin, 1);
+    ALLOC(h->d_finish, 1);
     ALLOC(h->d_first_low, (size_t)std::max(1, d.n_traces));
     ALLOC(h->d_flag, 4);
     ALLOC(h->d_errkey, 1);
@@ -667,6 +672,7 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
 #undef ALLOC
     p.pol = h->d_pol;
     p.first_low = h->d_first_low;
+    cudaMemset(h->d_finish, 0, sizeof(unsigned int));
     if ((ce = cudaMemcpy(h->d_pol, h->lane.data(), h->lane.size() * sizeof(DevPolicy), cudaMemcpyHostToDevice)) !=
         cudaSuccess) {
         magus_status s = cuda_fail(h, ce, "cudaMemcpy policies");
@@ -691,7 +697,7 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
 
     for (int i = 0; i < 5; ++i) cudaEventCreate(&h->ev[i]);
     if (d.flags & MAGUS_F_TIMING) {
-        h->tev.resize(4 * magus_replay::kTimingRing);
+        h->tev.resize(5 * magus_replay::kTimingRing);
         for (cudaEvent_t& e : h->tev) cudaEventCreate(&e);
     }
     for (const LaunchGroup& g : h->groups) {
@@ -767,18 +773,20 @@ extern "C" magus_status magus_replay_run(magus_replay_t* h, const float* d_trace
         if (st != MAGUS_OK) return st;
     }
     CU(h, cudaMemsetAsync(h->d_flag, 0, 4 * sizeof(unsigned int), s));
-    cudaEvent_t* tv = timing ? &h->tev[4 * (h->n_runs % magus_replay::kTimingRing)] : nullptr;
+    cudaEvent_t* tv = timing ? &h->tev[5 * (h->n_runs % magus_replay::kTimingRing)] : nullptr;
     if (timing) CU(h, cudaEventRecord(tv[0], s));
+    CU(h, cudaMemsetAsync(h->d_chain, 0, (size_t)p.n_lane * std::max(1, d.n_traces) * kChainBytes, s));
     if (has_work && p.n_seg > 1) {
         // speculation aid: first subsampled low tick of every trace
         CU(h, cudaMemsetAsync(h->d_first_low, 0x7F, (size_t)d.n_traces * sizeof(int32_t), s));
-        const int sub = 64, per_chunk = 32;
+        const int sub = 256, per_chunk = 16;   // every 256th row: 0.4% of the trace bytes
         const int64_t n_sub = ((int64_t)d.n_samples + sub - 1) / sub;
         dim3 gfl((unsigned)((d.n_traces + 127) / 128), (unsigned)((n_sub + per_chunk - 1) / per_chunk));
         magus_first_low_kernel<<<gfl, 128, 0, s>>>(d_trace, d.n_traces, d.n_samples, d.trace_stride, h->B_lo, sub,
                                                      per_chunk, h->d_first_low);
         CU(h, cudaGetLastError());
     }
+    if (timing) CU(h, cudaEventRecord(tv[1], s));
     if (has_work) {
         for (const LaunchGroup& g : h->groups) {
             ReplayParams pg = p;
@@ -791,18 +799,8 @@ extern "C" magus_status magus_replay_run(magus_replay_t* h, const float* d_trace
             g.kernel<<<g.n_ctas, g.threads, g.smem, s>>>(h->tmap, pg);
             CU(h, cudaGetLastError());
         }
-    } else {
-        const size_t nstat = (size_t)p.n_lane * p.n_seg * std::max(1, d.n_traces);
-        CU(h, cudaMemsetAsync(p.s_nhi, 0, nstat * 4, s));
-        CU(h, cudaMemsetAsync(p.s_nthr, 0, nstat * 4, s));
-        CU(h, cudaMemsetAsync(p.s_trans, 0, nstat * 4, s));
-        CU(h, cudaMemsetAsync(p.s_ev, 0, nstat * 4, s));
-        CU(h, cudaMemsetAsync(p.s_lock, 0, nstat * 4, s));
-        CU(h, cudaMemsetAsync(p.s_vmax, 0, nstat * 4, s));
-        CU(h, cudaMemsetAsync(p.s_sexc, 0, nstat * 8, s));
-        CU(h, cudaMemsetAsync(p.s_digest, 0, nstat * 8, s));
     }
-    if (timing) CU(h, cudaEventRecord(tv[1], s));
+    if (timing) CU(h, cudaEventRecord(tv[2], s));
     if (d.n_traces > 0) {
         const int G = h->fx.n_fgroups;
         const FixParams& fx = h->fx;
@@ -839,33 +837,27 @@ extern "C" magus_status magus_replay_run(magus_replay_t* h, const float* d_trace
             magus_fix_serial_kernel<<<gs, 256, 0, s>>>(p, ep, fx, d_trace);
             CU(h, cudaGetLastError());
         }
-        dim3 ge((unsigned)((d.n_traces + 255) / 256), (unsigned)p.n_lane);
-        magus_epilogue_kernel<<<ge, 256, 0, s>>>(p, ep);
+        const int has_smax = h->smax.empty() ? 0 : 1;
+        dim3 ge((unsigned)((d.n_traces + 255) / 256), (unsigned)(p.n_lane + has_smax));
+        magus_epilogue_kernel<<<ge, 256, 0, s>>>(p, ep, h->d_smax, (int)h->smax.size(), h->digest_all_hi);
         CU(h, cudaGetLastError());
-        if (!h->smax.empty()) {
-            const int64_t n = (int64_t)d.n_traces * (int64_t)h->smax.size();
-            magus_static_max_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(ep, d.n_traces, h->d_smax,
-                                                                               (int)h->smax.size(), h->digest_all_hi);
-            CU(h, cudaGetLastError());
-        }
     }
-    if (timing) CU(h, cudaEventRecord(tv[2], s));
+    if (timing) CU(h, cudaEventRecord(tv[3], s));
     {
+        // per-policy fixed-order sums; the last block also finishes the totals (and the argmin if world == 1)
         const int n_chunks = std::max(1, (d.n_traces + kTotTracesPerBlock - 1) / kTotTracesPerBlock);
-        magus_totals_kernel<<<dim3(d.n_policies, n_chunks), kTotThreads, 0, s>>>(h->d_rec, d.n_traces, d.n_policies,
-                                                                                 h->d_part);
-        CU(h, cudaGetLastError());
-        magus_totals_final_kernel<<<1, 256, 0, s>>>(h->d_part, n_chunks, d.n_policies, d.n_traces, h->d_totals);
+        magus_totals_kernel<<<dim3(d.n_policies, n_chunks), kTotThreads, 0, s>>>(
+            h->d_rec, d.n_traces, d.n_policies, h->d_part, h->d_finish, h->d_totals, d.world > 1 ? nullptr : h->d_argmin);
         CU(h, cudaGetLastError());
     }
     if (d.world > 1) {
         ncclResult_t r = nccl().AllReduce(h->d_totals, h->d_totals, (size_t)d.n_policies * MAGUS_N_TOTALS, ncclFloat64,
                                           ncclSum, h->comm, s);
         if (r != ncclSuccess) return fail(h, MAGUS_ERR_NCCL, std::string("ncclAllReduce: ") + nccl().GetErrorString(r));
+        magus_argmin_kernel<<<1, 32, 0, s>>>(h->d_totals, d.n_policies, h->d_argmin);
+        CU(h, cudaGetLastError());
     }
-    magus_argmin_kernel<<<1, 32, 0, s>>>(h->d_totals, d.n_policies, h->d_argmin);
-    CU(h, cudaGetLastError());
-    if (timing) CU(h, cudaEventRecord(tv[3], s));
+    if (timing) CU(h, cudaEventRecord(tv[4], s));
     if (h->d_codes && has_work) {
         const int P = d.n_policies;
         dim3 grid((unsigned)((d.dump_n_traces + 63) / 64), (unsigned)p.n_lane);
@@ -968,33 +960,32 @@ extern "C" magus_status magus_replay_results(magus_replay_t* h, magus_results* o
     return MAGUS_OK;
 }
 
-static magus_status timing_avg(magus_replay_t* h, int n_last, float out_ms[4]) {
+static magus_status timing_avg(magus_replay_t* h, int n_last, float out_ms[5]) {
     if (!h || !out_ms) return fail(h, MAGUS_ERR_INVALID_ARG, "NULL argument");
     if (!h->ran || h->tev.empty()) return fail(h, MAGUS_ERR_STATE, "no timed run (MAGUS_F_TIMING)");
     CU(h, cudaEventSynchronize(h->ev[4]));
     const int64_t n = std::min<int64_t>({(int64_t)std::max(1, n_last), h->n_runs, (int64_t)magus_replay::kTimingRing});
-    double acc[4] = {0, 0, 0, 0};
+    // events per run: 0 run start, 1 replay start (after the speculation pre-pass), 2 replay end,
+    // 3 fix-up + epilogue end, 4 totals (+ allreduce) + argmin end
+    const int iv[5][2] = {{1, 2}, {2, 3}, {3, 4}, {0, 4}, {0, 1}};
+    double acc[5] = {0, 0, 0, 0, 0};
     for (int64_t r = h->n_runs - n; r < h->n_runs; ++r) {
-        cudaEvent_t* tv = &h->tev[4 * (r % magus_replay::kTimingRing)];
-        float ms;
-        CU(h, cudaEventElapsedTime(&ms, tv[0], tv[1]));
-        acc[0] += ms;
-        CU(h, cudaEventElapsedTime(&ms, tv[1], tv[2]));
-        acc[1] += ms;
-        CU(h, cudaEventElapsedTime(&ms, tv[2], tv[3]));
-        acc[2] += ms;
-        CU(h, cudaEventElapsedTime(&ms, tv[0], tv[3]));
-        acc[3] += ms;
+        cudaEvent_t* tv = &h->tev[5 * (r % magus_replay::kTimingRing)];
+        for (int k = 0; k < 5; ++k) {
+            float ms;
+            CU(h, cudaEventElapsedTime(&ms, tv[iv[k][0]], tv[iv[k][1]]));
+            acc[k] += ms;
+        }
     }
-    for (int i = 0; i < 4; ++i) out_ms[i] = (float)(acc[i] / (double)n);
+    for (int i = 0; i < 5; ++i) out_ms[i] = (float)(acc[i] / (double)n);
     return MAGUS_OK;
 }
 
-extern "C" magus_status magus_replay_kernel_times(magus_replay_t* h, float out_ms[4]) {
+extern "C" magus_status magus_replay_kernel_times(magus_replay_t* h, float out_ms[5]) {
     return timing_avg(h, 1, out_ms);
 }
 
-extern "C" magus_status magus_replay_timing_summary(magus_replay_t* h, int32_t n_last, float out_ms[4]) {
+extern "C" magus_status magus_replay_timing_summary(magus_replay_t* h, int32_t n_last, float out_ms[5]) {
     return timing_avg(h, n_last, out_ms);
 }
 

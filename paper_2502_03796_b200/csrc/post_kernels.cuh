@@ -3,7 +3,6 @@
 //                                lane-level work stealing, then a serial per-chain fallback
 //   magus_epilogue_kernel        per-trace records (closed-form energy model from sufficient
 //                                statistics)
-//   magus_static_max_kernel      analytic records of STATIC_MAX policies (never throttled, A17/A21)
 //   magus_totals_kernel          per-policy fixed-order sums: thread-strided, warp-shuffle tree, smem
 //   magus_argmin_kernel          argmin over policies of the total EDP (ties -> lowest index, A23)
 //   magus_resim_kernel           per-tick decision codes for a dump window (test diagnostics)
@@ -232,14 +231,8 @@ __device__ void rerun_items(const ReplayParams& p, const EpiParams& e, const Fix
             t += n;
             const bool co = T::equal(tru, spec, pol);
             if (co || t >= seg_end) {
-                const int64_t si = stat_idx(p, q, s, j);
-                p.s_nhi[si] += dt.nhi - dp.nhi;
-                p.s_nthr[si] += dt.nthr - dp.nthr;
-                p.s_trans[si] += dt.trans - dp.trans;
-                p.s_ev[si] += dt.ev - dp.ev;
-                p.s_lock[si] += dt.lock - dp.lock;
-                p.s_sexc[si] += dt.sexc - dp.sexc;
-                p.s_digest[si] += dt.digest - dp.digest;
+                add_to_chain(p, q, j, dt.nhi - dp.nhi, dt.nthr - dp.nthr, dt.trans - dp.trans, dt.ev - dp.ev,
+                             dt.lock - dp.lock, dt.sexc - dp.sexc, dt.digest - dp.digest);
                 copy_state(p, pol, q, 1, s - 1, 0, s, j);   // the entry the statistics now belong to
                 if (!co) {                                    // the exit changed: stage it, re-check s+1
                     if (s + 1 < p.n_seg) T::save(tru, p, pol, 2, q, s, j);
@@ -305,14 +298,8 @@ __device__ bool rerun_segment(const ReplayParams& p, const DevPolicy& pol, int q
             break;
         }
     }
-    const int64_t si = stat_idx(p, q, s, j);
-    p.s_nhi[si] += dt.nhi - dp.nhi;
-    p.s_nthr[si] += dt.nthr - dp.nthr;
-    p.s_trans[si] += dt.trans - dp.trans;
-    p.s_ev[si] += dt.ev - dp.ev;
-    p.s_lock[si] += dt.lock - dp.lock;
-    p.s_sexc[si] += dt.sexc - dp.sexc;
-    p.s_digest[si] += dt.digest - dp.digest;
+    add_to_chain(p, q, j, dt.nhi - dp.nhi, dt.nthr - dp.nthr, dt.trans - dp.trans, dt.ev - dp.ev, dt.lock - dp.lock,
+                 dt.sexc - dp.sexc, dt.digest - dp.digest);
     return coalesced;
 }
 
@@ -376,44 +363,30 @@ __global__ void __launch_bounds__(256) magus_fix_serial_kernel(const ReplayParam
 }
 
 // ================================================================================= epilogue
-// One thread per (trace, lane policy): the segment statistics summed in segment order, then the
-// closed-form record.
-__global__ void __launch_bounds__(256) magus_epilogue_kernel(const ReplayParams p, const EpiParams e) {
+// One thread per (trace, lane policy): the chain's totals -> the closed-form record (section 8).  An
+// extra grid row (blockIdx.y == n_lane) writes the STATIC_MAX records: at f_max A = D <= bw_max, never
+// throttled, never a transition or a tune flag, digest of an all-f_max command stream (A17, A21).
+__global__ void __launch_bounds__(256) magus_epilogue_kernel(const ReplayParams p, const EpiParams e,
+                                                             const int* __restrict__ smax_policies, int n_smax,
+                                                             uint64_t digest_all_hi) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     const int q = blockIdx.y;
     if (j >= p.n_traces) return;
-    const DevPolicy pol = p.pol[q];
-    uint64_t nhi = 0, nthr = 0, trans = 0, ev = 0, lock = 0, dig = 0;
-    uint32_t vmax = 0;
-    double sexc = 0.0;
-#pragma unroll 8
-    for (int s = 0; s < p.n_seg; ++s) {
-        const int64_t si = stat_idx(p, q, s, j);
-        nhi += p.s_nhi[si];
-        nthr += p.s_nthr[si];
-        trans += p.s_trans[si];
-        ev += p.s_ev[si];
-        lock += p.s_lock[si];
-        dig += p.s_digest[si];
-        vmax = max(vmax, p.s_vmax[si]);
-        sexc += p.s_sexc[si];
+    if (q == p.n_lane) {
+        for (int i = 0; i < n_smax; ++i) {
+            TraceRec& r = e.rec[(int64_t)j * e.n_policies + smax_policies[i]];
+            finish_record(r, e, (double)e.w[j], (int64_t)e.n_samples, 0, 0, 0, 0, 0.0, digest_all_hi);
+        }
+        return;
     }
+    const DevPolicy pol = p.pol[q];
+    const int64_t ci = chain_idx(p, q, j);
     if (pol.policy_index >= 0) {
         TraceRec& r = e.rec[(int64_t)j * e.n_policies + pol.policy_index];
-        finish_record(r, e, (double)e.w[j], (int64_t)nhi, (int64_t)nthr, (int64_t)trans, (int64_t)ev, (int64_t)lock,
-                      sexc, dig);
+        finish_record(r, e, (double)e.w[j], (int64_t)p.c_nhi[ci], (int64_t)p.c_nthr[ci], (int64_t)p.c_trans[ci],
+                      (int64_t)p.c_ev[ci], (int64_t)p.c_lock[ci], p.c_sexc[ci], (uint64_t)p.c_digest[ci]);
     }
-    if (vmax > p.bwbits) atomicOr(e.flag_invalid, 1u);
-}
-
-// STATIC_MAX records: at f_max A = D <= bw_max, never throttled, never a transition or a tune flag.
-__global__ void magus_static_max_kernel(const EpiParams e, int n_traces, const int* __restrict__ smax_policies,
-                                        int n_smax, uint64_t digest_all_hi) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= (int64_t)n_traces * n_smax) return;
-    const int j = (int)(i / n_smax), pi = smax_policies[i % n_smax];
-    TraceRec& r = e.rec[(int64_t)j * e.n_policies + pi];
-    finish_record(r, e, (double)e.w[j], (int64_t)e.n_samples, 0, 0, 0, 0, 0.0, digest_all_hi);
+    if (p.c_vmax[ci] > p.bwbits) atomicOr(e.flag_invalid, 1u);
 }
 
 constexpr int kTotThreads = 256;
@@ -423,7 +396,9 @@ constexpr int kTotTracesPerBlock = 1024;
 // Stage 1: block (p, c) sums traces [c*1024, (c+1)*1024) of policy p in a fixed order (4 per thread
 // sequentially, then an xor-shuffle tree, then the 8 warp partials in order) -> part[p][c].
 __global__ void __launch_bounds__(kTotThreads) magus_totals_kernel(const TraceRec* __restrict__ rec, int n_traces,
-                                                                    int n_policies, double* __restrict__ part) {
+                                                                    int n_policies, double* __restrict__ part,
+                                                                    unsigned int* finish, double* __restrict__ totals,
+                                                                    int* __restrict__ argmin) {
     const int p = blockIdx.x, c = blockIdx.y;
     double acc[kNTot - 1];
 #pragma unroll
@@ -459,20 +434,38 @@ __global__ void __launch_bounds__(kTotThreads) magus_totals_kernel(const TraceRe
         for (int w = 0; w < kTotThreads / 32; ++w) sum += wp[w][threadIdx.x];
         part[((int64_t)p * gridDim.y + c) * (kNTot - 1) + threadIdx.x] = sum;
     }
-}
-
-// Stage 2 (one block): per policy, the chunk partials in chunk order -> totals[p][13]; then the argmin
-// over policies of the total EDP (ties -> lowest index, A23).  With world > 1 the allreduce runs
-// between this kernel's totals and magus_argmin_kernel.
-__global__ void magus_totals_final_kernel(const double* __restrict__ part, int n_chunks, int n_policies, int n_traces,
-                                          double* __restrict__ totals) {
-    for (int i = threadIdx.x; i < n_policies * (kNTot - 1); i += blockDim.x) {
-        const int p = i / (kNTot - 1), f = i % (kNTot - 1);
+    if (finish == nullptr) return;
+    // the last block to finish runs stage 2 (and the argmin when there is no cross-rank allreduce)
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(finish, 1u) == gridDim.x * gridDim.y - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const int n_chunks = gridDim.y, P = n_policies;
+    for (int i = threadIdx.x; i < P * (kNTot - 1); i += blockDim.x) {
+        const int pp = i / (kNTot - 1), f = i % (kNTot - 1);
         double sum = 0.0;
-        for (int c = 0; c < n_chunks; ++c) sum += part[((int64_t)p * n_chunks + c) * (kNTot - 1) + f];
-        totals[p * kNTot + f] = sum;
+        for (int cc = 0; cc < n_chunks; ++cc) sum += part[((int64_t)pp * n_chunks + cc) * (kNTot - 1) + f];
+        totals[pp * kNTot + f] = sum;
     }
-    for (int p = threadIdx.x; p < n_policies; p += blockDim.x) totals[p * kNTot + kNTot - 1] = (double)n_traces;
+    for (int pp = threadIdx.x; pp < P; pp += blockDim.x) totals[pp * kNTot + kNTot - 1] = (double)n_traces;
+    __syncthreads();
+    if (argmin != nullptr && threadIdx.x == 0) {
+        __threadfence_block();
+        int best = 0;
+        double bv = totals[3];
+        for (int pp = 1; pp < P; ++pp) {
+            const double v = totals[pp * kNTot + 3];
+            if (v < bv) {
+                bv = v;
+                best = pp;
+            }
+        }
+        *argmin = best;
+    }
+    if (threadIdx.x == 0) *finish = 0u;   // re-arm for the next run
 }
 
 __global__ void magus_argmin_kernel(const double* __restrict__ totals, int n_policies, int* __restrict__ argmin) {

@@ -204,16 +204,9 @@ __device__ __forceinline__ void consume(const CUtensorMap* tmap, const ReplayPar
         const int j = j0 + c;
         if (j >= p.n_traces) continue;
         T::save(st[c], p, pol, 1, q, seg, j);
-        const int64_t si = stat_idx(p, q, seg, j);
-        p.s_nhi[si] = ss[c].nhi;
-        p.s_nthr[si] = ss[c].nthr;
-        p.s_trans[si] = ss[c].trans;
-        p.s_ev[si] = ss[c].ev;
-        p.s_lock[si] = ss[c].lock;
-        p.s_vmax[si] = vmax;
-        p.s_sexc[si] = ss[c].sexc;
-        p.s_digest[si] = ss[c].digest;
+        add_to_chain(p, q, j, ss[c].nhi, ss[c].nthr, ss[c].trans, ss[c].ev, ss[c].lock, ss[c].sexc, ss[c].digest);
     }
+    if (j0 < p.n_traces) atomicMax(p.c_vmax + chain_idx(p, q, j0), vmax);   // lane-level validation maximum
 }
 
 // One kernel per chain kind T (register allocation is per instantiation): a launch covers the lane

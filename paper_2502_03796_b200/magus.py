@@ -286,14 +286,16 @@ class Replay:
         _check(lib.magus_replay_run_host(self._h, C.c_void_p(tp), C.c_void_p(wp), _stream_ptr(stream)), self._h)
 
     def kernel_times(self):
-        out = (C.c_float * 4)()
+        out = (C.c_float * 5)()
         _check(lib.magus_replay_kernel_times(self._h, out), self._h)
-        return dict(replay_ms=out[0], fixup_epilogue_ms=out[1], totals_allreduce_argmin_ms=out[2], run_ms=out[3])
+        return dict(replay_ms=out[0], fixup_epilogue_ms=out[1], totals_allreduce_argmin_ms=out[2], run_ms=out[3],
+                    prepass_ms=out[4])
 
     def timing_summary(self, n_last: int):
-        out = (C.c_float * 4)()
+        out = (C.c_float * 5)()
         _check(lib.magus_replay_timing_summary(self._h, n_last, out), self._h)
-        return dict(replay_ms=out[0], fixup_epilogue_ms=out[1], totals_allreduce_argmin_ms=out[2], run_ms=out[3])
+        return dict(replay_ms=out[0], fixup_epilogue_ms=out[1], totals_allreduce_argmin_ms=out[2], run_ms=out[3],
+                    prepass_ms=out[4])
 
     def results(self, per_trace: bool | None = None, words: bool | None = None, decisions: bool | None = None,
                 raise_on_trace_error: bool = True) -> Results:
