@@ -189,7 +189,7 @@ def run_ours(args, cfg):
     offset = rank * n                      # weak scaling: each rank owns its own n traces (global ids)
     tr = torch.empty((ns, stride), dtype=torch.float32, device=dev)
     w = torch.empty(n, dtype=torch.float32, device=dev)
-    stream = torch.cuda.current_stream(dev)
+    stream = torch.cuda.Stream(dev)          # a capturable stream: the library runs each step as a CUDA graph
     M.gen_traces(cfg["seed"], n, ns, cfg["class_mix"], tr, w, trace_stride=stride, global_trace_offset=offset,
                  stream=stream)
     nccl_id = None

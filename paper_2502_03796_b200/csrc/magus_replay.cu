@@ -306,6 +306,8 @@ struct magus_replay {
     std::vector<void*> allocs;
     DevPolicy* d_pol = nullptr;
     int* d_smax = nullptr;
+    int* d_lane_of_policy = nullptr;  // user policy -> lane policy (-1: STATIC_MAX, analytic)
+    int validate_lane = -1;           // lane of the validate-only pseudo policy, if any
     TraceRec* d_rec = nullptr;
     double* d_totals = nullptr;
     double* d_part = nullptr;         // per-policy chunk partials of the totals
@@ -329,6 +331,12 @@ struct magus_replay {
     std::vector<cudaEvent_t> tev;   // MAGUS_F_TIMING: 4 events per run, ring of kTimingRing runs
     int64_t n_runs = 0;
     ncclComm_t comm = nullptr;
+    cudaGraphExec_t gexec = nullptr;  // the captured run
+    cudaGraph_t graph = nullptr;
+    const float* g_trace = nullptr;
+    const float* g_w = nullptr;
+    cudaStream_t g_stream = nullptr;
+    std::vector<std::pair<cudaGraphNode_t, int>> g_events;   // event-record node -> timing slot index
     std::string err;
 };
 
@@ -633,6 +641,7 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
     if (!h->smax.empty()) {
         ALLOC(h->d_smax, h->smax.size());
     }
+    ALLOC(h->d_lane_of_policy, d.n_policies);
     if ((d.flags & MAGUS_F_DUMP_DECISIONS) && d.dump_n_traces > 0 && d.n_samples > 0) {
         ALLOC(h->d_codes, (size_t)d.n_samples * d.dump_n_traces * d.n_policies);
     }
@@ -667,7 +676,7 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
         h->fx.wl_count = h->d_wl_count;
         h->fx.wl_cursor = h->d_wl_count + 2 * G;
         h->fx.any_unresolved = h->d_wl_count + 3 * G;
-        h->fix_rounds = std::max(1, env_int("MAGUS_FIX_ROUNDS", 2));
+        h->fix_rounds = std::max(1, env_int("MAGUS_FIX_ROUNDS", 1));
     }
 #undef ALLOC
     p.pol = h->d_pol;
@@ -681,6 +690,14 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
     }
     if (!h->smax.empty())
         cudaMemcpy(h->d_smax, h->smax.data(), h->smax.size() * sizeof(int), cudaMemcpyHostToDevice);
+    {
+        std::vector<int> lop(d.n_policies, -1);
+        for (size_t q = 0; q < h->lane.size(); ++q) {
+            if (h->lane[q].policy_index >= 0) lop[h->lane[q].policy_index] = (int)q;
+            else h->validate_lane = (int)q;
+        }
+        cudaMemcpy(h->d_lane_of_policy, lop.data(), lop.size() * sizeof(int), cudaMemcpyHostToDevice);
+    }
 
     EpiParams& ep = h->ep;
     ep.n_policies = d.n_policies;
@@ -732,6 +749,8 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
 extern "C" void magus_replay_destroy(magus_replay_t* h) {
     if (!h) return;
     if (h->ran && h->run_stream) cudaStreamSynchronize(h->run_stream);
+    if (h->gexec) cudaGraphExecDestroy(h->gexec);
+    if (h->graph) cudaGraphDestroy(h->graph);
     if (h->comm && nccl_ok()) nccl().CommDestroy(h->comm);
     for (void* a : h->allocs) cudaFree(a);
     for (int i = 0; i < 5; ++i)
@@ -757,36 +776,34 @@ static magus_status encode_tmap(magus_replay_t* h, const float* d_trace) {
     return MAGUS_OK;
 }
 
-extern "C" magus_status magus_replay_run(magus_replay_t* h, const float* d_trace, const float* d_w, void* stream) {
-    if (!h) return fail(nullptr, MAGUS_ERR_INVALID_ARG, "NULL handle");
+// Enqueues one whole run on stream s (also used to capture the run's CUDA graph); tv = the 5 timing
+// events of this run (nullptr without MAGUS_F_TIMING).
+static magus_status enqueue_run(magus_replay_t* h, const float* d_trace, const float* d_w, cudaStream_t s,
+                                cudaEvent_t* tv, bool capturing) {
+    // inside a stream capture, only "external" records become event-record nodes of the graph
+    auto rec = [&](cudaEvent_t e) {
+        return capturing ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal) : cudaEventRecord(e, s);
+    };
     const magus_replay_desc& d = h->desc;
     const bool has_work = d.n_traces > 0 && d.n_samples > 0;
-    if (d.n_traces > 0 && (!d_trace || !d_w)) return fail(h, MAGUS_ERR_INVALID_ARG, "NULL trace or w");
-    if (has_work && ((uintptr_t)d_trace % 16 != 0)) return fail(h, MAGUS_ERR_ALIGN, "trace base must be 16-byte aligned");
-    cudaStream_t s = (cudaStream_t)stream;
-    const bool timing = (d.flags & MAGUS_F_TIMING) != 0;
+    const bool timing = tv != nullptr;
     ReplayParams p = h->rp;
     EpiParams ep = h->ep;
     ep.w = d_w;
-    if (has_work) {
-        magus_status st = encode_tmap(h, d_trace);
-        if (st != MAGUS_OK) return st;
-    }
     CU(h, cudaMemsetAsync(h->d_flag, 0, 4 * sizeof(unsigned int), s));
-    cudaEvent_t* tv = timing ? &h->tev[5 * (h->n_runs % magus_replay::kTimingRing)] : nullptr;
-    if (timing) CU(h, cudaEventRecord(tv[0], s));
+    if (timing) CU(h, rec(tv[0]));
     CU(h, cudaMemsetAsync(h->d_chain, 0, (size_t)p.n_lane * std::max(1, d.n_traces) * kChainBytes, s));
     if (has_work && p.n_seg > 1) {
         // speculation aid: first subsampled low tick of every trace
         CU(h, cudaMemsetAsync(h->d_first_low, 0x7F, (size_t)d.n_traces * sizeof(int32_t), s));
-        const int sub = 256, per_chunk = 16;   // every 256th row: 0.4% of the trace bytes
+        const int sub = 256, per_chunk = 4;    // every 256th row: 0.4% of the trace bytes
         const int64_t n_sub = ((int64_t)d.n_samples + sub - 1) / sub;
         dim3 gfl((unsigned)((d.n_traces + 127) / 128), (unsigned)((n_sub + per_chunk - 1) / per_chunk));
         magus_first_low_kernel<<<gfl, 128, 0, s>>>(d_trace, d.n_traces, d.n_samples, d.trace_stride, h->B_lo, sub,
                                                      per_chunk, h->d_first_low);
         CU(h, cudaGetLastError());
     }
-    if (timing) CU(h, cudaEventRecord(tv[1], s));
+    if (timing) CU(h, rec(tv[1]));
     if (has_work) {
         for (const LaunchGroup& g : h->groups) {
             ReplayParams pg = p;
@@ -800,7 +817,7 @@ extern "C" magus_status magus_replay_run(magus_replay_t* h, const float* d_trace
             CU(h, cudaGetLastError());
         }
     }
-    if (timing) CU(h, cudaEventRecord(tv[2], s));
+    if (timing) CU(h, rec(tv[2]));
     if (d.n_traces > 0) {
         const int G = h->fx.n_fgroups;
         const FixParams& fx = h->fx;
@@ -837,17 +854,14 @@ extern "C" magus_status magus_replay_run(magus_replay_t* h, const float* d_trace
             magus_fix_serial_kernel<<<gs, 256, 0, s>>>(p, ep, fx, d_trace);
             CU(h, cudaGetLastError());
         }
-        const int has_smax = h->smax.empty() ? 0 : 1;
-        dim3 ge((unsigned)((d.n_traces + 255) / 256), (unsigned)(p.n_lane + has_smax));
-        magus_epilogue_kernel<<<ge, 256, 0, s>>>(p, ep, h->d_smax, (int)h->smax.size(), h->digest_all_hi);
-        CU(h, cudaGetLastError());
     }
-    if (timing) CU(h, cudaEventRecord(tv[3], s));
+    if (timing) CU(h, rec(tv[3]));
     {
         // per-policy fixed-order sums; the last block also finishes the totals (and the argmin if world == 1)
         const int n_chunks = std::max(1, (d.n_traces + kTotTracesPerBlock - 1) / kTotTracesPerBlock);
         magus_totals_kernel<<<dim3(d.n_policies, n_chunks), kTotThreads, 0, s>>>(
-            h->d_rec, d.n_traces, d.n_policies, h->d_part, h->d_finish, h->d_totals, d.world > 1 ? nullptr : h->d_argmin);
+            p, ep, h->d_lane_of_policy, h->validate_lane, h->digest_all_hi, h->d_part, h->d_finish, h->d_totals,
+            d.world > 1 ? nullptr : h->d_argmin);
         CU(h, cudaGetLastError());
     }
     if (d.world > 1) {
@@ -857,7 +871,77 @@ extern "C" magus_status magus_replay_run(magus_replay_t* h, const float* d_trace
         magus_argmin_kernel<<<1, 32, 0, s>>>(h->d_totals, d.n_policies, h->d_argmin);
         CU(h, cudaGetLastError());
     }
-    if (timing) CU(h, cudaEventRecord(tv[4], s));
+    if (timing) CU(h, rec(tv[4]));
+    return MAGUS_OK;
+}
+
+// The run as a CUDA graph (re-captured when the buffers, the stream or the timing flag change); its
+// timing-event nodes are re-pointed at this run's ring slot before every launch.
+static magus_status launch_graph(magus_replay_t* h, const float* d_trace, const float* d_w, cudaStream_t s,
+                                 cudaEvent_t* tv) {
+    if (!h->gexec || h->g_trace != d_trace || h->g_w != d_w || h->g_stream != s) {
+        if (h->gexec) cudaGraphExecDestroy(h->gexec);
+        if (h->graph) cudaGraphDestroy(h->graph);
+        h->gexec = nullptr;
+        h->graph = nullptr;
+        h->g_events.clear();
+        CU(h, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        magus_status st = enqueue_run(h, d_trace, d_w, s, tv, true);
+        cudaGraph_t graph = nullptr;
+        const cudaError_t ce = cudaStreamEndCapture(s, &graph);
+        if (st != MAGUS_OK) {
+            if (graph) cudaGraphDestroy(graph);
+            return st;
+        }
+        if (ce != cudaSuccess) return cuda_fail(h, ce, "cudaStreamEndCapture");
+        size_t n_nodes = 0;
+        cudaGraphGetNodes(graph, nullptr, &n_nodes);
+        std::vector<cudaGraphNode_t> nodes(n_nodes);
+        cudaGraphGetNodes(graph, nodes.data(), &n_nodes);
+        const cudaError_t ie = cudaGraphInstantiate(&h->gexec, graph, 0);
+        if (ie != cudaSuccess) {
+            cudaGraphDestroy(graph);
+            return cuda_fail(h, ie, "cudaGraphInstantiate");
+        }
+        if (tv) {   // which ring-slot event each event-record node records
+            for (cudaGraphNode_t nd : nodes) {
+                cudaGraphNodeType ty;
+                cudaGraphNodeGetType(nd, &ty);
+                if (ty != cudaGraphNodeTypeEventRecord) continue;
+                cudaEvent_t ev;
+                cudaGraphEventRecordNodeGetEvent(nd, &ev);
+                for (int k = 0; k < 5; ++k)
+                    if (ev == tv[k]) h->g_events.push_back({nd, k});
+            }
+        }
+        h->graph = graph;   // kept: exec-node updates take the original graph's node handles
+        h->g_trace = d_trace;
+        h->g_w = d_w;
+        h->g_stream = s;
+    } else if (tv) {
+        for (const auto& ne : h->g_events) CU(h, cudaGraphExecEventRecordNodeSetEvent(h->gexec, ne.first, tv[ne.second]));
+    }
+    CU(h, cudaGraphLaunch(h->gexec, s));
+    return MAGUS_OK;
+}
+
+extern "C" magus_status magus_replay_run(magus_replay_t* h, const float* d_trace, const float* d_w, void* stream) {
+    if (!h) return fail(nullptr, MAGUS_ERR_INVALID_ARG, "NULL handle");
+    const magus_replay_desc& d = h->desc;
+    const bool has_work = d.n_traces > 0 && d.n_samples > 0;
+    if (d.n_traces > 0 && (!d_trace || !d_w)) return fail(h, MAGUS_ERR_INVALID_ARG, "NULL trace or w");
+    if (has_work && ((uintptr_t)d_trace % 16 != 0)) return fail(h, MAGUS_ERR_ALIGN, "trace base must be 16-byte aligned");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (has_work) {
+        magus_status st = encode_tmap(h, d_trace);
+        if (st != MAGUS_OK) return st;
+    }
+    cudaEvent_t* tv = (d.flags & MAGUS_F_TIMING) ? &h->tev[5 * (h->n_runs % magus_replay::kTimingRing)] : nullptr;
+    // graphs need a capturable (non-legacy-default) stream
+    const bool graph = s != nullptr && s != cudaStreamLegacy && s != cudaStreamPerThread && !env_int("MAGUS_NO_GRAPH", 0);
+    magus_status st = graph ? launch_graph(h, d_trace, d_w, s, tv) : enqueue_run(h, d_trace, d_w, s, tv, false);
+    if (st != MAGUS_OK) return st;
+    ReplayParams p = h->rp;
     if (h->d_codes && has_work) {
         const int P = d.n_policies;
         dim3 grid((unsigned)((d.dump_n_traces + 63) / 64), (unsigned)p.n_lane);
@@ -876,7 +960,6 @@ extern "C" magus_status magus_replay_run(magus_replay_t* h, const float* d_trace
     h->n_runs += 1;
     return MAGUS_OK;
 }
-
 extern "C" magus_status magus_replay_run_host(magus_replay_t* h, const float* trace, const float* w, void* stream) {
     if (!h) return fail(nullptr, MAGUS_ERR_INVALID_ARG, "NULL handle");
     const magus_replay_desc& d = h->desc;

@@ -395,11 +395,35 @@ constexpr int kTotTracesPerBlock = 1024;
 
 // Stage 1: block (p, c) sums traces [c*1024, (c+1)*1024) of policy p in a fixed order (4 per thread
 // sequentially, then an xor-shuffle tree, then the 8 warp partials in order) -> part[p][c].
-__global__ void __launch_bounds__(kTotThreads) magus_totals_kernel(const TraceRec* __restrict__ rec, int n_traces,
-                                                                    int n_policies, double* __restrict__ part,
-                                                                    unsigned int* finish, double* __restrict__ totals,
+__global__ void __launch_bounds__(kTotThreads) magus_totals_kernel(const ReplayParams rp, const EpiParams e,
+                                                                    const int* __restrict__ lane_of_policy,
+                                                                    int validate_lane, uint64_t digest_all_hi,
+                                                                    double* __restrict__ part, unsigned int* finish,
+                                                                    double* __restrict__ totals,
                                                                     int* __restrict__ argmin) {
+    const int n_traces = rp.n_traces, n_policies = e.n_policies;
+    TraceRec* rec = e.rec;
     const int p = blockIdx.x, c = blockIdx.y;
+    // the per-trace records of policy p for this chunk (section 8), then their fixed-order sums
+    {
+        const int q = lane_of_policy[p];
+        const int j_end0 = min(n_traces, (c + 1) * kTotTracesPerBlock);
+        for (int j = c * kTotTracesPerBlock + threadIdx.x; j < j_end0; j += kTotThreads) {
+            TraceRec& r = rec[(int64_t)j * n_policies + p];
+            if (q < 0) {   // STATIC_MAX: never throttled, no transition or tune flag (A17, A21)
+                finish_record(r, e, (double)e.w[j], (int64_t)e.n_samples, 0, 0, 0, 0, 0.0, digest_all_hi);
+            } else {
+                const int64_t ci = chain_idx(rp, q, j);
+                finish_record(r, e, (double)e.w[j], (int64_t)rp.c_nhi[ci], (int64_t)rp.c_nthr[ci],
+                              (int64_t)rp.c_trans[ci], (int64_t)rp.c_ev[ci], (int64_t)rp.c_lock[ci], rp.c_sexc[ci],
+                              (uint64_t)rp.c_digest[ci]);
+                if (rp.c_vmax[ci] > rp.bwbits) atomicOr(e.flag_invalid, 1u);
+            }
+            if (p == 0 && validate_lane >= 0 && rp.c_vmax[chain_idx(rp, validate_lane, j)] > rp.bwbits)
+                atomicOr(e.flag_invalid, 1u);
+        }
+        __syncthreads();   // this block's records are read back below by other threads of the block
+    }
     double acc[kNTot - 1];
 #pragma unroll
     for (int f = 0; f < kNTot - 1; ++f) acc[f] = 0.0;

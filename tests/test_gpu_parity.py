@@ -222,6 +222,29 @@ def test_determinism_and_virtual_ranks(M):
     np.testing.assert_allclose(parts[0].totals[:, :12] + parts[1].totals[:, :12], a.totals[:, :12], rtol=1e-9)
 
 
+def test_graph_path_matches_direct(M):
+    """On a non-default stream the library replays each run as a captured CUDA graph; results equal the
+    direct (stream-ordered launches) path, across graph reuse and a re-capture after a buffer change."""
+    n, ns = 300, 6000
+    tr, w = gpu_gen(M, 13, n, ns, 0, 300)
+    pols = PA.gpu_policies(CONFIGS[5]["policies"])
+    with M.Replay(n, ns, pols, trace_stride=300, flags=M.F_PER_TRACE_STATS | M.F_TIMING) as R:
+        R.run(tr, w)                              # default stream: direct launches
+        direct = R.results()
+        st = torch.cuda.Stream()
+        outs = []
+        for _ in range(3):                        # capture once, replay twice
+            R.run(tr, w, st)
+            outs.append(R.results())
+        tr2 = tr.clone()
+        R.run(tr2, w, st)                         # new buffer: re-capture
+        outs.append(R.results())
+        t = R.timing_summary(3)
+    for o in outs:
+        assert o.per_trace.tobytes() == direct.per_trace.tobytes() and np.array_equal(o.totals, direct.totals)
+    assert t["replay_ms"] > 0 and t["run_ms"] >= t["replay_ms"]
+
+
 def test_host_buffer_path(M):
     """magus_replay_run_host (the e2e path) gives the same results as the device path."""
     n, ns = 256, 5000
