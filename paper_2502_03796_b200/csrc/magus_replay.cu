@@ -453,7 +453,7 @@ static void choose_geometry(magus_replay_t* h, int n_sm) {
         }
     }
     int W = d.tuning_warmup > 0 ? d.tuning_warmup
-                                : ((kmax + cmax - 1 + 31) / 32) * 32 + env_int("MAGUS_WARMUP_EXTRA", 32);
+                                : ((kmax + cmax - 1 + 31) / 32) * 32 + env_int("MAGUS_WARMUP_EXTRA", 0);
     W = ((std::max(W, kmax + cmax - 1) + 31) / 32) * 32;
     const int N = std::max(1, d.n_samples);
     int base = 0;   // CTAs per segment over all launch groups

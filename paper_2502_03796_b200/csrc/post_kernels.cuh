@@ -391,7 +391,7 @@ __global__ void __launch_bounds__(256) magus_epilogue_kernel(const ReplayParams 
 
 constexpr int kTotThreads = 256;
 constexpr int kNTot = 13;              // MAGUS_N_TOTALS
-constexpr int kTotTracesPerBlock = 1024;
+constexpr int kTotTracesPerBlock = 256;   // one trace per thread per block: many blocks, short tails
 
 // Stage 1: block (p, c) sums traces [c*1024, (c+1)*1024) of policy p in a fixed order (4 per thread
 // sequentially, then an xor-shuffle tree, then the 8 warp partials in order) -> part[p][c].
