@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="target CPU work of the oracle baseline")
+    ap.add_argument("--ref-budget-s", type=float, default=150.0,
+                    help="--impl reference: wall-time budget of warmup + steps (sizes each step's sample)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--preroll-ms", type=float, default=600.0, help="untimed load before the timed region "
@@ -142,7 +144,7 @@ def run_reference(args, cfg):
     pols = [O.Policy(**d) for d in cfg["policies"]]
     cores = os.cpu_count() or 1
     # per-step sample sized so that warmup + steps finish in ~2-3 minutes
-    per_step_s = max(0.5, 150.0 / max(1, args.steps + args.warmup))
+    per_step_s = max(0.05, args.ref_budget_s / max(1, args.steps + args.warmup))
     n = min(cfg["n_traces"], cores)
     tr, w = O.gen_traces(O.GenDesc(seed=cfg["seed"], n_traces=n, n_samples=ns,
                                    class_mix=cfg["class_mix"]))
@@ -183,10 +185,10 @@ def run_ours(args, cfg):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    n = cfg.get("per_gpu_traces", cfg["n_traces"])
+    from paper_2502_03796_b200.sharding import weak_shard
+    offset, n = weak_shard(cfg.get("per_gpu_traces", cfg["n_traces"]), rank, world)   # global ids
     ns = cfg["n_samples"]
     stride = (n + 3) // 4 * 4
-    offset = rank * n                      # weak scaling: each rank owns its own n traces (global ids)
     tr = torch.empty((ns, stride), dtype=torch.float32, device=dev)
     w = torch.empty(n, dtype=torch.float32, device=dev)
     stream = torch.cuda.Stream(dev)          # a capturable stream: the library runs each step as a CUDA graph

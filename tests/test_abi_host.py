@@ -1,0 +1,128 @@
+"""The C-ABI library on a CPU-only box: it loads, exports every function include/magus_replay.h declares,
+validates configurations, derives the exact-equivalent thresholds on the host, and refuses to compute
+without a GPU (there is no CPU fallback).  -m "not gpu"."""
+import ctypes
+import math
+import os
+import random
+import subprocess
+
+import numpy as np
+import pytest
+
+from paper_2502_03796_b200 import magus as M
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_every_declared_symbol():
+    names = M.header_functions()
+    assert "magus_replay_create" in names and "magus_replay_run" in names and "magus_replay_results" in names
+    out = subprocess.run(["nm", "-D", "--defined-only", M.LIB_PATH], capture_output=True, text=True).stdout
+    exported = {l.split()[-1] for l in out.splitlines() if " T " in l}
+    missing = [n for n in names if n not in exported]
+    assert not missing, missing
+    lib = ctypes.CDLL(M.LIB_PATH)
+    for n in names:
+        getattr(lib, n)
+    assert M.abi_version() == 1
+
+
+def test_library_is_sm100a_only():
+    """Every kernel image in the library is sm_100a SASS (no PTX JIT, no other architecture)."""
+    out = subprocess.run(["cuobjdump", "--list-elf", M.LIB_PATH], capture_output=True, text=True).stdout
+    elves = [l for l in out.splitlines() if ".cubin" in l]
+    assert elves and all("sm_100a" in l for l in elves), out
+    ptx = subprocess.run(["cuobjdump", "--list-ptx", M.LIB_PATH], capture_output=True, text=True).stdout
+    assert ".ptx" not in ptx
+
+
+def test_sass_has_tma_and_no_fp64_division():
+    """The replay kernel stages tiles with TMA (UTMALDG) and never divides per tick (no MUFU.RCP64H/DMUL
+    Newton sequences): Alg. 1's division is replaced by exact-equivalent thresholds."""
+    sass = subprocess.run(["cuobjdump", "-sass", M.LIB_PATH], capture_output=True, text=True).stdout
+    funcs = sass.split("Function : ")
+    replay = [f for f in funcs if f.startswith("_ZN5magus19magus_replay_kernel")]
+    assert replay
+    for f in replay:
+        assert "UTMALDG" in f
+        assert "MUFU.RCP64H" not in f and "DMUL" not in f
+
+
+def test_no_cuda_device_means_error_not_fallback():
+    try:
+        import torch
+        if torch.cuda.is_available():
+            pytest.skip("this box has a GPU")
+    except ImportError:
+        pass
+    with pytest.raises(M.MagusError) as e:
+        M.Replay(8, 100, [M.Policy()])
+    assert e.value.status == M.ERR_CUDA
+
+
+@pytest.mark.parametrize("bad,key", [(dict(deriv_ticks=0), "deriv_ticks"), (dict(dec_threshold=0.5), "dec_threshold"),
+                                     (dict(inc_threshold=0.0), "inc_threshold"),
+                                     (dict(tune_log_capacity=65), "tune_log_capacity"),
+                                     (dict(high_freq_threshold=1.5), "high_freq_threshold"),
+                                     (dict(kind=M.TDP_DEFAULT, tdp_margin=1.0), "tdp_margin"),
+                                     (dict(kind=7), "kind")])
+def test_config_validation_names_the_key(bad, key):
+    """an invalid configuration is rejected before any device work, naming the key."""
+    with pytest.raises(M.MagusError) as e:
+        M.derive_thresholds(M.Policy(**bad), M.Model())
+    assert e.value.status == M.ERR_CONFIG and key in str(e.value)
+    with pytest.raises(M.MagusError) as e:
+        M.derive_thresholds(M.Policy(), M.Model(f_min_ghz=3.0))
+    assert "f_max_ghz" in str(e.value)
+
+
+def _alg1_fires(d, L, th):
+    return d / L > th
+
+
+def test_dinc_ddec_are_exact_boundaries():
+    """d*_inc is the largest double d with fl(d/L) <= theta_inc (Alg. 1 P:209 holds exactly iff d > d*);
+    d*_dec the smallest with fl(d/L) >= theta_dec.  Checked with Python floats (IEEE doubles)
+    at the boundary and one ulp either side, over random and paper-default parameters."""
+    rng = random.Random(3)
+    cases = [(1, 0.1, 1.0, -1.0), (3, 0.1, 1.0, -1.0), (8, 0.1, 0.5, -4.0)]
+    cases += [(rng.randint(1, 64), rng.choice([0.1, 0.05, 0.3, 1.0]), rng.uniform(1e-3, 50), -rng.uniform(1e-3, 50))
+              for _ in range(200)]
+    for k, dt, inc, dec in cases:
+        t = M.derive_thresholds(M.Policy(deriv_ticks=k, inc_threshold=inc, dec_threshold=dec), M.Model(sample_period_s=dt))
+        L = k * dt
+        assert t["L"] == L
+        di, dd = t["dinc"], t["ddec"]
+        assert not (di / L > inc) and (math.nextafter(di, math.inf) / L > inc)
+        assert not (dd / L < dec) and (math.nextafter(dd, -math.inf) / L < dec)
+
+
+def test_smin_and_tdp_boundaries():
+    """s_min = min{s : fl(s/C) >= theta_hf} (Alg. 2); the paper's 0.6 of 10 gives 6.
+    a*[f] = the smallest fp32 A with fl(P[f] + fl(c*A)) >= fl((1-m)*TDP)."""
+    assert M.derive_thresholds(M.Policy(), M.Model())["s_min"] == 6
+    for C in range(1, 65):
+        for th in (0.1, 0.25, 0.5, 0.6, 0.7, 0.75, 0.9, 1.0, 1 / 3):
+            s = M.derive_thresholds(M.Policy(tune_log_capacity=C, high_freq_threshold=th), M.Model())["s_min"]
+            want = next((x for x in range(C + 1) if x / C >= th), C + 1)
+            assert s == want, (C, th)
+    m = M.Model()
+    for tdp in (217.0, 230.0, 270.0, 400.0, 150.0):
+        t = M.derive_thresholds(M.Policy(kind=M.TDP_DEFAULT, tdp_w=tdp), m)
+        bound = (1.0 - 0.05) * tdp
+        for P, a in ((t["P_lo"], t["astar_lo"]), (t["P_hi"], t["astar_hi"])):
+            f = lambda A: (P + 0.5 * float(np.float32(A))) >= bound
+            if math.isinf(a):
+                assert not f(np.float32(np.finfo(np.float32).max))
+            else:
+                assert f(a)
+                if a > 0:
+                    assert not f(np.nextafter(np.float32(a), np.float32(0)))
+
+
+def test_default_model_constants():
+    """B_lo = fl32(20 * (0.8/2.2)) = 7.2727275; P_lo = 116 W, P_hi = 200 W (the K5 calibration)."""
+    t = M.derive_thresholds(M.Policy(), M.Model())
+    assert t["B_lo"] == float(np.float32(20 * (0.8 / 2.2))) and t["B_hi"] == 20.0
+    assert (t["P_lo"], t["P_hi"]) == (116.0, 200.0)
