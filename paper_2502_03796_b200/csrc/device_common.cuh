@@ -33,6 +33,8 @@ struct DevPolicy {
     int32_t guess_f;       // level guessed at a speculative segment start
     int32_t policy_index;  // index in the user's policy array
     uint32_t one;          // the constant 1, as data (keeps predicated increments on the FMA pipe)
+    int32_t sticky;        // k >= s_min: every edge locks Alg. 2, and after a lock Hold keeps f_max
+    int32_t _pad2;
 };
 
 // run-wide constants and scratch pointers
@@ -51,7 +53,7 @@ struct ReplayParams {
     int32_t _pad0;
     int64_t trace_stride;
     const DevPolicy* pol;  // [n_lane]
-    const int32_t* first_low;   // [n_traces] first subsampled tick with D <= B_lo (INT32_MAX if none)
+    const int32_t* first_low;   // [2][n_traces] first subsampled tick with D <= B_lo / D > B_lo (INT32_MAX: none)
     // chain states, SoA: [e (0 entry, 1 exit)][q][s][j]
     uint8_t* st_f;
     uint64_t* st_log;

@@ -337,6 +337,9 @@ struct magus_replay {
     const float* g_w = nullptr;
     cudaStream_t g_stream = nullptr;
     std::vector<std::pair<cudaGraphNode_t, int>> g_events;   // event-record node -> timing slot index
+    std::vector<cudaStream_t> aux;     // one per extra launch group (concurrent replay launches)
+    std::vector<cudaEvent_t> join_ev;
+    cudaEvent_t fork_ev = nullptr;
     std::string err;
 };
 
@@ -555,6 +558,7 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
             q.dinc = derive_dinc(L, p.inc_threshold);
             q.ddec = derive_ddec(L, p.dec_threshold);
             q.s_min = derive_smin(q.C, p.high_freq_threshold);
+            q.sticky = q.k >= q.s_min ? 1 : 0;
             q.f0 = 0;
             q.guess_f = 0;   // speculative segment start
         } else if (p.kind == MAGUS_POLICY_STATIC_MIN) {
@@ -635,7 +639,7 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
                                                                          kTotTracesPerBlock));
     ALLOC(h->d_argmin, 1);
     ALLOC(h->d_finish, 1);
-    ALLOC(h->d_first_low, (size_t)std::max(1, d.n_traces));
+    ALLOC(h->d_first_low, (size_t)2 * std::max(1, d.n_traces));
     ALLOC(h->d_flag, 4);
     ALLOC(h->d_errkey, 1);
     if (!h->smax.empty()) {
@@ -713,6 +717,15 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
     ep.fix_segments = (unsigned long long*)(h->d_flag + 2);
 
     for (int i = 0; i < 5; ++i) cudaEventCreate(&h->ev[i]);
+    cudaEventCreateWithFlags(&h->fork_ev, cudaEventDisableTiming);
+    for (size_t g = 1; g < h->groups.size(); ++g) {
+        cudaStream_t st;
+        cudaEvent_t ev;
+        cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+        cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+        h->aux.push_back(st);
+        h->join_ev.push_back(ev);
+    }
     if (d.flags & MAGUS_F_TIMING) {
         h->tev.resize(5 * magus_replay::kTimingRing);
         for (cudaEvent_t& e : h->tev) cudaEventCreate(&e);
@@ -756,6 +769,9 @@ extern "C" void magus_replay_destroy(magus_replay_t* h) {
     for (int i = 0; i < 5; ++i)
         if (h->ev[i]) cudaEventDestroy(h->ev[i]);
     for (cudaEvent_t e : h->tev) cudaEventDestroy(e);
+    for (cudaEvent_t e : h->join_ev) cudaEventDestroy(e);
+    for (cudaStream_t st : h->aux) cudaStreamDestroy(st);
+    if (h->fork_ev) cudaEventDestroy(h->fork_ev);
     delete h;
 }
 
@@ -795,7 +811,7 @@ static magus_status enqueue_run(magus_replay_t* h, const float* d_trace, const f
     CU(h, cudaMemsetAsync(h->d_chain, 0, (size_t)p.n_lane * std::max(1, d.n_traces) * kChainBytes, s));
     if (has_work && p.n_seg > 1) {
         // speculation aid: first subsampled low tick of every trace
-        CU(h, cudaMemsetAsync(h->d_first_low, 0x7F, (size_t)d.n_traces * sizeof(int32_t), s));
+        CU(h, cudaMemsetAsync(h->d_first_low, 0x7F, (size_t)2 * d.n_traces * sizeof(int32_t), s));
         const int sub = 256, per_chunk = 4;    // every 256th row: 0.4% of the trace bytes
         const int64_t n_sub = ((int64_t)d.n_samples + sub - 1) / sub;
         dim3 gfl((unsigned)((d.n_traces + 127) / 128), (unsigned)((n_sub + per_chunk - 1) / per_chunk));
@@ -805,7 +821,16 @@ static magus_status enqueue_run(magus_replay_t* h, const float* d_trace, const f
     }
     if (timing) CU(h, rec(tv[1]));
     if (has_work) {
-        for (const LaunchGroup& g : h->groups) {
+        // launch groups (one chain kind each) run concurrently: fork onto auxiliary streams and join
+        // (parallel branches when the run is captured as a graph)
+        const int G = (int)h->groups.size();
+        if (G > 1) {
+            CU(h, cudaEventRecord(h->fork_ev, s));
+            for (int g = 1; g < G; ++g) CU(h, cudaStreamWaitEvent(h->aux[g - 1], h->fork_ev, 0));
+        }
+        for (int gi = 0; gi < G; ++gi) {
+            const LaunchGroup& g = h->groups[gi];
+            cudaStream_t gs = gi == 0 ? s : h->aux[gi - 1];
             ReplayParams pg = p;
             pg.q_base = g.q_base;
             pg.nq = g.nq;
@@ -813,8 +838,12 @@ static magus_status enqueue_run(magus_replay_t* h, const float* d_trace, const f
             pg.npw = g.npw;
             pg.n_tblocks = g.n_tblocks;
             pg.n_pblocks = g.n_pblocks;
-            g.kernel<<<g.n_ctas, g.threads, g.smem, s>>>(h->tmap, pg);
+            g.kernel<<<g.n_ctas, g.threads, g.smem, gs>>>(h->tmap, pg);
             CU(h, cudaGetLastError());
+        }
+        for (int g = 1; g < G; ++g) {
+            CU(h, cudaEventRecord(h->join_ev[g - 1], h->aux[g - 1]));
+            CU(h, cudaStreamWaitEvent(s, h->join_ev[g - 1], 0));
         }
     }
     if (timing) CU(h, rec(tv[2]));

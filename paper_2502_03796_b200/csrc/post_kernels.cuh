@@ -274,15 +274,20 @@ __device__ bool rerun_segment(const ReplayParams& p, const DevPolicy& pol, int q
     for (int bt0 = seg_start; bt0 < seg_end; bt0 += 32) {
         const uint32_t fst = T::level(tru), fss = T::level(spec);
         const int n = min(32, seg_end - bt0);
-        for (int i = 0; i < n; ++i) {
-            const int t = bt0 + i;
-            const float D = __ldg(trace + (int64_t)t * p.trace_stride + j);
-            const TickOut ot = T::template tick<false>(tru, D, pol, p.B_lo, p.B_hi, true, true);
-            const TickOut os = T::template tick<false>(spec, D, pol, p.B_lo, p.B_hi, true, true);
-            wct = (wct << 1) | ot.cmd;
-            wcs = (wcs << 1) | os.cmd;
-            dt.nthr += ot.thr; dt.lock += ot.hf; if (ot.thr) dt.sexc += (double)D - (double)p.B_lo;
-            dp.nthr += os.thr; dp.lock += os.hf; if (os.thr) dp.sexc += (double)D - (double)p.B_lo;
+        float dv[32];   // the block's samples, loaded up front (32 loads in flight)
+#pragma unroll
+        for (int i = 0; i < 32; ++i) dv[i] = (i < n) ? __ldg(trace + (int64_t)(bt0 + i) * p.trace_stride + j) : 0.0f;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            if (i < n) {
+                const float D = dv[i];
+                const TickOut ot = T::template tick<false>(tru, D, pol, p.B_lo, p.B_hi, true, true);
+                const TickOut os = T::template tick<false>(spec, D, pol, p.B_lo, p.B_hi, true, true);
+                wct = (wct << 1) | ot.cmd;
+                wcs = (wcs << 1) | os.cmd;
+                dt.nthr += ot.thr; dt.lock += ot.hf; if (ot.thr) dt.sexc += (double)D - (double)p.B_lo;
+                dp.nthr += os.thr; dp.lock += os.hf; if (os.thr) dp.sexc += (double)D - (double)p.B_lo;
+            }
         }
         uint32_t ewt = 0, ews = 0;
         if constexpr (T::kWarmupRules) {
@@ -550,21 +555,29 @@ __global__ void magus_fill_codes_kernel(uint8_t* codes, int64_t n_rows, int P, i
     if (i < n_rows) codes[i * P + pi] = value;
 }
 
-// Speculation aid: first_low[j] = the first subsampled tick (stride `sub`) with
-// D <= B_lo, via atomicMin over tick chunks.  Pure performance hint: a wrong guess only costs a re-run.
+// Speculation aid: first_low[j] / first_low[n + j] = the first subsampled tick
+// (stride `sub`) with D <= B_lo / D > B_lo, via atomicMin over tick chunks.  Pure performance hint: a
+// wrong guess only costs a re-run.
 __global__ void __launch_bounds__(128) magus_first_low_kernel(const float* __restrict__ trace, int n_traces,
                                                               int n_samples, int64_t stride, float B_lo, int sub,
                                                               int per_chunk, int* __restrict__ first_low) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n_traces) return;
     const int64_t t_begin = (int64_t)blockIdx.y * per_chunk * sub;
+    bool got_low = false, got_high = false;
     for (int i = 0; i < per_chunk; ++i) {
         const int64_t t = t_begin + (int64_t)i * sub;
         if (t >= n_samples) break;
-        if (__ldg(trace + t * stride + j) <= B_lo) {
+        const float D = __ldg(trace + t * stride + j);
+        if (!got_low && D <= B_lo) {
             atomicMin(first_low + j, (int)t);
-            return;
+            got_low = true;
         }
+        if (!got_high && D > B_lo) {
+            atomicMin(first_low + n_traces + j, (int)t);
+            got_high = true;
+        }
+        if (got_low && got_high) return;
     }
 }
 

@@ -144,11 +144,15 @@ __device__ __forceinline__ void consume(const CUtensorMap* tmap, const ReplayPar
                     // that Alg. 1 sees even at f_min; a trace never below B_lo is never seen to rise (A14).
                     const float4 d0 = rows[0];
                     const float dd[4] = {d0.x, d0.y, d0.z, d0.w};
+                    // Policies whose edges always lock (k >= s_min) keep f_max after any low/high transition
+                    // (post-lock stickiness, K9).
 #pragma unroll
                     for (int c = 0; c < kChains; ++c) {
                         const int j = j0 + c;
                         const int fl = j < p.n_traces ? __ldg(p.first_low + j) : 0x7FFFFFFF;
-                        T::set_level(st[c], (dd[c] > B_lo && fl < G.tau_w) ? 1u : 0u);
+                        const int fh = j < p.n_traces ? __ldg(p.first_low + p.n_traces + j) : 0x7FFFFFFF;
+                        const bool hi = (dd[c] > B_lo && fl < G.tau_w) || (pol.sticky && fl < G.tau_w && fh < G.tau_w);
+                        T::set_level(st[c], hi ? 1u : 0u);
                         fstart[c] = T::level(st[c]);
                     }
                 }
