@@ -34,7 +34,8 @@ struct DevPolicy {
     int32_t policy_index;  // index in the user's policy array
     uint32_t one;          // the constant 1, as data (keeps predicated increments on the FMA pipe)
     int32_t sticky;        // k >= s_min: every edge locks Alg. 2, and after a lock Hold keeps f_max
-    int32_t _pad2;
+    float B_hi;            // B[f_max] (copy of the run constant, for the TDP fast tick)
+    uint32_t smin_sc;      // 32-bit-log kinds: s_min << (C-1), the lock threshold on the scaled window count
 };
 
 // run-wide constants and scratch pointers
@@ -88,6 +89,10 @@ __host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {   // splitmix64
     return z ^ (z >> 31);
 }
 static constexpr uint64_t kPhi = 0x9E3779B97F4A7C15ULL;
+
+// Chain kinds with C <= kMaxC32 keep the tune log in 32 bits and the scaled window count
+// (ones << (C-1), which must not overflow: C * 2^(C-1) < 2^32); larger logs use the 64-bit kinds.
+constexpr int kMaxC32 = 28;
 
 template <bool LOG64>
 struct LogWord { using T = uint32_t; };
@@ -175,7 +180,8 @@ struct MagusState {
     using LogT = typename LogWord<LOG64>::T;
     uint32_t f;     // level in effect for the next tick (0 LO, 1 HI)
     LogT evh;       // tune-flag history, newest at bit 0; the log is the low C bits
-    uint32_t cnt;   // ones in the log (derived from evh; carried so the fast path updates it incrementally)
+    uint32_t cnt;   // 32-bit log only: (ones in the log) << (C-1), kept incrementally by the 4-chain tick
+                    // (tick4_asm.cuh); derived from evh whenever a state is (re)built
     Ring<K> ring;
 };
 
@@ -203,7 +209,7 @@ __device__ __forceinline__ TickOut magus_tick(MagusState<K, LOG64>& s, float D, 
     const uint32_t ev = (inc || dec) ? 1u : 0u;
     s.evh = (s.evh << 1) | (typename LogWord<LOG64>::T)ev;
     const uint32_t cnt = popc_log<LOG64>(s.evh & (typename LogWord<LOG64>::T)pol.logmask);
-    s.cnt = cnt;
+    if constexpr (!LOG64) s.cnt = cnt << (pol.C - 1);
     bool hf = cnt >= (uint32_t)pol.s_min;
     if (SLOW && !full) hf = false;
     const uint32_t cmd = (hf || inc || (s.f && !dec)) ? 1u : 0u;
@@ -230,7 +236,9 @@ __device__ __forceinline__ TickOut tdp_tick(uint32_t& f, float D, const DevPolic
     return o;
 }
 
-// Per-(chain, segment) statistics accumulated over the segment's own ticks.
+// Per-(chain, segment) statistics accumulated over the segment's own ticks.  sexc = the throttling
+// excess X = sum over throttled ticks of (D - B_lo) (section 8): every term is exact in fp64, and so is
+// the sum (every throttled D is an fp32 multiple of ulp32(B_lo) and N * bw_max / ulp32(B_lo) < 2^53).
 struct SegStats {
     uint32_t nhi, nthr, trans, ev, lock, vmax;
     double sexc;

@@ -41,7 +41,7 @@ typedef void (*RerunKernel)(ReplayParams, EpiParams, FixParams, int, int, int, i
 // chain kind of a lane policy -> its kernel instantiation (one register allocation per kind)
 int ticker_key(const DevPolicy& q) {
     if (q.kind == LANE_MAGUS) {
-        const int l64 = q.C > 32 ? 1 : 0;
+        const int l64 = q.C > kMaxC32 ? 1 : 0;
         int k = q.k <= 8 ? q.k : 0;
         if (l64 && (k == 3 || k == 5 || k == 6 || k == 7)) k = 0;
         return 100 * l64 + k;   // 0..8, 100..108
@@ -49,8 +49,12 @@ int ticker_key(const DevPolicy& q) {
     return 1000 + q.kind;       // TDP, STATIC_MIN, VALIDATE
 }
 
-template <class T>
-ReplayKernel K() { return (ReplayKernel)magus_replay_kernel<T, kTC, kNStage>; }
+// CTAs per SM a MAGUS chain kind's kernel is built for (register budget): 1 for K >= 4, the generic ring
+// or the 64-bit log (they would spill under 128 registers), else 2 (also TDP / STATIC_MIN / VALIDATE).
+int minb_for(int key) { return key < 1000 && (key == 0 || key >= 4) ? 1 : 2; }
+
+template <class T, int MINB = 2>
+ReplayKernel K() { return (ReplayKernel)magus_replay_kernel<T, kTC, kNStage, MINB>; }
 
 // fix-up re-run kernel for a chain kind (nullptr: stateless kinds never mismatch)
 RerunKernel rerun_kernel_for(int key) {
@@ -68,20 +72,20 @@ RerunKernel rerun_kernel_for(int key) {
 
 ReplayKernel replay_kernel_for(int key) {
     switch (key) {
-        case 0: return K<MagusTicker<0, false>>();
-        case 1: return K<MagusTicker<1, false>>();
-        case 2: return K<MagusTicker<2, false>>();
-        case 3: return K<MagusTicker<3, false>>();
-        case 4: return K<MagusTicker<4, false>>();
-        case 5: return K<MagusTicker<5, false>>();
-        case 6: return K<MagusTicker<6, false>>();
-        case 7: return K<MagusTicker<7, false>>();
-        case 8: return K<MagusTicker<8, false>>();
-        case 100: return K<MagusTicker<0, true>>();
-        case 101: return K<MagusTicker<1, true>>();
-        case 102: return K<MagusTicker<2, true>>();
-        case 104: return K<MagusTicker<4, true>>();
-        case 108: return K<MagusTicker<8, true>>();
+        case 0: return K<MagusTicker<0, false>, 1>();
+        case 1: return K<MagusTicker<1, false>, 2>();
+        case 2: return K<MagusTicker<2, false>, 2>();
+        case 3: return K<MagusTicker<3, false>, 2>();
+        case 4: return K<MagusTicker<4, false>, 1>();
+        case 5: return K<MagusTicker<5, false>, 1>();
+        case 6: return K<MagusTicker<6, false>, 1>();
+        case 7: return K<MagusTicker<7, false>, 1>();
+        case 8: return K<MagusTicker<8, false>, 1>();
+        case 100: return K<MagusTicker<0, true>, 1>();
+        case 101: return K<MagusTicker<1, true>, 1>();
+        case 102: return K<MagusTicker<2, true>, 1>();
+        case 104: return K<MagusTicker<4, true>, 1>();
+        case 108: return K<MagusTicker<8, true>, 1>();
         case 1000 + LANE_TDP: return K<TdpTicker>();
         case 1000 + LANE_STATIC_MIN: return K<StaticMinTicker<false>>();
         default: return K<StaticMinTicker<true>>();
@@ -302,6 +306,9 @@ struct magus_replay {
     FixParams fx{};
     uint32_t* d_wl_count = nullptr;   // [2][G] + cursors [G] + any_unresolved (one allocation)
     int fix_rounds = 2;
+    int n_sm = 148;
+    int alloc_segments = 1;           // scratch is sized for this many segments (re-plans only shrink)
+    int replans = 0;
     // device memory
     std::vector<void*> allocs;
     DevPolicy* d_pol = nullptr;
@@ -418,7 +425,7 @@ extern "C" magus_status magus_nccl_unique_id(void* out128) {
 // Chooses, per launch group, the CTA shape, and globally the time segmentation:
 // enough independent chains to fill the SMs, whole waves of equal-work CTAs, warm-up W >= k + C - 1
 // (+ margin).
-static void choose_geometry(magus_replay_t* h, int n_sm) {
+static void choose_geometry(magus_replay_t* h, int n_sm, int forced_segments) {
     ReplayParams& p = h->rp;
     const magus_replay_desc& d = h->desc;
     const int Q = (int)h->lane.size();
@@ -427,7 +434,7 @@ static void choose_geometry(magus_replay_t* h, int n_sm) {
     p.n_samples = d.n_samples;
     p.trace_stride = d.trace_stride;
     p.n_groups = (d.n_traces + kTracesPerWarp - 1) / kTracesPerWarp;
-    const int ng_smem = (int)((100 * 1024) / (kNStage * Smem::kTileBytes));   // 2 CTAs per SM
+    // smem budget per CTA: 2 CTAs per SM (or 1 for the large-state kinds)
     h->groups.clear();
     for (int q = 0; q < Q;) {
         LaunchGroup g{};
@@ -438,6 +445,7 @@ static void choose_geometry(magus_replay_t* h, int n_sm) {
         g.nq = q - g.q_base;
         g.npw = std::min(g.nq, kMaxConsumerWarps);
         g.n_pblocks = (g.nq + g.npw - 1) / g.npw;
+        const int ng_smem = (int)(((minb_for(g.key) == 2 ? 100 : 200) * 1024) / (kNStage * Smem::kTileBytes));
         int ng = std::min(ng_smem, kMaxConsumerWarps / g.npw);
         ng = std::min(ng, env_int("MAGUS_NG", ng));
         g.ng = std::max(1, std::min(ng, std::max(1, p.n_groups)));
@@ -462,15 +470,22 @@ static void choose_geometry(magus_replay_t* h, int n_sm) {
     int base = 0;   // CTAs per segment over all launch groups
     for (const LaunchGroup& g : h->groups) base += g.n_tblocks * g.n_pblocks;
     int S = 1;
-    if (d.tuning_segments > 0) {
+    if (forced_segments > 0) {
+        S = forced_segments;
+    } else if (d.tuning_segments > 0) {
         S = d.tuning_segments;
     } else {
         // enough consumer warps for `target` per SM (each warp holds 4 chains per lane, so one warp per
         // SM sub-partition already has ILP; more warps hide more latency but need more segments, and
         // every speculative segment boundary can mismatch)
-        const int target = env_int("MAGUS_TARGET_WARPS_PER_SM", 8 * MAGUS_MINB);
-        int64_t warps_per_segment = 0;
-        for (const LaunchGroup& g : h->groups) warps_per_segment += (int64_t)p.n_groups * g.nq;
+        // target: 8 warps per resident CTA, weighted over the launch groups by their warps
+        int64_t warps_per_segment = 0, wtarget = 0;
+        for (const LaunchGroup& g : h->groups) {
+            warps_per_segment += (int64_t)p.n_groups * g.nq;
+            wtarget += (int64_t)p.n_groups * g.nq * 8 * minb_for(g.key);
+        }
+        const int target = env_int("MAGUS_TARGET_WARPS_PER_SM",
+                                   (int)(wtarget / std::max<int64_t>(1, warps_per_segment)));
         S = (int)std::max<int64_t>(1, ((int64_t)n_sm * target) / std::max<int64_t>(1, warps_per_segment));
         const int L0 = (((N + S - 1) / S) + 31) / 32 * 32;
         if (S > 1 && L0 < 4 * W) S = std::max(1, N / (4 * W));   // segments must dwarf their warm-up
@@ -486,6 +501,25 @@ static void choose_geometry(magus_replay_t* h, int n_sm) {
     p.seg_len = L;
     p.warmup = p.n_seg > 1 ? W : 0;
     p.n_blocks = (d.n_samples + 31) / 32;
+    // Spread small launches over every SM: while the launch groups together have fewer CTAs than
+    // SMs, halve the widest CTA (policy warps first, then tile groups).
+    auto total_ctas = [&]() {
+        int t = 0;
+        for (const LaunchGroup& g : h->groups) t += p.n_seg * g.n_tblocks * g.n_pblocks;
+        return t;
+    };
+    while (total_ctas() < n_sm) {
+        LaunchGroup* wide = nullptr;
+        for (LaunchGroup& g : h->groups)
+            if (g.ng * g.npw > 1 && (!wide || g.ng * g.npw > wide->ng * wide->npw)) wide = &g;
+        if (!wide) break;
+        if (wide->npw > 1) wide->npw = (wide->npw + 1) / 2;
+        else wide->ng = (wide->ng + 1) / 2;
+        wide->n_pblocks = (wide->nq + wide->npw - 1) / wide->npw;
+        wide->n_tblocks = std::max(1, (p.n_groups + wide->ng - 1) / wide->ng);
+        wide->threads = wide->ng * wide->npw * 32;
+        wide->smem = Smem::bytes(wide->ng);
+    }
     for (LaunchGroup& g : h->groups) g.n_ctas = p.n_seg * g.n_tblocks * g.n_pblocks;
 }
 
@@ -541,6 +575,7 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
         }
         DevPolicy q{};
         q.one = 1;
+        q.B_hi = h->B_hi;
         q.policy_index = i;
         q.k = 1;
         q.C = 1;
@@ -559,6 +594,7 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
             q.ddec = derive_ddec(L, p.dec_threshold);
             q.s_min = derive_smin(q.C, p.high_freq_threshold);
             q.sticky = q.k >= q.s_min ? 1 : 0;
+            q.smin_sc = q.C <= kMaxC32 ? (uint32_t)q.s_min << (q.C - 1) : 0u;
             q.f0 = 0;
             q.guess_f = 0;   // speculative segment start
         } else if (p.kind == MAGUS_POLICY_STATIC_MIN) {
@@ -597,7 +633,9 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
 
     std::stable_sort(h->lane.begin(), h->lane.end(),
                      [](const DevPolicy& a, const DevPolicy& b) { return ticker_key(a) < ticker_key(b); });
-    choose_geometry(h, n_sm);
+    choose_geometry(h, n_sm, 0);
+    h->n_sm = n_sm;
+    h->alloc_segments = h->rp.n_seg;
     ReplayParams& p = h->rp;
     p.B_lo = h->B_lo;
     p.B_hi = h->B_hi;
@@ -1030,6 +1068,30 @@ extern "C" magus_status magus_replay_results(magus_replay_t* h, magus_results* o
     out->warmup_ticks = h->rp.warmup;
     out->n_mismatched_segments = (int64_t)segs;
     out->fixup_rounds = (int32_t)fl[1];
+    // Adaptive re-plan: speculation pays only while few segment entries are wrong.
+    // When more than 1% of the speculative entries mismatched (e.g. policies whose level freezes on
+    // aliased oscillations), the next runs use half as many segments.  Results are exact either way.
+    if (d.tuning_segments == 0 && h->rp.n_seg > 1 && !env_int("MAGUS_NO_REPLAN", 0)) {
+        const double spec = (double)h->rp.n_lane * (h->rp.n_seg - 1) * std::max(1, d.n_traces);
+        if ((double)segs > 0.01 * spec) {
+            const int S_new = std::max(1, h->rp.n_seg / 2);
+            const ReplayParams keep = h->rp;
+            choose_geometry(h, h->n_sm, S_new);
+            // keep the scratch pointers, thresholds and constants; only the plan changed
+            ReplayParams np = keep;
+            np.n_seg = h->rp.n_seg;
+            np.seg_len = h->rp.seg_len;
+            np.warmup = h->rp.warmup;
+            h->rp = np;
+            for (const LaunchGroup& g : h->groups)
+                cudaFuncSetAttribute((const void*)g.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
+            if (h->gexec) cudaGraphExecDestroy(h->gexec);
+            if (h->graph) cudaGraphDestroy(h->graph);
+            h->gexec = nullptr;
+            h->graph = nullptr;
+            h->replans += 1;
+        }
+    }
     if (out->per_trace && (d.flags & MAGUS_F_PER_TRACE_STATS) && d.n_traces > 0)
         CU(h, cudaMemcpy(out->per_trace, h->d_rec, (size_t)d.n_traces * P * sizeof(TraceRec), cudaMemcpyDeviceToHost));
     if (out->words && (d.flags & MAGUS_F_DUMP_WORDS) && d.n_traces > 0 && h->rp.n_blocks > 0) {

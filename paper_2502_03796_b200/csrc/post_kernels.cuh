@@ -359,7 +359,7 @@ __global__ void __launch_bounds__(256) magus_fix_serial_kernel(const ReplayParam
     const DevPolicy pol = p.pol[q];
 #define MAGUS_SERIAL(...) serial_fixup<__VA_ARGS__>(p, e, pol, q, j, trace, lane)
     if (pol.kind == LANE_MAGUS) {
-        if (pol.C <= 32) MAGUS_SERIAL(MagusTicker<0, false>);
+        if (pol.C <= kMaxC32) MAGUS_SERIAL(MagusTicker<0, false>);
         else MAGUS_SERIAL(MagusTicker<0, true>);
     } else if (pol.kind == LANE_TDP) {
         MAGUS_SERIAL(TdpTicker);
@@ -540,7 +540,7 @@ __global__ void magus_resim_kernel(const ReplayParams p, const float* __restrict
     const int j = first + jd;
 #define MAGUS_RESIM(...) resim_chain<__VA_ARGS__>(p, pol, jd, j, n_win, P, trace, codes)
     if (pol.kind == LANE_MAGUS) {
-        if (pol.C <= 32) MAGUS_RESIM(MagusTicker<0, false>);
+        if (pol.C <= kMaxC32) MAGUS_RESIM(MagusTicker<0, false>);
         else MAGUS_RESIM(MagusTicker<0, true>);
     } else if (pol.kind == LANE_TDP) {
         MAGUS_RESIM(TdpTicker);

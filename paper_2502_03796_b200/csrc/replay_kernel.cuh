@@ -51,7 +51,7 @@ __device__ __forceinline__ SegGeom seg_geom(const ReplayParams& p, int seg) {
 __device__ __forceinline__ void acc_tick(SegStats& ss, uint32_t& vmax, const TickOut& o, float D, float B_lo) {
     ss.nthr += o.thr;
     ss.lock += o.hf;
-    if (o.thr) ss.sexc += (double)D - (double)B_lo;   // exact: both fp32 in [B_lo, bw_max] (section 8)
+    if (o.thr) ss.sexc += (double)D - (double)B_lo;   // exact (SegStats)
     vmax = max(vmax, __float_as_uint(D));
 }
 
@@ -64,7 +64,10 @@ __device__ __forceinline__ void issue_stage(const CUtensorMap* tmap, float* tile
     ptx::tma_load_2d(tile, tmap, full_bar, x, t0, cpol);
 }
 
-template <class T, int TC, int NSTAGE>
+// SOLO: the group has one policy warp, which consumes its own tiles -- its lane 0 refills a stage as soon
+// as the warp has read it (__syncwarp orders the lanes' shared-memory reads, whose values are already in
+// registers, before the refill), without the empty-barrier round trip.
+template <class T, int TC, int NSTAGE, bool SOLO>
 __device__ __forceinline__ void consume(const CUtensorMap* tmap, const ReplayParams& p, const DevPolicy& pol, int q,
                                         int tgroup, int seg, float* tiles, uint64_t* full, uint64_t* empty, int lane,
                                         bool producer) {
@@ -156,29 +159,47 @@ __device__ __forceinline__ void consume(const CUtensorMap* tmap, const ReplayPar
                         fstart[c] = T::level(st[c]);
                     }
                 }
-                for (int tt = 0; tt < TC; ++tt) {
-                    const int t = t0 + tt;
-                    if (t >= G.seg_end) break;
-                    const float4 d4 = rows[tt * (kTracesPerWarp / 4)];
-                    const float d[4] = {d4.x, d4.y, d4.z, d4.w};
-                    const bool ready = (t - G.tau_w) >= k;
-                    const bool lfull = (t - G.tau_w) >= k + C - 1;
+                if (T::kHasFast4 && t0 + TC <= G.seg_end) {
+                    // warm-up stage: the interleaved 4-chain tick with Alg. 1 / Alg. 2 gated per tick (A7, A8)
 #pragma unroll
-                    for (int c = 0; c < kChains; ++c) {
-                        const TickOut o = T::template tick<true>(st[c], d[c], pol, B_lo, B_hi, ready, lfull);
-                        wcmd[c] = (wcmd[c] << 1) | o.cmd;
-                        acc_tick(ss[c], vmax, o, d[c], B_lo);
+                    for (int tt = 0; tt < TC; ++tt) {
+                        const int r = t0 + tt - G.tau_w;
+                        const float4 d4 = rows[tt * (kTracesPerWarp / 4)];
+                        const float d[4] = {d4.x, d4.y, d4.z, d4.w};
+                        T::warm4(st, d, pol, B_lo, Blo_d, wcmd, ss, vmax, r >= k ? 1u : 0u,
+                                 r >= k + C - 1 ? 1u : 0u);
+                    }
+                } else {
+                    for (int tt = 0; tt < TC; ++tt) {
+                        const int t = t0 + tt;
+                        if (t >= G.seg_end) break;
+                        const float4 d4 = rows[tt * (kTracesPerWarp / 4)];
+                        const float d[4] = {d4.x, d4.y, d4.z, d4.w};
+                        const bool ready = (t - G.tau_w) >= k;
+                        const bool lfull = (t - G.tau_w) >= k + C - 1;
+#pragma unroll
+                        for (int c = 0; c < kChains; ++c) {
+                            const TickOut o = T::template tick<true>(st[c], d[c], pol, B_lo, B_hi, ready, lfull);
+                            wcmd[c] = (wcmd[c] << 1) | o.cmd;
+                            acc_tick(ss[c], vmax, o, d[c], B_lo);
+                        }
                     }
                 }
             }
             // release the stage; the group's producer lane refills it with stage i + NSTAGE once every
             // policy warp of the group has released it
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive_u32(empty0 + 8 * slot);
-            if (producer && i + NSTAGE < G.n_stages) {
-                ptx::mbar_wait_u32(empty0 + 8 * slot, phase);
-                ptx::tma_load_2d_u32(tile0 + slot * kTileBytes, tmap, full0 + 8 * slot, x,
-                                     G.tau_w + (i + NSTAGE) * TC, kTileBytes, cpol);
+            if constexpr (SOLO) {
+                if (producer && i + NSTAGE < G.n_stages)
+                    ptx::tma_load_2d_u32(tile0 + slot * kTileBytes, tmap, full0 + 8 * slot, x,
+                                         G.tau_w + (i + NSTAGE) * TC, kTileBytes, cpol);
+            } else {
+                if (lane == 0) ptx::mbar_arrive_u32(empty0 + 8 * slot);
+                if (producer && i + NSTAGE < G.n_stages) {
+                    ptx::mbar_wait_u32(empty0 + 8 * slot, phase);
+                    ptx::tma_load_2d_u32(tile0 + slot * kTileBytes, tmap, full0 + 8 * slot, x,
+                                         G.tau_w + (i + NSTAGE) * TC, kTileBytes, cpol);
+                }
             }
             ++i;
             if (++slot == NSTAGE) {
@@ -208,7 +229,8 @@ __device__ __forceinline__ void consume(const CUtensorMap* tmap, const ReplayPar
         const int j = j0 + c;
         if (j >= p.n_traces) continue;
         T::save(st[c], p, pol, 1, q, seg, j);
-        add_to_chain(p, q, j, ss[c].nhi, ss[c].nthr, ss[c].trans, ss[c].ev, ss[c].lock, ss[c].sexc, ss[c].digest);
+        add_to_chain(p, q, j, ss[c].nhi, ss[c].nthr, ss[c].trans, ss[c].ev, ss[c].lock, ss[c].sexc,
+                     ss[c].digest);
     }
     if (j0 < p.n_traces) atomicMax(p.c_vmax + chain_idx(p, q, j0), vmax);   // lane-level validation maximum
 }
@@ -217,11 +239,10 @@ __device__ __forceinline__ void consume(const CUtensorMap* tmap, const ReplayPar
 // policies [p.q_base, p.q_base + p.nq), all of kind T.  CTA = ng tile groups x npw policy warps
 // (<= 8 warps = 2 per SM sub-partition, so up to 255 registers per thread); lane 0 of each group's
 // first warp produces that group's tiles.
-#ifndef MAGUS_MINB
-#define MAGUS_MINB 2   // CTAs per SM: 2 x 8 warps = 4 warps per SM sub-partition (<= 128 registers)
-#endif
-template <class T, int TC, int NSTAGE>
-__global__ void __launch_bounds__(kMaxConsumerWarps * 32, MAGUS_MINB)
+// MINB = CTAs per SM the register budget is sized for: 2 (<= 128 registers, 16 warps per SM) for the
+// small-state chain kinds, 1 (<= 255 registers) for large rings / 64-bit logs, which would spill.
+template <class T, int TC, int NSTAGE, int MINB>
+__global__ void __launch_bounds__(kMaxConsumerWarps * 32, MINB)
     magus_replay_kernel(const __grid_constant__ CUtensorMap tmap, const ReplayParams p) {
     extern __shared__ __align__(1024) uint8_t smem[];
     using SM = ReplaySmem<TC, NSTAGE>;
@@ -253,8 +274,13 @@ __global__ void __launch_bounds__(kMaxConsumerWarps * 32, MAGUS_MINB)
     if (g >= p.ng || tgroup >= p.n_groups || w >= npw_active) return;
     const int q = p.q_base + pblock * p.npw + w;
     const DevPolicy pol = p.pol[q];
-    consume<T, TC, NSTAGE>(&tmap, p, pol, q, tgroup, seg, tiles + (size_t)g * NSTAGE * SM::kTileFloats,
-                           &full[g * NSTAGE], &empty[g * NSTAGE], lane, w == 0 && lane == 0);
+    float* gt = tiles + (size_t)g * NSTAGE * SM::kTileFloats;
+    if (npw_active == 1)
+        consume<T, TC, NSTAGE, true>(&tmap, p, pol, q, tgroup, seg, gt, &full[g * NSTAGE], &empty[g * NSTAGE], lane,
+                                     lane == 0);
+    else
+        consume<T, TC, NSTAGE, false>(&tmap, p, pol, q, tgroup, seg, gt, &full[g * NSTAGE], &empty[g * NSTAGE], lane,
+                                      w == 0 && lane == 0);
 }
 
 }  // namespace magus

@@ -43,7 +43,7 @@ struct MagusTicker {
                             s[2].cnt, s[3].cnt, vmax, D[0], D[1], D[2], D[3], s[0].ring.oldest(pol.k),
                             s[1].ring.oldest(pol.k), s[2].ring.oldest(pol.k), s[3].ring.oldest(pol.k),
                             __float_as_uint(D[0]), __float_as_uint(D[1]), __float_as_uint(D[2]), __float_as_uint(D[3]),
-                            B_lo, Blo_d, pol.dinc, pol.ddec, bitc, (uint32_t)pol.s_min, pol.one, mone);
+                            B_lo, Blo_d, pol.dinc, pol.ddec, bitc, pol.smin_sc, pol.one, mone);
             s[0].evh = e0;
             s[1].evh = e1;
             s[2].evh = e2;
@@ -54,70 +54,54 @@ struct MagusTicker {
             s[3].ring.push(ad3, pol.k);
         }
     }
+    // Warm-up ticks of the 4 chains (Alg. 1 once `ready`, Alg. 2 once `full`), same interleaved block.
+    __device__ __forceinline__ static void warm4(State* s, const float* D, const DevPolicy& pol, float B_lo,
+                                                 double Blo_d, uint32_t* wcmd, SegStats* ss, uint32_t& vmax,
+                                                 uint32_t ready, uint32_t full) {
+        if constexpr (!LOG64) {
+            double ad0, ad1, ad2, ad3;
+            uint32_t e0 = s[0].evh, e1 = s[1].evh, e2 = s[2].evh, e3 = s[3].evh;
+            const uint32_t bitc = 1u << (pol.C - 1), mone = 0xFFFFFFFFu * pol.one;
+            MAGUS_TICK4W_ASM(s[0].f, s[1].f, s[2].f, s[3].f, ad0, ad1, ad2, ad3, e0, e1, e2, e3, ss[0].sexc,
+                             ss[1].sexc, ss[2].sexc, ss[3].sexc, ss[0].lock, ss[1].lock, ss[2].lock, ss[3].lock,
+                             ss[0].nthr, ss[1].nthr, ss[2].nthr, ss[3].nthr, wcmd[0], wcmd[1], wcmd[2], wcmd[3],
+                             s[0].cnt, s[1].cnt, s[2].cnt, s[3].cnt, vmax, D[0], D[1], D[2], D[3],
+                             s[0].ring.oldest(pol.k), s[1].ring.oldest(pol.k), s[2].ring.oldest(pol.k),
+                             s[3].ring.oldest(pol.k), __float_as_uint(D[0]), __float_as_uint(D[1]),
+                             __float_as_uint(D[2]), __float_as_uint(D[3]), B_lo, Blo_d, pol.dinc, pol.ddec, bitc,
+                             pol.smin_sc, pol.one, mone, ready, full);
+            s[0].evh = e0;
+            s[1].evh = e1;
+            s[2].evh = e2;
+            s[3].evh = e3;
+            s[0].ring.push(ad0, pol.k);
+            s[1].ring.push(ad1, pol.k);
+            s[2].ring.push(ad2, pol.k);
+            s[3].ring.push(ad3, pol.k);
+        }
+    }
+    // One steady-state tick of one chain (the 64-bit-log kinds; the 32-bit kinds use fast4).
     __device__ __forceinline__ static void fast(State& s, float D, const DevPolicy& pol, float B_lo, double Blo_d,
                                                 uint32_t& wcmd, SegStats& ss, uint32_t& vmax) {
         const double old = s.ring.oldest(pol.k);
-        double Ad;
-        uint32_t f = s.f;
-        if constexpr (!LOG64) {
-            uint32_t evh = s.evh;
-            // one steady-state tick, predicates kept in registers (see DESIGN.md section 7 for the op budget)
-            // `one` is a runtime 1 (DevPolicy::one): ptxas keeps the predicated increments as IMADs on the FMA
-            // pipe instead of IADDs on the ALU pipe, which is the tighter of the two here.
-            asm("{\n\t"
-                ".reg .pred plo, pthr, pinc, pev, phf, pc, pk;\n\t"
-                ".reg .f64 dd, dv, dx;\n\t"
-                ".reg .b32 cnt;\n\t"
-                "setp.eq.u32 plo, %0, 0;\n\t"                       // level in effect is f_min
-                "setp.gt.and.f32 pthr, %8, %9, plo;\n\t"           // throttled: f_min and D > B_lo
-                "cvt.f64.f32 dd, %8;\n\t"
-                "mov.f64 %1, dd;\n\t"
-                "@pthr mov.f64 %1, %10;\n\t"                       // A = thr ? B_lo : D   (as fp64, exact)
-                "sub.f64 dv, %1, %11;\n\t"                         // d = A_t - A_{t-k}    (Alg. 1)
-                "sub.f64 dx, dd, %1;\n\t"                          // throttling excess D - A (0 unless thr)
-                "add.f64 %3, %3, dx;\n\t"
-                "setp.gt.f64 pinc, dv, %12;\n\t"                   // +1 iff d > d*_inc
-                "setp.lt.or.f64 pev, dv, %13, pinc;\n\t"           // tune flag: +1 or -1
-                "shl.b32 %2, %2, 1;\n\t"
-                "@pev mad.lo.u32 %2, %17, %17, %2;\n\t"
-                "and.b32 cnt, %2, %14;\n\t"
-                "popc.b32 cnt, cnt;\n\t"
-                "setp.ge.u32 phf, cnt, %15;\n\t"                   // Alg. 2 on the full log
-                "@phf mad.lo.u32 %4, %17, %17, %4;\n\t"
-                "@pthr mad.lo.u32 %5, %17, %17, %5;\n\t"
-                "or.pred pc, phf, pinc;\n\t"                       // lock or +1 -> f_max (A9)
-                "or.pred pk, plo, pev;\n\t"                        // keep f_max unless a flag or at f_min
-                "not.pred pk, pk;\n\t"
-                "or.pred pc, pc, pk;\n\t"
-                "selp.u32 %0, 1, 0, pc;\n\t"
-                "mad.lo.u32 %6, %6, 2, %0;\n\t"
-                "max.u32 %7, %7, %16;\n\t"
-                "}"
-                : "+r"(f), "=&d"(Ad), "+r"(evh), "+d"(ss.sexc), "+r"(ss.lock), "+r"(ss.nthr), "+r"(wcmd), "+r"(vmax)
-                : "f"(D), "f"(B_lo), "d"(Blo_d), "d"(old), "d"(pol.dinc), "d"(pol.ddec), "r"((uint32_t)pol.logmask),
-                  "r"((uint32_t)pol.s_min), "r"(__float_as_uint(D)), "r"(pol.one));
-            s.evh = evh;
-        } else {
-            const bool lo = f == 0u;
-            const bool thr = lo && (D > B_lo);
-            const double Dd = (double)D;
-            Ad = thr ? Blo_d : Dd;
-            const double d = Ad - old;
-            ss.sexc += Dd - Ad;
-            const bool inc = d > pol.dinc;
-            const bool ev = inc || (d < pol.ddec);
-            s.evh = (s.evh << 1) | (LogT)(ev ? 1u : 0u);
-            const uint32_t cnt = popc_log<LOG64>(s.evh & (LogT)pol.logmask);
-            s.cnt = cnt;
-            const bool hf = cnt >= (uint32_t)pol.s_min;
-            f = (hf || inc || (!lo && !ev)) ? 1u : 0u;
-            wcmd = (wcmd << 1) | f;
-            ss.lock += hf ? 1u : 0u;
-            ss.nthr += thr ? 1u : 0u;
-            vmax = max(vmax, __float_as_uint(D));
-        }
+        const uint32_t f = s.f;
+        const bool lo = f == 0u;
+        const bool thr = lo && (D > B_lo);
+        const double Dd = (double)D;
+        const double Ad = thr ? Blo_d : Dd;
+        const double d = Ad - old;
+        ss.sexc += Dd - Ad;
+        const bool inc = d > pol.dinc;
+        const bool ev = inc || (d < pol.ddec);
+        s.evh = (s.evh << 1) | (LogT)(ev ? 1u : 0u);
+        const uint32_t cnt = popc_log<LOG64>(s.evh & (LogT)pol.logmask);
+        const bool hf = cnt >= (uint32_t)pol.s_min;
+        s.f = (hf || inc || (!lo && !ev)) ? 1u : 0u;
+        wcmd = (wcmd << 1) | s.f;
+        ss.lock += hf ? 1u : 0u;
+        ss.nthr += thr ? 1u : 0u;
+        vmax = max(vmax, __float_as_uint(D));
         s.ring.push(Ad, pol.k);
-        s.f = f;
     }
     __device__ __forceinline__ static uint32_t level(const State& s) { return s.f; }
     __device__ __forceinline__ static void set_level(State& s, uint32_t f) { s.f = f; }
@@ -133,7 +117,7 @@ struct MagusTicker {
         const int64_t i = st_idx(p, e, q, seg, j);
         s.f = p.st_f[i];
         s.evh = (LogT)p.st_log[i];
-        s.cnt = popc_log<LOG64>(s.evh & (LogT)pol.logmask);
+        if constexpr (!LOG64) s.cnt = popc_log<LOG64>(s.evh & (LogT)pol.logmask) << (pol.C - 1);
         s.ring.set_all(p.st_ring + ring_idx(p, e, q, seg, 0, j), pol.k, (int64_t)p.n_traces);
     }
     // exact equality of the two stored states (e0, s0) and (e1, s1): level, log bits, ring values
@@ -156,13 +140,28 @@ struct MagusTicker {
 // ----------------------------------------------------------------------------------- TDP default
 struct TdpTicker {
     struct State { uint32_t f; };
-    static constexpr bool kHasFast = false;
+    static constexpr bool kHasFast = true;
     static constexpr bool kHasFast4 = false;
     __device__ __forceinline__ static uint32_t window_count(const State&, const DevPolicy&) { return 0; }
-    __device__ __forceinline__ static void fast(State&, float, const DevPolicy&, float, double, uint32_t&, SegStats&,
-                                                uint32_t&) {}
+    // tdp_tick + acc_tick of one tick, branch-free: A = min(D, B[f]); throttled iff D > B[f];
+    // next level f_min iff A >= a*[f] (the fp32 threshold equivalent of the power predicate, A24)
+    __device__ __forceinline__ static void fast(State& s, float D, const DevPolicy& pol, float B_lo, double Blo_d,
+                                                uint32_t& wcmd, SegStats& ss, uint32_t& vmax) {
+        const bool hi = s.f != 0u;
+        const float B = hi ? pol.B_hi : B_lo;
+        const bool thr = D > B;
+        const float A = fminf(D, B);
+        const uint32_t f = (A >= (hi ? pol.astar_hi : pol.astar_lo)) ? 0u : 1u;
+        ss.nthr += thr ? 1u : 0u;
+        ss.sexc += thr ? (double)D - Blo_d : 0.0;
+        vmax = max(vmax, __float_as_uint(D));
+        wcmd = (wcmd << 1) | f;
+        s.f = f;
+    }
     __device__ __forceinline__ static void fast4(State*, const float*, const DevPolicy&, float, double, uint32_t*,
                                                  SegStats*, uint32_t&) {}
+    __device__ __forceinline__ static void warm4(State*, const float*, const DevPolicy&, float, double, uint32_t*,
+                                                 SegStats*, uint32_t&, uint32_t, uint32_t) {}
     static constexpr bool kStateful = true;
     static constexpr bool kWarmupRules = false;
     __device__ __forceinline__ static void init(State& s, const DevPolicy& pol, bool exact_start) {
@@ -204,6 +203,8 @@ struct StaticMinTicker {
                                                 uint32_t&) {}
     __device__ __forceinline__ static void fast4(State*, const float*, const DevPolicy&, float, double, uint32_t*,
                                                  SegStats*, uint32_t&) {}
+    __device__ __forceinline__ static void warm4(State*, const float*, const DevPolicy&, float, double, uint32_t*,
+                                                 SegStats*, uint32_t&, uint32_t, uint32_t) {}
     static constexpr bool kStateful = false;
     static constexpr bool kWarmupRules = false;
     __device__ __forceinline__ static void init(State& s, const DevPolicy&, bool) { s.f = 0; }

@@ -1,70 +1,96 @@
 #!/usr/bin/env python
-"""Generate paper_2502_03796_b200/csrc/tick4_asm.cuh: one steady-state MAGUS tick
-for the 4 chains of a lane, written as PTX with the four chains' instructions interleaved so that
-ptxas sees independent work next to every dependency.  Semantics = magus_tick<K, false, false>:
+"""Generate paper_2502_03796_b200/csrc/tick4_asm.cuh: one MAGUS tick for the
+4 chains of a lane, written as PTX with the four chains' instructions interleaved so that ptxas sees
+independent work next to every dependency.  Semantics = magus_tick<K, false, SLOW>:
   thr = f_min && D > B_lo;  A = thr ? B_lo : D (fp64, exact);  d = A - A_{t-k}
-  +1 iff d > d*_inc; flag iff +1 or d < d*_dec;  log <<= 1 | flag;  cnt = ones in the last C flags
-  (incremental: + entering flag - flag leaving the window, bit C-1 of the old log);  lock iff cnt >= s_min
-  cmd = lock || +1 || (f_max && !flag);  excess += D - A;  counters; vmax = max(vmax, bits(D))."""
+  +1 iff d > d*_inc; flag iff +1 or d < d*_dec;  log <<= 1 | flag
+  cnt = (ones in the last C flags) << (C-1), kept incrementally: - (log & 2^(C-1)) (the flag leaving the
+  window, already in the scaled unit) + 2^(C-1) if flagged;  lock iff cnt >= s_min << (C-1)
+  cmd = lock || +1 || (f_max && !flag);  excess += D - A;  counters; vmax = max(vmax, bits(D)).
+Two macros: MAGUS_TICK4_ASM (steady state) and MAGUS_TICK4W_ASM (warm-up: Alg. 1 only once `rdy`
+(k+1 samples seen), Alg. 2 only once `full` (C flags logged), A7/A8)."""
 import os
 
 C = 4
-names = [(f"f{c}", "+r") for c in range(C)] + [(f"ad{c}", "=&d") for c in range(C)] + \
-        [(f"evh{c}", "+r") for c in range(C)] + [(f"exc{c}", "+d") for c in range(C)] + \
-        [(f"lock{c}", "+r") for c in range(C)] + [(f"nthr{c}", "+r") for c in range(C)] + \
-        [(f"wcmd{c}", "+r") for c in range(C)] + [(f"cnt{c}", "+r") for c in range(C)] + [("vmax", "+r")]
-inames = [(f"D{c}", "f") for c in range(C)] + [(f"old{c}", "d") for c in range(C)] + \
-         [(f"Dbits{c}", "r") for c in range(C)] + \
-         [("Blo", "f"), ("Blod", "d"), ("dinc", "d"), ("ddec", "d"), ("bitc", "r"), ("smin", "r"), ("one", "r"),
-          ("mone", "r")]
-idx = {n: f"%{i}" for i, (n, _) in enumerate(names + inames)}
-R = idx.__getitem__
-body = ["{", ".reg .pred plo<4>, pthr<4>, pinc<4>, pev<4>, phf<4>, pc<4>, pk<4>, pout<4>;",
-        ".reg .f64 dd<4>, dv<4>, dx<4>;", ".reg .b32 tb<4>;"]
-per_chain = [
-    "setp.eq.u32 plo{c}, {f}, 0;",                               # level in effect is f_min
-    "cvt.f64.f32 dd{c}, {D};",
-    "setp.gt.and.f32 pthr{c}, {D}, {Blo}, plo{c};",             # throttled (A14)
-    "selp.f64 {ad}, {Blod}, dd{c}, pthr{c};",                    # A as fp64 (exact)
-    "sub.f64 dv{c}, {ad}, {old};",                               # Alg. 1 derivative numerator
-    "setp.gt.f64 pinc{c}, dv{c}, {dinc};",                       # +1
-    "setp.lt.or.f64 pev{c}, dv{c}, {ddec}, pinc{c};",            # tune flag
-    "and.b32 tb{c}, {evh}, {bitc};",                             # the flag leaving the C-window
-    "setp.ne.u32 pout{c}, tb{c}, 0;",
-    "shl.b32 {evh}, {evh}, 1;",
-    "@pev{c} mad.lo.u32 {evh}, {one}, {one}, {evh};",
-    "@pout{c} mad.lo.u32 {cnt}, {mone}, {one}, {cnt};",          # window count: - leaving + entering flag
-    "@pev{c} mad.lo.u32 {cnt}, {one}, {one}, {cnt};",
-    "setp.ge.u32 phf{c}, {cnt}, {smin};",                        # Alg. 2
-    "or.pred pc{c}, phf{c}, pinc{c};",
-    "or.pred pk{c}, plo{c}, pev{c};",
-    "not.pred pk{c}, pk{c};",
-    "or.pred pc{c}, pc{c}, pk{c};",                              # lock || +1 || (f_max && !flag)
-    "selp.u32 {f}, 1, 0, pc{c};",
-    "mad.lo.u32 {wcmd}, {wcmd}, 2, {f};",
-    "sub.f64 dx{c}, dd{c}, {ad};",                               # throttling excess
-    "add.f64 {exc}, {exc}, dx{c};",
-    "@phf{c} mad.lo.u32 {lock}, {one}, {one}, {lock};",
-    "@pthr{c} mad.lo.u32 {nthr}, {one}, {one}, {nthr};",
-    "max.u32 {vmax}, {vmax}, {Dbits};",                          # validation (A17)
-]
-for tmpl in per_chain:
-    for c in range(C):
-        body.append(tmpl.format(c=c, f=R(f"f{c}"), D=R(f"D{c}"), Blo=R("Blo"), ad=R(f"ad{c}"), Blod=R("Blod"),
-                                old=R(f"old{c}"), dinc=R("dinc"), ddec=R("ddec"), evh=R(f"evh{c}"), one=R("one"),
-                                bitc=R("bitc"), mone=R("mone"), cnt=R(f"cnt{c}"), smin=R("smin"),
-                                wcmd=R(f"wcmd{c}"), exc=R(f"exc{c}"),
-                                lock=R(f"lock{c}"), nthr=R(f"nthr{c}"), vmax=R("vmax"), Dbits=R(f"Dbits{c}")))
-body.append("}")
-params = ", ".join(n for n, _ in names + inames)
-out = ["// GENERATED by scripts/gen_tick4.py -- do not edit.  One steady-state MAGUS tick for the 4 chains of a",
-       "// lane, the four chains' instructions interleaved (DESIGN.md section 7); semantics = magus_tick<K,..,false>.",
-       "#pragma once",
-       f"#define MAGUS_TICK4_ASM({params}) \\",
-       "    asm( \\"]
-out += [f'        "{l}\\n\\t" \\' for l in body]
-out.append("        : " + ", ".join(f'"{c}"({n})' for n, c in names) + " \\")
-out.append("        : " + ", ".join(f'"{c}"({n})' for n, c in inames) + ")")
+
+
+def build(warm):
+    names = [(f"f{c}", "+r") for c in range(C)] + [(f"ad{c}", "=&d") for c in range(C)] + \
+            [(f"evh{c}", "+r") for c in range(C)] + [(f"exc{c}", "+d") for c in range(C)] + \
+            [(f"lock{c}", "+r") for c in range(C)] + [(f"nthr{c}", "+r") for c in range(C)] + \
+            [(f"wcmd{c}", "+r") for c in range(C)] + [(f"cnt{c}", "+r") for c in range(C)] + [("vmax", "+r")]
+    inames = [(f"D{c}", "f") for c in range(C)] + [(f"old{c}", "d") for c in range(C)] + \
+             [(f"Dbits{c}", "r") for c in range(C)] + \
+             [("Blo", "f"), ("Blod", "d"), ("dinc", "d"), ("ddec", "d"), ("bitc", "r"), ("smin", "r"), ("one", "r"),
+              ("mone", "r")]
+    if warm:
+        inames += [("rdy", "r"), ("full", "r")]
+    idx = {n: f"%{i}" for i, (n, _) in enumerate(names + inames)}
+    R = idx.__getitem__
+    body = ["{", ".reg .pred plo<4>, pthr<4>, pinc<4>, pev<4>, phf<4>, pc<4>, pk<4>, pdec<4>, prdy, pfull;",
+            ".reg .f64 dd<4>, dv<4>, dx<4>;", ".reg .b32 tb<4>;"]
+    if warm:
+        body += [f"setp.ne.u32 prdy, {R('rdy')}, 0;", f"setp.ne.u32 pfull, {R('full')}, 0;"]
+    per_chain = [
+        "setp.eq.u32 plo{c}, {f}, 0;",                               # level in effect is f_min
+        "cvt.f64.f32 dd{c}, {D};",
+        "setp.gt.and.f32 pthr{c}, {D}, {Blo}, plo{c};",             # throttled (A14)
+        "selp.f64 {ad}, {Blod}, dd{c}, pthr{c};",                    # A as fp64 (exact)
+        "sub.f64 dv{c}, {ad}, {old};",                               # Alg. 1 derivative numerator
+    ]
+    if warm:
+        per_chain += [
+            "setp.gt.and.f64 pinc{c}, dv{c}, {dinc}, prdy;",         # +1, once k+1 samples were seen
+            "setp.lt.and.f64 pdec{c}, dv{c}, {ddec}, prdy;",
+            "or.pred pev{c}, pdec{c}, pinc{c};",                     # tune flag
+        ]
+    else:
+        per_chain += [
+            "setp.gt.f64 pinc{c}, dv{c}, {dinc};",                   # +1
+            "setp.lt.or.f64 pev{c}, dv{c}, {ddec}, pinc{c};",        # tune flag
+        ]
+    per_chain += [
+        "and.b32 tb{c}, {evh}, {bitc};",                             # the flag leaving the C-window (scaled)
+        "shl.b32 {evh}, {evh}, 1;",
+        "@pev{c} mad.lo.u32 {evh}, {one}, {one}, {evh};",
+        "mad.lo.u32 {cnt}, tb{c}, {mone}, {cnt};",                   # window count: - leaving + entering flag
+        "@pev{c} mad.lo.u32 {cnt}, {bitc}, {one}, {cnt};",
+        ("setp.ge.and.u32 phf{c}, {cnt}, {smin}, pfull;" if warm    # Alg. 2 on a full log (A8)
+         else "setp.ge.u32 phf{c}, {cnt}, {smin};"),
+        "or.pred pc{c}, phf{c}, pinc{c};",
+        "or.pred pk{c}, plo{c}, pev{c};",
+        "not.pred pk{c}, pk{c};",
+        "or.pred pc{c}, pc{c}, pk{c};",                              # lock || +1 || (f_max && !flag)
+        "selp.u32 {f}, 1, 0, pc{c};",
+        "mad.lo.u32 {wcmd}, {wcmd}, 2, {f};",
+        "sub.f64 dx{c}, dd{c}, {ad};",                               # throttling excess D - A (0 unless thr)
+        "add.f64 {exc}, {exc}, dx{c};",
+        "@phf{c} mad.lo.u32 {lock}, {one}, {one}, {lock};",
+        "@pthr{c} mad.lo.u32 {nthr}, {one}, {one}, {nthr};",
+        "max.u32 {vmax}, {vmax}, {Dbits};",                          # validation (A17)
+    ]
+    for tmpl in per_chain:
+        for c in range(C):
+            body.append(tmpl.format(c=c, f=R(f"f{c}"), D=R(f"D{c}"), Blo=R("Blo"), ad=R(f"ad{c}"), Blod=R("Blod"),
+                                    old=R(f"old{c}"), dinc=R("dinc"), ddec=R("ddec"), evh=R(f"evh{c}"), one=R("one"),
+                                    bitc=R("bitc"), mone=R("mone"), cnt=R(f"cnt{c}"), smin=R("smin"),
+                                    wcmd=R(f"wcmd{c}"), exc=R(f"exc{c}"),
+                                    lock=R(f"lock{c}"), nthr=R(f"nthr{c}"), vmax=R("vmax"), Dbits=R(f"Dbits{c}")))
+    body.append("}")
+    params = ", ".join(n for n, _ in names + inames)
+    name = "MAGUS_TICK4W_ASM" if warm else "MAGUS_TICK4_ASM"
+    out = [f"#define {name}({params}) \\", "    asm( \\"]
+    out += [f'        "{l}\\n\\t" \\' for l in body]
+    out.append("        : " + ", ".join(f'"{c}"({n})' for n, c in names) + " \\")
+    out.append("        : " + ", ".join(f'"{c}"({n})' for n, c in inames) + ")")
+    return out
+
+
+out = ["// GENERATED by scripts/gen_tick4.py -- do not edit.  One MAGUS tick for the 4 chains of a lane, the",
+       "// four chains' instructions interleaved (DESIGN.md section 7); semantics = magus_tick<K, false, SLOW>.",
+       "// cnt is the window count scaled by 2^(C-1).",
+       "#pragma once"]
+out += build(False) + [""] + build(True)
 path = os.path.join(os.path.dirname(__file__), "..", "paper_2502_03796_b200", "csrc", "tick4_asm.cuh")
 open(path, "w").write("\n".join(out) + "\n")
 print("wrote", os.path.normpath(path))
