@@ -93,7 +93,9 @@ typedef struct {
 #define MAGUS_F_PER_TRACE_STATS 0x1u  /* fill magus_results.per_trace */
 #define MAGUS_F_DUMP_WORDS      0x2u  /* per-(trace,policy) 32-tick cmd/tune-flag words from the replay kernel */
 #define MAGUS_F_DUMP_DECISIONS  0x4u  /* per-tick code bytes (DESIGN A27) for a window of traces */
-#define MAGUS_F_TIMING          0x8u  /* record CUDA events around each kernel (magus_replay_kernel_times) */
+#define MAGUS_F_TIMING          0x8u  /* record CUDA events around the replay kernel(s) (magus_replay_kernel_times) */
+#define MAGUS_F_TIMING_DETAIL   0x10u /* with MAGUS_F_TIMING: also around the pre-pass, fix-up and totals (each
+                                         event node costs a few microseconds of the run) */
 
 typedef struct {
     int32_t n_traces;             /* local traces in this rank's shard, >= 0 */
@@ -183,11 +185,11 @@ magus_status magus_replay_run_host(magus_replay_t* h, const float* trace, const 
 magus_status magus_replay_results(magus_replay_t* h, magus_results* out);
 
 /* Device milliseconds of the last run's kernels (needs MAGUS_F_TIMING; waits for the run), CUDA events
- * on the run's stream: out[0] replay kernel(s), out[1] fix-up + epilogue, out[2] totals + allreduce +
- * argmin, out[3] whole run, out[4] speculation pre-pass. */
+ * on the run's stream: out[0] replay kernel(s); with MAGUS_F_TIMING_DETAIL also out[1] fix-up, out[2]
+ * totals + allreduce + argmin, out[3] whole run, out[4] pre-pass, else -1. */
 magus_status magus_replay_kernel_times(magus_replay_t* h, float out_ms[5]);
 
-/* Same four intervals averaged over the last n_last runs (at most 256 are kept), e.g. the K runs of a
+/* Same intervals averaged over the last n_last runs (at most 256 are kept), e.g. the K runs of a
  * timed benchmark region.  Waits for the last run. */
 magus_status magus_replay_timing_summary(magus_replay_t* h, int32_t n_last, float out_ms[5]);
 
@@ -207,10 +209,11 @@ magus_status magus_derive_thresholds(const magus_policy* p, const magus_model* m
 
 int32_t magus_abi_version(void);
 
-/* Diagnostics: the launch geometry chosen at create: out = {n_segments, segment_len, warmup_ticks,
+/* Diagnostics: the current launch plan: out = {n_segments, segment_len, warmup_ticks,
  * tile_groups_per_cta, policy_warps_per_group, trace_blocks, policy_blocks, ctas, threads_per_cta,
- * smem_bytes, lane_policies, launch_groups}. */
-magus_status magus_replay_geometry(const magus_replay_t* h, int32_t out[12]);
+ * smem_bytes, lane_policies, launch_groups, kernels_per_run, 0, 0, 0} (first launch group's CTA shape;
+ * kernels_per_run = the library's kernel launches in one run, excluding the decision-dump re-simulation). */
+magus_status magus_replay_geometry(const magus_replay_t* h, int32_t out[16]);
 
 #ifdef __cplusplus
 }

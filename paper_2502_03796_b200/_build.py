@@ -42,21 +42,30 @@ def _deps():
                                                                __file__]
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, out: str | None = None) -> str:
+    """Compile the library; `out` (or MAGUS_LIB_OUT) = another output path, for build-variant experiments."""
+    out = out or os.environ.get("MAGUS_LIB_OUT")
+    if out:
+        return _compile(out, verbose)
     if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(d) for d in _deps()):
         return LIB
+    return _compile(LIB, verbose)
+
+
+def _compile(LIB: str, verbose: bool) -> str:
+    LIBDIR = os.path.dirname(os.path.abspath(LIB))
     os.makedirs(LIBDIR, exist_ok=True)
     nvcc = _nvcc()
     objs = []
     flags = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2,-ffp-contract=off",
                     "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"), "-I", _nccl_include()]
-    for key in ("MAGUS_TC", "MAGUS_NSTAGE", "MAGUS_MINB"):
+    for key in ("MAGUS_TC", "MAGUS_NSTAGE"):
         if os.environ.get(key):
             flags += [f"-D{key}={int(os.environ[key])}"]
     if os.environ.get("MAGUS_PTXAS_VERBOSE"):
         flags += ["-Xptxas", "-v"]
     for src in SOURCES:
-        obj = os.path.join(LIBDIR, os.path.splitext(src)[0] + ".o")
+        obj = os.path.join(LIBDIR, os.path.splitext(os.path.basename(LIB))[0] + "_" + os.path.splitext(src)[0] + ".o")
         cmd = [nvcc, "-c", os.path.join(CSRC, src), "-o", obj] + flags
         if verbose:
             print(" ".join(cmd), flush=True)

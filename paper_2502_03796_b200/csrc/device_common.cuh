@@ -73,6 +73,21 @@ struct ReplayParams {
     uint32_t* words;       // optional [q][j][n_blocks][2]
 };
 
+__host__ __device__ __forceinline__ uint64_t fix_item(int q, int s, int j) {
+    return ((uint64_t)q << 48) | ((uint64_t)(uint32_t)s << 32) | (uint64_t)(uint32_t)j;
+}
+
+// warp-aggregated append of `item` (lanes with want) to a worklist
+__device__ __forceinline__ void wl_append(uint64_t* wl, uint32_t* count, bool want, uint64_t item) {
+    const unsigned m = __ballot_sync(__activemask(), want);
+    if (!want) return;
+    const int leader = __ffs(m) - 1, lane = threadIdx.x & 31;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(count, (uint32_t)__popc(m));
+    base = __shfl_sync(m, base, leader);
+    wl[base + __popc(m & ((1u << lane) - 1u))] = item;
+}
+
 __host__ __device__ __forceinline__ int64_t st_idx(const ReplayParams& p, int e, int q, int s, int j) {
     return ((int64_t)(e * p.n_lane + q) * p.n_seg + s) * p.n_traces + j;
 }
@@ -249,6 +264,19 @@ struct SegStats {
         digest = 0;
     }
 };
+
+// Per-chain totals are zero at the start of every run: zeroed at creation, then by the totals kernel
+// right after it reads them.
+__device__ __forceinline__ void zero_chain(const ReplayParams& p, int64_t ci) {
+    p.c_nhi[ci] = 0;
+    p.c_nthr[ci] = 0;
+    p.c_trans[ci] = 0;
+    p.c_ev[ci] = 0;
+    p.c_lock[ci] = 0;
+    p.c_vmax[ci] = 0;
+    p.c_sexc[ci] = 0.0;
+    p.c_digest[ci] = 0;
+}
 
 // Add a segment's statistics (or a fix-up delta) to its chain's totals.
 __device__ __forceinline__ void add_to_chain(const ReplayParams& p, int q, int j, uint32_t nhi, uint32_t nthr,

@@ -99,6 +99,25 @@ struct LaunchGroup {
     size_t smem;
 };
 
+// Kernel launch with programmatic stream serialization (PDL) when `pdl`: the kernel may be scheduled
+// while its predecessor drains and waits in griddepcontrol.wait (ptx::pdl_wait) before touching the
+// predecessor's outputs.  Captured into the run's graph as a programmatic edge.
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl,
+                            Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k, ((KArgs)args)...);
+}
+
 thread_local std::string g_error;
 
 // ------------------------------------------------------------------------------------ NCCL (dlopen)
@@ -309,6 +328,7 @@ struct magus_replay {
     int n_sm = 148;
     int alloc_segments = 1;           // scratch is sized for this many segments (re-plans only shrink)
     int replans = 0;
+    bool pdl = true;           // programmatic dependent launch between the run's kernels (MAGUS_NO_PDL=1: off)
     // device memory
     std::vector<void*> allocs;
     DevPolicy* d_pol = nullptr;
@@ -317,11 +337,10 @@ struct magus_replay {
     int validate_lane = -1;           // lane of the validate-only pseudo policy, if any
     TraceRec* d_rec = nullptr;
     double* d_totals = nullptr;
-    double* d_part = nullptr;         // per-policy chunk partials of the totals
-    int* d_argmin = nullptr;
+    uint8_t* d_out = nullptr;         // [P][chunks][13] totals partials (fp64), then the 4 run flag words: one D2H copy
+    int n_chunks = 1;                 // trace chunks of the totals kernel
     int32_t* d_first_low = nullptr;   // [n_traces] speculation aid
     uint8_t* d_chain = nullptr;       // per-chain totals (ReplayParams::c_*)
-    unsigned int* d_finish = nullptr; // totals kernel: last-block counter
     unsigned int* d_flag = nullptr;     // [0] invalid flag, [1] fix rounds, [2..3] fix segments (u64)
     unsigned long long* d_errkey = nullptr;
     uint8_t* d_codes = nullptr;
@@ -335,7 +354,7 @@ struct magus_replay {
     const float* tmap_ptr = nullptr;
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};   // ev[4]: the run's completion
     static constexpr int kTimingRing = 256;
-    std::vector<cudaEvent_t> tev;   // MAGUS_F_TIMING: 4 events per run, ring of kTimingRing runs
+    std::vector<cudaEvent_t> tev;   // MAGUS_F_TIMING: 5 event slots per run, ring of kTimingRing runs
     int64_t n_runs = 0;
     ncclComm_t comm = nullptr;
     cudaGraphExec_t gexec = nullptr;  // the captured run
@@ -672,13 +691,12 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
         p.words = nullptr;
     }
     ALLOC(h->d_rec, (size_t)std::max(1, d.n_traces) * d.n_policies);
-    ALLOC(h->d_totals, (size_t)d.n_policies * MAGUS_N_TOTALS);
-    ALLOC(h->d_part, (size_t)d.n_policies * MAGUS_N_TOTALS * std::max(1, (d.n_traces + kTotTracesPerBlock - 1) /
-                                                                         kTotTracesPerBlock));
-    ALLOC(h->d_argmin, 1);
-    ALLOC(h->d_finish, 1);
+    h->n_chunks = std::max(1, (d.n_traces + kTotThreads - 1) / kTotThreads);
+    const size_t n_part = (size_t)d.n_policies * h->n_chunks * MAGUS_N_TOTALS;
+    ALLOC(h->d_out, n_part * sizeof(double) + 4 * sizeof(unsigned int));
+    h->d_totals = (double*)h->d_out;
+    h->d_flag = (unsigned int*)(h->d_out + n_part * sizeof(double));
     ALLOC(h->d_first_low, (size_t)2 * std::max(1, d.n_traces));
-    ALLOC(h->d_flag, 4);
     ALLOC(h->d_errkey, 1);
     if (!h->smax.empty()) {
         ALLOC(h->d_smax, h->smax.size());
@@ -719,11 +737,13 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
         h->fx.wl_cursor = h->d_wl_count + 2 * G;
         h->fx.any_unresolved = h->d_wl_count + 3 * G;
         h->fix_rounds = std::max(1, env_int("MAGUS_FIX_ROUNDS", 1));
+
     }
 #undef ALLOC
     p.pol = h->d_pol;
     p.first_low = h->d_first_low;
-    cudaMemset(h->d_finish, 0, sizeof(unsigned int));
+    cudaMemset(h->d_chain, 0, nchain * kChainBytes);   // zero at every run start from here on (totals kernel)
+    h->pdl = !env_int("MAGUS_NO_PDL", 0);
     if ((ce = cudaMemcpy(h->d_pol, h->lane.data(), h->lane.size() * sizeof(DevPolicy), cudaMemcpyHostToDevice)) !=
         cudaSuccess) {
         magus_status s = cuda_fail(h, ce, "cudaMemcpy policies");
@@ -835,29 +855,39 @@ static magus_status encode_tmap(magus_replay_t* h, const float* d_trace) {
 static magus_status enqueue_run(magus_replay_t* h, const float* d_trace, const float* d_w, cudaStream_t s,
                                 cudaEvent_t* tv, bool capturing) {
     // inside a stream capture, only "external" records become event-record nodes of the graph
-    auto rec = [&](cudaEvent_t e) {
-        return capturing ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal) : cudaEventRecord(e, s);
+    // inside a capture, the event-record node just added is the stream's only capture dependency: keep
+    // it with its timing slot so that graph replays can re-point it (launch_graph)
+    auto rec = [&](int k) -> cudaError_t {
+        if (!capturing) return cudaEventRecord(tv[k], s);
+        cudaError_t e = cudaEventRecordWithFlags(tv[k], s, cudaEventRecordExternal);
+        if (e != cudaSuccess) return e;
+        cudaStreamCaptureStatus cs;
+        const cudaGraphNode_t* deps = nullptr;
+        size_t nd = 0;
+        e = cudaStreamGetCaptureInfo(s, &cs, nullptr, nullptr, &deps, &nd);
+        if (e == cudaSuccess && nd == 1) h->g_events.push_back({deps[0], k});
+        return e;
     };
     const magus_replay_desc& d = h->desc;
     const bool has_work = d.n_traces > 0 && d.n_samples > 0;
-    const bool timing = tv != nullptr;
+    const bool timing = tv != nullptr;   // events around the replay kernel(s)
+    const bool detail = timing && (d.flags & MAGUS_F_TIMING_DETAIL);   // ... and around every phase
     ReplayParams p = h->rp;
     EpiParams ep = h->ep;
     ep.w = d_w;
-    CU(h, cudaMemsetAsync(h->d_flag, 0, 4 * sizeof(unsigned int), s));
-    if (timing) CU(h, rec(tv[0]));
-    CU(h, cudaMemsetAsync(h->d_chain, 0, (size_t)p.n_lane * std::max(1, d.n_traces) * kChainBytes, s));
-    if (has_work && p.n_seg > 1) {
-        // speculation aid: first subsampled low tick of every trace
-        CU(h, cudaMemsetAsync(h->d_first_low, 0x7F, (size_t)2 * d.n_traces * sizeof(int32_t), s));
-        const int sub = 256, per_chunk = 4;    // every 256th row: 0.4% of the trace bytes
-        const int64_t n_sub = ((int64_t)d.n_samples + sub - 1) / sub;
-        dim3 gfl((unsigned)((d.n_traces + 127) / 128), (unsigned)((n_sub + per_chunk - 1) / per_chunk));
-        magus_first_low_kernel<<<gfl, 128, 0, s>>>(d_trace, d.n_traces, d.n_samples, d.trace_stride, h->B_lo, sub,
-                                                     per_chunk, h->d_first_low);
-        CU(h, cudaGetLastError());
+    if (detail) CU(h, rec(0));
+    {
+        // pre-pass: zeroes the run's flag / worklist words; for segmented runs also the speculation aid
+        // (first subsampled low / high tick of every trace).  The per-chain totals are
+        // already zero (creation, then the previous run's totals kernel).
+        const bool seg = has_work && p.n_seg > 1;
+        const int n_blk = seg ? (d.n_traces + kPrepassTraces - 1) / kPrepassTraces : 1;
+        CU(h, launch_k(magus_prepass_kernel, dim3((unsigned)n_blk), dim3(kPrepassTraces * kPrepassSlices), 0, s, false,
+                       d_trace, d.n_traces, d.n_samples, (int64_t)d.trace_stride, h->B_lo, 256,
+                       seg ? h->d_first_low : (int*)nullptr, (uint32_t*)h->d_flag, 4, h->d_wl_count,
+                       3 * h->fx.n_fgroups + 1, h->fx.unresolved, p.n_lane));
     }
-    if (timing) CU(h, rec(tv[1]));
+    if (timing) CU(h, rec(1));
     if (has_work) {
         // launch groups (one chain kind each) run concurrently: fork onto auxiliary streams and join
         // (parallel branches when the run is captured as a graph)
@@ -876,69 +906,67 @@ static magus_status enqueue_run(magus_replay_t* h, const float* d_trace, const f
             pg.npw = g.npw;
             pg.n_tblocks = g.n_tblocks;
             pg.n_pblocks = g.n_pblocks;
-            g.kernel<<<g.n_ctas, g.threads, g.smem, gs>>>(h->tmap, pg);
-            CU(h, cudaGetLastError());
+            CU(h, launch_k(g.kernel, dim3((unsigned)g.n_ctas), dim3((unsigned)g.threads), g.smem, gs,
+                           h->pdl && G == 1 && !timing, h->tmap, pg));
         }
         for (int g = 1; g < G; ++g) {
             CU(h, cudaEventRecord(h->join_ev[g - 1], h->aux[g - 1]));
             CU(h, cudaStreamWaitEvent(s, h->join_ev[g - 1], 0));
         }
     }
-    if (timing) CU(h, rec(tv[2]));
+    if (timing) CU(h, rec(2));
     if (d.n_traces > 0) {
         const int G = h->fx.n_fgroups;
         const FixParams& fx = h->fx;
         if (has_work && p.n_seg > 1) {
-            // exact fix-up: round 1 checks every segment entry; later rounds only re-check the
-            // successors of segments whose exit changed; a serial walk finishes the rest.
-            CU(h, cudaMemsetAsync(h->d_wl_count, 0, (3 * G + 1) * sizeof(uint32_t), s));
-            CU(h, cudaMemsetAsync(fx.unresolved, 0, (size_t)p.n_lane * d.n_traces, s));
+            // exact fix-up: round 1 checks every segment entry against the previous exit; later rounds
+            // only re-check the successors of segments whose exit changed; a serial walk finishes the rest
+            // (worklist counters and `unresolved` zeroed by the pre-pass).
+            const bool pd = h->pdl;
             dim3 gc((unsigned)((d.n_traces + 255) / 256), (unsigned)(p.n_seg - 1), (unsigned)p.n_lane);
-            magus_fix_check_all_kernel<<<gc, 256, 0, s>>>(p, fx);
-            CU(h, cudaGetLastError());
-            const unsigned rr_blocks = 148 * 4;
-            for (int g = 0; g < G; ++g) {
-                RerunKernel rk = rerun_kernel_for(h->groups[g].key);
-                if (!rk) continue;
-                rk<<<rr_blocks, 256, 0, s>>>(p, ep, fx, g, 0, 1, 1, d_trace);
-                CU(h, cudaGetLastError());
-            }
-            for (int r = 2; r <= h->fix_rounds; ++r) {
-                CU(h, cudaMemsetAsync(fx.wl_count, 0, G * sizeof(uint32_t), s));                 // buf 0
-                magus_fix_check_cand_kernel<<<148, 256, 0, s>>>(p, fx, 1, 0, 0);
-                CU(h, cudaGetLastError());
-                CU(h, cudaMemsetAsync(fx.wl_count + G, 0, 2 * G * sizeof(uint32_t), s));         // buf 1 + cursors
+            CU(h, launch_k(magus_fix_check_all_kernel, gc, dim3(256), 0, s, pd && !timing, p, fx));
+            const cudaStream_t fs = s;
+            magus_status fst = [&]() -> magus_status {
+                const unsigned rr_blocks = 148 * 4;
                 for (int g = 0; g < G; ++g) {
                     RerunKernel rk = rerun_kernel_for(h->groups[g].key);
                     if (!rk) continue;
-                    rk<<<rr_blocks, 256, 0, s>>>(p, ep, fx, g, 0, 1, r, d_trace);
-                    CU(h, cudaGetLastError());
+                    CU(h, launch_k(rk, dim3(rr_blocks), dim3(256), 0, fs, pd, p, ep, fx, g, 0, 1, 1, d_trace));
                 }
-            }
-            magus_fix_check_cand_kernel<<<148, 256, 0, s>>>(p, fx, 1, 0, 1);
-            CU(h, cudaGetLastError());
-            dim3 gs((unsigned)((d.n_traces + 7) / 8), (unsigned)p.n_lane);
-            magus_fix_serial_kernel<<<gs, 256, 0, s>>>(p, ep, fx, d_trace);
-            CU(h, cudaGetLastError());
+                for (int r = 2; r <= h->fix_rounds; ++r) {
+                    CU(h, cudaMemsetAsync(fx.wl_count, 0, G * sizeof(uint32_t), fs));                 // buf 0
+                    magus_fix_check_cand_kernel<<<148, 256, 0, fs>>>(p, fx, 1, 0, 0);
+                    CU(h, cudaGetLastError());
+                    CU(h, cudaMemsetAsync(fx.wl_count + G, 0, 2 * G * sizeof(uint32_t), fs));         // buf 1 + cursors
+                    for (int g = 0; g < G; ++g) {
+                        RerunKernel rk = rerun_kernel_for(h->groups[g].key);
+                        if (!rk) continue;
+                        rk<<<rr_blocks, 256, 0, fs>>>(p, ep, fx, g, 0, 1, r, d_trace);
+                        CU(h, cudaGetLastError());
+                    }
+                }
+                CU(h, launch_k(magus_fix_check_cand_kernel, dim3(148), dim3(256), 0, fs, pd, p, fx, 1, 0, 1));
+                dim3 gs((unsigned)((d.n_traces + 7) / 8), (unsigned)p.n_lane);
+                CU(h, launch_k(magus_fix_serial_kernel, gs, dim3(256), 0, fs, pd, p, ep, fx, d_trace));
+                return MAGUS_OK;
+            }();
+            if (fst != MAGUS_OK) return fst;
         }
     }
-    if (timing) CU(h, rec(tv[3]));
+    if (detail) CU(h, rec(3));
     {
-        // per-policy fixed-order sums; the last block also finishes the totals (and the argmin if world == 1)
-        const int n_chunks = std::max(1, (d.n_traces + kTotTracesPerBlock - 1) / kTotTracesPerBlock);
-        magus_totals_kernel<<<dim3(d.n_policies, n_chunks), kTotThreads, 0, s>>>(
-            p, ep, h->d_lane_of_policy, h->validate_lane, h->digest_all_hi, h->d_part, h->d_finish, h->d_totals,
-            d.world > 1 ? nullptr : h->d_argmin);
-        CU(h, cudaGetLastError());
+        // per-trace records and per-(policy, trace chunk) fixed-order partial sums (the host adds the chunks)
+        CU(h, launch_k(magus_totals_kernel, dim3(d.n_policies, h->n_chunks), dim3(kTotThreads), 0, s,
+                       h->pdl && !detail, p, ep, (const int*)h->d_lane_of_policy, h->validate_lane, h->digest_all_hi,
+                       (d.flags & MAGUS_F_PER_TRACE_STATS) ? 1 : 0, h->d_totals));
     }
     if (d.world > 1) {
-        ncclResult_t r = nccl().AllReduce(h->d_totals, h->d_totals, (size_t)d.n_policies * MAGUS_N_TOTALS, ncclFloat64,
+        ncclResult_t r = nccl().AllReduce(h->d_totals, h->d_totals,
+                                          (size_t)d.n_policies * h->n_chunks * MAGUS_N_TOTALS, ncclFloat64,
                                           ncclSum, h->comm, s);
         if (r != ncclSuccess) return fail(h, MAGUS_ERR_NCCL, std::string("ncclAllReduce: ") + nccl().GetErrorString(r));
-        magus_argmin_kernel<<<1, 32, 0, s>>>(h->d_totals, d.n_policies, h->d_argmin);
-        CU(h, cudaGetLastError());
     }
-    if (timing) CU(h, rec(tv[4]));
+    if (detail) CU(h, rec(4));
     return MAGUS_OK;
 }
 
@@ -961,25 +989,10 @@ static magus_status launch_graph(magus_replay_t* h, const float* d_trace, const 
             return st;
         }
         if (ce != cudaSuccess) return cuda_fail(h, ce, "cudaStreamEndCapture");
-        size_t n_nodes = 0;
-        cudaGraphGetNodes(graph, nullptr, &n_nodes);
-        std::vector<cudaGraphNode_t> nodes(n_nodes);
-        cudaGraphGetNodes(graph, nodes.data(), &n_nodes);
         const cudaError_t ie = cudaGraphInstantiate(&h->gexec, graph, 0);
         if (ie != cudaSuccess) {
             cudaGraphDestroy(graph);
             return cuda_fail(h, ie, "cudaGraphInstantiate");
-        }
-        if (tv) {   // which ring-slot event each event-record node records
-            for (cudaGraphNode_t nd : nodes) {
-                cudaGraphNodeType ty;
-                cudaGraphNodeGetType(nd, &ty);
-                if (ty != cudaGraphNodeTypeEventRecord) continue;
-                cudaEvent_t ev;
-                cudaGraphEventRecordNodeGetEvent(nd, &ev);
-                for (int k = 0; k < 5; ++k)
-                    if (ev == tv[k]) h->g_events.push_back({nd, k});
-            }
         }
         h->graph = graph;   // kept: exec-node updates take the original graph's node handles
         h->g_trace = d_trace;
@@ -1054,14 +1067,24 @@ extern "C" magus_status magus_replay_results(magus_replay_t* h, magus_results* o
     CU(h, cudaEventSynchronize(h->ev[4]));
     CU(h, cudaGetLastError());
     const int P = d.n_policies;
-    if (out->policy_totals)
-        CU(h, cudaMemcpy(out->policy_totals, h->d_totals, (size_t)P * MAGUS_N_TOTALS * sizeof(double),
-                         cudaMemcpyDeviceToHost));
+    // one copy: the totals partials and the run's flag words (adjacent on the device); the chunks are
+    // added here in chunk order (fixed order: the result does not depend on timing or the rank layout)
+    const size_t n_part = (size_t)P * h->n_chunks * MAGUS_N_TOTALS;
+    std::vector<double> part(n_part + 2);
+    CU(h, cudaMemcpy(part.data(), h->d_out, n_part * sizeof(double) + 4 * sizeof(unsigned int), cudaMemcpyDeviceToHost));
+    std::vector<double> tot((size_t)P * MAGUS_N_TOTALS, 0.0);
+    for (int pp = 0; pp < P; ++pp)
+        for (int c = 0; c < h->n_chunks; ++c)
+            for (int f = 0; f < MAGUS_N_TOTALS; ++f)
+                tot[(size_t)pp * MAGUS_N_TOTALS + f] += part[((size_t)pp * h->n_chunks + c) * MAGUS_N_TOTALS + f];
+    if (out->policy_totals) std::memcpy(out->policy_totals, tot.data(), tot.size() * sizeof(double));
+    // argmin over policies of the total EDP, ties -> lowest index (A23)
     int am = 0;
-    CU(h, cudaMemcpy(&am, h->d_argmin, sizeof(int), cudaMemcpyDeviceToHost));
+    for (int pp = 1; pp < P; ++pp)
+        if (tot[(size_t)pp * MAGUS_N_TOTALS + 3] < tot[(size_t)am * MAGUS_N_TOTALS + 3]) am = pp;
     out->argmin_policy = am;
     unsigned int fl[4] = {0, 0, 0, 0};
-    CU(h, cudaMemcpy(fl, h->d_flag, sizeof(fl), cudaMemcpyDeviceToHost));
+    std::memcpy(fl, part.data() + n_part, sizeof(fl));
     unsigned long long segs = 0;
     std::memcpy(&segs, &fl[2], 8);
     out->n_segments = h->rp.n_seg;
@@ -1140,18 +1163,19 @@ static magus_status timing_avg(magus_replay_t* h, int n_last, float out_ms[5]) {
     CU(h, cudaEventSynchronize(h->ev[4]));
     const int64_t n = std::min<int64_t>({(int64_t)std::max(1, n_last), h->n_runs, (int64_t)magus_replay::kTimingRing});
     // events per run: 0 run start, 1 replay start (after the speculation pre-pass), 2 replay end,
-    // 3 fix-up + epilogue end, 4 totals (+ allreduce) + argmin end
+    // 3 fix-up end, 4 totals (+ allreduce) + argmin end; only 1 and 2 without MAGUS_F_TIMING_DETAIL
     const int iv[5][2] = {{1, 2}, {2, 3}, {3, 4}, {0, 4}, {0, 1}};
+    const int n_iv = (h->desc.flags & MAGUS_F_TIMING_DETAIL) ? 5 : 1;
     double acc[5] = {0, 0, 0, 0, 0};
     for (int64_t r = h->n_runs - n; r < h->n_runs; ++r) {
         cudaEvent_t* tv = &h->tev[5 * (r % magus_replay::kTimingRing)];
-        for (int k = 0; k < 5; ++k) {
+        for (int k = 0; k < n_iv; ++k) {
             float ms;
             CU(h, cudaEventElapsedTime(&ms, tv[iv[k][0]], tv[iv[k][1]]));
             acc[k] += ms;
         }
     }
-    for (int i = 0; i < 5; ++i) out_ms[i] = (float)(acc[i] / (double)n);
+    for (int i = 0; i < 5; ++i) out_ms[i] = i < n_iv ? (float)(acc[i] / (double)n) : -1.0f;
     return MAGUS_OK;
 }
 
@@ -1164,14 +1188,24 @@ extern "C" magus_status magus_replay_timing_summary(magus_replay_t* h, int32_t n
 }
 
 // Diagnostics: the chosen geometry (first launch group's CTA shape).
-extern "C" magus_status magus_replay_geometry(const magus_replay_t* h, int32_t out[12]) {
+extern "C" magus_status magus_replay_geometry(const magus_replay_t* h, int32_t out[16]) {
     if (!h || !out) return MAGUS_ERR_INVALID_ARG;
     const ReplayParams& p = h->rp;
+    const magus_replay_desc& d = h->desc;
     int ctas = 0;
     for (const LaunchGroup& g : h->groups) ctas += g.n_ctas;
     const LaunchGroup& g0 = h->groups.front();
-    const int32_t v[12] = {p.n_seg, p.seg_len, p.warmup, g0.ng, g0.npw, g0.n_tblocks, g0.n_pblocks, ctas,
-                           g0.threads, (int32_t)g0.smem, p.n_lane, (int32_t)h->groups.size()};
+    // kernel launches of one run, as enqueue_run issues them
+    const bool has_work = d.n_traces > 0 && d.n_samples > 0;
+    int nk = 1 + (has_work ? (int)h->groups.size() : 0);          // pre-pass, replay per launch group
+    if (has_work && p.n_seg > 1) {
+        int nr = 0;
+        for (const LaunchGroup& g : h->groups) nr += rerun_kernel_for(g.key) ? 1 : 0;
+        nk += 1 + nr * h->fix_rounds + (h->fix_rounds - 1) + 2;  // check, re-run rounds, candidate checks, serial
+    }
+    nk += 1;                                                      // totals
+    const int32_t v[16] = {p.n_seg, p.seg_len, p.warmup, g0.ng, g0.npw, g0.n_tblocks, g0.n_pblocks, ctas,
+                           g0.threads, (int32_t)g0.smem, p.n_lane, (int32_t)h->groups.size(), nk, 0, 0, 0};
     std::memcpy(out, v, sizeof(v));
     return MAGUS_OK;
 }

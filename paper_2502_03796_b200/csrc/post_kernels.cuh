@@ -1,14 +1,14 @@
-// post_kernels.cuh -- after the replay kernel:
+// post_kernels.cuh -- the kernels around the replay kernel:
+//   magus_prepass_kernel         run start: zeroes the run's scratch words, speculation aid (first_low)
 //   magus_fix_*_kernel           exact fix-up of speculative time segments: worklist rounds with
 //                                lane-level work stealing, then a serial per-chain fallback
-//   magus_epilogue_kernel        per-trace records (closed-form energy model from sufficient
-//                                statistics)
-//   magus_totals_kernel          per-policy fixed-order sums: thread-strided, warp-shuffle tree, smem
-//   magus_argmin_kernel          argmin over policies of the total EDP (ties -> lowest index, A23)
+//   magus_totals_kernel          per-trace records (closed-form energy model from sufficient statistics,
+//                                DESIGN.md section 8) and per-policy fixed-order sums
 //   magus_resim_kernel           per-tick decision codes for a dump window (test diagnostics)
 //   magus_scan_invalid_kernel    first invalid (trace, tick) when the replay flagged one
 #pragma once
 #include "device_common.cuh"
+#include "ptx.cuh"
 #include "tickers.cuh"
 
 namespace magus {
@@ -88,20 +88,9 @@ struct FixParams {
     unsigned int* any_unresolved;
 };
 
-__device__ __forceinline__ uint64_t fix_item(int q, int s, int j) {
-    return ((uint64_t)q << 48) | ((uint64_t)(uint32_t)s << 32) | (uint64_t)(uint32_t)j;
-}
-
 // warp-aggregated append of `item` (lanes with want) to list `buf` of group g
 __device__ __forceinline__ void fix_append(const FixParams& f, int buf, int g, bool want, uint64_t item) {
-    const unsigned m = __ballot_sync(__activemask(), want);
-    if (!want) return;
-    const int leader = __ffs(m) - 1, lane = threadIdx.x & 31;
-    uint32_t base = 0;
-    if (lane == leader) base = atomicAdd(&f.wl_count[buf * f.n_fgroups + g], (uint32_t)__popc(m));
-    base = __shfl_sync(m, base, leader);
-    const uint32_t rank = __popc(m & ((1u << lane) - 1u));
-    f.wl[(int64_t)buf * f.cap_total + f.grp_off[g] + base + rank] = item;
+    wl_append(f.wl + (int64_t)buf * f.cap_total + f.grp_off[g], &f.wl_count[buf * f.n_fgroups + g], want, item);
 }
 
 template <class T>
@@ -128,6 +117,7 @@ __device__ __forceinline__ void copy_state(const ReplayParams& p, const DevPolic
 
 // Round 1: every (q, s >= 1, j) whose speculative entry differs from the previous exit.
 __global__ void __launch_bounds__(256) magus_fix_check_all_kernel(const ReplayParams p, const FixParams f) {
+    ptx::pdl_wait();
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     const int s = blockIdx.y + 1, q = blockIdx.z;
     if (j >= p.n_traces) return;
@@ -140,6 +130,7 @@ __global__ void __launch_bounds__(256) magus_fix_check_all_kernel(const ReplayPa
 // predecessor's new exit (staged in e = 2) and check the entry again.
 __global__ void __launch_bounds__(256) magus_fix_check_cand_kernel(const ReplayParams p, const FixParams f, int buf_in,
                                                                    int buf_out, int mark_unresolved) {
+    ptx::pdl_wait();
     for (int g = 0; g < f.n_fgroups; ++g) {
         const uint32_t n = f.wl_count[buf_in * f.n_fgroups + g];
         for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < ((n + 31u) & ~31u); i += gridDim.x * blockDim.x) {
@@ -256,6 +247,7 @@ template <class T>
 __global__ void __launch_bounds__(256) magus_fix_rerun_kernel(const ReplayParams p, const EpiParams e, const FixParams f,
                                                               int g, int buf_in, int buf_out, int round,
                                                               const float* __restrict__ trace) {
+    ptx::pdl_wait();
     if (f.wl_count[buf_in * f.n_fgroups + g] == 0) return;
     rerun_items<T>(p, e, f, g, buf_in, buf_out, round, trace);
 }
@@ -351,6 +343,7 @@ __device__ void serial_fixup(const ReplayParams& p, const EpiParams& e, const De
 
 __global__ void __launch_bounds__(256) magus_fix_serial_kernel(const ReplayParams p, const EpiParams e, const FixParams f,
                                                                const float* __restrict__ trace) {
+    ptx::pdl_wait();
     if (*f.any_unresolved == 0) return;
     const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
@@ -367,87 +360,62 @@ __global__ void __launch_bounds__(256) magus_fix_serial_kernel(const ReplayParam
 #undef MAGUS_SERIAL
 }
 
-// ================================================================================= epilogue
-// One thread per (trace, lane policy): the chain's totals -> the closed-form record (section 8).  An
-// extra grid row (blockIdx.y == n_lane) writes the STATIC_MAX records: at f_max A = D <= bw_max, never
-// throttled, never a transition or a tune flag, digest of an all-f_max command stream (A17, A21).
-__global__ void __launch_bounds__(256) magus_epilogue_kernel(const ReplayParams p, const EpiParams e,
-                                                             const int* __restrict__ smax_policies, int n_smax,
-                                                             uint64_t digest_all_hi) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    const int q = blockIdx.y;
-    if (j >= p.n_traces) return;
-    if (q == p.n_lane) {
-        for (int i = 0; i < n_smax; ++i) {
-            TraceRec& r = e.rec[(int64_t)j * e.n_policies + smax_policies[i]];
-            finish_record(r, e, (double)e.w[j], (int64_t)e.n_samples, 0, 0, 0, 0, 0.0, digest_all_hi);
-        }
-        return;
-    }
-    const DevPolicy pol = p.pol[q];
-    const int64_t ci = chain_idx(p, q, j);
-    if (pol.policy_index >= 0) {
-        TraceRec& r = e.rec[(int64_t)j * e.n_policies + pol.policy_index];
-        finish_record(r, e, (double)e.w[j], (int64_t)p.c_nhi[ci], (int64_t)p.c_nthr[ci], (int64_t)p.c_trans[ci],
-                      (int64_t)p.c_ev[ci], (int64_t)p.c_lock[ci], p.c_sexc[ci], (uint64_t)p.c_digest[ci]);
-    }
-    if (p.c_vmax[ci] > p.bwbits) atomicOr(e.flag_invalid, 1u);
-}
-
-constexpr int kTotThreads = 256;
+// ================================================================================= totals
+// One thread per (trace, policy): the chain's totals -> the closed-form record (section 8), STATIC_MAX
+// records from their closed form (at f_max A = D <= bw_max: never throttled, never a transition or a
+// tune flag, digest of an all-f_max command stream, A17 / A21); then fixed-order per-policy sums.
+constexpr int kTotThreads = 256;       // = traces per chunk
 constexpr int kNTot = 13;              // MAGUS_N_TOTALS
-constexpr int kTotTracesPerBlock = 256;   // one trace per thread per block: many blocks, short tails
 
-// Stage 1: block (p, c) sums traces [c*1024, (c+1)*1024) of policy p in a fixed order (4 per thread
-// sequentially, then an xor-shuffle tree, then the 8 warp partials in order) -> part[p][c].
+// Block (p, c): the closed-form records of policy p for traces [256 c, 256 c + 256), one per thread (written
+// out only when requested), then their fixed-order sum: an xor-shuffle tree per warp, the 8 warp partials
+// in order -> part[p][c][0..11], part[p][c][12] = the chunk's trace count.  The host (or, across ranks,
+// the allreduce and then the host) adds the chunks in order.  Reading a chain's totals zeroes them for
+// the next run; a sample above bw_max (or invalid) raises the run's flag (A17).
 __global__ void __launch_bounds__(kTotThreads) magus_totals_kernel(const ReplayParams rp, const EpiParams e,
                                                                     const int* __restrict__ lane_of_policy,
                                                                     int validate_lane, uint64_t digest_all_hi,
-                                                                    double* __restrict__ part, unsigned int* finish,
-                                                                    double* __restrict__ totals,
-                                                                    int* __restrict__ argmin) {
+                                                                    int write_rec, double* __restrict__ part) {
+    ptx::pdl_wait();
     const int n_traces = rp.n_traces, n_policies = e.n_policies;
-    TraceRec* rec = e.rec;
     const int p = blockIdx.x, c = blockIdx.y;
-    // the per-trace records of policy p for this chunk (section 8), then their fixed-order sums
-    {
-        const int q = lane_of_policy[p];
-        const int j_end0 = min(n_traces, (c + 1) * kTotTracesPerBlock);
-        for (int j = c * kTotTracesPerBlock + threadIdx.x; j < j_end0; j += kTotThreads) {
-            TraceRec& r = rec[(int64_t)j * n_policies + p];
-            if (q < 0) {   // STATIC_MAX: never throttled, no transition or tune flag (A17, A21)
-                finish_record(r, e, (double)e.w[j], (int64_t)e.n_samples, 0, 0, 0, 0, 0.0, digest_all_hi);
-            } else {
-                const int64_t ci = chain_idx(rp, q, j);
-                finish_record(r, e, (double)e.w[j], (int64_t)rp.c_nhi[ci], (int64_t)rp.c_nthr[ci],
-                              (int64_t)rp.c_trans[ci], (int64_t)rp.c_ev[ci], (int64_t)rp.c_lock[ci], rp.c_sexc[ci],
-                              (uint64_t)rp.c_digest[ci]);
-                if (rp.c_vmax[ci] > rp.bwbits) atomicOr(e.flag_invalid, 1u);
-            }
-            if (p == 0 && validate_lane >= 0 && rp.c_vmax[chain_idx(rp, validate_lane, j)] > rp.bwbits)
-                atomicOr(e.flag_invalid, 1u);
-        }
-        __syncthreads();   // this block's records are read back below by other threads of the block
-    }
+    const int q = lane_of_policy[p];
+    const int j = c * kTotThreads + threadIdx.x;
     double acc[kNTot - 1];
 #pragma unroll
     for (int f = 0; f < kNTot - 1; ++f) acc[f] = 0.0;
-    const int j_end = min(n_traces, (c + 1) * kTotTracesPerBlock);
-    for (int j = c * kTotTracesPerBlock + threadIdx.x; j < j_end; j += kTotThreads) {
-        const TraceRec& r = rec[(int64_t)j * n_policies + p];
-        acc[0] += r.E;
-        acc[1] += r.E_pkg;
-        acc[2] += r.T;
-        acc[3] += r.EDP;
-        acc[4] += r.slowdown;
-        acc[5] += r.energy_saving;
-        acc[6] += r.edp_saving;
-        acc[7] += (double)r.n_hi;
-        acc[8] += (double)r.n_thr;
-        acc[9] += (double)r.transitions;
-        acc[10] += (double)r.tune_events;
-        acc[11] += (double)r.lock_ticks;
+    bool invalid = false;
+    if (j < n_traces) {
+        TraceRec r;
+        if (q < 0) {   // STATIC_MAX: never throttled, no transition or tune flag (A17, A21)
+            finish_record(r, e, (double)e.w[j], (int64_t)e.n_samples, 0, 0, 0, 0, 0.0, digest_all_hi);
+        } else {
+            const int64_t ci = chain_idx(rp, q, j);
+            finish_record(r, e, (double)e.w[j], (int64_t)rp.c_nhi[ci], (int64_t)rp.c_nthr[ci], (int64_t)rp.c_trans[ci],
+                          (int64_t)rp.c_ev[ci], (int64_t)rp.c_lock[ci], rp.c_sexc[ci], (uint64_t)rp.c_digest[ci]);
+            invalid |= rp.c_vmax[ci] > rp.bwbits;
+            zero_chain(rp, ci);   // every chain is read exactly once per run: leave it zeroed for the next
+        }
+        if (p == 0 && validate_lane >= 0) {
+            const int64_t ci = chain_idx(rp, validate_lane, j);
+            invalid |= rp.c_vmax[ci] > rp.bwbits;
+            zero_chain(rp, ci);
+        }
+        if (write_rec) e.rec[(int64_t)j * n_policies + p] = r;
+        acc[0] = r.E;
+        acc[1] = r.E_pkg;
+        acc[2] = r.T;
+        acc[3] = r.EDP;
+        acc[4] = r.slowdown;
+        acc[5] = r.energy_saving;
+        acc[6] = r.edp_saving;
+        acc[7] = (double)r.n_hi;
+        acc[8] = (double)r.n_thr;
+        acc[9] = (double)r.transitions;
+        acc[10] = (double)r.tune_events;
+        acc[11] = (double)r.lock_ticks;
     }
+    if (__any_sync(0xffffffffu, invalid) && (threadIdx.x & 31) == 0) atomicOr(e.flag_invalid, 1u);
 #pragma unroll
     for (int f = 0; f < kNTot - 1; ++f)
 #pragma unroll
@@ -458,57 +426,15 @@ __global__ void __launch_bounds__(kTotThreads) magus_totals_kernel(const ReplayP
 #pragma unroll
         for (int f = 0; f < kNTot - 1; ++f) wp[warp][f] = acc[f];
     __syncthreads();
+    double* out = part + ((int64_t)p * gridDim.y + c) * kNTot;
     if (threadIdx.x < kNTot - 1) {
         double sum = 0.0;
+#pragma unroll
         for (int w = 0; w < kTotThreads / 32; ++w) sum += wp[w][threadIdx.x];
-        part[((int64_t)p * gridDim.y + c) * (kNTot - 1) + threadIdx.x] = sum;
+        out[threadIdx.x] = sum;
+    } else if (threadIdx.x == kNTot - 1) {
+        out[kNTot - 1] = (double)max(0, min(kTotThreads, n_traces - c * kTotThreads));
     }
-    if (finish == nullptr) return;
-    // the last block to finish runs stage 2 (and the argmin when there is no cross-rank allreduce)
-    __shared__ bool last;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) last = atomicAdd(finish, 1u) == gridDim.x * gridDim.y - 1;
-    __syncthreads();
-    if (!last) return;
-    __threadfence();
-    const int n_chunks = gridDim.y, P = n_policies;
-    for (int i = threadIdx.x; i < P * (kNTot - 1); i += blockDim.x) {
-        const int pp = i / (kNTot - 1), f = i % (kNTot - 1);
-        double sum = 0.0;
-        for (int cc = 0; cc < n_chunks; ++cc) sum += part[((int64_t)pp * n_chunks + cc) * (kNTot - 1) + f];
-        totals[pp * kNTot + f] = sum;
-    }
-    for (int pp = threadIdx.x; pp < P; pp += blockDim.x) totals[pp * kNTot + kNTot - 1] = (double)n_traces;
-    __syncthreads();
-    if (argmin != nullptr && threadIdx.x == 0) {
-        __threadfence_block();
-        int best = 0;
-        double bv = totals[3];
-        for (int pp = 1; pp < P; ++pp) {
-            const double v = totals[pp * kNTot + 3];
-            if (v < bv) {
-                bv = v;
-                best = pp;
-            }
-        }
-        *argmin = best;
-    }
-    if (threadIdx.x == 0) *finish = 0u;   // re-arm for the next run
-}
-
-__global__ void magus_argmin_kernel(const double* __restrict__ totals, int n_policies, int* __restrict__ argmin) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    int best = 0;
-    double bv = totals[3];
-    for (int p = 1; p < n_policies; ++p) {
-        const double v = totals[p * kNTot + 3];
-        if (v < bv) {
-            bv = v;
-            best = p;
-        }
-    }
-    *argmin = best;
 }
 
 // Per-tick codes (DESIGN A27) for traces [first, first + n) of every policy, re-simulated from t = 0
@@ -555,29 +481,59 @@ __global__ void magus_fill_codes_kernel(uint8_t* codes, int64_t n_rows, int P, i
     if (i < n_rows) codes[i * P + pi] = value;
 }
 
-// Speculation aid: first_low[j] / first_low[n + j] = the first subsampled tick
-// (stride `sub`) with D <= B_lo / D > B_lo, via atomicMin over tick chunks.  Pure performance hint: a
-// wrong guess only costs a re-run.
-__global__ void __launch_bounds__(128) magus_first_low_kernel(const float* __restrict__ trace, int n_traces,
-                                                              int n_samples, int64_t stride, float B_lo, int sub,
-                                                              int per_chunk, int* __restrict__ first_low) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= n_traces) return;
-    const int64_t t_begin = (int64_t)blockIdx.y * per_chunk * sub;
-    bool got_low = false, got_high = false;
-    for (int i = 0; i < per_chunk; ++i) {
-        const int64_t t = t_begin + (int64_t)i * sub;
-        if (t >= n_samples) break;
-        const float D = __ldg(trace + t * stride + j);
-        if (!got_low && D <= B_lo) {
-            atomicMin(first_low + j, (int)t);
-            got_low = true;
+// Start of every run.  Block 0 zeroes the run's flag and worklist words (no memset nodes).  With
+// first_low != nullptr (segmented runs), the speculation aid: first_low[j] /
+// first_low[n + j] = the first subsampled tick (stride `sub`) with D <= B_lo / D > B_lo, or INT_MAX.
+// Block = 32 traces x 32 row slices; each thread scans its slice in increasing t, the slices are
+// reduced in shared memory.  Pure performance hint: a wrong guess only costs a re-run.
+constexpr int kPrepassTraces = 32, kPrepassSlices = 32;
+__global__ void __launch_bounds__(kPrepassTraces * kPrepassSlices)
+    magus_prepass_kernel(const float* __restrict__ trace, int n_traces, int n_samples, int64_t stride, float B_lo,
+                         int sub, int* __restrict__ first_low, uint32_t* __restrict__ zero_a, int n_zero_a,
+                         uint32_t* __restrict__ zero_b, int n_zero_b, uint8_t* __restrict__ unresolved, int n_lane) {
+    ptx::pdl_trigger();   // the replay kernel may start its pipeline fill; it waits before reading first_low
+    if (blockIdx.x == 0) {
+        for (int i = threadIdx.x; i < n_zero_a; i += blockDim.x) zero_a[i] = 0u;
+        for (int i = threadIdx.x; i < n_zero_b; i += blockDim.x) zero_b[i] = 0u;
+    }
+    if (first_low == nullptr) return;
+    const int tx = threadIdx.x % kPrepassTraces, ty = threadIdx.x / kPrepassTraces;
+    const int j = blockIdx.x * kPrepassTraces + tx;
+    if (j < n_traces)   // chains left for the serial fix-up walk (set by the last check)
+        for (int q = ty; q < n_lane; q += kPrepassSlices) unresolved[(int64_t)q * n_traces + j] = 0;
+    int lo = 0x7FFFFFFF, hi = 0x7FFFFFFF;
+    if (j < n_traces) {
+        const int n_sub = (n_samples + sub - 1) / sub;
+        constexpr int kBatch = 16;   // loads in flight per thread: one batch covers 16 * 32 * sub ticks
+        for (int i0 = ty; i0 < n_sub; i0 += kBatch * kPrepassSlices) {
+            float d[kBatch];
+#pragma unroll
+            for (int u = 0; u < kBatch; ++u) {
+                const int i = i0 + u * kPrepassSlices;
+                d[u] = i < n_sub ? __ldg(trace + (int64_t)i * sub * stride + j) : 0.0f;
+            }
+#pragma unroll
+            for (int u = 0; u < kBatch; ++u) {
+                const int i = i0 + u * kPrepassSlices;
+                if (i < n_sub) {
+                    if (lo == 0x7FFFFFFF && d[u] <= B_lo) lo = i * sub;
+                    if (hi == 0x7FFFFFFF && d[u] > B_lo) hi = i * sub;
+                }
+            }
+            if (lo != 0x7FFFFFFF && hi != 0x7FFFFFFF) break;
         }
-        if (!got_high && D > B_lo) {
-            atomicMin(first_low + n_traces + j, (int)t);
-            got_high = true;
+    }
+    __shared__ int s_lo[kPrepassSlices][kPrepassTraces], s_hi[kPrepassSlices][kPrepassTraces];
+    s_lo[ty][tx] = lo;
+    s_hi[ty][tx] = hi;
+    __syncthreads();
+    if (ty == 0 && j < n_traces) {
+        for (int y = 1; y < kPrepassSlices; ++y) {
+            lo = min(lo, s_lo[y][tx]);
+            hi = min(hi, s_hi[y][tx]);
         }
-        if (got_low && got_high) return;
+        first_low[j] = lo;
+        first_low[n_traces + j] = hi;
     }
 }
 

@@ -83,6 +83,7 @@ __device__ __forceinline__ void consume(const CUtensorMap* tmap, const ReplayPar
         for (int i = 0; i < NSTAGE && i < G.n_stages; ++i)
             ptx::tma_load_2d_u32(tile0 + i * kTileBytes, tmap, full0 + 8 * i, x, G.tau_w + i * TC, kTileBytes, cpol);
     }
+    ptx::pdl_wait();   // first_low and the scratch words come from the pre-pass (launched just before)
     const int j0 = tgroup * kTracesPerWarp + lane * kChains;
     const float B_lo = p.B_lo, B_hi = p.B_hi;
     const double Blo_d = (double)B_lo;
@@ -225,10 +226,12 @@ __device__ __forceinline__ void consume(const CUtensorMap* tmap, const ReplayPar
     }
 
 #pragma unroll
+    for (int c = 0; c < kChains; ++c)
+        if (j0 + c < p.n_traces) T::save(st[c], p, pol, 1, q, seg, j0 + c);
+#pragma unroll
     for (int c = 0; c < kChains; ++c) {
         const int j = j0 + c;
         if (j >= p.n_traces) continue;
-        T::save(st[c], p, pol, 1, q, seg, j);
         add_to_chain(p, q, j, ss[c].nhi, ss[c].nthr, ss[c].trans, ss[c].ev, ss[c].lock, ss[c].sexc,
                      ss[c].digest);
     }

@@ -120,14 +120,15 @@ struct MagusTicker {
         if constexpr (!LOG64) s.cnt = popc_log<LOG64>(s.evh & (LogT)pol.logmask) << (pol.C - 1);
         s.ring.set_all(p.st_ring + ring_idx(p, e, q, seg, 0, j), pol.k, (int64_t)p.n_traces);
     }
-    // exact equality of the two stored states (e0, s0) and (e1, s1): level, log bits, ring values
+    // exact equality of the two stored states (e0, s0) and (e1, s1): level, log bits, ring values.
+    // L2-coherent loads (__ldcg): the replay kernel compares states written by other SMs in the same launch.
     __device__ __forceinline__ static bool stored_equal(const ReplayParams& p, const DevPolicy& pol, int q, int e0,
                                                         int s0, int e1, int s1, int j) {
         const int64_t a = st_idx(p, e0, q, s0, j), b = st_idx(p, e1, q, s1, j);
-        if (p.st_f[a] != p.st_f[b] || p.st_log[a] != p.st_log[b]) return false;
+        if (__ldcg(p.st_f + a) != __ldcg(p.st_f + b) || __ldcg(p.st_log + a) != __ldcg(p.st_log + b)) return false;
         for (int r = 0; r < pol.k; ++r)
-            if (__float_as_uint(p.st_ring[ring_idx(p, e0, q, s0, r, j)]) !=
-                __float_as_uint(p.st_ring[ring_idx(p, e1, q, s1, r, j)]))
+            if (__float_as_uint(__ldcg(p.st_ring + ring_idx(p, e0, q, s0, r, j))) !=
+                __float_as_uint(__ldcg(p.st_ring + ring_idx(p, e1, q, s1, r, j))))
                 return false;
         return true;
     }
@@ -186,7 +187,7 @@ struct TdpTicker {
     }
     __device__ __forceinline__ static bool stored_equal(const ReplayParams& p, const DevPolicy&, int q, int e0, int s0,
                                                         int e1, int s1, int j) {
-        return p.st_f[st_idx(p, e0, q, s0, j)] == p.st_f[st_idx(p, e1, q, s1, j)];
+        return __ldcg(p.st_f + st_idx(p, e0, q, s0, j)) == __ldcg(p.st_f + st_idx(p, e1, q, s1, j));
     }
     __device__ __forceinline__ static bool equal(const State& x, const State& y, const DevPolicy&) { return x.f == y.f; }
 };

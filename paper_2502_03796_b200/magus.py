@@ -16,14 +16,15 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libmagus_replay.so")
+# MAGUS_LIB_PATH: experiments only (a build variant, e.g. scripts/variant_build.sh); default = the in-tree build
+LIB_PATH = os.environ.get("MAGUS_LIB_PATH") or os.path.join(_HERE, "lib", "libmagus_replay.so")
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "magus_replay.h")
 
 MAGUS_OK, ERR_INVALID_ARG, ERR_CONFIG, ERR_ALIGN, ERR_TRACE, ERR_STATE, ERR_OOM, ERR_CUDA, ERR_NCCL = range(9)
 STATUS_NAMES = ["MAGUS_OK", "MAGUS_ERR_INVALID_ARG", "MAGUS_ERR_CONFIG", "MAGUS_ERR_ALIGN", "MAGUS_ERR_TRACE",
                 "MAGUS_ERR_STATE", "MAGUS_ERR_OOM", "MAGUS_ERR_CUDA", "MAGUS_ERR_NCCL"]
 MAGUS, STATIC_MAX, STATIC_MIN, TDP_DEFAULT = 0, 1, 2, 3
-F_PER_TRACE_STATS, F_DUMP_WORDS, F_DUMP_DECISIONS, F_TIMING = 0x1, 0x2, 0x4, 0x8
+F_PER_TRACE_STATS, F_DUMP_WORDS, F_DUMP_DECISIONS, F_TIMING, F_TIMING_DETAIL = 0x1, 0x2, 0x4, 0x8, 0x10
 TOTAL_FIELDS = ["E", "E_pkg", "T", "EDP", "slowdown", "energy_saving", "edp_saving", "n_hi", "n_thr",
                 "transitions", "tune_events", "lock_ticks", "n_traces"]
 N_TOTALS = len(TOTAL_FIELDS)
@@ -266,11 +267,11 @@ class Replay:
         self.close()
 
     def geometry(self) -> dict:
-        g = (C.c_int32 * 12)()
+        g = (C.c_int32 * 16)()
         _check(lib.magus_replay_geometry(self._h, g), self._h)
         keys = ["n_segments", "segment_len", "warmup_ticks", "tile_groups_per_cta", "policy_warps_per_group",
                 "trace_blocks", "policy_blocks", "ctas", "threads_per_cta", "smem_bytes", "lane_policies",
-                "launch_groups"]
+                "launch_groups", "kernels_per_run"]
         return dict(zip(keys, list(g)))
 
     def run(self, trace, w, stream=None):

@@ -30,7 +30,8 @@ def main():
     M.gen_traces(cfg["seed"], n, ns, cfg["class_mix"], tr, w, trace_stride=stride, stream=stream)
     pols = [M.Policy(**d) for d in cfg["policies"]]
     for S in segs:
-        R = M.Replay(n, ns, pols, M.Model(), trace_stride=stride, flags=M.F_TIMING, tuning_segments=S)
+        R = M.Replay(n, ns, pols, M.Model(), trace_stride=stride, flags=M.F_TIMING | M.F_TIMING_DETAIL,
+                     tuning_segments=S)
         for _ in range(3):
             R.run(tr, w, stream)
             res = R.results()
@@ -46,10 +47,23 @@ def main():
         ts = R.timing_summary(K)
         res = R.results()
         g = R.geometry()
-        print(f"cfg{ci} S_req={S} S={res.n_segments} W={res.warmup_ticks} ms={ms:.4f} "
+        del R
+        # the same plan without per-kernel timing events (every kernel edge programmatic)
+        R2 = M.Replay(n, ns, pols, M.Model(), trace_stride=stride, tuning_segments=res.n_segments)
+        for _ in range(3):
+            R2.run(tr, w, stream)
+            R2.results()
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        for _ in range(K):
+            R2.run(tr, w, stream)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ms2 = e0.elapsed_time(e1) / K
+        del R2
+        print(f"cfg{ci} S_req={S} S={res.n_segments} W={res.warmup_ticks} ms={ms:.4f} ms_notiming={ms2:.4f} "
               f"mism={res.n_mismatched_segments} rounds={res.fixup_rounds} "
               + " ".join(f"{k}={v:.4f}" for k, v in ts.items()) + f" geo={g}", flush=True)
-        del R
         time.sleep(0.2)
 
 

@@ -228,7 +228,7 @@ def test_graph_path_matches_direct(M):
     n, ns = 300, 6000
     tr, w = gpu_gen(M, 13, n, ns, 0, 300)
     pols = PA.gpu_policies(CONFIGS[5]["policies"])
-    with M.Replay(n, ns, pols, trace_stride=300, flags=M.F_PER_TRACE_STATS | M.F_TIMING) as R:
+    with M.Replay(n, ns, pols, trace_stride=300, flags=M.F_PER_TRACE_STATS | M.F_TIMING | M.F_TIMING_DETAIL) as R:
         R.run(tr, w)                              # default stream: direct launches
         direct = R.results()
         st = torch.cuda.Stream()
@@ -243,6 +243,32 @@ def test_graph_path_matches_direct(M):
     for o in outs:
         assert o.per_trace.tobytes() == direct.per_trace.tobytes() and np.array_equal(o.totals, direct.totals)
     assert t["replay_ms"] > 0 and t["run_ms"] >= t["replay_ms"]
+
+
+def test_repeated_runs_reuse_scratch(M):
+    """One handle, alternating inputs, graph and direct launches: every run equals the oracle.  The run
+    scratch (segment-boundary counters, worklists, per-chain totals) is re-armed inside the kernels, so a
+    stale word would corrupt the following run; the inputs are chosen so that speculative segment entries
+    do mismatch (adversarial traces, lock-sticky sweep policies)."""
+    n, ns, S = 200, 9_000, 9
+    pols = CONFIGS[5]["policies"] + sweep64()[40:44]
+    data = [gpu_gen(M, 21, n, ns, 2, 200), gpu_gen(M, 22, n, ns, 1, 200)]
+    refs = []
+    for tr, w in data:
+        rec, _ = oracle_run(tr.cpu().numpy(), w.cpu().numpy(), pols, n)
+        refs.append(rec)
+    st = torch.cuda.Stream()
+    with M.Replay(n, ns, PA.gpu_policies(pols), trace_stride=200, flags=M.F_PER_TRACE_STATS,
+                  tuning_segments=S) as R:
+        mism = 0
+        for it in range(6):
+            tr, w = data[it % 2]
+            R.run(tr, w, st if it >= 2 else None)
+            res = R.results()
+            mism += res.n_mismatched_segments
+            PA.compare_records(res.per_trace, refs[it % 2], f"run {it}")
+            np.testing.assert_allclose(res.totals, PA.oracle_totals(refs[it % 2]), rtol=1e-9, atol=1e-9)
+    assert mism > 0, "inputs should exercise the fix-up"
 
 
 def test_host_buffer_path(M):
