@@ -338,6 +338,7 @@ struct magus_replay {
     TraceRec* d_rec = nullptr;
     double* d_totals = nullptr;
     uint8_t* d_out = nullptr;         // [P][chunks][13] totals partials (fp64), then the 4 run flag words: one D2H copy
+    double* d_fin = nullptr;          // world > 1: [P][13] per-policy totals, allreduced across ranks
     int n_chunks = 1;                 // trace chunks of the totals kernel
     int32_t* d_first_low = nullptr;   // [n_traces] speculation aid
     uint8_t* d_chain = nullptr;       // per-chain totals (ReplayParams::c_*)
@@ -696,6 +697,9 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
     ALLOC(h->d_out, n_part * sizeof(double) + 4 * sizeof(unsigned int));
     h->d_totals = (double*)h->d_out;
     h->d_flag = (unsigned int*)(h->d_out + n_part * sizeof(double));
+    if (d.world > 1) {
+        ALLOC(h->d_fin, (size_t)d.n_policies * MAGUS_N_TOTALS);
+    }
     ALLOC(h->d_first_low, (size_t)2 * std::max(1, d.n_traces));
     ALLOC(h->d_errkey, 1);
     if (!h->smax.empty()) {
@@ -961,9 +965,10 @@ static magus_status enqueue_run(magus_replay_t* h, const float* d_trace, const f
                        (d.flags & MAGUS_F_PER_TRACE_STATS) ? 1 : 0, h->d_totals));
     }
     if (d.world > 1) {
-        ncclResult_t r = nccl().AllReduce(h->d_totals, h->d_totals,
-                                          (size_t)d.n_policies * h->n_chunks * MAGUS_N_TOTALS, ncclFloat64,
-                                          ncclSum, h->comm, s);
+        CU(h, launch_k(magus_chunk_sum_kernel, dim3(d.n_policies), dim3(32), 0, s, h->pdl && !detail,
+                       (const double*)h->d_totals, h->n_chunks, h->d_fin));
+        ncclResult_t r = nccl().AllReduce(h->d_fin, h->d_fin, (size_t)d.n_policies * MAGUS_N_TOTALS, ncclFloat64, ncclSum,
+                                          h->comm, s);
         if (r != ncclSuccess) return fail(h, MAGUS_ERR_NCCL, std::string("ncclAllReduce: ") + nccl().GetErrorString(r));
     }
     if (detail) CU(h, rec(4));
@@ -1073,10 +1078,14 @@ extern "C" magus_status magus_replay_results(magus_replay_t* h, magus_results* o
     std::vector<double> part(n_part + 2);
     CU(h, cudaMemcpy(part.data(), h->d_out, n_part * sizeof(double) + 4 * sizeof(unsigned int), cudaMemcpyDeviceToHost));
     std::vector<double> tot((size_t)P * MAGUS_N_TOTALS, 0.0);
-    for (int pp = 0; pp < P; ++pp)
-        for (int c = 0; c < h->n_chunks; ++c)
-            for (int f = 0; f < MAGUS_N_TOTALS; ++f)
-                tot[(size_t)pp * MAGUS_N_TOTALS + f] += part[((size_t)pp * h->n_chunks + c) * MAGUS_N_TOTALS + f];
+    if (d.world > 1) {   // chunk sums on the device (same order), then the cross-rank allreduce
+        CU(h, cudaMemcpy(tot.data(), h->d_fin, tot.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    } else {
+        for (int pp = 0; pp < P; ++pp)
+            for (int c = 0; c < h->n_chunks; ++c)
+                for (int f = 0; f < MAGUS_N_TOTALS; ++f)
+                    tot[(size_t)pp * MAGUS_N_TOTALS + f] += part[((size_t)pp * h->n_chunks + c) * MAGUS_N_TOTALS + f];
+    }
     if (out->policy_totals) std::memcpy(out->policy_totals, tot.data(), tot.size() * sizeof(double));
     // argmin over policies of the total EDP, ties -> lowest index (A23)
     int am = 0;
@@ -1203,7 +1212,7 @@ extern "C" magus_status magus_replay_geometry(const magus_replay_t* h, int32_t o
         for (const LaunchGroup& g : h->groups) nr += rerun_kernel_for(g.key) ? 1 : 0;
         nk += 1 + nr * h->fix_rounds + (h->fix_rounds - 1) + 2;  // check, re-run rounds, candidate checks, serial
     }
-    nk += 1;                                                      // totals
+    nk += 1 + (d.world > 1 ? 1 : 0);                              // totals (+ chunk sums before the allreduce)
     const int32_t v[16] = {p.n_seg, p.seg_len, p.warmup, g0.ng, g0.npw, g0.n_tblocks, g0.n_pblocks, ctas,
                            g0.threads, (int32_t)g0.smem, p.n_lane, (int32_t)h->groups.size(), nk, 0, 0, 0};
     std::memcpy(out, v, sizeof(v));

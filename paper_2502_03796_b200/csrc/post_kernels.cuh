@@ -437,6 +437,17 @@ __global__ void __launch_bounds__(kTotThreads) magus_totals_kernel(const ReplayP
     }
 }
 
+// world > 1: the chunk partials of policy p added in chunk order -> fin[p][0..12] (the same size on every
+// rank, whatever its trace count, so the allreduce that follows is well formed).
+__global__ void magus_chunk_sum_kernel(const double* __restrict__ part, int n_chunks, double* __restrict__ fin) {
+    ptx::pdl_wait();
+    const int p = blockIdx.x, f = threadIdx.x;
+    if (f >= kNTot) return;
+    double sum = 0.0;
+    for (int c = 0; c < n_chunks; ++c) sum += part[((int64_t)p * n_chunks + c) * kNTot + f];
+    fin[p * kNTot + f] = sum;
+}
+
 // Per-tick codes (DESIGN A27) for traces [first, first + n) of every policy, re-simulated from t = 0
 // with the same tick functions as the replay kernel.  codes: [n_samples][n][P].
 template <class T>

@@ -39,7 +39,7 @@ for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1]) / len(kv[1])):
 live = bench["kernel_ms"]
 lines += ["", f"live CUDA-event split of the same bench (ms per step): {json.dumps(live)}",
           f"replay share of the step: ncu {100 * max(v for k, v in step.items() if 'replay_kernel' in k) / tot:.1f}%"
-          f" vs live {100 * live['replay_ms'] / live['run_ms']:.1f}%"]
+          f" vs live {100 * live['replay_ms'] / bench['ms_per_step']:.1f}%"]
 open(os.path.join(prof, f"{rnd}_launches.txt"), "w").write("\n".join(lines) + "\n")
 
 # full capture
@@ -65,8 +65,9 @@ st = sorted(((k, float(d[k][0].replace(",", ""))) for k in d
              if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio")
              and d[k][0].replace(",", "").replace(".", "").isdigit()), key=lambda t: -t[1])
 out += ["", "warp stalls per issued instruction:"] + [f"   {k[34:-33]:40s} {x:7.3f}" for k, x in st[:10] if x > 0.02]
-rb = float(d["dram__bytes_read.sum"][0].replace(",", "")) * (1e9 if d["dram__bytes_read.sum"][1] == "Gbyte" else 1e6)
-wb = float(d["dram__bytes_write.sum"][0].replace(",", "")) * (1e9 if d["dram__bytes_write.sum"][1] == "Gbyte" else 1e6)
+UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+rb = float(d["dram__bytes_read.sum"][0].replace(",", "")) * UNIT[d["dram__bytes_read.sum"][1]]
+wb = float(d["dram__bytes_write.sum"][0].replace(",", "")) * UNIT[d["dram__bytes_write.sum"][1]]
 alg = bench["roofline"]["bytes_per_launch"]
 out += ["", f"DRAM traffic per launch {rb + wb:.4e} B vs algorithmic {alg:.4e} B (4 B per trace-sample): "
             f"x{(rb + wb) / alg:.3f}  (warm-up overlap of speculative segments + state/statistics writes)",
