@@ -270,7 +270,8 @@ def run_ours(args, cfg):
         e2e_ms = float(e2e_t[0])
         e2e = {"value": total_samples / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms, "steps": k_e2e,
                "h2d_bytes_per_step": int(th.numel() * 4 + wh.numel() * 4),
-               "d2h_bytes_per_step": int(len(pols) * M.N_TOTALS * 8 + 4 * 4),
+               # magus_replay_results: one copy of the per-(policy, 256-trace chunk) partials + 4 flag words
+               "d2h_bytes_per_step": int(len(pols) * ((n + 255) // 256) * M.N_TOTALS * 8 + 4 * 4),
                "path": "magus_replay_run_host + magus_replay_results (pinned host buffers)"}
         del th, wh
 
