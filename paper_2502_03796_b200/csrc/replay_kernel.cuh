@@ -210,16 +210,27 @@ __device__ __forceinline__ void consume(const CUtensorMap* tmap, const ReplayPar
         }
         if (counting) {
             const int n = min(32, G.seg_end - bt0);
-            const int64_t b = bt0 >> 5;
-            uint32_t* wbase = p.words ? p.words + ((int64_t)q * p.n_traces * p.n_blocks + b) * 2 : nullptr;
+            if (n == 32 && p.words == nullptr) {   // the common case: a whole block, no word dump
 #pragma unroll
-            for (int c = 0; c < kChains; ++c) {
-                uint32_t ew;
-                if constexpr (T::kWarmupRules) ew = (uint32_t)st[c].evh;
-                else ew = 0u;
-                uint32_t* wout = (wbase && j0 + c < p.n_traces) ? wbase + (int64_t)(j0 + c) * p.n_blocks * 2 : nullptr;
-                if (n == 32) fold_full_block(ss[c], wcmd[c], ew, fstart[c], bkey, wout);
-                else fold_block(ss[c], wcmd[c], ew, fstart[c], n, b, wout);
+                for (int c = 0; c < kChains; ++c) {
+                    uint32_t ew;
+                    if constexpr (T::kWarmupRules) ew = (uint32_t)st[c].evh;
+                    else ew = 0u;
+                    fold_full_block(ss[c], wcmd[c], ew, fstart[c], bkey, nullptr);
+                }
+            } else {
+                const int64_t b = bt0 >> 5;
+                uint32_t* wbase = p.words ? p.words + ((int64_t)q * p.n_traces * p.n_blocks + b) * 2 : nullptr;
+#pragma unroll
+                for (int c = 0; c < kChains; ++c) {
+                    uint32_t ew;
+                    if constexpr (T::kWarmupRules) ew = (uint32_t)st[c].evh;
+                    else ew = 0u;
+                    uint32_t* wout =
+                        (wbase && j0 + c < p.n_traces) ? wbase + (int64_t)(j0 + c) * p.n_blocks * 2 : nullptr;
+                    if (n == 32) fold_full_block(ss[c], wcmd[c], ew, fstart[c], bkey, wout);
+                    else fold_block(ss[c], wcmd[c], ew, fstart[c], n, b, wout);
+                }
             }
         }
         bkey += kPhi;
