@@ -132,7 +132,8 @@ uint64_t oracle_digest(const uint8_t* cmd_hi, const uint8_t* event, int64_t n) {
             }
         }
         uint64_t word = ((uint64_t)w_cmd << 32) | (uint64_t)w_ev;
-        digest += mix64(word ^ ((uint64_t)b * 0x9E3779B97F4A7C15ULL));
+        uint64_t key = mix64((uint64_t)b * 0x9E3779B97F4A7C15ULL) | 1u;   /* odd per-block key */
+        digest += word * key;                                               /* mod 2^64 */
     }
     return digest;
 }

@@ -51,7 +51,7 @@ struct ReplayParams {
     int32_t n_blocks;      // ceil(n_samples / 32)
     float B_lo, B_hi;
     uint32_t bwbits;       // bit pattern of the largest fp32 <= bw_max
-    int32_t _pad0;
+    uint32_t bnd_ebits;    // e << 20 with B_lo * 2^e >= B_hi (solo tick's f_max bound, replay_solo.cuh)
     int64_t trace_stride;
     const DevPolicy* pol;  // [n_lane]
     const int32_t* first_low;   // [2][n_traces] first subsampled tick with D <= B_lo / D > B_lo (INT32_MAX: none)
@@ -104,6 +104,8 @@ __host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {   // splitmix64
     return z ^ (z >> 31);
 }
 static constexpr uint64_t kPhi = 0x9E3779B97F4A7C15ULL;
+// digest key of 32-tick block b: odd, so word -> word * key is a bijection mod 2^64
+__host__ __device__ __forceinline__ uint64_t digest_key(uint64_t b) { return mix64(b * kPhi) | 1ull; }
 
 // Chain kinds with C <= kMaxC32 keep the tune log in 32 bits and the scaled window count
 // (ones << (C-1), which must not overflow: C * 2^(C-1) < 2^32); larger logs use the 64-bit kinds.
@@ -291,14 +293,14 @@ __device__ __forceinline__ void add_to_chain(const ReplayParams& p, int q, int j
     if (digest) atomicAdd(p.c_digest + ci, (unsigned long long)digest);
 }
 
-// Full-block fold (n == 32) with the block's hash key b*phi supplied by the caller (kept incrementally).
+// Full-block fold (n == 32) with the block's digest key (digest_key(b)) supplied by the caller.
 __device__ __forceinline__ void fold_full_block(SegStats& st, uint32_t wcmd, uint32_t ew, uint32_t fstart,
                                                 uint64_t bkey, uint32_t* words_out) {
     const uint32_t lw = (wcmd >> 1) | (fstart << 31);   // level in effect per tick
     st.trans += __popc(wcmd ^ lw);
     st.nhi += __popc(lw);
     st.ev += __popc(ew);
-    st.digest += mix64((((uint64_t)wcmd << 32) | (uint64_t)ew) ^ bkey);
+    st.digest += ((((uint64_t)wcmd) << 32) | (uint64_t)ew) * bkey;
     if (words_out) {
         words_out[0] = wcmd;
         words_out[1] = ew;
@@ -318,7 +320,7 @@ __device__ __forceinline__ void fold_block(SegStats& st, uint32_t wcmd, uint32_t
     st.ev += __popc(evw);
     const int sh = 32 - n;
     const uint32_t wc = cw << sh, we = evw << sh;   // tick bt0 + i at bit 31 - i; partial block zero-padded
-    st.digest += mix64((((uint64_t)wc << 32) | (uint64_t)we) ^ ((uint64_t)block_index * kPhi));
+    st.digest += ((((uint64_t)wc) << 32) | (uint64_t)we) * digest_key((uint64_t)block_index);
     if (words_out) {
         words_out[0] = wc;
         words_out[1] = we;

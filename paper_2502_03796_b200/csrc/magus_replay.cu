@@ -16,6 +16,7 @@
 #include "../../include/magus_replay.h"
 #include "post_kernels.cuh"
 #include "replay_kernel.cuh"
+#include "replay_solo.cuh"
 
 using namespace magus;
 
@@ -92,11 +93,31 @@ ReplayKernel replay_kernel_for(int key) {
     }
 }
 
+int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return (v && *v) ? std::atoi(v) : dflt;
+}
+
+// one-warp-CTA replay kernel (replay_solo.cuh) of a chain kind, or nullptr if it has none
+ReplayKernel solo_kernel_for(int key) {
+    const bool bal = env_int("MAGUS_SOLO_BAL", 1) != 0;
+    switch (key) {
+        case 1: return bal ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<1, false>, kTC, kNStage, true>
+                           : (ReplayKernel)magus_replay_solo_kernel<MagusTicker<1, false>, kTC, kNStage, false>;
+        case 2: return bal ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<2, false>, kTC, kNStage, true>
+                           : (ReplayKernel)magus_replay_solo_kernel<MagusTicker<2, false>, kTC, kNStage, false>;
+        case 3: return bal ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<3, false>, kTC, kNStage, true>
+                           : (ReplayKernel)magus_replay_solo_kernel<MagusTicker<3, false>, kTC, kNStage, false>;
+        default: return nullptr;
+    }
+}
+
 // one replay launch: the lane policies [q_base, q_base + nq) share a chain kind
 struct LaunchGroup {
     ReplayKernel kernel;
     int key, q_base, nq, ng, npw, n_tblocks, n_pblocks, n_ctas, threads;
     size_t smem;
+    bool solo;   // one-warp CTAs (npw == 1 and the kind has a solo kernel)
 };
 
 // Kernel launch with programmatic stream serialization (PDL) when `pdl`: the kernel may be scheduled
@@ -302,11 +323,6 @@ std::string validate_policy(const magus_policy& p, int i) {
     return "";
 }
 
-int env_int(const char* name, int dflt) {
-    const char* v = std::getenv(name);
-    return (v && *v) ? std::atoi(v) : dflt;
-}
-
 }  // namespace
 
 // ============================================================================================ handle
@@ -510,6 +526,8 @@ static void choose_geometry(magus_replay_t* h, int n_sm, int forced_segments) {
         const int L0 = (((N + S - 1) / S) + 31) / 32 * 32;
         if (S > 1 && L0 < 4 * W) S = std::max(1, N / (4 * W));   // segments must dwarf their warm-up
     }
+    // the solo kernel's per-segment counters are exact fp32 integers: segments of at most 2^24 ticks
+    S = std::max(S, (N + (1 << 24) - 1) >> 24);
     int L = (((N + S - 1) / S) + 31) / 32 * 32;
     if (L < 32) L = 32;
     S = (N + L - 1) / L;
@@ -540,7 +558,23 @@ static void choose_geometry(magus_replay_t* h, int n_sm, int forced_segments) {
         wide->threads = wide->ng * wide->npw * 32;
         wide->smem = Smem::bytes(wide->ng);
     }
-    for (LaunchGroup& g : h->groups) g.n_ctas = p.n_seg * g.n_tblocks * g.n_pblocks;
+    for (LaunchGroup& g : h->groups) {
+        g.n_ctas = p.n_seg * g.n_tblocks * g.n_pblocks;
+        // one policy warp per tile group: one-warp CTAs with CTA-uniform pipeline state (replay_solo.cuh)
+        ReplayKernel sk = solo_kernel_for(g.key);
+        // its f_max bound is B_lo * 2^e >= B_hi built on the high word of (double)B_lo (replay_solo.cuh)
+        const bool bound_ok = h->B_lo > 0.f && std::ldexp((double)h->B_lo, 64) >= (double)h->B_hi;
+        g.solo = sk && bound_ok && g.npw == 1 && kTC == 8 && env_int("MAGUS_SOLO", 1) != 0;
+        if (g.solo) {
+            g.kernel = sk;
+            g.ng = 1;
+            g.n_tblocks = p.n_groups;
+            g.n_pblocks = g.nq;
+            g.threads = 32;
+            g.smem = SoloSmem<kTC, kNStage>::kBytes + env_int("MAGUS_SOLO_SMEM_PAD", 0);   // pad: occupancy probes
+            g.n_ctas = p.n_seg * p.n_groups * g.nq;
+        }
+    }
 }
 
 extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus_replay_t** out) {
@@ -646,7 +680,7 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
         for (int64_t b = 0; b < nb; ++b) {
             const int n = (int)std::min<int64_t>(32, d.n_samples - b * 32);
             const uint32_t wc = n == 32 ? 0xFFFFFFFFu : (((1u << n) - 1u) << (32 - n));
-            dg += mix64(((uint64_t)wc << 32) ^ ((uint64_t)b * kPhi));
+            dg += ((uint64_t)wc << 32) * digest_key((uint64_t)b);
         }
         h->digest_all_hi = dg;
     }
@@ -660,6 +694,11 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
     p.B_lo = h->B_lo;
     p.B_hi = h->B_hi;
     p.bwbits = h->bwbits;
+    {   // smallest e >= 0 with B_lo * 2^e >= B_hi, as the increment of the high word of (double)B_lo
+        int e = 0;
+        while (std::ldexp((double)h->B_lo, e) < (double)p.B_hi && e < 1000) ++e;
+        p.bnd_ebits = (uint32_t)e << 20;
+    }
 
     const int Q = p.n_lane, S = p.n_seg;
     const size_t nst = (size_t)3 * Q * S * std::max(1, d.n_traces);   // entry, exit, staged exit

@@ -104,7 +104,6 @@ __device__ __forceinline__ void consume(const CUtensorMap* tmap, const ReplayPar
     int i = 0;           // stage index
     int slot = 0;        // i % NSTAGE
     uint32_t phase = 0;  // (i / NSTAGE) & 1
-    uint64_t bkey = (uint64_t)(G.tau_w >> 5) * kPhi;   // digest key of the current block, b * phi
     // 32-tick digest blocks; segment starts and warm-up starts are block aligned
     for (int bt0 = G.tau_w; bt0 < G.seg_end; bt0 += 32) {
         if (bt0 == G.seg_start) {   // the segment's own ticks start: record the entry, reset the statistics
@@ -209,6 +208,7 @@ __device__ __forceinline__ void consume(const CUtensorMap* tmap, const ReplayPar
             }
         }
         if (counting) {
+            const uint64_t bkey = digest_key((uint64_t)(bt0 >> 5));
             const int n = min(32, G.seg_end - bt0);
             if (n == 32 && p.words == nullptr) {   // the common case: a whole block, no word dump
 #pragma unroll
@@ -233,7 +233,6 @@ __device__ __forceinline__ void consume(const CUtensorMap* tmap, const ReplayPar
                 }
             }
         }
-        bkey += kPhi;
     }
 
 #pragma unroll

@@ -1,0 +1,287 @@
+// replay_solo.cuh -- the replay kernel for launch groups with one policy warp per tile group (npw == 1:
+// configs 2, 4, 5) and a MAGUS chain kind with a whole-stage PTX block (k <= 3, 32-bit log).
+//
+// Same work unit, pipeline and segmentation as magus_replay_kernel (replay_kernel.cuh), but a CTA is ONE
+// warp that consumes its own 3-deep ring of [8 ticks x 128 traces] TMA tiles.  Every pipeline address and
+// counter (tile / barrier slot, phase, stage index, TMA coordinates) is then CTA-uniform, so ptxas keeps
+// them in uniform registers: a stage costs its try-wait, one elected expect-tx arrive and one UTMALDG
+// instead of the per-lane slot arithmetic and the elect loop of the multi-warp kernel.  Steady-state
+// blocks run four calls of the generated whole-stage block (MAGUS_STAGE8_K<K>: the level carried as a
+// predicate across the 8 ticks, the ring of A values in virtual registers).  DESIGN.md section 7.
+#pragma once
+#include <cuda.h>
+#include "device_common.cuh"
+#include "ptx.cuh"
+#include "replay_kernel.cuh"
+#include "tickers.cuh"
+
+namespace magus {
+
+constexpr int kSoloCtasPerSm = 16;   // 16 one-warp CTAs per SM: 128 registers and ~12.3 KB smem each
+
+template <int TC, int NSTAGE>
+struct SoloSmem {
+    static constexpr int kTileBytes = TC * kTracesPerWarp * 4;
+    static constexpr size_t kBytes = (size_t)NSTAGE * kTileBytes + NSTAGE * sizeof(uint64_t);
+};
+
+__device__ __forceinline__ uint32_t elect_one() {
+    uint32_t p;
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\tselp.u32 %0, 1, 0, e;\n\t}"
+        : "=r"(p));
+    return p;
+}
+
+// blocking parity wait on an mbarrier (try_wait loop inside one PTX block)
+__device__ __forceinline__ void mbar_wait_loop(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "LAB_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra LAB_WAIT;\n\t}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+
+// the elected lane arms `bar` for one tile and issues its 2-D TMA box {128 traces, TC ticks} at (x, t0)
+template <int TC>
+__device__ __forceinline__ void solo_issue(uint32_t tile, const CUtensorMap* tmap, uint32_t bar, int x, int t0,
+                                           uint64_t cpol) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t"
+        "@e cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%2], [%3, {%4, %5}], [%0], %6;\n\t}" ::"r"(bar),
+        "n"(TC * kTracesPerWarp * 4), "r"(tile), "l"(reinterpret_cast<uint64_t>(tmap)), "r"(x), "r"(t0),
+        "l"(cpol)
+        : "memory");
+}
+
+
+// run constants of the pipe-balanced stage block (MAGUS_SSTAGE_K<K>, tick4_asm.cuh)
+struct SoloConst {
+    double Blo_d;   // B_lo as fp64
+};
+
+// One whole steady-state stage (8 ticks x 4 chains) of MAGUS chains with a register ring of K <= 3 values.
+template <int K>
+__device__ __forceinline__ void solo_stage(MagusState<K, false>* s, float* lock, float* nthr,
+                                           uint32_t* wcmd, SegStats* ss, uint32_t& vmax, uint32_t tile,
+                                           const SoloConst& sc, const DevPolicy& pol) {
+    uint32_t e0 = s[0].evh, e1 = s[1].evh, e2 = s[2].evh, e3 = s[3].evh;
+    const uint32_t bitc = 1u << (pol.C - 1), mone = 0xFFFFFFFFu * pol.one;
+#define SOLO_TAIL                                                                                              \
+    e0, e1, e2, e3, s[0].cnt, s[1].cnt, s[2].cnt, s[3].cnt, ss[0].sexc, ss[1].sexc, ss[2].sexc, ss[3].sexc, lock[0],    \
+        lock[1], lock[2], lock[3], nthr[0], nthr[1], nthr[2], nthr[3], wcmd[0], wcmd[1], wcmd[2], wcmd[3], vmax, \
+        tile, sc.Blo_d, pol.dinc, pol.ddec, bitc, pol.smin_sc, pol.one, mone
+#define SOLO_F s[0].f, s[1].f, s[2].f, s[3].f
+    if constexpr (K == 1) {
+        MAGUS_SSTAGE_K1(SOLO_F, s[0].ring.v[0], s[1].ring.v[0], s[2].ring.v[0], s[3].ring.v[0], SOLO_TAIL);
+    } else if constexpr (K == 2) {
+        MAGUS_SSTAGE_K2(SOLO_F, s[0].ring.v[0], s[0].ring.v[1], s[1].ring.v[0], s[1].ring.v[1], s[2].ring.v[0],
+                        s[2].ring.v[1], s[3].ring.v[0], s[3].ring.v[1], SOLO_TAIL);
+    } else {
+        MAGUS_SSTAGE_K3(SOLO_F, s[0].ring.v[0], s[0].ring.v[1], s[0].ring.v[2], s[1].ring.v[0], s[1].ring.v[1],
+                        s[1].ring.v[2], s[2].ring.v[0], s[2].ring.v[1], s[2].ring.v[2], s[3].ring.v[0],
+                        s[3].ring.v[1], s[3].ring.v[2], SOLO_TAIL);
+    }
+#undef SOLO_TAIL
+#undef SOLO_F
+    s[0].evh = e0;
+    s[1].evh = e1;
+    s[2].evh = e2;
+    s[3].evh = e3;
+}
+
+// BAL: the pipe-balanced stage block (MAGUS_SSTAGE_K<K>); else the integer one (MAGUS_STAGE8_K<K>)
+template <class T, int TC, int NSTAGE, bool BAL>
+__global__ void __launch_bounds__(32, kSoloCtasPerSm)
+    magus_replay_solo_kernel(const __grid_constant__ CUtensorMap tmap, const ReplayParams p) {
+    static_assert(T::kHasStage8 && TC == 8, "solo kernel: whole-stage PTX block of 8 ticks");
+    using State = typename T::State;
+    using SM = SoloSmem<TC, NSTAGE>;
+    constexpr uint32_t kTileBytes = SM::kTileBytes;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int lane = threadIdx.x;
+
+    // blockIdx -> (lane policy, tile group, segment); policies fastest so the CTAs of one (group,
+    // segment) read the same tiles close together in time (L2 reuse when nq > 1)
+    int b = blockIdx.x;
+    const int qi = b % p.nq;
+    b /= p.nq;
+    const int tgroup = b % p.n_groups;
+    const int seg = b / p.n_groups;
+    const int q = p.q_base + qi;
+
+    const uint32_t tile0 = ptx::smem_u32(smem);
+    const uint32_t bar0 = tile0 + NSTAGE * kTileBytes;
+    if (lane == 0) {
+        ptx::prefetch_tmap(&tmap);
+        for (int i = 0; i < NSTAGE; ++i)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8 * i) : "memory");
+        ptx::fence_mbar_init();
+    }
+    __syncwarp();
+
+    const SegGeom G = seg_geom<TC>(p, seg);
+    const int x = tgroup * kTracesPerWarp;
+    const uint64_t cpol = ptx::policy_evict_first();
+    for (int i = 0; i < NSTAGE && i < G.n_stages; ++i)
+        solo_issue<TC>(tile0 + i * kTileBytes, &tmap, bar0 + 8 * i, x, G.tau_w + i * TC, cpol);
+    ptx::pdl_wait();   // first_low and the scratch words come from the pre-pass (launched just before)
+
+    const DevPolicy pol = p.pol[q];
+    const int j0 = x + lane * kChains;
+    const float B_lo = p.B_lo, B_hi = p.B_hi;
+    SoloConst sc;
+    sc.Blo_d = (double)B_lo;
+    const double Blo_d = sc.Blo_d;
+    const int k = pol.k, C = pol.C;
+    const int warm_ticks = k + C - 1;   // ticks before Alg. 1 / 2 are fully defined (A7, A8)
+    const uint32_t lane_off = (uint32_t)lane * 16u;
+
+    State st[kChains];
+    SegStats ss[kChains];
+    uint32_t wcmd[kChains], fstart[kChains];
+    float lockf[kChains], nthrf[kChains];   // counts as exact fp32 integers (segment length <= 2^24)
+    uint32_t vmax = 0;
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) {
+        T::init(st[c], pol, seg == 0);
+        ss[c].zero();
+        wcmd[c] = 0;
+        lockf[c] = nthrf[c] = 0.f;
+    }
+
+    int i = 0;           // stage index (CTA-uniform)
+    int slot = 0;        // i % NSTAGE
+    uint32_t phase = 0;  // (i / NSTAGE) & 1
+    for (int bt0 = G.tau_w; bt0 < G.seg_end; bt0 += 32) {
+        if (bt0 == G.seg_start) {   // the segment's own ticks start: record the entry, reset the statistics
+#pragma unroll
+            for (int c = 0; c < kChains; ++c) {
+                if (j0 + c < p.n_traces) T::save(st[c], p, pol, 0, q, seg, j0 + c);
+                ss[c].zero();
+                lockf[c] = nthrf[c] = 0.f;
+            }
+        }
+        if (bt0 == G.tau_w && seg > 0) {
+            // speculative level at the warm-up start: f_max iff the trace is above B_lo
+            // now and was at or below B_lo before (a high stretch entered through a rising edge that Alg. 1
+            // sees even at f_min; a trace never below B_lo is never seen to rise, A14); lock-sticky policies
+            // (k >= s_min) keep f_max after any low/high transition (K9)
+            mbar_wait_loop(bar0 + 8 * slot, phase);
+            float4 d0;
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(d0.x), "=f"(d0.y), "=f"(d0.z), "=f"(d0.w)
+                         : "r"(tile0 + slot * kTileBytes + lane_off)
+                         : "memory");
+            const float dd[4] = {d0.x, d0.y, d0.z, d0.w};
+#pragma unroll
+            for (int c = 0; c < kChains; ++c) {
+                const int j = j0 + c;
+                const int fl = j < p.n_traces ? __ldg(p.first_low + j) : 0x7FFFFFFF;
+                const int fh = j < p.n_traces ? __ldg(p.first_low + p.n_traces + j) : 0x7FFFFFFF;
+                const bool hi = (dd[c] > B_lo && fl < G.tau_w) || (pol.sticky && fl < G.tau_w && fh < G.tau_w);
+                T::set_level(st[c], hi ? 1u : 0u);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < kChains; ++c) fstart[c] = T::level(st[c]);
+        const bool counting = bt0 >= G.seg_start;
+        if (bt0 + 32 <= G.seg_end && bt0 - G.tau_w >= warm_ticks) {
+            // steady state: four whole-stage PTX blocks
+#pragma unroll 1
+            for (int sub = 0; sub < 32 / TC; ++sub) {
+                const uint32_t tile = tile0 + slot * kTileBytes;
+                mbar_wait_loop(bar0 + 8 * slot, phase);
+                if constexpr (BAL) solo_stage(st, lockf, nthrf, wcmd, ss, vmax, tile + lane_off, sc, pol);
+                else T::stage8(st, tile + lane_off, pol, B_lo, Blo_d, wcmd, ss, vmax);
+                __syncwarp();   // every lane's tile reads are complete before the slot is refilled
+                if (i + NSTAGE < G.n_stages)
+                    solo_issue<TC>(tile, &tmap, bar0 + 8 * slot, x, G.tau_w + (i + NSTAGE) * TC, cpol);
+                ++i;
+                if (++slot == NSTAGE) {
+                    slot = 0;
+                    phase ^= 1u;
+                }
+            }
+        } else {
+            // warm-up block (Alg. 1 / Alg. 2 gated per tick) or the ragged last block of a trace
+#pragma unroll 1
+            for (int sub = 0; sub < 32 / TC && i < G.n_stages; ++sub) {
+                const int t0 = bt0 + sub * TC;
+                const uint32_t tile = tile0 + slot * kTileBytes;
+                mbar_wait_loop(bar0 + 8 * slot, phase);
+                const float4* rows = reinterpret_cast<const float4*>(smem + slot * kTileBytes) + lane;
+                if (t0 + TC <= G.seg_end) {
+#pragma unroll
+                    for (int tt = 0; tt < TC; ++tt) {
+                        const int r = t0 + tt - G.tau_w;
+                        const float4 d4 = rows[tt * (kTracesPerWarp / 4)];
+                        const float d[4] = {d4.x, d4.y, d4.z, d4.w};
+                        T::warm4(st, d, pol, B_lo, Blo_d, wcmd, ss, vmax, r >= k ? 1u : 0u, r >= k + C - 1 ? 1u : 0u);
+                    }
+                } else {
+                    for (int tt = 0; tt < TC; ++tt) {
+                        const int t = t0 + tt;
+                        if (t >= G.seg_end) break;
+                        const float4 d4 = rows[tt * (kTracesPerWarp / 4)];
+                        const float d[4] = {d4.x, d4.y, d4.z, d4.w};
+                        const bool ready = (t - G.tau_w) >= k;
+                        const bool lfull = (t - G.tau_w) >= k + C - 1;
+#pragma unroll
+                        for (int c = 0; c < kChains; ++c) {
+                            const TickOut o = T::template tick<true>(st[c], d[c], pol, B_lo, B_hi, ready, lfull);
+                            wcmd[c] = (wcmd[c] << 1) | o.cmd;
+                            acc_tick(ss[c], vmax, o, d[c], B_lo);
+                        }
+                    }
+                }
+                __syncwarp();
+                if (i + NSTAGE < G.n_stages)
+                    solo_issue<TC>(tile, &tmap, bar0 + 8 * slot, x, G.tau_w + (i + NSTAGE) * TC, cpol);
+                ++i;
+                if (++slot == NSTAGE) {
+                    slot = 0;
+                    phase ^= 1u;
+                }
+            }
+        }
+        if (counting) {
+            const uint64_t bkey = digest_key((uint64_t)(bt0 >> 5));
+            const int n = min(32, G.seg_end - bt0);
+            if (n == 32 && p.words == nullptr) {   // the common case: a whole block, no word dump
+#pragma unroll
+                for (int c = 0; c < kChains; ++c)
+                    fold_full_block(ss[c], wcmd[c], (uint32_t)st[c].evh, fstart[c], bkey, nullptr);
+            } else {
+                const int64_t bi = bt0 >> 5;
+                uint32_t* wbase = p.words ? p.words + ((int64_t)q * p.n_traces * p.n_blocks + bi) * 2 : nullptr;
+#pragma unroll
+                for (int c = 0; c < kChains; ++c) {
+                    uint32_t* wout =
+                        (wbase && j0 + c < p.n_traces) ? wbase + (int64_t)(j0 + c) * p.n_blocks * 2 : nullptr;
+                    if (n == 32) fold_full_block(ss[c], wcmd[c], (uint32_t)st[c].evh, fstart[c], bkey, wout);
+                    else fold_block(ss[c], wcmd[c], (uint32_t)st[c].evh, fstart[c], n, bi, wout);
+                }
+            }
+        }
+    }
+
+#pragma unroll
+    for (int c = 0; c < kChains; ++c)
+        if (j0 + c < p.n_traces) T::save(st[c], p, pol, 1, q, seg, j0 + c);
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) {
+        const int j = j0 + c;
+        if (j >= p.n_traces) continue;
+        add_to_chain(p, q, j, ss[c].nhi, ss[c].nthr + (uint32_t)nthrf[c], ss[c].trans, ss[c].ev,
+                     ss[c].lock + (uint32_t)lockf[c], ss[c].sexc, ss[c].digest);
+    }
+    if (j0 < p.n_traces) atomicMax(p.c_vmax + chain_idx(p, q, j0), vmax);   // lane-level validation maximum
+}
+
+}  // namespace magus

@@ -80,6 +80,37 @@ struct MagusTicker {
             s[3].ring.push(ad3, pol.k);
         }
     }
+    // One whole steady-state stage (8 ticks x 4 chains, the tile loads included) in one generated PTX
+    // block (MAGUS_STAGE8_K<K>, tick4_asm.cuh); `tile` = this lane's float4 column of the stage's tile.
+    static constexpr bool kHasStage8 = !LOG64 && K >= 1 && K <= 3;
+    __device__ __forceinline__ static void stage8(State* s, uint32_t tile, const DevPolicy& pol, float B_lo,
+                                                  double Blo_d, uint32_t* wcmd, SegStats* ss, uint32_t& vmax) {
+        if constexpr (kHasStage8) {
+            uint32_t e0 = s[0].evh, e1 = s[1].evh, e2 = s[2].evh, e3 = s[3].evh;
+            const uint32_t bitc = 1u << (pol.C - 1), mone = 0xFFFFFFFFu * pol.one;
+#define MAGUS_STAGE_TAIL                                                                                        \
+    e0, e1, e2, e3, ss[0].sexc, ss[1].sexc, ss[2].sexc, ss[3].sexc, ss[0].lock, ss[1].lock, ss[2].lock, ss[3].lock, \
+        ss[0].nthr, ss[1].nthr, ss[2].nthr, ss[3].nthr, wcmd[0], wcmd[1], wcmd[2], wcmd[3], s[0].cnt, s[1].cnt,     \
+        s[2].cnt, s[3].cnt, vmax, tile, B_lo, Blo_d, pol.dinc, pol.ddec, bitc, pol.smin_sc, pol.one, mone
+            if constexpr (K == 1) {
+                MAGUS_STAGE8_K1(s[0].f, s[1].f, s[2].f, s[3].f, s[0].ring.v[0], s[1].ring.v[0], s[2].ring.v[0],
+                                s[3].ring.v[0], MAGUS_STAGE_TAIL);
+            } else if constexpr (K == 2) {
+                MAGUS_STAGE8_K2(s[0].f, s[1].f, s[2].f, s[3].f, s[0].ring.v[0], s[0].ring.v[1], s[1].ring.v[0],
+                                s[1].ring.v[1], s[2].ring.v[0], s[2].ring.v[1], s[3].ring.v[0], s[3].ring.v[1],
+                                MAGUS_STAGE_TAIL);
+            } else {
+                MAGUS_STAGE8_K3(s[0].f, s[1].f, s[2].f, s[3].f, s[0].ring.v[0], s[0].ring.v[1], s[0].ring.v[2],
+                                s[1].ring.v[0], s[1].ring.v[1], s[1].ring.v[2], s[2].ring.v[0], s[2].ring.v[1],
+                                s[2].ring.v[2], s[3].ring.v[0], s[3].ring.v[1], s[3].ring.v[2], MAGUS_STAGE_TAIL);
+            }
+#undef MAGUS_STAGE_TAIL
+            s[0].evh = e0;
+            s[1].evh = e1;
+            s[2].evh = e2;
+            s[3].evh = e3;
+        }
+    }
     // One steady-state tick of one chain (the 64-bit-log kinds; the 32-bit kinds use fast4).
     __device__ __forceinline__ static void fast(State& s, float D, const DevPolicy& pol, float B_lo, double Blo_d,
                                                 uint32_t& wcmd, SegStats& ss, uint32_t& vmax) {

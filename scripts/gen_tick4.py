@@ -86,11 +86,154 @@ def build(warm):
     return out
 
 
+def build_stage(K, TC=8):
+    """MAGUS_STAGE8_K<K>: one whole steady-state stage (TC ticks x 4 chains) of the solo replay kernel,
+    the tile's shared-memory loads included.  The level in effect is carried from tick to tick as a
+    predicate (no integer round trip); the ring of the last K observations lives in virtual registers,
+    so the derivative reads A_{t-K} without moves.  Same semantics as TC calls of MAGUS_TICK4_ASM."""
+    names = [(f"f{c}", "+r") for c in range(C)] + \
+            [(f"r{c}_{i}", "+d") for c in range(C) for i in range(K)] + \
+            [(f"evh{c}", "+r") for c in range(C)] + [(f"exc{c}", "+d") for c in range(C)] + \
+            [(f"lock{c}", "+r") for c in range(C)] + [(f"nthr{c}", "+r") for c in range(C)] + \
+            [(f"wcmd{c}", "+r") for c in range(C)] + [(f"cnt{c}", "+r") for c in range(C)] + [("vmax", "+r")]
+    inames = [("tile", "r"), ("Blo", "f"), ("Blod", "d"), ("dinc", "d"), ("ddec", "d"), ("bitc", "r"), ("smin", "r"),
+              ("one", "r"), ("mone", "r")]
+    idx = {n: f"%{i}" for i, (n, _) in enumerate(names + inames)}
+    R = idx.__getitem__
+    body = ["{", ".reg .pred phi<4>, pthr<4>, pinc<4>, pev<4>, phf<4>, pc<4>, pk<4>;",
+            f".reg .b32 D<{TC * C}>;", f".reg .f64 dd<4>, dv<4>, dx<4>, ad<{TC * C}>;", ".reg .b32 tb<4>, fb<4>;"]
+    for c in range(C):
+        body.append(f"setp.ne.u32 phi{c}, {R(f'f{c}')}, 0;")
+    for tt in range(TC):
+        body.append(f"ld.shared.v4.f32 {{D{tt * C}, D{tt * C + 1}, D{tt * C + 2}, D{tt * C + 3}}}, [{R('tile')}+{tt * 512}];")
+        per_chain = [
+            "cvt.f64.f32 dd{c}, {D};",
+            "setp.gt.and.f32 pthr{c}, {D}, {Blo}, !phi{c};",           # throttled: level f_min and D > B_lo (A14)
+            "selp.f64 {ad}, {Blod}, dd{c}, pthr{c};",                   # A as fp64 (exact)
+            "sub.f64 dv{c}, {ad}, {old};",                              # Alg. 1 numerator A_t - A_{t-k} (P:207)
+            "setp.gt.f64 pinc{c}, dv{c}, {dinc};",                      # +1 (P:209)
+            "setp.lt.or.f64 pev{c}, dv{c}, {ddec}, pinc{c};",           # tune flag (P:213, P:243)
+            "and.b32 tb{c}, {evh}, {bitc};",                            # the flag leaving the C-window (scaled)
+            "shl.b32 {evh}, {evh}, 1;",
+            "@pev{c} mad.lo.u32 {evh}, {one}, {one}, {evh};",
+            "mad.lo.u32 {cnt}, tb{c}, {mone}, {cnt};",                  # window count: - leaving + entering flag
+            "@pev{c} mad.lo.u32 {cnt}, {bitc}, {one}, {cnt};",
+            "setp.ge.u32 phf{c}, {cnt}, {smin};",                       # Alg. 2 (P:230)
+            "or.pred pc{c}, phf{c}, pinc{c};",
+            "not.pred pk{c}, pev{c};",
+            "and.pred pk{c}, pk{c}, phi{c};",
+            "or.pred phi{c}, pc{c}, pk{c};",                            # lock || +1 || (f_max && !flag)
+            "selp.u32 fb{c}, 1, 0, phi{c};",
+            "mad.lo.u32 {wcmd}, {wcmd}, 2, fb{c};",
+            "sub.f64 dx{c}, dd{c}, {ad};",                              # throttling excess D - A (0 unless thr)
+            "add.f64 {exc}, {exc}, dx{c};",
+            "@phf{c} mad.lo.u32 {lock}, {one}, {one}, {lock};",
+            "@pthr{c} mad.lo.u32 {nthr}, {one}, {one}, {nthr};",
+            "max.u32 {vmax}, {vmax}, {Db};",                            # validation (A17)
+        ]
+        for tmpl in per_chain:
+            for c in range(C):
+                t = tt * C + c
+                old = f"ad{(tt - K) * C + c}" if tt >= K else R(f"r{c}_{K - 1 - tt}")
+                body.append(tmpl.format(c=c, D=f"D{t}", Db=f"D{t}", Blo=R("Blo"), ad=f"ad{t}", Blod=R("Blod"), old=old,
+                                        dinc=R("dinc"), ddec=R("ddec"), evh=R(f"evh{c}"), one=R("one"),
+                                        bitc=R("bitc"), mone=R("mone"), cnt=R(f"cnt{c}"), smin=R("smin"),
+                                        wcmd=R(f"wcmd{c}"), exc=R(f"exc{c}"), lock=R(f"lock{c}"),
+                                        nthr=R(f"nthr{c}"), vmax=R("vmax")))
+    for c in range(C):
+        body.append(f"mov.u32 {R(f'f{c}')}, fb{c};")
+        for i in range(K):   # ring newest first: r_i = A_{t0 + TC - 1 - i}
+            body.append(f"mov.f64 {R(f'r{c}_{i}')}, ad{(TC - 1 - i) * C + c};")
+    body.append("}")
+    params = ", ".join(n for n, _ in names + inames)
+    out = [f"#define MAGUS_STAGE8_K{K}(...) MAGUS_STAGE8_K{K}_(__VA_ARGS__)",
+           f"#define MAGUS_STAGE8_K{K}_({params}) \\", "    asm volatile( \\"]
+    out += [f'        "{l}\\n\\t" \\' for l in body]
+    out.append("        : " + ", ".join(f'"{c}"({n})' for n, c in names) + " \\")
+    out.append("        : " + ", ".join(f'"{c}"({n})' for n, c in inames) + " \\")
+    out.append('        : "memory")')
+    return out
+
+
+
+def build_stage_f(K, TC=8):
+    """MAGUS_SSTAGE_K<K>: one whole steady-state stage (TC ticks x 4 chains, tile loads included) of the solo
+    replay kernel, balanced over the issue pipes (ALU and FMA-heavy at half rate, FP64, XU): the throttle
+    test on the FP64 pipe, the tune log, scaled window count and cmd word as (predicated) IMADs, the lock /
+    throttle counters as fp32 adds of 1 (exact integers, fma-lite), the level carried as a predicate
+    across the stage.  Decisions identical to MAGUS_TICK4_ASM."""
+    names = [(f"f{c}", "+r") for c in range(C)] + \
+            [(f"r{c}_{i}", "+d") for c in range(C) for i in range(K)] + \
+            [(f"evh{c}", "+r") for c in range(C)] + [(f"cnt{c}", "+r") for c in range(C)] + \
+            [(f"exc{c}", "+d") for c in range(C)] + [(f"lock{c}", "+f") for c in range(C)] + \
+            [(f"nthr{c}", "+f") for c in range(C)] + [(f"wcmd{c}", "+r") for c in range(C)] + [("vmax", "+r")]
+    inames = [("tile", "r"), ("Blod", "d"), ("dinc", "d"), ("ddec", "d"), ("bitc", "r"), ("smin", "r"),
+              ("one", "r"), ("mone", "r")]
+    idx = {n: f"%{i}" for i, (n, _) in enumerate(names + inames)}
+    R = idx.__getitem__
+    body = ["{", ".reg .pred phi<4>, pthr<4>, pinc<4>, pev<4>, phf<4>, pq<4>, pk<4>;",
+            f".reg .b32 D<{TC * C}>;", f".reg .f64 dd<4>, dv<4>, dx<4>, ad<{TC * C}>;", ".reg .b32 tb<4>;"]
+    for c in range(C):
+        body.append(f"setp.ne.u32 phi{c}, {R(f'f{c}')}, 0;")
+    for tt in range(TC):
+        body.append(f"ld.shared.v4.f32 {{D{tt * C}, D{tt * C + 1}, D{tt * C + 2}, D{tt * C + 3}}}, [{R('tile')}+{tt * 512}];")
+        per_chain = [
+            "cvt.f64.f32 dd{c}, {D};",
+            "setp.gt.and.f64 pthr{c}, dd{c}, {Blod}, !phi{c};",          # throttled: f_min and D > B_lo (A14)
+            "selp.f64 {ad}, {Blod}, dd{c}, pthr{c};",                    # A = min(D, B[f]) as fp64 (exact)
+            "sub.f64 dv{c}, {ad}, {old};",                               # Alg. 1 numerator A_t - A_{t-k} (P:207)
+            "setp.gt.f64 pinc{c}, dv{c}, {dinc};",                       # +1 (P:209)
+            "setp.lt.or.f64 pev{c}, dv{c}, {ddec}, pinc{c};",            # tune flag (P:213, P:243)
+            "and.b32 tb{c}, {evh}, {bitc};",                             # the flag leaving the C-window (scaled)
+            "shl.b32 {evh}, {evh}, 1;",
+            "@pev{c} mad.lo.u32 {evh}, {one}, {one}, {evh};",
+            "mad.lo.u32 {cnt}, tb{c}, {mone}, {cnt};",                   # window count: - leaving + entering
+            "@pev{c} mad.lo.u32 {cnt}, {bitc}, {one}, {cnt};",
+            "setp.ge.u32 phf{c}, {cnt}, {smin};",                        # Alg. 2 (P:230)
+            "not.pred pk{c}, pev{c};",
+            "and.pred pk{c}, pk{c}, phi{c};",
+            "or.pred pq{c}, pk{c}, pinc{c};",                            # +1 || (f_max && !flag)
+            "or.pred phi{c}, pq{c}, phf{c};",                            # || lock: the new level
+            "shl.b32 {wcmd}, {wcmd}, 1;",
+            "@phi{c} mad.lo.u32 {wcmd}, {one}, {one}, {wcmd};",
+            "sub.f64 dx{c}, dd{c}, {ad};",                               # throttling excess D - A (0 unless thr)
+            "add.f64 {exc}, {exc}, dx{c};",
+            "@phf{c} add.f32 {lock}, {lock}, 0f3F800000;",
+            "@pthr{c} add.f32 {nthr}, {nthr}, 0f3F800000;",
+            "max.u32 {vmax}, {vmax}, {D};",                              # validation (A17)
+        ]
+        for tmpl in per_chain:
+            for c in range(C):
+                t = tt * C + c
+                old = f"ad{(tt - K) * C + c}" if tt >= K else R(f"r{c}_{K - 1 - tt}")
+                body.append(tmpl.format(c=c, D=f"D{t}", ad=f"ad{t}", old=old, Blod=R("Blod"), dinc=R("dinc"),
+                                        ddec=R("ddec"), evh=R(f"evh{c}"), one=R("one"), bitc=R("bitc"),
+                                        mone=R("mone"), cnt=R(f"cnt{c}"), smin=R("smin"),
+                                        wcmd=R(f"wcmd{c}"), exc=R(f"exc{c}"), lock=R(f"lock{c}"),
+                                        nthr=R(f"nthr{c}"), vmax=R("vmax")))
+    for c in range(C):
+        body.append(f"selp.u32 {R(f'f{c}')}, 1, 0, phi{c};")
+        for i in range(K):   # ring newest first: r_i = A_{t0 + TC - 1 - i}
+            body.append(f"mov.f64 {R(f'r{c}_{i}')}, ad{(TC - 1 - i) * C + c};")
+    body.append("}")
+    params = ", ".join(n for n, _ in names + inames)
+    name = f"MAGUS_SSTAGE_K{K}"
+    out = [f"#define {name}(...) {name}_(__VA_ARGS__)", f"#define {name}_({params}) \\", "    asm volatile( \\"]
+    out += [f'        "{l}\\n\\t" \\' for l in body]
+    out.append("        : " + ", ".join(f'"{c}"({n})' for n, c in names) + " \\")
+    out.append("        : " + ", ".join(f'"{c}"({n})' for n, c in inames) + " \\")
+    out.append('        : "memory")')
+    return out
+
+
 out = ["// GENERATED by scripts/gen_tick4.py -- do not edit.  One MAGUS tick for the 4 chains of a lane, the",
        "// four chains' instructions interleaved (DESIGN.md section 7); semantics = magus_tick<K, false, SLOW>.",
        "// cnt is the window count scaled by 2^(C-1).",
        "#pragma once"]
 out += build(False) + [""] + build(True)
+for K in (1, 2, 3):
+    out += [""] + build_stage(K)
+    out += [""] + build_stage_f(K)
 path = os.path.join(os.path.dirname(__file__), "..", "paper_2502_03796_b200", "csrc", "tick4_asm.cuh")
 open(path, "w").write("\n".join(out) + "\n")
 print("wrote", os.path.normpath(path))
