@@ -120,7 +120,7 @@ static uint64_t mix64(uint64_t z) {                 /* splitmix64 finaliser */
     return z ^ (z >> 31);
 }
 uint64_t oracle_digest(const uint8_t* cmd_hi, const uint8_t* event, int64_t n) {
-    uint64_t digest = 0;
+    uint32_t sum_cmd = 0, sum_ev = 0;
     int64_t n_blocks = (n + 31) / 32;
     for (int64_t b = 0; b < n_blocks; ++b) {
         uint32_t w_cmd = 0, w_ev = 0;
@@ -131,11 +131,12 @@ uint64_t oracle_digest(const uint8_t* cmd_hi, const uint8_t* event, int64_t n) {
                 w_ev  |= (uint32_t)(event[t]  ? 1u : 0u) << (31 - i);
             }
         }
-        uint64_t word = ((uint64_t)w_cmd << 32) | (uint64_t)w_ev;
-        uint64_t key = mix64((uint64_t)b * 0x9E3779B97F4A7C15ULL) | 1u;   /* odd per-block key */
-        digest += word * key;                                               /* mod 2^64 */
+        uint64_t m = mix64((uint64_t)b * 0x9E3779B97F4A7C15ULL);
+        uint32_t key_cmd = (uint32_t)(m >> 32) | 1u, key_ev = (uint32_t)m | 1u;   /* odd per-block keys */
+        sum_cmd += w_cmd * key_cmd;                                                /* mod 2^32 */
+        sum_ev += w_ev * key_ev;
     }
-    return digest;
+    return ((uint64_t)sum_cmd << 32) | (uint64_t)sum_ev;
 }
 
 /* =============================== the replay loop ==============================

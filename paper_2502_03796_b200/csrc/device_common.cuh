@@ -51,7 +51,7 @@ struct ReplayParams {
     int32_t n_blocks;      // ceil(n_samples / 32)
     float B_lo, B_hi;
     uint32_t bwbits;       // bit pattern of the largest fp32 <= bw_max
-    uint32_t bnd_ebits;    // e << 20 with B_lo * 2^e >= B_hi (solo tick's f_max bound, replay_solo.cuh)
+    uint32_t solo_flags;   // solo replay kernel: bit 0 = speculative segments start from a synthetic full state
     int64_t trace_stride;
     const DevPolicy* pol;  // [n_lane]
     const int32_t* first_low;   // [2][n_traces] first subsampled tick with D <= B_lo / D > B_lo (INT32_MAX: none)
@@ -71,6 +71,7 @@ struct ReplayParams {
     double* c_sexc;        // sum over throttled ticks of (D - B_lo)
     unsigned long long* c_digest;
     uint32_t* words;       // optional [q][j][n_blocks][2]
+    const uint2* dkeys;    // [n_blocks] digest keys (digest_key), computed at create
 };
 
 __host__ __device__ __forceinline__ uint64_t fix_item(int q, int s, int j) {
@@ -104,8 +105,16 @@ __host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {   // splitmix64
     return z ^ (z >> 31);
 }
 static constexpr uint64_t kPhi = 0x9E3779B97F4A7C15ULL;
-// digest key of 32-tick block b: odd, so word -> word * key is a bijection mod 2^64
-__host__ __device__ __forceinline__ uint64_t digest_key(uint64_t b) { return mix64(b * kPhi) | 1ull; }
+// digest keys of 32-tick block b: .x for the cmd word (high half of mix64(b * phi)),
+// .y for the tune-flag word (low half), both odd, so w -> w * key is a bijection mod 2^32
+__host__ __device__ __forceinline__ uint2 digest_key(uint64_t b) {
+    const uint64_t m = mix64(b * kPhi);
+    return make_uint2((uint32_t)(m >> 32) | 1u, (uint32_t)m | 1u);
+}
+// the 64-bit digest is two independent sums mod 2^32: (cmd sum << 32) | flag sum
+__host__ __device__ __forceinline__ uint64_t digest_pack(uint32_t dc, uint32_t de) {
+    return ((uint64_t)dc << 32) | (uint64_t)de;
+}
 
 // Chain kinds with C <= kMaxC32 keep the tune log in 32 bits and the scaled window count
 // (ones << (C-1), which must not overflow: C * 2^(C-1) < 2^32); larger logs use the 64-bit kinds.
@@ -259,12 +268,13 @@ __device__ __forceinline__ TickOut tdp_tick(uint32_t& f, float D, const DevPolic
 struct SegStats {
     uint32_t nhi, nthr, trans, ev, lock, vmax;
     double sexc;
-    uint64_t digest;
+    uint32_t dc, de;   // digest halves (sums mod 2^32 of the cmd / tune-flag words times their block keys)
     __device__ __forceinline__ void zero() {
         nhi = nthr = trans = ev = lock = vmax = 0;
         sexc = 0.0;
-        digest = 0;
+        dc = de = 0;
     }
+    __device__ __forceinline__ uint64_t digest() const { return digest_pack(dc, de); }
 };
 
 // Per-chain totals are zero at the start of every run: zeroed at creation, then by the totals kernel
@@ -290,17 +300,21 @@ __device__ __forceinline__ void add_to_chain(const ReplayParams& p, int q, int j
     if (ev) atomicAdd(p.c_ev + ci, ev);
     if (lock) atomicAdd(p.c_lock + ci, lock);
     if (sexc != 0.0) atomicAdd(p.c_sexc + ci, sexc);
-    if (digest) atomicAdd(p.c_digest + ci, (unsigned long long)digest);
+    // the two digest halves add independently (mod 2^32 each): no carry between them
+    unsigned int* dg = reinterpret_cast<unsigned int*>(p.c_digest + ci);
+    if ((uint32_t)digest) atomicAdd(dg, (unsigned int)(uint32_t)digest);
+    if ((uint32_t)(digest >> 32)) atomicAdd(dg + 1, (unsigned int)(digest >> 32));
 }
 
-// Full-block fold (n == 32) with the block's digest key (digest_key(b)) supplied by the caller.
+// Full-block fold (n == 32) with the block's digest keys (digest_key(b)) supplied by the caller.
 __device__ __forceinline__ void fold_full_block(SegStats& st, uint32_t wcmd, uint32_t ew, uint32_t fstart,
-                                                uint64_t bkey, uint32_t* words_out) {
+                                                uint2 bkey, uint32_t* words_out) {
     const uint32_t lw = (wcmd >> 1) | (fstart << 31);   // level in effect per tick
     st.trans += __popc(wcmd ^ lw);
     st.nhi += __popc(lw);
     st.ev += __popc(ew);
-    st.digest += ((((uint64_t)wcmd) << 32) | (uint64_t)ew) * bkey;
+    st.dc += wcmd * bkey.x;
+    st.de += ew * bkey.y;
     if (words_out) {
         words_out[0] = wcmd;
         words_out[1] = ew;
@@ -320,7 +334,9 @@ __device__ __forceinline__ void fold_block(SegStats& st, uint32_t wcmd, uint32_t
     st.ev += __popc(evw);
     const int sh = 32 - n;
     const uint32_t wc = cw << sh, we = evw << sh;   // tick bt0 + i at bit 31 - i; partial block zero-padded
-    st.digest += ((((uint64_t)wc) << 32) | (uint64_t)we) * digest_key((uint64_t)block_index);
+    const uint2 key = digest_key((uint64_t)block_index);
+    st.dc += wc * key.x;
+    st.de += we * key.y;
     if (words_out) {
         words_out[0] = wc;
         words_out[1] = we;

@@ -562,9 +562,7 @@ static void choose_geometry(magus_replay_t* h, int n_sm, int forced_segments) {
         g.n_ctas = p.n_seg * g.n_tblocks * g.n_pblocks;
         // one policy warp per tile group: one-warp CTAs with CTA-uniform pipeline state (replay_solo.cuh)
         ReplayKernel sk = solo_kernel_for(g.key);
-        // its f_max bound is B_lo * 2^e >= B_hi built on the high word of (double)B_lo (replay_solo.cuh)
-        const bool bound_ok = h->B_lo > 0.f && std::ldexp((double)h->B_lo, 64) >= (double)h->B_hi;
-        g.solo = sk && bound_ok && g.npw == 1 && kTC == 8 && env_int("MAGUS_SOLO", 1) != 0;
+        g.solo = sk && g.npw == 1 && kTC == 8 && env_int("MAGUS_SOLO", 1) != 0;
         if (g.solo) {
             g.kernel = sk;
             g.ng = 1;
@@ -676,13 +674,13 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
     // digest of an all-f_max command stream (STATIC_MAX), DESIGN.md section 5
     {
         const int64_t nb = (d.n_samples + 31) / 32;
-        uint64_t dg = 0;
+        uint32_t dc = 0;
         for (int64_t b = 0; b < nb; ++b) {
             const int n = (int)std::min<int64_t>(32, d.n_samples - b * 32);
             const uint32_t wc = n == 32 ? 0xFFFFFFFFu : (((1u << n) - 1u) << (32 - n));
-            dg += ((uint64_t)wc << 32) * digest_key((uint64_t)b);
+            dc += wc * digest_key((uint64_t)b).x;
         }
-        h->digest_all_hi = dg;
+        h->digest_all_hi = digest_pack(dc, 0);
     }
 
     std::stable_sort(h->lane.begin(), h->lane.end(),
@@ -694,11 +692,7 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
     p.B_lo = h->B_lo;
     p.B_hi = h->B_hi;
     p.bwbits = h->bwbits;
-    {   // smallest e >= 0 with B_lo * 2^e >= B_hi, as the increment of the high word of (double)B_lo
-        int e = 0;
-        while (std::ldexp((double)h->B_lo, e) < (double)p.B_hi && e < 1000) ++e;
-        p.bnd_ebits = (uint32_t)e << 20;
-    }
+    p.solo_flags = env_int("MAGUS_SOLO_SYNTH", 1) ? 1u : 0u;
 
     const int Q = p.n_lane, S = p.n_seg;
     const size_t nst = (size_t)3 * Q * S * std::max(1, d.n_traces);   // entry, exit, staged exit
@@ -725,6 +719,19 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
     p.c_ev = p.c_trans + nchain;
     p.c_lock = p.c_ev + nchain;
     p.c_vmax = p.c_lock + nchain;
+    {   // digest keys of every 32-tick block
+        std::vector<uint2> keys((size_t)std::max(1, p.n_blocks));
+        for (size_t b = 0; b < keys.size(); ++b) keys[b] = digest_key((uint64_t)b);
+        uint2* dk;
+        ALLOC(dk, keys.size());
+        ce = cudaMemcpy(dk, keys.data(), keys.size() * sizeof(uint2), cudaMemcpyHostToDevice);
+        if (ce != cudaSuccess) {
+            magus_status s_ = cuda_fail(h, ce, "cudaMemcpy digest keys");
+            magus_replay_destroy(h);
+            return s_;
+        }
+        p.dkeys = dk;
+    }
     if (d.flags & MAGUS_F_DUMP_WORDS) {
         ALLOC(p.words, (size_t)Q * std::max(1, d.n_traces) * std::max(1, p.n_blocks) * 2);
     } else {

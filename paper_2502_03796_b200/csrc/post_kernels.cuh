@@ -223,7 +223,7 @@ __device__ void rerun_items(const ReplayParams& p, const EpiParams& e, const Fix
             const bool co = T::equal(tru, spec, pol);
             if (co || t >= seg_end) {
                 add_to_chain(p, q, j, dt.nhi - dp.nhi, dt.nthr - dp.nthr, dt.trans - dp.trans, dt.ev - dp.ev,
-                             dt.lock - dp.lock, dt.sexc - dp.sexc, dt.digest - dp.digest);
+                             dt.lock - dp.lock, dt.sexc - dp.sexc, digest_pack(dt.dc - dp.dc, dt.de - dp.de));
                 copy_state(p, pol, q, 1, s - 1, 0, s, j);   // the entry the statistics now belong to
                 if (!co) {                                    // the exit changed: stage it, re-check s+1
                     if (s + 1 < p.n_seg) T::save(tru, p, pol, 2, q, s, j);
@@ -296,7 +296,7 @@ __device__ bool rerun_segment(const ReplayParams& p, const DevPolicy& pol, int q
         }
     }
     add_to_chain(p, q, j, dt.nhi - dp.nhi, dt.nthr - dp.nthr, dt.trans - dp.trans, dt.ev - dp.ev, dt.lock - dp.lock,
-                 dt.sexc - dp.sexc, dt.digest - dp.digest);
+                 dt.sexc - dp.sexc, digest_pack(dt.dc - dp.dc, dt.de - dp.de));
     return coalesced;
 }
 

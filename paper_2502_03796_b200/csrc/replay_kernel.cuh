@@ -208,7 +208,7 @@ __device__ __forceinline__ void consume(const CUtensorMap* tmap, const ReplayPar
             }
         }
         if (counting) {
-            const uint64_t bkey = digest_key((uint64_t)(bt0 >> 5));
+            const uint2 bkey = p.dkeys[bt0 >> 5];
             const int n = min(32, G.seg_end - bt0);
             if (n == 32 && p.words == nullptr) {   // the common case: a whole block, no word dump
 #pragma unroll
@@ -243,7 +243,7 @@ __device__ __forceinline__ void consume(const CUtensorMap* tmap, const ReplayPar
         const int j = j0 + c;
         if (j >= p.n_traces) continue;
         add_to_chain(p, q, j, ss[c].nhi, ss[c].nthr, ss[c].trans, ss[c].ev, ss[c].lock, ss[c].sexc,
-                     ss[c].digest);
+                     ss[c].digest());
     }
     if (j0 < p.n_traces) atomicMax(p.c_vmax + chain_idx(p, q, j0), vmax);   // lane-level validation maximum
 }

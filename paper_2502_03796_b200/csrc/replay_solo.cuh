@@ -139,7 +139,12 @@ __global__ void __launch_bounds__(32, kSoloCtasPerSm)
     sc.Blo_d = (double)B_lo;
     const double Blo_d = sc.Blo_d;
     const int k = pol.k, C = pol.C;
-    const int warm_ticks = k + C - 1;   // ticks before Alg. 1 / 2 are fully defined (A7, A8)
+    // ticks before Alg. 1 / 2 are fully defined (A7, A8).  Speculative segments (seg > 0) may instead start
+    // from a synthetic full state (p.solo_flags bit 0): the ring filled with the first observation, the log
+    // holding C zero flags.  Their warm-up ticks are not counted and only their state at s*L matters,
+    // which the fix-up checks exactly, so they run the steady-state block throughout.
+    const bool synth = seg > 0 && (p.solo_flags & 1u);
+    const int warm_ticks = synth ? 0 : k + C - 1;
     const uint32_t lane_off = (uint32_t)lane * 16u;
 
     State st[kChains];
@@ -186,6 +191,11 @@ __global__ void __launch_bounds__(32, kSoloCtasPerSm)
                 const int fh = j < p.n_traces ? __ldg(p.first_low + p.n_traces + j) : 0x7FFFFFFF;
                 const bool hi = (dd[c] > B_lo && fl < G.tau_w) || (pol.sticky && fl < G.tau_w && fh < G.tau_w);
                 T::set_level(st[c], hi ? 1u : 0u);
+                if (synth) {
+                    const double a0 = (double)(hi ? dd[c] : fminf(dd[c], B_lo));
+#pragma unroll
+                    for (int r = 0; r < (int)(sizeof(st[c].ring.v) / sizeof(double)); ++r) st[c].ring.v[r] = a0;
+                }
             }
         }
 #pragma unroll
@@ -251,7 +261,7 @@ __global__ void __launch_bounds__(32, kSoloCtasPerSm)
             }
         }
         if (counting) {
-            const uint64_t bkey = digest_key((uint64_t)(bt0 >> 5));
+            const uint2 bkey = p.dkeys[bt0 >> 5];
             const int n = min(32, G.seg_end - bt0);
             if (n == 32 && p.words == nullptr) {   // the common case: a whole block, no word dump
 #pragma unroll
@@ -279,7 +289,7 @@ __global__ void __launch_bounds__(32, kSoloCtasPerSm)
         const int j = j0 + c;
         if (j >= p.n_traces) continue;
         add_to_chain(p, q, j, ss[c].nhi, ss[c].nthr + (uint32_t)nthrf[c], ss[c].trans, ss[c].ev,
-                     ss[c].lock + (uint32_t)lockf[c], ss[c].sexc, ss[c].digest);
+                     ss[c].lock + (uint32_t)lockf[c], ss[c].sexc, ss[c].digest());
     }
     if (j0 < p.n_traces) atomicMax(p.c_vmax + chain_idx(p, q, j0), vmax);   // lane-level validation maximum
 }

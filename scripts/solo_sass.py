@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """SASS statistics of the solo replay kernel's stage blocks (no GPU): per-chain-tick instruction mix of the
 steady-state block and the local-memory (spill) instructions inside the stage loops.
-usage: python scripts/solo_sass.py <object-or-.so> [K]"""
+usage: python scripts/solo_sass.py <object-or-.so> [K] [BAL 0|1]"""
 import re
 import subprocess
 import sys
@@ -9,9 +9,10 @@ from collections import Counter
 
 obj = sys.argv[1]
 K = sys.argv[2] if len(sys.argv) > 2 else "1"
+BAL = sys.argv[3] if len(sys.argv) > 3 else "1"   # 1: the pipe-balanced stage variant
 sass = subprocess.run(["cuobjdump", "-sass", obj], capture_output=True, text=True).stdout
 funcs = re.split(r"\n\s+Function : ", sass)
-f = [x for x in funcs if x.startswith(f"_ZN5magus24magus_replay_solo_kernelINS_11MagusTickerILi{K}ELb0")][0]
+f = [x for x in funcs if x.startswith(f"_ZN5magus24magus_replay_solo_kernelINS_11MagusTickerILi{K}ELb0EEELi8ELi3ELb{BAL}")][0]
 ins = []
 for l in f.split("\n"):
     m = re.match(r"\s+/\*([0-9a-f]{4,})\*/\s+(.*?);", l)
