@@ -291,7 +291,8 @@ def run_ours(args, cfg):
                                                                     else ""),
                        "l2": "inputs 1.64 GB/GPU >> 126 MB L2; no flush needed" if ns * n * 4 > 4e8 else "L2-resident"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic, "kernel": "magus_replay_kernel", "replay_ms": tsum["replay_ms"],
+                         "traffic": traffic,
+                         "kernel": "magus_replay_solo_kernel" if geo.get("solo_groups") else "magus_replay_kernel", "replay_ms": tsum["replay_ms"],
                          "replay_ms_max_over_ranks": replay_ms_max, "bytes_per_launch": bytes_per_launch,
                          "peak_source": peak_src},
             "e2e": e2e,

@@ -62,6 +62,7 @@ def _compile(LIB: str, verbose: bool) -> str:
     for key in ("MAGUS_TC", "MAGUS_NSTAGE"):
         if os.environ.get(key):
             flags += [f"-D{key}={int(os.environ[key])}"]
+    flags += os.environ.get("MAGUS_DEFS", "").split()   # build-variant experiments, e.g. "-DMAGUS_SOLO_UNROLL=2"
     if os.environ.get("MAGUS_PTXAS_VERBOSE"):
         flags += ["-Xptxas", "-v"]
     for src in SOURCES:

@@ -17,6 +17,10 @@
 
 namespace magus {
 
+#ifndef MAGUS_SOLO_UNROLL
+#define MAGUS_SOLO_UNROLL 1
+#endif
+
 constexpr int kSoloCtasPerSm = 16;   // 16 one-warp CTAs per SM: 128 registers and ~12.3 KB smem each
 
 template <int TC, int NSTAGE>
@@ -203,7 +207,11 @@ __global__ void __launch_bounds__(32, kSoloCtasPerSm)
         const bool counting = bt0 >= G.seg_start;
         if (bt0 + 32 <= G.seg_end && bt0 - G.tau_w >= warm_ticks) {
             // steady state: four whole-stage PTX blocks
+#if MAGUS_SOLO_UNROLL == 2
+#pragma unroll 2
+#else
 #pragma unroll 1
+#endif
             for (int sub = 0; sub < 32 / TC; ++sub) {
                 const uint32_t tile = tile0 + slot * kTileBytes;
                 mbar_wait_loop(bar0 + 8 * slot, phase);

@@ -38,7 +38,7 @@ for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1]) / len(kv[1])):
     lines.append(f"{k[:100]:100s} {len(v):8d} {m:9.1f} {share}")
 live = bench["kernel_ms"]
 lines += ["", f"live CUDA-event split of the same bench (ms per step): {json.dumps(live)}",
-          f"replay share of the step: ncu {100 * max(v for k, v in step.items() if 'replay_kernel' in k) / tot:.1f}%"
+          f"replay share of the step: ncu {100 * max(v for k, v in step.items() if 'magus_replay' in k) / tot:.1f}%"
           f" vs live {100 * live['replay_ms'] / bench['ms_per_step']:.1f}%"]
 open(os.path.join(prof, f"{rnd}_launches.txt"), "w").write("\n".join(lines) + "\n")
 
