@@ -56,7 +56,7 @@ keys = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__
         "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
         "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "smsp__inst_executed_op_tma_ld.sum",
         "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"]
-out = [f"# ncu --set full --clock-control none of magus_replay_kernel ({rnd}, {tag}), bench config "
+out = [f"# ncu --set full --clock-control none of the replay kernel ({rnd}, {tag}), bench config "
        f"{bench['config']['workload']}", ""]
 for k in keys:
     if k in d:
@@ -64,7 +64,8 @@ for k in keys:
 st = sorted(((k, float(d[k][0].replace(",", ""))) for k in d
              if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio")
              and d[k][0].replace(",", "").replace(".", "").isdigit()), key=lambda t: -t[1])
-out += ["", "warp stalls per issued instruction:"] + [f"   {k[34:-33]:40s} {x:7.3f}" for k, x in st[:10] if x > 0.02]
+out += ["", "warp stalls per issued instruction:"] + [f"   {k[len('smsp__average_warps_issue_stalled_'):-len('_per_issue_active.ratio')]:40s} {x:7.3f}"
+                                                   for k, x in st[:10] if x > 0.02]
 UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 rb = float(d["dram__bytes_read.sum"][0].replace(",", "")) * UNIT[d["dram__bytes_read.sum"][1]]
 wb = float(d["dram__bytes_write.sum"][0].replace(",", "")) * UNIT[d["dram__bytes_write.sum"][1]]
