@@ -57,6 +57,48 @@ int minb_for(int key) { return key < 1000 && (key == 0 || key >= 4) ? 1 : 2; }
 template <class T, int MINB = 2>
 ReplayKernel K() { return (ReplayKernel)magus_replay_kernel<T, kTC, kNStage, MINB>; }
 
+int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return (v && *v) ? std::atoi(v) : dflt;
+}
+
+// the lockstep walk (one-warp CTAs, lane = chain; post_kernels.cuh) covers these chain kinds
+bool lockstep_walk(int key) {
+    return ((key >= 1 && key <= 8) || key == 1000 + LANE_TDP) && env_int("MAGUS_WALK_LOCKSTEP", 1);
+}
+
+// chain-walk fix-up kernel for a chain kind (nullptr: stateless kinds never mismatch)
+typedef void (*WalkKernel)(ReplayParams, EpiParams, FixParams, int, const float*);
+WalkKernel walk_kernel_for(int key) {
+    if (lockstep_walk(key)) {
+        switch (key) {
+            case 1: return magus_fix_lockstep_kernel<MagusTicker<1, false>>;
+            case 2: return magus_fix_lockstep_kernel<MagusTicker<2, false>>;
+            case 3: return magus_fix_lockstep_kernel<MagusTicker<3, false>>;
+            case 4: return magus_fix_lockstep_kernel<MagusTicker<4, false>>;
+            case 5: return magus_fix_lockstep_kernel<MagusTicker<5, false>>;
+            case 6: return magus_fix_lockstep_kernel<MagusTicker<6, false>>;
+            case 7: return magus_fix_lockstep_kernel<MagusTicker<7, false>>;
+            case 8: return magus_fix_lockstep_kernel<MagusTicker<8, false>>;
+            default: return magus_fix_lockstep_kernel<TdpTicker>;
+        }
+    }
+    switch (key) {   // one thread per chain (the generic ring, the 64-bit logs; MAGUS_WALK_LOCKSTEP=0)
+        case 1: return magus_fix_walk_kernel<MagusTicker<1, false>>;
+        case 2: return magus_fix_walk_kernel<MagusTicker<2, false>>;
+        case 3: return magus_fix_walk_kernel<MagusTicker<3, false>>;
+        case 4: return magus_fix_walk_kernel<MagusTicker<4, false>>;
+        case 5: return magus_fix_walk_kernel<MagusTicker<5, false>>;
+        case 6: return magus_fix_walk_kernel<MagusTicker<6, false>>;
+        case 7: return magus_fix_walk_kernel<MagusTicker<7, false>>;
+        case 8: return magus_fix_walk_kernel<MagusTicker<8, false>>;
+        case 1000 + LANE_TDP: return magus_fix_walk_kernel<TdpTicker>;
+        case 1000 + LANE_STATIC_MIN: return nullptr;
+        case 1000 + LANE_VALIDATE: return nullptr;
+        default: return key >= 100 ? magus_fix_walk_kernel<MagusTicker<0, true>> : magus_fix_walk_kernel<MagusTicker<0, false>>;
+    }
+}
+
 // fix-up re-run kernel for a chain kind (nullptr: stateless kinds never mismatch)
 RerunKernel rerun_kernel_for(int key) {
     switch (key) {
@@ -91,11 +133,6 @@ ReplayKernel replay_kernel_for(int key) {
         case 1000 + LANE_STATIC_MIN: return K<StaticMinTicker<false>>();
         default: return K<StaticMinTicker<true>>();
     }
-}
-
-int env_int(const char* name, int dflt) {
-    const char* v = std::getenv(name);
-    return (v && *v) ? std::atoi(v) : dflt;
 }
 
 // one-warp-CTA replay kernel (replay_solo.cuh) of a chain kind, or nullptr if it has none
@@ -341,9 +378,11 @@ struct magus_replay {
     FixParams fx{};
     uint32_t* d_wl_count = nullptr;   // [2][G] + cursors [G] + any_unresolved (one allocation)
     int fix_rounds = 2;
+    bool walk_fix = true;             // chain-walk fix-up (else worklist rounds + serial fallback)
     int n_sm = 148;
     int alloc_segments = 1;           // scratch is sized for this many segments (re-plans only shrink)
     int replans = 0;
+    double replan_frac = 0.25;        // re-plan above this fraction of wrong speculative entries
     bool pdl = true;           // programmatic dependent launch between the run's kernels (MAGUS_NO_PDL=1: off)
     // device memory
     std::vector<void*> allocs;
@@ -775,6 +814,11 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
         ALLOC(h->fx.wl, (size_t)2 * std::max<int64_t>(1, total));
         ALLOC(h->d_wl_count, (size_t)3 * G + 1);
         ALLOC(h->fx.unresolved, (size_t)Q * std::max(1, d.n_traces));
+        ALLOC(h->fx.first_bad, (size_t)Q * std::max(1, d.n_traces));
+        {   // INT_MAX ("no wrong entry") between runs: the walk kernel restores what it reads
+            std::vector<int32_t> inf((size_t)Q * std::max(1, d.n_traces), 0x7FFFFFFF);
+            cudaMemcpy(h->fx.first_bad, inf.data(), inf.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+        }
         cudaMemcpy(d_gol, grp_of_lane.data(), Q * sizeof(int32_t), cudaMemcpyHostToDevice);
         cudaMemcpy(d_first, first.data(), G * sizeof(int32_t), cudaMemcpyHostToDevice);
         cudaMemcpy(d_off, off.data(), G * sizeof(int64_t), cudaMemcpyHostToDevice);
@@ -787,6 +831,9 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
         h->fx.wl_cursor = h->d_wl_count + 2 * G;
         h->fx.any_unresolved = h->d_wl_count + 3 * G;
         h->fix_rounds = std::max(1, env_int("MAGUS_FIX_ROUNDS", 1));
+        h->walk_fix = env_int("MAGUS_FIX_WALK", 1) != 0;
+        h->replan_frac = env_int("MAGUS_REPLAN_PCT", 101) / 100.0;   // > 100: never (the chain walk's cost
+                                                                      // does not grow with the segment count)
 
     }
 #undef ALLOC
@@ -968,7 +1015,20 @@ static magus_status enqueue_run(magus_replay_t* h, const float* d_trace, const f
     if (d.n_traces > 0) {
         const int G = h->fx.n_fgroups;
         const FixParams& fx = h->fx;
-        if (has_work && p.n_seg > 1) {
+        if (has_work && p.n_seg > 1 && h->walk_fix) {
+            // exact fix-up, one pass per chain in time order (magus_fix_walk_kernel): every launch group's
+            // chains scan their boundaries and re-run from the first wrong entry on
+            dim3 gc((unsigned)((d.n_traces + 255) / 256), (unsigned)(p.n_seg - 1), (unsigned)p.n_lane);
+            CU(h, launch_k(magus_fix_mark_kernel, gc, dim3(256), 0, s, h->pdl && !timing, p, h->fx));
+            for (const LaunchGroup& g : h->groups) {
+                WalkKernel wk = walk_kernel_for(g.key);
+                if (!wk) continue;
+                // the lockstep walk: one-warp CTAs, spread over the SMs (a walk is latency-bound)
+                const int tpb = lockstep_walk(g.key) ? 32 : 128;
+                dim3 gw((unsigned)((d.n_traces + tpb - 1) / tpb), (unsigned)g.nq);
+                CU(h, launch_k(wk, gw, dim3(tpb), 0, s, h->pdl, p, ep, h->fx, g.q_base, d_trace));
+            }
+        } else if (has_work && p.n_seg > 1) {
             // exact fix-up: round 1 checks every segment entry against the previous exit; later rounds
             // only re-check the successors of segments whose exit changed; a serial walk finishes the rest
             // (worklist counters and `unresolved` zeroed by the pre-pass).
@@ -1151,7 +1211,7 @@ extern "C" magus_status magus_replay_results(magus_replay_t* h, magus_results* o
     // aliased oscillations), the next runs use half as many segments.  Results are exact either way.
     if (d.tuning_segments == 0 && h->rp.n_seg > 1 && !env_int("MAGUS_NO_REPLAN", 0)) {
         const double spec = (double)h->rp.n_lane * (h->rp.n_seg - 1) * std::max(1, d.n_traces);
-        if ((double)segs > 0.01 * spec) {
+        if ((double)segs > h->replan_frac * spec) {
             const int S_new = std::max(1, h->rp.n_seg / 2);
             const ReplayParams keep = h->rp;
             choose_geometry(h, h->n_sm, S_new);
@@ -1256,7 +1316,8 @@ extern "C" magus_status magus_replay_geometry(const magus_replay_t* h, int32_t o
     if (has_work && p.n_seg > 1) {
         int nr = 0;
         for (const LaunchGroup& g : h->groups) nr += rerun_kernel_for(g.key) ? 1 : 0;
-        nk += 1 + nr * h->fix_rounds + (h->fix_rounds - 1) + 2;  // check, re-run rounds, candidate checks, serial
+        if (h->walk_fix) nk += 1 + nr;                            // mark + one chain-walk kernel per launch group
+        else nk += 1 + nr * h->fix_rounds + (h->fix_rounds - 1) + 2;   // check, re-run rounds, candidate checks, serial
     }
     nk += 1 + (d.world > 1 ? 1 : 0);                              // totals (+ chunk sums before the allreduce)
     int solo = 0;

@@ -86,6 +86,7 @@ struct FixParams {
     uint32_t* wl_cursor;      // [n_fgroups] work-stealing cursors
     uint8_t* unresolved;      // [Q][n_traces] chains left for the serial walk
     unsigned int* any_unresolved;
+    int32_t* first_bad;       // [Q][n_traces] chain walk: first wrong segment entry (INT_MAX: none)
 };
 
 // warp-aggregated append of `item` (lanes with want) to list `buf` of group g
@@ -113,6 +114,17 @@ __device__ __forceinline__ void copy_state(const ReplayParams& p, const DevPolic
     if (pol.kind == LANE_MAGUS)
         for (int r = 0; r < pol.k; ++r)
             p.st_ring[ring_idx(p, e_dst, q, s_dst, r, j)] = p.st_ring[ring_idx(p, e_src, q, s_src, r, j)];
+}
+
+// Chain walk, step 1: every (q, s >= 1, j) whose speculative entry differs from the previous exit lowers
+// the chain's first_bad to s (first_bad is INT_MAX between runs: the walk kernel resets what it reads).
+__global__ void __launch_bounds__(256) magus_fix_mark_kernel(const ReplayParams p, const FixParams f) {
+    ptx::pdl_wait();
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int s = blockIdx.y + 1, q = blockIdx.z;
+    if (j >= p.n_traces) return;
+    const DevPolicy pol = p.pol[q];
+    if (entry_mismatch_any(p, pol, q, s, j)) atomicMin(f.first_bad + (int64_t)q * p.n_traces + j, s);
 }
 
 // Round 1: every (q, s >= 1, j) whose speculative entry differs from the previous exit.
@@ -358,6 +370,365 @@ __global__ void __launch_bounds__(256) magus_fix_serial_kernel(const ReplayParam
         MAGUS_SERIAL(TdpTicker);
     }
 #undef MAGUS_SERIAL
+}
+
+// ------------------------------------------------------------------ latency-optimised re-run (chain walk)
+// One MAGUS tick with a short loop-carried path: everything that depends only on the sample and on the
+// ring (A_{t-k}, known k ticks ahead) is computed for both levels first -- the f_min observation, both
+// derivative numerators and their Alg. 1 flags -- and the level in effect only selects among them.
+// The chain-to-chain dependency is then select -> log / window count -> Alg. 2 -> decision.  Same
+// decisions as magus_tick (the incremental window count of tick4_asm.cuh, scaled by 2^(C-1)).
+template <int K>
+__device__ __forceinline__ TickOut walk_tick(MagusState<K, false>& s, float D, double dd, const DevPolicy& pol,
+                                             float B_lo, double Blo_d, uint32_t bitc) {
+    const double old = s.ring.oldest(pol.k);
+    const bool thr_lo = D > B_lo;                     // throttled if the level in effect is f_min (A14)
+    const double ad_lo = thr_lo ? Blo_d : dd;
+    const double dv_lo = ad_lo - old, dv_hi = dd - old;
+    const bool inc_lo = dv_lo > pol.dinc, dec_lo = dv_lo < pol.ddec;
+    const bool inc_hi = dv_hi > pol.dinc, dec_hi = dv_hi < pol.ddec;
+    const bool hi = s.f != 0u;
+    const bool inc = hi ? inc_hi : inc_lo, dec = hi ? dec_hi : dec_lo;
+    const bool ev = inc || dec;
+    const uint32_t leaving = s.evh & bitc;
+    s.evh = (s.evh << 1) | (ev ? 1u : 0u);
+    s.cnt = s.cnt - leaving + (ev ? bitc : 0u);
+    const bool hf = s.cnt >= pol.smin_sc;
+    TickOut o;
+    o.cmd = (hf || inc || (hi && !dec)) ? 1u : 0u;
+    o.thr = (!hi && thr_lo) ? 1u : 0u;
+    o.ev = ev ? 1u : 0u;
+    o.hf = hf ? 1u : 0u;
+    o.sig = 0;
+    s.ring.push(hi ? dd : ad_lo, pol.k);
+    s.f = o.cmd;
+    return o;
+}
+
+// rerun_segment for the register-ring MAGUS kinds: walk_tick for the true and the speculative state side
+// by side (two independent recurrences per lane), whole 32-tick blocks without per-tick predicates, and
+// the samples of the next two blocks loaded while the current block is stepped (strided rows of the
+// trace: one sector each; the loads, not the arithmetic, bound a lone walking warp otherwise).
+template <int K, bool FULL>
+__device__ __forceinline__ void walk_block(MagusState<K, false>& tru, MagusState<K, false>& spec, SegStats& dt,
+                                           SegStats& dp, const float* dv, int n, const DevPolicy& pol, float B_lo,
+                                           double Blo_d, uint32_t bitc, uint32_t& wct, uint32_t& wcs) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+        if (FULL || i < n) {
+            const float D = dv[i];
+            const double dd = (double)D;
+            const TickOut ot = walk_tick<K>(tru, D, dd, pol, B_lo, Blo_d, bitc);
+            const TickOut os = walk_tick<K>(spec, D, dd, pol, B_lo, Blo_d, bitc);
+            wct = (wct << 1) | ot.cmd;
+            wcs = (wcs << 1) | os.cmd;
+            dt.nthr += ot.thr;
+            dt.lock += ot.hf;
+            dt.sexc += ot.thr ? dd - Blo_d : 0.0;
+            dp.nthr += os.thr;
+            dp.lock += os.hf;
+            dp.sexc += os.thr ? dd - Blo_d : 0.0;
+        }
+    }
+}
+
+template <int K>
+__device__ bool rerun_segment_walk(const ReplayParams& p, const DevPolicy& pol, int q, int s, int j,
+                                   const float* trace, MagusState<K, false>& tru, MagusState<K, false>& spec) {
+    const int seg_start = s * p.seg_len;
+    const int seg_end = min(seg_start + p.seg_len, p.n_samples);
+    const double Blo_d = (double)p.B_lo;
+    const uint32_t bitc = 1u << (pol.C - 1);
+    SegStats dt, dp;
+    dt.zero();
+    dp.zero();
+    bool coalesced = false;
+    const float* col = trace + j;
+    float n1[32], n2[32];   // samples of the next two blocks
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+        n1[i] = (seg_start + i < seg_end) ? __ldg(col + (int64_t)(seg_start + i) * p.trace_stride) : 0.0f;
+        n2[i] = (seg_start + 32 + i < seg_end) ? __ldg(col + (int64_t)(seg_start + 32 + i) * p.trace_stride) : 0.0f;
+    }
+    for (int bt0 = seg_start; bt0 < seg_end; bt0 += 32) {
+        float dv[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            dv[i] = n1[i];
+            n1[i] = n2[i];
+        }
+        const int nb = bt0 + 64;
+        if (nb + 32 <= seg_end) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) n2[i] = __ldg(col + (int64_t)(nb + i) * p.trace_stride);
+        } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) n2[i] = (nb + i < seg_end) ? __ldg(col + (int64_t)(nb + i) * p.trace_stride) : 0.f;
+        }
+        const uint32_t fst = tru.f, fss = spec.f;
+        const int n = min(32, seg_end - bt0);
+        uint32_t wct = 0, wcs = 0;
+        if (n == 32) walk_block<K, true>(tru, spec, dt, dp, dv, n, pol, p.B_lo, Blo_d, bitc, wct, wcs);
+        else walk_block<K, false>(tru, spec, dt, dp, dv, n, pol, p.B_lo, Blo_d, bitc, wct, wcs);
+        const int64_t b = bt0 >> 5;
+        uint32_t* wout = p.words ? p.words + (((int64_t)q * p.n_traces + j) * p.n_blocks + b) * 2 : nullptr;
+        fold_block(dt, wct, tru.evh, fst, n, b, wout);
+        fold_block(dp, wcs, spec.evh, fss, n, b, nullptr);
+        if (MagusTicker<K, false>::equal(tru, spec, pol)) {
+            coalesced = true;
+            break;
+        }
+    }
+    add_to_chain(p, q, j, dt.nhi - dp.nhi, dt.nthr - dp.nthr, dt.trans - dp.trans, dt.ev - dp.ev, dt.lock - dp.lock,
+                 dt.sexc - dp.sexc, digest_pack(dt.dc - dp.dc, dt.de - dp.de));
+    return coalesced;
+}
+
+template <class T>
+struct WalkRerun {
+    __device__ static bool run(const ReplayParams& p, const DevPolicy& pol, int q, int s, int j, const float* trace,
+                               typename T::State& tru, typename T::State& spec) {
+        return rerun_segment<T>(p, pol, q, s, j, trace, tru, spec);
+    }
+};
+template <int K>
+struct WalkRerun<MagusTicker<K, false>> {
+    __device__ static bool run(const ReplayParams& p, const DevPolicy& pol, int q, int s, int j, const float* trace,
+                               MagusState<K, false>& tru, MagusState<K, false>& spec) {
+        if constexpr (K >= 1) return rerun_segment_walk<K>(p, pol, q, s, j, trace, tru, spec);
+        else return rerun_segment<MagusTicker<K, false>>(p, pol, q, s, j, trace, tru, spec);
+    }
+};
+
+// ------------------------------------------------------------------ lockstep chain walk (k <= 3)
+// A warp walks the 32 consecutive chains (traces) of its lanes in lockstep, lane = chain, each lane
+// stepping its true and its speculative state over the same samples with the generated 2-chain stage
+// block (MAGUS_WSTAGE_K<K>, tick4_asm.cuh).  The warp's loads are one coalesced row segment per tick.
+// Segments in which no lane of the warp walks are skipped; within a segment a lane stops at the block
+// end where its two states coalesce (adding the statistics delta of its prefix), and the warp leaves the
+// segment when every lane has stopped.  Lanes that do not walk step garbage that is never used.
+template <int K>
+__device__ __forceinline__ void walk_stage(MagusState<K, false>* st, float* lock, float* nthr, uint32_t* wcmd,
+                                           SegStats* ss, const float* d8, const DevPolicy& pol, double Blo_d) {
+    uint32_t e0 = st[0].evh, e1 = st[1].evh;
+    const uint32_t bitc = 1u << (pol.C - 1), mone = 0xFFFFFFFFu * pol.one;
+#define WALK_TAIL                                                                                                \
+    e0, e1, st[0].cnt, st[1].cnt, ss[0].sexc, ss[1].sexc, lock[0], lock[1], nthr[0], nthr[1], wcmd[0], wcmd[1],    \
+        __float_as_uint(d8[0]), __float_as_uint(d8[1]), __float_as_uint(d8[2]), __float_as_uint(d8[3]),            \
+        __float_as_uint(d8[4]), __float_as_uint(d8[5]), __float_as_uint(d8[6]), __float_as_uint(d8[7]), Blo_d,      \
+        pol.dinc, pol.ddec, bitc, pol.smin_sc, pol.one, mone
+#define R0(i) st[0].ring.v[i]
+#define R1(i) st[1].ring.v[i]
+    if constexpr (K == 1) {
+        MAGUS_WSTAGE_K1(st[0].f, st[1].f, R0(0), R1(0), WALK_TAIL);
+    } else if constexpr (K == 2) {
+        MAGUS_WSTAGE_K2(st[0].f, st[1].f, R0(0), R0(1), R1(0), R1(1), WALK_TAIL);
+    } else if constexpr (K == 3) {
+        MAGUS_WSTAGE_K3(st[0].f, st[1].f, R0(0), R0(1), R0(2), R1(0), R1(1), R1(2), WALK_TAIL);
+    } else if constexpr (K == 4) {
+        MAGUS_WSTAGE_K4(st[0].f, st[1].f, R0(0), R0(1), R0(2), R0(3), R1(0), R1(1), R1(2), R1(3), WALK_TAIL);
+    } else if constexpr (K == 5) {
+        MAGUS_WSTAGE_K5(st[0].f, st[1].f, R0(0), R0(1), R0(2), R0(3), R0(4), R1(0), R1(1), R1(2), R1(3), R1(4),
+                        WALK_TAIL);
+    } else if constexpr (K == 6) {
+        MAGUS_WSTAGE_K6(st[0].f, st[1].f, R0(0), R0(1), R0(2), R0(3), R0(4), R0(5), R1(0), R1(1), R1(2), R1(3),
+                        R1(4), R1(5), WALK_TAIL);
+    } else if constexpr (K == 7) {
+        MAGUS_WSTAGE_K7(st[0].f, st[1].f, R0(0), R0(1), R0(2), R0(3), R0(4), R0(5), R0(6), R1(0), R1(1), R1(2),
+                        R1(3), R1(4), R1(5), R1(6), WALK_TAIL);
+    } else {
+        MAGUS_WSTAGE_K8(st[0].f, st[1].f, R0(0), R0(1), R0(2), R0(3), R0(4), R0(5), R0(6), R0(7), R1(0), R1(1),
+                        R1(2), R1(3), R1(4), R1(5), R1(6), R1(7), WALK_TAIL);
+    }
+#undef R0
+#undef R1
+#undef WALK_TAIL
+    st[0].evh = e0;
+    st[1].evh = e1;
+}
+
+// the samples [t0, min(t0 + 32, end)) of one trace column (coalesced across the warp's lanes)
+__device__ __forceinline__ void walk_load(float* v, const float* col, int t0, int end, int64_t stride) {
+    const float* c = col + (int64_t)t0 * stride;
+    if (t0 + 32 <= end) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = __ldg(c + i * stride);
+    } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = (t0 + i < end) ? __ldg(c + i * stride) : 0.f;
+    }
+}
+
+// lockstep step of one whole 32-tick block for the pair (true, speculative) of every lane
+template <class T>
+struct LockstepStep;
+template <int K>
+struct LockstepStep<MagusTicker<K, false>> {
+    __device__ __forceinline__ static void run(MagusState<K, false>* st, float* lock, float* nthr, uint32_t* wcmd,
+                                               SegStats* ss, const float* dv, const DevPolicy& pol,
+                                               const ReplayParams&, double Blo_d) {
+#pragma unroll
+        for (int g = 0; g < 4; ++g) walk_stage<K>(st, lock, nthr, wcmd, ss, dv + 8 * g, pol, Blo_d);
+    }
+};
+template <>
+struct LockstepStep<TdpTicker> {
+    __device__ __forceinline__ static void run(TdpTicker::State* st, float*, float*, uint32_t* wcmd, SegStats* ss,
+                                               const float* dv, const DevPolicy& pol, const ReplayParams& p,
+                                               double Blo_d) {
+        uint32_t vmax = 0;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            TdpTicker::fast(st[0], dv[i], pol, p.B_lo, Blo_d, wcmd[0], ss[0], vmax);
+            TdpTicker::fast(st[1], dv[i], pol, p.B_lo, Blo_d, wcmd[1], ss[1], vmax);
+        }
+    }
+};
+
+// one tick of the ragged last block (any chain kind)
+template <class T>
+__device__ __forceinline__ void lockstep_tick(typename T::State& st, float D, const DevPolicy& pol,
+                                              const ReplayParams& p, double Blo_d, uint32_t& wc, SegStats& ss) {
+    TickOut o;
+    if constexpr (T::kWarmupRules) o = walk_tick<sizeof(st.ring.v) / sizeof(double)>(st, D, (double)D, pol, p.B_lo,
+                                                                                      Blo_d, 1u << (pol.C - 1));
+    else o = T::template tick<false>(st, D, pol, p.B_lo, p.B_hi, true, true);
+    wc = (wc << 1) | o.cmd;
+    ss.nthr += o.thr;
+    ss.lock += o.hf;
+    if (o.thr) ss.sexc += (double)D - Blo_d;
+}
+
+template <class T>
+__global__ void __launch_bounds__(32) magus_fix_lockstep_kernel(const ReplayParams p, const EpiParams e,
+                                                                const FixParams f, int q_base,
+                                                                const float* __restrict__ trace) {
+    ptx::pdl_wait();
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int q = q_base + blockIdx.y;
+    const bool valid = j < p.n_traces;
+    int s0 = 0x7FFFFFFF;
+    if (valid) {
+        const int64_t ci = (int64_t)q * p.n_traces + j;
+        s0 = f.first_bad[ci];
+        if (s0 < 0x7FFFFFFF) f.first_bad[ci] = 0x7FFFFFFF;   // reset for the next run
+    }
+    const int ws = __reduce_min_sync(0xffffffffu, s0);
+    if (ws >= p.n_seg) return;   // warp-uniform
+    const DevPolicy pol = p.pol[q];
+    const double Blo_d = (double)p.B_lo;
+    const float* col = trace + (valid ? j : 0);
+    typename T::State st[2];   // [0] true state, [1] speculative state
+    bool walking = false;      // this lane's true state differs from its stored trajectory
+    int walked = 0;
+    for (int s = ws; s < p.n_seg; ++s) {
+        if (walking) {
+            T::load(st[1], p, pol, 0, q, s, j);
+            if (T::equal(st[0], st[1], pol)) walking = false;
+        } else if (valid && s >= s0 && !T::stored_equal(p, pol, q, 0, s, 1, s - 1, j)) {
+            T::load(st[0], p, pol, 1, q, s - 1, j);
+            T::load(st[1], p, pol, 0, q, s, j);
+            walking = true;
+        }
+        if (!__any_sync(0xffffffffu, walking)) continue;
+        walked += walking ? 1 : 0;
+        const int seg_start = s * p.seg_len, seg_end = min(seg_start + p.seg_len, p.n_samples);
+        SegStats ss[2];
+        ss[0].zero();
+        ss[1].zero();
+        float lock[2] = {0.f, 0.f}, nthr[2] = {0.f, 0.f};
+        bool active = walking;
+        // the samples of the next two blocks are loaded while the current block is stepped
+        float n1[32], n2[32];
+        walk_load(n1, col, seg_start, seg_end, p.trace_stride);
+        if (seg_start + 32 < seg_end) walk_load(n2, col, seg_start + 32, seg_end, p.trace_stride);
+        for (int bt0 = seg_start; bt0 < seg_end; bt0 += 32) {
+            if (!__any_sync(0xffffffffu, active)) break;
+            const int n = min(32, seg_end - bt0);
+            float dv[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                dv[i] = n1[i];
+                n1[i] = n2[i];
+            }
+            if (bt0 + 64 < seg_end) walk_load(n2, col, bt0 + 64, seg_end, p.trace_stride);
+            const uint32_t fs0 = T::level(st[0]), fs1 = T::level(st[1]);
+            uint32_t wcmd[2] = {0u, 0u};
+            if (n == 32) {
+                LockstepStep<T>::run(st, lock, nthr, wcmd, ss, dv, pol, p, Blo_d);
+            } else {   // the ragged last block of a trace
+                for (int i = 0; i < n; ++i) {
+                    lockstep_tick<T>(st[0], dv[i], pol, p, Blo_d, wcmd[0], ss[0]);
+                    lockstep_tick<T>(st[1], dv[i], pol, p, Blo_d, wcmd[1], ss[1]);
+                }
+            }
+            const int64_t b = bt0 >> 5;
+            uint32_t* wout = (active && p.words) ? p.words + (((int64_t)q * p.n_traces + j) * p.n_blocks + b) * 2
+                                                 : nullptr;
+            uint32_t ew0 = 0, ew1 = 0;
+            if constexpr (T::kWarmupRules) {
+                ew0 = (uint32_t)st[0].evh;
+                ew1 = (uint32_t)st[1].evh;
+            }
+            fold_block(ss[0], wcmd[0], ew0, fs0, n, b, wout);
+            fold_block(ss[1], wcmd[1], ew1, fs1, n, b, nullptr);
+            const bool same = T::equal(st[0], st[1], pol);
+            if (active && (same || bt0 + 32 >= seg_end)) {   // coalesced (the rest is right), or segment end
+                add_to_chain(p, q, j, ss[0].nhi - ss[1].nhi,
+                             ss[0].nthr - ss[1].nthr + ((uint32_t)nthr[0] - (uint32_t)nthr[1]),
+                             ss[0].trans - ss[1].trans, ss[0].ev - ss[1].ev,
+                             ss[0].lock - ss[1].lock + ((uint32_t)lock[0] - (uint32_t)lock[1]),
+                             ss[0].sexc - ss[1].sexc, digest_pack(ss[0].dc - ss[1].dc, ss[0].de - ss[1].de));
+                walking = !same;   // carry the true exit into the next boundary
+                active = false;
+            }
+        }
+    }
+    if (walked) {
+        atomicAdd(e.fix_segments, (unsigned long long)walked);
+        atomicMax(e.fix_rounds, walked);
+    }
+}
+
+// ------------------------------------------------------------------ chain walk (default fix-up, exact)
+// One thread per chain (q, j): scans the segment boundaries in order; at the first entry that differs
+// from the previous exit it re-runs that segment from the true state next to the speculative one
+// (rerun_segment: until they coalesce at a block end, else to the segment end), and carries the true
+// state on across later boundaries until it agrees with a stored entry again.  Every chain is thus
+// fixed in one pass, in time order, whatever the number of consecutive wrong guesses (phase-ambiguous
+// limit cycles of oscillating traces make a wrong guess persist: DESIGN.md section 9).  T: the chain
+// kind of the launch group (register ring for k in {1, 2, 4, 8}).
+template <class T>
+__global__ void __launch_bounds__(128) magus_fix_walk_kernel(const ReplayParams p, const EpiParams e, const FixParams f,
+                                                             int q_base, const float* __restrict__ trace) {
+    ptx::pdl_wait();
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int q = q_base + blockIdx.y;
+    if (j >= p.n_traces) return;
+    const int s0 = f.first_bad[(int64_t)q * p.n_traces + j];   // first wrong entry (magus_fix_mark_kernel)
+    if (s0 >= p.n_seg) return;
+    f.first_bad[(int64_t)q * p.n_traces + j] = 0x7FFFFFFF;       // reset for the next run
+    const DevPolicy pol = p.pol[q];
+    typename T::State tru, spec;
+    bool carry = false;   // tru holds the true exit of segment s - 1, which the stored one is not
+    int walked = 0;
+    for (int s = s0; s < p.n_seg; ++s) {
+        if (!carry) {
+            if (T::stored_equal(p, pol, q, 0, s, 1, s - 1, j)) continue;
+            T::load(tru, p, pol, 1, q, s - 1, j);
+        }
+        T::load(spec, p, pol, 0, q, s, j);
+        if (carry && T::equal(tru, spec, pol)) {
+            carry = false;
+            continue;
+        }
+        ++walked;
+        carry = !WalkRerun<T>::run(p, pol, q, s, j, trace, tru, spec);
+    }
+    if (walked) {
+        atomicAdd(e.fix_segments, (unsigned long long)walked);
+        atomicMax(e.fix_rounds, walked);
+    }
 }
 
 // ================================================================================= totals

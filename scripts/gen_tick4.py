@@ -156,18 +156,23 @@ def build_stage(K, TC=8):
 
 
 
-def build_stage_f(K, TC=8):
+def build_stage_f(K, TC=8, walk=False):
     """MAGUS_SSTAGE_K<K>: one whole steady-state stage (TC ticks x 4 chains, tile loads included) of the solo
     replay kernel, balanced over the issue pipes (ALU and FMA-heavy at half rate, FP64, XU): the throttle
     test on the FP64 pipe, the tune log, scaled window count and cmd word as (predicated) IMADs, the lock /
     throttle counters as fp32 adds of 1 (exact integers, fma-lite), the level carried as a predicate
-    across the stage.  Decisions identical to MAGUS_TICK4_ASM."""
+    across the stage.  Decisions identical to MAGUS_TICK4_ASM.
+    walk=True: MAGUS_WSTAGE_K<K>, the chain walk's stage (post_kernels.cuh): two chains -- the true and the
+    speculative state of ONE trace -- stepped over the same 8 samples, passed in registers; no validation
+    maximum (the replay already took it)."""
+    C = 2 if walk else 4
     names = [(f"f{c}", "+r") for c in range(C)] + \
             [(f"r{c}_{i}", "+d") for c in range(C) for i in range(K)] + \
             [(f"evh{c}", "+r") for c in range(C)] + [(f"cnt{c}", "+r") for c in range(C)] + \
             [(f"exc{c}", "+d") for c in range(C)] + [(f"lock{c}", "+f") for c in range(C)] + \
-            [(f"nthr{c}", "+f") for c in range(C)] + [(f"wcmd{c}", "+r") for c in range(C)] + [("vmax", "+r")]
-    inames = [("tile", "r"), ("Blod", "d"), ("dinc", "d"), ("ddec", "d"), ("bitc", "r"), ("smin", "r"),
+            [(f"nthr{c}", "+f") for c in range(C)] + [(f"wcmd{c}", "+r") for c in range(C)] + \
+            ([] if walk else [("vmax", "+r")])
+    inames = ([(f"S{tt}", "r") for tt in range(TC)] if walk else [("tile", "r")]) + [("Blod", "d"), ("dinc", "d"), ("ddec", "d"), ("bitc", "r"), ("smin", "r"),
               ("one", "r"), ("mone", "r")]
     idx = {n: f"%{i}" for i, (n, _) in enumerate(names + inames)}
     R = idx.__getitem__
@@ -176,7 +181,10 @@ def build_stage_f(K, TC=8):
     for c in range(C):
         body.append(f"setp.ne.u32 phi{c}, {R(f'f{c}')}, 0;")
     for tt in range(TC):
-        body.append(f"ld.shared.v4.f32 {{D{tt * C}, D{tt * C + 1}, D{tt * C + 2}, D{tt * C + 3}}}, [{R('tile')}+{tt * 512}];")
+        if walk:
+            body += [f"mov.b32 D{tt * C + c}, {R(f'S{tt}')};" for c in range(C)]
+        else:
+            body.append(f"ld.shared.v4.f32 {{D{tt * C}, D{tt * C + 1}, D{tt * C + 2}, D{tt * C + 3}}}, [{R('tile')}+{tt * 512}];")
         per_chain = [
             "cvt.f64.f32 dd{c}, {D};",
             "setp.gt.and.f64 pthr{c}, dd{c}, {Blod}, !phi{c};",          # throttled: f_min and D > B_lo (A14)
@@ -200,8 +208,7 @@ def build_stage_f(K, TC=8):
             "add.f64 {exc}, {exc}, dx{c};",
             "@phf{c} add.f32 {lock}, {lock}, 0f3F800000;",
             "@pthr{c} add.f32 {nthr}, {nthr}, 0f3F800000;",
-            "max.u32 {vmax}, {vmax}, {D};",                              # validation (A17)
-        ]
+        ] + ([] if walk else ["max.u32 {vmax}, {vmax}, {D};"])        # validation (A17)
         for tmpl in per_chain:
             for c in range(C):
                 t = tt * C + c
@@ -210,14 +217,14 @@ def build_stage_f(K, TC=8):
                                         ddec=R("ddec"), evh=R(f"evh{c}"), one=R("one"), bitc=R("bitc"),
                                         mone=R("mone"), cnt=R(f"cnt{c}"), smin=R("smin"),
                                         wcmd=R(f"wcmd{c}"), exc=R(f"exc{c}"), lock=R(f"lock{c}"),
-                                        nthr=R(f"nthr{c}"), vmax=R("vmax")))
+                                        nthr=R(f"nthr{c}"), vmax=None if walk else R("vmax")))
     for c in range(C):
         body.append(f"selp.u32 {R(f'f{c}')}, 1, 0, phi{c};")
         for i in range(K):   # ring newest first: r_i = A_{t0 + TC - 1 - i}
             body.append(f"mov.f64 {R(f'r{c}_{i}')}, ad{(TC - 1 - i) * C + c};")
     body.append("}")
     params = ", ".join(n for n, _ in names + inames)
-    name = f"MAGUS_SSTAGE_K{K}"
+    name = f"MAGUS_{'W' if walk else 'S'}STAGE_K{K}"
     out = [f"#define {name}(...) {name}_(__VA_ARGS__)", f"#define {name}_({params}) \\", "    asm volatile( \\"]
     out += [f'        "{l}\\n\\t" \\' for l in body]
     out.append("        : " + ", ".join(f'"{c}"({n})' for n, c in names) + " \\")
@@ -234,6 +241,8 @@ out += build(False) + [""] + build(True)
 for K in (1, 2, 3):
     out += [""] + build_stage(K)
     out += [""] + build_stage_f(K)
+for K in range(1, 9):
+    out += [""] + build_stage_f(K, walk=True)
 path = os.path.join(os.path.dirname(__file__), "..", "paper_2502_03796_b200", "csrc", "tick4_asm.cuh")
 open(path, "w").write("\n".join(out) + "\n")
 print("wrote", os.path.normpath(path))
