@@ -656,10 +656,13 @@ __global__ void __launch_bounds__(32) magus_fix_lockstep_kernel(const ReplayPara
             uint32_t wcmd[2] = {0u, 0u};
             if (n == 32) {
                 LockstepStep<T>::run(st, lock, nthr, wcmd, ss, dv, pol, p, Blo_d);
-            } else {   // the ragged last block of a trace
-                for (int i = 0; i < n; ++i) {
-                    lockstep_tick<T>(st[0], dv[i], pol, p, Blo_d, wcmd[0], ss[0]);
-                    lockstep_tick<T>(st[1], dv[i], pol, p, Blo_d, wcmd[1], ss[1]);
+            } else {   // the ragged last block of a trace (static indices: dv stays in registers)
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    if (i < n) {
+                        lockstep_tick<T>(st[0], dv[i], pol, p, Blo_d, wcmd[0], ss[0]);
+                        lockstep_tick<T>(st[1], dv[i], pol, p, Blo_d, wcmd[1], ss[1]);
+                    }
                 }
             }
             const int64_t b = bt0 >> 5;

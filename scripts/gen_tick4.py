@@ -156,7 +156,7 @@ def build_stage(K, TC=8):
 
 
 
-def build_stage_f(K, TC=8, walk=False):
+def build_stage_f(K, TC=8, walk=False, traces=1):
     """MAGUS_SSTAGE_K<K>: one whole steady-state stage (TC ticks x 4 chains, tile loads included) of the solo
     replay kernel, balanced over the issue pipes (ALU and FMA-heavy at half rate, FP64, XU): the throttle
     test on the FP64 pipe, the tune log, scaled window count and cmd word as (predicated) IMADs, the lock /
@@ -165,14 +165,14 @@ def build_stage_f(K, TC=8, walk=False):
     walk=True: MAGUS_WSTAGE_K<K>, the chain walk's stage (post_kernels.cuh): two chains -- the true and the
     speculative state of ONE trace -- stepped over the same 8 samples, passed in registers; no validation
     maximum (the replay already took it)."""
-    C = 2 if walk else 4
+    C = 2 * traces if walk else 4   # walk: chains (2t, 2t+1) = (true, speculative) state of trace t
     names = [(f"f{c}", "+r") for c in range(C)] + \
             [(f"r{c}_{i}", "+d") for c in range(C) for i in range(K)] + \
             [(f"evh{c}", "+r") for c in range(C)] + [(f"cnt{c}", "+r") for c in range(C)] + \
             [(f"exc{c}", "+d") for c in range(C)] + [(f"lock{c}", "+f") for c in range(C)] + \
             [(f"nthr{c}", "+f") for c in range(C)] + [(f"wcmd{c}", "+r") for c in range(C)] + \
             ([] if walk else [("vmax", "+r")])
-    inames = ([(f"S{tt}", "r") for tt in range(TC)] if walk else [("tile", "r")]) + [("Blod", "d"), ("dinc", "d"), ("ddec", "d"), ("bitc", "r"), ("smin", "r"),
+    inames = ([(f"S{u}_{tt}", "r") for u in range(traces) for tt in range(TC)] if walk else [("tile", "r")]) + [("Blod", "d"), ("dinc", "d"), ("ddec", "d"), ("bitc", "r"), ("smin", "r"),
               ("one", "r"), ("mone", "r")]
     idx = {n: f"%{i}" for i, (n, _) in enumerate(names + inames)}
     R = idx.__getitem__
@@ -182,7 +182,7 @@ def build_stage_f(K, TC=8, walk=False):
         body.append(f"setp.ne.u32 phi{c}, {R(f'f{c}')}, 0;")
     for tt in range(TC):
         if walk:
-            body += [f"mov.b32 D{tt * C + c}, {R(f'S{tt}')};" for c in range(C)]
+            body += [f"mov.b32 D{tt * C + c}, {R(f'S{c // 2}_{tt}')};" for c in range(C)]
         else:
             body.append(f"ld.shared.v4.f32 {{D{tt * C}, D{tt * C + 1}, D{tt * C + 2}, D{tt * C + 3}}}, [{R('tile')}+{tt * 512}];")
         per_chain = [
@@ -224,7 +224,7 @@ def build_stage_f(K, TC=8, walk=False):
             body.append(f"mov.f64 {R(f'r{c}_{i}')}, ad{(TC - 1 - i) * C + c};")
     body.append("}")
     params = ", ".join(n for n, _ in names + inames)
-    name = f"MAGUS_{'W' if walk else 'S'}STAGE_K{K}"
+    name = f"MAGUS_{'W' if walk else 'S'}STAGE{'2' if traces == 2 else ''}_K{K}"
     out = [f"#define {name}(...) {name}_(__VA_ARGS__)", f"#define {name}_({params}) \\", "    asm volatile( \\"]
     out += [f'        "{l}\\n\\t" \\' for l in body]
     out.append("        : " + ", ".join(f'"{c}"({n})' for n, c in names) + " \\")

@@ -304,3 +304,25 @@ def test_full_size_sampled(M, cfg):
     # totals = fixed-order sums of the records (within 1e-9 of an exactly rounded sum)
     np.testing.assert_allclose(res.totals, PA.oracle_totals(res.per_trace), rtol=1e-9)
     print("geometry", res.geometry, "mismatched segments", res.n_mismatched_segments, "rounds", res.fixup_rounds)
+
+
+def test_cfg4_shard_sampled(M):
+    """cfg 4 as one rank of the 8-GPU run sees it (rank 5: global traces [40960, 49152) x 10^6 samples,
+    32.8 GB), in the bench's launch configuration: the oscillating class (C4) makes speculative
+    segment entries wrong through whole traces, so the chain-walk fix-up runs over ~10^6 ticks; sampled
+    traces (global ids, including both ends of the shard) must match the oracle bit-exactly on counts and
+    digests, 1e-9 on energies."""
+    c = CONFIGS[4]
+    n, ns, rank = c["per_gpu_traces"], c["n_samples"], 5
+    off = rank * n
+    tr, w = gpu_gen(M, c["seed"], n, ns, c["class_mix"], n, offset=off)
+    res = run_gpu(M, tr, w, c["policies"], n, ns, n, flags=M.F_PER_TRACE_STATS, offset=off)
+    del tr
+    rng = np.random.default_rng(4)
+    ids = np.unique(np.r_[rng.choice(n, 10, replace=False), [0, 4, 9, n - 1]])   # 4, 9: class C4 (j mod 5)
+    rec, _, _ = O.gen_replay(O.GenDesc(seed=c["seed"], n_traces=n, n_samples=ns, class_mix=c["class_mix"],
+                                       global_trace_offset=off), ids, PA.oracle_policies(c["policies"]))
+    PA.compare_records(res.per_trace[ids], rec, "cfg4-shard")
+    np.testing.assert_allclose(res.totals, PA.oracle_totals(res.per_trace), rtol=1e-9)
+    assert res.n_mismatched_segments > 0, "the shard should exercise the chain walk"
+    print("geometry", res.geometry, "mismatched segments", res.n_mismatched_segments, "rounds", res.fixup_rounds)
