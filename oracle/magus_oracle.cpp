@@ -311,4 +311,37 @@ int oracle_replay_batch(const float* trace, int32_t n_traces, int64_t n_samples,
     return used;
 }
 
+/* ========================= active savings ========================
+ * "we measure active power and energy savings, excluding idle power.  For instance, if MAGUS reduces
+ * total power consumption from 200W to 150W on a system with 100W idle power, the active power saving
+ * is (100 - 50)/100 = 50%".  Fractions (not percent), like the other savings here.
+ * Returns 0, or 1 when the baseline has no active power (p_base <= p_idle) or p < p_idle. */
+int oracle_active_saving(double p, double p_base, double p_idle, double* out) {
+    if (!(p_base > p_idle) || p < p_idle || p_idle < 0) return 1;
+    *out = ((p_base - p_idle) - (p - p_idle)) / (p_base - p_idle);
+    return 0;
+}
+
+/* Job-level active savings of a policy against a baseline over the same n traces (A29):
+ * mean powers P = sum(E)/sum(T), P_b = sum(E_b)/sum(T_b); active energies E_a = sum(E) - p_idle*sum(T),
+ * E_a,b = sum(E_b) - p_idle*sum(T_b).  out = {active power saving, active energy saving,
+ * active EDP saving} = {oracle_active_saving(P, P_b, p_idle), 1 - E_a/E_a,b,
+ * 1 - (E_a*sum(T))/(E_a,b*sum(T_b))}.  Plain running sums in index order. */
+int oracle_active_savings_job(const double* E, const double* T, const double* E_b, const double* T_b, int64_t n,
+                              double p_idle, double out[3]) {
+    double sE = 0, sT = 0, sEb = 0, sTb = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        sE += E[i];
+        sT += T[i];
+        sEb += E_b[i];
+        sTb += T_b[i];
+    }
+    if (!(sT > 0) || !(sTb > 0)) return 1;
+    if (oracle_active_saving(sE / sT, sEb / sTb, p_idle, &out[0])) return 1;
+    const double Ea = sE - p_idle * sT, Eab = sEb - p_idle * sTb;
+    out[1] = 1.0 - Ea / Eab;
+    out[2] = 1.0 - (Ea * sT) / (Eab * sTb);
+    return 0;
+}
+
 } /* extern "C" */

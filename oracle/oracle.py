@@ -75,6 +75,11 @@ def lib():
         L.oracle_pkg_power_at.argtypes = [C.c_double, C.POINTER(OModel)]
         L.oracle_digest.restype = C.c_uint64
         L.oracle_digest.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
+        L.oracle_active_saving.restype = C.c_int
+        L.oracle_active_saving.argtypes = [C.c_double, C.c_double, C.c_double, C.POINTER(C.c_double)]
+        L.oracle_active_savings_job.restype = C.c_int
+        L.oracle_active_savings_job.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+                                                C.c_double, C.POINTER(C.c_double)]
         L.oracle_replay.restype = C.c_int
         L.oracle_replay.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_float, C.POINTER(OPolicy),
                                     C.POINTER(OModel), C.c_void_p, C.c_void_p, C.c_int64]
@@ -179,6 +184,23 @@ def digest(cmd_hi, events) -> int:
     c = np.ascontiguousarray(cmd_hi, dtype=np.uint8)
     e = np.ascontiguousarray(events, dtype=np.uint8)
     return int(lib().oracle_digest(c.ctypes.data, e.ctypes.data, len(c)))
+
+
+def active_saving(p: float, p_base: float, p_idle: float) -> float:
+    """P:399 active power saving (fraction); ValueError if the baseline has no active power or p < p_idle."""
+    out = C.c_double()
+    if lib().oracle_active_saving(p, p_base, p_idle, C.byref(out)):
+        raise ValueError("no active power in baseline, or power below idle")
+    return out.value
+
+
+def active_savings_job(E, T, E_base, T_base, p_idle: float):
+    """Job-level (active power, active energy, active EDP) savings, A29."""
+    arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in (E, T, E_base, T_base)]
+    out = (C.c_double * 3)()
+    if lib().oracle_active_savings_job(*[a.ctypes.data for a in arrs], len(arrs[0]), p_idle, out):
+        raise ValueError("no active power in baseline, or power below idle")
+    return tuple(out)
 
 
 def replay(D, w: float, policy: Policy, model: Model | None = None, codes: bool = False):

@@ -392,3 +392,40 @@ def test_digest_definition():
         assert O.digest(c2, ev) != d
         e2 = ev.copy(); e2[t] ^= 1
         assert O.digest(cmd, e2) != d
+
+
+# --------------------------------------------------------------------------- NEXT-4: active savings
+
+def test_active_saving_paper_example():
+    """P:401 worked example: total power 200 W -> 150 W with 100 W idle power is a 50% active saving."""
+    g = json.load(open(os.path.join(GOLD, "paper_numbers.json")))["active_power_example"]
+    assert O.active_saving(g["p"], g["p_base_w"], g["p_idle_w"]) == g["active_saving"]
+
+
+def test_active_saving_properties():
+    """p_idle = 0 reduces to the plain power saving; p = p_base gives 0; a common positive
+    rescaling of the watts changes nothing (powers of two: exact); a baseline without active power or a power
+    below idle is an error."""
+    for p, pb in ((150.0, 200.0), (87.5, 287.0), (300.0, 250.0)):
+        assert O.active_saving(p, pb, 0.0) == pytest.approx(1 - p / pb, rel=1e-15)
+        assert O.active_saving(pb, pb, 30.0) == 0.0
+        assert O.active_saving(4 * p, 4 * pb, 4 * 30.0) == O.active_saving(p, pb, 30.0)
+    with pytest.raises(ValueError):
+        O.active_saving(150.0, 100.0, 100.0)
+    with pytest.raises(ValueError):
+        O.active_saving(90.0, 200.0, 100.0)
+
+
+def test_active_savings_job_hand_example():
+    """DESIGN.md A29 on a two-trace job, derived by hand in exact rationals: E = [100, 300] J, T = [1, 2] s;
+    baseline E_b = [150, 400] J, T_b = [1, 1.5] s; 50 W idle.  Mean powers 400/3 and 220 W; active energies
+    400 - 150 = 250 J and 550 - 125 = 425 J."""
+    from fractions import Fraction as F
+    P, Pb, Ea, Eab = F(400, 3), F(220), F(250), F(425)
+    want = (float((Pb - P) / (Pb - 50)), float(1 - Ea / Eab), float(1 - (Ea * 3) / (Eab * F(5, 2))))
+    got = O.active_savings_job([100, 300], [1, 2], [150, 400], [1, 1.5], 50.0)
+    assert got == pytest.approx(want, rel=1e-14)
+    # with no idle power the active savings are the plain job-level power / energy / EDP savings
+    got0 = O.active_savings_job([100, 300], [1, 2], [150, 400], [1, 1.5], 0.0)
+    assert got0 == pytest.approx((float(1 - P / Pb), float(1 - F(400, 550)), float(1 - F(400 * 3) / F(550 * 5, 2))),
+                                 rel=1e-14)
