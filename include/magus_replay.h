@@ -207,6 +207,20 @@ const char*  magus_last_error(void);   /* errors of calls that have no handle (c
 magus_status magus_derive_thresholds(const magus_policy* p, const magus_model* m,
                                      double out_d[5], float out_f[4], int32_t out_i[1]);
 
+/* Host-only (no GPU needed), NEXT-4 (A29): job-level savings of policy
+ * `policy` against policy `baseline` with the system's idle power p_idle_w (W) excluded, from the per-policy
+ * totals of magus_replay_results (policy_totals[n_policies][MAGUS_N_TOTALS]; the job = every trace of every
+ * rank).  With mean powers P = E/T and P_b = E_b/T_b of the two policies and active energies
+ * E_a = E - p_idle_w*T, E_a,b = E_b - p_idle_w*T_b:
+ *   out[0] = ((P_b - p_idle_w) - (P - p_idle_w)) / (P_b - p_idle_w)   active power saving
+ *   out[1] = 1 - E_a / E_a,b                                          active energy saving
+ *   out[2] = 1 - (E_a * T) / (E_a,b * T_b)                            active EDP saving
+ * (fractions).  MAGUS_ERR_INVALID_ARG: NULL pointers, indices outside [0, n_policies), p_idle_w < 0, a
+ * non-positive total time, a baseline without active power (P_b <= p_idle_w) or P < p_idle_w;
+ * out is left untouched then. */
+magus_status magus_active_savings(const double* policy_totals, int32_t n_policies, int32_t policy,
+                                  int32_t baseline, double p_idle_w, double out[3]);
+
 int32_t magus_abi_version(void);
 
 /* Diagnostics: the current launch plan: out = {n_segments, segment_len, warmup_ticks,

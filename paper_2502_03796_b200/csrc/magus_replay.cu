@@ -464,6 +464,29 @@ extern "C" const char* magus_replay_last_error(const magus_replay_t* h) {
     return h ? h->err.c_str() : g_error.c_str();
 }
 
+// NEXT-4: active savings of a policy against a baseline from the job's per-policy totals.
+extern "C" magus_status magus_active_savings(const double* tot, int32_t n_policies, int32_t policy, int32_t baseline,
+                                             double p_idle_w, double out[3]) {
+    if (!tot || !out) return fail(nullptr, MAGUS_ERR_INVALID_ARG, "magus_active_savings: NULL argument");
+    if (policy < 0 || policy >= n_policies || baseline < 0 || baseline >= n_policies)
+        return fail(nullptr, MAGUS_ERR_INVALID_ARG, "magus_active_savings: policy index outside [0, n_policies)");
+    const double E = tot[(size_t)policy * MAGUS_N_TOTALS + MAGUS_TOT_E];
+    const double T = tot[(size_t)policy * MAGUS_N_TOTALS + MAGUS_TOT_T];
+    const double Eb = tot[(size_t)baseline * MAGUS_N_TOTALS + MAGUS_TOT_E];
+    const double Tb = tot[(size_t)baseline * MAGUS_N_TOTALS + MAGUS_TOT_T];
+    if (!(T > 0.0) || !(Tb > 0.0)) return fail(nullptr, MAGUS_ERR_INVALID_ARG, "magus_active_savings: zero total time");
+    if (!(p_idle_w >= 0.0)) return fail(nullptr, MAGUS_ERR_INVALID_ARG, "magus_active_savings: p_idle_w must be >= 0");
+    const double P = E / T, Pb = Eb / Tb;
+    if (!(Pb > p_idle_w)) return fail(nullptr, MAGUS_ERR_INVALID_ARG, "magus_active_savings: no active power in baseline");
+    if (P < p_idle_w) return fail(nullptr, MAGUS_ERR_INVALID_ARG, "magus_active_savings: mean power below idle power");
+    const double active = Pb - p_idle_w;                        // the baseline's active power
+    const double Ea = E - p_idle_w * T, Eab = Eb - p_idle_w * Tb;   // active energies
+    out[0] = (active - (P - p_idle_w)) / active;
+    out[1] = 1.0 - Ea / Eab;
+    out[2] = 1.0 - (Ea * T) / (Eab * Tb);
+    return MAGUS_OK;
+}
+
 extern "C" magus_status magus_derive_thresholds(const magus_policy* p, const magus_model* m, double out_d[5],
                                                 float out_f[4], int32_t out_i[1]) {
     if (!p || !m || !out_d || !out_f || !out_i) return fail(nullptr, MAGUS_ERR_INVALID_ARG, "NULL argument");

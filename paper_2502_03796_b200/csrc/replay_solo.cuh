@@ -21,7 +21,10 @@ namespace magus {
 #define MAGUS_SOLO_UNROLL 1
 #endif
 
-constexpr int kSoloCtasPerSm = 16;   // 16 one-warp CTAs per SM: 128 registers and ~12.3 KB smem each
+#ifndef MAGUS_SOLO_CTAS_PER_SM
+#define MAGUS_SOLO_CTAS_PER_SM 16
+#endif
+constexpr int kSoloCtasPerSm = MAGUS_SOLO_CTAS_PER_SM;   // 16 one-warp CTAs per SM: 128 registers and ~12.3 KB smem each
 
 template <int TC, int NSTAGE>
 struct SoloSmem {

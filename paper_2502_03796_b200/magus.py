@@ -109,6 +109,9 @@ lib.magus_replay_timing_summary.restype = _S
 lib.magus_replay_timing_summary.argtypes = [C.c_void_p, C.c_int32, C.POINTER(C.c_float)]
 lib.magus_replay_destroy.restype = None
 lib.magus_replay_destroy.argtypes = [C.c_void_p]
+lib.magus_active_savings.restype = _S
+lib.magus_active_savings.argtypes = [C.POINTER(C.c_double), C.c_int32, C.c_int32, C.c_int32, C.c_double,
+                                     C.POINTER(C.c_double)]
 lib.magus_derive_thresholds.restype = _S
 lib.magus_derive_thresholds.argtypes = [C.POINTER(c_policy), C.POINTER(c_model), C.POINTER(C.c_double),
                                         C.POINTER(C.c_float), C.POINTER(C.c_int32)]
@@ -186,6 +189,16 @@ def derive_thresholds(policy: Policy, model: Model):
     _check(lib.magus_derive_thresholds(C.byref(policy.c()), C.byref(model.c()), d, f, i))
     return dict(dinc=d[0], ddec=d[1], L=d[2], P_lo=d[3], P_hi=d[4], B_lo=f[0], B_hi=f[1], astar_lo=f[2],
                 astar_hi=f[3], s_min=i[0])
+
+
+def active_savings(policy_totals, policy: int, baseline: int, p_idle_w: float):
+    """Host-only, NEXT-4: (active power, active energy, active EDP) savings of `policy` against
+    `baseline` with the idle power excluded, from Results.totals ([n_policies][N_TOTALS])."""
+    t = np.ascontiguousarray(policy_totals, dtype=np.float64)
+    out = (C.c_double * 3)()
+    _check(lib.magus_active_savings(t.ctypes.data_as(C.POINTER(C.c_double)), t.shape[0], policy, baseline,
+                                    p_idle_w, out))
+    return tuple(out)
 
 
 def nccl_unique_id() -> bytes:

@@ -126,3 +126,26 @@ def test_default_model_constants():
     t = M.derive_thresholds(M.Policy(), M.Model())
     assert t["B_lo"] == float(np.float32(20 * (0.8 / 2.2))) and t["B_hi"] == 20.0
     assert (t["P_lo"], t["P_hi"]) == (116.0, 200.0)
+
+
+def test_active_savings_host_matches_oracle():
+    """NEXT-4: magus_active_savings on synthetic per-policy totals equals the oracle's job-level
+    active savings (one trace per policy, so the job sums are the totals); errors as SPEC.md:435 says."""
+    from oracle import oracle as O
+    rng = np.random.default_rng(7)
+    for _ in range(50):
+        tot = np.zeros((3, M.N_TOTALS))
+        tot[:, 0] = rng.uniform(100.0, 5000.0, 3)          # E
+        tot[:, 2] = rng.uniform(1.0, 20.0, 3)              # T
+        P = tot[:, 0] / tot[:, 2]
+        p_idle = float(rng.uniform(0.0, 0.9) * min(P))
+        for pol, base in ((0, 1), (2, 1), (1, 1)):
+            got = M.active_savings(tot, pol, base, p_idle)
+            want = O.active_savings_job([tot[pol, 0]], [tot[pol, 2]], [tot[base, 0]], [tot[base, 2]], p_idle)
+            assert got == pytest.approx(want, rel=1e-12, abs=1e-15)
+    tot = np.zeros((2, M.N_TOTALS))
+    tot[:, 0], tot[:, 2] = (150.0, 200.0), (1.0, 1.0)
+    assert M.active_savings(tot, 0, 1, 100.0)[0] == 0.5          # the paper's example, P:401
+    for bad in ((0, 1, 250.0), (0, 2, 10.0), (0, 1, -1.0), (0, 1, 160.0)):
+        with pytest.raises(M.MagusError):
+            M.active_savings(tot, *bad)

@@ -326,3 +326,17 @@ def test_cfg4_shard_sampled(M):
     np.testing.assert_allclose(res.totals, PA.oracle_totals(res.per_trace), rtol=1e-9)
     assert res.n_mismatched_segments > 0, "the shard should exercise the chain walk"
     print("geometry", res.geometry, "mismatched segments", res.n_mismatched_segments, "rounds", res.fixup_rounds)
+
+
+def test_active_savings_from_gpu_totals(M):
+    """NEXT-4: active power / energy / EDP savings of MAGUS against the static-max baseline from
+    the GPU run's per-policy totals, with the paper's single-GPU (30 W) and 4-GPU (200 W) idle powers
+    (P:397), equal the oracle's job-level active savings from its own per-trace records (1e-9)."""
+    c = SMALL["cfg2-small"]
+    tr, w = gpu_gen(M, c["seed"], c["n"], c["ns"], c["mix"])
+    res = run_gpu(M, tr, w, c["policies"], c["n"], c["ns"], (c["n"] + 3) // 4 * 4, flags=M.F_PER_TRACE_STATS)
+    rec, _ = oracle_run(tr.cpu().numpy(), w.cpu().numpy(), c["policies"], c["n"])
+    for p_idle in (30.0, 200.0):
+        got = M.active_savings(res.totals, 0, 1, p_idle)
+        want = O.active_savings_job(rec["E"][:, 0], rec["T"][:, 0], rec["E"][:, 1], rec["T"][:, 1], p_idle)
+        np.testing.assert_allclose(got, want, rtol=1e-9, atol=1e-12)
