@@ -137,16 +137,18 @@ ReplayKernel replay_kernel_for(int key) {
 
 // one-warp-CTA replay kernel (replay_solo.cuh) of a chain kind, or nullptr if it has none
 ReplayKernel solo_kernel_for(int key) {
-    const bool bal = env_int("MAGUS_SOLO_BAL", 1) != 0;
+    const int v = env_int("MAGUS_SOLO_BAL", 2);   // stage block variant (replay_solo.cuh)
+#define SOLO_K(KK)                                                                                               \
+    (v == 0   ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 0>                    \
+     : v == 2 ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 2>                    \
+              : (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 1>)
     switch (key) {
-        case 1: return bal ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<1, false>, kTC, kNStage, true>
-                           : (ReplayKernel)magus_replay_solo_kernel<MagusTicker<1, false>, kTC, kNStage, false>;
-        case 2: return bal ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<2, false>, kTC, kNStage, true>
-                           : (ReplayKernel)magus_replay_solo_kernel<MagusTicker<2, false>, kTC, kNStage, false>;
-        case 3: return bal ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<3, false>, kTC, kNStage, true>
-                           : (ReplayKernel)magus_replay_solo_kernel<MagusTicker<3, false>, kTC, kNStage, false>;
+        case 1: return SOLO_K(1);
+        case 2: return SOLO_K(2);
+        case 3: return SOLO_K(3);
         default: return nullptr;
     }
+#undef SOLO_K
 }
 
 // one replay launch: the lane policies [q_base, q_base + nq) share a chain kind

@@ -70,10 +70,11 @@ __device__ __forceinline__ void solo_issue(uint32_t tile, const CUtensorMap* tma
 // run constants of the pipe-balanced stage block (MAGUS_SSTAGE_K<K>, tick4_asm.cuh)
 struct SoloConst {
     double Blo_d;   // B_lo as fp64
+    float B_lo;
 };
 
 // One whole steady-state stage (8 ticks x 4 chains) of MAGUS chains with a register ring of K <= 3 values.
-template <int K>
+template <int K, bool THR32 = false>
 __device__ __forceinline__ void solo_stage(MagusState<K, false>* s, float* lock, float* nthr,
                                            uint32_t* wcmd, SegStats* ss, uint32_t& vmax, uint32_t tile,
                                            const SoloConst& sc, const DevPolicy& pol) {
@@ -83,17 +84,31 @@ __device__ __forceinline__ void solo_stage(MagusState<K, false>* s, float* lock,
     e0, e1, e2, e3, s[0].cnt, s[1].cnt, s[2].cnt, s[3].cnt, ss[0].sexc, ss[1].sexc, ss[2].sexc, ss[3].sexc, lock[0],    \
         lock[1], lock[2], lock[3], nthr[0], nthr[1], nthr[2], nthr[3], wcmd[0], wcmd[1], wcmd[2], wcmd[3], vmax, \
         tile, sc.Blo_d, pol.dinc, pol.ddec, bitc, pol.smin_sc, pol.one, mone
+#define SOLO_TAILF                                                                                             \
+    e0, e1, e2, e3, s[0].cnt, s[1].cnt, s[2].cnt, s[3].cnt, ss[0].sexc, ss[1].sexc, ss[2].sexc, ss[3].sexc, lock[0], \
+        lock[1], lock[2], lock[3], nthr[0], nthr[1], nthr[2], nthr[3], wcmd[0], wcmd[1], wcmd[2], wcmd[3], vmax,   \
+        tile, sc.B_lo, sc.Blo_d, pol.dinc, pol.ddec, bitc, pol.smin_sc, pol.one, mone
 #define SOLO_F s[0].f, s[1].f, s[2].f, s[3].f
-    if constexpr (K == 1) {
-        MAGUS_SSTAGE_K1(SOLO_F, s[0].ring.v[0], s[1].ring.v[0], s[2].ring.v[0], s[3].ring.v[0], SOLO_TAIL);
-    } else if constexpr (K == 2) {
-        MAGUS_SSTAGE_K2(SOLO_F, s[0].ring.v[0], s[0].ring.v[1], s[1].ring.v[0], s[1].ring.v[1], s[2].ring.v[0],
-                        s[2].ring.v[1], s[3].ring.v[0], s[3].ring.v[1], SOLO_TAIL);
+#define SOLO_R1 s[0].ring.v[0], s[1].ring.v[0], s[2].ring.v[0], s[3].ring.v[0]
+#define SOLO_R2                                                                                                \
+    s[0].ring.v[0], s[0].ring.v[1], s[1].ring.v[0], s[1].ring.v[1], s[2].ring.v[0], s[2].ring.v[1], s[3].ring.v[0], \
+        s[3].ring.v[1]
+#define SOLO_R3                                                                                                \
+    s[0].ring.v[0], s[0].ring.v[1], s[0].ring.v[2], s[1].ring.v[0], s[1].ring.v[1], s[1].ring.v[2], s[2].ring.v[0], \
+        s[2].ring.v[1], s[2].ring.v[2], s[3].ring.v[0], s[3].ring.v[1], s[3].ring.v[2]
+    if constexpr (THR32) {   // throttle test as an fp32 compare on the ALU pipe (less FP64 work, less power)
+        if constexpr (K == 1) MAGUS_SSTAGEF_K1(SOLO_F, SOLO_R1, SOLO_TAILF);
+        else if constexpr (K == 2) MAGUS_SSTAGEF_K2(SOLO_F, SOLO_R2, SOLO_TAILF);
+        else MAGUS_SSTAGEF_K3(SOLO_F, SOLO_R3, SOLO_TAILF);
     } else {
-        MAGUS_SSTAGE_K3(SOLO_F, s[0].ring.v[0], s[0].ring.v[1], s[0].ring.v[2], s[1].ring.v[0], s[1].ring.v[1],
-                        s[1].ring.v[2], s[2].ring.v[0], s[2].ring.v[1], s[2].ring.v[2], s[3].ring.v[0],
-                        s[3].ring.v[1], s[3].ring.v[2], SOLO_TAIL);
+        if constexpr (K == 1) MAGUS_SSTAGE_K1(SOLO_F, SOLO_R1, SOLO_TAIL);
+        else if constexpr (K == 2) MAGUS_SSTAGE_K2(SOLO_F, SOLO_R2, SOLO_TAIL);
+        else MAGUS_SSTAGE_K3(SOLO_F, SOLO_R3, SOLO_TAIL);
     }
+#undef SOLO_TAILF
+#undef SOLO_R1
+#undef SOLO_R2
+#undef SOLO_R3
 #undef SOLO_TAIL
 #undef SOLO_F
     s[0].evh = e0;
@@ -102,8 +117,9 @@ __device__ __forceinline__ void solo_stage(MagusState<K, false>* s, float* lock,
     s[3].evh = e3;
 }
 
-// BAL: the pipe-balanced stage block (MAGUS_SSTAGE_K<K>); else the integer one (MAGUS_STAGE8_K<K>)
-template <class T, int TC, int NSTAGE, bool BAL>
+// BAL: 0 = the integer stage block (MAGUS_STAGE8_K<K>), 1 = the pipe-balanced one (MAGUS_SSTAGE_K<K>),
+// 2 = balanced with the throttle test on the ALU pipe (MAGUS_SSTAGEF_K<K>)
+template <class T, int TC, int NSTAGE, int BAL>
 __global__ void __launch_bounds__(32, kSoloCtasPerSm)
     magus_replay_solo_kernel(const __grid_constant__ CUtensorMap tmap, const ReplayParams p) {
     static_assert(T::kHasStage8 && TC == 8, "solo kernel: whole-stage PTX block of 8 ticks");
@@ -144,6 +160,7 @@ __global__ void __launch_bounds__(32, kSoloCtasPerSm)
     const float B_lo = p.B_lo, B_hi = p.B_hi;
     SoloConst sc;
     sc.Blo_d = (double)B_lo;
+    sc.B_lo = B_lo;
     const double Blo_d = sc.Blo_d;
     const int k = pol.k, C = pol.C;
     // ticks before Alg. 1 / 2 are fully defined (A7, A8).  Speculative segments (seg > 0) may instead start
@@ -218,7 +235,9 @@ __global__ void __launch_bounds__(32, kSoloCtasPerSm)
             for (int sub = 0; sub < 32 / TC; ++sub) {
                 const uint32_t tile = tile0 + slot * kTileBytes;
                 mbar_wait_loop(bar0 + 8 * slot, phase);
-                if constexpr (BAL) solo_stage(st, lockf, nthrf, wcmd, ss, vmax, tile + lane_off, sc, pol);
+                if constexpr (BAL == 1) solo_stage(st, lockf, nthrf, wcmd, ss, vmax, tile + lane_off, sc, pol);
+                else if constexpr (BAL == 2)
+                    solo_stage<T::kRingK, true>(st, lockf, nthrf, wcmd, ss, vmax, tile + lane_off, sc, pol);
                 else T::stage8(st, tile + lane_off, pol, B_lo, Blo_d, wcmd, ss, vmax);
                 __syncwarp();   // every lane's tile reads are complete before the slot is refilled
                 if (i + NSTAGE < G.n_stages)

@@ -13,6 +13,7 @@ struct MagusTicker {
     using LogT = typename LogWord<LOG64>::T;
     static constexpr bool kStateful = true;
     static constexpr bool kWarmupRules = true;   // Alg. 1 needs k+1 samples, Alg. 2 a full log
+    static constexpr int kRingK = K;
 
     __device__ __forceinline__ static void init(State& s, const DevPolicy& pol, bool exact_start) {
         s.f = exact_start ? (uint32_t)pol.f0 : (uint32_t)pol.guess_f;

@@ -5,7 +5,7 @@ TAG=$1; shift
 OUT=gpurun_out; mkdir -p $OUT
 timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider -x > $OUT/${TAG}_pytest_gpu.log 2>&1
 echo "pytest rc=$?" >> $OUT/${TAG}_pytest_gpu.log
-for rep in 1 2 3; do
+for rep in 1 2 3 4; do
   for v in "$@"; do
     name=${v%%=*}; envs=${v#*=}
     env $envs timeout 300 python bench.py --no-e2e --no-cpu-baseline --steps 30 --preroll-ms 300 \

@@ -156,7 +156,7 @@ def build_stage(K, TC=8):
 
 
 
-def build_stage_f(K, TC=8, walk=False, traces=1):
+def build_stage_f(K, TC=8, walk=False, traces=1, thr64=True):
     """MAGUS_SSTAGE_K<K>: one whole steady-state stage (TC ticks x 4 chains, tile loads included) of the solo
     replay kernel, balanced over the issue pipes (ALU and FMA-heavy at half rate, FP64, XU): the throttle
     test on the FP64 pipe, the tune log, scaled window count and cmd word as (predicated) IMADs, the lock /
@@ -172,7 +172,8 @@ def build_stage_f(K, TC=8, walk=False, traces=1):
             [(f"exc{c}", "+d") for c in range(C)] + [(f"lock{c}", "+f") for c in range(C)] + \
             [(f"nthr{c}", "+f") for c in range(C)] + [(f"wcmd{c}", "+r") for c in range(C)] + \
             ([] if walk else [("vmax", "+r")])
-    inames = ([(f"S{u}_{tt}", "r") for u in range(traces) for tt in range(TC)] if walk else [("tile", "r")]) + [("Blod", "d"), ("dinc", "d"), ("ddec", "d"), ("bitc", "r"), ("smin", "r"),
+    inames = ([(f"S{u}_{tt}", "r") for u in range(traces) for tt in range(TC)] if walk else [("tile", "r")]) + \
+             ([] if thr64 else [("Blo", "f")]) + [("Blod", "d"), ("dinc", "d"), ("ddec", "d"), ("bitc", "r"), ("smin", "r"),
               ("one", "r"), ("mone", "r")]
     idx = {n: f"%{i}" for i, (n, _) in enumerate(names + inames)}
     R = idx.__getitem__
@@ -187,7 +188,8 @@ def build_stage_f(K, TC=8, walk=False, traces=1):
             body.append(f"ld.shared.v4.f32 {{D{tt * C}, D{tt * C + 1}, D{tt * C + 2}, D{tt * C + 3}}}, [{R('tile')}+{tt * 512}];")
         per_chain = [
             "cvt.f64.f32 dd{c}, {D};",
-            "setp.gt.and.f64 pthr{c}, dd{c}, {Blod}, !phi{c};",          # throttled: f_min and D > B_lo (A14)
+            ("setp.gt.and.f64 pthr{c}, dd{c}, {Blod}, !phi{c};" if thr64  # throttled: f_min and D > B_lo (A14)
+             else "setp.gt.and.f32 pthr{c}, {D}, {Blo}, !phi{c};"),
             "selp.f64 {ad}, {Blod}, dd{c}, pthr{c};",                    # A = min(D, B[f]) as fp64 (exact)
             "sub.f64 dv{c}, {ad}, {old};",                               # Alg. 1 numerator A_t - A_{t-k}
             "setp.gt.f64 pinc{c}, dv{c}, {dinc};",                       # +1
@@ -214,6 +216,7 @@ def build_stage_f(K, TC=8, walk=False, traces=1):
                 t = tt * C + c
                 old = f"ad{(tt - K) * C + c}" if tt >= K else R(f"r{c}_{K - 1 - tt}")
                 body.append(tmpl.format(c=c, D=f"D{t}", ad=f"ad{t}", old=old, Blod=R("Blod"), dinc=R("dinc"),
+                                        Blo=None if thr64 else R("Blo"),
                                         ddec=R("ddec"), evh=R(f"evh{c}"), one=R("one"), bitc=R("bitc"),
                                         mone=R("mone"), cnt=R(f"cnt{c}"), smin=R("smin"),
                                         wcmd=R(f"wcmd{c}"), exc=R(f"exc{c}"), lock=R(f"lock{c}"),
@@ -224,7 +227,7 @@ def build_stage_f(K, TC=8, walk=False, traces=1):
             body.append(f"mov.f64 {R(f'r{c}_{i}')}, ad{(TC - 1 - i) * C + c};")
     body.append("}")
     params = ", ".join(n for n, _ in names + inames)
-    name = f"MAGUS_{'W' if walk else 'S'}STAGE{'2' if traces == 2 else ''}_K{K}"
+    name = f"MAGUS_{'W' if walk else 'S'}STAGE{'2' if traces == 2 else ''}{'' if thr64 else 'F'}_K{K}"
     out = [f"#define {name}(...) {name}_(__VA_ARGS__)", f"#define {name}_({params}) \\", "    asm volatile( \\"]
     out += [f'        "{l}\\n\\t" \\' for l in body]
     out.append("        : " + ", ".join(f'"{c}"({n})' for n, c in names) + " \\")
@@ -241,6 +244,7 @@ out += build(False) + [""] + build(True)
 for K in (1, 2, 3):
     out += [""] + build_stage(K)
     out += [""] + build_stage_f(K)
+    out += [""] + build_stage_f(K, thr64=False)
 for K in range(1, 9):
     out += [""] + build_stage_f(K, walk=True)
 path = os.path.join(os.path.dirname(__file__), "..", "paper_2502_03796_b200", "csrc", "tick4_asm.cuh")

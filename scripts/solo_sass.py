@@ -12,7 +12,7 @@ K = sys.argv[2] if len(sys.argv) > 2 else "1"
 BAL = sys.argv[3] if len(sys.argv) > 3 else "1"   # 1: the pipe-balanced stage variant
 sass = subprocess.run(["cuobjdump", "-sass", obj], capture_output=True, text=True).stdout
 funcs = re.split(r"\n\s+Function : ", sass)
-f = [x for x in funcs if x.startswith(f"_ZN5magus24magus_replay_solo_kernelINS_11MagusTickerILi{K}ELb0EEELi8ELi3ELb{BAL}")][0]
+f = [x for x in funcs if x.startswith(f"_ZN5magus24magus_replay_solo_kernelINS_11MagusTickerILi{K}ELb0EEELi8ELi3ELi{BAL}")][0]
 ins = []
 for l in f.split("\n"):
     m = re.match(r"\s+/\*([0-9a-f]{4,})\*/\s+(.*?);", l)
