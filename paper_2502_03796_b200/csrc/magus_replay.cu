@@ -37,7 +37,6 @@ constexpr int kTC = MAGUS_TC;        // ticks per TMA stage ([TC x 128] fp32 til
 constexpr int kNStage = MAGUS_NSTAGE;  // stages per tile group
 using Smem = ReplaySmem<kTC, kNStage>;
 typedef void (*ReplayKernel)(CUtensorMap, ReplayParams);
-typedef void (*RerunKernel)(ReplayParams, EpiParams, FixParams, int, int, int, int, const float*);
 
 // chain kind of a lane policy -> its kernel instantiation (one register allocation per kind)
 int ticker_key(const DevPolicy& q) {
@@ -96,20 +95,6 @@ WalkKernel walk_kernel_for(int key) {
         case 1000 + LANE_STATIC_MIN: return nullptr;
         case 1000 + LANE_VALIDATE: return nullptr;
         default: return key >= 100 ? magus_fix_walk_kernel<MagusTicker<0, true>> : magus_fix_walk_kernel<MagusTicker<0, false>>;
-    }
-}
-
-// fix-up re-run kernel for a chain kind (nullptr: stateless kinds never mismatch)
-RerunKernel rerun_kernel_for(int key) {
-    switch (key) {
-        case 1: return magus_fix_rerun_kernel<MagusTicker<1, false>>;
-        case 2: return magus_fix_rerun_kernel<MagusTicker<2, false>>;
-        case 4: return magus_fix_rerun_kernel<MagusTicker<4, false>>;
-        case 8: return magus_fix_rerun_kernel<MagusTicker<8, false>>;
-        case 1000 + LANE_TDP: return magus_fix_rerun_kernel<TdpTicker>;
-        case 1000 + LANE_STATIC_MIN: return nullptr;
-        case 1000 + LANE_VALIDATE: return nullptr;
-        default: return key >= 100 ? magus_fix_rerun_kernel<MagusTicker<0, true>> : magus_fix_rerun_kernel<MagusTicker<0, false>>;
     }
 }
 
@@ -378,9 +363,6 @@ struct magus_replay {
     EpiParams ep{};
     std::vector<LaunchGroup> groups;
     FixParams fx{};
-    uint32_t* d_wl_count = nullptr;   // [2][G] + cursors [G] + any_unresolved (one allocation)
-    int fix_rounds = 2;
-    bool walk_fix = true;             // chain-walk fix-up (else worklist rounds + serial fallback)
     int n_sm = 148;
     int alloc_segments = 1;           // scratch is sized for this many segments (re-plans only shrink)
     int replans = 0;
@@ -819,47 +801,14 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
     if ((d.flags & MAGUS_F_DUMP_DECISIONS) && d.dump_n_traces > 0 && d.n_samples > 0) {
         ALLOC(h->d_codes, (size_t)d.n_samples * d.dump_n_traces * d.n_policies);
     }
-    {   // fix-up worklists
-        const int G = (int)h->groups.size();
-        std::vector<int32_t> grp_of_lane(Q), first(G);
-        std::vector<int64_t> off(G);
-        int64_t total = 0;
-        for (int g = 0; g < G; ++g) {
-            first[g] = h->groups[g].q_base;
-            off[g] = total;
-            for (int q = h->groups[g].q_base; q < h->groups[g].q_base + h->groups[g].nq; ++q) grp_of_lane[q] = g;
-            total += (int64_t)h->groups[g].nq * std::max(0, S - 1) * std::max(1, d.n_traces);
-        }
-        int32_t* d_gol;
-        int32_t* d_first;
-        int64_t* d_off;
-        ALLOC(d_gol, Q);
-        ALLOC(d_first, G);
-        ALLOC(d_off, G);
-        ALLOC(h->fx.wl, (size_t)2 * std::max<int64_t>(1, total));
-        ALLOC(h->d_wl_count, (size_t)3 * G + 1);
-        ALLOC(h->fx.unresolved, (size_t)Q * std::max(1, d.n_traces));
+    {   // chain-walk fix-up
         ALLOC(h->fx.first_bad, (size_t)Q * std::max(1, d.n_traces));
         {   // INT_MAX ("no wrong entry") between runs: the walk kernel restores what it reads
             std::vector<int32_t> inf((size_t)Q * std::max(1, d.n_traces), 0x7FFFFFFF);
             cudaMemcpy(h->fx.first_bad, inf.data(), inf.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
         }
-        cudaMemcpy(d_gol, grp_of_lane.data(), Q * sizeof(int32_t), cudaMemcpyHostToDevice);
-        cudaMemcpy(d_first, first.data(), G * sizeof(int32_t), cudaMemcpyHostToDevice);
-        cudaMemcpy(d_off, off.data(), G * sizeof(int64_t), cudaMemcpyHostToDevice);
-        h->fx.n_fgroups = G;
-        h->fx.cap_total = (int32_t)std::max<int64_t>(1, total);
-        h->fx.grp_of_lane = d_gol;
-        h->fx.grp_first_lane = d_first;
-        h->fx.grp_off = d_off;
-        h->fx.wl_count = h->d_wl_count;
-        h->fx.wl_cursor = h->d_wl_count + 2 * G;
-        h->fx.any_unresolved = h->d_wl_count + 3 * G;
-        h->fix_rounds = std::max(1, env_int("MAGUS_FIX_ROUNDS", 1));
-        h->walk_fix = env_int("MAGUS_FIX_WALK", 1) != 0;
         h->replan_frac = env_int("MAGUS_REPLAN_PCT", 101) / 100.0;   // > 100: never (the chain walk's cost
                                                                       // does not grow with the segment count)
-
     }
 #undef ALLOC
     p.pol = h->d_pol;
@@ -999,15 +948,14 @@ static magus_status enqueue_run(magus_replay_t* h, const float* d_trace, const f
     ep.w = d_w;
     if (detail) CU(h, rec(0));
     {
-        // pre-pass: zeroes the run's flag / worklist words; for segmented runs also the speculation aid
+        // pre-pass: zeroes the run's flag words; for segmented runs also the speculation aid
         // (first subsampled low / high tick of every trace).  The per-chain totals are
         // already zero (creation, then the previous run's totals kernel).
         const bool seg = has_work && p.n_seg > 1;
         const int n_blk = seg ? (d.n_traces + kPrepassTraces - 1) / kPrepassTraces : 1;
         CU(h, launch_k(magus_prepass_kernel, dim3((unsigned)n_blk), dim3(kPrepassTraces * kPrepassSlices), 0, s, false,
                        d_trace, d.n_traces, d.n_samples, (int64_t)d.trace_stride, h->B_lo, 256,
-                       seg ? h->d_first_low : (int*)nullptr, (uint32_t*)h->d_flag, 4, h->d_wl_count,
-                       3 * h->fx.n_fgroups + 1, h->fx.unresolved, p.n_lane));
+                       seg ? h->d_first_low : (int*)nullptr, (uint32_t*)h->d_flag, 4));
     }
     if (timing) CU(h, rec(1));
     if (has_work) {
@@ -1038,11 +986,9 @@ static magus_status enqueue_run(magus_replay_t* h, const float* d_trace, const f
     }
     if (timing) CU(h, rec(2));
     if (d.n_traces > 0) {
-        const int G = h->fx.n_fgroups;
-        const FixParams& fx = h->fx;
-        if (has_work && p.n_seg > 1 && h->walk_fix) {
-            // exact fix-up, one pass per chain in time order (magus_fix_walk_kernel): every launch group's
-            // chains scan their boundaries and re-run from the first wrong entry on
+        if (has_work && p.n_seg > 1) {
+            // exact fix-up: the first wrong entry of every chain, then one walk per
+            // chain in time order from there (magus_fix_lockstep_kernel; magus_fix_walk_kernel for the rest)
             dim3 gc((unsigned)((d.n_traces + 255) / 256), (unsigned)(p.n_seg - 1), (unsigned)p.n_lane);
             CU(h, launch_k(magus_fix_mark_kernel, gc, dim3(256), 0, s, h->pdl && !timing, p, h->fx));
             for (const LaunchGroup& g : h->groups) {
@@ -1053,39 +999,6 @@ static magus_status enqueue_run(magus_replay_t* h, const float* d_trace, const f
                 dim3 gw((unsigned)((d.n_traces + tpb - 1) / tpb), (unsigned)g.nq);
                 CU(h, launch_k(wk, gw, dim3(tpb), 0, s, h->pdl, p, ep, h->fx, g.q_base, d_trace));
             }
-        } else if (has_work && p.n_seg > 1) {
-            // exact fix-up: round 1 checks every segment entry against the previous exit; later rounds
-            // only re-check the successors of segments whose exit changed; a serial walk finishes the rest
-            // (worklist counters and `unresolved` zeroed by the pre-pass).
-            const bool pd = h->pdl;
-            dim3 gc((unsigned)((d.n_traces + 255) / 256), (unsigned)(p.n_seg - 1), (unsigned)p.n_lane);
-            CU(h, launch_k(magus_fix_check_all_kernel, gc, dim3(256), 0, s, pd && !timing, p, fx));
-            const cudaStream_t fs = s;
-            magus_status fst = [&]() -> magus_status {
-                const unsigned rr_blocks = 148 * 4;
-                for (int g = 0; g < G; ++g) {
-                    RerunKernel rk = rerun_kernel_for(h->groups[g].key);
-                    if (!rk) continue;
-                    CU(h, launch_k(rk, dim3(rr_blocks), dim3(256), 0, fs, pd, p, ep, fx, g, 0, 1, 1, d_trace));
-                }
-                for (int r = 2; r <= h->fix_rounds; ++r) {
-                    CU(h, cudaMemsetAsync(fx.wl_count, 0, G * sizeof(uint32_t), fs));                 // buf 0
-                    magus_fix_check_cand_kernel<<<148, 256, 0, fs>>>(p, fx, 1, 0, 0);
-                    CU(h, cudaGetLastError());
-                    CU(h, cudaMemsetAsync(fx.wl_count + G, 0, 2 * G * sizeof(uint32_t), fs));         // buf 1 + cursors
-                    for (int g = 0; g < G; ++g) {
-                        RerunKernel rk = rerun_kernel_for(h->groups[g].key);
-                        if (!rk) continue;
-                        rk<<<rr_blocks, 256, 0, fs>>>(p, ep, fx, g, 0, 1, r, d_trace);
-                        CU(h, cudaGetLastError());
-                    }
-                }
-                CU(h, launch_k(magus_fix_check_cand_kernel, dim3(148), dim3(256), 0, fs, pd, p, fx, 1, 0, 1));
-                dim3 gs((unsigned)((d.n_traces + 7) / 8), (unsigned)p.n_lane);
-                CU(h, launch_k(magus_fix_serial_kernel, gs, dim3(256), 0, fs, pd, p, ep, fx, d_trace));
-                return MAGUS_OK;
-            }();
-            if (fst != MAGUS_OK) return fst;
         }
     }
     if (detail) CU(h, rec(3));
@@ -1339,10 +1252,9 @@ extern "C" magus_status magus_replay_geometry(const magus_replay_t* h, int32_t o
     const bool has_work = d.n_traces > 0 && d.n_samples > 0;
     int nk = 1 + (has_work ? (int)h->groups.size() : 0);          // pre-pass, replay per launch group
     if (has_work && p.n_seg > 1) {
-        int nr = 0;
-        for (const LaunchGroup& g : h->groups) nr += rerun_kernel_for(g.key) ? 1 : 0;
-        if (h->walk_fix) nk += 1 + nr;                            // mark + one chain-walk kernel per launch group
-        else nk += 1 + nr * h->fix_rounds + (h->fix_rounds - 1) + 2;   // check, re-run rounds, candidate checks, serial
+        int nw = 0;
+        for (const LaunchGroup& g : h->groups) nw += walk_kernel_for(g.key) ? 1 : 0;
+        nk += 1 + nw;                                             // mark + one chain-walk kernel per launch group
     }
     nk += 1 + (d.world > 1 ? 1 : 0);                              // totals (+ chunk sums before the allreduce)
     int solo = 0;

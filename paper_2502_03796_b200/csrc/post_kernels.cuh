@@ -1,7 +1,7 @@
 // post_kernels.cuh -- the kernels around the replay kernel:
 //   magus_prepass_kernel         run start: zeroes the run's scratch words, speculation aid (first_low)
-//   magus_fix_*_kernel           exact fix-up of speculative time segments: worklist rounds with
-//                                lane-level work stealing, then a serial per-chain fallback
+//   magus_fix_mark_kernel,       exact fix-up of speculative time segments: the first wrong entry of
+//   magus_fix_lockstep_kernel    every chain, then one walk per chain in time order
 //   magus_totals_kernel          per-trace records (closed-form energy model from sufficient statistics,
 //                                DESIGN.md section 8) and per-policy fixed-order sums
 //   magus_resim_kernel           per-tick decision codes for a dump window (test diagnostics)
@@ -70,29 +70,12 @@ __device__ __forceinline__ void finish_record(TraceRec& r, const EpiParams& e, d
 // It is exact iff E_s equals the previous segment's true exit X_{s-1}.  Where they differ, the
 // segment is re-run from X_{s-1} next to the speculative trajectory from E_s until the two
 // coalesce (identical state at a 32-tick block end -- from then on they are identical); the
-// statistics delta (true - speculative) over the re-run prefix is added to the segment's stored
-// statistics.  If they never coalesce, the segment's exit changes and segment s+1 is checked
-// again in the next round.  Rounds are worklists processed with lane-level work stealing; a
-// serial per-chain walk finishes whatever is left after the last round.
+// statistics delta (true - speculative) over the re-run prefix is added to the chain's totals.  If
+// they never coalesce, the true exit is carried into the next boundary (the chain walk).
 
 struct FixParams {
-    int32_t n_fgroups;        // launch groups (one chain kind each)
-    int32_t cap_total;        // items per worklist buffer
-    const int32_t* grp_of_lane;   // [Q]
-    const int32_t* grp_first_lane;   // [n_fgroups] a lane of the group (its DevPolicy gives the kind)
-    const int64_t* grp_off;   // [n_fgroups] offset of the group's region in a worklist buffer
-    uint64_t* wl;             // [2][cap_total] items: q << 48 | s << 32 | j
-    uint32_t* wl_count;       // [2][n_fgroups]
-    uint32_t* wl_cursor;      // [n_fgroups] work-stealing cursors
-    uint8_t* unresolved;      // [Q][n_traces] chains left for the serial walk
-    unsigned int* any_unresolved;
-    int32_t* first_bad;       // [Q][n_traces] chain walk: first wrong segment entry (INT_MAX: none)
+    int32_t* first_bad;       // [Q][n_traces] first wrong segment entry of a chain (INT_MAX: none)
 };
-
-// warp-aggregated append of `item` (lanes with want) to list `buf` of group g
-__device__ __forceinline__ void fix_append(const FixParams& f, int buf, int g, bool want, uint64_t item) {
-    wl_append(f.wl + (int64_t)buf * f.cap_total + f.grp_off[g], &f.wl_count[buf * f.n_fgroups + g], want, item);
-}
 
 template <class T>
 __device__ __forceinline__ bool entry_mismatch(const ReplayParams& p, const DevPolicy& pol, int q, int s, int j) {
@@ -103,17 +86,6 @@ __device__ __forceinline__ bool entry_mismatch_any(const ReplayParams& p, const 
     if (pol.kind == LANE_MAGUS) return entry_mismatch<MagusTicker<0, true>>(p, pol, q, s, j);
     if (pol.kind == LANE_TDP) return entry_mismatch<TdpTicker>(p, pol, q, s, j);
     return false;
-}
-
-// copy stored state (e_src, s_src) -> (e_dst, s_dst) for chain (q, j)
-__device__ __forceinline__ void copy_state(const ReplayParams& p, const DevPolicy& pol, int q, int e_src, int s_src,
-                                           int e_dst, int s_dst, int j) {
-    const int64_t a = st_idx(p, e_src, q, s_src, j), b = st_idx(p, e_dst, q, s_dst, j);
-    p.st_f[b] = p.st_f[a];
-    p.st_log[b] = p.st_log[a];
-    if (pol.kind == LANE_MAGUS)
-        for (int r = 0; r < pol.k; ++r)
-            p.st_ring[ring_idx(p, e_dst, q, s_dst, r, j)] = p.st_ring[ring_idx(p, e_src, q, s_src, r, j)];
 }
 
 // Chain walk, step 1: every (q, s >= 1, j) whose speculative entry differs from the previous exit lowers
@@ -127,144 +99,7 @@ __global__ void __launch_bounds__(256) magus_fix_mark_kernel(const ReplayParams 
     if (entry_mismatch_any(p, pol, q, s, j)) atomicMin(f.first_bad + (int64_t)q * p.n_traces + j, s);
 }
 
-// Round 1: every (q, s >= 1, j) whose speculative entry differs from the previous exit.
-__global__ void __launch_bounds__(256) magus_fix_check_all_kernel(const ReplayParams p, const FixParams f) {
-    ptx::pdl_wait();
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    const int s = blockIdx.y + 1, q = blockIdx.z;
-    if (j >= p.n_traces) return;
-    const DevPolicy pol = p.pol[q];
-    const bool mism = entry_mismatch_any(p, pol, q, s, j);
-    fix_append(f, 0, f.grp_of_lane[q], mism, fix_item(q, s, j));
-}
-
-// Rounds >= 2: candidates (segments whose predecessor changed its exit in the last round): commit the
-// predecessor's new exit (staged in e = 2) and check the entry again.
-__global__ void __launch_bounds__(256) magus_fix_check_cand_kernel(const ReplayParams p, const FixParams f, int buf_in,
-                                                                   int buf_out, int mark_unresolved) {
-    ptx::pdl_wait();
-    for (int g = 0; g < f.n_fgroups; ++g) {
-        const uint32_t n = f.wl_count[buf_in * f.n_fgroups + g];
-        for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < ((n + 31u) & ~31u); i += gridDim.x * blockDim.x) {
-            bool mism = false;
-            uint64_t item = 0;
-            if (i < n) {
-                item = f.wl[(int64_t)buf_in * f.cap_total + f.grp_off[g] + i];
-                const int q = (int)(item >> 48), s = (int)((item >> 32) & 0xFFFF), j = (int)(item & 0xFFFFFFFFu);
-                const DevPolicy pol = p.pol[q];
-                copy_state(p, pol, q, 2, s - 1, 1, s - 1, j);
-                mism = entry_mismatch_any(p, pol, q, s, j);
-                if (mism && mark_unresolved) {
-                    f.unresolved[(int64_t)q * p.n_traces + j] = 1;
-                    atomicOr(f.any_unresolved, 1u);
-                }
-            }
-            if (!mark_unresolved) fix_append(f, buf_out, g, mism, item);
-        }
-    }
-}
-
-// Lane-level work stealing over the items of one group; the 32-tick block step stays converged.
-template <class T>
-__device__ void rerun_items(const ReplayParams& p, const EpiParams& e, const FixParams& f, int g, int buf_in,
-                            int buf_out, int round, const float* __restrict__ trace) {
-    using State = typename T::State;
-    const uint32_t n_items = f.wl_count[buf_in * f.n_fgroups + g];
-    State tru, spec;
-    SegStats dt, dp;
-    int q = 0, s = 0, j = 0, t = 0, seg_end = 0;
-    bool active = false;
-    DevPolicy pol = p.pol[f.grp_first_lane[g]];
-    unsigned long long done = 0;
-    bool exhausted = false;
-    const int lane = threadIdx.x & 31;
-    for (;;) {
-        // lanes without an item grab the next ones with one warp-aggregated atomic
-        const unsigned need = __ballot_sync(0xffffffffu, !active && !exhausted);
-        if (need) {
-            uint32_t base = 0;
-            const int leader = __ffs(need) - 1;
-            if (lane == leader) base = atomicAdd(&f.wl_cursor[g], (uint32_t)__popc(need));
-            base = __shfl_sync(0xffffffffu, base, leader);
-            const uint32_t idx = base + __popc(need & ((1u << lane) - 1u));
-            if (((need >> lane) & 1u) && idx >= n_items) exhausted = true;
-            if (((need >> lane) & 1u) && idx < n_items) {
-                const uint64_t item = f.wl[(int64_t)buf_in * f.cap_total + f.grp_off[g] + idx];
-                q = (int)(item >> 48);
-                s = (int)((item >> 32) & 0xFFFF);
-                j = (int)(item & 0xFFFFFFFFu);
-                pol = p.pol[q];
-                T::load(tru, p, pol, 1, q, s - 1, j);
-                T::load(spec, p, pol, 0, q, s, j);
-                dt.zero();
-                dp.zero();
-                t = s * p.seg_len;
-                seg_end = min(t + p.seg_len, p.n_samples);
-                active = true;
-            }
-        }
-        if (!__any_sync(0xffffffffu, active)) break;
-        if (active) {
-            const int n = min(32, seg_end - t);
-            float dv[32];
-#pragma unroll
-            for (int i = 0; i < 32; ++i) dv[i] = (i < n) ? __ldg(trace + (int64_t)(t + i) * p.trace_stride + j) : 0.0f;
-            const uint32_t fst = T::level(tru), fss = T::level(spec);
-            uint32_t wct = 0, wcs = 0;
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                if (i < n) {
-                    const TickOut ot = T::template tick<false>(tru, dv[i], pol, p.B_lo, p.B_hi, true, true);
-                    const TickOut os = T::template tick<false>(spec, dv[i], pol, p.B_lo, p.B_hi, true, true);
-                    wct = (wct << 1) | ot.cmd;
-                    wcs = (wcs << 1) | os.cmd;
-                    dt.nthr += ot.thr; dt.lock += ot.hf; if (ot.thr) dt.sexc += (double)dv[i] - (double)p.B_lo;
-                    dp.nthr += os.thr; dp.lock += os.hf; if (os.thr) dp.sexc += (double)dv[i] - (double)p.B_lo;
-                }
-            }
-            uint32_t ewt = 0, ews = 0;
-            if constexpr (T::kWarmupRules) {
-                ewt = (uint32_t)tru.evh;
-                ews = (uint32_t)spec.evh;
-            }
-            const int64_t b = t >> 5;
-            uint32_t* wout = p.words ? p.words + (((int64_t)q * p.n_traces + j) * p.n_blocks + b) * 2 : nullptr;
-            fold_block(dt, wct, ewt, fst, n, b, wout);
-            fold_block(dp, wcs, ews, fss, n, b, nullptr);
-            t += n;
-            const bool co = T::equal(tru, spec, pol);
-            if (co || t >= seg_end) {
-                add_to_chain(p, q, j, dt.nhi - dp.nhi, dt.nthr - dp.nthr, dt.trans - dp.trans, dt.ev - dp.ev,
-                             dt.lock - dp.lock, dt.sexc - dp.sexc, digest_pack(dt.dc - dp.dc, dt.de - dp.de));
-                copy_state(p, pol, q, 1, s - 1, 0, s, j);   // the entry the statistics now belong to
-                if (!co) {                                    // the exit changed: stage it, re-check s+1
-                    if (s + 1 < p.n_seg) T::save(tru, p, pol, 2, q, s, j);
-                    else T::save(tru, p, pol, 1, q, s, j);
-                }
-                ++done;
-                active = false;
-                const bool cand = !co && s + 1 < p.n_seg;
-                if (cand) fix_append(f, buf_out, g, true, fix_item(q, s + 1, j));
-            }
-        }
-    }
-    if (done) {
-        atomicAdd(e.fix_segments, done);
-        atomicMax(e.fix_rounds, round);
-    }
-}
-
-// One instantiation per chain kind (registers are allocated per kind); launched per launch group.
-template <class T>
-__global__ void __launch_bounds__(256) magus_fix_rerun_kernel(const ReplayParams p, const EpiParams e, const FixParams f,
-                                                              int g, int buf_in, int buf_out, int round,
-                                                              const float* __restrict__ trace) {
-    ptx::pdl_wait();
-    if (f.wl_count[buf_in * f.n_fgroups + g] == 0) return;
-    rerun_items<T>(p, e, f, g, buf_in, buf_out, round, trace);
-}
-
-// ------------------------------------------------------------------ serial walk (fallback, exact)
+// ------------------------------------------------------------------ one segment re-run (generic kinds)
 template <class T>
 __device__ bool rerun_segment(const ReplayParams& p, const DevPolicy& pol, int q, int s, int j, const float* trace,
                               typename T::State& tru, typename T::State& spec) {
@@ -310,66 +145,6 @@ __device__ bool rerun_segment(const ReplayParams& p, const DevPolicy& pol, int q
     add_to_chain(p, q, j, dt.nhi - dp.nhi, dt.nthr - dp.nthr, dt.trans - dp.trans, dt.ev - dp.ev, dt.lock - dp.lock,
                  dt.sexc - dp.sexc, digest_pack(dt.dc - dp.dc, dt.de - dp.de));
     return coalesced;
-}
-
-// One warp per unresolved chain, lanes = segments; rounds until every entry equals the previous exit.
-template <class T>
-__device__ void serial_fixup(const ReplayParams& p, const EpiParams& e, const DevPolicy& pol, int q, int j,
-                             const float* trace, int lane) {
-    int rounds = 0;
-    unsigned long long reruns = 0;
-    for (;;) {
-        bool any = false;
-        for (int base = 1; base < p.n_seg; base += 32) {
-            const int s = base + lane;
-            const bool need = s < p.n_seg && !T::stored_equal(p, pol, q, 0, s, 1, s - 1, j);
-            const unsigned m = __ballot_sync(0xffffffffu, need);
-            if (m == 0) continue;
-            any = true;
-            typename T::State tru, spec;
-            if (need) {
-                T::load(tru, p, pol, 1, q, s - 1, j);
-                T::load(spec, p, pol, 0, q, s, j);
-            }
-            __syncwarp();
-            if (need) {
-                const typename T::State entry = tru;   // the entry the corrected statistics belong to
-                const bool co = rerun_segment<T>(p, pol, q, s, j, trace, tru, spec);
-                T::save(entry, p, pol, 0, q, s, j);
-                if (!co) T::save(tru, p, pol, 1, q, s, j);
-                ++reruns;
-            }
-            __syncwarp();
-        }
-        if (!any) break;
-        ++rounds;
-    }
-    unsigned long long rr = reruns;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) rr += __shfl_xor_sync(0xffffffffu, rr, o);
-    if (lane == 0 && rr) {
-        atomicAdd(e.fix_segments, rr);
-        atomicMax(e.fix_rounds, 100 + rounds);   // >= 100: the serial fallback ran
-    }
-}
-
-__global__ void __launch_bounds__(256) magus_fix_serial_kernel(const ReplayParams p, const EpiParams e, const FixParams f,
-                                                               const float* __restrict__ trace) {
-    ptx::pdl_wait();
-    if (*f.any_unresolved == 0) return;
-    const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    const int q = blockIdx.y;
-    if (j >= p.n_traces || !f.unresolved[(int64_t)q * p.n_traces + j]) return;
-    const DevPolicy pol = p.pol[q];
-#define MAGUS_SERIAL(...) serial_fixup<__VA_ARGS__>(p, e, pol, q, j, trace, lane)
-    if (pol.kind == LANE_MAGUS) {
-        if (pol.C <= kMaxC32) MAGUS_SERIAL(MagusTicker<0, false>);
-        else MAGUS_SERIAL(MagusTicker<0, true>);
-    } else if (pol.kind == LANE_TDP) {
-        MAGUS_SERIAL(TdpTicker);
-    }
-#undef MAGUS_SERIAL
 }
 
 // ------------------------------------------------------------------ latency-optimised re-run (chain walk)
@@ -874,18 +649,14 @@ __global__ void magus_fill_codes_kernel(uint8_t* codes, int64_t n_rows, int P, i
 constexpr int kPrepassTraces = 32, kPrepassSlices = 32;
 __global__ void __launch_bounds__(kPrepassTraces * kPrepassSlices)
     magus_prepass_kernel(const float* __restrict__ trace, int n_traces, int n_samples, int64_t stride, float B_lo,
-                         int sub, int* __restrict__ first_low, uint32_t* __restrict__ zero_a, int n_zero_a,
-                         uint32_t* __restrict__ zero_b, int n_zero_b, uint8_t* __restrict__ unresolved, int n_lane) {
+                         int sub, int* __restrict__ first_low, uint32_t* __restrict__ zero_a, int n_zero_a) {
     ptx::pdl_trigger();   // the replay kernel may start its pipeline fill; it waits before reading first_low
     if (blockIdx.x == 0) {
         for (int i = threadIdx.x; i < n_zero_a; i += blockDim.x) zero_a[i] = 0u;
-        for (int i = threadIdx.x; i < n_zero_b; i += blockDim.x) zero_b[i] = 0u;
     }
     if (first_low == nullptr) return;
     const int tx = threadIdx.x % kPrepassTraces, ty = threadIdx.x / kPrepassTraces;
     const int j = blockIdx.x * kPrepassTraces + tx;
-    if (j < n_traces)   // chains left for the serial fix-up walk (set by the last check)
-        for (int q = ty; q < n_lane; q += kPrepassSlices) unresolved[(int64_t)q * n_traces + j] = 0;
     int lo = 0x7FFFFFFF, hi = 0x7FFFFFFF;
     if (j < n_traces) {
         const int n_sub = (n_samples + sub - 1) / sub;

@@ -1,5 +1,6 @@
 #!/bin/bash
-# GPU tests, then the bench of configs 2-5 with the chain-walk fix-up (default) and the worklist rounds.
+# GPU tests, then the bench of configs 2-5 (two runs each; MAGUS_FIX_WALK no longer selects anything: the
+# worklist-rounds fix-up it compared against was removed after the A/B in profiles/r01_fixup_walk_ab.txt).
 TAG=${1:-fix}
 OUT=gpurun_out; mkdir -p $OUT
 timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider -x > $OUT/${TAG}_pytest_gpu.log 2>&1
