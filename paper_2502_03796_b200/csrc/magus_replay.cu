@@ -66,9 +66,24 @@ bool lockstep_walk(int key) {
     return ((key >= 1 && key <= 8) || key == 1000 + LANE_TDP) && env_int("MAGUS_WALK_LOCKSTEP", 1);
 }
 
+// the split walk (64-thread CTAs: one warp per recurrence of 32 traces) covers the register-ring MAGUS kinds
+bool split_walk(int key) { return key >= 1 && key <= 8 && env_int("MAGUS_WALK_SPLIT", 1); }
+
 // chain-walk fix-up kernel for a chain kind (nullptr: stateless kinds never mismatch)
 typedef void (*WalkKernel)(ReplayParams, EpiParams, FixParams, int, const float*);
 WalkKernel walk_kernel_for(int key) {
+    if (split_walk(key)) {
+        switch (key) {
+            case 1: return magus_fix_split_kernel<1>;
+            case 2: return magus_fix_split_kernel<2>;
+            case 3: return magus_fix_split_kernel<3>;
+            case 4: return magus_fix_split_kernel<4>;
+            case 5: return magus_fix_split_kernel<5>;
+            case 6: return magus_fix_split_kernel<6>;
+            case 7: return magus_fix_split_kernel<7>;
+            default: return magus_fix_split_kernel<8>;
+        }
+    }
     if (lockstep_walk(key)) {
         switch (key) {
             case 1: return magus_fix_lockstep_kernel<MagusTicker<1, false>>;
@@ -995,8 +1010,9 @@ static magus_status enqueue_run(magus_replay_t* h, const float* d_trace, const f
                 WalkKernel wk = walk_kernel_for(g.key);
                 if (!wk) continue;
                 // the lockstep walk: one-warp CTAs, spread over the SMs (a walk is latency-bound)
-                const int tpb = lockstep_walk(g.key) ? 32 : 128;
-                dim3 gw((unsigned)((d.n_traces + tpb - 1) / tpb), (unsigned)g.nq);
+                const int tpb = split_walk(g.key) ? 64 : lockstep_walk(g.key) ? 32 : 128;
+                const int per_cta = split_walk(g.key) ? 32 : tpb;   // traces per CTA
+                dim3 gw((unsigned)((d.n_traces + per_cta - 1) / per_cta), (unsigned)g.nq);
                 CU(h, launch_k(wk, gw, dim3(tpb), 0, s, h->pdl, p, ep, h->fx, g.q_base, d_trace));
             }
         }

@@ -468,6 +468,177 @@ __global__ void __launch_bounds__(32) magus_fix_lockstep_kernel(const ReplayPara
     }
 }
 
+// ------------------------------------------------------------------ split chain walk (MAGUS, k <= 8)
+// The lockstep walk with its two recurrences in two warps: warp 0 of a 64-thread CTA steps the true
+// states of 32 traces, warp 1 their speculative states, each with the one-chain stage block
+// (MAGUS_WSTAGE1F_K<k>).  A walking warp is alone on its SM sub-partition and issues ~0.3 instructions
+// per cycle, so halving the instructions each warp issues per tick nearly halves the walk.  The warps
+// meet at a named barrier at every segment boundary and every 32-tick block end: warp 1 publishes its
+// state and statistics in shared memory, warp 0 compares, adds the deltas and publishes the decisions.
+template <int K>
+__device__ __forceinline__ void walk_stage1(MagusState<K, false>& st, float& lock, float& nthr, uint32_t& wcmd,
+                                            SegStats& ss, const float* d8, const DevPolicy& pol, float B_lo,
+                                            double Blo_d) {
+    uint32_t e0 = st.evh;
+    const uint32_t bitc = 1u << (pol.C - 1), mone = 0xFFFFFFFFu * pol.one;
+#define W1_TAIL                                                                                                  \
+    e0, st.cnt, ss.sexc, lock, nthr, wcmd, __float_as_uint(d8[0]), __float_as_uint(d8[1]), __float_as_uint(d8[2]), \
+        __float_as_uint(d8[3]), __float_as_uint(d8[4]), __float_as_uint(d8[5]), __float_as_uint(d8[6]),             \
+        __float_as_uint(d8[7]), B_lo, Blo_d, pol.dinc, pol.ddec, bitc, pol.smin_sc, pol.one, mone
+#define R(i) st.ring.v[i]
+    if constexpr (K == 1) MAGUS_WSTAGE1F_K1(st.f, R(0), W1_TAIL);
+    else if constexpr (K == 2) MAGUS_WSTAGE1F_K2(st.f, R(0), R(1), W1_TAIL);
+    else if constexpr (K == 3) MAGUS_WSTAGE1F_K3(st.f, R(0), R(1), R(2), W1_TAIL);
+    else if constexpr (K == 4) MAGUS_WSTAGE1F_K4(st.f, R(0), R(1), R(2), R(3), W1_TAIL);
+    else if constexpr (K == 5) MAGUS_WSTAGE1F_K5(st.f, R(0), R(1), R(2), R(3), R(4), W1_TAIL);
+    else if constexpr (K == 6) MAGUS_WSTAGE1F_K6(st.f, R(0), R(1), R(2), R(3), R(4), R(5), W1_TAIL);
+    else if constexpr (K == 7) MAGUS_WSTAGE1F_K7(st.f, R(0), R(1), R(2), R(3), R(4), R(5), R(6), W1_TAIL);
+    else MAGUS_WSTAGE1F_K8(st.f, R(0), R(1), R(2), R(3), R(4), R(5), R(6), R(7), W1_TAIL);
+#undef R
+#undef W1_TAIL
+    st.evh = e0;
+}
+
+template <int K>
+struct SplitXchg {   // what warp 1 (speculative) publishes for warp 0 (true), per lane
+    uint32_t f, evh;
+    double ring[K];
+    SegStats ss;
+    float lock, nthr;
+    int32_t s0;
+    uint32_t flags;   // from warp 0: bit 0 walking, bit 1 active
+};
+
+__device__ __forceinline__ void split_bar() { asm volatile("bar.sync 1, 64;" ::: "memory"); }
+
+template <int K>
+__global__ void __launch_bounds__(64) magus_fix_split_kernel(const ReplayParams p, const EpiParams e,
+                                                             const FixParams f, int q_base,
+                                                             const float* __restrict__ trace) {
+    ptx::pdl_wait();
+    using T = MagusTicker<K, false>;
+    __shared__ SplitXchg<K> x[32];
+    const int role = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int j = blockIdx.x * 32 + lane;
+    const int q = q_base + blockIdx.y;
+    const bool valid = j < p.n_traces;
+    if (role == 0) {
+        int s0 = 0x7FFFFFFF;
+        if (valid) {
+            const int64_t ci = (int64_t)q * p.n_traces + j;
+            s0 = f.first_bad[ci];
+            if (s0 < 0x7FFFFFFF) f.first_bad[ci] = 0x7FFFFFFF;   // reset for the next run
+        }
+        x[lane].s0 = s0;
+    }
+    split_bar();
+    const int s0 = x[lane].s0;
+    const int ws = __reduce_min_sync(0xffffffffu, s0);
+    if (ws >= p.n_seg) return;   // uniform over both warps
+    const DevPolicy pol = p.pol[q];
+    const double Blo_d = (double)p.B_lo;
+    const float* col = trace + (valid ? j : 0);
+    MagusState<K, false> st;   // warp 0: true state, warp 1: speculative state
+    bool walking = false;
+    int walked = 0;
+    for (int s = ws; s < p.n_seg; ++s) {
+        const bool chk = !walking && valid && s >= s0 && !T::stored_equal(p, pol, q, 0, s, 1, s - 1, j);
+        if (role == 1 && (walking || chk)) T::load(st, p, pol, 0, q, s, j);
+        if (role == 0 && chk) T::load(st, p, pol, 1, q, s - 1, j);
+        if (role == 1) {
+            x[lane].f = st.f;
+            x[lane].evh = st.evh;
+#pragma unroll
+            for (int r = 0; r < K; ++r) x[lane].ring[r] = st.ring.v[r];
+        }
+        split_bar();
+        if (role == 0) {
+            if (walking) {
+                MagusState<K, false> o;
+                o.f = x[lane].f;
+                o.evh = x[lane].evh;
+#pragma unroll
+                for (int r = 0; r < K; ++r) o.ring.v[r] = x[lane].ring[r];
+                walking = !T::equal(st, o, pol);
+            } else if (chk) {
+                walking = true;
+            }
+            x[lane].flags = walking ? 1u : 0u;
+        }
+        split_bar();
+        if (role == 1) walking = (x[lane].flags & 1u) != 0u;
+        if (!__any_sync(0xffffffffu, walking)) continue;   // the same answer in both warps
+        walked += walking ? 1 : 0;
+        const int seg_start = s * p.seg_len, seg_end = min(seg_start + p.seg_len, p.n_samples);
+        SegStats ss;
+        ss.zero();
+        float lock = 0.f, nthr = 0.f;
+        bool active = walking;
+        float nxt[32];
+        walk_load(nxt, col, seg_start, seg_end, p.trace_stride);
+        for (int bt0 = seg_start; bt0 < seg_end; bt0 += 32) {
+            if (!__any_sync(0xffffffffu, active)) break;   // the same answer in both warps
+            const int n = min(32, seg_end - bt0);
+            float dv[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) dv[i] = nxt[i];
+            if (bt0 + 32 < seg_end) walk_load(nxt, col, bt0 + 32, seg_end, p.trace_stride);
+            const uint32_t fs = st.f;
+            uint32_t wcmd = 0u;
+            if (n == 32) {
+#pragma unroll
+                for (int g = 0; g < 4; ++g) walk_stage1<K>(st, lock, nthr, wcmd, ss, dv + 8 * g, pol, p.B_lo, Blo_d);
+            } else {   // the ragged last block (static indices keep the samples in registers)
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                    if (i < n) lockstep_tick<T>(st, dv[i], pol, p, Blo_d, wcmd, ss);
+            }
+            const int64_t b = bt0 >> 5;
+            uint32_t* wout = (role == 0 && active && p.words)
+                                 ? p.words + (((int64_t)q * p.n_traces + j) * p.n_blocks + b) * 2
+                                 : nullptr;
+            fold_block(ss, wcmd, st.evh, fs, n, b, wout);
+            if (role == 1) {
+                x[lane].f = st.f;
+                x[lane].evh = st.evh;
+#pragma unroll
+                for (int r = 0; r < K; ++r) x[lane].ring[r] = st.ring.v[r];
+                x[lane].ss = ss;
+                x[lane].lock = lock;
+                x[lane].nthr = nthr;
+            }
+            split_bar();
+            if (role == 0) {
+                MagusState<K, false> o;
+                o.f = x[lane].f;
+                o.evh = x[lane].evh;
+#pragma unroll
+                for (int r = 0; r < K; ++r) o.ring.v[r] = x[lane].ring[r];
+                const bool same = T::equal(st, o, pol);
+                if (active && (same || bt0 + 32 >= seg_end)) {   // coalesced (the rest is right), or segment end
+                    const SegStats& c = x[lane].ss;
+                    add_to_chain(p, q, j, ss.nhi - c.nhi, ss.nthr - c.nthr + ((uint32_t)nthr - (uint32_t)x[lane].nthr),
+                                 ss.trans - c.trans, ss.ev - c.ev,
+                                 ss.lock - c.lock + ((uint32_t)lock - (uint32_t)x[lane].lock), ss.sexc - c.sexc,
+                                 digest_pack(ss.dc - c.dc, ss.de - c.de));
+                    walking = !same;   // carry the true exit into the next boundary
+                    active = false;
+                }
+                x[lane].flags = (walking ? 1u : 0u) | (active ? 2u : 0u);
+            }
+            split_bar();
+            if (role == 1) {
+                walking = (x[lane].flags & 1u) != 0u;
+                active = (x[lane].flags & 2u) != 0u;
+            }
+        }
+    }
+    if (walked && role == 0) {
+        atomicAdd(e.fix_segments, (unsigned long long)walked);
+        atomicMax(e.fix_rounds, walked);
+    }
+}
+
 // ------------------------------------------------------------------ chain walk (default fix-up, exact)
 // One thread per chain (q, j): scans the segment boundaries in order; at the first entry that differs
 // from the previous exit it re-runs that segment from the true state next to the speculative one

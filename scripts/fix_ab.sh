@@ -1,5 +1,5 @@
 #!/bin/bash
-# GPU tests, then the bench of configs 2-5 (two runs each; MAGUS_FIX_WALK no longer selects anything: the
+# GPU tests, then the bench of configs 2-5 with MAGUS_WALK_SPLIT=1 / 0 (split vs lockstep chain walk; the
 # worklist-rounds fix-up it compared against was removed after the A/B in profiles/r01_fixup_walk_ab.txt).
 TAG=${1:-fix}
 OUT=gpurun_out; mkdir -p $OUT
@@ -7,7 +7,7 @@ timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider -x > $OUT/${TAG
 echo "pytest rc=$?" >> $OUT/${TAG}_pytest_gpu.log
 for c in 5 3 4 2; do
   for v in 1 0; do  # MAGUS_FIX_WALK
-    MAGUS_FIX_WALK=$v timeout 600 python bench.py --config $c --no-e2e --no-cpu-baseline --steps 10 --warmup 3 \
+    MAGUS_WALK_SPLIT=$v timeout 600 python bench.py --config $c --no-e2e --no-cpu-baseline --steps 10 --warmup 3 \
         > $OUT/${TAG}_cfg${c}_walk$v.json 2>> $OUT/${TAG}.err
   done
 done

@@ -156,7 +156,7 @@ def build_stage(K, TC=8):
 
 
 
-def build_stage_f(K, TC=8, walk=False, traces=1, thr64=True):
+def build_stage_f(K, TC=8, walk=False, traces=1, thr64=True, one=False):
     """MAGUS_SSTAGE_K<K>: one whole steady-state stage (TC ticks x 4 chains, tile loads included) of the solo
     replay kernel, balanced over the issue pipes (ALU and FMA-heavy at half rate, FP64, XU): the throttle
     test on the FP64 pipe, the tune log, scaled window count and cmd word as (predicated) IMADs, the lock /
@@ -165,7 +165,8 @@ def build_stage_f(K, TC=8, walk=False, traces=1, thr64=True):
     walk=True: MAGUS_WSTAGE_K<K>, the chain walk's stage (post_kernels.cuh): two chains -- the true and the
     speculative state of ONE trace -- stepped over the same 8 samples, passed in registers; no validation
     maximum (the replay already took it)."""
-    C = 2 * traces if walk else 4   # walk: chains (2t, 2t+1) = (true, speculative) state of trace t
+    C = (1 if one else 2 * traces) if walk else 4   # walk: chains (2t, 2t+1) = (true, speculative) of trace t;
+                                                    # one: a single chain (the split walk, one state per warp)
     names = [(f"f{c}", "+r") for c in range(C)] + \
             [(f"r{c}_{i}", "+d") for c in range(C) for i in range(K)] + \
             [(f"evh{c}", "+r") for c in range(C)] + [(f"cnt{c}", "+r") for c in range(C)] + \
@@ -227,7 +228,7 @@ def build_stage_f(K, TC=8, walk=False, traces=1, thr64=True):
             body.append(f"mov.f64 {R(f'r{c}_{i}')}, ad{(TC - 1 - i) * C + c};")
     body.append("}")
     params = ", ".join(n for n, _ in names + inames)
-    name = f"MAGUS_{'W' if walk else 'S'}STAGE{'2' if traces == 2 else ''}{'' if thr64 else 'F'}_K{K}"
+    name = f"MAGUS_{'W' if walk else 'S'}STAGE{'2' if traces == 2 else ''}{'1' if one else ''}{'' if thr64 else 'F'}_K{K}"
     out = [f"#define {name}(...) {name}_(__VA_ARGS__)", f"#define {name}_({params}) \\", "    asm volatile( \\"]
     out += [f'        "{l}\\n\\t" \\' for l in body]
     out.append("        : " + ", ".join(f'"{c}"({n})' for n, c in names) + " \\")
@@ -247,6 +248,7 @@ for K in (1, 2, 3):
     out += [""] + build_stage_f(K, thr64=False)
 for K in range(1, 9):
     out += [""] + build_stage_f(K, walk=True)
+    out += [""] + build_stage_f(K, walk=True, one=True, thr64=False)
 path = os.path.join(os.path.dirname(__file__), "..", "paper_2502_03796_b200", "csrc", "tick4_asm.cuh")
 open(path, "w").write("\n".join(out) + "\n")
 print("wrote", os.path.normpath(path))
