@@ -1006,14 +1006,28 @@ static magus_status enqueue_run(magus_replay_t* h, const float* d_trace, const f
             // chain in time order from there (magus_fix_lockstep_kernel; magus_fix_walk_kernel for the rest)
             dim3 gc((unsigned)((d.n_traces + 255) / 256), (unsigned)(p.n_seg - 1), (unsigned)p.n_lane);
             CU(h, launch_k(magus_fix_mark_kernel, gc, dim3(256), 0, s, h->pdl && !timing, p, h->fx));
-            for (const LaunchGroup& g : h->groups) {
-                WalkKernel wk = walk_kernel_for(g.key);
-                if (!wk) continue;
-                // the lockstep walk: one-warp CTAs, spread over the SMs (a walk is latency-bound)
+            // the launch groups' walks are independent (different chains): concurrent streams (parallel
+            // graph branches), like the replay launches
+            std::vector<const LaunchGroup*> wg;
+            for (const LaunchGroup& g : h->groups)
+                if (walk_kernel_for(g.key)) wg.push_back(&g);
+            const int W = (int)wg.size();
+            if (W > 1) {
+                CU(h, cudaEventRecord(h->fork_ev, s));
+                for (int i = 1; i < W; ++i) CU(h, cudaStreamWaitEvent(h->aux[i - 1], h->fork_ev, 0));
+            }
+            for (int i = 0; i < W; ++i) {
+                const LaunchGroup& g = *wg[i];
+                // split walk: 64-thread CTAs of 32 traces; lockstep walk: one-warp CTAs (a walk is latency-bound)
                 const int tpb = split_walk(g.key) ? 64 : lockstep_walk(g.key) ? 32 : 128;
                 const int per_cta = split_walk(g.key) ? 32 : tpb;   // traces per CTA
                 dim3 gw((unsigned)((d.n_traces + per_cta - 1) / per_cta), (unsigned)g.nq);
-                CU(h, launch_k(wk, gw, dim3(tpb), 0, s, h->pdl, p, ep, h->fx, g.q_base, d_trace));
+                CU(h, launch_k(walk_kernel_for(g.key), gw, dim3(tpb), 0, i == 0 ? s : h->aux[i - 1], h->pdl && i == 0,
+                               p, ep, h->fx, g.q_base, d_trace));
+            }
+            for (int i = 1; i < W; ++i) {
+                CU(h, cudaEventRecord(h->join_ev[i - 1], h->aux[i - 1]));
+                CU(h, cudaStreamWaitEvent(s, h->join_ev[i - 1], 0));
             }
         }
     }
