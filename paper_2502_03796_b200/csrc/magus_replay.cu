@@ -753,7 +753,7 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
     p.B_lo = h->B_lo;
     p.B_hi = h->B_hi;
     p.bwbits = h->bwbits;
-    p.solo_flags = env_int("MAGUS_SOLO_SYNTH", 1) ? 1u : 0u;
+    p.solo_flags = env_int("MAGUS_SOLO_SYNTH", 0) ? 1u : 0u;   // off: see DESIGN.md section 9
 
     const int Q = p.n_lane, S = p.n_seg;
     const size_t nst = (size_t)3 * Q * S * std::max(1, d.n_traces);   // entry, exit, staged exit

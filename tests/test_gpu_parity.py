@@ -306,37 +306,28 @@ def test_full_size_sampled(M, cfg):
     print("geometry", res.geometry, "mismatched segments", res.n_mismatched_segments, "rounds", res.fixup_rounds)
 
 
-def test_cfg4_shard_sampled(M):
+def test_cfg4_shard_sampled(M, monkeypatch):
     """cfg 4 as one rank of the 8-GPU run sees it (rank 5: global traces [40960, 49152) x 10^6 samples,
-    32.8 GB), in the bench's launch configuration: the oscillating class (C4) makes speculative
-    segment entries wrong through whole traces, so the chain-walk fix-up runs over ~10^6 ticks; sampled
-    traces (global ids, including both ends of the shard) must match the oracle bit-exactly on counts and
-    digests, 1e-9 on energies."""
+    32.8 GB), in the bench's launch configuration, and again with the solo kernel's synthetic warm-up state
+    (MAGUS_SOLO_SYNTH=1): it lands the oscillating class (C4) on phase-shifted limit cycles, so speculative
+    entries stay wrong through whole traces and the chain walk runs over ~10^6 ticks.  Sampled traces (global
+    ids, including both ends of the shard) must match the oracle bit-exactly on counts and digests, 1e-9 on
+    energies, both times."""
     c = CONFIGS[4]
     n, ns, rank = c["per_gpu_traces"], c["n_samples"], 5
     off = rank * n
     tr, w = gpu_gen(M, c["seed"], n, ns, c["class_mix"], n, offset=off)
-    res = run_gpu(M, tr, w, c["policies"], n, ns, n, flags=M.F_PER_TRACE_STATS, offset=off)
-    del tr
     rng = np.random.default_rng(4)
     ids = np.unique(np.r_[rng.choice(n, 10, replace=False), [0, 4, 9, n - 1]])   # 4, 9: class C4 (j mod 5)
     rec, _, _ = O.gen_replay(O.GenDesc(seed=c["seed"], n_traces=n, n_samples=ns, class_mix=c["class_mix"],
                                        global_trace_offset=off), ids, PA.oracle_policies(c["policies"]))
-    PA.compare_records(res.per_trace[ids], rec, "cfg4-shard")
-    np.testing.assert_allclose(res.totals, PA.oracle_totals(res.per_trace), rtol=1e-9)
-    assert res.n_mismatched_segments > 0, "the shard should exercise the chain walk"
-    print("geometry", res.geometry, "mismatched segments", res.n_mismatched_segments, "rounds", res.fixup_rounds)
-
-
-def test_active_savings_from_gpu_totals(M):
-    """NEXT-4: active power / energy / EDP savings of MAGUS against the static-max baseline from
-    the GPU run's per-policy totals, with the paper's single-GPU (30 W) and 4-GPU (200 W) idle powers
-    (P:397), equal the oracle's job-level active savings from its own per-trace records (1e-9)."""
-    c = SMALL["cfg2-small"]
-    tr, w = gpu_gen(M, c["seed"], c["n"], c["ns"], c["mix"])
-    res = run_gpu(M, tr, w, c["policies"], c["n"], c["ns"], (c["n"] + 3) // 4 * 4, flags=M.F_PER_TRACE_STATS)
-    rec, _ = oracle_run(tr.cpu().numpy(), w.cpu().numpy(), c["policies"], c["n"])
-    for p_idle in (30.0, 200.0):
-        got = M.active_savings(res.totals, 0, 1, p_idle)
-        want = O.active_savings_job(rec["E"][:, 0], rec["T"][:, 0], rec["E"][:, 1], rec["T"][:, 1], p_idle)
-        np.testing.assert_allclose(got, want, rtol=1e-9, atol=1e-12)
+    mism = []
+    for synth in ("0", "1"):
+        monkeypatch.setenv("MAGUS_SOLO_SYNTH", synth)
+        res = run_gpu(M, tr, w, c["policies"], n, ns, n, flags=M.F_PER_TRACE_STATS, offset=off)
+        PA.compare_records(res.per_trace[ids], rec, f"cfg4-shard synth={synth}")
+        np.testing.assert_allclose(res.totals, PA.oracle_totals(res.per_trace), rtol=1e-9)
+        mism.append(res.n_mismatched_segments)
+        print("synth", synth, "geometry", res.geometry, "mismatched", res.n_mismatched_segments,
+              "walked", res.fixup_rounds)
+    assert mism[1] > 0, "the synthetic warm-up state should exercise the chain walk"
