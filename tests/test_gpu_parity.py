@@ -331,3 +331,17 @@ def test_cfg4_shard_sampled(M, monkeypatch):
         print("synth", synth, "geometry", res.geometry, "mismatched", res.n_mismatched_segments,
               "walked", res.fixup_rounds)
     assert mism[1] > 0, "the synthetic warm-up state should exercise the chain walk"
+
+
+def test_active_savings_from_gpu_totals(M):
+    """NEXT-4: active power / energy / EDP savings of MAGUS against the static-max baseline from
+    the GPU run's per-policy totals, with the paper's single-GPU (30 W) and 4-GPU (200 W) idle powers
+    (P:397), equal the oracle's job-level active savings from its own per-trace records (1e-9)."""
+    c = SMALL["cfg2-small"]
+    tr, w = gpu_gen(M, c["seed"], c["n"], c["ns"], c["mix"])
+    res = run_gpu(M, tr, w, c["policies"], c["n"], c["ns"], (c["n"] + 3) // 4 * 4, flags=M.F_PER_TRACE_STATS)
+    rec, _ = oracle_run(tr.cpu().numpy(), w.cpu().numpy(), c["policies"], c["n"])
+    for p_idle in (30.0, 200.0):
+        got = M.active_savings(res.totals, 0, 1, p_idle)
+        want = O.active_savings_job(rec["E"][:, 0], rec["T"][:, 0], rec["E"][:, 1], rec["T"][:, 1], p_idle)
+        np.testing.assert_allclose(got, want, rtol=1e-9, atol=1e-12)
