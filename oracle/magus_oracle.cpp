@@ -195,9 +195,10 @@ int oracle_replay(const float* D, int64_t n, int64_t stride, float w,
 
     for (int64_t t = 0; t < n; ++t) {
         const float Dt = D[t * stride];
-        /* 1 observe */
+        /* 1 observe: closed loop, the throughput the workload attains at the level in effect [A14];
+           open loop, a recorded throughput observed as is [A30] */
         const float B = (f == O_HI) ? B_hi : B_lo;
-        const float A = (Dt < B) ? Dt : B;
+        const float A = (m->observe == 1) ? Dt : ((Dt < B) ? Dt : B);
         /* 2 duration */
         const bool thr = (A < Dt);
         double tau;

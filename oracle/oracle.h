@@ -29,7 +29,8 @@ typedef struct {
     double  f_min_ghz, f_max_ghz; /* 0.8 / 2.2 GHz */
     double  bw_max_gbps;          /* bandwidth at f_max */
     int32_t bw_shape;             /* 0 Linear, 1 Saturating */
-    int32_t _pad;
+    int32_t observe;              /* 0 closed loop: A = min(D, B[f]) [A14]; 1 open loop: the recorded
+                                     throughput is observed as is, A = D [A30] */
     double  bw_knee;
     double  p_pkg_idle_w, p_core_active_w, p_uncore_min_w, p_uncore_max_w, p_exponent;
     double  p_gpu_active_w;       /* GPU power while the trace runs */

@@ -429,3 +429,47 @@ def test_active_savings_job_hand_example():
     got0 = O.active_savings_job([100, 300], [1, 2], [150, 400], [1, 1.5], 0.0)
     assert got0 == pytest.approx((float(1 - P / Pb), float(1 - F(400, 550)), float(1 - F(400 * 3) / F(550 * 5, 2))),
                                  rel=1e-14)
+
+
+# --------------------------------------------------------------------------- NEXT-3: open-loop observation
+
+def test_open_loop_step_hand_derived():
+    """A30 (open loop, recorded throughput observed as is) on a hand-stepped rising edge: D = [2]x4 + [15]x8,
+    defaults (k = 1, theta = +-1 GB/s/s, C = 10), bw_max = 22 GB/s (B_lo = 8), w = 0.5.  A = D, so the only
+    tune flag is the edge at t = 4 (d = 13 GB/s over 0.1 s > 1): Increase -> f_max from t = 5, then Hold.
+    No tick is throttled: T = 12 * 0.1 s; E_pkg = 200 W * 0.7 s + 116 W * 0.5 s = 198 J; E = 198 + 87 * 1.2.
+    (Closed loop, A14, sees the throttled jump 2 -> 8 at f_min and then 8 -> 15: two flags, a dilated tick.)"""
+    D = np.array([2.0] * 4 + [15.0] * 8, np.float32)
+    r, codes = O.replay(D, 0.5, O.Policy(), O.Model(bw_max_gbps=22.0, observe=1), codes=True)
+    assert (r["tune_events"], r["transitions"], r["n_hi"], r["n_thr"], r["lock_ticks"]) == (1, 1, 7, 0, 0)
+    assert [int(c & 1) for c in codes] == [0] * 4 + [1] * 8
+    assert r["T"] == pytest.approx(1.2, rel=1e-12) and r["E_pkg"] == pytest.approx(198.0, rel=1e-12)
+    assert r["E"] == pytest.approx(198.0 + 87.0 * 1.2, rel=1e-12)
+    rc, _ = O.replay(D, 0.5, O.Policy(), O.Model(bw_max_gbps=22.0), codes=True)
+    assert (rc["tune_events"], rc["transitions"], rc["n_thr"]) == (2, 1, 1)
+
+
+def test_open_loop_equals_closed_loop_below_b_lo():
+    """A30 vs A14: when no sample exceeds B_lo no tick can be throttled at either level, so A = D in both
+    modes and every record is identical, for every policy kind."""
+    rng = np.random.default_rng(30)
+    D = rng.uniform(0.0, 7.0, 3000).astype(np.float32)   # B_lo = 7.27 at the default model
+    for pol in (O.Policy(), O.Policy(deriv_ticks=3, tune_log_capacity=5, high_freq_threshold=0.4),
+                O.Policy(kind=O.TDP_DEFAULT, tdp_w=217.0), O.Policy(kind=O.STATIC_MIN)):
+        a, _ = O.replay(D, 0.7, pol, O.Model(), codes=True)
+        b, _ = O.replay(D, 0.7, pol, O.Model(observe=1), codes=True)
+        for f in ("n_hi", "n_thr", "transitions", "tune_events", "lock_ticks", "digest", "T", "E"):
+            assert a[f] == b[f], f
+
+
+def test_open_loop_flags_depend_on_the_trace_only():
+    """A30: with A = D the Alg. 1 signal, hence every tune flag, is a function of the trace and of (k, theta)
+    alone -- the same for policies that differ only in C and theta_hf (whose levels differ); the closed loop
+    has no such property on a trace that crosses B_lo (A14)."""
+    rng = np.random.default_rng(31)
+    D = np.repeat(rng.uniform(0.5, 19.0, 400), rng.integers(1, 6, 400))[:1500].astype(np.float32)
+    pa, pb = O.Policy(tune_log_capacity=10, high_freq_threshold=0.6), O.Policy(tune_log_capacity=4, high_freq_threshold=0.5)
+    _, ca = O.replay(D, 0.6, pa, O.Model(observe=1), codes=True)
+    _, cb = O.replay(D, 0.6, pb, O.Model(observe=1), codes=True)
+    assert np.array_equal(ca & 0x34, cb & 0x34)            # flag bit and signal bits
+    assert not np.array_equal(ca & 0x81, cb & 0x81)        # while the levels do differ
