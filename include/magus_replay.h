@@ -81,7 +81,9 @@ typedef struct {
     double  f_min_ghz, f_max_ghz; /* 0 < f_min < f_max; 0.8 / 2.2 */
     double  bw_max_gbps;          /* > 0, bandwidth at f_max */
     int32_t bw_shape;             /* 0 Linear, 1 Saturating */
-    int32_t _reserved0;
+    int32_t observe;              /* 0 closed loop: the governor observes A = min(D, bandwidth(level)) (A14);
+                                     1 open loop: the trace is a recorded throughput observed as is, A = D,
+                                     never throttled (NEXT-3, DESIGN A30) */
     double  bw_knee;              /* Saturating only, (0, 1] */
     double  p_pkg_idle_w, p_core_active_w, p_uncore_min_w, p_uncore_max_w; /* >= 0, max >= min */
     double  p_exponent;           /* >= 1 */

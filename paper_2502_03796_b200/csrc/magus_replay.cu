@@ -331,6 +331,7 @@ std::string validate_model(const magus_model& m) {
     if (!(finite(m.bw_max_gbps) && m.bw_max_gbps > 0)) return "bw_max_gbps must be finite and > 0";
     if (m.bw_shape != 0 && m.bw_shape != 1) return "bw_shape must be 0 (Linear) or 1 (Saturating)";
     if (m.bw_shape == 1 && !(m.bw_knee > 0 && m.bw_knee <= 1)) return "bw_knee must be in (0, 1]";
+    if (m.observe != 0 && m.observe != 1) return "observe must be 0 (closed loop) or 1 (open loop)";
     const double pw[] = {m.p_pkg_idle_w, m.p_core_active_w, m.p_uncore_min_w, m.p_uncore_max_w, m.p_gpu_active_w,
                          m.dram_w_per_gbps};
     const char* names[] = {"p_pkg_idle_w", "p_core_active_w", "p_uncore_min_w", "p_uncore_max_w",
@@ -750,7 +751,9 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
     h->n_sm = n_sm;
     h->alloc_segments = h->rp.n_seg;
     ReplayParams& p = h->rp;
-    p.B_lo = h->B_lo;
+    // the kernels' throttle threshold: B_lo; +inf in open loop (A30: A = D, no tick is ever throttled).
+    // The epilogue keeps the true B_lo (its throttling excess is then 0).
+    p.B_lo = d.model.observe == 1 ? __builtin_inff() : h->B_lo;
     p.B_hi = h->B_hi;
     p.bwbits = h->bwbits;
     p.solo_flags = env_int("MAGUS_SOLO_SYNTH", 0) ? 1u : 0u;   // off: see DESIGN.md section 9

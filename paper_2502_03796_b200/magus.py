@@ -44,7 +44,7 @@ class c_policy(C.Structure):
 
 class c_model(C.Structure):
     _fields_ = [("sample_period_s", C.c_double), ("f_min_ghz", C.c_double), ("f_max_ghz", C.c_double),
-                ("bw_max_gbps", C.c_double), ("bw_shape", C.c_int32), ("_reserved0", C.c_int32),
+                ("bw_max_gbps", C.c_double), ("bw_shape", C.c_int32), ("observe", C.c_int32),
                 ("bw_knee", C.c_double), ("p_pkg_idle_w", C.c_double), ("p_core_active_w", C.c_double),
                 ("p_uncore_min_w", C.c_double), ("p_uncore_max_w", C.c_double), ("p_exponent", C.c_double),
                 ("p_gpu_active_w", C.c_double), ("dram_w_per_gbps", C.c_double)]
@@ -168,9 +168,10 @@ class Model:
     p_exponent: float = 1.0
     p_gpu_active_w: float = 87.0
     dram_w_per_gbps: float = 0.5
+    observe: int = 0              # 0 closed loop (A14); 1 open loop: a recorded throughput observed as is (A30)
 
     def c(self) -> c_model:
-        return c_model(self.sample_period_s, self.f_min_ghz, self.f_max_ghz, self.bw_max_gbps, self.bw_shape, 0,
+        return c_model(self.sample_period_s, self.f_min_ghz, self.f_max_ghz, self.bw_max_gbps, self.bw_shape, self.observe,
                        self.bw_knee, self.p_pkg_idle_w, self.p_core_active_w, self.p_uncore_min_w,
                        self.p_uncore_max_w, self.p_exponent, self.p_gpu_active_w, self.dram_w_per_gbps)
 

@@ -345,3 +345,21 @@ def test_active_savings_from_gpu_totals(M):
         got = M.active_savings(res.totals, 0, 1, p_idle)
         want = O.active_savings_job(rec["E"][:, 0], rec["T"][:, 0], rec["E"][:, 1], rec["T"][:, 1], p_idle)
         np.testing.assert_allclose(got, want, rtol=1e-9, atol=1e-12)
+
+
+@pytest.mark.parametrize("segments", [0, 5])
+def test_open_loop_mode(M, segments):
+    """NEXT-3 open-loop observation (magus_model.observe = 1, DESIGN A30: a recorded throughput observed as
+    is, A = D, never throttled) on the mixed-kinds set: per-trace records, 32-tick words and per-tick codes
+    equal the oracle's open-loop replay; no tick is throttled."""
+    s = SMALL["mixed-kinds"]
+    stride = (s["n"] + 3) // 4 * 4
+    tr, w = gpu_gen(M, s["seed"], s["n"], s["ns"], s["mix"], stride)
+    res = run_gpu(M, tr, w, s["policies"], s["n"], s["ns"], stride, segments=segments, dump=(0, 4),
+                  model=M.Model(observe=1))
+    rec, codes = oracle_run(tr.cpu().numpy(), w.cpu().numpy(), s["policies"], s["n"], model=O.Model(observe=1))
+    PA.compare_records(res.per_trace, rec, "open-loop")
+    assert np.array_equal(res.words, PA.pack_words(codes))
+    assert np.array_equal(res.decisions, codes[:, :4, :])
+    assert int(rec["n_thr"].sum()) == 0 and int(res.per_trace["n_thr"].sum()) == 0
+    np.testing.assert_allclose(res.totals, PA.oracle_totals(rec), rtol=1e-9, atol=1e-9)
