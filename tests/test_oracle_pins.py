@@ -473,3 +473,36 @@ def test_open_loop_flags_depend_on_the_trace_only():
     _, cb = O.replay(D, 0.6, pb, O.Model(observe=1), codes=True)
     assert np.array_equal(ca & 0x34, cb & 0x34)            # flag bit and signal bits
     assert not np.array_equal(ca & 0x81, cb & 0x81)        # while the levels do differ
+
+
+# --------------------------------------------------------------------------- NEXT-3: byte counters
+
+def test_counters_spec_examples():
+    """counts 1e9 -> 2e9 over 0.1 s is 1e10 B/s (10 GB/s); equal counts are 0 B/s; a counter
+    that drops (reset to 0) is discarded -- the round repeats the last valid throughput (A31) -- and the
+    baseline re-arms, so the next interval is measured from the reset value."""
+    counts = np.array([1_000_000_000, 2_000_000_000, 2_000_000_000, 0, 500_000_000], np.uint64)
+    thr, resets = O.counters_to_throughput(counts, period=0.1)
+    assert thr[:, 0].tolist() == [10.0, 0.0, 0.0, 5.0] and resets == 1
+    thr, resets = O.counters_to_throughput(np.array([5, 3, 1, 4_000_000_001], np.uint64), period=0.5)
+    assert thr[:, 0].tolist() == [0.0, 0.0, np.float32(8.0)] and resets == 2   # no valid interval before: 0
+
+
+def test_counters_timestamps_and_rounding():
+    """Per-row timestamps give the difference quotient over the actual intervals; a non-increasing timestamp
+    is an error; each value is the fp64 quotient rounded once to fp32 (checked against exact
+    rationals)."""
+    from fractions import Fraction as F
+    rng = np.random.default_rng(32)
+    n = 50
+    steps = rng.integers(0, 3_000_000_000, (n, 3)).astype(np.uint64)
+    counts = np.cumsum(steps, axis=0, dtype=np.uint64)
+    times = np.cumsum(rng.uniform(0.05, 0.2, n))
+    thr, resets = O.counters_to_throughput(counts, times=times)
+    assert resets == 0
+    for i in (0, 17, 48):
+        for j in range(3):
+            q = F(int(counts[i + 1, j] - counts[i, j])) / F(float(times[i + 1] - times[i])) / F(10**9)
+            assert abs(F(float(thr[i, j])) - q) <= q * F(1, 2**23)    # within half an fp32 ulp (+ fp64 rounding)
+    with pytest.raises(ValueError):
+        O.counters_to_throughput(counts, times=np.r_[times[:10], times[9], times[11:]])
