@@ -16,7 +16,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libmagus_replay.so")
-SOURCES = ["magus_replay.cu", "gen_traces.cu"]
+SOURCES = ["magus_replay.cu", "gen_traces.cu", "ingest.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

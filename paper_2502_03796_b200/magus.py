@@ -109,6 +109,9 @@ lib.magus_replay_timing_summary.restype = _S
 lib.magus_replay_timing_summary.argtypes = [C.c_void_p, C.c_int32, C.POINTER(C.c_float)]
 lib.magus_replay_destroy.restype = None
 lib.magus_replay_destroy.argtypes = [C.c_void_p]
+lib.magus_counters_to_trace.restype = _S
+lib.magus_counters_to_trace.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, C.c_int64, C.c_double,
+                                        C.c_void_p, C.c_void_p, C.c_void_p]
 lib.magus_active_savings.restype = _S
 lib.magus_active_savings.argtypes = [C.POINTER(C.c_double), C.c_int32, C.c_int32, C.c_int32, C.c_double,
                                      C.POINTER(C.c_double)]
@@ -190,6 +193,24 @@ def derive_thresholds(policy: Policy, model: Model):
     _check(lib.magus_derive_thresholds(C.byref(policy.c()), C.byref(model.c()), d, f, i))
     return dict(dinc=d[0], ddec=d[1], L=d[2], P_lo=d[3], P_hi=d[4], B_lo=f[0], B_hi=f[1], astar_lo=f[2],
                 astar_hi=f[3], s_min=i[0])
+
+
+def counters_to_trace(counts, trace, n_traces: int, period_s: float = 0.1, times=None, stream=None):
+    """NEXT-3: recorded cumulative byte counters (CUDA uint64 tensor [n_rows][stride], as int64 storage) ->
+    trace (CUDA fp32 tensor [n_rows-1][stride], GB/s); times: optional CUDA fp64 tensor [n_rows].  Returns
+    (discarded intervals, non-increasing timestamps) after synchronising the stream."""
+    import torch
+    rep = torch.zeros(2, dtype=torch.int64, device=counts.device)
+    _check(lib.magus_counters_to_trace(C.c_void_p(counts.data_ptr()),
+                                       C.c_void_p(times.data_ptr()) if times is not None else None, n_traces,
+                                       counts.shape[0], counts.shape[1], period_s, C.c_void_p(trace.data_ptr()),
+                                       C.c_void_p(rep.data_ptr()), _stream_ptr(stream)))
+    if stream is not None:
+        stream.synchronize()
+    else:
+        torch.cuda.synchronize(counts.device)
+    r = rep.cpu().tolist()
+    return int(r[0]), int(r[1])
 
 
 def active_savings(policy_totals, policy: int, baseline: int, p_idle_w: float):

@@ -363,3 +363,31 @@ def test_open_loop_mode(M, segments):
     assert np.array_equal(res.decisions, codes[:, :4, :])
     assert int(rec["n_thr"].sum()) == 0 and int(res.per_trace["n_thr"].sum()) == 0
     np.testing.assert_allclose(res.totals, PA.oracle_totals(rec), rtol=1e-9, atol=1e-9)
+
+
+@pytest.mark.parametrize("with_times", [False, True])
+def test_counters_to_trace_and_open_loop_replay(M, with_times):
+    """NEXT-3 front end: recorded byte counters (with wraps / resets, a ragged column count) -> trace on the
+    GPU equals the oracle's conversion bit for bit (A31); the open-loop replay of that trace (A30) equals the
+    oracle's open-loop replay of its own conversion."""
+    rng = np.random.default_rng(33)
+    n, rows, stride = 150, 3001, 152
+    steps = rng.integers(0, 1_700_000_000, (rows, stride)).astype(np.uint64)   # <= 19 GB/s over >= 0.09 s
+    steps[rng.random((rows, stride)) < 0.3] //= 40                              # low phases
+    counts = np.cumsum(steps, axis=0, dtype=np.uint64)
+    for i, j in sorted(zip(rng.integers(1, rows, 40), rng.integers(0, n, 40))):   # counter resets, in time
+        counts[i:, j] -= counts[i, j] - np.uint64(rng.integers(0, 1000))        # order (values stay >= 0)
+    times = np.cumsum(rng.uniform(0.09, 0.11, rows)) if with_times else None
+    want, want_resets = O.counters_to_throughput(counts, period=0.1, times=times, n_traces=n)
+    want[:, n:] = 0.0
+    dc = torch.from_numpy(counts.view(np.int64)).cuda()
+    dt = torch.from_numpy(times).cuda() if with_times else None
+    tr = torch.empty((rows - 1, stride), dtype=torch.float32, device="cuda")
+    resets, bad = M.counters_to_trace(dc, tr, n, period_s=0.1, times=dt)
+    assert bad == 0 and resets == want_resets > 0
+    assert np.array_equal(tr.cpu().numpy().view(np.uint32), want.view(np.uint32))
+    w = torch.full((n,), 0.7, dtype=torch.float32, device="cuda")
+    pols = [pol(), pol(kind=STATIC_MAX), pol(deriv_ticks=2, tune_log_capacity=6)]
+    res = run_gpu(M, tr, w, pols, n, rows - 1, stride, segments=4, model=M.Model(observe=1))
+    rec, _ = oracle_run(want, np.full(n, 0.7, np.float32), pols, n, model=O.Model(observe=1))
+    PA.compare_records(res.per_trace, rec, "counters open loop")
