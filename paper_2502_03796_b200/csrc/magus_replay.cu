@@ -576,15 +576,15 @@ static void choose_geometry(magus_replay_t* h, int n_sm, int forced_segments) {
         // enough consumer warps for `target` per SM (each warp holds 4 chains per lane, so one warp per
         // SM sub-partition already has ILP; more warps hide more latency but need more segments, and
         // every speculative segment boundary can mismatch)
-        // target: 8 warps per resident CTA, weighted over the launch groups by their warps
-        int64_t warps_per_segment = 0, wtarget = 0;
+        // target: 8 warps per resident CTA (16 per SM for the 2-CTA kinds) for EACH launch group on its
+        // own -- the groups run concurrently but their per-tick costs differ (a MAGUS group next to cheap
+        // TDP groups must still fill the GPU: cfg 5 step 1.39 -> 1.04 ms against a warp-weighted target)
+        S = 1;
         for (const LaunchGroup& g : h->groups) {
-            warps_per_segment += (int64_t)p.n_groups * g.nq;
-            wtarget += (int64_t)p.n_groups * g.nq * 8 * minb_for(g.key);
+            const int64_t wps = std::max<int64_t>(1, (int64_t)p.n_groups * g.nq);   // warps per segment
+            const int target = env_int("MAGUS_TARGET_WARPS_PER_SM", 8 * minb_for(g.key));
+            S = (int)std::max<int64_t>(S, ((int64_t)n_sm * target) / wps);
         }
-        const int target = env_int("MAGUS_TARGET_WARPS_PER_SM",
-                                   (int)(wtarget / std::max<int64_t>(1, warps_per_segment)));
-        S = (int)std::max<int64_t>(1, ((int64_t)n_sm * target) / std::max<int64_t>(1, warps_per_segment));
         const int L0 = (((N + S - 1) / S) + 31) / 32 * 32;
         if (S > 1 && L0 < 4 * W) S = std::max(1, N / (4 * W));   // segments must dwarf their warm-up
     }
