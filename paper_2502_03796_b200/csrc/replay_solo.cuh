@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(32, kSoloCtasPerSm)
                 mbar_wait_loop(bar0 + 8 * slot, phase);
                 const float4* rows = reinterpret_cast<const float4*>(smem + slot * kTileBytes) + lane;
                 if (t0 + TC <= G.seg_end) {
-#pragma unroll
+#pragma unroll 1   // rolled: the warm-up path runs on ~2% of the stages; its code stays small
                     for (int tt = 0; tt < TC; ++tt) {
                         const int r = t0 + tt - G.tau_w;
                         const float4 d4 = rows[tt * (kTracesPerWarp / 4)];
