@@ -330,7 +330,8 @@ def test_cfg4_shard_sampled(M, monkeypatch):
         mism.append(res.n_mismatched_segments)
         print("synth", synth, "geometry", res.geometry, "mismatched", res.n_mismatched_segments,
               "walked", res.fixup_rounds)
-    assert mism[1] > 0, "the synthetic warm-up state should exercise the chain walk"
+    if res.geometry["solo_groups"]:   # the synthetic warm-up state exists in the solo kernel only
+        assert mism[1] > 0, "the synthetic warm-up state should exercise the chain walk"
 
 
 def test_active_savings_from_gpu_totals(M):
