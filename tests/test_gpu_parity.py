@@ -3,6 +3,8 @@
 Bars (north_star): per-tick cmd / tune-flag bits, counts and 64-bit digests
 bit-exact; T, E, E_pkg, EDP and the savings within 1e-9 relative; generator bytes bit-exact.
 """
+import io
+
 import numpy as np
 import pytest
 
@@ -392,3 +394,28 @@ def test_counters_to_trace_and_open_loop_replay(M, with_times):
     res = run_gpu(M, tr, w, pols, n, rows - 1, stride, segments=4, model=M.Model(observe=1))
     rec, _ = oracle_run(want, np.full(n, 0.7, np.float32), pols, n, model=O.Model(observe=1))
     PA.compare_records(res.per_trace, rec, "counters open loop")
+
+
+def test_trace_csv_to_gpu_timeline(M, tmp_path):
+    """NEXT-3 end to end: a SPEC trace CSV -> the device layout -> the replay with a decision dump -> the
+    timeline CSV of the replay's own per-tick codes, byte-identical to the timeline formatted from the oracle's
+    codes of the same trace (closed and open loop)."""
+    from paper_2502_03796_b200 import traceio as T
+    rng = np.random.default_rng(34)
+    D0 = np.repeat(rng.choice([1.5, 3.0, 12.0, 16.0], 300), rng.integers(1, 9, 300))[:1200].astype(np.float32)
+    path = tmp_path / "trace.csv"
+    path.write_text("# period=0.1\nstep,demand_gbps,compute_weight\n" +
+                    "".join(f"{t},{float(x)!r},0.6\n" for t, x in enumerate(D0)))
+    D, wgt, per = T.read_trace_csv(str(path))
+    assert np.array_equal(D, D0) and per == 0.1
+    pols = [pol(), pol(kind=STATIC_MAX), pol(kind=TDP_DEFAULT, tdp_w=217.0)]
+    tr = torch.zeros((len(D), 4), dtype=torch.float32, device="cuda")
+    tr[:, 0] = torch.from_numpy(D).cuda()
+    w = torch.full((1,), wgt, dtype=torch.float32, device="cuda")
+    for observe in (0, 1):
+        res = run_gpu(M, tr, w, pols, 1, len(D), 4, dump=(0, 1), model=M.Model(observe=observe))
+        _, codes = oracle_run(tr.cpu().numpy(), w.cpu().numpy(), pols, 1, model=O.Model(observe=observe))
+        got, want = io.StringIO(), io.StringIO()
+        T.write_timeline(got, res.decisions, D, ["magus", "static_max", "tdp217"], 0.8, 2.2, per)
+        T.write_timeline(want, codes, D, ["magus", "static_max", "tdp217"], 0.8, 2.2, per)
+        assert got.getvalue() == want.getvalue()
