@@ -22,6 +22,7 @@
  *   S5.4    metrics: perf loss, pkg power saving, energy saving
  *           (pkg + GPU), EDP
  *   S6.1    jump "directly to the lower bound"
+ *   NEXT-1  wall-clock governor rounds (oracle_replay_wallclock) SPEC.md:348-362, DESIGN A32
  *
  * Where the paper is silent the readings A1-A25 of DESIGN.md section 3 apply
  * (they are cited inline as [A<n>]).  The closed-loop power/performance model
@@ -310,6 +311,149 @@ int oracle_replay_batch(const float* trace, int32_t n_traces, int64_t n_samples,
     for (int32_t i = 0; i < used; ++i) pool.emplace_back(worker);
     for (auto& th : pool) th.join();
     return used;
+}
+
+/* ====================== wall-clock governor rounds (NEXT-1) ======================
+ * The other reading of the time model (A32): the governor runs every Delta of wall time while
+ * the workload works through its trace entries; a throttled entry spans several rounds, and the governor
+ * samples the entry in progress each round.  Entry j is one Delta of work at full speed; at level f it
+ * progresses at rate r = 1 / (w + (1 - w) * D_j / A) per round (the A16 dilation) when throttled, else 1.
+ * Per round t (level f, entry e, remaining fraction rho of e):
+ *   sample   A = min(D_e, B[f]) (A14; A = D_e in open loop, A30), throttled iff A < D_e
+ *   progress u = 1 round of time: while u > 0: need = rho / r(e, f); if need > u: rho -= u * r, u = 0;
+ *            else u -= need, e += 1, rho = 1 (the next entry continues at the same level); the run ends
+ *            when e == n, the round lasting (1 - u) * Delta
+ *   energy   E_pkg += P[f] * used * Delta, E += (P[f] + P_gpu) * used * Delta, T += used * Delta
+ *   decide   the same Alg. 1 / Alg. 2 / decision / baselines as oracle_replay on this round's A
+ * Counts are per round; n_thr counts rounds whose sample was throttled.  n_rounds_out = rounds run;
+ * codes (optional, cap bytes) = the per-round code bytes of oracle_replay; the digest is over rounds.
+ * The static-max baseline is unchanged (never throttled: one entry per round, T_b = n * Delta). */
+int oracle_replay_wallclock(const float* D, int64_t n, int64_t stride, float w, const OPolicy* pol, const OModel* m,
+                            OResult* out, int64_t* n_rounds_out, uint8_t* codes, int64_t codes_cap) {
+    std::memset(out, 0, sizeof(OResult));
+    out->err_tick = -1;
+    *n_rounds_out = 0;
+    const double Delta = m->sample_period_s;
+    const float  B_hi = (float)oracle_bandwidth_at(m->f_max_ghz, m);
+    const float  B_lo = (float)oracle_bandwidth_at(m->f_min_ghz, m);
+    const double P_hi = oracle_pkg_power_at(m->f_max_ghz, m);
+    const double P_lo = oracle_pkg_power_at(m->f_min_ghz, m);
+    const double P_gpu = m->p_gpu_active_w;
+    const double wd = (double)w;
+    for (int64_t t = 0; t < n; ++t) {
+        float d = D[t * stride];
+        if (!(d >= 0.0f) || !((double)d <= m->bw_max_gbps)) {
+            out->status = 2;
+            out->err_tick = t;
+            return 2;
+        }
+    }
+    int f = (pol->kind == O_MAGUS || pol->kind == O_STATIC_MIN) ? O_LO : O_HI;
+    const int    k = pol->deriv_ticks;
+    const double direv_length = (double)k * Delta;
+    const int    C = pol->tune_log_capacity;
+    std::deque<double> mem_throughput_ls;
+    std::deque<int>    uncore_tune_ls;
+    std::vector<uint8_t> cmd_bits, ev_bits;
+    double E_pkg = 0.0, E = 0.0, T = 0.0;
+
+    int64_t e = 0;       /* entry in progress */
+    double rho = 1.0;    /* its remaining work fraction */
+    int64_t t = 0;       /* round */
+    while (e < n) {
+        /* sample the entry in progress */
+        const float De = D[e * stride];
+        const float B = (f == O_HI) ? B_hi : B_lo;
+        const float A = (m->observe == 1) ? De : ((De < B) ? De : B);
+        const bool thr = (A < De);
+        /* progress through one round of wall time at level f */
+        double u = 1.0;
+        while (u > 0.0 && e < n) {
+            const float Dc = D[e * stride];
+            const float Ac = (m->observe == 1) ? Dc : ((Dc < B) ? Dc : B);
+            double r;
+            if (Ac < Dc) r = 1.0 / (wd + (1.0 - wd) * ((double)Dc / (double)Ac));
+            else         r = 1.0;
+            const double need = rho / r;
+            if (need > u) {
+                rho = rho - u * r;
+                u = 0.0;
+            } else {
+                u = u - need;
+                e += 1;
+                rho = 1.0;
+            }
+        }
+        const double used = 1.0 - u;
+        const double P = (f == O_HI) ? P_hi : P_lo;
+        E_pkg += P * (used * Delta);
+        E += (P + P_gpu) * (used * Delta);
+        T += used * Delta;
+        out->n_hi += (f == O_HI);
+        out->n_thr += thr;
+
+        int cmd = f, sig = 0, ready = 0, event = 0, hf = 0;
+        if (pol->kind == O_MAGUS) {
+            mem_throughput_ls.push_back((double)A);
+            if ((int64_t)mem_throughput_ls.size() > k + 1) mem_throughput_ls.pop_front();
+            if ((int64_t)mem_throughput_ls.size() == k + 1) {
+                ready = 1;
+                sig = Mem_throughput_Trend_Prediction(pol->inc_threshold, pol->dec_threshold,
+                                                      mem_throughput_ls, direv_length);
+                event = (sig != 0) ? 1 : 0;
+                uncore_tune_ls.push_back(event);
+                if ((int64_t)uncore_tune_ls.size() > C) uncore_tune_ls.pop_front();
+                out->tune_events += event;
+            }
+            if ((int64_t)uncore_tune_ls.size() == C)
+                hf = high_freq_detection(pol->high_freq_threshold, uncore_tune_ls) ? 1 : 0;
+            if (hf) cmd = O_HI;
+            else if (sig == 1) cmd = O_HI;
+            else if (sig == -1) cmd = O_LO;
+            else cmd = f;
+        } else if (pol->kind == O_TDP_DEFAULT) {
+            double pkg_plus_dram = P + m->dram_w_per_gbps * (double)A;
+            double bound = (1.0 - pol->tdp_margin) * pol->tdp_w;
+            cmd = (pkg_plus_dram >= bound) ? O_LO : O_HI;
+        } else {
+            cmd = f;
+        }
+        out->lock_ticks += hf;
+        if (cmd != f) out->transitions += 1;
+        cmd_bits.push_back((uint8_t)(cmd == O_HI));
+        ev_bits.push_back((uint8_t)event);
+        if (codes && t < codes_cap) {
+            uint8_t c = 0;
+            c |= (uint8_t)(cmd == O_HI);
+            c |= (uint8_t)(ready << 1);
+            c |= (uint8_t)(event << 2);
+            c |= (uint8_t)(hf << 3);
+            c |= (uint8_t)((sig == 1 ? 1 : (sig == -1 ? 2 : 0)) << 4);
+            c |= (uint8_t)((thr ? 1 : 0) << 6);
+            c |= (uint8_t)((f == O_HI ? 1 : 0) << 7);
+            codes[t] = c;
+        }
+        f = cmd;
+        t += 1;
+    }
+    *n_rounds_out = t;
+    out->T = T;
+    out->E_pkg = E_pkg;
+    out->E = E;
+    out->EDP = E * T;
+    double T_b = 0.0;
+    for (int64_t i = 0; i < n; ++i) T_b += Delta;
+    double E_b = (P_hi + P_gpu) * T_b;
+    out->T_base = T_b;
+    out->E_base = E_b;
+    if (n > 0) {
+        out->slowdown = T / T_b - 1.0;
+        out->energy_saving = 1.0 - E / E_b;
+        out->edp_saving = 1.0 - (E * T) / (E_b * T_b);
+        out->pkg_power_saving = 1.0 - (E_pkg / T) / P_hi;
+    }
+    out->digest = oracle_digest(cmd_bits.data(), ev_bits.data(), t);
+    return 0;
 }
 
 /* ===================== recorded byte counters -> throughput (NEXT-3) =====================

@@ -80,6 +80,10 @@ def lib():
         L.oracle_active_savings_job.restype = C.c_int
         L.oracle_active_savings_job.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
                                                 C.c_double, C.POINTER(C.c_double)]
+        L.oracle_replay_wallclock.restype = C.c_int
+        L.oracle_replay_wallclock.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_float, C.POINTER(OPolicy),
+                                              C.POINTER(OModel), C.c_void_p, C.POINTER(C.c_int64), C.c_void_p,
+                                              C.c_int64]
         L.oracle_counters_to_throughput.restype = C.c_int64
         L.oracle_counters_to_throughput.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int64,
                                                     C.c_double, C.c_void_p]
@@ -236,6 +240,23 @@ def replay(D, w: float, policy: Policy, model: Model | None = None, codes: bool 
                         cbuf.ctypes.data if codes else None, 1)
     res = {n: out[n][0].item() for n in RESULT_DTYPE.names if not n.startswith("_")}
     return res, cbuf
+
+
+def replay_wallclock(D, w: float, policy: Policy, model: Model | None = None, codes: bool = False):
+    """NEXT-1 (DESIGN A32): one trace replayed with wall-clock governor rounds.  Returns (result dict with
+    'n_rounds', per-round codes or None)."""
+    model = model or Model()
+    D = np.ascontiguousarray(D, dtype=np.float32)
+    out = np.zeros(1, dtype=RESULT_DTYPE)
+    cap = 3 * len(D) + 8 if codes else 0
+    cbuf = np.zeros(max(1, cap), dtype=np.uint8)
+    nr = C.c_int64()
+    lib().oracle_replay_wallclock(D.ctypes.data, len(D), 1, float(np.float32(w)), C.byref(policy.c()),
+                                  C.byref(model.c()), out.ctypes.data, C.byref(nr),
+                                  cbuf.ctypes.data if codes else None, cap)
+    res = {n: out[n][0].item() for n in RESULT_DTYPE.names if not n.startswith("_")}
+    res["n_rounds"] = nr.value
+    return res, (cbuf[:min(nr.value, cap)] if codes else None)
 
 
 def replay_batch(trace, w, policies, model: Model | None = None, codes: bool = False, n_threads: int = 0):

@@ -506,3 +506,75 @@ def test_counters_timestamps_and_rounding():
             assert abs(F(float(thr[i, j])) - q) <= q * F(1, 2**23)    # within half an fp32 ulp (+ fp64 rounding)
     with pytest.raises(ValueError):
         O.counters_to_throughput(counts, times=np.r_[times[:10], times[9], times[11:]])
+
+
+# --------------------------------------------------------------------------- NEXT-1: wall-clock rounds (A32)
+
+B_LO = float(np.float32(20.0 * (0.8 / 2.2)))
+
+
+def test_wallclock_spec_examples():
+    """SPEC.md:356-360 (A32): at f_min with demand = 2 x B_lo and compute weight 0 an entry's work takes two
+    governor rounds; with demand <= B_lo, or compute weight 1, one round.  Static-min over n entries:
+    2n rounds and T = 2n * Delta (resp. n, n * Delta); E = (P_lo + P_gpu) * T."""
+    n = 37
+    pol = O.Policy(kind=O.STATIC_MIN)
+    r, c = O.replay_wallclock(np.full(n, 2 * B_LO, np.float32), 0.0, pol, codes=True)
+    assert r["n_rounds"] == 2 * n and r["n_thr"] == 2 * n and r["T"] == pytest.approx(2 * n * 0.1, rel=1e-14)
+    assert r["E"] == pytest.approx((116.0 + 87.0) * 2 * n * 0.1, rel=1e-14)
+    for D, w in ((np.full(n, B_LO, np.float32), 0.0), (np.full(n, 2 * B_LO, np.float32), 1.0)):
+        r, _ = O.replay_wallclock(D, w, pol)
+        assert r["n_rounds"] == n and r["T"] == pytest.approx(n * 0.1, rel=1e-14)
+    # static max is never throttled: one entry per round, T = T_base (A2)
+    D = np.random.default_rng(32).uniform(0, 20, 500).astype(np.float32)
+    r, _ = O.replay_wallclock(D, 0.3, O.Policy(kind=O.STATIC_MAX))
+    assert r["n_rounds"] == 500 and r["n_thr"] == 0 and r["T"] == pytest.approx(r["T_base"], rel=1e-14)
+
+
+def test_wallclock_static_time_conservation():
+    """A32 at a fixed level: the rounds' used time adds up to the sum of the entries' dilations, closed
+    form T = Delta * sum_j (w + (1 - w) D_j / min(D_j, B_lo)) for throttled entries (1 otherwise), and the
+    number of rounds is ceil(T / Delta) (every round but the last is whole)."""
+    rng = np.random.default_rng(33)
+    D = rng.uniform(0, 20, 2000).astype(np.float32)
+    w = 0.35
+    r, _ = O.replay_wallclock(D, w, O.Policy(kind=O.STATIC_MIN))
+    d = D.astype(np.float64)
+    dil = np.where(d > B_LO, float(np.float32(w)) + (1 - float(np.float32(w))) * d / B_LO, 1.0)
+    assert r["T"] == pytest.approx(0.1 * math.fsum(dil), rel=1e-12)
+    assert r["n_rounds"] == math.ceil(math.fsum(dil) - 1e-9)
+
+
+def test_wallclock_equals_entry_replay_when_unthrottled():
+    """A32 reduces to the per-entry replay (A14) when no round can be throttled (every D <= B_lo): one
+    entry per round, identical codes, counts, digest, T and E, for every policy kind."""
+    rng = np.random.default_rng(34)
+    D = rng.uniform(0.0, 7.0, 3000).astype(np.float32)
+    for pol in (O.Policy(), O.Policy(deriv_ticks=3, tune_log_capacity=5, high_freq_threshold=0.4),
+                O.Policy(kind=O.TDP_DEFAULT, tdp_w=217.0), O.Policy(kind=O.STATIC_MAX)):
+        a, ca = O.replay(D, 0.7, pol, codes=True)
+        b, cb = O.replay_wallclock(D, 0.7, pol, codes=True)
+        assert b["n_rounds"] == len(D) and np.array_equal(ca, cb)
+        for f in ("n_hi", "n_thr", "transitions", "tune_events", "lock_ticks", "digest", "T", "E", "E_pkg"):
+            assert a[f] == b[f], f
+
+
+@pytest.mark.parametrize("seed,w,kind,observe", [(40, 0.0, "magus", 0), (41, 0.5, "magus", 0), (42, 0.9, "magus", 0),
+                                                  (43, 0.3, "tdp", 0), (44, 0.2, "magus", 1), (45, 0.0, "static_min", 0)])
+def test_wallclock_bruteforce(seed, w, kind, observe):
+    """A32 against the independent brute force (tests/_bruteforce.py): exact rational time accounting,
+    full-prefix Alg. 1 / Alg. 2.  Piecewise-constant traces crossing B_lo (so entries span rounds, levels
+    change mid-entry, and the lock engages)."""
+    rng = np.random.default_rng(seed)
+    D = np.repeat(rng.uniform(0.5, 19.5, 60), rng.integers(3, 15, 60))[:300].astype(np.float32)
+    k, C, hf = 2, 6, 0.5
+    pk = {"magus": O.MAGUS, "tdp": O.TDP_DEFAULT, "static_min": O.STATIC_MIN}[kind]
+    pol = O.Policy(kind=pk, deriv_ticks=k, tune_log_capacity=C, high_freq_threshold=hf, tdp_w=217.0)
+    r, codes = O.replay_wallclock(D, w, pol, O.Model(observe=observe), codes=True)
+    rows, tot = BF.replay_wallclock_prefix(D, w, k, 1.0, -1.0, C, hf, kind=kind, tdp=217.0, observe=observe)
+    assert r["n_rounds"] == len(rows)
+    assert np.array_equal(codes, BF.rows_to_codes(rows))
+    for f in ("T", "E", "E_pkg"):
+        assert r[f] == pytest.approx(tot[f], rel=1e-12), f
+    if kind == "magus" and observe == 0:
+        assert r["n_thr"] > 0 and r["n_rounds"] > len(D) and r["lock_ticks"] > 0 and r["transitions"] > 5
