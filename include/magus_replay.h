@@ -98,6 +98,14 @@ typedef struct {
 #define MAGUS_F_TIMING          0x8u  /* record CUDA events around the replay kernel(s) (magus_replay_kernel_times) */
 #define MAGUS_F_TIMING_DETAIL   0x10u /* with MAGUS_F_TIMING: also around the pre-pass, fix-up and totals (each
                                          event node costs a few microseconds of the run) */
+#define MAGUS_F_WALLCLOCK       0x20u /* NEXT-1 time model (A32): the governor runs
+                                         every Delta of WALL time while each trace entry is one Delta of work at
+                                         full speed, so a throttled entry spans several governor rounds and the
+                                         governor samples the entry in progress.  Records, totals, digests and
+                                         counts are per round; MAGUS_F_DUMP_DECISIONS gets the first n_samples
+                                         rounds (a chain runs >= n_samples rounds); MAGUS_F_DUMP_WORDS is
+                                         refused; STATIC_MAX is unchanged (never throttled: one entry per
+                                         round).  Default (flag clear): one governor tick per entry (A15) */
 
 typedef struct {
     int32_t n_traces;             /* local traces in this rank's shard, >= 0 */

@@ -17,6 +17,7 @@
 #include "post_kernels.cuh"
 #include "replay_kernel.cuh"
 #include "replay_solo.cuh"
+#include "wallclock.cuh"
 
 using namespace magus;
 
@@ -391,6 +392,8 @@ struct magus_replay {
     int* d_lane_of_policy = nullptr;  // user policy -> lane policy (-1: STATIC_MAX, analytic)
     int validate_lane = -1;           // lane of the validate-only pseudo policy, if any
     TraceRec* d_rec = nullptr;
+    bool wall = false;                // MAGUS_F_WALLCLOCK: wall-clock governor rounds (A32)
+    TraceRec* d_wrec = nullptr;       // wall: [n_lane][n_traces] lane-chain records
     double* d_totals = nullptr;
     uint8_t* d_out = nullptr;         // [P][chunks][13] totals partials (fp64), then the 4 run flag words: one D2H copy
     double* d_fin = nullptr;          // world > 1: [P][13] per-policy totals, allreduced across ranks
@@ -650,6 +653,8 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
     if ((d.flags & MAGUS_F_DUMP_DECISIONS) &&
         (d.dump_first_trace < 0 || d.dump_n_traces < 0 || d.dump_first_trace + d.dump_n_traces > d.n_traces))
         return fail(nullptr, MAGUS_ERR_INVALID_ARG, "dump window outside [0, n_traces)");
+    if ((d.flags & MAGUS_F_WALLCLOCK) && (d.flags & MAGUS_F_DUMP_WORDS))
+        return fail(nullptr, MAGUS_ERR_INVALID_ARG, "MAGUS_F_DUMP_WORDS is not available with MAGUS_F_WALLCLOCK");
     if (d.tuning_warmup < 0 || d.tuning_warmup % 32 != 0)
         return fail(nullptr, MAGUS_ERR_INVALID_ARG, "tuning_warmup must be a multiple of 32");
     std::string e = validate_model(d.model);
@@ -747,7 +752,8 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
 
     std::stable_sort(h->lane.begin(), h->lane.end(),
                      [](const DevPolicy& a, const DevPolicy& b) { return ticker_key(a) < ticker_key(b); });
-    choose_geometry(h, n_sm, 0);
+    h->wall = (d.flags & MAGUS_F_WALLCLOCK) != 0;
+    choose_geometry(h, n_sm, h->wall ? 1 : 0);   // wall-clock rounds: no time segmentation
     h->n_sm = n_sm;
     h->alloc_segments = h->rp.n_seg;
     ReplayParams& p = h->rp;
@@ -802,6 +808,9 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
         p.words = nullptr;
     }
     ALLOC(h->d_rec, (size_t)std::max(1, d.n_traces) * d.n_policies);
+    if (h->wall) {
+        ALLOC(h->d_wrec, nchain);
+    }
     h->n_chunks = std::max(1, (d.n_traces + kTotThreads - 1) / kTotThreads);
     const size_t n_part = (size_t)d.n_policies * h->n_chunks * MAGUS_N_TOTALS;
     ALLOC(h->d_out, n_part * sizeof(double) + 4 * sizeof(unsigned int));
@@ -976,7 +985,12 @@ static magus_status enqueue_run(magus_replay_t* h, const float* d_trace, const f
                        seg ? h->d_first_low : (int*)nullptr, (uint32_t*)h->d_flag, 4));
     }
     if (timing) CU(h, rec(1));
-    if (has_work) {
+    if (has_work && h->wall) {
+        // wall-clock governor rounds (A32): one thread per chain, no segmentation and no fix-up
+        WallParams wp{h->d_wrec, h->d_codes, d.dump_first_trace, d.dump_n_traces, d.n_policies};
+        dim3 gw((unsigned)((d.n_traces + 127) / 128), (unsigned)p.n_lane);
+        CU(h, launch_k(magus_wallclock_kernel, gw, dim3(128), 0, s, h->pdl && !timing, p, ep, wp, d_trace));
+    } else if (has_work) {
         // launch groups (one chain kind each) run concurrently: fork onto auxiliary streams and join
         // (parallel branches when the run is captured as a graph)
         const int G = (int)h->groups.size();
@@ -1039,7 +1053,8 @@ static magus_status enqueue_run(magus_replay_t* h, const float* d_trace, const f
         // per-trace records and per-(policy, trace chunk) fixed-order partial sums (the host adds the chunks)
         CU(h, launch_k(magus_totals_kernel, dim3(d.n_policies, h->n_chunks), dim3(kTotThreads), 0, s,
                        h->pdl && !detail, p, ep, (const int*)h->d_lane_of_policy, h->validate_lane, h->digest_all_hi,
-                       (d.flags & MAGUS_F_PER_TRACE_STATS) ? 1 : 0, h->d_totals));
+                       (d.flags & MAGUS_F_PER_TRACE_STATS) ? 1 : 0, (const TraceRec*)(has_work ? h->d_wrec : nullptr),
+                       h->d_totals));
     }
     if (d.world > 1) {
         CU(h, launch_k(magus_chunk_sum_kernel, dim3(d.n_policies), dim3(32), 0, s, h->pdl && !detail,
@@ -1107,7 +1122,8 @@ extern "C" magus_status magus_replay_run(magus_replay_t* h, const float* d_trace
     if (h->d_codes && has_work) {
         const int P = d.n_policies;
         dim3 grid((unsigned)((d.dump_n_traces + 63) / 64), (unsigned)p.n_lane);
-        magus_resim_kernel<<<grid, 64, 0, s>>>(p, d_trace, d.dump_first_trace, d.dump_n_traces, P, h->d_codes);
+        if (!h->wall)   // (the wall-clock kernel writes its rounds' codes itself)
+            magus_resim_kernel<<<grid, 64, 0, s>>>(p, d_trace, d.dump_first_trace, d.dump_n_traces, P, h->d_codes);
         CU(h, cudaGetLastError());
         const int64_t rows = (int64_t)d.n_samples * d.dump_n_traces;
         for (int pi : h->smax) {
@@ -1283,8 +1299,8 @@ extern "C" magus_status magus_replay_geometry(const magus_replay_t* h, int32_t o
     const LaunchGroup& g0 = h->groups.front();
     // kernel launches of one run, as enqueue_run issues them
     const bool has_work = d.n_traces > 0 && d.n_samples > 0;
-    int nk = 1 + (has_work ? (int)h->groups.size() : 0);          // pre-pass, replay per launch group
-    if (has_work && p.n_seg > 1) {
+    int nk = 1 + (has_work ? (h->wall ? 1 : (int)h->groups.size()) : 0);   // pre-pass, replay per launch group
+    if (has_work && p.n_seg > 1 && !h->wall) {
         int nw = 0;
         for (const LaunchGroup& g : h->groups) nw += walk_kernel_for(g.key) ? 1 : 0;
         nk += 1 + nw;                                             // mark + one chain-walk kernel per launch group

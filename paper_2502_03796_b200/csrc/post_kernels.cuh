@@ -695,7 +695,8 @@ constexpr int kNTot = 13;              // MAGUS_N_TOTALS
 __global__ void __launch_bounds__(kTotThreads) magus_totals_kernel(const ReplayParams rp, const EpiParams e,
                                                                     const int* __restrict__ lane_of_policy,
                                                                     int validate_lane, uint64_t digest_all_hi,
-                                                                    int write_rec, double* __restrict__ part) {
+                                                                    int write_rec, const TraceRec* __restrict__ wrec,
+                                                                    double* __restrict__ part) {
     ptx::pdl_wait();
     const int n_traces = rp.n_traces, n_policies = e.n_policies;
     const int p = blockIdx.x, c = blockIdx.y;
@@ -709,6 +710,11 @@ __global__ void __launch_bounds__(kTotThreads) magus_totals_kernel(const ReplayP
         TraceRec r;
         if (q < 0) {   // STATIC_MAX: never throttled, no transition or tune flag (A17, A21)
             finish_record(r, e, (double)e.w[j], (int64_t)e.n_samples, 0, 0, 0, 0, 0.0, digest_all_hi);
+        } else if (wrec) {   // wall-clock rounds (A32): the chain's record as the wall-clock kernel wrote it
+            const int64_t ci = chain_idx(rp, q, j);
+            r = wrec[ci];
+            invalid |= rp.c_vmax[ci] > rp.bwbits;
+            zero_chain(rp, ci);
         } else {
             const int64_t ci = chain_idx(rp, q, j);
             finish_record(r, e, (double)e.w[j], (int64_t)rp.c_nhi[ci], (int64_t)rp.c_nthr[ci], (int64_t)rp.c_trans[ci],

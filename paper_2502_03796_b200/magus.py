@@ -25,6 +25,7 @@ STATUS_NAMES = ["MAGUS_OK", "MAGUS_ERR_INVALID_ARG", "MAGUS_ERR_CONFIG", "MAGUS_
                 "MAGUS_ERR_STATE", "MAGUS_ERR_OOM", "MAGUS_ERR_CUDA", "MAGUS_ERR_NCCL"]
 MAGUS, STATIC_MAX, STATIC_MIN, TDP_DEFAULT = 0, 1, 2, 3
 F_PER_TRACE_STATS, F_DUMP_WORDS, F_DUMP_DECISIONS, F_TIMING, F_TIMING_DETAIL = 0x1, 0x2, 0x4, 0x8, 0x10
+F_WALLCLOCK = 0x20   # NEXT-1 wall-clock governor rounds (A32)
 TOTAL_FIELDS = ["E", "E_pkg", "T", "EDP", "slowdown", "energy_saving", "edp_saving", "n_hi", "n_thr",
                 "transitions", "tune_events", "lock_ticks", "n_traces"]
 N_TOTALS = len(TOTAL_FIELDS)

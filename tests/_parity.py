@@ -84,3 +84,24 @@ def oracle_totals(ora_rec):
             out[p, i] = math.fsum(float(x) for x in ora_rec[k][:, p])
         out[p, 12] = n
     return out
+
+
+def oracle_wallclock(tr_host, w_host, policies, n_traces, model, dump=(0, 0)):
+    """NEXT-1 (A32): the oracle's wall-clock replay of every (trace, policy) chain -> (records [n][P] in the
+    oracle's record dtype, codes [n_samples][dump n][P] of the first n_samples rounds of the dump window)."""
+    from oracle import oracle as O
+    ns = tr_host.shape[0]
+    pols = oracle_policies(policies)
+    rec = np.zeros((n_traces, len(pols)), dtype=O.RESULT_DTYPE)
+    codes = np.zeros((ns, dump[1], len(pols)), np.uint8)
+    for j in range(n_traces):
+        col = np.ascontiguousarray(tr_host[:, j])
+        for p, pp in enumerate(pols):
+            want = dump[0] <= j < dump[0] + dump[1]
+            r, c = O.replay_wallclock(col, float(w_host[j]), pp, model, codes=want)
+            for f in O.RESULT_DTYPE.names:
+                if not f.startswith("_"):
+                    rec[j, p][f] = r[f]
+            if want:
+                codes[:, j - dump[0], p] = c[:ns]
+    return rec, codes

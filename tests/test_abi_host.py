@@ -149,3 +149,11 @@ def test_active_savings_host_matches_oracle():
     for bad in ((0, 1, 250.0), (0, 2, 10.0), (0, 1, -1.0), (0, 1, 160.0)):
         with pytest.raises(M.MagusError):
             M.active_savings(tot, *bad)
+
+
+def test_wallclock_flag_rejects_word_dump():
+    """NEXT-1 (A32): the per-32-tick word dump has no meaning per round; the combination is refused at create,
+    before any device work (so this holds on a CPU-only host too)."""
+    with pytest.raises(M.MagusError) as e:
+        M.Replay(8, 100, [M.Policy()], flags=M.F_WALLCLOCK | M.F_DUMP_WORDS)
+    assert e.value.status == M.ERR_INVALID_ARG and "WALLCLOCK" in str(e.value)

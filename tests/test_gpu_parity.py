@@ -419,3 +419,52 @@ def test_trace_csv_to_gpu_timeline(M, tmp_path):
         T.write_timeline(got, res.decisions, D, ["magus", "static_max", "tdp217"], 0.8, 2.2, per)
         T.write_timeline(want, codes, D, ["magus", "static_max", "tdp217"], 0.8, 2.2, per)
         assert got.getvalue() == want.getvalue()
+
+
+# ------------------------------------------------------------------------------------- NEXT-1 wall clock
+
+@pytest.mark.parametrize("name,observe", [("mixed-kinds", 0), ("cfg3-small", 0), ("cfg5-small", 0),
+                                          ("mixed-kinds", 1)])
+def test_wallclock_rounds(M, name, observe):
+    """NEXT-1 (MAGUS_F_WALLCLOCK, DESIGN A32): governor rounds of Delta wall time, throttled entries spanning
+    several rounds.  Per-(trace, policy) records (counts and digests per round, bit-exact; T / E within 1e-9),
+    the first n_samples rounds' codes of a dump window, and the totals, against the oracle's
+    oracle_replay_wallclock."""
+    s = SMALL[name]
+    n, ns = min(s["n"], 96), min(s["ns"], 4000)
+    stride = (n + 3) // 4 * 4
+    tr, w = gpu_gen(M, s["seed"], n, ns, s["mix"], stride)
+    res = run_gpu(M, tr, w, s["policies"], n, ns, stride, flags=M.F_PER_TRACE_STATS | M.F_WALLCLOCK,
+                  dump=(n - 6, 6), model=M.Model(observe=observe))
+    rec, codes = PA.oracle_wallclock(tr.cpu().numpy(), w.cpu().numpy(), s["policies"], n,
+                                     O.Model(observe=observe), dump=(n - 6, 6))
+    PA.compare_records(res.per_trace, rec, f"wallclock {name}")
+    assert np.array_equal(res.decisions, codes)
+    np.testing.assert_allclose(res.totals, PA.oracle_totals(rec), rtol=1e-9, atol=1e-9)
+    if observe == 0:
+        assert rec["T"].sum() > ns * 0.1 * n * 1.001   # entries did span rounds
+    assert res.geometry["kernels_per_run"] == 3
+
+
+def test_wallclock_edge_cases(M):
+    """A32 edge cases: one sample, a 31/33-round ragged digest block, an all-throttled static-min trace at
+    2 x B_lo with w = 0 (exactly two rounds per entry), and invalid samples still reported."""
+    b_lo = float(np.float32(20.0 * (0.8 / 2.2)))
+    pols = [pol(), pol(kind=STATIC_MIN), pol(kind=STATIC_MAX)]
+    for ns, val in ((1, 5.0), (31, 2 * b_lo), (33, 1.0), (40, 2 * b_lo)):
+        n = 4
+        tr = torch.full((ns, n), val, dtype=torch.float32, device="cuda")
+        w = torch.zeros(n, dtype=torch.float32, device="cuda")
+        res = run_gpu(M, tr, w, pols, n, ns, n, flags=M.F_PER_TRACE_STATS | M.F_WALLCLOCK, dump=(0, 2))
+        rec, codes = PA.oracle_wallclock(tr.cpu().numpy(), w.cpu().numpy(), pols, n, O.Model(), dump=(0, 2))
+        PA.compare_records(res.per_trace, rec, f"edge ns={ns}")
+        assert np.array_equal(res.decisions, codes)
+        if val == 2 * b_lo:
+            assert res.per_trace["T"][0, 1] == pytest.approx(2 * ns * 0.1, rel=1e-12)
+    tr = torch.full((50, 4), 3.0, dtype=torch.float32, device="cuda")
+    tr[17, 2] = float("nan")
+    w = torch.zeros(4, dtype=torch.float32, device="cuda")
+    with M.Replay(4, 50, PA.gpu_policies(pols), M.Model(), trace_stride=4, flags=M.F_WALLCLOCK) as R:
+        R.run(tr, w)
+        with pytest.raises(M.MagusError):
+            R.results()
