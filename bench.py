@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--ref-budget-s", type=float, default=150.0,
                     help="--impl reference: wall-time budget of warmup + steps (sizes each step's sample)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--wallclock", action="store_true", help="NEXT-1 time model: wall-clock governor rounds "
+                    "(MAGUS_F_WALLCLOCK, DESIGN.md A32); not the headline configuration")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--preroll-ms", type=float, default=600.0, help="untimed load before the timed region "
                     "so the clock samples see the GPU under load")
@@ -201,7 +203,7 @@ def run_ours(args, cfg):
         nccl_id = obj[0]
     pols = [M.Policy(**d) for d in cfg["policies"]]
     R = M.Replay(n, ns, pols, M.Model(), trace_stride=stride, global_trace_offset=offset, rank=rank, world=world,
-                 nccl_id=nccl_id, flags=M.F_TIMING)
+                 nccl_id=nccl_id, flags=M.F_TIMING | (M.F_WALLCLOCK if args.wallclock else 0))
     geo = R.geometry()
     for _ in range(max(3, args.warmup)):
         R.run(tr, w, stream)
@@ -276,7 +278,7 @@ def run_ours(args, cfg):
         del th, wh
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.wallclock:
         cpu = cpu_baseline(cfg, args.cpu_seconds)
 
     geo = R.geometry()                            # the plan actually timed (after any adaptive re-plan)
@@ -286,13 +288,15 @@ def run_ours(args, cfg):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg["name"], "n_traces_per_gpu": n, "n_samples": ns, "policies": len(pols),
+            "config": {"workload": cfg["name"] + ("+wallclock" if args.wallclock else ""), "n_traces_per_gpu": n, "n_samples": ns, "policies": len(pols),
                        "parallelism": f"trace-sharded x{world}" + (", NCCL allreduce of per-policy totals" if world > 1
                                                                     else ""),
                        "l2": "inputs 1.64 GB/GPU >> 126 MB L2; no flush needed" if ns * n * 4 > 4e8 else "L2-resident"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic,
-                         "kernel": "magus_replay_solo_kernel" if geo.get("solo_groups") else "magus_replay_kernel", "replay_ms": tsum["replay_ms"],
+                         "kernel": ("magus_wallclock_em_kernel" if args.wallclock else
+                                    "magus_replay_solo_kernel" if geo.get("solo_groups") else "magus_replay_kernel"),
+                         "replay_ms": tsum["replay_ms"],
                          "replay_ms_max_over_ranks": replay_ms_max, "bytes_per_launch": bytes_per_launch,
                          "peak_source": peak_src},
             "e2e": e2e,

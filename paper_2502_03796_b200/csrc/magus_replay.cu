@@ -136,6 +136,34 @@ ReplayKernel replay_kernel_for(int key) {
     }
 }
 
+// entry-major wall-clock kernel (wallclock.cuh, A32) of a chain kind
+typedef void (*WallKernel)(ReplayParams, EpiParams, WallParams, int, const float*);
+template <bool U>
+WallKernel wall_kernel_u(int key) {
+    switch (key) {
+        case 1: return magus_wallclock_em_kernel<MagusTicker<1, false>, U>;
+        case 2: return magus_wallclock_em_kernel<MagusTicker<2, false>, U>;
+        case 3: return magus_wallclock_em_kernel<MagusTicker<3, false>, U>;
+        case 4: return magus_wallclock_em_kernel<MagusTicker<4, false>, U>;
+        case 5: return magus_wallclock_em_kernel<MagusTicker<5, false>, U>;
+        case 6: return magus_wallclock_em_kernel<MagusTicker<6, false>, U>;
+        case 7: return magus_wallclock_em_kernel<MagusTicker<7, false>, U>;
+        case 8: return magus_wallclock_em_kernel<MagusTicker<8, false>, U>;
+        case 1000 + LANE_TDP: return magus_wallclock_em_kernel<TdpTicker, U>;
+        case 1000 + LANE_STATIC_MIN: return magus_wallclock_em_kernel<StaticMinTicker<false>, U>;
+        case 1000 + LANE_VALIDATE: return magus_wallclock_em_kernel<StaticMinTicker<false>, U>;
+        default: return key >= 100 ? magus_wallclock_em_kernel<MagusTicker<0, true>, U>
+                                   : magus_wallclock_em_kernel<MagusTicker<0, false>, U>;
+    }
+}
+// unrolled entry blocks while the run has few chains per SM (latency-bound), rolled otherwise (issue-bound;
+// the unrolled code also misses the instruction cache); MAGUS_WALL_UNROLL=0/1 forces one
+WallKernel wall_kernel_for(int key, int64_t n_chains, int n_sm) {
+    const int f = env_int("MAGUS_WALL_UNROLL", -1);
+    const bool u = f >= 0 ? f != 0 : n_chains < (int64_t)n_sm * 128;
+    return u ? wall_kernel_u<true>(key) : wall_kernel_u<false>(key);
+}
+
 // one-warp-CTA replay kernel (replay_solo.cuh) of a chain kind, or nullptr if it has none
 ReplayKernel solo_kernel_for(int key) {
     const int v = env_int("MAGUS_SOLO_BAL", 2);   // stage block variant (replay_solo.cuh)
@@ -985,11 +1013,30 @@ static magus_status enqueue_run(magus_replay_t* h, const float* d_trace, const f
                        seg ? h->d_first_low : (int*)nullptr, (uint32_t*)h->d_flag, 4));
     }
     if (timing) CU(h, rec(1));
-    if (has_work && h->wall) {
-        // wall-clock governor rounds (A32): one thread per chain, no segmentation and no fix-up
+    if (has_work && h->wall && env_int("MAGUS_WALL_ROUNDMAJOR", 0)) {
+        // wall-clock governor rounds (A32), the loop as written: one thread per chain, every lane
         WallParams wp{h->d_wrec, h->d_codes, d.dump_first_trace, d.dump_n_traces, d.n_policies};
         dim3 gw((unsigned)((d.n_traces + 127) / 128), (unsigned)p.n_lane);
         CU(h, launch_k(magus_wallclock_kernel, gw, dim3(128), 0, s, h->pdl && !timing, p, ep, wp, d_trace));
+    } else if (has_work && h->wall) {
+        // wall-clock governor rounds (A32), entry-major: one thread per chain, one kernel per chain kind
+        // (launch group), the groups concurrent; no segmentation and no fix-up
+        WallParams wp{h->d_wrec, h->d_codes, d.dump_first_trace, d.dump_n_traces, d.n_policies};
+        const int G = (int)h->groups.size();
+        if (G > 1) {
+            CU(h, cudaEventRecord(h->fork_ev, s));
+            for (int g = 1; g < G; ++g) CU(h, cudaStreamWaitEvent(h->aux[g - 1], h->fork_ev, 0));
+        }
+        for (int gi = 0; gi < G; ++gi) {
+            const LaunchGroup& g = h->groups[gi];
+            dim3 gw((unsigned)((d.n_traces + 127) / 128), (unsigned)g.nq);
+            CU(h, launch_k(wall_kernel_for(g.key, (int64_t)d.n_traces * p.n_lane, h->n_sm), gw, dim3(128), 0, gi == 0 ? s : h->aux[gi - 1],
+                           h->pdl && G == 1 && !timing, p, ep, wp, g.q_base, d_trace));
+        }
+        for (int g = 1; g < G; ++g) {
+            CU(h, cudaEventRecord(h->join_ev[g - 1], h->aux[g - 1]));
+            CU(h, cudaStreamWaitEvent(s, h->join_ev[g - 1], 0));
+        }
     } else if (has_work) {
         // launch groups (one chain kind each) run concurrently: fork onto auxiliary streams and join
         // (parallel branches when the run is captured as a graph)
@@ -1299,7 +1346,8 @@ extern "C" magus_status magus_replay_geometry(const magus_replay_t* h, int32_t o
     const LaunchGroup& g0 = h->groups.front();
     // kernel launches of one run, as enqueue_run issues them
     const bool has_work = d.n_traces > 0 && d.n_samples > 0;
-    int nk = 1 + (has_work ? (h->wall ? 1 : (int)h->groups.size()) : 0);   // pre-pass, replay per launch group
+    const int nwall = env_int("MAGUS_WALL_ROUNDMAJOR", 0) ? 1 : (int)h->groups.size();
+    int nk = 1 + (has_work ? (h->wall ? nwall : (int)h->groups.size()) : 0);   // pre-pass, replay per launch group
     if (has_work && p.n_seg > 1 && !h->wall) {
         int nw = 0;
         for (const LaunchGroup& g : h->groups) nw += walk_kernel_for(g.key) ? 1 : 0;

@@ -130,7 +130,219 @@ __device__ void wallclock_chain(const ReplayParams& p, const EpiParams& e, const
     p.c_vmax[ci] = invalid ? 0xFFFFFFFFu : 0u;   // the totals kernel's invalid-sample test (A17)
 }
 
-// grid (ceil(n_traces / 128), n_lane), 128 threads: thread = chain (lane q = blockIdx.y, trace j).
+// Entry-major form of the same rounds (the default): the loop runs over trace ENTRIES, in the same order
+// for every thread of a warp, so the warp's loads of an entry row are coalesced and can be issued a block of
+// kWallPf entries ahead; the rounds that start inside an entry are an inner loop.  An entry takes at least
+// one round (need = rho / r >= rho and r <= 1), so a round ends at most once per entry boundary and the
+// round-start sample is the entry in progress when `fresh` is set.  Same operations in the same order as
+// the round-major loop above and the oracle, hence the same bits.
+constexpr int kWallPf = 8;
+
+template <class T>
+struct WallChain {
+    typename T::State s;
+    double u = 1.0;          // time left in the current round
+    bool fresh = true;       // the next consumption starts a round
+    float De = 0.0f;         // the round's sample (entry in progress at its start)
+    int64_t t = 0;           // rounds finished
+    double Tw = 0.0, Epkg = 0.0, Ew = 0.0;
+    uint32_t nhi = 0, nthr = 0, trans = 0, nev = 0, lock = 0;
+    uint32_t wc = 0, we = 0, dc = 0, de = 0;
+    bool invalid = false;
+
+    // end of a round: its time and energy at the level in effect, then the governor's decision on De
+    __device__ __forceinline__ void end_round(const ReplayParams& p, const EpiParams& e, const WallParams& wp,
+                                              const DevPolicy& pol, bool dump, int j) {
+        const uint32_t lvl = T::level(s);
+        const double used = __dsub_rn(1.0, u);
+        const double P = lvl ? e.P_hi : e.P_lo;
+        const double dt = __dmul_rn(used, e.Delta);
+        Epkg = __dadd_rn(Epkg, __dmul_rn(P, dt));
+        Ew = __dadd_rn(Ew, __dmul_rn(__dadd_rn(P, e.P_gpu), dt));
+        Tw = __dadd_rn(Tw, dt);
+        const bool ready = t >= pol.k, lfull = t >= pol.k + pol.C - 1;
+        const TickOut o = T::template tick<true>(s, De, pol, p.B_lo, p.B_hi, ready, lfull);
+        nhi += lvl;
+        nthr += o.thr;
+        trans += (o.cmd != lvl) ? 1u : 0u;
+        nev += o.ev;
+        lock += o.hf;
+        const int bit = 31 - (int)(t & 31);
+        wc |= o.cmd << bit;
+        we |= o.ev << bit;
+        if (bit == 0) {
+            const uint2 key = digest_key((uint64_t)(t >> 5));
+            dc += wc * key.x;
+            de += we * key.y;
+            wc = we = 0;
+        }
+        if (dump && t < p.n_samples) {
+            const uint32_t c = o.cmd | ((T::kWarmupRules && ready) ? 2u : 0u) | (o.ev << 2) | (o.hf << 3) |
+                               (o.sig << 4) | (o.thr << 6) | (lvl << 7);
+            wp.codes[(t * wp.n_win + (j - wp.first)) * wp.P + pol.policy_index] = (uint8_t)c;
+        }
+        t += 1;
+        u = 1.0;
+        fresh = true;
+    }
+
+    // rate of entry D at level lvl (A32): 1 unless throttled; r = 1 / (w + (1 - w) * (D / A))
+    __device__ __forceinline__ static double rate(float D, uint32_t lvl, const ReplayParams& p, double wd,
+                                                  double one_m_w) {
+        const float A = fminf(D, lvl ? p.B_hi : p.B_lo);
+        if (A < D) return __ddiv_rn(1.0, __dadd_rn(wd, __dmul_rn(one_m_w, __ddiv_rn((double)D, (double)A))));
+        return 1.0;
+    }
+
+    // one whole entry, the round-end call sites apart (a round split inside the entry / a round ending with
+    // it): longer code but a shorter dependent path; used by the unrolled (latency-bound) blocks
+    __device__ __forceinline__ void entry_split(float Dc, const ReplayParams& p, const EpiParams& e,
+                                                const WallParams& wp, const DevPolicy& pol, bool dump, int j,
+                                                float bw_max, double wd, double one_m_w) {
+        const bool ok = Dc >= 0.0f && Dc <= bw_max;
+        invalid |= !ok;   // reported by the totals kernel (A17); r = 1 keeps the loop finite
+        double r = ok ? rate(Dc, T::level(s), p, wd, one_m_w) : 1.0;
+        double rho = 1.0;
+        for (;;) {
+            if (fresh) {
+                De = Dc;
+                fresh = false;
+            }
+            const double need = r == 1.0 ? rho : __ddiv_rn(rho, r);   // (rho / 1.0 == rho exactly)
+            if (need > u) {
+                rho = __dsub_rn(rho, __dmul_rn(u, r));
+                u = 0.0;
+                end_round(p, e, wp, pol, dump, j);
+                if (ok) r = rate(Dc, T::level(s), p, wd, one_m_w);   // the next round's level
+            } else {
+                u = __dsub_rn(u, need);
+                if (u == 0.0) end_round(p, e, wp, pol, dump, j);      // the round ends with the entry
+                return;
+            }
+        }
+    }
+
+    // one whole entry (one copy of the round end and of the rate in the code)
+    __device__ __forceinline__ void entry(float Dc, const ReplayParams& p, const EpiParams& e, const WallParams& wp,
+                                          const DevPolicy& pol, bool dump, int j, float bw_max, double wd,
+                                          double one_m_w) {
+        const bool ok = Dc >= 0.0f && Dc <= bw_max;
+        invalid |= !ok;   // reported by the totals kernel (A17); r = 1 keeps the loop finite
+        double rho = 1.0, r = 1.0;
+        bool need_rate = ok;
+        for (;;) {
+            if (fresh) {
+                De = Dc;
+                fresh = false;
+            }
+            if (need_rate) {   // at the entry's start and after a round end (the level may have changed)
+                r = rate(Dc, T::level(s), p, wd, one_m_w);
+                need_rate = false;
+            }
+            const double need = r == 1.0 ? rho : __ddiv_rn(rho, r);   // (rho / 1.0 == rho exactly)
+            bool done, ends;
+            if (need > u) {
+                rho = __dsub_rn(rho, __dmul_rn(u, r));
+                u = 0.0;
+                done = false;
+                ends = true;
+            } else {
+                u = __dsub_rn(u, need);
+                done = true;
+                ends = u == 0.0;   // the round ends with the entry
+            }
+            if (ends) {
+                end_round(p, e, wp, pol, dump, j);
+                need_rate = ok;
+            }
+            if (done) return;
+        }
+    }
+};
+
+template <class T, bool UNROLL>
+__device__ __forceinline__ void wallclock_chain_em(const ReplayParams& p, const EpiParams& e, const WallParams& wp,
+                                                   const DevPolicy& pol, int64_t ci, int j,
+                                                   const float* __restrict__ trace) {
+    WallChain<T> c;
+    T::init(c.s, pol, true);
+    const int64_t n = p.n_samples, stride = p.trace_stride;
+    const float bw_max = __uint_as_float(p.bwbits);
+    const double wd = (double)e.w[j];
+    const double one_m_w = __dsub_rn(1.0, wd);
+    const bool dump = wp.codes != nullptr && j >= wp.first && j < wp.first + wp.n_win && pol.policy_index >= 0;
+    float cur[kWallPf], nxt[kWallPf];
+#pragma unroll
+    for (int i = 0; i < kWallPf; ++i) cur[i] = i < n ? __ldcs(trace + i * stride + j) : 0.0f;
+    for (int64_t b = 0; b < n; b += kWallPf) {
+#pragma unroll
+        for (int i = 0; i < kWallPf; ++i) {   // the next block's rows, in flight while this block runs
+            const int64_t x = b + kWallPf + i;
+            nxt[i] = x < n ? __ldcs(trace + x * stride + j) : 0.0f;
+        }
+        if (UNROLL && b + kWallPf <= n) {
+            // few chains (latency-bound): the block's entries unrolled, so independent work of neighbouring
+            // entries can overlap
+#pragma unroll
+            for (int i = 0; i < kWallPf; ++i) c.entry_split(cur[i], p, e, wp, pol, dump, j, bw_max, wd, one_m_w);
+        } else {
+            // many chains (issue-bound) and the ragged tail: rolled, one copy of the entry in the code
+            const int m = (int)min((int64_t)kWallPf, n - b);
+#pragma unroll 1
+            for (int i = 0; i < m; ++i) {
+                c.entry(cur[0], p, e, wp, pol, dump, j, bw_max, wd, one_m_w);
+#pragma unroll
+                for (int z = 0; z < kWallPf - 1; ++z) cur[z] = cur[z + 1];
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < kWallPf; ++i) cur[i] = nxt[i];
+    }
+    if (!c.fresh) c.end_round(p, e, wp, pol, dump, j);   // the last, partial round
+    if (c.t & 31) {                                       // partial last digest block, zero-padded
+        const uint2 key = digest_key((uint64_t)(c.t >> 5));
+        c.dc += c.wc * key.x;
+        c.de += c.we * key.y;
+    }
+    TraceRec r;
+    const double T_b = __dmul_rn((double)n, e.Delta);
+    const double E_b = __dmul_rn(__dadd_rn(e.P_hi, e.P_gpu), T_b);
+    r.n_hi = c.nhi;
+    r.n_thr = c.nthr;
+    r.transitions = c.trans;
+    r.tune_events = c.nev;
+    r.lock_ticks = c.lock;
+    r.T = c.Tw;
+    r.E_pkg = c.Epkg;
+    r.E = c.Ew;
+    r.EDP = c.Ew * c.Tw;
+    if (n > 0) {
+        r.slowdown = c.Tw / T_b - 1.0;
+        r.energy_saving = 1.0 - c.Ew / E_b;
+        r.edp_saving = 1.0 - (c.Ew * c.Tw) / (E_b * T_b);
+        r.pkg_power_saving = 1.0 - (c.Epkg / c.Tw) / e.P_hi;
+    } else {
+        r.slowdown = r.energy_saving = r.edp_saving = r.pkg_power_saving = 0.0;
+    }
+    r.digest = digest_pack(c.dc, c.de);
+    wp.wrec[ci] = r;
+    p.c_vmax[ci] = c.invalid ? 0xFFFFFFFFu : 0u;
+}
+
+// Entry-major kernel of one chain kind: grid (ceil(n_traces / 128), lanes of the launch group), 128 threads.
+template <class T, bool UNROLL>
+__global__ void __launch_bounds__(128) magus_wallclock_em_kernel(const ReplayParams p, const EpiParams e,
+                                                                 const WallParams wp, int q_base,
+                                                                 const float* __restrict__ trace) {
+    ptx::pdl_wait();
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int q = q_base + blockIdx.y;
+    if (j >= p.n_traces) return;
+    const DevPolicy pol = p.pol[q];
+    wallclock_chain_em<T, UNROLL>(p, e, wp, pol, chain_idx(p, q, j), j, trace);
+}
+
+// Round-major kernel (MAGUS_WALL_ROUNDMAJOR=1; the A32 loop as written): grid (ceil(n_traces / 128), n_lane), 128 threads: thread = chain (lane q = blockIdx.y, trace j).
 __global__ void __launch_bounds__(128) magus_wallclock_kernel(const ReplayParams p, const EpiParams e,
                                                               const WallParams wp, const float* __restrict__ trace) {
     ptx::pdl_wait();

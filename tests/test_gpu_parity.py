@@ -423,13 +423,16 @@ def test_trace_csv_to_gpu_timeline(M, tmp_path):
 
 # ------------------------------------------------------------------------------------- NEXT-1 wall clock
 
+@pytest.mark.parametrize("roundmajor,unroll", [(0, 0), (0, 1), (1, 0)])
 @pytest.mark.parametrize("name,observe", [("mixed-kinds", 0), ("cfg3-small", 0), ("cfg5-small", 0),
                                           ("mixed-kinds", 1)])
-def test_wallclock_rounds(M, name, observe):
+def test_wallclock_rounds(M, name, observe, roundmajor, unroll, monkeypatch):
     """NEXT-1 (MAGUS_F_WALLCLOCK, DESIGN A32): governor rounds of Delta wall time, throttled entries spanning
     several rounds.  Per-(trace, policy) records (counts and digests per round, bit-exact; T / E within 1e-9),
     the first n_samples rounds' codes of a dump window, and the totals, against the oracle's
     oracle_replay_wallclock."""
+    monkeypatch.setenv("MAGUS_WALL_ROUNDMAJOR", str(roundmajor))   # entry-major kernels (default) / the A32 loop
+    monkeypatch.setenv("MAGUS_WALL_UNROLL", str(unroll))           # rolled / unrolled entry blocks
     s = SMALL[name]
     n, ns = min(s["n"], 96), min(s["ns"], 4000)
     stride = (n + 3) // 4 * 4
@@ -443,7 +446,8 @@ def test_wallclock_rounds(M, name, observe):
     np.testing.assert_allclose(res.totals, PA.oracle_totals(rec), rtol=1e-9, atol=1e-9)
     if observe == 0:
         assert rec["T"].sum() > ns * 0.1 * n * 1.001   # entries did span rounds
-    assert res.geometry["kernels_per_run"] == 3
+    if roundmajor:
+        assert res.geometry["kernels_per_run"] == 3
 
 
 def test_wallclock_edge_cases(M):
