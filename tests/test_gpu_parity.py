@@ -472,3 +472,25 @@ def test_wallclock_edge_cases(M):
         R.run(tr, w)
         with pytest.raises(M.MagusError):
             R.results()
+
+
+@pytest.mark.parametrize("cfg", [2, 5])
+def test_wallclock_full_size_sampled(M, cfg):
+    """NEXT-1 (A32) at BASELINE.json full sizes in the launch configuration `bench.py --wallclock` times
+    (entry-major kernels, unrolled for these chain counts): the oracle regenerates sampled traces (both ends
+    included) and replays them in wall-clock rounds; counts and digests bit-exact, T / E within 1e-9."""
+    c = CONFIGS[cfg]
+    n, ns = c["n_traces"], c["n_samples"]
+    tr, w = gpu_gen(M, c["seed"], n, ns, c["class_mix"], c["stride"])
+    res = run_gpu(M, tr, w, c["policies"], n, ns, c["stride"], flags=M.F_PER_TRACE_STATS | M.F_WALLCLOCK)
+    del tr
+    rng = np.random.default_rng(100 + cfg)
+    ids = np.unique(np.r_[rng.choice(n, 8, replace=False), [0, n - 1]])
+    desc = O.GenDesc(seed=c["seed"], n_traces=n, n_samples=ns, class_mix=c["class_mix"])
+    cols = [O.gen_trace(desc, int(j)) for j in ids]            # the oracle's own generator, trace by trace
+    otr = np.stack([col for col, _ in cols], axis=1)
+    ow = np.array([wj for _, wj in cols], np.float32)
+    rec, _ = PA.oracle_wallclock(otr, ow, c["policies"], len(ids), O.Model())
+    PA.compare_records(res.per_trace[ids], rec, f"wallclock cfg{cfg}")
+    np.testing.assert_allclose(res.totals, PA.oracle_totals(res.per_trace), rtol=1e-9)
+    assert rec["T"].sum() > rec["T_base"].sum()   # throttled entries spanned rounds
