@@ -494,3 +494,23 @@ def test_wallclock_full_size_sampled(M, cfg):
     PA.compare_records(res.per_trace[ids], rec, f"wallclock cfg{cfg}")
     np.testing.assert_allclose(res.totals, PA.oracle_totals(res.per_trace), rtol=1e-9)
     assert rec["T"].sum() > rec["T_base"].sum()   # throttled entries spanned rounds
+
+
+@pytest.mark.parametrize("unroll", [0, 1])
+def test_wallclock_window_and_log_sizes(M, unroll, monkeypatch):
+    """NEXT-1 (A32) through every ticker the wall-clock kernels instantiate: register rings k = 3, 5, 7, the
+    generic ring (k = 9, 16), the 64-bit tune log (C = 33, 64), TDP at 270 W, static min; records and codes
+    against the oracle."""
+    monkeypatch.setenv("MAGUS_WALL_UNROLL", str(unroll))
+    n, ns = 70, 3000
+    tr, w = gpu_gen(M, 77, n, ns, 1, 72)
+    pols = [pol(deriv_ticks=3, tune_log_capacity=5, high_freq_threshold=0.5, inc_threshold=0.5, dec_threshold=-0.5),
+            pol(deriv_ticks=5, tune_log_capacity=7), pol(deriv_ticks=7, tune_log_capacity=12),
+            pol(deriv_ticks=9, tune_log_capacity=10), pol(deriv_ticks=16, tune_log_capacity=33, high_freq_threshold=0.5),
+            pol(deriv_ticks=3, tune_log_capacity=64, high_freq_threshold=0.3),
+            pol(kind=TDP_DEFAULT, tdp_w=270.0), pol(kind=STATIC_MIN)]
+    res = run_gpu(M, tr, w, pols, n, ns, 72, flags=M.F_PER_TRACE_STATS | M.F_WALLCLOCK, dump=(0, 3))
+    rec, codes = PA.oracle_wallclock(tr.cpu().numpy(), w.cpu().numpy(), pols, n, O.Model(), dump=(0, 3))
+    PA.compare_records(res.per_trace, rec, "wallclock k/C")
+    assert np.array_equal(res.decisions, codes)
+    assert rec["lock_ticks"].sum() > 0 and rec["n_thr"].sum() > 0
