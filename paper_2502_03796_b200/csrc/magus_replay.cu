@@ -1356,8 +1356,15 @@ extern "C" magus_status magus_replay_geometry(const magus_replay_t* h, int32_t o
     nk += 1 + (d.world > 1 ? 1 : 0);                              // totals (+ chunk sums before the allreduce)
     int solo = 0;
     for (const LaunchGroup& g : h->groups) solo += g.solo ? 1 : 0;
+    int32_t threads = g0.threads, smem = (int32_t)g0.smem;
+    if (h->wall) {   // the wall-clock kernels (A32): one 128-thread CTA per 128 chains of a launch group
+        ctas = ((d.n_traces + 127) / 128) * p.n_lane;   // (the launch groups partition the lanes)
+        threads = 128;
+        smem = 0;
+        solo = 0;
+    }
     const int32_t v[16] = {p.n_seg, p.seg_len, p.warmup, g0.ng, g0.npw, g0.n_tblocks, g0.n_pblocks, ctas,
-                           g0.threads, (int32_t)g0.smem, p.n_lane, (int32_t)h->groups.size(), nk, solo, 0, 0};
+                           threads, smem, p.n_lane, (int32_t)h->groups.size(), nk, solo, 0, 0};
     std::memcpy(out, v, sizeof(v));
     return MAGUS_OK;
 }

@@ -448,6 +448,8 @@ def test_wallclock_rounds(M, name, observe, roundmajor, unroll, monkeypatch):
         assert rec["T"].sum() > ns * 0.1 * n * 1.001   # entries did span rounds
     if roundmajor:
         assert res.geometry["kernels_per_run"] == 3
+    assert res.geometry["threads_per_cta"] == 128 and res.geometry["solo_groups"] == 0
+    assert res.geometry["ctas"] == (n + 127) // 128 * res.geometry["lane_policies"]
 
 
 def test_wallclock_edge_cases(M):
