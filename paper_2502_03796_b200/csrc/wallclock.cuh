@@ -136,7 +136,10 @@ __device__ void wallclock_chain(const ReplayParams& p, const EpiParams& e, const
 // one round (need = rho / r >= rho and r <= 1), so a round ends at most once per entry boundary and the
 // round-start sample is the entry in progress when `fresh` is set.  Same operations in the same order as
 // the round-major loop above and the oracle, hence the same bits.
-constexpr int kWallPf = 8;
+#ifndef MAGUS_WALL_PF
+#define MAGUS_WALL_PF 8
+#endif
+constexpr int kWallPf = MAGUS_WALL_PF;   // entries per prefetched block
 
 template <class T>
 struct WallChain {
