@@ -150,6 +150,14 @@ def test_empty_inputs(M):
     assert np.all(res.per_trace["T"] == 0) and np.all(res.per_trace["n_hi"] == 0)
     res = run_gpu(M, tr, w, CONFIGS[2]["policies"], 0, 100, 4)
     assert np.all(res.totals == 0)
+    # the same in the wall-clock time model (A32): no rounds, zero records and totals
+    pols = CONFIGS[5]["policies"]
+    res = run_gpu(M, tr, w, pols, 3, 0, 4, flags=M.F_PER_TRACE_STATS | M.F_WALLCLOCK)
+    rec, _ = PA.oracle_wallclock(np.zeros((0, 3), np.float32), np.zeros(3, np.float32), pols, 3, O.Model())
+    PA.compare_records(res.per_trace, rec, "wallclock n_samples=0")
+    assert np.all(res.per_trace["T"] == 0) and np.all(res.per_trace["digest"] == 0)
+    res = run_gpu(M, tr, w, pols, 0, 100, 4, flags=M.F_WALLCLOCK)
+    assert np.all(res.totals == 0)
 
 
 def test_handwritten_trace_through_gpu(M):
