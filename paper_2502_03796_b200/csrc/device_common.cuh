@@ -44,6 +44,7 @@ struct ReplayParams {
     int32_t n_lane;        // Q lane policies (state / statistics arrays are indexed by lane 0..Q-1)
     int32_t q_base, nq;    // lanes covered by the current replay launch (all of one chain kind)
     int32_t n_seg, seg_len, warmup;
+    int32_t seg_long;      // the first seg_long segments are seg_len + 32 ticks long (CTA balance), the rest seg_len
     int32_t n_groups;      // ceil(n_traces / 128)
     int32_t ng, npw;       // CTA: ng tile groups x npw policy warps (+1 producer warp)
     int32_t n_tblocks, n_pblocks;
@@ -94,6 +95,15 @@ __host__ __device__ __forceinline__ int64_t st_idx(const ReplayParams& p, int e,
 }
 __host__ __device__ __forceinline__ int64_t ring_idx(const ReplayParams& p, int e, int q, int s, int r, int j) {
     return (((int64_t)(e * p.n_lane + q) * p.n_seg + s) * p.kr + r) * p.n_traces + j;
+}
+// Time segment s covers ticks [seg_begin(s), seg_finish(s)): every boundary is a
+// multiple of 32 (the digest / word blocks).
+__host__ __device__ __forceinline__ int seg_begin(const ReplayParams& p, int s) {
+    return s * p.seg_len + 32 * (s < p.seg_long ? s : p.seg_long);
+}
+__host__ __device__ __forceinline__ int seg_finish(const ReplayParams& p, int s) {
+    const int e = seg_begin(p, s + 1);
+    return e < p.n_samples ? e : p.n_samples;
 }
 __host__ __device__ __forceinline__ int64_t chain_idx(const ReplayParams& p, int q, int j) {
     return (int64_t)q * p.n_traces + j;

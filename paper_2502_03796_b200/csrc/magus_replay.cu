@@ -599,6 +599,8 @@ static void choose_geometry(magus_replay_t* h, int n_sm, int forced_segments) {
     int base = 0;   // CTAs per segment over all launch groups
     for (const LaunchGroup& g : h->groups) base += g.n_tblocks * g.n_pblocks;
     int S = 1;
+    int S_auto = 0;   // the automatic plan's segment count before rounding to 32-tick multiples
+    p.seg_long = 0;
     if (forced_segments > 0) {
         S = forced_segments;
     } else if (d.tuning_segments > 0) {
@@ -618,6 +620,7 @@ static void choose_geometry(magus_replay_t* h, int n_sm, int forced_segments) {
         }
         const int L0 = (((N + S - 1) / S) + 31) / 32 * 32;
         if (S > 1 && L0 < 4 * W) S = std::max(1, N / (4 * W));   // segments must dwarf their warm-up
+        S_auto = S;
     }
     // the solo kernel's per-segment counters are exact fp32 integers: segments of at most 2^24 ticks
     S = std::max(S, (N + (1 << 24) - 1) >> 24);
@@ -627,6 +630,18 @@ static void choose_geometry(magus_replay_t* h, int n_sm, int forced_segments) {
     if (S > 1 && L < W) {   // forced segmentation too fine for the warm-up: fall back to fewer segments
         L = ((W + 31) / 32) * 32;
         S = (N + L - 1) / L;
+    }
+    // CTA balance: rounding the length up to 32 ticks can drop the count below the plan (config 2: 74 ->
+    // 73 segments, 2,336 CTAs on 2,368 slots, so most SMs run 16 full CTAs while the mean is 15.8).  Keep
+    // the planned count with two lengths instead: the first seg_long segments 32 ticks longer.
+    if (S_auto > S && S_auto <= N / 32 && env_int("MAGUS_SEG_BALANCE", 1)) {
+        const int Lb = (N / S_auto) / 32 * 32;
+        const int extra = (N - S_auto * Lb + 31) / 32;   // < S_auto: N / S_auto - Lb < 32
+        if (Lb >= 32 && Lb >= W && Lb + 32 <= (1 << 24)) {
+            S = S_auto;
+            L = Lb;
+            p.seg_long = extra;
+        }
     }
     p.n_seg = std::max(1, S);
     p.seg_len = L;
@@ -1253,6 +1268,7 @@ extern "C" magus_status magus_replay_results(magus_replay_t* h, magus_results* o
             ReplayParams np = keep;
             np.n_seg = h->rp.n_seg;
             np.seg_len = h->rp.seg_len;
+            np.seg_long = h->rp.seg_long;
             np.warmup = h->rp.warmup;
             h->rp = np;
             for (const LaunchGroup& g : h->groups)

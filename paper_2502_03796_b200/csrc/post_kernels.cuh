@@ -103,8 +103,8 @@ __global__ void __launch_bounds__(256) magus_fix_mark_kernel(const ReplayParams 
 template <class T>
 __device__ bool rerun_segment(const ReplayParams& p, const DevPolicy& pol, int q, int s, int j, const float* trace,
                               typename T::State& tru, typename T::State& spec) {
-    const int seg_start = s * p.seg_len;
-    const int seg_end = min(seg_start + p.seg_len, p.n_samples);
+    const int seg_start = seg_begin(p, s);
+    const int seg_end = seg_finish(p, s);
     SegStats dt, dp;
     dt.zero();
     dp.zero();
@@ -210,8 +210,8 @@ __device__ __forceinline__ void walk_block(MagusState<K, false>& tru, MagusState
 template <int K>
 __device__ bool rerun_segment_walk(const ReplayParams& p, const DevPolicy& pol, int q, int s, int j,
                                    const float* trace, MagusState<K, false>& tru, MagusState<K, false>& spec) {
-    const int seg_start = s * p.seg_len;
-    const int seg_end = min(seg_start + p.seg_len, p.n_samples);
+    const int seg_start = seg_begin(p, s);
+    const int seg_end = seg_finish(p, s);
     const double Blo_d = (double)p.B_lo;
     const uint32_t bitc = 1u << (pol.C - 1);
     SegStats dt, dp;
@@ -407,7 +407,7 @@ __global__ void __launch_bounds__(32) magus_fix_lockstep_kernel(const ReplayPara
         }
         if (!__any_sync(0xffffffffu, walking)) continue;
         walked += walking ? 1 : 0;
-        const int seg_start = s * p.seg_len, seg_end = min(seg_start + p.seg_len, p.n_samples);
+        const int seg_start = seg_begin(p, s), seg_end = seg_finish(p, s);
         SegStats ss[2];
         ss[0].zero();
         ss[1].zero();
@@ -569,7 +569,7 @@ __global__ void __launch_bounds__(64) magus_fix_split_kernel(const ReplayParams 
         if (role == 1) walking = (x[lane].flags & 1u) != 0u;
         if (!__any_sync(0xffffffffu, walking)) continue;   // the same answer in both warps
         walked += walking ? 1 : 0;
-        const int seg_start = s * p.seg_len, seg_end = min(seg_start + p.seg_len, p.n_samples);
+        const int seg_start = seg_begin(p, s), seg_end = seg_finish(p, s);
         SegStats ss;
         ss.zero();
         float lock = 0.f, nthr = 0.f;

@@ -39,8 +39,8 @@ struct SegGeom {
 template <int TC>
 __device__ __forceinline__ SegGeom seg_geom(const ReplayParams& p, int seg) {
     SegGeom g;
-    g.seg_start = seg * p.seg_len;
-    g.seg_end = min(g.seg_start + p.seg_len, p.n_samples);
+    g.seg_start = seg_begin(p, seg);
+    g.seg_end = seg_finish(p, seg);
     g.tau_w = seg == 0 ? 0 : g.seg_start - p.warmup;
     g.n_stages = (g.seg_end - g.tau_w + TC - 1) / TC;
     return g;
