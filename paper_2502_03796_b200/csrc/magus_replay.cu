@@ -1380,7 +1380,7 @@ extern "C" magus_status magus_replay_geometry(const magus_replay_t* h, int32_t o
         solo = 0;
     }
     const int32_t v[16] = {p.n_seg, p.seg_len, p.warmup, g0.ng, g0.npw, g0.n_tblocks, g0.n_pblocks, ctas,
-                           threads, smem, p.n_lane, (int32_t)h->groups.size(), nk, solo, 0, 0};
+                           threads, smem, p.n_lane, (int32_t)h->groups.size(), nk, solo, p.seg_long, 0};
     std::memcpy(out, v, sizeof(v));
     return MAGUS_OK;
 }
