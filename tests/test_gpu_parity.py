@@ -4,6 +4,7 @@ Bars (north_star): per-tick cmd / tune-flag bits, counts an
 bit-exact; T, E, E_pkg, EDP and the savings within 1e-9 relative; generator bytes bit-exact.
 """
 import io
+import os
 
 import numpy as np
 import pytest
@@ -311,7 +312,8 @@ def test_full_size_sampled(M, cfg):
     rec, _, _ = O.gen_replay(O.GenDesc(seed=c["seed"], n_traces=n, n_samples=ns, class_mix=c["class_mix"]), ids,
                              PA.oracle_policies(c["policies"]))
     PA.compare_records(res.per_trace[ids], rec, f"cfg{cfg}")
-    if cfg in (2, 5):   # the two-length segment plan (17 x 1376 + 57 x 1344 ticks) is what these runs exercise
+    if cfg in (2, 5) and os.environ.get("MAGUS_SEG_BALANCE", "1") != "0":
+        # the two-length segment plan (17 x 1376 + 57 x 1344 ticks) is what these runs exercise
         assert res.geometry["n_segments"] == 74 and res.geometry["seg_long"] == 17
     # totals = fixed-order sums of the records (within 1e-9 of an exactly rounded sum)
     np.testing.assert_allclose(res.totals, PA.oracle_totals(res.per_trace), rtol=1e-9)
