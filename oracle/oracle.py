@@ -100,6 +100,9 @@ def lib():
         L.oracle_gen_replay.restype = C.c_int
         L.oracle_gen_replay.argtypes = [C.POINTER(OGenDesc), C.c_void_p, C.c_int32, C.c_int32, C.c_void_p,
                                         C.POINTER(OModel), C.c_void_p, C.c_void_p, C.c_int32]
+        L.oracle_gen_replay_codes.restype = C.c_int
+        L.oracle_gen_replay_codes.argtypes = [C.POINTER(OGenDesc), C.c_void_p, C.c_int32, C.c_int32, C.c_void_p,
+                                              C.POINTER(OModel), C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32]
         _lib = L
     return _lib
 
@@ -303,3 +306,18 @@ def gen_replay(desc: GenDesc, trace_ids, policies, model: Model | None = None, n
     used = lib().oracle_gen_replay(C.byref(desc.c()), ids.ctypes.data, len(ids), P, pols, C.byref(model.c()),
                                    out.ctypes.data, w.ctypes.data, n_threads)
     return out, w, used
+
+
+def gen_replay_codes(desc: GenDesc, trace_ids, policies, model: Model | None = None, n_threads: int = 0):
+    """gen_replay that also returns every tick's code byte: (results[n_ids][P], codes[n_ids][P][n_samples] uint8,
+    w[n_ids], threads)."""
+    model = model or Model()
+    ids = np.ascontiguousarray(trace_ids, dtype=np.int64)
+    P = len(policies)
+    pols = (OPolicy * P)(*[p.c() for p in policies])
+    out = np.zeros((len(ids), P), dtype=RESULT_DTYPE)
+    w = np.zeros(len(ids), dtype=np.float32)
+    codes = np.zeros((len(ids), P, desc.n_samples), dtype=np.uint8)
+    used = lib().oracle_gen_replay_codes(C.byref(desc.c()), ids.ctypes.data, len(ids), P, pols, C.byref(model.c()),
+                                         out.ctypes.data, w.ctypes.data, codes.ctypes.data, n_threads)
+    return out, codes, w, used

@@ -16,10 +16,11 @@
 
 extern "C" {
 
-/* out: [n_ids][n_policies]; w_out: [n_ids] (optional).  Returns the number of threads used. */
-int oracle_gen_replay(const OGenDesc* g, const int64_t* j_locals, int32_t n_ids,
-                      int32_t n_policies, const OPolicy* pols, const OModel* m,
-                      OResult* out, float* w_out, int32_t n_threads) {
+/* out: [n_ids][n_policies]; w_out: [n_ids] (optional); codes: [n_ids][n_policies][n_samples] per-tick code
+ * bytes (optional, the same codes oracle_replay writes).  Returns the number of threads used. */
+int oracle_gen_replay_codes(const OGenDesc* g, const int64_t* j_locals, int32_t n_ids,
+                            int32_t n_policies, const OPolicy* pols, const OModel* m,
+                            OResult* out, float* w_out, uint8_t* codes, int32_t n_threads) {
     if (n_threads <= 0) n_threads = (int32_t)std::max(1u, std::thread::hardware_concurrency());
     std::atomic<int32_t> next(0);
     auto worker = [&]() {
@@ -31,7 +32,8 @@ int oracle_gen_replay(const OGenDesc* g, const int64_t* j_locals, int32_t n_ids,
             if (w_out) w_out[i] = w;
             for (int32_t p = 0; p < n_policies; ++p)
                 oracle_replay(col.data(), g->n_samples, 1, w, &pols[p], m,
-                              &out[(int64_t)i * n_policies + p], nullptr, 0);
+                              &out[(int64_t)i * n_policies + p],
+                              codes ? codes + ((int64_t)i * n_policies + p) * g->n_samples : nullptr, 1);
         }
     };
     int32_t used = std::min<int32_t>(n_threads, std::max<int32_t>(1, n_ids));
@@ -39,6 +41,12 @@ int oracle_gen_replay(const OGenDesc* g, const int64_t* j_locals, int32_t n_ids,
     for (int32_t t = 0; t < used; ++t) pool.emplace_back(worker);
     for (auto& th : pool) th.join();
     return used;
+}
+
+int oracle_gen_replay(const OGenDesc* g, const int64_t* j_locals, int32_t n_ids,
+                      int32_t n_policies, const OPolicy* pols, const OModel* m,
+                      OResult* out, float* w_out, int32_t n_threads) {
+    return oracle_gen_replay_codes(g, j_locals, n_ids, n_policies, pols, m, out, w_out, nullptr, n_threads);
 }
 
 } /* extern "C" */

@@ -72,6 +72,22 @@ def pack_words(codes):
     return np.transpose(out, (2, 1, 0, 3)).copy()             # [P][n][nb][2]
 
 
+def pack_words_tpn(codes):
+    """codes [n][P][n_samples] uint8 (oracle.gen_replay_codes layout) -> words [P][n][n_blocks][2] uint32
+    (cmd, tune flag), tick 32b+i at bit 31-i, partial last block zero-padded."""
+    n, P, ns = codes.shape
+    nb = (ns + 31) // 32
+    out = np.empty((P, n, nb, 2), np.uint32)
+    for bit, slot in ((0, 0), (2, 1)):
+        b = ((codes >> bit) & 1).astype(np.uint8)
+        if nb * 32 != ns:
+            b = np.concatenate([b, np.zeros((n, P, nb * 32 - ns), np.uint8)], axis=2)
+        packed = np.packbits(b, axis=2, bitorder="big")              # [n][P][nb * 4] bytes, tick 0 at the MSB
+        words = packed.reshape(n, P, nb, 4).view(">u4")[..., 0]        # big-endian: byte 0 holds ticks 0-7
+        out[..., slot] = np.transpose(words, (1, 0, 2))
+    return out
+
+
 def oracle_totals(ora_rec):
     """Per-policy sums the library reports (MAGUS_TOT_*), from oracle per-trace records (math.fsum)."""
     import math

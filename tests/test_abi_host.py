@@ -157,3 +157,17 @@ def test_wallclock_flag_rejects_word_dump():
     with pytest.raises(M.MagusError) as e:
         M.Replay(8, 100, [M.Policy()], flags=M.F_WALLCLOCK | M.F_DUMP_WORDS)
     assert e.value.status == M.ERR_INVALID_ARG and "WALLCLOCK" in str(e.value)
+
+
+@pytest.mark.parametrize("shape,knee", [(0, 1.0), (1, 0.5), (1, 0.25), (1, 1.0), (1, 0.9)])
+def test_library_bandwidth_endpoints_equal_oracle(shape, knee):
+    """The library's closed-loop bandwidths B_lo = fl32(bandwidth_at(f_min)), B_hi and powers P_lo, P_hi
+    (magus_derive_thresholds, host side) equal the pinned oracle's SPEC.md:330-347 model for the Linear
+    and the Saturating shapes (K14); the two sides share no code."""
+    from oracle import oracle as O
+    for e in (1.0, 2.5):
+        th = M.derive_thresholds(M.Policy(), M.Model(bw_shape=shape, bw_knee=knee, p_exponent=e))
+        om = O.Model(bw_shape=shape, bw_knee=knee, p_exponent=e)
+        assert th["B_lo"] == np.float32(O.bandwidth_at(0.8, om))
+        assert th["B_hi"] == np.float32(O.bandwidth_at(2.2, om))
+        assert th["P_lo"] == O.pkg_power_at(0.8, om) and th["P_hi"] == O.pkg_power_at(2.2, om)

@@ -117,6 +117,30 @@ def test_small_configs(M, name, segments):
         assert res.n_segments == 7
 
 
+@pytest.mark.parametrize("segments", [0, 5])
+@pytest.mark.parametrize("name", ["mixed-kinds", "cfg5-small", "cfg2-small"])
+def test_saturating_bandwidth_model(M, name, segments):
+    """SPEC.md:330-338 Saturating bandwidth (bw_shape = 1) with knee 0.5: B_lo = fl32(20 (0.8/2.2)/0.5)
+    = 14.545 GB/s instead of the Linear 7.27, so the throttle threshold, the closed-loop observation and
+    the energy epilogue all run on the saturating value; records, words and a code dump against the
+    oracle's replay under the same model."""
+    s = SMALL[name]
+    stride = (s["n"] + 3) // 4 * 4
+    tr, w = gpu_gen(M, s["seed"], s["n"], s["ns"], s["mix"], stride)
+    th = M.derive_thresholds(M.Policy(), M.Model(bw_shape=1, bw_knee=0.5))
+    assert th["B_lo"] == np.float32(20.0 * ((0.8 / 2.2) / 0.5)) != np.float32(20.0 * (0.8 / 2.2))
+    res = run_gpu(M, tr, w, s["policies"], s["n"], s["ns"], stride, segments=segments, dump=(0, 4),
+                  model=M.Model(bw_shape=1, bw_knee=0.5))
+    rec, codes = oracle_run(tr.cpu().numpy(), w.cpu().numpy(), s["policies"], s["n"],
+                            model=O.Model(bw_shape=1, bw_knee=0.5))
+    PA.compare_records(res.per_trace, rec, f"saturating {name}")
+    assert np.array_equal(res.words, PA.pack_words(codes))
+    assert np.array_equal(res.decisions, codes[:, :4, :])
+    np.testing.assert_allclose(res.totals, PA.oracle_totals(rec), rtol=1e-9, atol=1e-9)
+    lin, _ = oracle_run(tr.cpu().numpy(), w.cpu().numpy(), s["policies"], s["n"])
+    assert not np.array_equal(lin["n_thr"], rec["n_thr"])   # the model changed what the loop saw
+
+
 @pytest.mark.parametrize("k,C,hf", [(1, 1, 1.0), (2, 10, 0.6), (5, 7, 0.5), (8, 10, 0.4), (9, 10, 0.6),
                                     (16, 33, 0.6), (33, 64, 0.5), (64, 64, 0.9), (4, 64, 0.3), (7, 40, 0.6),
                                     (1, 32, 0.6), (3, 33, 0.6)])
@@ -296,56 +320,102 @@ def test_host_buffer_path(M):
 
 # ------------------------------------------------------------------------------------- full size
 
+def _oracle_all_traces(desc, n, policies, chunk, words_gpu=None, word_ids=None, model=None):
+    """The oracle over EVERY local trace of a generated shard (its own generator, trace by trace, all host
+    cores), in chunks; returns its records [n][P].  With words_gpu ([P][n][n_blocks][2] from the replay
+    kernel, MAGUS_F_DUMP_WORDS), every trace in word_ids (default: all) also has its per-tick cmd and
+    tune-flag bits compared with the oracle's codes; returns (records, traces whose words were compared)."""
+    pols = PA.oracle_policies(policies)
+    rec = np.zeros((n, len(pols)), dtype=O.RESULT_DTYPE)
+    want_words = set(range(n)) if word_ids is None else set(int(j) for j in word_ids)
+    n_words = 0
+    for a in range(0, n, chunk):
+        ids = np.arange(a, min(n, a + chunk))
+        wid = [j for j in ids if j in want_words] if words_gpu is not None else []
+        rest = np.setdiff1d(ids, np.array(wid, np.int64))
+        if len(rest):
+            r, _, _ = O.gen_replay(desc, rest, pols, model)
+            rec[rest] = r
+        if wid:
+            wid = np.array(wid, np.int64)
+            r, codes, _, _ = O.gen_replay_codes(desc, wid, pols, model)
+            rec[wid] = r
+            want = PA.pack_words_tpn(codes)
+            got = words_gpu[:, wid]
+            bad = np.argwhere(np.any(got != want, axis=-1))
+            assert bad.size == 0, f"per-tick words differ at (policy, trace, block) {bad[0].tolist()}"
+            n_words += len(wid)
+    return rec, n_words
+
+
 @pytest.mark.parametrize("cfg", [2, 5, 3])
-def test_full_size_sampled(M, cfg):
-    """BASELINE.json full sizes in the bench's launch configuration (automatic segmentation): the GPU
-    replays every trace; the oracle regenerates a sample of traces one by one (including the ragged
-    last tile) and must match bit-exactly on counts and digests, 1e-9 on energies; totals over all
-    traces are checked against the per-trace records' properties."""
+def test_full_size_every_trace(M, cfg):
+    """BASELINE.json full sizes in the bench's launch configuration (automatic segmentation): the GPU replays
+    every trace; the oracle regenerates EVERY trace with its own generator and replays it under EVERY policy.
+    Bit-exact: every (trace, policy) record's counts and digest, and every tick's cmd and tune-flag bit from
+    the replay kernel's 32-tick words (MAGUS_F_DUMP_WORDS; cfg 3: the words of 256 traces x 65 policies, the
+    records of all 1,024); 1e-9: T, E, E_pkg, EDP, the savings and the per-policy totals against the oracle's
+    (math.fsum) totals.  A 64-trace decision dump (magus_resim_kernel) is checked against the replay kernel's
+    own words and, byte for byte, against the oracle's codes."""
     c = CONFIGS[cfg]
     n, ns = c["n_traces"], c["n_samples"]
     tr, w = gpu_gen(M, c["seed"], n, ns, c["class_mix"], c["stride"])
-    res = run_gpu(M, tr, w, c["policies"], n, ns, c["stride"], flags=M.F_PER_TRACE_STATS)
+    dump0 = n - 64
+    res = run_gpu(M, tr, w, c["policies"], n, ns, c["stride"],
+                  flags=M.F_PER_TRACE_STATS | M.F_DUMP_WORDS, dump=(dump0, 64))
     del tr
-    rng = np.random.default_rng(cfg)
-    ids = np.unique(np.r_[rng.choice(n, 24, replace=False), [0, 1, 2, n - 1]])
-    rec, _, _ = O.gen_replay(O.GenDesc(seed=c["seed"], n_traces=n, n_samples=ns, class_mix=c["class_mix"]), ids,
-                             PA.oracle_policies(c["policies"]))
-    PA.compare_records(res.per_trace[ids], rec, f"cfg{cfg}")
+    desc = O.GenDesc(seed=c["seed"], n_traces=n, n_samples=ns, class_mix=c["class_mix"])
+    word_ids = None if cfg != 3 else np.r_[np.arange(0, 128), np.arange(n - 128, n)]
+    rec, n_words = _oracle_all_traces(desc, n, c["policies"], 32 if cfg == 3 else 256, res.words, word_ids)
+    PA.compare_records(res.per_trace, rec, f"cfg{cfg}")
+    np.testing.assert_allclose(res.totals, PA.oracle_totals(rec), rtol=1e-9, atol=1e-9)
+    edp = PA.oracle_totals(rec)[:, 3]
+    assert res.totals[res.argmin_policy, 3] <= edp.min() * (1 + 1e-9)
+    # the decision dump's cmd / tune-flag bits are the replay kernel's own words ...
+    assert np.array_equal(PA.pack_words(res.decisions), res.words[:, dump0:])
+    # ... and every code byte (level, ready, flag, lock, signal, throttled) is the oracle's
+    _, codes, _, _ = O.gen_replay_codes(desc, np.arange(dump0, n), PA.oracle_policies(c["policies"]))
+    assert np.array_equal(res.decisions, np.transpose(codes, (2, 0, 1)))
     if cfg in (2, 5) and os.environ.get("MAGUS_SEG_BALANCE", "1") != "0":
         # the two-length segment plan (17 x 1376 + 57 x 1344 ticks) is what these runs exercise
         assert res.geometry["n_segments"] == 74 and res.geometry["seg_long"] == 17
-    # totals = fixed-order sums of the records (within 1e-9 of an exactly rounded sum)
-    np.testing.assert_allclose(res.totals, PA.oracle_totals(res.per_trace), rtol=1e-9)
-    print("geometry", res.geometry, "mismatched segments", res.n_mismatched_segments, "rounds", res.fixup_rounds)
+    P = len(c["policies"])
+    print(f"cfg{cfg}: compared records of {n} x {P} (trace, policy) chains, per-tick words of {n_words} x {P} "
+          f"chains ({n_words * P * ns:,} ticks), codes of 64 x {P}; geometry {res.geometry}, "
+          f"mismatched segments {res.n_mismatched_segments}")
 
 
-def test_cfg4_shard_sampled(M, monkeypatch):
+def test_cfg4_shard_every_trace(M, monkeypatch):
     """cfg 4 as one rank of the 8-GPU run sees it (rank 5: global traces [40960, 49152) x 10^6 samples,
     32.8 GB), in the bench's launch configuration, and again with the solo kernel's synthetic warm-up state
     (MAGUS_SOLO_SYNTH=1): it lands the oscillating class (C4) on phase-shifted limit cycles, so speculative
-    entries stay wrong through whole traces and the chain walk runs over ~10^6 ticks.  Sampled traces (global
-    ids, including both ends of the shard) must match the oracle bit-exactly on counts and digests, 1e-9 on
-    energies, both times."""
+    entries stay wrong through whole traces and the chain walk runs over ~10^6 ticks.  EVERY trace of the
+    shard is regenerated and replayed by the oracle: counts and digests bit-exact, 1e-9 on energies and on
+    the per-policy totals, both times; the per-tick words of 64 traces (both shard ends and C4 traces)
+    bit-exact."""
     c = CONFIGS[4]
     n, ns, rank = c["per_gpu_traces"], c["n_samples"], 5
     off = rank * n
     tr, w = gpu_gen(M, c["seed"], n, ns, c["class_mix"], n, offset=off)
-    rng = np.random.default_rng(4)
-    ids = np.unique(np.r_[rng.choice(n, 10, replace=False), [0, 4, 9, n - 1]])   # 4, 9: class C4 (j mod 5)
-    rec, _, _ = O.gen_replay(O.GenDesc(seed=c["seed"], n_traces=n, n_samples=ns, class_mix=c["class_mix"],
-                                       global_trace_offset=off), ids, PA.oracle_policies(c["policies"]))
+    desc = O.GenDesc(seed=c["seed"], n_traces=n, n_samples=ns, class_mix=c["class_mix"], global_trace_offset=off)
+    word_ids = np.r_[np.arange(0, 24), np.arange(n - 24, n), np.arange(4, 4 * 5 * 16, 5)[:16] + 100]
     mism = []
+    rec = None
     for synth in ("0", "1"):
         monkeypatch.setenv("MAGUS_SOLO_SYNTH", synth)
-        res = run_gpu(M, tr, w, c["policies"], n, ns, n, flags=M.F_PER_TRACE_STATS, offset=off)
-        PA.compare_records(res.per_trace[ids], rec, f"cfg4-shard synth={synth}")
-        np.testing.assert_allclose(res.totals, PA.oracle_totals(res.per_trace), rtol=1e-9)
+        flags = M.F_PER_TRACE_STATS | (M.F_DUMP_WORDS if synth == "0" else 0)
+        res = run_gpu(M, tr, w, c["policies"], n, ns, n, flags=flags, offset=off)
+        if rec is None:
+            rec, n_words = _oracle_all_traces(desc, n, c["policies"], 512, res.words, word_ids)
+            assert n_words == len(set(word_ids.tolist()))
+        PA.compare_records(res.per_trace, rec, f"cfg4-shard synth={synth}")
+        np.testing.assert_allclose(res.totals, PA.oracle_totals(rec), rtol=1e-9, atol=1e-9)
         mism.append(res.n_mismatched_segments)
-        print("synth", synth, "geometry", res.geometry, "mismatched", res.n_mismatched_segments,
-              "walked", res.fixup_rounds)
-    if res.geometry["solo_groups"]:   # the synthetic warm-up state exists in the solo kernel only
-        assert mism[1] > 0, "the synthetic warm-up state should exercise the chain walk"
+        print(f"synth {synth}: compared {n} x {len(c['policies'])} records; geometry {res.geometry}, "
+              f"mismatched {res.n_mismatched_segments}, walked {res.fixup_rounds}")
+        del res
+    if mism[1] == 0:
+        pytest.fail("the synthetic warm-up state should exercise the chain walk")
 
 
 def test_active_savings_from_gpu_totals(M):

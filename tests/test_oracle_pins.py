@@ -578,3 +578,80 @@ def test_wallclock_bruteforce(seed, w, kind, observe):
         assert r[f] == pytest.approx(tot[f], rel=1e-12), f
     if kind == "magus" and observe == 0:
         assert r["n_thr"] > 0 and r["n_rounds"] > len(D) and r["lock_ticks"] > 0 and r["transitions"] > 5
+
+
+# --------------------------------------------------------------------------- K14: platform model (SPEC simsys)
+
+def test_bandwidth_linear_spec_examples():
+    """K14: Linear bandwidth_at(f_max) = bw_max; bw_max = 2e10, f_max = 2.2 GHz,
+    f = 0.8 GHz -> 2e10 * 0.8/2.2 ~ 7.27e9.  A wrong ratio (f_min/f, f_max/f) fails the second value."""
+    m = O.Model(bw_max_gbps=20.0)
+    assert O.bandwidth_at(2.2, m) == 20.0
+    assert O.bandwidth_at(0.8, m) == pytest.approx(7.2727272727, rel=1e-10)
+
+
+def test_bandwidth_saturating_spec_example_and_hand_values():
+    """K14: Saturating bw_max * min(1, (f/f_max)/knee).
+    - S:338: knee 0.5 at f = 0.6 f_max -> bw_max (above the knee the bandwidth saturates);
+    - hand value below the knee: knee 0.5, f = 0.8, f_max = 2.2, bw_max = 20 -> 20 * (0.8/2.2)/0.5
+      = 14.5454...; a `ratio * knee` slip gives 3.64, a missing min() gives > bw_max above the knee;
+    - exactly at the knee (f = knee * f_max) -> bw_max; knee = 1 is the Linear model;
+    - non-decreasing in f, equal to bw_max at f_max (SPEC.md:317 invariants)."""
+    m = O.Model(bw_max_gbps=20.0, bw_shape=1, bw_knee=0.5)
+    assert O.bandwidth_at(0.6 * 2.2, m) == 20.0
+    assert O.bandwidth_at(0.8, m) == pytest.approx(20.0 * (0.8 / 2.2) / 0.5, rel=1e-15)
+    assert O.bandwidth_at(0.8, m) == pytest.approx(14.545454545454545, rel=1e-12)
+    assert O.bandwidth_at(1.1, m) == 20.0            # f / f_max = 0.5 = knee
+    assert O.bandwidth_at(2.0, m) == 20.0
+    m1 = O.Model(bw_max_gbps=20.0, bw_shape=1, bw_knee=1.0)
+    lin = O.Model(bw_max_gbps=20.0)
+    fs = np.linspace(0.8, 2.2, 57)
+    for f in fs:
+        assert O.bandwidth_at(f, m1) == O.bandwidth_at(f, lin)
+    for knee in (0.25, 0.5, 0.9):
+        mk = O.Model(bw_max_gbps=20.0, bw_shape=1, bw_knee=knee)
+        vals = [O.bandwidth_at(f, mk) for f in fs]
+        assert all(b >= a for a, b in zip(vals, vals[1:]))
+        assert vals[-1] == 20.0
+        assert vals[0] == pytest.approx(20.0 * min(1.0, (0.8 / 2.2) / knee), rel=1e-15)
+
+
+def test_uncore_power_spec_examples_and_exponent():
+    """K14 (SPEC.md:339-347): p_min + (p_max - p_min) ((f - f_min)/(f_max - f_min))^e.
+    Endpoints give exactly p_uncore_min / p_uncore_max for every exponent (the replay only
+    ever evaluates the endpoints, A19); exponent 1 at the midpoint is the arithmetic mean (S:347);
+    hand values for e = 2 (a quarter of the way up at the midpoint) and e = 3.  Package power adds
+    p_pkg_idle + p_core_active: 60 + 40 + 16 = 116 W and 200 W with the default model."""
+    for e in (1.0, 1.7, 2.0, 3.0):
+        m = O.Model(p_exponent=e)
+        assert O.uncore_power_at(0.8, m) == 16.0
+        assert O.uncore_power_at(2.2, m) == 100.0
+    assert O.uncore_power_at(1.5, O.Model(p_exponent=1.0)) == pytest.approx(58.0, rel=1e-14)
+    assert O.uncore_power_at(1.5, O.Model(p_exponent=2.0)) == pytest.approx(16.0 + 84.0 / 4, rel=1e-14)
+    assert O.uncore_power_at(1.15, O.Model(p_exponent=3.0)) == pytest.approx(16.0 + 84.0 / 64, rel=1e-13)
+    assert O.pkg_power_at(0.8, O.Model()) == 116.0 and O.pkg_power_at(2.2, O.Model()) == 200.0
+
+
+def test_saturating_model_in_the_replay_closed_form():
+    """K14: the closed loop of the replay with the Saturating model.  With knee 0.5, B_lo =
+    fl32(20 * (0.8/2.2)/0.5) = fl32(14.5454...).  STATIC_MIN on a constant demand D = 16 > B_lo is
+    throttled every tick: T = N Delta (w + (1 - w) D / B_lo) (A16), E_pkg = P_lo T; on
+    D = 12 < B_lo (but above the Linear B_lo 7.27) nothing is throttled, so the saturating B_lo, not the
+    Linear one, is in the loop.  MAGUS on a 12 -> 16 step at f_min sees A rise only to B_lo."""
+    m = O.Model(bw_shape=1, bw_knee=0.5)
+    b_lo = float(np.float32(20.0 * ((0.8 / 2.2) / 0.5)))   # operand order of A26
+    n, w = 200, float(np.float32(0.3))   # compute_weight is an fp32 input
+    r, codes = O.replay(np.full(n, 16.0, np.float32), w, O.Policy(kind=O.STATIC_MIN), m, codes=True)
+    assert r["n_thr"] == n
+    assert r["T"] == pytest.approx(n * 0.1 * (w + (1 - w) * 16.0 / b_lo), rel=1e-12)
+    assert r["E_pkg"] == pytest.approx(116.0 * r["T"], rel=1e-12)
+    r, _ = O.replay(np.full(n, 12.0, np.float32), w, O.Policy(kind=O.STATIC_MIN), m)
+    assert r["n_thr"] == 0 and r["T"] == pytest.approx(n * 0.1, rel=1e-12)
+    r_lin, _ = O.replay(np.full(n, 12.0, np.float32), w, O.Policy(kind=O.STATIC_MIN), O.Model())
+    assert r_lin["n_thr"] == n
+    # MAGUS at f_min on 12 then 16: the observed step is 12 -> B_lo (a rise of 2.55 GB/s in one tick > 1
+    # GB/s/s * 0.1 s), so Alg. 1 returns +1 and the governor goes to f_max on the step tick
+    D = np.r_[np.full(50, 12.0), np.full(50, 16.0)].astype(np.float32)
+    r, codes = O.replay(D, w, O.Policy(), m, codes=True)
+    assert codes[49] & 1 == 0 and codes[50] & 1 == 1 and (codes[50] >> 4) & 3 == 1
+    assert r["n_thr"] == 1
