@@ -52,6 +52,10 @@ def parse():
     ap.add_argument("--wallclock", action="store_true", help="NEXT-1 time model: wall-clock governor rounds "
                     "(MAGUS_F_WALLCLOCK, DESIGN.md A32); not the headline configuration")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--nccl", action="store_true", help="run the cross-rank exchange (process group, MAGUS_F_NCCL: "
+                    "chunk sums + NCCL allreduce inside the step's graph) even at N = 1")
+    ap.add_argument("--policy-shards", type=int, default=1, help="parameter-grid split: this many columns of the "
+                    "world replay disjoint policy slices (magus_grid_plan); the rest shard the traces (weak)")
     ap.add_argument("--preroll-ms", type=float, default=600.0, help="untimed load before the timed region "
                     "so the clock samples see the GPU under load")
     return ap.parse_args()
@@ -185,10 +189,14 @@ def run_ours(args, cfg):
     rank, world, local = env_rank()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    dist_on = world > 1 or args.nccl
+    if dist_on:
         dist.init_process_group("nccl", device_id=dev)
-    from paper_2502_03796_b200.sharding import weak_shard
-    offset, n = weak_shard(cfg.get("per_gpu_traces", cfg["n_traces"]), rank, world)   # global ids
+    from paper_2502_03796_b200.sharding import grid_shard
+    ps = args.policy_shards
+    n_pol_glob = len(cfg["policies"])
+    per_shard = cfg.get("per_gpu_traces", cfg["n_traces"])      # traces per trace shard (weak over trace shards)
+    offset, n, p_off, n_pol = grid_shard(per_shard * (world // ps), n_pol_glob, rank, world, ps)   # global ids
     ns = cfg["n_samples"]
     stride = (n + 3) // 4 * 4
     tr = torch.empty((ns, stride), dtype=torch.float32, device=dev)
@@ -197,13 +205,14 @@ def run_ours(args, cfg):
     M.gen_traces(cfg["seed"], n, ns, cfg["class_mix"], tr, w, trace_stride=stride, global_trace_offset=offset,
                  stream=stream)
     nccl_id = None
-    if world > 1:
+    if dist_on:
         obj = [M.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
-    pols = [M.Policy(**d) for d in cfg["policies"]]
+    pols = [M.Policy(**d) for d in cfg["policies"][p_off:p_off + n_pol]]
     R = M.Replay(n, ns, pols, M.Model(), trace_stride=stride, global_trace_offset=offset, rank=rank, world=world,
-                 nccl_id=nccl_id, flags=M.F_TIMING | (M.F_WALLCLOCK if args.wallclock else 0))
+                 nccl_id=nccl_id, n_policies_global=n_pol_glob, policy_offset=p_off,
+                 flags=M.F_TIMING | (M.F_WALLCLOCK if args.wallclock else 0) | (M.F_NCCL if args.nccl else 0))
     geo = R.geometry()
     for _ in range(max(3, args.warmup)):
         R.run(tr, w, stream)
@@ -215,7 +224,7 @@ def run_ours(args, cfg):
         for _ in range(20):
             R.run(tr, w, stream)
         torch.cuda.synchronize(dev)
-    if world > 1:
+    if dist_on:
         dist.barrier()
     torch.cuda.synchronize(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -224,17 +233,17 @@ def run_ours(args, cfg):
         R.run(tr, w, stream)
     e1.record(stream)
     torch.cuda.synchronize(dev)
-    if world > 1:
+    if dist_on:
         dist.barrier()
     clocks = sampler.stop()
     ms = e0.elapsed_time(e1) / args.steps
     tsum = R.timing_summary(args.steps)          # per-kernel CUDA events of the same K runs, same stream
     res = R.results()
     ms_t = torch.tensor([ms, tsum["replay_ms"]], dtype=torch.float64, device=dev)
-    if world > 1:
+    if dist_on:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_max, replay_ms_max = float(ms_t[0]), float(ms_t[1])
-    total_samples = n * ns * world
+    total_samples = n * ns * (world // ps)     # trace-samples of the job (each under all of its policies)
     value = total_samples / (ms_max / 1e3)
 
     # roofline of the dominant kernel (the replay): 4 algorithmic bytes per trace-sample per launch
@@ -258,7 +267,7 @@ def run_ours(args, cfg):
         R.run_host(th, wh, stream)
         R.results()
         k_e2e = max(1, min(args.steps, 5))
-        if world > 1:
+        if dist_on:
             dist.barrier()
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
@@ -267,7 +276,7 @@ def run_ours(args, cfg):
             R.results()                           # D2H of the step's totals + argmin (synchronising)
         e2e_ms = 1e3 * (time.perf_counter() - t0) / k_e2e
         e2e_t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-        if world > 1:
+        if dist_on:
             dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
         e2e_ms = float(e2e_t[0])
         e2e = {"value": total_samples / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms, "steps": k_e2e,
@@ -286,11 +295,13 @@ def run_ours(args, cfg):
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
+            "scaling": "weak" if ps == 1 else "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg["name"] + ("+wallclock" if args.wallclock else ""), "n_traces_per_gpu": n, "n_samples": ns, "policies": len(pols),
-                       "parallelism": f"trace-sharded x{world}" + (", NCCL allreduce of per-policy totals" if world > 1
-                                                                    else ""),
+                       "policies_global": n_pol_glob,
+                       "parallelism": f"trace-sharded x{world // ps}" + (f", parameter grid x{ps}" if ps > 1 else "")
+                                      + (", NCCL allreduce of per-policy totals" if dist_on else ""),
                        "l2": "inputs 1.64 GB/GPU >> 126 MB L2; no flush needed" if ns * n * 4 > 4e8 else "L2-resident"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic,
@@ -312,7 +323,7 @@ def run_ours(args, cfg):
         }
         print(json.dumps(out), flush=True)
     R.close()
-    if world > 1:
+    if dist_on:
         dist.destroy_process_group()
 
 

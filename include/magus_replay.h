@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define MAGUS_ABI_VERSION 1
+#define MAGUS_ABI_VERSION 2
 
 typedef enum {
     MAGUS_OK = 0,
@@ -106,6 +106,10 @@ typedef struct {
                                          rounds (a chain runs >= n_samples rounds); MAGUS_F_DUMP_WORDS is
                                          refused; STATIC_MAX is unchanged (never throttled: one entry per
                                          round).  Default (flag clear): one governor tick per entry (A15) */
+#define MAGUS_F_NCCL            0x40u /* run the cross-rank exchange (per-policy chunk sums on the device, then the
+                                         NCCL allreduce of the global [n_policies_global][MAGUS_N_TOTALS]) even at
+                                         world == 1, on a one-rank communicator (nccl_unique_id may be NULL then);
+                                         world > 1 always runs it */
 
 typedef struct {
     int32_t n_traces;             /* local traces in this rank's shard, >= 0 */
@@ -122,6 +126,16 @@ typedef struct {
     int32_t dump_first_trace, dump_n_traces;   /* MAGUS_F_DUMP_DECISIONS window (local ids) */
     int32_t tuning_segments;      /* 0 = automatic time segmentation; else the segment count (tests) */
     int32_t tuning_warmup;        /* 0 = automatic warm-up ticks; else the warm-up (multiple of 32) */
+    /* Parameter-grid split (north_star "by trace and parameter grid"): this rank replays
+     * its traces under the global policies [policy_offset, policy_offset + n_policies) of a policy set of
+     * n_policies_global points (0 = n_policies: no split).  policy_totals and argmin_policy are then global:
+     * the allreduce sums every rank's slice into the global [n_policies_global][MAGUS_N_TOTALS]; per_trace,
+     * words and decisions stay local ([..][n_policies]).  With the exchange on (world > 1 or MAGUS_F_NCCL),
+     * create checks across ranks that every global policy is owned by some rank, that all owners of a policy
+     * passed the same parameters, and that all ranks agree on the model, n_samples and n_policies_global
+     * (MAGUS_ERR_CONFIG naming the disagreement otherwise). */
+    int32_t n_policies_global;
+    int32_t policy_offset;
 } magus_replay_desc;
 
 /* Per-policy totals (fp64), after the cross-rank allreduce. Index with MAGUS_TOT_*. */
@@ -141,12 +155,17 @@ typedef struct {
 
 /* Caller-owned host arrays; a NULL member is skipped. */
 typedef struct {
-    double*            policy_totals;  /* [n_policies][MAGUS_N_TOTALS] */
+    double*            policy_totals;  /* [n_policies_global][MAGUS_N_TOTALS]: sums over traces (and ranks) of the
+                                          per-(trace, policy) records -- E, E_pkg, T, EDP, the counts, and the SUMS
+                                          of the per-trace fractions slowdown / energy_saving / edp_saving (their
+                                          mean is the sum / MAGUS_TOT_N_TRACES; job-level ratios from the summed
+                                          energies and times: magus_active_savings with p_idle_w = 0).  Rows of
+                                          global policies outside this rank's slice are 0 without the exchange */
     magus_trace_stats* per_trace;      /* [n_traces][n_policies] (needs MAGUS_F_PER_TRACE_STATS) */
     uint32_t*          words;          /* [n_policies][n_traces][n_blocks][2] = {w_cmd, w_ev}, n_blocks =
                                           ceil(n_samples/32) (needs MAGUS_F_DUMP_WORDS) */
     uint8_t*           decisions;      /* [n_samples][dump_n_traces][n_policies] (needs MAGUS_F_DUMP_DECISIONS) */
-    int32_t  argmin_policy;            /* out: argmin over policies of total EDP, ties -> lowest index (A23) */
+    int32_t  argmin_policy;            /* out: global index, magus_totals_argmin of policy_totals (A23) */
     int32_t  err_trace;                /* out: first local trace with an invalid sample, else -1 */
     int64_t  err_tick;                 /* out: its first invalid tick, else -1 */
     int32_t  n_segments;               /* out: time segments per trace used by the run */
@@ -243,6 +262,20 @@ magus_status magus_derive_thresholds(const magus_policy* p, const magus_model* m
  * out is left untouched then. */
 magus_status magus_active_savings(const double* policy_totals, int32_t n_policies, int32_t policy,
                                   int32_t baseline, double p_idle_w, double out[3]);
+
+/* Host-only (no GPU needed): the argmin the library reports (A23): over the policies whose
+ * MAGUS_TOT_N_TRACES total is > 0 (all policies when none is), the one with the least total EDP; ties -> the
+ * lowest index.  policy_totals: [n_policies][MAGUS_N_TOTALS].  MAGUS_ERR_INVALID_ARG on NULL or n_policies < 1. */
+magus_status magus_totals_argmin(const double* policy_totals, int32_t n_policies, int32_t* out);
+
+/* Host-only (no GPU needed): the rank's share of a 2-D (trace x parameter-grid) split.
+ * The world is policy_shards columns of world / policy_shards trace shards; rank r owns trace shard
+ * r / policy_shards and policy slice r % policy_shards.  Traces [0, n_traces) and policies [0, n_policies) are
+ * cut into contiguous ranges whose sizes differ by at most one.  out = {global_trace_offset, n_traces_local,
+ * policy_offset, n_policies_local}.  MAGUS_ERR_INVALID_ARG unless 0 <= rank < world, policy_shards >= 1 divides
+ * world, n_traces >= 0 and 1 <= policy_shards <= n_policies. */
+magus_status magus_grid_plan(int32_t world, int32_t rank, int32_t policy_shards, int64_t n_traces,
+                             int32_t n_policies, int64_t out[4]);
 
 int32_t magus_abi_version(void);
 

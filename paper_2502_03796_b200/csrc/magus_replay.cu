@@ -424,7 +424,10 @@ struct magus_replay {
     TraceRec* d_wrec = nullptr;       // wall: [n_lane][n_traces] lane-chain records
     double* d_totals = nullptr;
     uint8_t* d_out = nullptr;         // [P][chunks][13] totals partials (fp64), then the 4 run flag words: one D2H copy
-    double* d_fin = nullptr;          // world > 1: [P][13] per-policy totals, allreduced across ranks
+    double* d_fin = nullptr;          // exchange on: [P_glob][13] per-policy totals, allreduced across ranks
+    double* d_fin_local = nullptr;    // exchange on: [P_glob][13], this rank's slice rows (the rest stays 0)
+    int P_glob = 1, p_off = 0;        // parameter-grid split: global policy count, global index of local policy 0
+    bool xchg = false;                // the cross-rank exchange runs (world > 1 or MAGUS_F_NCCL)
     int n_chunks = 1;                 // trace chunks of the totals kernel
     int32_t* d_first_low = nullptr;   // [n_traces] speculation aid
     uint8_t* d_chain = nullptr;       // per-chain totals (ReplayParams::c_*)
@@ -515,6 +518,38 @@ extern "C" magus_status magus_active_savings(const double* tot, int32_t n_polici
     out[0] = (active - (P - p_idle_w)) / active;
     out[1] = 1.0 - Ea / Eab;
     out[2] = 1.0 - (Ea * T) / (Eab * Tb);
+    return MAGUS_OK;
+}
+
+extern "C" magus_status magus_totals_argmin(const double* tot, int32_t n_policies, int32_t* out) {
+    if (!tot || !out || n_policies < 1) return fail(nullptr, MAGUS_ERR_INVALID_ARG, "magus_totals_argmin: bad argument");
+    bool any = false;
+    for (int32_t p = 0; p < n_policies; ++p) any = any || tot[(size_t)p * MAGUS_N_TOTALS + MAGUS_TOT_N_TRACES] > 0.0;
+    int32_t am = -1;
+    for (int32_t p = 0; p < n_policies; ++p) {
+        if (any && !(tot[(size_t)p * MAGUS_N_TOTALS + MAGUS_TOT_N_TRACES] > 0.0)) continue;
+        if (am < 0 || tot[(size_t)p * MAGUS_N_TOTALS + MAGUS_TOT_EDP] < tot[(size_t)am * MAGUS_N_TOTALS + MAGUS_TOT_EDP])
+            am = p;
+    }
+    *out = am;
+    return MAGUS_OK;
+}
+
+extern "C" magus_status magus_grid_plan(int32_t world, int32_t rank, int32_t policy_shards, int64_t n_traces,
+                                        int32_t n_policies, int64_t out[4]) {
+    if (!out || world < 1 || rank < 0 || rank >= world || policy_shards < 1 || world % policy_shards != 0 ||
+        n_traces < 0 || policy_shards > n_policies)
+        return fail(nullptr, MAGUS_ERR_INVALID_ARG,
+                    "magus_grid_plan: need 0 <= rank < world, policy_shards dividing world, "
+                    "1 <= policy_shards <= n_policies, n_traces >= 0");
+    const int64_t trace_shards = world / policy_shards, ts = rank / policy_shards, ps = rank % policy_shards;
+    auto cut = [](int64_t n, int64_t parts, int64_t i, int64_t* off, int64_t* cnt) {   // sizes differ by <= 1
+        const int64_t base = n / parts, extra = n % parts;
+        *off = i * base + std::min(i, extra);
+        *cnt = base + (i < extra ? 1 : 0);
+    };
+    cut(n_traces, trace_shards, ts, &out[0], &out[1]);
+    cut(n_policies, policy_shards, ps, &out[2], &out[3]);
     return MAGUS_OK;
 }
 
@@ -683,6 +718,66 @@ static void choose_geometry(magus_replay_t* h, int n_sm, int forced_segments) {
     }
 }
 
+// Cross-rank consistency of a run with the exchange on (collective; called by create on every rank).  Every rank
+// writes a record: a header every rank fills identically (model, n_samples, n_policies_global) and one slot per
+// global policy, filled with the policy's bytes by the ranks that own it (their slice) and neutral elsewhere
+// (0x00 for the MAX copy, 0xFF for the MIN copy).  After a byte-wise MAX and MIN allreduce the two copies are
+// equal iff all ranks agree on the header, every owner of a policy passed the same parameters, and every
+// global policy has an owner.
+static magus_status check_ranks_agree(magus_replay_t* h) {
+    const magus_replay_desc& d = h->desc;
+    struct Header {
+        magus_model model;
+        int32_t n_samples, n_policies_global;
+    } hd;
+    std::memset(&hd, 0, sizeof(hd));
+    hd.model = d.model;
+    hd.n_samples = d.n_samples;
+    hd.n_policies_global = h->P_glob;
+    const size_t slot = sizeof(magus_policy), n_bytes = sizeof(Header) + (size_t)h->P_glob * slot;
+    std::vector<uint8_t> mx(n_bytes, 0x00), mn(n_bytes, 0xFF);
+    std::memcpy(mx.data(), &hd, sizeof(hd));
+    std::memcpy(mn.data(), &hd, sizeof(hd));
+    for (int i = 0; i < d.n_policies; ++i) {
+        magus_policy p = h->pols[i];
+        p._reserved0 = 0;
+        uint8_t* a = mx.data() + sizeof(Header) + (size_t)(h->p_off + i) * slot;
+        std::memcpy(a, &p, slot);
+        std::memcpy(mn.data() + (a - mx.data()), &p, slot);
+    }
+    uint8_t* dbuf = nullptr;
+    cudaError_t ce = cudaMalloc(&dbuf, 2 * n_bytes);
+    if (ce != cudaSuccess) return cuda_fail(h, ce, "cudaMalloc rank check");
+    cudaStream_t st = nullptr;
+    cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    cudaMemcpyAsync(dbuf, mx.data(), n_bytes, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(dbuf + n_bytes, mn.data(), n_bytes, cudaMemcpyHostToDevice, st);
+    ncclResult_t r1 = nccl().AllReduce(dbuf, dbuf, n_bytes, ncclUint8, ncclMax, h->comm, st);
+    ncclResult_t r2 = nccl().AllReduce(dbuf + n_bytes, dbuf + n_bytes, n_bytes, ncclUint8, ncclMin, h->comm, st);
+    cudaMemcpyAsync(mx.data(), dbuf, n_bytes, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(mn.data(), dbuf + n_bytes, n_bytes, cudaMemcpyDeviceToHost, st);
+    ce = cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+    cudaFree(dbuf);
+    if (r1 != ncclSuccess || r2 != ncclSuccess)
+        return fail(h, MAGUS_ERR_NCCL, std::string("rank check allreduce: ") +
+                                           nccl().GetErrorString(r1 != ncclSuccess ? r1 : r2));
+    if (ce != cudaSuccess) return cuda_fail(h, ce, "rank check");
+    if (std::memcmp(mx.data(), mn.data(), sizeof(Header)) != 0)
+        return fail(h, MAGUS_ERR_CONFIG, "ranks disagree on the model, n_samples or n_policies_global");
+    for (int g = 0; g < h->P_glob; ++g) {
+        const uint8_t* a = mx.data() + sizeof(Header) + (size_t)g * slot;
+        const uint8_t* b = mn.data() + sizeof(Header) + (size_t)g * slot;
+        if (std::memcmp(a, b, slot) == 0) continue;
+        bool unowned = true;
+        for (size_t i = 0; i < slot; ++i) unowned = unowned && a[i] == 0x00 && b[i] == 0xFF;
+        return fail(h, MAGUS_ERR_CONFIG, unowned ? "global policy " + std::to_string(g) + " is owned by no rank"
+                                                 : "ranks disagree on the parameters of global policy " +
+                                                       std::to_string(g));
+    }
+    return MAGUS_OK;
+}
+
 extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus_replay_t** out) {
     if (out) *out = nullptr;
     if (!desc || !out) return fail(nullptr, MAGUS_ERR_INVALID_ARG, "magus_replay_create: NULL argument");
@@ -700,6 +795,10 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
         return fail(nullptr, MAGUS_ERR_INVALID_ARG, "MAGUS_F_DUMP_WORDS is not available with MAGUS_F_WALLCLOCK");
     if (d.tuning_warmup < 0 || d.tuning_warmup % 32 != 0)
         return fail(nullptr, MAGUS_ERR_INVALID_ARG, "tuning_warmup must be a multiple of 32");
+    const int P_glob = d.n_policies_global > 0 ? d.n_policies_global : d.n_policies;
+    if (d.n_policies_global < 0 || d.policy_offset < 0 || (int64_t)d.policy_offset + d.n_policies > P_glob)
+        return fail(nullptr, MAGUS_ERR_INVALID_ARG,
+                    "policy slice [policy_offset, policy_offset + n_policies) must lie in [0, n_policies_global)");
     std::string e = validate_model(d.model);
     if (!e.empty()) return fail(nullptr, MAGUS_ERR_CONFIG, "model." + e);
     for (int i = 0; i < d.n_policies; ++i) {
@@ -859,8 +958,13 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
     ALLOC(h->d_out, n_part * sizeof(double) + 4 * sizeof(unsigned int));
     h->d_totals = (double*)h->d_out;
     h->d_flag = (unsigned int*)(h->d_out + n_part * sizeof(double));
-    if (d.world > 1) {
-        ALLOC(h->d_fin, (size_t)d.n_policies * MAGUS_N_TOTALS);
+    h->P_glob = P_glob;
+    h->p_off = d.policy_offset;
+    h->xchg = d.world > 1 || (d.flags & MAGUS_F_NCCL);
+    if (h->xchg) {
+        ALLOC(h->d_fin, (size_t)P_glob * MAGUS_N_TOTALS);
+        ALLOC(h->d_fin_local, (size_t)P_glob * MAGUS_N_TOTALS);
+        cudaMemset(h->d_fin_local, 0, (size_t)P_glob * MAGUS_N_TOTALS * sizeof(double));   // rows of other slices
     }
     ALLOC(h->d_first_low, (size_t)2 * std::max(1, d.n_traces));
     ALLOC(h->d_errkey, 1);
@@ -937,7 +1041,7 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
             return s;
         }
     }
-    if (d.world > 1) {
+    if (h->xchg) {
         if (!nccl_ok()) {
             magus_status s = fail(h, MAGUS_ERR_NCCL, "libnccl.so.2 could not be loaded");
             g_error = h->err;
@@ -945,11 +1049,26 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
             return s;
         }
         ncclUniqueId id;
-        std::memcpy(&id, desc->nccl_unique_id, sizeof(id));
+        if (desc->nccl_unique_id) {
+            std::memcpy(&id, desc->nccl_unique_id, sizeof(id));
+        } else {   // world == 1 (MAGUS_F_NCCL): a one-rank communicator of our own
+            ncclResult_t r = nccl().GetUniqueId(&id);
+            if (r != ncclSuccess) {
+                magus_status s = fail(h, MAGUS_ERR_NCCL, std::string("ncclGetUniqueId: ") + nccl().GetErrorString(r));
+                magus_replay_destroy(h);
+                return s;
+            }
+        }
         ncclResult_t r = nccl().CommInitRank(&h->comm, d.world, id, d.rank);
         if (r != ncclSuccess) {
             magus_status s = fail(h, MAGUS_ERR_NCCL, std::string("ncclCommInitRank: ") + nccl().GetErrorString(r));
             h->comm = nullptr;
+            magus_replay_destroy(h);
+            return s;
+        }
+        magus_status s = check_ranks_agree(h);
+        if (s != MAGUS_OK) {
+            g_error = h->err;
             magus_replay_destroy(h);
             return s;
         }
@@ -1118,11 +1237,12 @@ static magus_status enqueue_run(magus_replay_t* h, const float* d_trace, const f
                        (d.flags & MAGUS_F_PER_TRACE_STATS) ? 1 : 0, (const TraceRec*)(has_work ? h->d_wrec : nullptr),
                        h->d_totals));
     }
-    if (d.world > 1) {
+    if (h->xchg) {
+        // this rank's per-policy sums into its slice rows of the global [P_glob][13], then one allreduce (sum)
         CU(h, launch_k(magus_chunk_sum_kernel, dim3(d.n_policies), dim3(32), 0, s, h->pdl && !detail,
-                       (const double*)h->d_totals, h->n_chunks, h->d_fin));
-        ncclResult_t r = nccl().AllReduce(h->d_fin, h->d_fin, (size_t)d.n_policies * MAGUS_N_TOTALS, ncclFloat64, ncclSum,
-                                          h->comm, s);
+                       (const double*)h->d_totals, h->n_chunks, h->d_fin_local + (size_t)h->p_off * MAGUS_N_TOTALS));
+        ncclResult_t r = nccl().AllReduce(h->d_fin_local, h->d_fin, (size_t)h->P_glob * MAGUS_N_TOTALS, ncclFloat64,
+                                          ncclSum, h->comm, s);
         if (r != ncclSuccess) return fail(h, MAGUS_ERR_NCCL, std::string("ncclAllReduce: ") + nccl().GetErrorString(r));
     }
     if (detail) CU(h, rec(4));
@@ -1232,20 +1352,19 @@ extern "C" magus_status magus_replay_results(magus_replay_t* h, magus_results* o
     const size_t n_part = (size_t)P * h->n_chunks * MAGUS_N_TOTALS;
     std::vector<double> part(n_part + 2);
     CU(h, cudaMemcpy(part.data(), h->d_out, n_part * sizeof(double) + 4 * sizeof(unsigned int), cudaMemcpyDeviceToHost));
-    std::vector<double> tot((size_t)P * MAGUS_N_TOTALS, 0.0);
-    if (d.world > 1) {   // chunk sums on the device (same order), then the cross-rank allreduce
+    std::vector<double> tot((size_t)h->P_glob * MAGUS_N_TOTALS, 0.0);
+    if (h->xchg) {   // chunk sums on the device (same order), then the cross-rank allreduce
         CU(h, cudaMemcpy(tot.data(), h->d_fin, tot.size() * sizeof(double), cudaMemcpyDeviceToHost));
-    } else {
+    } else {         // this rank's slice rows
         for (int pp = 0; pp < P; ++pp)
             for (int c = 0; c < h->n_chunks; ++c)
                 for (int f = 0; f < MAGUS_N_TOTALS; ++f)
-                    tot[(size_t)pp * MAGUS_N_TOTALS + f] += part[((size_t)pp * h->n_chunks + c) * MAGUS_N_TOTALS + f];
+                    tot[(size_t)(h->p_off + pp) * MAGUS_N_TOTALS + f] +=
+                        part[((size_t)pp * h->n_chunks + c) * MAGUS_N_TOTALS + f];
     }
     if (out->policy_totals) std::memcpy(out->policy_totals, tot.data(), tot.size() * sizeof(double));
-    // argmin over policies of the total EDP, ties -> lowest index (A23)
-    int am = 0;
-    for (int pp = 1; pp < P; ++pp)
-        if (tot[(size_t)pp * MAGUS_N_TOTALS + 3] < tot[(size_t)am * MAGUS_N_TOTALS + 3]) am = pp;
+    int32_t am = 0;   // argmin over policies of the total EDP, ties -> lowest index (A23)
+    magus_totals_argmin(tot.data(), h->P_glob, &am);
     out->argmin_policy = am;
     unsigned int fl[4] = {0, 0, 0, 0};
     std::memcpy(fl, part.data() + n_part, sizeof(fl));
@@ -1369,7 +1488,7 @@ extern "C" magus_status magus_replay_geometry(const magus_replay_t* h, int32_t o
         for (const LaunchGroup& g : h->groups) nw += walk_kernel_for(g.key) ? 1 : 0;
         nk += 1 + nw;                                             // mark + one chain-walk kernel per launch group
     }
-    nk += 1 + (d.world > 1 ? 1 : 0);                              // totals (+ chunk sums before the allreduce)
+    nk += 1 + (h->xchg ? 1 : 0);                                  // totals (+ chunk sums before the allreduce)
     int solo = 0;
     for (const LaunchGroup& g : h->groups) solo += g.solo ? 1 : 0;
     int32_t threads = g0.threads, smem = (int32_t)g0.smem;

@@ -26,6 +26,7 @@ STATUS_NAMES = ["MAGUS_OK", "MAGUS_ERR_INVALID_ARG", "MAGUS_ERR_CONFIG", "MAGUS_
 MAGUS, STATIC_MAX, STATIC_MIN, TDP_DEFAULT = 0, 1, 2, 3
 F_PER_TRACE_STATS, F_DUMP_WORDS, F_DUMP_DECISIONS, F_TIMING, F_TIMING_DETAIL = 0x1, 0x2, 0x4, 0x8, 0x10
 F_WALLCLOCK = 0x20   # NEXT-1 wall-clock governor rounds (A32)
+F_NCCL = 0x40        # the cross-rank exchange (chunk sums + NCCL allreduce) also at world == 1
 TOTAL_FIELDS = ["E", "E_pkg", "T", "EDP", "slowdown", "energy_saving", "edp_saving", "n_hi", "n_thr",
                 "transitions", "tune_events", "lock_ticks", "n_traces"]
 N_TOTALS = len(TOTAL_FIELDS)
@@ -56,7 +57,8 @@ class c_desc(C.Structure):
                 ("global_trace_offset", C.c_int64), ("n_policies", C.c_int32), ("_reserved0", C.c_int32),
                 ("policies", C.POINTER(c_policy)), ("model", c_model), ("rank", C.c_int32), ("world", C.c_int32),
                 ("nccl_unique_id", C.c_void_p), ("flags", C.c_uint32), ("dump_first_trace", C.c_int32),
-                ("dump_n_traces", C.c_int32), ("tuning_segments", C.c_int32), ("tuning_warmup", C.c_int32)]
+                ("dump_n_traces", C.c_int32), ("tuning_segments", C.c_int32), ("tuning_warmup", C.c_int32),
+                ("n_policies_global", C.c_int32), ("policy_offset", C.c_int32)]
 
 
 class c_trace_stats(C.Structure):
@@ -116,12 +118,16 @@ lib.magus_counters_to_trace.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_i
 lib.magus_active_savings.restype = _S
 lib.magus_active_savings.argtypes = [C.POINTER(C.c_double), C.c_int32, C.c_int32, C.c_int32, C.c_double,
                                      C.POINTER(C.c_double)]
+lib.magus_totals_argmin.restype = _S
+lib.magus_totals_argmin.argtypes = [C.POINTER(C.c_double), C.c_int32, C.POINTER(C.c_int32)]
+lib.magus_grid_plan.restype = _S
+lib.magus_grid_plan.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_int32, C.POINTER(C.c_int64)]
 lib.magus_derive_thresholds.restype = _S
 lib.magus_derive_thresholds.argtypes = [C.POINTER(c_policy), C.POINTER(c_model), C.POINTER(C.c_double),
                                         C.POINTER(C.c_float), C.POINTER(C.c_int32)]
 lib.magus_replay_geometry.restype = _S
 lib.magus_replay_geometry.argtypes = [C.c_void_p, C.POINTER(C.c_int32)]
-assert lib.magus_abi_version() == 1, "ABI version mismatch"
+assert lib.magus_abi_version() == 2, "ABI version mismatch"
 
 
 def header_functions(path: str = HEADER):
@@ -186,6 +192,22 @@ def abi_version() -> int:
     return lib.magus_abi_version()
 
 
+def totals_argmin(policy_totals) -> int:
+    """Host-only: the library's argmin over policies of the total EDP (policies with traces; ties -> lowest)."""
+    t = np.ascontiguousarray(policy_totals, dtype=np.float64)
+    out = C.c_int32()
+    _check(lib.magus_totals_argmin(t.ctypes.data_as(C.POINTER(C.c_double)), t.shape[0], C.byref(out)))
+    return out.value
+
+
+def grid_plan(world: int, rank: int, policy_shards: int, n_traces: int, n_policies: int):
+    """Host-only: (global_trace_offset, n_traces, policy_offset, n_policies) of `rank` in a 2-D split of
+    n_traces traces x n_policies policies over world ranks, policy_shards of them across the policies."""
+    out = (C.c_int64 * 4)()
+    _check(lib.magus_grid_plan(world, rank, policy_shards, n_traces, n_policies, out))
+    return tuple(int(x) for x in out)
+
+
 def derive_thresholds(policy: Policy, model: Model):
     """Host-only: {'dinc','ddec','L','P_lo','P_hi','B_lo','B_hi','astar_lo','astar_hi','s_min'}."""
     d = (C.c_double * 5)()
@@ -247,7 +269,7 @@ def gen_traces(seed: int, n_traces: int, n_samples: int, class_mix: int, trace, 
 
 @dataclass
 class Results:
-    totals: np.ndarray                 # [P][13] fp64
+    totals: np.ndarray                 # [n_policies_global][13] fp64
     argmin_policy: int
     per_trace: np.ndarray | None       # structured [n_traces][P]
     words: np.ndarray | None           # [P][n_traces][n_blocks][2] uint32
@@ -270,7 +292,7 @@ class Replay:
     def __init__(self, n_traces: int, n_samples: int, policies, model: Model | None = None, *, trace_stride: int = 0,
                  global_trace_offset: int = 0, rank: int = 0, world: int = 1, nccl_id: bytes | None = None,
                  flags: int = 0, dump_first_trace: int = 0, dump_n_traces: int = 0, tuning_segments: int = 0,
-                 tuning_warmup: int = 0):
+                 tuning_warmup: int = 0, n_policies_global: int = 0, policy_offset: int = 0):
         self.policies = list(policies)
         self.model = model or Model()
         self.n_traces, self.n_samples = n_traces, n_samples
@@ -278,12 +300,13 @@ class Replay:
         self.flags = flags
         self.dump_first_trace, self.dump_n_traces = dump_first_trace, dump_n_traces
         P = len(self.policies)
+        self.n_policies_global = n_policies_global or P
         self._pols = (c_policy * max(1, P))(*[p.c() for p in self.policies])
         self._nccl = C.create_string_buffer(nccl_id, 128) if nccl_id else None
         desc = c_desc(n_traces, n_samples, self.trace_stride, global_trace_offset, P, 0,
                       C.cast(self._pols, C.POINTER(c_policy)), self.model.c(), rank, world,
                       C.cast(self._nccl, C.c_void_p) if self._nccl else None, flags, dump_first_trace,
-                      dump_n_traces, tuning_segments, tuning_warmup)
+                      dump_n_traces, tuning_segments, tuning_warmup, n_policies_global, policy_offset)
         h = C.c_void_p()
         _check(lib.magus_replay_create(C.byref(desc), C.byref(h)))
         self._h = h
@@ -337,7 +360,7 @@ class Replay:
     def results(self, per_trace: bool | None = None, words: bool | None = None, decisions: bool | None = None,
                 raise_on_trace_error: bool = True) -> Results:
         P = len(self.policies)
-        totals = np.zeros((P, N_TOTALS), np.float64)
+        totals = np.zeros((self.n_policies_global, N_TOTALS), np.float64)
         per = words_a = dec = None
         if per_trace if per_trace is not None else (self.flags & F_PER_TRACE_STATS):
             per = np.zeros((self.n_traces, P), TRACE_STATS_DTYPE)

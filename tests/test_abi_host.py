@@ -25,7 +25,7 @@ def test_library_exports_every_declared_symbol():
     lib = ctypes.CDLL(M.LIB_PATH)
     for n in names:
         getattr(lib, n)
-    assert M.abi_version() == 1
+    assert M.abi_version() == 2
 
 
 def test_library_is_sm100a_only():

@@ -257,6 +257,69 @@ def test_determinism_and_virtual_ranks(M):
     np.testing.assert_allclose(parts[0].totals[:, :12] + parts[1].totals[:, :12], a.totals[:, :12], rtol=1e-9)
 
 
+@pytest.mark.parametrize("graph", [False, True])
+def test_nccl_exchange_world1_equals_local(M, graph):
+    """The cross-rank exchange on one B200 (MAGUS_F_NCCL at world = 1: a one-rank NCCL communicator):
+    magus_chunk_sum_kernel, then ncclAllReduce on the run's stream -- inside the captured CUDA graph on a
+    non-default stream -- give the same per-policy totals (the chunks are added in the same order) and the
+    same argmin as the host sum without NCCL, and both equal the oracle's totals within 1e-9."""
+    s = SMALL["cfg5-small"]
+    pols = s["policies"] + [pol(deriv_ticks=2, high_freq_threshold=0.4)]
+    stride = (s["n"] + 3) // 4 * 4
+    tr, w = gpu_gen(M, s["seed"], s["n"], s["ns"], s["mix"], stride)
+    st = torch.cuda.Stream() if graph else None
+    out = {}
+    for nccl in (0, 1):
+        with M.Replay(s["n"], s["ns"], PA.gpu_policies(pols), trace_stride=stride,
+                      flags=M.F_PER_TRACE_STATS | (M.F_NCCL if nccl else 0)) as R:
+            for _ in range(2):                  # graph capture, then a replay of the captured graph
+                R.run(tr, w, st)
+                res = R.results()
+            res.geometry = R.geometry()
+        out[nccl] = res
+    assert np.array_equal(out[0].totals, out[1].totals) and out[0].argmin_policy == out[1].argmin_policy
+    assert out[1].geometry["kernels_per_run"] == out[0].geometry["kernels_per_run"] + 1
+    assert out[0].per_trace.tobytes() == out[1].per_trace.tobytes()
+    rec, _ = oracle_run(tr.cpu().numpy(), w.cpu().numpy(), pols, s["n"])
+    np.testing.assert_allclose(out[1].totals, PA.oracle_totals(rec), rtol=1e-9, atol=1e-9)
+
+
+def test_parameter_grid_slices(M):
+    """North star "shards by trace and parameter grid" on one GPU: a 2 x 2 grid of
+    virtual ranks (two trace shards x two policy slices, magus_grid_plan) run one after the other; each
+    rank's per-trace records are its block of the single run's records, its totals land in its policy rows of
+    the global [P][13], and the four add up to the single run's totals (argmin equal).  With the exchange on
+    (MAGUS_F_NCCL, one rank), a slice that leaves global policies without an owner is refused at create by the
+    cross-rank consistency check (MAGUS_ERR_CONFIG), and a full slice passes it."""
+    s = SMALL["mixed-kinds"]
+    pols = s["policies"]
+    n, ns, P = s["n"], s["ns"], len(s["policies"])
+    tr, w = gpu_gen(M, s["seed"], n, ns, s["mix"], (n + 3) // 4 * 4)
+    full = run_gpu(M, tr, w, pols, n, ns, (n + 3) // 4 * 4, flags=M.F_PER_TRACE_STATS)
+    acc = np.zeros_like(full.totals)
+    for r in range(4):
+        t0, nt, p0, npol = M.grid_plan(4, r, 2, n, P)
+        trs, ws = gpu_gen(M, s["seed"], nt, ns, s["mix"], offset=t0)
+        with M.Replay(nt, ns, PA.gpu_policies(pols[p0:p0 + npol]), trace_stride=(nt + 3) // 4 * 4,
+                      global_trace_offset=t0, flags=M.F_PER_TRACE_STATS, n_policies_global=P,
+                      policy_offset=p0) as R:
+            R.run(trs, ws)
+            res = R.results()
+        assert res.totals.shape == full.totals.shape
+        assert np.all(res.totals[:p0] == 0) and np.all(res.totals[p0 + npol:] == 0)
+        assert res.per_trace.tobytes() == np.ascontiguousarray(full.per_trace[t0:t0 + nt, p0:p0 + npol]).tobytes()
+        acc += res.totals
+    np.testing.assert_allclose(acc, full.totals, rtol=1e-12)
+    assert M.totals_argmin(acc) == full.argmin_policy
+    with pytest.raises(M.MagusError) as e:
+        M.Replay(n, ns, PA.gpu_policies(pols[:2]), flags=M.F_NCCL, n_policies_global=P, policy_offset=0)
+    assert e.value.status == M.ERR_CONFIG and "owned by no rank" in str(e.value)
+    with M.Replay(n, ns, PA.gpu_policies(pols), flags=M.F_NCCL, n_policies_global=P) as R:
+        R.run(tr, w)
+        res = R.results()
+    np.testing.assert_allclose(res.totals, full.totals, rtol=1e-12)
+
+
 def test_graph_path_matches_direct(M):
     """On a non-default stream the library replays each run as a captured CUDA graph; results equal the
     direct (stream-ordered launches) path, across graph reuse and a re-capture after a buffer change."""
