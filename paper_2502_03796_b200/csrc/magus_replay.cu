@@ -165,11 +165,15 @@ WallKernel wall_kernel_for(int key, int64_t n_chains, int n_sm) {
 }
 
 // one-warp-CTA replay kernel (replay_solo.cuh) of a chain kind, or nullptr if it has none
-ReplayKernel solo_kernel_for(int key) {
-    const int v = env_int("MAGUS_SOLO_BAL", 2);   // stage block variant (replay_solo.cuh)
+ReplayKernel solo_kernel_for(int key, bool sym) {
+    int v = env_int("MAGUS_SOLO_BAL", 2);   // stage block variant (replay_solo.cuh)
+    if (v == 9 && !sym) v = 3;              // |d| > d*_inc needs d*_dec == -d*_inc
 #define SOLO_K(KK)                                                                                               \
     (v == 0   ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 0>                    \
      : v == 2 ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 2>                    \
+     : v == 3 ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 3>                    \
+     : v == 4 ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 4>                    \
+     : v == 9 ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 9>                    \
               : (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 1>)
     switch (key) {
         case 1: return SOLO_K(1);
@@ -704,7 +708,9 @@ static void choose_geometry(magus_replay_t* h, int n_sm, int forced_segments) {
     for (LaunchGroup& g : h->groups) {
         g.n_ctas = p.n_seg * g.n_tblocks * g.n_pblocks;
         // one policy warp per tile group: one-warp CTAs with CTA-uniform pipeline state (replay_solo.cuh)
-        ReplayKernel sk = solo_kernel_for(g.key);
+        bool sym = true;   // every lane policy of the group has d*_dec == -d*_inc (the |d| tune-flag test)
+        for (int q = g.q_base; q < g.q_base + g.nq; ++q) sym = sym && h->lane[q].ddec == -h->lane[q].dinc;
+        ReplayKernel sk = solo_kernel_for(g.key, sym);
         g.solo = sk && g.npw == 1 && kTC == 8 && env_int("MAGUS_SOLO", 1) != 0;
         if (g.solo) {
             g.kernel = sk;

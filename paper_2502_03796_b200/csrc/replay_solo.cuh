@@ -73,6 +73,69 @@ struct SoloConst {
     float B_lo;
 };
 
+// One whole steady-state stage (8 ticks x 4 chains) of MAGUS chains with a register ring of K <= 3 values,
+// with the 3-DSETP / 1-PLOP3 level logic: V = 3 Alg. 2 by popcount (MAGUS_PSTAGE_K<K>), V = 4 by the scaled
+// incremental count (MAGUS_QSTAGE_K<K>); V = 5 / 6 the same with the chains interleaved in pairs, V = 7 / 8 one
+// chain after the other (predicate-register pressure).
+#ifndef MAGUS_PQ_GROUP
+#define MAGUS_PQ_GROUP 4
+#endif
+#define PQ_CAT3(a, b, c) a##b##c
+#define PQ_NAME(P, G, K) PQ_CAT3(P, G, K)
+template <int K, int V>
+__device__ __forceinline__ void solo_stage_pq(MagusState<K, false>* s, float* lock, float* nthr, uint32_t* wcmd,
+                                              SegStats* ss, uint32_t& vmax, uint32_t tile, const SoloConst& sc,
+                                              const DevPolicy& pol) {
+    uint32_t e0 = s[0].evh, e1 = s[1].evh, e2 = s[2].evh, e3 = s[3].evh;
+#define PQ_F s[0].f, s[1].f, s[2].f, s[3].f
+#define PQ_R1 s[0].ring.v[0], s[1].ring.v[0], s[2].ring.v[0], s[3].ring.v[0]
+#define PQ_R2                                                                                                  \
+    s[0].ring.v[0], s[0].ring.v[1], s[1].ring.v[0], s[1].ring.v[1], s[2].ring.v[0], s[2].ring.v[1], s[3].ring.v[0], \
+        s[3].ring.v[1]
+#define PQ_R3                                                                                                  \
+    s[0].ring.v[0], s[0].ring.v[1], s[0].ring.v[2], s[1].ring.v[0], s[1].ring.v[1], s[1].ring.v[2], s[2].ring.v[0], \
+        s[2].ring.v[1], s[2].ring.v[2], s[3].ring.v[0], s[3].ring.v[1], s[3].ring.v[2]
+#define PQ_STATS                                                                                               \
+    ss[0].sexc, ss[1].sexc, ss[2].sexc, ss[3].sexc, lock[0], lock[1], lock[2], lock[3], nthr[0], nthr[1], nthr[2], \
+        nthr[3], wcmd[0], wcmd[1], wcmd[2], wcmd[3], vmax, tile, sc.B_lo, sc.Blo_d, pol.dinc, pol.ddec
+#define PQ_P(G, KK) PQ_NAME(MAGUS_PSTAGE, G, KK)
+#define PQ_Q(G, KK) PQ_NAME(MAGUS_QSTAGE, G, KK)
+#define PQ_CNT s[0].cnt, s[1].cnt, s[2].cnt, s[3].cnt
+    const uint32_t maskc = (uint32_t)pol.logmask, smin = (uint32_t)pol.s_min;
+    const uint32_t bitc = 1u << (pol.C - 1), mone = 0xFFFFFFFFu * pol.one;
+#define PQ_BODY(G)                                                                                             \
+    if constexpr (V % 2 == 1) {                                                                                \
+        if constexpr (K == 1) PQ_P(G, _K1)(PQ_F, PQ_R1, e0, e1, e2, e3, PQ_STATS, maskc, smin, pol.one);         \
+        else if constexpr (K == 2) PQ_P(G, _K2)(PQ_F, PQ_R2, e0, e1, e2, e3, PQ_STATS, maskc, smin, pol.one);    \
+        else PQ_P(G, _K3)(PQ_F, PQ_R3, e0, e1, e2, e3, PQ_STATS, maskc, smin, pol.one);                          \
+    } else {                                                                                                   \
+        if constexpr (K == 1)                                                                                  \
+            PQ_Q(G, _K1)(PQ_F, PQ_R1, e0, e1, e2, e3, PQ_CNT, PQ_STATS, bitc, pol.smin_sc, pol.one, mone);       \
+        else if constexpr (K == 2)                                                                             \
+            PQ_Q(G, _K2)(PQ_F, PQ_R2, e0, e1, e2, e3, PQ_CNT, PQ_STATS, bitc, pol.smin_sc, pol.one, mone);       \
+        else PQ_Q(G, _K3)(PQ_F, PQ_R3, e0, e1, e2, e3, PQ_CNT, PQ_STATS, bitc, pol.smin_sc, pol.one, mone);      \
+    }
+    if constexpr (V <= 4) { PQ_BODY() }
+    else if constexpr (V <= 6) { PQ_BODY(G2) }
+    else if constexpr (V <= 8) { PQ_BODY(G1) }
+    else if constexpr (V <= 10) { PQ_BODY(S) }
+    else if constexpr (V <= 12) { PQ_BODY(SG2) }
+    else { PQ_BODY(SG1) }
+#undef PQ_BODY
+#undef PQ_CNT
+#undef PQ_P
+#undef PQ_Q
+#undef PQ_F
+#undef PQ_R1
+#undef PQ_R2
+#undef PQ_R3
+#undef PQ_STATS
+    s[0].evh = e0;
+    s[1].evh = e1;
+    s[2].evh = e2;
+    s[3].evh = e3;
+}
+
 // One whole steady-state stage (8 ticks x 4 chains) of MAGUS chains with a register ring of K <= 3 values.
 template <int K, bool THR32 = false>
 __device__ __forceinline__ void solo_stage(MagusState<K, false>* s, float* lock, float* nthr,
@@ -118,7 +181,8 @@ __device__ __forceinline__ void solo_stage(MagusState<K, false>* s, float* lock,
 }
 
 // BAL: 0 = the integer stage block (MAGUS_STAGE8_K<K>), 1 = the pipe-balanced one (MAGUS_SSTAGE_K<K>),
-// 2 = balanced with the throttle test on the ALU pipe (MAGUS_SSTAGEF_K<K>)
+// 2 = balanced with the throttle test on the ALU pipe (MAGUS_SSTAGEF_K<K>), 3 / 4 = the 3-DSETP level logic with
+// Alg. 2 by popcount / by the incremental count (MAGUS_PSTAGE_K<K> / MAGUS_QSTAGE_K<K>)
 template <class T, int TC, int NSTAGE, int BAL>
 __global__ void __launch_bounds__(32, kSoloCtasPerSm)
     magus_replay_solo_kernel(const __grid_constant__ CUtensorMap tmap, const ReplayParams p) {
@@ -238,6 +302,8 @@ __global__ void __launch_bounds__(32, kSoloCtasPerSm)
                 if constexpr (BAL == 1) solo_stage(st, lockf, nthrf, wcmd, ss, vmax, tile + lane_off, sc, pol);
                 else if constexpr (BAL == 2)
                     solo_stage<T::kRingK, true>(st, lockf, nthrf, wcmd, ss, vmax, tile + lane_off, sc, pol);
+                else if constexpr (BAL >= 3)
+                    solo_stage_pq<T::kRingK, BAL>(st, lockf, nthrf, wcmd, ss, vmax, tile + lane_off, sc, pol);
                 else T::stage8(st, tile + lane_off, pol, B_lo, Blo_d, wcmd, ss, vmax);
                 __syncwarp();   // every lane's tile reads are complete before the slot is refilled
                 if (i + NSTAGE < G.n_stages)

@@ -237,6 +237,108 @@ def build_stage_f(K, TC=8, walk=False, traces=1, thr64=True, one=False):
     return out
 
 
+def build_stage_p(K, TC=8, popc=True, group=4, sym=False):
+    """MAGUS_PSTAGE_K<K> (popc=True) / MAGUS_QSTAGE_K<K> (popc=False): the solo kernel's steady-state stage
+    (TC ticks x 4 chains, tile loads included) with fewer instructions per chain-tick than MAGUS_SSTAGEF_K<K>:
+    - the new level is hf | +1 | (level & !dec): one DSETP gives (d >= d*_dec) & level directly, so the
+      predicate logic is three DSETPs, one ISETP and one 3-input PLOP3 (ptxas otherwise re-evaluates the
+      +1 and Alg. 2 compares in OR form);
+    - popc=True: Alg. 2's window count is popc(log & (2^C - 1)) (LOP3 + POPC, no incremental count: the
+      XU pipe then carries the conversion and the popcount); popc=False keeps the scaled incremental count
+      (LOP3 + two IMADs) and compares against s_min << (C-1).
+    Decisions identical to MAGUS_TICK4_ASM."""
+    C = 4
+    names = [(f"f{c}", "+r") for c in range(C)] + \
+            [(f"r{c}_{i}", "+d") for c in range(C) for i in range(K)] + \
+            [(f"evh{c}", "+r") for c in range(C)] + \
+            ([] if popc else [(f"cnt{c}", "+r") for c in range(C)]) + \
+            [(f"exc{c}", "+d") for c in range(C)] + [(f"lock{c}", "+f") for c in range(C)] + \
+            [(f"nthr{c}", "+f") for c in range(C)] + [(f"wcmd{c}", "+r") for c in range(C)] + [("vmax", "+r")]
+    inames = [("tile", "r"), ("Blo", "f"), ("Blod", "d"), ("dinc", "d"), ("ddec", "d")] + \
+             ([("maskc", "r"), ("smin", "r"), ("one", "r")] if popc else
+              [("bitc", "r"), ("smin", "r"), ("one", "r"), ("mone", "r")])
+    idx = {n: f"%{i}" for i, (n, _) in enumerate(names + inames)}
+    R = idx.__getitem__
+    body = ["{", ".reg .pred phi<4>, pthr<4>, pinc<4>, pev<4>, phf<4>, pk<4>, pq<4>;",
+            f".reg .b32 D<{TC * C}>;", f".reg .f64 dd<4>, dv<4>, da<4>, dx<4>, ad<{TC * C}>;",
+            ".reg .b32 tb<4>, wv<4>, pc<4>;"]
+    for c in range(C):
+        body.append(f"setp.ne.u32 phi{c}, {R(f'f{c}')}, 0;")
+    for tt in range(TC):
+        body.append(f"ld.shared.v4.f32 {{D{tt * C}, D{tt * C + 1}, D{tt * C + 2}, D{tt * C + 3}}}, [{R('tile')}+{tt * 512}];")
+        per_chain = [
+            "cvt.f64.f32 dd{c}, {D};",
+            "setp.gt.and.f32 pthr{c}, {D}, {Blo}, !phi{c};",             # throttled: f_min and D > B_lo (A14)
+            "selp.f64 {ad}, {Blod}, dd{c}, pthr{c};",                     # A = min(D, B[f]) as fp64 (exact)
+            "sub.f64 dv{c}, {ad}, {old};",                                # Alg. 1 numerator A_t - A_{t-k} (P:207)
+        ] + ([
+            "abs.f64 da{c}, dv{c};",                                      # symmetric thresholds (d*_dec = -d*_inc):
+            "setp.gt.f64 pev{c}, da{c}, {dinc};",                         # tune flag iff |d| > d*_inc (P:213, P:243)
+        ] if sym else [
+            "setp.gt.f64 pinc{c}, dv{c}, {dinc};",                        # +1 (P:209)
+            "setp.lt.or.f64 pev{c}, dv{c}, {ddec}, pinc{c};",             # tune flag: +1 or -1 (P:213, P:243)
+        ]) + [
+            "setp.ge.and.f64 pk{c}, dv{c}, {ddec}, phi{c};",              # level kept: f_max and not -1
+        ] + ([
+            "setp.gt.or.f64 pk{c}, dv{c}, {dinc}, pk{c};",                # ... or +1
+        ] if sym else [])
+        if popc:
+            per_chain += [
+                "shl.b32 {evh}, {evh}, 1;",
+                "@pev{c} mad.lo.u32 {evh}, {one}, {one}, {evh};",
+                "and.b32 wv{c}, {evh}, {maskc};",                         # the last C flags
+                "popc.b32 pc{c}, wv{c};",
+                "setp.ge.u32 phf{c}, pc{c}, {smin};",                     # Alg. 2 (P:229-230)
+            ]
+        else:
+            per_chain += [
+                "and.b32 tb{c}, {evh}, {bitc};",                          # the flag leaving the C-window (scaled)
+                "shl.b32 {evh}, {evh}, 1;",
+                "@pev{c} mad.lo.u32 {evh}, {one}, {one}, {evh};",
+                "mad.lo.u32 {cnt}, tb{c}, {mone}, {cnt};",                # window count: - leaving + entering
+                "@pev{c} mad.lo.u32 {cnt}, {bitc}, {one}, {cnt};",
+                "setp.ge.u32 phf{c}, {cnt}, {smin};",                     # Alg. 2 (P:230)
+            ]
+        per_chain += ([
+            "or.pred phi{c}, pk{c}, phf{c};",                             # lock || +1 || (f_max && !-1)
+        ] if sym else [
+            "or.pred pq{c}, pinc{c}, pk{c};",
+            "or.pred phi{c}, pq{c}, phf{c};",                             # lock || +1 || (f_max && !-1)
+        ]) + [
+            "shl.b32 {wcmd}, {wcmd}, 1;",
+            "@phi{c} mad.lo.u32 {wcmd}, {one}, {one}, {wcmd};",
+            "sub.f64 dx{c}, dd{c}, {ad};",                                # throttling excess D - A (0 unless thr)
+            "add.f64 {exc}, {exc}, dx{c};",
+            "@phf{c} add.f32 {lock}, {lock}, 0f3F800000;",
+            "@pthr{c} add.f32 {nthr}, {nthr}, 0f3F800000;",
+            "max.u32 {vmax}, {vmax}, {D};",                               # validation (A17)
+        ]
+        for g0 in range(0, C, group):
+          for tmpl in per_chain:
+            for c in range(g0, g0 + group):
+                t = tt * C + c
+                old = f"ad{(tt - K) * C + c}" if tt >= K else R(f"r{c}_{K - 1 - tt}")
+                body.append(tmpl.format(c=c, D=f"D{t}", ad=f"ad{t}", old=old, Blo=R("Blo"), Blod=R("Blod"),
+                                        dinc=R("dinc"), ddec=R("ddec"), evh=R(f"evh{c}"), one=R("one"),
+                                        maskc=R("maskc") if popc else None, bitc=None if popc else R("bitc"),
+                                        mone=None if popc else R("mone"), cnt=None if popc else R(f"cnt{c}"),
+                                        smin=R("smin"), wcmd=R(f"wcmd{c}"), exc=R(f"exc{c}"), lock=R(f"lock{c}"),
+                                        nthr=R(f"nthr{c}"), vmax=R("vmax")))
+    for c in range(C):
+        body.append(f"selp.u32 {R(f'f{c}')}, 1, 0, phi{c};")
+        for i in range(K):   # ring newest first: r_i = A_{t0 + TC - 1 - i}
+            body.append(f"mov.f64 {R(f'r{c}_{i}')}, ad{(TC - 1 - i) * C + c};")
+    body.append("}")
+    params = ", ".join(n for n, _ in names + inames)
+    name = f"MAGUS_{'P' if popc else 'Q'}STAGE{'S' if sym else ''}{'' if group == 4 else 'G' + str(group)}_K{K}"
+    out = [f"#define {name}(...) {name}_(__VA_ARGS__)", f"#define {name}_({params}) \\", "    asm volatile( \\"]
+    out += [f'        "{l}\\n\\t" \\' for l in body]
+    out.append("        : " + ", ".join(f'"{c}"({n})' for n, c in names) + " \\")
+    out.append("        : " + ", ".join(f'"{c}"({n})' for n, c in inames) + " \\")
+    out.append('        : "memory")')
+    return out
+
+
 out = ["// GENERATED by scripts/gen_tick4.py -- do not edit.  One MAGUS tick for the 4 chains of a lane, the",
        "// four chains' instructions interleaved (DESIGN.md section 7); semantics = magus_tick<K, false, SLOW>.",
        "// cnt is the window count scaled by 2^(C-1).",
@@ -246,6 +348,10 @@ for K in (1, 2, 3):
     out += [""] + build_stage(K)
     out += [""] + build_stage_f(K)
     out += [""] + build_stage_f(K, thr64=False)
+    for g in (4, 2, 1):
+        for sym in (False, True):
+            out += [""] + build_stage_p(K, popc=True, group=g, sym=sym)
+            out += [""] + build_stage_p(K, popc=False, group=g, sym=sym)
 for K in range(1, 9):
     out += [""] + build_stage_f(K, walk=True)
     out += [""] + build_stage_f(K, walk=True, one=True, thr64=False)

@@ -88,6 +88,18 @@ def pack_words_tpn(codes):
     return out
 
 
+def compare_totals(gpu_totals, ora_rec, label=""):
+    """Per-policy totals (MAGUS_TOT_*) against the oracle's (math.fsum of its records): E, E_pkg, T, EDP and the
+    counts within 1e-9 relative; the three fraction columns (slowdown, energy_saving, edp_saving) are SUMS of
+    n per-trace fractions, each held to 1e-9 absolute (FRAC_ATOL), so their bar is n * 1e-9 absolute."""
+    want = oracle_totals(ora_rec)
+    n = ora_rec.shape[0]
+    frac = [4, 5, 6]
+    other = [i for i in range(want.shape[1]) if i not in frac]
+    np.testing.assert_allclose(gpu_totals[:, other], want[:, other], rtol=RTOL, atol=ATOL, err_msg=label)
+    np.testing.assert_allclose(gpu_totals[:, frac], want[:, frac], rtol=0, atol=max(1, n) * FRAC_ATOL, err_msg=label)
+
+
 def oracle_totals(ora_rec):
     """Per-policy sums the library reports (MAGUS_TOT_*), from oracle per-trace records (math.fsum)."""
     import math

@@ -110,7 +110,7 @@ def test_small_configs(M, name, segments):
     PA.compare_records(res.per_trace, rec, name)
     assert np.array_equal(res.words, PA.pack_words(codes))
     assert np.array_equal(res.decisions, codes[:, s["n"] - 5:, :])
-    np.testing.assert_allclose(res.totals, PA.oracle_totals(rec), rtol=1e-9, atol=1e-9)
+    PA.compare_totals(res.totals, rec)
     edp = PA.oracle_totals(rec)[:, 3]
     assert res.totals[res.argmin_policy, 3] <= edp.min() * (1 + 1e-9)
     if segments == 7:
@@ -136,7 +136,7 @@ def test_saturating_bandwidth_model(M, name, segments):
     PA.compare_records(res.per_trace, rec, f"saturating {name}")
     assert np.array_equal(res.words, PA.pack_words(codes))
     assert np.array_equal(res.decisions, codes[:, :4, :])
-    np.testing.assert_allclose(res.totals, PA.oracle_totals(rec), rtol=1e-9, atol=1e-9)
+    PA.compare_totals(res.totals, rec)
     lin, _ = oracle_run(tr.cpu().numpy(), w.cpu().numpy(), s["policies"], s["n"])
     assert not np.array_equal(lin["n_thr"], rec["n_thr"])   # the model changed what the loop saw
 
@@ -281,7 +281,7 @@ def test_nccl_exchange_world1_equals_local(M, graph):
     assert out[1].geometry["kernels_per_run"] == out[0].geometry["kernels_per_run"] + 1
     assert out[0].per_trace.tobytes() == out[1].per_trace.tobytes()
     rec, _ = oracle_run(tr.cpu().numpy(), w.cpu().numpy(), pols, s["n"])
-    np.testing.assert_allclose(out[1].totals, PA.oracle_totals(rec), rtol=1e-9, atol=1e-9)
+    PA.compare_totals(out[1].totals, rec)
 
 
 def test_parameter_grid_slices(M):
@@ -365,7 +365,7 @@ def test_repeated_runs_reuse_scratch(M):
             res = R.results()
             mism += res.n_mismatched_segments
             PA.compare_records(res.per_trace, refs[it % 2], f"run {it}")
-            np.testing.assert_allclose(res.totals, PA.oracle_totals(refs[it % 2]), rtol=1e-9, atol=1e-9)
+            PA.compare_totals(res.totals, refs[it % 2])
     assert mism > 0, "inputs should exercise the fix-up"
 
 
@@ -431,7 +431,7 @@ def test_full_size_every_trace(M, cfg):
     word_ids = None if cfg != 3 else np.r_[np.arange(0, 128), np.arange(n - 128, n)]
     rec, n_words = _oracle_all_traces(desc, n, c["policies"], 32 if cfg == 3 else 256, res.words, word_ids)
     PA.compare_records(res.per_trace, rec, f"cfg{cfg}")
-    np.testing.assert_allclose(res.totals, PA.oracle_totals(rec), rtol=1e-9, atol=1e-9)
+    PA.compare_totals(res.totals, rec)
     edp = PA.oracle_totals(rec)[:, 3]
     assert res.totals[res.argmin_policy, 3] <= edp.min() * (1 + 1e-9)
     # the decision dump's cmd / tune-flag bits are the replay kernel's own words ...
@@ -472,7 +472,7 @@ def test_cfg4_shard_every_trace(M, monkeypatch):
             rec, n_words = _oracle_all_traces(desc, n, c["policies"], 512, res.words, word_ids)
             assert n_words == len(set(word_ids.tolist()))
         PA.compare_records(res.per_trace, rec, f"cfg4-shard synth={synth}")
-        np.testing.assert_allclose(res.totals, PA.oracle_totals(rec), rtol=1e-9, atol=1e-9)
+        PA.compare_totals(res.totals, rec)
         mism.append(res.n_mismatched_segments)
         print(f"synth {synth}: compared {n} x {len(c['policies'])} records; geometry {res.geometry}, "
               f"mismatched {res.n_mismatched_segments}, walked {res.fixup_rounds}")
@@ -510,7 +510,7 @@ def test_open_loop_mode(M, segments):
     assert np.array_equal(res.words, PA.pack_words(codes))
     assert np.array_equal(res.decisions, codes[:, :4, :])
     assert int(rec["n_thr"].sum()) == 0 and int(res.per_trace["n_thr"].sum()) == 0
-    np.testing.assert_allclose(res.totals, PA.oracle_totals(rec), rtol=1e-9, atol=1e-9)
+    PA.compare_totals(res.totals, rec)
 
 
 @pytest.mark.parametrize("with_times", [False, True])
@@ -588,7 +588,7 @@ def test_wallclock_rounds(M, name, observe, roundmajor, unroll, monkeypatch):
                                      O.Model(observe=observe), dump=(n - 6, 6))
     PA.compare_records(res.per_trace, rec, f"wallclock {name}")
     assert np.array_equal(res.decisions, codes)
-    np.testing.assert_allclose(res.totals, PA.oracle_totals(rec), rtol=1e-9, atol=1e-9)
+    PA.compare_totals(res.totals, rec)
     if observe == 0:
         assert rec["T"].sum() > ns * 0.1 * n * 1.001   # entries did span rounds
     if roundmajor:
