@@ -165,9 +165,45 @@ WallKernel wall_kernel_for(int key, int64_t n_chains, int n_sm) {
 }
 
 // one-warp-CTA replay kernel (replay_solo.cuh) of a chain kind, or nullptr if it has none
-ReplayKernel solo_kernel_for(int key, bool sym) {
+ReplayKernel solo_kernel_for(int key, bool sym, bool bits_ok) {
     int v = env_int("MAGUS_SOLO_BAL", 2);   // stage block variant (replay_solo.cuh)
     if (v == 9 && !sym) v = 3;              // |d| > d*_inc needs d*_dec == -d*_inc
+    if (v >= 10 && v <= 17) {   // the unified-stage kernel; v - 10 = VAR bits (1 |d| test, 2 incremental count,
+                                // 4 integer sample conversion)
+        int var = v - 10;
+        if (!sym) var &= ~1;
+        if (!bits_ok) var &= ~4;
+#define USOLO(KK, VV) (ReplayKernel) magus_replay_usolo_kernel<MagusTicker<KK, false>, kTC, kNStage, VV>
+#define USOLO_K(KK)                                                                                             \
+    switch (var) {                                                                                              \
+        case 0: return USOLO(KK, 0);                                                                            \
+        case 1: return USOLO(KK, 1);                                                                            \
+        case 2: return USOLO(KK, 2);                                                                            \
+        case 3: return USOLO(KK, 3);                                                                            \
+        case 4: return USOLO(KK, 4);                                                                            \
+        case 5: return USOLO(KK, 5);                                                                            \
+        case 6: return USOLO(KK, 6);                                                                            \
+        default: return USOLO(KK, 7);                                                                           \
+    }
+        switch (key) {
+            case 1: USOLO_K(1)
+            case 2: USOLO_K(2)
+            case 3: USOLO_K(3)
+            default: return nullptr;
+        }
+#undef USOLO_K
+#undef USOLO
+    }
+    switch (key) {
+            case 1: return sym ? (ReplayKernel)magus_replay_usolo_kernel<MagusTicker<1, false>, kTC, kNStage, true>
+                               : (ReplayKernel)magus_replay_usolo_kernel<MagusTicker<1, false>, kTC, kNStage, false>;
+            case 2: return sym ? (ReplayKernel)magus_replay_usolo_kernel<MagusTicker<2, false>, kTC, kNStage, true>
+                               : (ReplayKernel)magus_replay_usolo_kernel<MagusTicker<2, false>, kTC, kNStage, false>;
+            case 3: return sym ? (ReplayKernel)magus_replay_usolo_kernel<MagusTicker<3, false>, kTC, kNStage, true>
+                               : (ReplayKernel)magus_replay_usolo_kernel<MagusTicker<3, false>, kTC, kNStage, false>;
+            default: return nullptr;
+        }
+    }
 #define SOLO_K(KK)                                                                                               \
     (v == 0   ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 0>                    \
      : v == 2 ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 2>                    \
@@ -685,6 +721,9 @@ static void choose_geometry(magus_replay_t* h, int n_sm, int forced_segments) {
     p.n_seg = std::max(1, S);
     p.seg_len = L;
     p.warmup = p.n_seg > 1 ? W : 0;
+    // the unified-stage solo kernel's own (shorter) warm-up: a multiple of 8 ticks covering k + C - 1
+    p.solo_warm = std::min(std::max(((kmax + cmax - 1 + 7) / 8) * 8, (env_int("MAGUS_SOLO_WARM", 16) + 7) / 8 * 8),
+                           std::max(p.warmup, 8));
     p.n_blocks = (d.n_samples + 31) / 32;
     // Spread small launches over every SM: while the launch groups together have fewer CTAs than
     // SMs, halve the widest CTA (policy warps first, then tile groups).
@@ -709,8 +748,15 @@ static void choose_geometry(magus_replay_t* h, int n_sm, int forced_segments) {
         g.n_ctas = p.n_seg * g.n_tblocks * g.n_pblocks;
         // one policy warp per tile group: one-warp CTAs with CTA-uniform pipeline state (replay_solo.cuh)
         bool sym = true;   // every lane policy of the group has d*_dec == -d*_inc (the |d| tune-flag test)
-        for (int q = g.q_base; q < g.q_base + g.nq; ++q) sym = sym && h->lane[q].ddec == -h->lane[q].dinc;
-        ReplayKernel sk = solo_kernel_for(g.key, sym);
+        // the integer fp32 -> fp64 sample conversion changes no decision when both thresholds are >= 2^-60 in
+        // magnitude and B_lo is a normal fp32
+        bool bits_ok = h->B_lo >= 0x1p-126f;
+        for (int q = g.q_base; q < g.q_base + g.nq; ++q) {
+            const DevPolicy& lp = h->lane[q];
+            sym = sym && lp.ddec == -lp.dinc;
+            bits_ok = bits_ok && lp.dinc >= 0x1p-60 && lp.ddec <= -0x1p-60;
+        }
+        ReplayKernel sk = solo_kernel_for(g.key, sym, bits_ok);
         g.solo = sk && g.npw == 1 && kTC == 8 && env_int("MAGUS_SOLO", 1) != 0;
         if (g.solo) {
             g.kernel = sk;

@@ -17,6 +17,8 @@
 
 namespace magus {
 
+#define K_OF(T) T::kRingK
+
 #ifndef MAGUS_SOLO_UNROLL
 #define MAGUS_SOLO_UNROLL 1
 #endif
@@ -359,6 +361,241 @@ __global__ void __launch_bounds__(32, kSoloCtasPerSm)
         if (counting) {
             const uint2 bkey = p.dkeys[bt0 >> 5];
             const int n = min(32, G.seg_end - bt0);
+            if (n == 32 && p.words == nullptr) {   // the common case: a whole block, no word dump
+#pragma unroll
+                for (int c = 0; c < kChains; ++c)
+                    fold_full_block(ss[c], wcmd[c], (uint32_t)st[c].evh, fstart[c], bkey, nullptr);
+            } else {
+                const int64_t bi = bt0 >> 5;
+                uint32_t* wbase = p.words ? p.words + ((int64_t)q * p.n_traces * p.n_blocks + bi) * 2 : nullptr;
+#pragma unroll
+                for (int c = 0; c < kChains; ++c) {
+                    uint32_t* wout =
+                        (wbase && j0 + c < p.n_traces) ? wbase + (int64_t)(j0 + c) * p.n_blocks * 2 : nullptr;
+                    if (n == 32) fold_full_block(ss[c], wcmd[c], (uint32_t)st[c].evh, fstart[c], bkey, wout);
+                    else fold_block(ss[c], wcmd[c], (uint32_t)st[c].evh, fstart[c], n, bi, wout);
+                }
+            }
+        }
+    }
+
+#pragma unroll
+    for (int c = 0; c < kChains; ++c)
+        if (j0 + c < p.n_traces) T::save(st[c], p, pol, 1, q, seg, j0 + c);
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) {
+        const int j = j0 + c;
+        if (j >= p.n_traces) continue;
+        add_to_chain(p, q, j, ss[c].nhi, ss[c].nthr + (uint32_t)nthrf[c], ss[c].trans, ss[c].ev,
+                     ss[c].lock + (uint32_t)lockf[c], ss[c].sexc, ss[c].digest());
+    }
+    if (j0 < p.n_traces) atomicMax(p.c_vmax + chain_idx(p, q, j0), vmax);   // lane-level validation maximum
+}
+
+// ===================================================================================================================
+// The unified-stage solo kernel: one generated stage block (MAGUS_USTAGE{S}_K<K>) for the
+// warm-up and the steady state.  Alg. 1 is gated by a NaN-filled ring at the start of the chain's run, Alg. 2 by
+// warp-uniform per-tick masks (zero until C flags have been logged), so the warm-up needs no per-tick path and can
+// be short: speculative segments start p.solo_warm ticks (a multiple of 8, >= k + C - 1) before their first tick
+// instead of a whole 32-tick block.  Only the ragged last stage of a trace uses the generic per-tick tick.
+// VAR bits: 1 = symmetric thresholds (the |d| tune-flag test), 2 = Alg. 2 by the scaled incremental count (else
+// by popcount), 4 = the fp32 -> fp64 sample conversion by integer ops (else F2F).  g[]: the per-tick Alg. 2 gates.
+#define USTAGE_NAME(S, I, B, KK) MAGUS_USTAGE##S##I##B##_K##KK
+template <int K, int VAR>
+__device__ __forceinline__ void solo_ustage(MagusState<K, false>* s, float* lock, float* nthr, uint32_t* wcmd,
+                                           SegStats* ss, uint32_t& vmax, uint32_t tile, const SoloConst& sc,
+                                           const DevPolicy& pol, const uint32_t* g, uint32_t smin, uint32_t bitc,
+                                           uint32_t mone) {
+    uint32_t e0 = s[0].evh, e1 = s[1].evh, e2 = s[2].evh, e3 = s[3].evh;
+#define U_F s[0].f, s[1].f, s[2].f, s[3].f
+#define U_R1 s[0].ring.v[0], s[1].ring.v[0], s[2].ring.v[0], s[3].ring.v[0]
+#define U_R2                                                                                                  \
+    s[0].ring.v[0], s[0].ring.v[1], s[1].ring.v[0], s[1].ring.v[1], s[2].ring.v[0], s[2].ring.v[1], s[3].ring.v[0], \
+        s[3].ring.v[1]
+#define U_R3                                                                                                  \
+    s[0].ring.v[0], s[0].ring.v[1], s[0].ring.v[2], s[1].ring.v[0], s[1].ring.v[1], s[1].ring.v[2], s[2].ring.v[0], \
+        s[2].ring.v[1], s[2].ring.v[2], s[3].ring.v[0], s[3].ring.v[1], s[3].ring.v[2]
+#define U_CNT s[0].cnt, s[1].cnt, s[2].cnt, s[3].cnt,
+#define U_MID                                                                                                 \
+    ss[0].sexc, ss[1].sexc, ss[2].sexc, ss[3].sexc, lock[0], lock[1], lock[2], lock[3], nthr[0], nthr[1], nthr[2], \
+        nthr[3], wcmd[0], wcmd[1], wcmd[2], wcmd[3], vmax, tile, sc.B_lo, sc.Blo_d, pol.dinc, pol.ddec, g[0], g[1],  \
+        g[2], g[3], g[4], g[5], g[6], g[7]
+#define U_RING(KK) U_R##KK
+#define U_CALLP(S, B, KK) USTAGE_NAME(S, , B, KK)(U_F, U_RING(KK), e0, e1, e2, e3, U_MID, smin, pol.one)
+#define U_CALLI(S, B, KK) USTAGE_NAME(S, I, B, KK)(U_F, U_RING(KK), e0, e1, e2, e3, U_CNT U_MID, bitc, mone, pol.one)
+#define U_BY_K(CALL, S, B)                                                                                     \
+    if constexpr (K == 1) CALL(S, B, 1);                                                                       \
+    else if constexpr (K == 2) CALL(S, B, 2);                                                                  \
+    else CALL(S, B, 3);
+    constexpr bool kSym = VAR & 1, kInc = VAR & 2, kBits = VAR & 4;
+    if constexpr (kSym && kInc && kBits) { U_BY_K(U_CALLI, S, B) }
+    else if constexpr (kSym && kInc) { U_BY_K(U_CALLI, S, ) }
+    else if constexpr (kSym && kBits) { U_BY_K(U_CALLP, S, B) }
+    else if constexpr (kSym) { U_BY_K(U_CALLP, S, ) }
+    else if constexpr (kInc && kBits) { U_BY_K(U_CALLI, , B) }
+    else if constexpr (kInc) { U_BY_K(U_CALLI, , ) }
+    else if constexpr (kBits) { U_BY_K(U_CALLP, , B) }
+    else { U_BY_K(U_CALLP, , ) }
+#undef U_BY_K
+#undef U_CALLI
+#undef U_CALLP
+#undef U_RING
+#undef U_MID
+#undef U_CNT
+#undef U_F
+#undef U_R1
+#undef U_R2
+#undef U_R3
+    s[0].evh = e0;
+    s[1].evh = e1;
+    s[2].evh = e2;
+    s[3].evh = e3;
+}
+
+template <class T, int TC, int NSTAGE, int VAR>
+__global__ void __launch_bounds__(32, kSoloCtasPerSm)
+    magus_replay_usolo_kernel(const __grid_constant__ CUtensorMap tmap, const ReplayParams p) {
+    static_assert(T::kHasStage8 && TC == 8, "solo kernel: whole-stage PTX block of 8 ticks");
+    using State = typename T::State;
+    using SM = SoloSmem<TC, NSTAGE>;
+    constexpr uint32_t kTileBytes = SM::kTileBytes;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int lane = threadIdx.x;
+
+    int b = blockIdx.x;   // -> (lane policy, tile group, segment), policies fastest
+    const int qi = b % p.nq;
+    b /= p.nq;
+    const int tgroup = b % p.n_groups;
+    const int seg = b / p.n_groups;
+    const int q = p.q_base + qi;
+
+    const uint32_t tile0 = ptx::smem_u32(smem);
+    const uint32_t bar0 = tile0 + NSTAGE * kTileBytes;
+    if (lane == 0) {
+        ptx::prefetch_tmap(&tmap);
+        for (int i = 0; i < NSTAGE; ++i)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8 * i) : "memory");
+        ptx::fence_mbar_init();
+    }
+    __syncwarp();
+
+    const int seg_start = seg_begin(p, seg), seg_end = seg_finish(p, seg);
+    const int tau_w = seg == 0 ? 0 : seg_start - p.solo_warm;
+    const int n_stages = (seg_end - tau_w + TC - 1) / TC;
+    const int x = tgroup * kTracesPerWarp;
+    const uint64_t cpol = ptx::policy_evict_first();
+    for (int i = 0; i < NSTAGE && i < n_stages; ++i)
+        solo_issue<TC>(tile0 + i * kTileBytes, &tmap, bar0 + 8 * i, x, tau_w + i * TC, cpol);
+    ptx::pdl_wait();   // first_low and the scratch words come from the pre-pass (launched just before)
+
+    const DevPolicy pol = p.pol[q];
+    const int j0 = x + lane * kChains;
+    const float B_lo = p.B_lo, B_hi = p.B_hi;
+    SoloConst sc;
+    sc.Blo_d = (double)B_lo;
+    sc.B_lo = B_lo;
+    const int k = pol.k, C = pol.C, kc1 = k + C - 1;
+    const uint32_t smin = (uint32_t)pol.s_min, bitc = 1u << (pol.C - 1), mone = 0xFFFFFFFFu * pol.one;
+    // Alg. 2 gate of a tick once the log is full / before (A8): the window mask / 0 (popcount), the scaled lock
+    // threshold / never (incremental count)
+    const uint32_t g_full = (VAR & 2) ? pol.smin_sc : (uint32_t)pol.logmask, g_not = (VAR & 2) ? 0xFFFFFFFFu : 0u;
+    const uint32_t lane_off = (uint32_t)lane * 16u;
+
+    State st[kChains];
+    SegStats ss[kChains];
+    uint32_t wcmd[kChains], fstart[kChains];
+    float lockf[kChains], nthrf[kChains];   // counts as exact fp32 integers (segment length <= 2^24)
+    uint32_t vmax = 0;
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) {
+        T::init(st[c], pol, seg == 0);
+#pragma unroll
+        for (int r = 0; r < T::kRingK; ++r) st[c].ring.v[r] = __longlong_as_double(0x7FF8000000000000LL);   // A7 gate
+        ss[c].zero();
+        wcmd[c] = 0;
+        lockf[c] = nthrf[c] = 0.f;
+    }
+    // per-tick Alg. 2 gates of the next stage (A8): g_full once k + C - 1 ticks of the run have passed
+    uint32_t m[TC];
+    auto set_masks = [&](int r0) {
+#pragma unroll
+        for (int t = 0; t < TC; ++t) m[t] = (r0 + t >= kc1) ? g_full : g_not;
+    };
+    set_masks(0);
+
+    if (seg > 0) {
+        // speculative level at the warm-up start: f_max iff the trace is above B_lo now and
+        // was at or below B_lo before; lock-sticky policies (k >= s_min) keep f_max after any low/high transition
+        mbar_wait_loop(bar0, 0);
+        float4 d0;
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(d0.x), "=f"(d0.y), "=f"(d0.z), "=f"(d0.w)
+                     : "r"(tile0 + lane_off)
+                     : "memory");
+        const float dd[4] = {d0.x, d0.y, d0.z, d0.w};
+#pragma unroll
+        for (int c = 0; c < kChains; ++c) {
+            const int j = j0 + c;
+            const int fl = j < p.n_traces ? __ldg(p.first_low + j) : 0x7FFFFFFF;
+            const int fh = j < p.n_traces ? __ldg(p.first_low + p.n_traces + j) : 0x7FFFFFFF;
+            const bool hi = (dd[c] > B_lo && fl < tau_w) || (pol.sticky && fl < tau_w && fh < tau_w);
+            T::set_level(st[c], hi ? 1u : 0u);
+        }
+    }
+
+    // One loop over the run's stages (one call site of the stage block: the warm-up stages, then the segment's
+    // own ticks in 32-tick blocks of four stages).  All branch conditions are CTA-uniform.
+    int slot = 0;        // i % NSTAGE
+    uint32_t phase = 0;  // (i / NSTAGE) & 1
+#pragma unroll 1
+    for (int i = 0; i < n_stages; ++i) {
+        const int t0 = tau_w + i * TC;
+        if (t0 >= seg_start && ((t0 - seg_start) & 31) == 0) {
+            if (t0 == seg_start && seg > 0) {   // the segment's own ticks start: record the entry state
+#pragma unroll
+                for (int c = 0; c < kChains; ++c) {
+                    if (j0 + c < p.n_traces) T::save(st[c], p, pol, 0, q, seg, j0 + c);
+                    ss[c].zero();
+                    lockf[c] = nthrf[c] = 0.f;
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < kChains; ++c) fstart[c] = T::level(st[c]);
+        }
+        const uint32_t tile = tile0 + slot * kTileBytes;
+        mbar_wait_loop(bar0 + 8 * slot, phase);
+        if (t0 + TC <= seg_end) {
+            solo_ustage<K_OF(T), VAR>(st, lockf, nthrf, wcmd, ss, vmax, tile + lane_off, sc, pol, m, smin, bitc, mone);
+        } else {   // the ragged last stage of a trace: per tick
+            const float4* rows = reinterpret_cast<const float4*>(smem + slot * kTileBytes) + lane;
+#pragma unroll 1
+            for (int tt = 0; tt < TC; ++tt) {
+                const int t = t0 + tt;
+                if (t >= seg_end) break;
+                const float4 d4 = rows[tt * (kTracesPerWarp / 4)];
+                const float d[4] = {d4.x, d4.y, d4.z, d4.w};
+                const bool ready = (t - tau_w) >= k;
+                const bool lfull = (t - tau_w) >= kc1;
+#pragma unroll
+                for (int c = 0; c < kChains; ++c) {
+                    const TickOut o = T::template tick<true>(st[c], d[c], pol, B_lo, B_hi, ready, lfull);
+                    wcmd[c] = (wcmd[c] << 1) | o.cmd;
+                    acc_tick(ss[c], vmax, o, d[c], B_lo);
+                }
+            }
+        }
+        __syncwarp();   // every lane's tile reads are complete before the slot is refilled
+        if (i + NSTAGE < n_stages) solo_issue<TC>(tile, &tmap, bar0 + 8 * slot, x, tau_w + (i + NSTAGE) * TC, cpol);
+        if (++slot == NSTAGE) {
+            slot = 0;
+            phase ^= 1u;
+        }
+        if ((t0 - tau_w) < kc1) set_masks(t0 + TC - tau_w);   // masks settle at maskc after the gated stages
+        const int t1 = t0 + TC;
+        if (t0 >= seg_start && (((t1 - seg_start) & 31) == 0 || t1 >= seg_end)) {   // a 32-tick block ends
+            const int bt0 = seg_start + ((t0 - seg_start) & ~31);
+            const uint2 bkey = p.dkeys[bt0 >> 5];
+            const int n = min(32, seg_end - bt0);
             if (n == 32 && p.words == nullptr) {   // the common case: a whole block, no word dump
 #pragma unroll
                 for (int c = 0; c < kChains; ++c)

@@ -339,6 +339,109 @@ def build_stage_p(K, TC=8, popc=True, group=4, sym=False):
     return out
 
 
+
+def build_stage_u(K, TC=8, sym=False, popc=True, bits=False):
+    """MAGUS_USTAGE{S}{I}{B}_K<K>: the solo kernel's one stage block for warm-up AND steady state (TC ticks x 4
+    chains, tile loads included), with the 3-DSETP level logic (the new level is lock | +1 | (level & !-1)).
+    - Alg. 1 gating (A7) by data: a chain (re)starts with its ring of A values filled with NaN, so the first k
+      derivatives are NaN and every comparison on them is false (no tune flag; the level is kept: the 'not -1'
+      test is the unordered setp.geu) -- the paper's "not ready" without a per-tick predicate;
+    - Alg. 2 gating (A8) by per-tick warp-uniform operands g0..g7: popc=True (Alg. 2 = popc(log & g_t) >= s_min)
+      g_t = the low-C-bits mask once C flags have been logged (tick >= k + C - 1 of the chain's run), else 0;
+      popc=False (I: the scaled incremental window count, no XU popcount) g_t = s_min << (C-1) once full, else
+      0xFFFFFFFF.  Not-ready ticks shift zeros into the flag register; they have left the window when it is full.
+    - sym (S): the tune flag is |d| > d*_inc (policies with d*_dec == -d*_inc).
+    - bits (B): the fp32 -> fp64 conversion of a sample by integer ops (hi = (x >> 3) + 0x38000000, lo = x << 29)
+      instead of F2F on the XU pipe.  Exact for normal samples; a zero or subnormal sample becomes 2^-127 + x/2,
+      which changes no decision when |d*_inc|, |d*_dec| >= 2^-60 and B_lo is normal: the
+      host uses this variant only then."""
+    C = 4
+    names = [(f"f{c}", "+r") for c in range(C)] + \
+            [(f"r{c}_{i}", "+d") for c in range(C) for i in range(K)] + \
+            [(f"evh{c}", "+r") for c in range(C)] + \
+            ([] if popc else [(f"cnt{c}", "+r") for c in range(C)]) + \
+            [(f"exc{c}", "+d") for c in range(C)] + [(f"lock{c}", "+f") for c in range(C)] + \
+            [(f"nthr{c}", "+f") for c in range(C)] + [(f"wcmd{c}", "+r") for c in range(C)] + [("vmax", "+r")]
+    inames = [("tile", "r"), ("Blo", "f"), ("Blod", "d"), ("dinc", "d"), ("ddec", "d")] + \
+             [(f"g{tt}", "r") for tt in range(TC)] + ([("smin", "r")] if popc else [("bitc", "r"), ("mone", "r")]) + \
+             [("one", "r")]
+    idx = {n: f"%{i}" for i, (n, _) in enumerate(names + inames)}
+    R = idx.__getitem__
+    body = ["{", ".reg .pred phi<4>, pthr<4>, pinc<4>, pev<4>, phf<4>, pk<4>;",
+            f".reg .b32 D<{TC * C}>;", f".reg .f64 dd<4>, dv<4>, da<4>, dx<4>, ad<{TC * C}>;",
+            ".reg .b32 wv<4>, pc<4>, tb<4>, xh<4>, xl<4>;"]
+    for c in range(C):
+        body.append(f"setp.ne.u32 phi{c}, {R(f'f{c}')}, 0;")
+    for tt in range(TC):
+        body.append(f"ld.shared.v4.f32 {{D{tt * C}, D{tt * C + 1}, D{tt * C + 2}, D{tt * C + 3}}}, [{R('tile')}+{tt * 512}];")
+        conv = ([
+            "shr.u32 xh{c}, {D}, 3;",
+            "add.u32 xh{c}, xh{c}, 0x38000000;",
+            "shl.b32 xl{c}, {D}, 29;",
+            "mov.b64 dd{c}, {{xl{c}, xh{c}}};",
+        ] if bits else ["cvt.f64.f32 dd{c}, {D};"])
+        per_chain = conv + [
+            "setp.gt.and.f32 pthr{c}, {D}, {Blo}, !phi{c};",             # throttled: f_min and D > B_lo (A14)
+            "selp.f64 {ad}, {Blod}, dd{c}, pthr{c};",                     # A = min(D, B[f]) as fp64 (exact)
+            "sub.f64 dv{c}, {ad}, {old};",                                # Alg. 1 numerator A_t - A_{t-k} (P:207)
+        ] + ([
+            "abs.f64 da{c}, dv{c};",
+            "setp.gt.f64 pev{c}, da{c}, {dinc};",                         # tune flag iff |d| > d*_inc (P:213, P:243)
+            "setp.geu.and.f64 pk{c}, dv{c}, {ddec}, phi{c};",             # level kept: f_max and not -1
+            "setp.gt.or.f64 pk{c}, dv{c}, {dinc}, pk{c};",                # ... or +1 (P:209)
+        ] if sym else [
+            "setp.gt.f64 pinc{c}, dv{c}, {dinc};",                        # +1 (P:209)
+            "setp.lt.or.f64 pev{c}, dv{c}, {ddec}, pinc{c};",             # tune flag: +1 or -1 (P:213, P:243)
+            "setp.geu.and.f64 pk{c}, dv{c}, {ddec}, phi{c};",             # level kept: f_max and not -1
+            "or.pred pk{c}, pk{c}, pinc{c};",
+        ]) + ([
+            "shl.b32 {evh}, {evh}, 1;",
+            "@pev{c} mad.lo.u32 {evh}, {one}, {one}, {evh};",
+            "and.b32 wv{c}, {evh}, {g};",                                 # the last C flags once the log is full
+            "popc.b32 pc{c}, wv{c};",
+            "setp.ge.u32 phf{c}, pc{c}, {smin};",                         # Alg. 2 (P:229-230)
+        ] if popc else [
+            "and.b32 tb{c}, {evh}, {bitc};",                              # the flag leaving the C-window (scaled)
+            "shl.b32 {evh}, {evh}, 1;",
+            "@pev{c} mad.lo.u32 {evh}, {one}, {one}, {evh};",
+            "mad.lo.u32 {cnt}, tb{c}, {mone}, {cnt};",                    # window count: - leaving + entering
+            "@pev{c} mad.lo.u32 {cnt}, {bitc}, {one}, {cnt};",
+            "setp.ge.u32 phf{c}, {cnt}, {g};",                            # Alg. 2 (P:230), once the log is full
+        ]) + [
+            "or.pred phi{c}, pk{c}, phf{c};",                             # lock || +1 || (f_max && !-1)
+            "shl.b32 {wcmd}, {wcmd}, 1;",
+            "@phi{c} mad.lo.u32 {wcmd}, {one}, {one}, {wcmd};",
+            "sub.f64 dx{c}, dd{c}, {ad};",                                # throttling excess D - A (0 unless thr)
+            "add.f64 {exc}, {exc}, dx{c};",
+            "@phf{c} add.f32 {lock}, {lock}, 0f3F800000;",
+            "@pthr{c} add.f32 {nthr}, {nthr}, 0f3F800000;",
+            "max.u32 {vmax}, {vmax}, {D};",                               # validation (A17)
+        ]
+        for tmpl in per_chain:
+            for c in range(C):
+                t = tt * C + c
+                old = f"ad{(tt - K) * C + c}" if tt >= K else R(f"r{c}_{K - 1 - tt}")
+                body.append(tmpl.format(c=c, D=f"D{t}", ad=f"ad{t}", old=old, Blo=R("Blo"), Blod=R("Blod"),
+                                        dinc=R("dinc"), ddec=R("ddec"), evh=R(f"evh{c}"), one=R("one"),
+                                        g=R(f"g{tt}"), smin=R("smin") if popc else None,
+                                        bitc=None if popc else R("bitc"), mone=None if popc else R("mone"),
+                                        cnt=None if popc else R(f"cnt{c}"), wcmd=R(f"wcmd{c}"), exc=R(f"exc{c}"),
+                                        lock=R(f"lock{c}"), nthr=R(f"nthr{c}"), vmax=R("vmax")))
+    for c in range(C):
+        body.append(f"selp.u32 {R(f'f{c}')}, 1, 0, phi{c};")
+        for i in range(K):   # ring newest first: r_i = A_{t0 + TC - 1 - i}
+            body.append(f"mov.f64 {R(f'r{c}_{i}')}, ad{(TC - 1 - i) * C + c};")
+    body.append("}")
+    params = ", ".join(n for n, _ in names + inames)
+    name = f"MAGUS_USTAGE{'S' if sym else ''}{'' if popc else 'I'}{'B' if bits else ''}_K{K}"
+    out = [f"#define {name}(...) {name}_(__VA_ARGS__)", f"#define {name}_({params}) \\", "    asm volatile( \\"]
+    out += [f'        "{l}\\n\\t" \\' for l in body]
+    out.append("        : " + ", ".join(f'"{c}"({n})' for n, c in names) + " \\")
+    out.append("        : " + ", ".join(f'"{c}"({n})' for n, c in inames) + " \\")
+    out.append('        : "memory")')
+    return out
+
+
 out = ["// GENERATED by scripts/gen_tick4.py -- do not edit.  One MAGUS tick for the 4 chains of a lane, the",
        "// four chains' instructions interleaved (DESIGN.md section 7); semantics = magus_tick<K, false, SLOW>.",
        "// cnt is the window count scaled by 2^(C-1).",
@@ -348,6 +451,10 @@ for K in (1, 2, 3):
     out += [""] + build_stage(K)
     out += [""] + build_stage_f(K)
     out += [""] + build_stage_f(K, thr64=False)
+    for sym in (False, True):
+        for popc in (True, False):
+            for bits in (False, True):
+                out += [""] + build_stage_u(K, sym=sym, popc=popc, bits=bits)
     for g in (4, 2, 1):
         for sym in (False, True):
             out += [""] + build_stage_p(K, popc=True, group=g, sym=sym)

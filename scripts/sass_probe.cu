@@ -8,3 +8,7 @@
 #endif
 template __global__ void magus::magus_replay_solo_kernel<magus::MagusTicker<PROBE_K, false>, 8, 3, PROBE_V>(
     const __grid_constant__ CUtensorMap, const magus::ReplayParams);
+#ifdef PROBE_U
+template __global__ void magus::magus_replay_usolo_kernel<magus::MagusTicker<PROBE_K, false>, 8, 3, PROBE_U>(
+    const __grid_constant__ CUtensorMap, const magus::ReplayParams);
+#endif
