@@ -194,16 +194,6 @@ ReplayKernel solo_kernel_for(int key, bool sym, bool bits_ok) {
 #undef USOLO_K
 #undef USOLO
     }
-    switch (key) {
-            case 1: return sym ? (ReplayKernel)magus_replay_usolo_kernel<MagusTicker<1, false>, kTC, kNStage, true>
-                               : (ReplayKernel)magus_replay_usolo_kernel<MagusTicker<1, false>, kTC, kNStage, false>;
-            case 2: return sym ? (ReplayKernel)magus_replay_usolo_kernel<MagusTicker<2, false>, kTC, kNStage, true>
-                               : (ReplayKernel)magus_replay_usolo_kernel<MagusTicker<2, false>, kTC, kNStage, false>;
-            case 3: return sym ? (ReplayKernel)magus_replay_usolo_kernel<MagusTicker<3, false>, kTC, kNStage, true>
-                               : (ReplayKernel)magus_replay_usolo_kernel<MagusTicker<3, false>, kTC, kNStage, false>;
-            default: return nullptr;
-        }
-    }
 #define SOLO_K(KK)                                                                                               \
     (v == 0   ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 0>                    \
      : v == 2 ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 2>                    \
