@@ -196,16 +196,18 @@ magus_status magus_gen_traces(const magus_gen_desc* desc, float* d_trace, float*
 
 /* NEXT-3 front end ("obtaining memory throughput data"; A31): recorded
  * cumulative byte counters -> the replay's trace layout.  d_counts: device [n_rows][stride] uint64
- * (time-major, trace-minor); d_times: device [n_rows] seconds, or NULL for a uniform period_s.  Writes
- * d_trace[n_rows - 1][stride] fp32 GB/s (padding columns 0): interval i = rows i -> i + 1 =
- * ((double)(c[i+1] - c[i]) / dt) / 1e9, rounded once to fp32.  An interval whose counter decreased
- * (wrap / reset) is discarded and repeats the last valid interval's throughput of its trace (0 before
- * any).  d_report: device, 2 x uint64, zeroed by the call: [0] = discarded intervals, [1] = intervals
- * whose timestamp did not increase (the caller must treat the trace as invalid).  Stream-ordered;
- * MAGUS_ERR_INVALID_ARG on NULL pointers or bad sizes, MAGUS_ERR_CUDA without a device. */
+ * (time-major, trace-minor); d_times: device [n_rows] seconds, or NULL for a uniform period_s.  Interval
+ * i = rows i -> i + 1 has throughput ((double)(c[i+1] - c[i]) / dt) / 1e9 GB/s, rounded once to fp32.  An
+ * interval whose counter decreased (wrap / reset) is discarded with no governor round: trace j's
+ * rounds are its valid intervals in time order, written to rows [0, n_valid[j]) of its column of
+ * d_trace[n_rows - 1][stride]; the rows after them (and padding columns) are 0.0 and are not rounds -- replay
+ * the first min_j n_valid[j] rows, or each trace with its own count.  d_n_valid: device [n_traces] int64, or
+ * NULL.  d_report: device, 2 x uint64, zeroed by the call: [0] = discarded intervals, [1] = intervals whose
+ * timestamp did not increase (the caller must treat the trace as invalid).  Stream-ordered (stream-ordered
+ * scratch allocation); MAGUS_ERR_INVALID_ARG on NULL pointers or bad sizes, MAGUS_ERR_CUDA without a device. */
 magus_status magus_counters_to_trace(const uint64_t* d_counts, const double* d_times, int32_t n_traces,
                                      int64_t n_rows, int64_t stride, double period_s, float* d_trace,
-                                     unsigned long long* d_report, void* cuda_stream);
+                                     int64_t* d_n_valid, unsigned long long* d_report, void* cuda_stream);
 
 /* Validates desc (every invariant of section "magus_policy"/"magus_model"; A17), derives the
  * exact-equivalent thresholds, allocates device scratch, creates the NCCL communicator when

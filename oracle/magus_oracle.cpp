@@ -457,37 +457,36 @@ int oracle_replay_wallclock(const float* D, int64_t n, int64_t stride, float w, 
 }
 
 /* ===================== recorded byte counters -> throughput (NEXT-3) =====================
- * "obtaining memory throughput data": a monotone cumulative byte counter read every round gives the
- * round's throughput as the difference quotient (count_now - count_prev) / (t_now - t_prev).
- * counts: [n_rows][stride] uint64 (time-major, trace-minor, like the traces); times: [n_rows] seconds, or
- * NULL for a uniform `period`.  out: [n_rows - 1][stride] fp32 GB/s, interval i = rows i -> i + 1, computed
- * as ((double)(c1 - c0) / dt) / 1e9 and rounded once to fp32.  A counter that decreased (wrap / reset,
- * the sample is discarded and the baseline re-armed) gives no new measurement: in the
- * one-sample-per-round replay that round repeats the last valid interval's throughput, 0 before any [A31].
- * Returns the number of discarded intervals, or -1 if a timestamp does not increase. */
+ * read_throughput: throughput = (count_now - count_prev) / (t_now - t_prev), here in GB/s
+ * (1 GB/s = 1e9 B/s [A3]): ((double)(c1 - c0) / dt) / 1e9, rounded once to fp32.  A counter that decreased
+ * (wrap / reset) is an error whose sample is discarded and whose baseline is re-armed; "counter
+ * reset to 0 -> sample discarded, no governor round": the interval yields no round at all [A31].  So trace j's
+ * rounds are its valid intervals in time order: out[0 .. n_valid[j]) of its column, the rest of the column
+ * 0.0 (padding, not rounds).  A non-increasing timestamp is an error (returns -1).  Returns the number of
+ * discarded intervals. */
 int64_t oracle_counters_to_throughput(const uint64_t* counts, const double* times, int64_t n_rows, int32_t n_traces,
-                                      int64_t stride, double period, float* out) {
+                                      int64_t stride, double period, float* out, int64_t* n_valid) {
     for (int64_t i = 0; i + 1 < n_rows; ++i) {
         double dt = times ? times[i + 1] - times[i] : period;
         if (!(dt > 0.0)) return -1;
     }
-    int64_t resets = 0;
+    int64_t discarded = 0;
     for (int32_t j = 0; j < n_traces; ++j) {
-        float last = 0.0f;                                   /* last valid interval's throughput */
+        int64_t k = 0;                                       /* rounds of trace j so far */
         for (int64_t i = 0; i + 1 < n_rows; ++i) {
             uint64_t c0 = counts[i * stride + j], c1 = counts[(i + 1) * stride + j];
-            if (c1 < c0) {                                   /* reset: discarded, the round repeats `last` */
-                ++resets;
-                out[i * stride + j] = last;
+            if (c1 < c0) {                                   /* wrap / reset: no round */
+                ++discarded;
                 continue;
             }
             double dt = times ? times[i + 1] - times[i] : period;
-            float v = (float)(((double)(c1 - c0) / dt) / 1e9);
-            out[i * stride + j] = v;
-            last = v;
+            out[k * stride + j] = (float)(((double)(c1 - c0) / dt) / 1e9);
+            ++k;
         }
+        n_valid[j] = k;
+        for (int64_t i = k; i + 1 < n_rows; ++i) out[i * stride + j] = 0.0f;   /* padding */
     }
-    return resets;
+    return discarded;
 }
 
 /* ========================= active savings ========================

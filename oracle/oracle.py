@@ -86,7 +86,7 @@ def lib():
                                               C.c_int64]
         L.oracle_counters_to_throughput.restype = C.c_int64
         L.oracle_counters_to_throughput.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int64,
-                                                    C.c_double, C.c_void_p]
+                                                    C.c_double, C.c_void_p, C.c_void_p]
         L.oracle_replay.restype = C.c_int
         L.oracle_replay.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_float, C.POINTER(OPolicy),
                                     C.POINTER(OModel), C.c_void_p, C.c_void_p, C.c_int64]
@@ -199,20 +199,23 @@ def digest(cmd_hi, events) -> int:
 
 def counters_to_throughput(counts, period: float = 0.1, times=None, n_traces: int | None = None):
     """Recorded cumulative byte counters [n_rows][stride] (uint64) -> throughput [n_rows-1][stride] fp32 GB/s
-    (DESIGN A31).  Returns (throughput, number of discarded intervals); ValueError when a
-    timestamp does not increase."""
+    (DESIGN A31): trace j's rounds are its valid intervals in time order, at rows
+    [0, n_valid[j]) of its column; a wrap / reset interval yields no round; the rest of the column is 0.0.
+    Returns (throughput, n_valid [n_traces] int64, number of discarded intervals); ValueError when a timestamp
+    does not increase."""
     c = np.ascontiguousarray(counts, dtype=np.uint64)
     if c.ndim == 1:
         c = c[:, None]
     n_rows, stride = c.shape
     n_traces = stride if n_traces is None else n_traces
     out = np.zeros((max(0, n_rows - 1), stride), dtype=np.float32)
+    nv = np.zeros(max(1, n_traces), dtype=np.int64)
     t = None if times is None else np.ascontiguousarray(times, dtype=np.float64)
     r = lib().oracle_counters_to_throughput(c.ctypes.data, None if t is None else t.ctypes.data, n_rows, n_traces,
-                                            stride, period, out.ctypes.data)
+                                            stride, period, out.ctypes.data, nv.ctypes.data)
     if r < 0:
         raise ValueError("timestamps must increase")
-    return out, int(r)
+    return out, nv[:n_traces], int(r)
 
 
 def active_saving(p: float, p_base: float, p_idle: float) -> float:

@@ -7,6 +7,8 @@
 // yields the same bytes.  Every fp32 operation is an explicit round-to-nearest intrinsic (no FMA
 // contraction), so the device reproduces the IEEE host result exactly.
 #include <cuda_runtime.h>
+
+#include <algorithm>
 #include <cstdint>
 #include "../../include/magus_replay.h"
 
@@ -175,7 +177,9 @@ extern "C" magus_status magus_gen_traces(const magus_gen_desc* desc, float* d_tr
     if (g.n_samples == 0 || g.trace_stride == 0) return MAGUS_OK;
     float bw = (float)g.bw_max_gbps;
     if ((double)bw > g.bw_max_gbps) bw = nextafterf(bw, 0.0f);
-    const int64_t chunk = g.class_mix == 2 ? g.n_samples : 1024;
+    // ticks per thread: 1024, more when grid.y would exceed 65535 chunks (the bytes do not depend on the chunking:
+    // counter-based per (trace, tick); the adversarial class walks its trace in one sequential pass)
+    const int64_t chunk = g.class_mix == 2 ? g.n_samples : std::max<int64_t>(1024, (g.n_samples + 65534) / 65535);
     const int64_t n_chunks = (g.n_samples + chunk - 1) / chunk;
     dim3 block(128), grid((unsigned)((g.trace_stride + 127) / 128), (unsigned)n_chunks);
     magus::gen::gen_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(g, bw, chunk, d_trace, d_w);

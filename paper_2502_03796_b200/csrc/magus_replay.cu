@@ -1330,7 +1330,7 @@ extern "C" magus_status magus_replay_run(magus_replay_t* h, const float* d_trace
     if (!h) return fail(nullptr, MAGUS_ERR_INVALID_ARG, "NULL handle");
     const magus_replay_desc& d = h->desc;
     const bool has_work = d.n_traces > 0 && d.n_samples > 0;
-    if (d.n_traces > 0 && (!d_trace || !d_w)) return fail(h, MAGUS_ERR_INVALID_ARG, "NULL trace or w");
+    if ((has_work && !d_trace) || (d.n_traces > 0 && !d_w)) return fail(h, MAGUS_ERR_INVALID_ARG, "NULL trace or w");
     if (has_work && ((uintptr_t)d_trace % 16 != 0)) return fail(h, MAGUS_ERR_ALIGN, "trace base must be 16-byte aligned");
     cudaStream_t s = (cudaStream_t)stream;
     if (has_work) {
@@ -1416,9 +1416,10 @@ extern "C" magus_status magus_replay_results(magus_replay_t* h, magus_results* o
     out->warmup_ticks = h->rp.warmup;
     out->n_mismatched_segments = (int64_t)segs;
     out->fixup_rounds = (int32_t)fl[1];
-    // Adaptive re-plan: speculation pays only while few segment entries are wrong.
-    // When more than 1% of the speculative entries mismatched (e.g. policies whose level freezes on
-    // aliased oscillations), the next runs use half as many segments.  Results are exact either way.
+    // Adaptive re-plan, off by default (MAGUS_REPLAN_PCT = 101, i.e. never): when more than
+    // MAGUS_REPLAN_PCT % of the speculative entries mismatched, the next runs use half as many segments.  The
+    // chain walk's cost does not grow with the segment count, so this only starves the replay of parallelism.
+    // Results are exact either way.
     if (d.tuning_segments == 0 && h->rp.n_seg > 1 && !env_int("MAGUS_NO_REPLAN", 0)) {
         const double spec = (double)h->rp.n_lane * (h->rp.n_seg - 1) * std::max(1, d.n_traces);
         if ((double)segs > h->replan_frac * spec) {

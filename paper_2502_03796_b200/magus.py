@@ -114,7 +114,7 @@ lib.magus_replay_destroy.restype = None
 lib.magus_replay_destroy.argtypes = [C.c_void_p]
 lib.magus_counters_to_trace.restype = _S
 lib.magus_counters_to_trace.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, C.c_int64, C.c_double,
-                                        C.c_void_p, C.c_void_p, C.c_void_p]
+                                        C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
 lib.magus_active_savings.restype = _S
 lib.magus_active_savings.argtypes = [C.POINTER(C.c_double), C.c_int32, C.c_int32, C.c_int32, C.c_double,
                                      C.POINTER(C.c_double)]
@@ -220,20 +220,23 @@ def derive_thresholds(policy: Policy, model: Model):
 
 def counters_to_trace(counts, trace, n_traces: int, period_s: float = 0.1, times=None, stream=None):
     """NEXT-3: recorded cumulative byte counters (CUDA uint64 tensor [n_rows][stride], as int64 storage) ->
-    trace (CUDA fp32 tensor [n_rows-1][stride], GB/s); times: optional CUDA fp64 tensor [n_rows].  Returns
-    (discarded intervals, non-increasing timestamps) after synchronising the stream."""
+    trace (CUDA fp32 tensor [n_rows-1][stride], GB/s): trace j's rounds are rows [0, n_valid[j]) of its column (a
+    wrap / reset interval yields no round, DESIGN A31); times: optional CUDA fp64 tensor [n_rows].  Returns
+    (n_valid as a numpy int64 array [n_traces], discarded intervals, non-increasing timestamps) after
+    synchronising the stream."""
     import torch
     rep = torch.zeros(2, dtype=torch.int64, device=counts.device)
+    nv = torch.zeros(max(1, n_traces), dtype=torch.int64, device=counts.device)
     _check(lib.magus_counters_to_trace(C.c_void_p(counts.data_ptr()),
                                        C.c_void_p(times.data_ptr()) if times is not None else None, n_traces,
                                        counts.shape[0], counts.shape[1], period_s, C.c_void_p(trace.data_ptr()),
-                                       C.c_void_p(rep.data_ptr()), _stream_ptr(stream)))
+                                       C.c_void_p(nv.data_ptr()), C.c_void_p(rep.data_ptr()), _stream_ptr(stream)))
     if stream is not None:
         stream.synchronize()
     else:
         torch.cuda.synchronize(counts.device)
     r = rep.cpu().tolist()
-    return int(r[0]), int(r[1])
+    return nv.cpu().numpy()[:n_traces], int(r[0]), int(r[1])
 
 
 def active_savings(policy_totals, policy: int, baseline: int, p_idle_w: float):

@@ -68,6 +68,7 @@ def main():
     rng = np.random.default_rng(1)
     counts = np.cumsum(rng.integers(0, 1_000_000_000, (300, 132)).astype(np.uint64), axis=0, dtype=np.uint64)
     tr = torch.empty((299, 132), dtype=torch.float32, device="cuda")
+    counts[150:, 7] -= counts[150, 7]   # a reset
     M.counters_to_trace(torch.from_numpy(counts.view(np.int64)).cuda(), tr, 130, period_s=0.1)
     torch.cuda.synchronize()
     print("ingest: ok", flush=True)

@@ -175,6 +175,10 @@ def test_empty_inputs(M):
     assert np.all(res.per_trace["T"] == 0) and np.all(res.per_trace["n_hi"] == 0)
     res = run_gpu(M, tr, w, CONFIGS[2]["policies"], 0, 100, 4)
     assert np.all(res.totals == 0)
+    with M.Replay(3, 0, PA.gpu_policies(CONFIGS[2]["policies"]), trace_stride=4, flags=M.F_PER_TRACE_STATS) as R:
+        R.run_host(np.zeros((0, 4), np.float32), np.full(3, 0.5, np.float32))   # the host path, no samples
+        res = R.results()
+    assert np.all(res.per_trace["T"] == 0) and res.totals[0, 12] == 3
     # the same in the wall-clock time model (A32): no rounds, zero records and totals
     pols = CONFIGS[5]["policies"]
     res = run_gpu(M, tr, w, pols, 3, 0, 4, flags=M.F_PER_TRACE_STATS | M.F_WALLCLOCK)
@@ -515,9 +519,10 @@ def test_open_loop_mode(M, segments):
 
 @pytest.mark.parametrize("with_times", [False, True])
 def test_counters_to_trace_and_open_loop_replay(M, with_times):
-    """NEXT-3 front end: recorded byte counters (with wraps / resets, a ragged column count) -> trace on the
-    GPU equals the oracle's conversion bit for bit (A31); the open-loop replay of that trace (A30) equals the
-    oracle's open-loop replay of its own conversion."""
+    """NEXT-3 front end: recorded byte counters (with wraps / resets, some at the start of a trace or at a
+    256-row chunk boundary, a ragged column count) -> trace on the GPU equals the oracle's conversion bit for bit,
+    and so do the per-trace round counts (a discarded interval yields no round, A31); the open-loop replay of the
+    first min(n_valid) rounds (A30) equals the oracle's open-loop replay of its own conversion."""
     rng = np.random.default_rng(33)
     n, rows, stride = 150, 3001, 152
     steps = rng.integers(0, 1_700_000_000, (rows, stride)).astype(np.uint64)   # <= 19 GB/s over >= 0.09 s
@@ -525,19 +530,23 @@ def test_counters_to_trace_and_open_loop_replay(M, with_times):
     counts = np.cumsum(steps, axis=0, dtype=np.uint64)
     for i, j in sorted(zip(rng.integers(1, rows, 40), rng.integers(0, n, 40))):   # counter resets, in time
         counts[i:, j] -= counts[i, j] - np.uint64(rng.integers(0, 1000))        # order (values stay >= 0)
+    counts[1:, 5] -= counts[1, 5] - np.uint64(3)                                  # reset in the first interval
+    counts[257:, 9] -= counts[257, 9] - np.uint64(1)                              # ... at a chunk boundary
     times = np.cumsum(rng.uniform(0.09, 0.11, rows)) if with_times else None
-    want, want_resets = O.counters_to_throughput(counts, period=0.1, times=times, n_traces=n)
+    want, want_nv, want_resets = O.counters_to_throughput(counts, period=0.1, times=times, n_traces=n)
     want[:, n:] = 0.0
     dc = torch.from_numpy(counts.view(np.int64)).cuda()
     dt = torch.from_numpy(times).cuda() if with_times else None
     tr = torch.empty((rows - 1, stride), dtype=torch.float32, device="cuda")
-    resets, bad = M.counters_to_trace(dc, tr, n, period_s=0.1, times=dt)
-    assert bad == 0 and resets == want_resets > 0
+    nv, resets, bad = M.counters_to_trace(dc, tr, n, period_s=0.1, times=dt)
+    assert bad == 0 and resets == want_resets > 0 and np.array_equal(nv, want_nv)
+    assert want_nv.min() < rows - 1
     assert np.array_equal(tr.cpu().numpy().view(np.uint32), want.view(np.uint32))
     w = torch.full((n,), 0.7, dtype=torch.float32, device="cuda")
     pols = [pol(), pol(kind=STATIC_MAX), pol(deriv_ticks=2, tune_log_capacity=6)]
-    res = run_gpu(M, tr, w, pols, n, rows - 1, stride, segments=4, model=M.Model(observe=1))
-    rec, _ = oracle_run(want, np.full(n, 0.7, np.float32), pols, n, model=O.Model(observe=1))
+    ns = int(want_nv.min())
+    res = run_gpu(M, tr[:ns], w, pols, n, ns, stride, segments=4, model=M.Model(observe=1))
+    rec, _ = oracle_run(want[:ns], np.full(n, 0.7, np.float32), pols, n, model=O.Model(observe=1))
     PA.compare_records(res.per_trace, rec, "counters open loop")
 
 

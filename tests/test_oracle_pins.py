@@ -479,13 +479,20 @@ def test_open_loop_flags_depend_on_the_trace_only():
 
 def test_counters_spec_examples():
     """counts 1e9 -> 2e9 over 0.1 s is 1e10 B/s (10 GB/s); equal counts are 0 B/s; a counter
-    that drops (reset to 0) is discarded -- the round repeats the last valid throughput (A31) -- and the
-    baseline re-arms, so the next interval is measured from the reset value."""
+    reset to 0 -> "sample discarded, no governor round": the interval yields no round at all -- the
+    trace's rounds are its valid intervals in time order, padded with 0 after n_valid (A31) -- and the baseline
+    re-arms, so the next interval is measured from the reset value."""
     counts = np.array([1_000_000_000, 2_000_000_000, 2_000_000_000, 0, 500_000_000], np.uint64)
-    thr, resets = O.counters_to_throughput(counts, period=0.1)
-    assert thr[:, 0].tolist() == [10.0, 0.0, 0.0, 5.0] and resets == 1
-    thr, resets = O.counters_to_throughput(np.array([5, 3, 1, 4_000_000_001], np.uint64), period=0.5)
-    assert thr[:, 0].tolist() == [0.0, 0.0, np.float32(8.0)] and resets == 2   # no valid interval before: 0
+    thr, nv, discarded = O.counters_to_throughput(counts, period=0.1)
+    assert thr[:, 0].tolist() == [10.0, 0.0, 5.0, 0.0] and nv.tolist() == [3] and discarded == 1
+    # leading resets: no round before the first valid interval (no made-up 0 GB/s sample)
+    thr, nv, discarded = O.counters_to_throughput(np.array([5, 3, 1, 4_000_000_001], np.uint64), period=0.5)
+    assert thr[:, 0].tolist() == [np.float32(8.0), 0.0, 0.0] and nv.tolist() == [1] and discarded == 2
+    # columns are independent: each trace keeps its own rounds
+    two = np.array([[0, 0], [10**9, 5], [2 * 10**9, 2], [3 * 10**9, 10**9 + 2]], np.uint64)
+    thr, nv, discarded = O.counters_to_throughput(two, period=1.0)
+    assert nv.tolist() == [3, 2] and discarded == 1
+    assert thr[:, 0].tolist() == [1.0, 1.0, 1.0] and thr[:, 1].tolist() == [np.float32(5e-9), 1.0, 0.0]
 
 
 def test_counters_timestamps_and_rounding():
@@ -498,8 +505,8 @@ def test_counters_timestamps_and_rounding():
     steps = rng.integers(0, 3_000_000_000, (n, 3)).astype(np.uint64)
     counts = np.cumsum(steps, axis=0, dtype=np.uint64)
     times = np.cumsum(rng.uniform(0.05, 0.2, n))
-    thr, resets = O.counters_to_throughput(counts, times=times)
-    assert resets == 0
+    thr, nv, resets = O.counters_to_throughput(counts, times=times)
+    assert resets == 0 and nv.tolist() == [n - 1] * 3
     for i in (0, 17, 48):
         for j in range(3):
             q = F(int(counts[i + 1, j] - counts[i, j])) / F(float(times[i + 1] - times[i])) / F(10**9)
