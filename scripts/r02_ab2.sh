@@ -3,6 +3,8 @@
 # usage: bash scripts/r02_ab2.sh TAG "<name>=<ENV=V ...>" ...
 TAG=$1; shift
 OUT=gpurun_out; mkdir -p $OUT
+timeout 1500 python -m pytest tests -m gpu -q -s -p no:cacheprovider -x --durations=10 > $OUT/${TAG}_pytest_gpu.log 2>&1
+echo "pytest rc=$?" >> $OUT/${TAG}_pytest_gpu.log
 for v in "$@"; do
   name=${v%%=*}; envs=${v#*=}
   env $envs timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider -x \
