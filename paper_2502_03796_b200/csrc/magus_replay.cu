@@ -168,6 +168,7 @@ WallKernel wall_kernel_for(int key, int64_t n_chains, int n_sm) {
 ReplayKernel solo_kernel_for(int key, bool sym, bool bits_ok) {
     int v = env_int("MAGUS_SOLO_BAL", 2);   // stage block variant (replay_solo.cuh)
     if (v == 9 && !sym) v = 3;              // |d| > d*_inc needs d*_dec == -d*_inc
+    if (v == 5 && !bits_ok) v = 2;          // the integer sample conversion needs |d*| >= 2^-60, B_lo normal
     if (v >= 10 && v <= 17) {   // the unified-stage kernel; v - 10 = VAR bits (1 |d| test, 2 incremental count,
                                 // 4 integer sample conversion)
         int var = v - 10;
@@ -199,6 +200,7 @@ ReplayKernel solo_kernel_for(int key, bool sym, bool bits_ok) {
      : v == 2 ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 2>                    \
      : v == 3 ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 3>                    \
      : v == 4 ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 4>                    \
+     : v == 5 ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 5>                    \
      : v == 9 ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 9>                    \
               : (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 1>)
     switch (key) {

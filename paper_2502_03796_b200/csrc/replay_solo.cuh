@@ -139,7 +139,8 @@ __device__ __forceinline__ void solo_stage_pq(MagusState<K, false>* s, float* lo
 }
 
 // One whole steady-state stage (8 ticks x 4 chains) of MAGUS chains with a register ring of K <= 3 values.
-template <int K, bool THR32 = false>
+// BITS: the fp32 -> fp64 sample conversion by integer ops (MAGUS_SSTAGEFB_K<K>, no XU), THR32 only.
+template <int K, bool THR32 = false, bool BITS = false>
 __device__ __forceinline__ void solo_stage(MagusState<K, false>* s, float* lock, float* nthr,
                                            uint32_t* wcmd, SegStats* ss, uint32_t& vmax, uint32_t tile,
                                            const SoloConst& sc, const DevPolicy& pol) {
@@ -161,7 +162,11 @@ __device__ __forceinline__ void solo_stage(MagusState<K, false>* s, float* lock,
 #define SOLO_R3                                                                                                \
     s[0].ring.v[0], s[0].ring.v[1], s[0].ring.v[2], s[1].ring.v[0], s[1].ring.v[1], s[1].ring.v[2], s[2].ring.v[0], \
         s[2].ring.v[1], s[2].ring.v[2], s[3].ring.v[0], s[3].ring.v[1], s[3].ring.v[2]
-    if constexpr (THR32) {   // throttle test as an fp32 compare on the ALU pipe (less FP64 work, less power)
+    if constexpr (THR32 && BITS) {
+        if constexpr (K == 1) MAGUS_SSTAGEFB_K1(SOLO_F, SOLO_R1, SOLO_TAILF);
+        else if constexpr (K == 2) MAGUS_SSTAGEFB_K2(SOLO_F, SOLO_R2, SOLO_TAILF);
+        else MAGUS_SSTAGEFB_K3(SOLO_F, SOLO_R3, SOLO_TAILF);
+    } else if constexpr (THR32) {   // throttle test as an fp32 compare on the ALU pipe (less FP64 work, less power)
         if constexpr (K == 1) MAGUS_SSTAGEF_K1(SOLO_F, SOLO_R1, SOLO_TAILF);
         else if constexpr (K == 2) MAGUS_SSTAGEF_K2(SOLO_F, SOLO_R2, SOLO_TAILF);
         else MAGUS_SSTAGEF_K3(SOLO_F, SOLO_R3, SOLO_TAILF);
@@ -304,7 +309,9 @@ __global__ void __launch_bounds__(32, kSoloCtasPerSm)
                 if constexpr (BAL == 1) solo_stage(st, lockf, nthrf, wcmd, ss, vmax, tile + lane_off, sc, pol);
                 else if constexpr (BAL == 2)
                     solo_stage<T::kRingK, true>(st, lockf, nthrf, wcmd, ss, vmax, tile + lane_off, sc, pol);
-                else if constexpr (BAL >= 3)
+                else if constexpr (BAL == 5)
+                    solo_stage<T::kRingK, true, true>(st, lockf, nthrf, wcmd, ss, vmax, tile + lane_off, sc, pol);
+                else if constexpr (BAL == 3 || BAL == 4 || BAL >= 9)
                     solo_stage_pq<T::kRingK, BAL>(st, lockf, nthrf, wcmd, ss, vmax, tile + lane_off, sc, pol);
                 else T::stage8(st, tile + lane_off, pol, B_lo, Blo_d, wcmd, ss, vmax);
                 __syncwarp();   // every lane's tile reads are complete before the slot is refilled

@@ -156,7 +156,7 @@ def build_stage(K, TC=8):
 
 
 
-def build_stage_f(K, TC=8, walk=False, traces=1, thr64=True, one=False):
+def build_stage_f(K, TC=8, walk=False, traces=1, thr64=True, one=False, bits=False):
     """MAGUS_SSTAGE_K<K>: one whole steady-state stage (TC ticks x 4 chains, tile loads included) of the solo
     replay kernel, balanced over the issue pipes (ALU and FMA-heavy at half rate, FP64, XU): the throttle
     test on the FP64 pipe, the tune log, scaled window count and cmd word as (predicated) IMADs, the lock /
@@ -179,7 +179,7 @@ def build_stage_f(K, TC=8, walk=False, traces=1, thr64=True, one=False):
     idx = {n: f"%{i}" for i, (n, _) in enumerate(names + inames)}
     R = idx.__getitem__
     body = ["{", ".reg .pred phi<4>, pthr<4>, pinc<4>, pev<4>, phf<4>, pq<4>, pk<4>;",
-            f".reg .b32 D<{TC * C}>;", f".reg .f64 dd<4>, dv<4>, dx<4>, ad<{TC * C}>;", ".reg .b32 tb<4>;"]
+            f".reg .b32 D<{TC * C}>;", f".reg .f64 dd<4>, dv<4>, dx<4>, ad<{TC * C}>;", ".reg .b32 tb<4>, xh<4>, xl<4>;"]
     for c in range(C):
         body.append(f"setp.ne.u32 phi{c}, {R(f'f{c}')}, 0;")
     for tt in range(TC):
@@ -187,8 +187,12 @@ def build_stage_f(K, TC=8, walk=False, traces=1, thr64=True, one=False):
             body += [f"mov.b32 D{tt * C + c}, {R(f'S{c // 2}_{tt}')};" for c in range(C)]
         else:
             body.append(f"ld.shared.v4.f32 {{D{tt * C}, D{tt * C + 1}, D{tt * C + 2}, D{tt * C + 3}}}, [{R('tile')}+{tt * 512}];")
-        per_chain = [
-            "cvt.f64.f32 dd{c}, {D};",
+        per_chain = ([
+            "shr.u32 xh{c}, {D}, 3;",                                    # fp32 -> fp64 by integer ops (no XU):
+            "add.u32 xh{c}, xh{c}, 0x38000000;",                         # exact for normal samples (DESIGN 7)
+            "shl.b32 xl{c}, {D}, 29;",
+            "mov.b64 dd{c}, {{xl{c}, xh{c}}};",
+        ] if bits else ["cvt.f64.f32 dd{c}, {D};"]) + [
             ("setp.gt.and.f64 pthr{c}, dd{c}, {Blod}, !phi{c};" if thr64  # throttled: f_min and D > B_lo (A14)
              else "setp.gt.and.f32 pthr{c}, {D}, {Blo}, !phi{c};"),
             "selp.f64 {ad}, {Blod}, dd{c}, pthr{c};",                    # A = min(D, B[f]) as fp64 (exact)
@@ -228,7 +232,7 @@ def build_stage_f(K, TC=8, walk=False, traces=1, thr64=True, one=False):
             body.append(f"mov.f64 {R(f'r{c}_{i}')}, ad{(TC - 1 - i) * C + c};")
     body.append("}")
     params = ", ".join(n for n, _ in names + inames)
-    name = f"MAGUS_{'W' if walk else 'S'}STAGE{'2' if traces == 2 else ''}{'1' if one else ''}{'' if thr64 else 'F'}_K{K}"
+    name = f"MAGUS_{'W' if walk else 'S'}STAGE{'2' if traces == 2 else ''}{'1' if one else ''}{'' if thr64 else 'F'}{'B' if bits else ''}_K{K}"
     out = [f"#define {name}(...) {name}_(__VA_ARGS__)", f"#define {name}_({params}) \\", "    asm volatile( \\"]
     out += [f'        "{l}\\n\\t" \\' for l in body]
     out.append("        : " + ", ".join(f'"{c}"({n})' for n, c in names) + " \\")
@@ -451,6 +455,7 @@ for K in (1, 2, 3):
     out += [""] + build_stage(K)
     out += [""] + build_stage_f(K)
     out += [""] + build_stage_f(K, thr64=False)
+    out += [""] + build_stage_f(K, thr64=False, bits=True)
     for sym in (False, True):
         for popc in (True, False):
             for bits in (False, True):
