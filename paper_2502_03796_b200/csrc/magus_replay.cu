@@ -759,6 +759,21 @@ static void choose_geometry(magus_replay_t* h, int n_sm, int forced_segments) {
             g.smem = SoloSmem<kTC, kNStage>::kBytes + env_int("MAGUS_SOLO_SMEM_PAD", 0);   // pad: occupancy probes
             g.n_ctas = p.n_seg * p.n_groups * g.nq;
         }
+        // TDP_DEFAULT groups: the TDP solo kernel, NP policies per warp sharing the samples (MAGUS_TDP_SOLO = NP in
+        // {1, 2}; 0: the multi-warp kernel)
+        const int tnp = env_int("MAGUS_TDP_SOLO", 2);
+        if (g.key == 1000 + LANE_TDP && kTC == 8 && (tnp == 1 || tnp == 2)) {
+            g.solo = true;
+            g.kernel = tnp == 1 ? (ReplayKernel)magus_replay_tsolo_kernel<1, kTC, kNStage>
+                                : (ReplayKernel)magus_replay_tsolo_kernel<2, kTC, kNStage>;
+            g.ng = 1;
+            g.npw = 1;
+            g.n_tblocks = p.n_groups;
+            g.n_pblocks = (g.nq + tnp - 1) / tnp;
+            g.threads = 32;
+            g.smem = SoloSmem<kTC, kNStage>::kBytes;
+            g.n_ctas = p.n_seg * p.n_groups * g.n_pblocks;
+        }
     }
 }
 

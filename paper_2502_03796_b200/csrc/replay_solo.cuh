@@ -634,4 +634,186 @@ __global__ void __launch_bounds__(32, kSoloCtasPerSm)
     if (j0 < p.n_traces) atomicMax(p.c_vmax + chain_idx(p, q, j0), vmax);   // lane-level validation maximum
 }
 
+// ===================================================================================================================
+// The TDP_DEFAULT solo kernel (the Intel-default baseline): one-warp CTAs with the solo kernel's TMA ring;
+// a warp runs NP TDP policies on the same 128 traces (4 per lane), so the samples are read once for the NP
+// policies.  One generated stage block per 8 ticks (MAGUS_TSTAGE<NP>, tick4_asm.cuh).  The throttled demand is
+// summed in fp64 as sum(D) (a 0/1 DFMA, exact) and turned into the excess sum(D - B_lo) = sum(D) - n_thr B_lo once
+// per segment (exact: DESIGN.md section 8).  Speculative segments start p.warmup ticks early at the guessed
+// level (f_max); the exact fix-up is the TDP lockstep walk.
+template <int NP, int TC, int NSTAGE>
+__global__ void __launch_bounds__(32, kSoloCtasPerSm)
+    magus_replay_tsolo_kernel(const __grid_constant__ CUtensorMap tmap, const ReplayParams p) {
+    static_assert(TC == 8, "TDP solo kernel: whole-stage PTX block of 8 ticks");
+    constexpr int NC = 4 * NP;   // chains per lane
+    using SM = SoloSmem<TC, NSTAGE>;
+    constexpr uint32_t kTileBytes = SM::kTileBytes;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int lane = threadIdx.x;
+    const int npairs = (p.nq + NP - 1) / NP;
+    int b = blockIdx.x;
+    const int pi = b % npairs;
+    b /= npairs;
+    const int tgroup = b % p.n_groups;
+    const int seg = b / p.n_groups;
+    int qs[NP];
+    bool live[NP];
+#pragma unroll
+    for (int u = 0; u < NP; ++u) {
+        const int qi = pi * NP + u;
+        live[u] = qi < p.nq;
+        qs[u] = p.q_base + (live[u] ? qi : pi * NP);   // a missing second policy repeats the first, unrecorded
+    }
+
+    const uint32_t tile0 = ptx::smem_u32(smem);
+    const uint32_t bar0 = tile0 + NSTAGE * kTileBytes;
+    if (lane == 0) {
+        ptx::prefetch_tmap(&tmap);
+        for (int i = 0; i < NSTAGE; ++i)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8 * i) : "memory");
+        ptx::fence_mbar_init();
+    }
+    __syncwarp();
+    const SegGeom G = seg_geom<TC>(p, seg);
+    const int x = tgroup * kTracesPerWarp;
+    const uint64_t cpol = ptx::policy_evict_first();
+    for (int i = 0; i < NSTAGE && i < G.n_stages; ++i)
+        solo_issue<TC>(tile0 + i * kTileBytes, &tmap, bar0 + 8 * i, x, G.tau_w + i * TC, cpol);
+    ptx::pdl_wait();
+
+    const int j0 = x + lane * kChains;
+    const float B_lo = p.B_lo;
+    const double Blo_d = (double)B_lo;
+    float ahi[NP], alo[NP];
+    uint32_t f[NC], wcmd[NC], fstart[NC];
+    double exc[NC];
+    float nthrf[NC];
+    uint32_t nhi[NC], trans[NC], dc[NC];
+    uint32_t one = 1, vmax = 0;
+#pragma unroll
+    for (int u = 0; u < NP; ++u) {
+        const DevPolicy pol = p.pol[qs[u]];
+        one = pol.one;
+        ahi[u] = pol.astar_hi;
+        alo[u] = B_lo >= pol.astar_lo ? pol.astar_lo : __int_as_float(0x7F800000);   // A = min(D, B_lo) at f_min
+#pragma unroll
+        for (int c = 0; c < 4; ++c) f[u * 4 + c] = seg == 0 ? (uint32_t)pol.f0 : (uint32_t)pol.guess_f;
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        wcmd[c] = 0;
+        exc[c] = 0.0;
+        nthrf[c] = 0.f;
+        nhi[c] = trans[c] = dc[c] = 0;
+    }
+    const uint32_t lane_off = (uint32_t)lane * 16u;
+    int i = 0, slot = 0;
+    uint32_t phase = 0;
+#pragma unroll 1
+    for (int bt0 = G.tau_w; bt0 < G.seg_end; bt0 += 32) {
+        if (bt0 == G.seg_start) {
+#pragma unroll
+            for (int u = 0; u < NP; ++u)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const int j = j0 + c, cc = u * 4 + c;
+                    if (j < p.n_traces && live[u]) {
+                        const int64_t si = st_idx(p, 0, qs[u], seg, j);
+                        p.st_f[si] = (uint8_t)f[cc];
+                        p.st_log[si] = 0;
+                    }
+                    exc[cc] = 0.0;
+                    nthrf[cc] = 0.f;
+                    nhi[cc] = trans[cc] = dc[cc] = 0;
+                }
+        }
+#pragma unroll
+        for (int c = 0; c < NC; ++c) fstart[c] = f[c];
+#pragma unroll 1
+        for (int sub = 0; sub < 32 / TC && i < G.n_stages; ++sub) {
+            const int t0 = bt0 + sub * TC;
+            const uint32_t tile = tile0 + slot * kTileBytes;
+            mbar_wait_loop(bar0 + 8 * slot, phase);
+            if (t0 + TC <= G.seg_end) {
+                if constexpr (NP == 1)
+                    MAGUS_TSTAGE1(f[0], f[1], f[2], f[3], exc[0], exc[1], exc[2], exc[3], nthrf[0], nthrf[1], nthrf[2],
+                                  nthrf[3], wcmd[0], wcmd[1], wcmd[2], wcmd[3], vmax, tile + lane_off, B_lo, ahi[0],
+                                  alo[0], one);
+                else
+                    MAGUS_TSTAGE2(f[0], f[1], f[2], f[3], f[4], f[5], f[6], f[7], exc[0], exc[1], exc[2], exc[3],
+                                  exc[4], exc[5], exc[6], exc[7], nthrf[0], nthrf[1], nthrf[2], nthrf[3], nthrf[4],
+                                  nthrf[5], nthrf[6], nthrf[7], wcmd[0], wcmd[1], wcmd[2], wcmd[3], wcmd[4], wcmd[5],
+                                  wcmd[6], wcmd[7], vmax, tile + lane_off, B_lo, ahi[0], ahi[1], alo[0], alo[1], one);
+            } else {   // the ragged last stage of a trace: the same tick, per tick
+                const float4* rows = reinterpret_cast<const float4*>(smem + slot * kTileBytes) + lane;
+#pragma unroll 1
+                for (int tt = 0; tt < TC; ++tt) {
+                    if (t0 + tt >= G.seg_end) break;
+                    const float4 d4 = rows[tt * (kTracesPerWarp / 4)];
+                    const float d[4] = {d4.x, d4.y, d4.z, d4.w};
+#pragma unroll
+                    for (int cc = 0; cc < NC; ++cc) {
+                        const float D = d[cc % 4];
+                        const bool thr = f[cc] == 0u && D > B_lo;
+                        const float a = f[cc] ? ahi[cc / 4] : alo[cc / 4];
+                        f[cc] = D < a ? 1u : 0u;
+                        exc[cc] = __fma_rn(thr ? 1.0 : 0.0, (double)D, exc[cc]);
+                        nthrf[cc] += thr ? 1.f : 0.f;
+                        wcmd[cc] = (wcmd[cc] << 1) | f[cc];
+                    }
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) vmax = max(vmax, __float_as_uint(d[c]));
+                }
+            }
+            __syncwarp();
+            if (i + NSTAGE < G.n_stages) solo_issue<TC>(tile, &tmap, bar0 + 8 * slot, x, G.tau_w + (i + NSTAGE) * TC, cpol);
+            ++i;
+            if (++slot == NSTAGE) {
+                slot = 0;
+                phase ^= 1u;
+            }
+        }
+        if (bt0 >= G.seg_start) {   // fold the 32-tick block: level / transition counts and the digest (no tune flags)
+            const int n = min(32, G.seg_end - bt0);
+            const int64_t bi = bt0 >> 5;
+            const uint2 bkey = p.dkeys[bi];
+#pragma unroll
+            for (int u = 0; u < NP; ++u) {
+                uint32_t* wbase =
+                    (p.words && live[u]) ? p.words + ((int64_t)qs[u] * p.n_traces * p.n_blocks + bi) * 2 : nullptr;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const int cc = u * 4 + c;
+                    const uint32_t mask = n >= 32 ? 0xFFFFFFFFu : ((1u << n) - 1u);
+                    const uint32_t cw = wcmd[cc] & mask;
+                    const uint32_t lw = ((wcmd[cc] >> 1) & (mask >> 1)) | (fstart[cc] << (n - 1));
+                    trans[cc] += __popc(cw ^ lw);
+                    nhi[cc] += __popc(lw);
+                    const uint32_t wc = cw << (32 - n);
+                    dc[cc] += wc * (n == 32 ? bkey.x : digest_key((uint64_t)bi).x);
+                    if (wbase && j0 + c < p.n_traces) {
+                        uint32_t* wo = wbase + (int64_t)(j0 + c) * p.n_blocks * 2;
+                        wo[0] = wc;
+                        wo[1] = 0u;
+                    }
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < NP; ++u)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int j = j0 + c, cc = u * 4 + c;
+            if (j >= p.n_traces || !live[u]) continue;
+            const int64_t si = st_idx(p, 1, qs[u], seg, j);
+            p.st_f[si] = (uint8_t)f[cc];
+            p.st_log[si] = 0;
+            const uint32_t nthr = (uint32_t)nthrf[cc];
+            const double sexc = exc[cc] - (double)nthr * Blo_d;   // sum(D - B_lo) over throttled ticks, exact
+            add_to_chain(p, qs[u], j, nhi[cc], nthr, trans[cc], 0u, 0u, sexc, digest_pack(dc[cc], 0u));
+        }
+    if (j0 < p.n_traces) atomicMax(p.c_vmax + chain_idx(p, qs[0], j0), vmax);
+}
+
 }  // namespace magus

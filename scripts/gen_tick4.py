@@ -446,6 +446,64 @@ def build_stage_u(K, TC=8, sym=False, popc=True, bits=False):
     return out
 
 
+def build_stage_t(NP, TC=8):
+    """MAGUS_TSTAGE{NP}: one steady stage (TC ticks x 4 traces x NP TDP_DEFAULT policies) of the TDP solo kernel
+    (the Intel-default baseline, A24).  Per (trace, policy) chain and tick:
+      throttled = f_min && D > B_lo (A14);  next level f_max iff D < a[f] -- a[f_max] = a*_hi; a[f_min] = a*_lo if
+      B_lo >= a*_lo else +inf (A = min(D, B_lo) at f_min), the host-derived exact equivalents of
+      fl(P[f] + fl(c A)) >= fl((1 - m) TDP) (DESIGN.md section 8);
+      sum of D over throttled ticks in fp64 by one DFMA with a 0/1 factor (exact: the terms are multiples of
+      ulp(B_lo), section 8; the kernel subtracts n_thr * B_lo once per segment); the throttled count as an fp32 add;
+      the cmd word.  The sample's fp64 value is converted once per trace and shared by the NP policies."""
+    C = 4 * NP
+    names = [(f"f{c}", "+r") for c in range(C)] + [(f"exc{c}", "+d") for c in range(C)] + \
+            [(f"nthr{c}", "+f") for c in range(C)] + [(f"wcmd{c}", "+r") for c in range(C)] + [("vmax", "+r")]
+    inames = [("tile", "r"), ("Blo", "f")] + [(f"ahi{p}", "f") for p in range(NP)] + \
+             [(f"alo{p}", "f") for p in range(NP)] + [("one", "r")]
+    idx = {n: f"%{i}" for i, (n, _) in enumerate(names + inames)}
+    R = idx.__getitem__
+    body = ["{", f".reg .pred phi<{C}>, pthr<{C}>;", f".reg .b32 D<{TC * 4}>, a<{C}>, sh<{C}>;",
+            f".reg .f64 dd<4>, s<{C}>;"]
+    for c in range(C):
+        body.append(f"setp.ne.u32 phi{c}, {R(f'f{c}')}, 0;")
+    for tt in range(TC):
+        body.append(f"ld.shared.v4.f32 {{D{tt * 4}, D{tt * 4 + 1}, D{tt * 4 + 2}, D{tt * 4 + 3}}}, [{R('tile')}+{tt * 512}];")
+        for u in range(4):
+            body.append(f"cvt.f64.f32 dd{u}, D{tt * 4 + u};")
+        body.append(f"max.u32 {R('vmax')}, {R('vmax')}, D{tt * 4};")
+        body.append(f"max.u32 {R('vmax')}, {R('vmax')}, D{tt * 4 + 1};")
+        body.append(f"max.u32 {R('vmax')}, {R('vmax')}, D{tt * 4 + 2};")
+        body.append(f"max.u32 {R('vmax')}, {R('vmax')}, D{tt * 4 + 3};")
+        per_chain = [
+            "setp.gt.and.f32 pthr{c}, {D}, {Blo}, !phi{c};",             # throttled (A14)
+            "selp.f32 a{c}, {ahi}, {alo}, phi{c};",                       # a*[f] (A24)
+            "setp.lt.f32 phi{c}, {D}, a{c};",                             # next level f_max iff A < a*[f]
+            "selp.b32 sh{c}, 0x3FF00000, 0, pthr{c};",
+            "mov.b64 s{c}, {{0, sh{c}}};",                                # 1.0 if throttled, else 0.0
+            "fma.rn.f64 {exc}, s{c}, {dd}, {exc};",                       # sum of D over throttled ticks (exact)
+            "@pthr{c} add.f32 {nthr}, {nthr}, 0f3F800000;",
+            "shl.b32 {wcmd}, {wcmd}, 1;",
+            "@phi{c} mad.lo.u32 {wcmd}, {one}, {one}, {wcmd};",
+        ]
+        for tmpl in per_chain:
+            for c in range(C):
+                u, pp = c % 4, c // 4
+                body.append(tmpl.format(c=c, D=f"D{tt * 4 + u}", dd=f"dd{u}", Blo=R("Blo"), ahi=R(f"ahi{pp}"),
+                                        alo=R(f"alo{pp}"), exc=R(f"exc{c}"), nthr=R(f"nthr{c}"), wcmd=R(f"wcmd{c}"),
+                                        one=R("one")))
+    for c in range(C):
+        body.append(f"selp.u32 {R(f'f{c}')}, 1, 0, phi{c};")
+    body.append("}")
+    params = ", ".join(n for n, _ in names + inames)
+    name = f"MAGUS_TSTAGE{NP}"
+    out = [f"#define {name}(...) {name}_(__VA_ARGS__)", f"#define {name}_({params}) \\", "    asm volatile( \\"]
+    out += [f'        "{l}\\n\\t" \\' for l in body]
+    out.append("        : " + ", ".join(f'"{c}"({n})' for n, c in names) + " \\")
+    out.append("        : " + ", ".join(f'"{c}"({n})' for n, c in inames) + " \\")
+    out.append('        : "memory")')
+    return out
+
+
 out = ["// GENERATED by scripts/gen_tick4.py -- do not edit.  One MAGUS tick for the 4 chains of a lane, the",
        "// four chains' instructions interleaved (DESIGN.md section 7); semantics = magus_tick<K, false, SLOW>.",
        "// cnt is the window count scaled by 2^(C-1).",
@@ -467,6 +525,8 @@ for K in (1, 2, 3):
 for K in range(1, 9):
     out += [""] + build_stage_f(K, walk=True)
     out += [""] + build_stage_f(K, walk=True, one=True, thr64=False)
+for NP in (1, 2):
+    out += [""] + build_stage_t(NP)
 path = os.path.join(os.path.dirname(__file__), "..", "paper_2502_03796_b200", "csrc", "tick4_asm.cuh")
 open(path, "w").write("\n".join(out) + "\n")
 print("wrote", os.path.normpath(path))

@@ -12,3 +12,7 @@ template __global__ void magus::magus_replay_solo_kernel<magus::MagusTicker<PROB
 template __global__ void magus::magus_replay_usolo_kernel<magus::MagusTicker<PROBE_K, false>, 8, 3, PROBE_U>(
     const __grid_constant__ CUtensorMap, const magus::ReplayParams);
 #endif
+#ifdef PROBE_T
+template __global__ void magus::magus_replay_tsolo_kernel<PROBE_T, 8, 3>(const __grid_constant__ CUtensorMap,
+                                                                         const magus::ReplayParams);
+#endif
