@@ -475,6 +475,11 @@ __global__ void __launch_bounds__(32) magus_fix_lockstep_kernel(const ReplayPara
 // per cycle, so halving the instructions each warp issues per tick nearly halves the walk.  The warps
 // meet at a named barrier at every segment boundary and every 32-tick block end: warp 1 publishes its
 // state and statistics in shared memory, warp 0 compares, adds the deltas and publishes the decisions.
+// MAGUS_WALK_LOOKAHEAD: the split walk's stage block with both levels' decisions evaluated ahead of the level
+// (MAGUS_WSTAGE1L_K<K>: a short loop-carried dependency for the latency-bound walk), else MAGUS_WSTAGE1F_K<K>
+#ifndef MAGUS_WALK_LOOKAHEAD
+#define MAGUS_WALK_LOOKAHEAD 1
+#endif
 template <int K>
 __device__ __forceinline__ void walk_stage1(MagusState<K, false>& st, float& lock, float& nthr, uint32_t& wcmd,
                                             SegStats& ss, const float* d8, const DevPolicy& pol, float B_lo,
@@ -486,6 +491,16 @@ __device__ __forceinline__ void walk_stage1(MagusState<K, false>& st, float& loc
         __float_as_uint(d8[3]), __float_as_uint(d8[4]), __float_as_uint(d8[5]), __float_as_uint(d8[6]),             \
         __float_as_uint(d8[7]), B_lo, Blo_d, pol.dinc, pol.ddec, bitc, pol.smin_sc, pol.one, mone
 #define R(i) st.ring.v[i]
+#if MAGUS_WALK_LOOKAHEAD
+    if constexpr (K == 1) MAGUS_WSTAGE1L_K1(st.f, R(0), W1_TAIL);
+    else if constexpr (K == 2) MAGUS_WSTAGE1L_K2(st.f, R(0), R(1), W1_TAIL);
+    else if constexpr (K == 3) MAGUS_WSTAGE1L_K3(st.f, R(0), R(1), R(2), W1_TAIL);
+    else if constexpr (K == 4) MAGUS_WSTAGE1L_K4(st.f, R(0), R(1), R(2), R(3), W1_TAIL);
+    else if constexpr (K == 5) MAGUS_WSTAGE1L_K5(st.f, R(0), R(1), R(2), R(3), R(4), W1_TAIL);
+    else if constexpr (K == 6) MAGUS_WSTAGE1L_K6(st.f, R(0), R(1), R(2), R(3), R(4), R(5), W1_TAIL);
+    else if constexpr (K == 7) MAGUS_WSTAGE1L_K7(st.f, R(0), R(1), R(2), R(3), R(4), R(5), R(6), W1_TAIL);
+    else MAGUS_WSTAGE1L_K8(st.f, R(0), R(1), R(2), R(3), R(4), R(5), R(6), R(7), W1_TAIL);
+#else
     if constexpr (K == 1) MAGUS_WSTAGE1F_K1(st.f, R(0), W1_TAIL);
     else if constexpr (K == 2) MAGUS_WSTAGE1F_K2(st.f, R(0), R(1), W1_TAIL);
     else if constexpr (K == 3) MAGUS_WSTAGE1F_K3(st.f, R(0), R(1), R(2), W1_TAIL);
@@ -494,6 +509,7 @@ __device__ __forceinline__ void walk_stage1(MagusState<K, false>& st, float& loc
     else if constexpr (K == 6) MAGUS_WSTAGE1F_K6(st.f, R(0), R(1), R(2), R(3), R(4), R(5), W1_TAIL);
     else if constexpr (K == 7) MAGUS_WSTAGE1F_K7(st.f, R(0), R(1), R(2), R(3), R(4), R(5), R(6), W1_TAIL);
     else MAGUS_WSTAGE1F_K8(st.f, R(0), R(1), R(2), R(3), R(4), R(5), R(6), R(7), W1_TAIL);
+#endif
 #undef R
 #undef W1_TAIL
     st.evh = e0;

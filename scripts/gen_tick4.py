@@ -504,6 +504,86 @@ def build_stage_t(NP, TC=8):
     return out
 
 
+def build_stage_wl(K, TC=8):
+    """MAGUS_WSTAGE1L_K<K>: the chain walk's one-chain stage (TC ticks of one (trace, policy) recurrence, samples
+    passed in registers), same operands and decisions as MAGUS_WSTAGE1F_K<K>, restructured for a short loop-carried
+    dependency (a walking warp is alone on its SM sub-partition: latency-bound).  Everything that does not depend
+    on the level in effect is evaluated for BOTH levels ahead of it -- A at f_min / f_max, both derivatives
+    against A_{t-k} (known k ticks earlier), their +1 / -1 / flag predicates, and the Alg. 2 window count with
+    and without a new flag -- so the level recurrence per tick is three predicate selections:
+      flag = level ? flag_max : flag_min;  lock = flag ? (cnt+1 >= s_min) : (cnt >= s_min);
+      new level = lock | (level ? (+1_max | !-1_max) : +1_min)."""
+    names = [("f0", "+r")] + [(f"r0_{i}", "+d") for i in range(K)] + \
+            [("evh0", "+r"), ("cnt0", "+r"), ("exc0", "+d"), ("lock0", "+f"), ("nthr0", "+f"), ("wcmd0", "+r")]
+    inames = [(f"S0_{tt}", "r") for tt in range(TC)] + [("Blo", "f"), ("Blod", "d"), ("dinc", "d"), ("ddec", "d"),
+                                                         ("bitc", "r"), ("smin", "r"), ("one", "r"), ("mone", "r")]
+    idx = {n: f"%{i}" for i, (n, _) in enumerate(names + inames)}
+    R = idx.__getitem__
+    body = ["{", ".reg .pred phi, pgt, iL, cL, iH, cH, eL, eH, gH, px, pev, h0, h1, phf, pthr;",
+            f".reg .f64 dd, aL, dvL, dvH, dx, ad<{TC}>;", ".reg .b32 tb, c0, c1;",
+            f"setp.ne.u32 phi, {R('f0')}, 0;"]
+    for tt in range(TC):
+        D = R(f"S0_{tt}")
+        old = f"ad{tt - K}" if tt >= K else R(f"r0_{K - 1 - tt}")
+        body += [
+            f"cvt.f64.f32 dd, {D};",
+            f"setp.gt.f32 pgt, {D}, {R('Blo')};",                          # D > B_lo: throttled at f_min (A14)
+            f"selp.f64 aL, {R('Blod')}, dd, pgt;",                         # A at f_min; A at f_max = D
+            f"sub.f64 dvL, aL, {old};",                                    # Alg. 1 numerators for both levels (P:207)
+            f"sub.f64 dvH, dd, {old};",
+            f"setp.gt.f64 iL, dvL, {R('dinc')};",                          # +1 (P:209), -1 (P:213) at each level
+            f"setp.lt.f64 cL, dvL, {R('ddec')};",
+            f"setp.gt.f64 iH, dvH, {R('dinc')};",
+            f"setp.lt.f64 cH, dvH, {R('ddec')};",
+            "or.pred eL, iL, cL;",                                        # tune flag at each level (P:243)
+            "or.pred eH, iH, cH;",
+            "not.pred gH, cH;",
+            "or.pred gH, gH, iH;",                                        # at f_max: +1 or not -1 keeps / sets f_max
+            f"and.b32 tb, {R('evh0')}, {R('bitc')};",                      # the flag leaving the C-window (scaled)
+            f"mad.lo.u32 c0, tb, {R('mone')}, {R('cnt0')};",               # window count without / with a new flag
+            f"add.u32 c1, c0, {R('bitc')};",
+            f"setp.ge.u32 h0, c0, {R('smin')};",
+            f"setp.ge.u32 h1, c1, {R('smin')};",
+            # ---- the level-dependent part
+            "and.pred px, phi, gH;",                                      # level & (+1 | !-1) at f_max ...
+            "not.pred pthr, phi;",
+            "and.pred pev, pthr, iL;",
+            "or.pred px, px, pev;",                                       # ... | (!level & +1 at f_min)
+            "and.pred pev, phi, eH;",
+            "and.pred pthr, pthr, eL;",
+            "or.pred pev, pev, pthr;",                                    # the tune flag at the level in effect
+            "and.pred phf, pev, h1;",
+            "not.pred pthr, pev;",
+            "and.pred pthr, pthr, h0;",
+            "or.pred phf, phf, pthr;",                                    # Alg. 2 on the updated window (P:230)
+            f"selp.f64 ad{tt}, dd, aL, phi;",                              # A in effect (the ring value)
+            "not.pred pthr, phi;",
+            "and.pred pthr, pthr, pgt;",                                  # throttled
+            f"selp.b32 {R('cnt0')}, c1, c0, pev;",
+            f"shl.b32 {R('evh0')}, {R('evh0')}, 1;",
+            f"@pev add.u32 {R('evh0')}, {R('evh0')}, 1;",
+            "or.pred phi, phf, px;",                                      # lock || +1 || (f_max && !-1)
+            f"shl.b32 {R('wcmd0')}, {R('wcmd0')}, 1;",
+            f"@phi add.u32 {R('wcmd0')}, {R('wcmd0')}, 1;",
+            f"sub.f64 dx, dd, ad{tt};",                                    # throttling excess D - A (0 unless thr)
+            f"add.f64 {R('exc0')}, {R('exc0')}, dx;",
+            f"@phf add.f32 {R('lock0')}, {R('lock0')}, 0f3F800000;",
+            f"@pthr add.f32 {R('nthr0')}, {R('nthr0')}, 0f3F800000;",
+        ]
+    body.append(f"selp.u32 {R('f0')}, 1, 0, phi;")
+    for i in range(K):
+        body.append(f"mov.f64 {R(f'r0_{i}')}, ad{TC - 1 - i};")
+    body.append("}")
+    params = ", ".join(n for n, _ in names + inames)
+    name = f"MAGUS_WSTAGE1L_K{K}"
+    out = [f"#define {name}(...) {name}_(__VA_ARGS__)", f"#define {name}_({params}) \\", "    asm volatile( \\"]
+    out += [f'        "{l}\\n\\t" \\' for l in body]
+    out.append("        : " + ", ".join(f'"{c}"({n})' for n, c in names) + " \\")
+    out.append("        : " + ", ".join(f'"{c}"({n})' for n, c in inames) + " \\")
+    out.append('        : "memory")')
+    return out
+
+
 out = ["// GENERATED by scripts/gen_tick4.py -- do not edit.  One MAGUS tick for the 4 chains of a lane, the",
        "// four chains' instructions interleaved (DESIGN.md section 7); semantics = magus_tick<K, false, SLOW>.",
        "// cnt is the window count scaled by 2^(C-1).",
@@ -527,6 +607,8 @@ for K in range(1, 9):
     out += [""] + build_stage_f(K, walk=True, one=True, thr64=False)
 for NP in (1, 2):
     out += [""] + build_stage_t(NP)
+for K in range(1, 9):
+    out += [""] + build_stage_wl(K)
 path = os.path.join(os.path.dirname(__file__), "..", "paper_2502_03796_b200", "csrc", "tick4_asm.cuh")
 open(path, "w").write("\n".join(out) + "\n")
 print("wrote", os.path.normpath(path))
