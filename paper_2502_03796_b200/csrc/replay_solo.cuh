@@ -810,7 +810,8 @@ __global__ void __launch_bounds__(32, kSoloCtasPerSm)
             p.st_f[si] = (uint8_t)f[cc];
             p.st_log[si] = 0;
             const uint32_t nthr = (uint32_t)nthrf[cc];
-            const double sexc = exc[cc] - (double)nthr * Blo_d;   // sum(D - B_lo) over throttled ticks, exact
+            // sum(D - B_lo) over throttled ticks, exact; no throttled tick: 0 (the open-loop mode's B_lo is +inf)
+            const double sexc = nthr ? exc[cc] - (double)nthr * Blo_d : 0.0;
             add_to_chain(p, qs[u], j, nhi[cc], nthr, trans[cc], 0u, 0u, sexc, digest_pack(dc[cc], 0u));
         }
     if (j0 < p.n_traces) atomicMax(p.c_vmax + chain_idx(p, qs[0], j0), vmax);
