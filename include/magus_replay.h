@@ -283,11 +283,13 @@ int32_t magus_abi_version(void);
 
 /* Diagnostics: the current launch plan: out = {n_segments, segment_len, warmup_ticks,
  * tile_groups_per_cta, policy_warps_per_group, trace_blocks, policy_blocks, ctas, threads_per_cta,
- * smem_bytes, lane_policies, launch_groups, kernels_per_run, solo_groups, seg_long, 0} (seg_long: the first
+ * smem_bytes, lane_policies, launch_groups, kernels_per_run, solo_groups, seg_long, wide_groups} (seg_long: the first
  * seg_long segments are segment_len + 32 ticks long, the rest segment_len; MAGUS_F_WALLCLOCK: ctas and
  * threads_per_cta of the wall-clock kernels, smem 0, solo_groups 0; otherwise the first launch group's CTA
  * shape; kernels_per_run = the library's kernel launches in one run, excluding the decision-dump
- * re-simulation; solo_groups = launch groups run by the one-warp-CTA kernel magus_replay_solo_kernel). */
+ * re-simulation; solo_groups = launch groups run by the one-warp-CTA kernel magus_replay_solo_kernel;
+ * wide_groups = launch groups run unsegmented by magus_replay_wide_kernel, one (trace, policy) chain per lane:
+ * many-policy sweeps, DESIGN.md section 9a -- then n_segments = 1 and there is no fix-up). */
 magus_status magus_replay_geometry(const magus_replay_t* h, int32_t out[16]);
 
 #ifdef __cplusplus

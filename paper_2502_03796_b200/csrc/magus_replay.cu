@@ -17,6 +17,7 @@
 #include "post_kernels.cuh"
 #include "replay_kernel.cuh"
 #include "replay_solo.cuh"
+#include "replay_wide.cuh"
 #include "wallclock.cuh"
 
 using namespace magus;
@@ -164,6 +165,21 @@ WallKernel wall_kernel_for(int key, int64_t n_chains, int n_sm) {
     return u ? wall_kernel_u<true>(key) : wall_kernel_u<false>(key);
 }
 
+// unsegmented one-chain-per-lane replay kernel (replay_wide.cuh) of a chain kind, or nullptr if it has none
+ReplayKernel wide_kernel_for(int key) {
+    switch (key) {
+        case 1: return magus_replay_wide_kernel<1>;
+        case 2: return magus_replay_wide_kernel<2>;
+        case 3: return magus_replay_wide_kernel<3>;
+        case 4: return magus_replay_wide_kernel<4>;
+        case 5: return magus_replay_wide_kernel<5>;
+        case 6: return magus_replay_wide_kernel<6>;
+        case 7: return magus_replay_wide_kernel<7>;
+        case 8: return magus_replay_wide_kernel<8>;
+        default: return nullptr;
+    }
+}
+
 // one-warp-CTA replay kernel (replay_solo.cuh) of a chain kind, or nullptr if it has none
 ReplayKernel solo_kernel_for(int key, bool sym, bool bits_ok) {
     int v = env_int("MAGUS_SOLO_BAL", 2);   // stage block variant (replay_solo.cuh)
@@ -218,6 +234,7 @@ struct LaunchGroup {
     int key, q_base, nq, ng, npw, n_tblocks, n_pblocks, n_ctas, threads;
     size_t smem;
     bool solo;   // one-warp CTAs (npw == 1 and the kind has a solo kernel)
+    bool wide;   // the unsegmented one-chain-per-lane kernel (replay_wide.cuh), fed by the 4-trace tensor map
 };
 
 // Kernel launch with programmatic stream serialization (PDL) when `pdl`: the kernel may be scheduled
@@ -473,6 +490,7 @@ struct magus_replay {
     cudaStream_t run_stream = nullptr;
     bool ran = false;
     CUtensorMap tmap{};
+    CUtensorMap tmap_w{};   // box {16 traces, 32 ticks}: the wide kernel's tiles
     const float* tmap_ptr = nullptr;
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};   // ev[4]: the run's completion
     static constexpr int kTimingRing = 256;
@@ -658,6 +676,47 @@ static void choose_geometry(magus_replay_t* h, int n_sm, int forced_segments) {
             cmax = std::max(cmax, q.C);
             p.kr = std::max(p.kr, q.k);
         }
+    }
+    // Unsegmented plan: when every launch group is a MAGUS kind with a wide kernel and one
+    // chain per lane already gives enough warps (>= MAGUS_WIDE_WARPS_PER_SM per SM, default 12; the lanes at least
+    // 3/4 used), replay each chain whole -- no speculation, no fix-up.  MAGUS_WIDE = 0 never, 1 whenever possible.
+    bool wide = forced_segments == 0 && d.tuning_segments == 0 && d.tuning_warmup == 0 && d.n_traces > 0;
+    {
+        int64_t warps = 0, lanes_used = 0, lanes_all = 0;   // lanes: policy points per trace, used / allotted
+        for (const LaunchGroup& g : h->groups) {
+            wide = wide && wide_kernel_for(g.key) != nullptr;
+            const int64_t pbs = (g.nq + kWidePpc - 1) / kWidePpc;
+            warps += pbs * ((d.n_traces + kWideTpc - 1) / kWideTpc) * kWideWarps;
+            lanes_used += g.nq;
+            lanes_all += pbs * kWidePpc;
+        }
+        const int mode = env_int("MAGUS_WIDE", -1);
+        if (mode == 0) wide = false;
+        else if (mode != 1)
+            wide = wide && warps >= (int64_t)n_sm * env_int("MAGUS_WIDE_WARPS_PER_SM", 12) && 4 * lanes_used >= 3 * lanes_all;
+    }
+    if (wide) {
+        p.n_seg = 1;
+        p.seg_len = std::max(1, d.n_samples);
+        p.seg_long = 0;
+        p.warmup = 0;
+        p.solo_warm = 8;
+        p.kr = 1;
+        for (const DevPolicy& q : h->lane) p.kr = std::max(p.kr, q.k);
+        p.n_blocks = (d.n_samples + 31) / 32;
+        for (LaunchGroup& g : h->groups) {
+            g.wide = true;
+            g.solo = false;
+            g.kernel = wide_kernel_for(g.key);
+            g.ng = 1;
+            g.npw = 1;
+            g.n_pblocks = (g.nq + kWidePpc - 1) / kWidePpc;
+            g.n_tblocks = (d.n_traces + kWideTpc - 1) / kWideTpc;
+            g.threads = kWideThreads;
+            g.smem = WideSmem::kBytes;
+            g.n_ctas = g.n_pblocks * g.n_tblocks;
+        }
+        return;
     }
     int W = d.tuning_warmup > 0 ? d.tuning_warmup
                                 : ((kmax + cmax - 1 + 31) / 32) * 32 + env_int("MAGUS_WARMUP_EXTRA", 0);
@@ -1165,6 +1224,11 @@ static magus_status encode_tmap(magus_replay_t* h, const float* d_trace) {
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(h, MAGUS_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    cuuint32_t box_w[2] = {(cuuint32_t)kWideTpc, (cuuint32_t)kWideTC};
+    r = enc(&h->tmap_w, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)d_trace, gdim, gstride, box_w, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(h, MAGUS_ERR_CUDA, "cuTensorMapEncodeTiled (wide) failed: " + std::to_string((int)r));
     h->tmap_ptr = d_trace;
     return MAGUS_OK;
 }
@@ -1249,7 +1313,7 @@ static magus_status enqueue_run(magus_replay_t* h, const float* d_trace, const f
             pg.n_tblocks = g.n_tblocks;
             pg.n_pblocks = g.n_pblocks;
             CU(h, launch_k(g.kernel, dim3((unsigned)g.n_ctas), dim3((unsigned)g.threads), g.smem, gs,
-                           h->pdl && G == 1 && !timing, h->tmap, pg));
+                           h->pdl && G == 1 && !timing, g.wide ? h->tmap_w : h->tmap, pg));
         }
         for (int g = 1; g < G; ++g) {
             CU(h, cudaEventRecord(h->join_ev[g - 1], h->aux[g - 1]));
@@ -1549,8 +1613,11 @@ extern "C" magus_status magus_replay_geometry(const magus_replay_t* h, int32_t o
         nk += 1 + nw;                                             // mark + one chain-walk kernel per launch group
     }
     nk += 1 + (h->xchg ? 1 : 0);                                  // totals (+ chunk sums before the allreduce)
-    int solo = 0;
-    for (const LaunchGroup& g : h->groups) solo += g.solo ? 1 : 0;
+    int solo = 0, wide = 0;
+    for (const LaunchGroup& g : h->groups) {
+        solo += g.solo ? 1 : 0;
+        wide += g.wide ? 1 : 0;
+    }
     int32_t threads = g0.threads, smem = (int32_t)g0.smem;
     if (h->wall) {   // the wall-clock kernels (A32): one 128-thread CTA per 128 chains of a launch group
         ctas = ((d.n_traces + 127) / 128) * p.n_lane;   // (the launch groups partition the lanes)
@@ -1559,7 +1626,7 @@ extern "C" magus_status magus_replay_geometry(const magus_replay_t* h, int32_t o
         solo = 0;
     }
     const int32_t v[16] = {p.n_seg, p.seg_len, p.warmup, g0.ng, g0.npw, g0.n_tblocks, g0.n_pblocks, ctas,
-                           threads, smem, p.n_lane, (int32_t)h->groups.size(), nk, solo, p.seg_long, 0};
+                           threads, smem, p.n_lane, (int32_t)h->groups.size(), nk, solo, p.seg_long, wide};
     std::memcpy(out, v, sizeof(v));
     return MAGUS_OK;
 }

@@ -478,7 +478,7 @@ __global__ void __launch_bounds__(32) magus_fix_lockstep_kernel(const ReplayPara
 // MAGUS_WALK_LOOKAHEAD: the split walk's stage block with both levels' decisions evaluated ahead of the level
 // (MAGUS_WSTAGE1L_K<K>: a short loop-carried dependency for the latency-bound walk), else MAGUS_WSTAGE1F_K<K>
 #ifndef MAGUS_WALK_LOOKAHEAD
-#define MAGUS_WALK_LOOKAHEAD 1
+#define MAGUS_WALK_LOOKAHEAD 0   // measured slower (cfg 3 fix-up 9.4 vs 6.6 ms, profiles/r02_walk_ab.txt)
 #endif
 template <int K>
 __device__ __forceinline__ void walk_stage1(MagusState<K, false>& st, float& lock, float& nthr, uint32_t& wcmd,

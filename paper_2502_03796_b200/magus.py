@@ -333,7 +333,7 @@ class Replay:
         _check(lib.magus_replay_geometry(self._h, g), self._h)
         keys = ["n_segments", "segment_len", "warmup_ticks", "tile_groups_per_cta", "policy_warps_per_group",
                 "trace_blocks", "policy_blocks", "ctas", "threads_per_cta", "smem_bytes", "lane_policies",
-                "launch_groups", "kernels_per_run", "solo_groups", "seg_long"]
+                "launch_groups", "kernels_per_run", "solo_groups", "seg_long", "wide_groups"]
         return dict(zip(keys, list(g)))
 
     def run(self, trace, w, stream=None):

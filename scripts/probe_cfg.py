@@ -49,7 +49,7 @@ def main():
         g = R.geometry()
         del R
         # the same plan without per-kernel timing events (every kernel edge programmatic)
-        R2 = M.Replay(n, ns, pols, M.Model(), trace_stride=stride, tuning_segments=res.n_segments)
+        R2 = M.Replay(n, ns, pols, M.Model(), trace_stride=stride, tuning_segments=S)
         for _ in range(3):
             R2.run(tr, w, stream)
             R2.results()

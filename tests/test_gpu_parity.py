@@ -156,6 +156,58 @@ def test_window_and_log_sizes(M, k, C, hf):
     assert np.array_equal(res.words, PA.pack_words(codes))
 
 
+WIDE_CASES = {
+    # config 3's 64-point sweep (k in {1, 2, 4, 8}: four launch groups of 16 points) + static max
+    "cfg3-small": (SMALL["cfg3-small"]["policies"], 64, 4_000, 1),
+    # every register-ring k, logs up to C = 28, 3 points per group (13 idle lanes per 16), a ragged trace count
+    # and a ragged last block
+    "k1-8": ([pol(deriv_ticks=k, tune_log_capacity=C, high_freq_threshold=hf, inc_threshold=th, dec_threshold=-th)
+              for k in range(1, 9) for (C, hf, th) in ((10, 0.6, 1.0), (28, 0.5, 0.5), (3, 0.7, 2.0))],
+             133, 5_003, 3),
+    # shorter than the warm-up of the longest log (k + C - 1 > n_samples) and a single partial block
+    "short": ([pol(deriv_ticks=k, tune_log_capacity=28) for k in (1, 4, 8)] + [pol(kind=STATIC_MAX)], 21, 33, 1),
+}
+
+
+@pytest.mark.parametrize("model", ["linear", "saturating", "open-loop"])
+@pytest.mark.parametrize("name", list(WIDE_CASES))
+def test_wide_unsegmented_plan(M, name, model, monkeypatch):
+    """The unsegmented one-chain-per-lane plan (magus_replay_wide_kernel), forced with
+    MAGUS_WIDE=1: records, every tick's cmd / tune-flag word, a decision dump and the totals against the oracle,
+    under the Linear and Saturating bandwidth models and the open-loop observation (A30)."""
+    monkeypatch.setenv("MAGUS_WIDE", "1")
+    pols, n, ns, mix = WIDE_CASES[name]
+    stride = (n + 3) // 4 * 4
+    tr, w = gpu_gen(M, 31 + n, n, ns, mix, stride)
+    gm = dict(linear=(M.Model(), O.Model()), saturating=(M.Model(bw_shape=1, bw_knee=0.5), O.Model(bw_shape=1, bw_knee=0.5)),
+              **{"open-loop": (M.Model(observe=1), O.Model(observe=1))})[model]
+    res = run_gpu(M, tr, w, pols, n, ns, stride, dump=(n - 3, 3), model=gm[0])
+    geo = res.geometry
+    assert geo["wide_groups"] == geo["launch_groups"] and res.n_segments == 1, geo
+    rec, codes = oracle_run(tr.cpu().numpy(), w.cpu().numpy(), pols, n, model=gm[1])
+    PA.compare_records(res.per_trace, rec, f"wide {name} {model}")
+    assert np.array_equal(res.words, PA.pack_words(codes))
+    assert np.array_equal(res.decisions, codes[:, n - 3:, :])
+    PA.compare_totals(res.totals, rec)
+    edp = PA.oracle_totals(rec)[:, 3]
+    assert res.totals[res.argmin_policy, 3] <= edp.min() * (1 + 1e-9)
+
+
+def test_wide_plan_choice(M, monkeypatch):
+    """The automatic plan picks the unsegmented kernel for config 3's sweep (65,536 chains) and the segmented
+    solo kernel for config 2 (4,096 chains); MAGUS_WIDE=0 turns it off."""
+    for ci, want in ((3, 4), (2, 0)):
+        c = CONFIGS[ci]
+        with M.Replay(c["n_traces"], c["n_samples"], PA.gpu_policies(c["policies"]), trace_stride=c["stride"]) as R:
+            g = R.geometry()
+        assert g["wide_groups"] == want, (ci, g)
+        assert (g["n_segments"] == 1) == (want > 0), (ci, g)
+    monkeypatch.setenv("MAGUS_WIDE", "0")
+    c = CONFIGS[3]
+    with M.Replay(c["n_traces"], c["n_samples"], PA.gpu_policies(c["policies"]), trace_stride=c["stride"]) as R:
+        assert R.geometry()["wide_groups"] == 0
+
+
 @pytest.mark.parametrize("n,ns", [(1, 1), (1, 31), (3, 33), (5, 32), (128, 64), (129, 95), (4, 1000)])
 def test_tiny_and_ragged(M, n, ns):
     stride = (n + 3) // 4 * 4
