@@ -166,18 +166,20 @@ WallKernel wall_kernel_for(int key, int64_t n_chains, int n_sm) {
 }
 
 // unsegmented one-chain-per-lane replay kernel (replay_wide.cuh) of a chain kind, or nullptr if it has none
-ReplayKernel wide_kernel_for(int key) {
+ReplayKernel wide_kernel_for(int key, int nc) {
+#define WIDE_K(KK) (nc == 1 ? (ReplayKernel)magus_replay_wide_kernel<KK, 1> : (ReplayKernel)magus_replay_wide_kernel<KK, 2>)
     switch (key) {
-        case 1: return magus_replay_wide_kernel<1>;
-        case 2: return magus_replay_wide_kernel<2>;
-        case 3: return magus_replay_wide_kernel<3>;
-        case 4: return magus_replay_wide_kernel<4>;
-        case 5: return magus_replay_wide_kernel<5>;
-        case 6: return magus_replay_wide_kernel<6>;
-        case 7: return magus_replay_wide_kernel<7>;
-        case 8: return magus_replay_wide_kernel<8>;
+        case 1: return WIDE_K(1);
+        case 2: return WIDE_K(2);
+        case 3: return WIDE_K(3);
+        case 4: return WIDE_K(4);
+        case 5: return WIDE_K(5);
+        case 6: return WIDE_K(6);
+        case 7: return WIDE_K(7);
+        case 8: return WIDE_K(8);
         default: return nullptr;
     }
+#undef WIDE_K
 }
 
 // one-warp-CTA replay kernel (replay_solo.cuh) of a chain kind, or nullptr if it has none
@@ -684,7 +686,7 @@ static void choose_geometry(magus_replay_t* h, int n_sm, int forced_segments) {
     {
         int64_t warps = 0, lanes_used = 0, lanes_all = 0;   // lanes: policy points per trace, used / allotted
         for (const LaunchGroup& g : h->groups) {
-            wide = wide && wide_kernel_for(g.key) != nullptr;
+            wide = wide && wide_kernel_for(g.key, 1) != nullptr;
             const int64_t pbs = (g.nq + kWidePpc - 1) / kWidePpc;
             warps += pbs * ((d.n_traces + kWideTpc - 1) / kWideTpc) * kWideWarps;
             lanes_used += g.nq;
@@ -707,12 +709,15 @@ static void choose_geometry(magus_replay_t* h, int n_sm, int forced_segments) {
         for (LaunchGroup& g : h->groups) {
             g.wide = true;
             g.solo = false;
-            g.kernel = wide_kernel_for(g.key);
+            // chains per thread: 1; MAGUS_WIDE_NC=2: two policy points sharing the samples (7% fewer instructions,
+            // but measured slower: cfg 3 10.7 vs 7.0 ms, profiles/r02_cfg3_wide.txt)
+            const int nc = env_int("MAGUS_WIDE_NC", 1) == 2 ? 2 : 1;
+            g.kernel = wide_kernel_for(g.key, nc);
             g.ng = 1;
             g.npw = 1;
             g.n_pblocks = (g.nq + kWidePpc - 1) / kWidePpc;
             g.n_tblocks = (d.n_traces + kWideTpc - 1) / kWideTpc;
-            g.threads = kWideThreads;
+            g.threads = kWideThreads / nc;
             g.smem = WideSmem::kBytes;
             g.n_ctas = g.n_pblocks * g.n_tblocks;
         }

@@ -73,22 +73,70 @@ __device__ __forceinline__ void wide_stage(MagusState<K, false>& st, float& lock
     st.evh = e0;
 }
 
-// MAGUS chains with a register ring of K <= 8 values and a 32-bit tune log (C <= 28).  Launch: one 256-thread CTA
-// per (16-trace column, block of 16 policy points), policy blocks fastest; p.n_pblocks = ceil(nq / 16).
+// 8 ticks of two chains of one trace (two policy points) sharing the samples (MAGUS_WSTAGE2P_K<K>)
 template <int K>
-__global__ void __launch_bounds__(kWideThreads, 2)
+__device__ __forceinline__ void wide_stage2(MagusState<K, false>* st, float* lock, float* nthr, uint32_t* wcmd,
+                                            double* sexc, const float* d8, const DevPolicy* pol, float B_lo,
+                                            double Blo_d, const uint32_t* bitc, uint32_t mone) {
+    uint32_t e0 = st[0].evh, e1 = st[1].evh;
+#define WD2_TAIL                                                                                                 \
+    e0, e1, st[0].cnt, st[1].cnt, sexc[0], sexc[1], lock[0], lock[1], nthr[0], nthr[1], wcmd[0], wcmd[1],         \
+        __float_as_uint(d8[0]), __float_as_uint(d8[1]), __float_as_uint(d8[2]), __float_as_uint(d8[3]),             \
+        __float_as_uint(d8[4]), __float_as_uint(d8[5]), __float_as_uint(d8[6]), __float_as_uint(d8[7]), B_lo,      \
+        Blo_d, pol[0].dinc, pol[1].dinc, pol[0].ddec, pol[1].ddec, bitc[0], bitc[1], pol[0].smin_sc, pol[1].smin_sc, \
+        pol[0].one, mone
+#define R0(i) st[0].ring.v[i]
+#define R1(i) st[1].ring.v[i]
+    if constexpr (K == 1) MAGUS_WSTAGE2P_K1(st[0].f, st[1].f, R0(0), R1(0), WD2_TAIL);
+    else if constexpr (K == 2) MAGUS_WSTAGE2P_K2(st[0].f, st[1].f, R0(0), R0(1), R1(0), R1(1), WD2_TAIL);
+    else if constexpr (K == 3) MAGUS_WSTAGE2P_K3(st[0].f, st[1].f, R0(0), R0(1), R0(2), R1(0), R1(1), R1(2), WD2_TAIL);
+    else if constexpr (K == 4)
+        MAGUS_WSTAGE2P_K4(st[0].f, st[1].f, R0(0), R0(1), R0(2), R0(3), R1(0), R1(1), R1(2), R1(3), WD2_TAIL);
+    else if constexpr (K == 5)
+        MAGUS_WSTAGE2P_K5(st[0].f, st[1].f, R0(0), R0(1), R0(2), R0(3), R0(4), R1(0), R1(1), R1(2), R1(3), R1(4),
+                          WD2_TAIL);
+    else if constexpr (K == 6)
+        MAGUS_WSTAGE2P_K6(st[0].f, st[1].f, R0(0), R0(1), R0(2), R0(3), R0(4), R0(5), R1(0), R1(1), R1(2), R1(3),
+                          R1(4), R1(5), WD2_TAIL);
+    else if constexpr (K == 7)
+        MAGUS_WSTAGE2P_K7(st[0].f, st[1].f, R0(0), R0(1), R0(2), R0(3), R0(4), R0(5), R0(6), R1(0), R1(1), R1(2),
+                          R1(3), R1(4), R1(5), R1(6), WD2_TAIL);
+    else
+        MAGUS_WSTAGE2P_K8(st[0].f, st[1].f, R0(0), R0(1), R0(2), R0(3), R0(4), R0(5), R0(6), R0(7), R1(0), R1(1),
+                          R1(2), R1(3), R1(4), R1(5), R1(6), R1(7), WD2_TAIL);
+#undef R0
+#undef R1
+#undef WD2_TAIL
+    st[0].evh = e0;
+    st[1].evh = e1;
+}
+
+// MAGUS chains with a register ring of K <= 8 values and a 32-bit tune log (C <= 28).  NC = chains per thread: 1, or
+// 2 = two policy points of the same trace sharing the samples (one shared-memory load, fp32 -> fp64 conversion and
+// validation maximum per tick for both).  Launch: one (256 / NC)-thread CTA per (16-trace column, block of 16 policy
+// points), policy blocks fastest; p.n_pblocks = ceil(nq / 16).
+template <int K, int NC>
+__global__ void __launch_bounds__(kWideThreads / NC, 2)
     magus_replay_wide_kernel(const __grid_constant__ CUtensorMap tmap, const ReplayParams p) {
+    static_assert(NC == 1 || NC == 2, "wide kernel: one or two chains per thread");
     using T = MagusTicker<K, false>;
     constexpr uint32_t kTileBytes = WideSmem::kTileBytes;
+    constexpr int kWarps = kWideWarps / NC;
+    constexpr int kPerTrace = kWidePpc / NC;   // threads per trace
     extern __shared__ __align__(1024) uint8_t smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int pb = blockIdx.x % p.n_pblocks;
     const int x = (blockIdx.x / p.n_pblocks) * kWideTpc;
-    const int qi = pb * kWidePpc + (tid % kWidePpc);
-    const int jl = tid / kWidePpc;
+    const int jl = tid / kPerTrace;
     const int j = x + jl;
-    const bool live = qi < p.nq && j < p.n_traces;
-    const int q = p.q_base + (qi < p.nq ? qi : p.nq - 1);   // idle lanes replay a live point, unrecorded
+    int q[NC];
+    bool live[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        const int qi = pb * kWidePpc + (tid % kPerTrace) * NC + c;
+        live[c] = qi < p.nq && j < p.n_traces;
+        q[c] = p.q_base + (qi < p.nq ? qi : p.nq - 1);   // idle chains replay a live point, unrecorded
+    }
 
     const uint32_t tile0 = ptx::smem_u32(smem);
     const uint32_t full0 = tile0 + kWideNStage * kTileBytes, empty0 = full0 + 8 * kWideNStage;
@@ -99,7 +147,7 @@ __global__ void __launch_bounds__(kWideThreads, 2)
             ptx::prefetch_tmap(&tmap);
             for (int i = 0; i < kWideNStage; ++i) {
                 asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full0 + 8 * i) : "memory");
-                asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(empty0 + 8 * i), "r"(kWideWarps) : "memory");
+                asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(empty0 + 8 * i), "r"(kWarps) : "memory");
             }
             ptx::fence_mbar_init();
         }
@@ -110,18 +158,24 @@ __global__ void __launch_bounds__(kWideThreads, 2)
     __syncthreads();   // the barriers are initialised before any warp waits on them
     ptx::pdl_wait();   // the pre-pass zeroes the run's flag words (launched just before)
 
-    const DevPolicy pol = p.pol[q];
+    DevPolicy pol[NC];
+    uint32_t bitc[NC];
+    typename T::State st[NC];
+    SegStats ss[NC];
+    float lockf[NC], nthrf[NC];   // per-block counts from the stage block (exact fp32 integers <= 32)
+    int warm = 0;                 // ticks before Alg. 1 / Alg. 2 are defined for every chain (A7, A8): per-tick path
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        pol[c] = p.pol[q[c]];
+        bitc[c] = 1u << (pol[c].C - 1);
+        warm = max(warm, pol[c].k + pol[c].C - 1);
+        T::init(st[c], pol[c], true);   // the exact initial state (A10): no speculation
+        ss[c].zero();
+        lockf[c] = nthrf[c] = 0.f;
+    }
     const float B_lo = p.B_lo, B_hi = p.B_hi;
     const double Blo_d = (double)B_lo;
-    const uint32_t bitc = 1u << (pol.C - 1), mone = 0xFFFFFFFFu * pol.one;
-    const int k = pol.k, C = pol.C;
-    const int warm = k + C - 1;   // ticks before Alg. 1 / Alg. 2 are both defined (A7, A8): per-tick path
-
-    typename T::State st;
-    T::init(st, pol, true);   // the exact initial state (A10): no speculation
-    SegStats ss;
-    ss.zero();
-    float lockf = 0.f, nthrf = 0.f;   // per-block counts from the stage block (exact fp32 integers <= 32)
+    const uint32_t mone = 0xFFFFFFFFu * pol[0].one;
     uint32_t vmax = 0;
     int slot = 0;
     uint32_t phase = 0;
@@ -131,8 +185,12 @@ __global__ void __launch_bounds__(kWideThreads, 2)
         const int n = min(kWideTC, N - bt0);
         mbar_wait_loop(full0 + 8 * slot, phase);
         const float* colp = reinterpret_cast<const float*>(smem + slot * kTileBytes) + jl;   // stride 16 floats
-        const uint32_t fstart = T::level(st);
-        uint32_t wcmd = 0;
+        uint32_t fstart[NC], wcmd[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            fstart[c] = T::level(st[c]);
+            wcmd[c] = 0;
+        }
         if (n == kWideTC && bt0 >= warm) {
 #pragma unroll
             for (int g = 0; g < kWideTC / 8; ++g) {
@@ -143,7 +201,14 @@ __global__ void __launch_bounds__(kWideThreads, 2)
                                          max(__float_as_uint(d8[2]), __float_as_uint(d8[3]))),
                                      max(max(__float_as_uint(d8[4]), __float_as_uint(d8[5])),
                                          max(__float_as_uint(d8[6]), __float_as_uint(d8[7])))));
-                wide_stage<K>(st, lockf, nthrf, wcmd, ss.sexc, d8, pol, B_lo, Blo_d, bitc, mone);
+                if constexpr (NC == 1)
+                    wide_stage<K>(st[0], lockf[0], nthrf[0], wcmd[0], ss[0].sexc, d8, pol[0], B_lo, Blo_d, bitc[0], mone);
+                else {
+                    double sx[2] = {ss[0].sexc, ss[1].sexc};
+                    wide_stage2<K>(st, lockf, nthrf, wcmd, sx, d8, pol, B_lo, Blo_d, bitc, mone);
+                    ss[0].sexc = sx[0];
+                    ss[1].sexc = sx[1];
+                }
             }
         } else {
             // warm-up block (Alg. 1 / Alg. 2 gated per tick) or the ragged last block of the trace
@@ -151,9 +216,13 @@ __global__ void __launch_bounds__(kWideThreads, 2)
             for (int tt = 0; tt < n; ++tt) {
                 const float D = colp[tt * kWideTpc];
                 const int t = bt0 + tt;
-                const TickOut o = T::template tick<true>(st, D, pol, B_lo, B_hi, t >= k, t >= warm);
-                wcmd = (wcmd << 1) | o.cmd;
-                acc_tick(ss, vmax, o, D, B_lo);
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    const TickOut o = T::template tick<true>(st[c], D, pol[c], B_lo, B_hi, t >= pol[c].k,
+                                                             t >= pol[c].k + pol[c].C - 1);
+                    wcmd[c] = (wcmd[c] << 1) | o.cmd;
+                    acc_tick(ss[c], vmax, o, D, B_lo);
+                }
             }
         }
         // release the stage; warp 0 refills it with stage i + NSTAGE once all warps have released it
@@ -167,17 +236,24 @@ __global__ void __launch_bounds__(kWideThreads, 2)
             slot = 0;
             phase ^= 1u;
         }
-        ss.lock += (uint32_t)lockf;
-        ss.nthr += (uint32_t)nthrf;
-        lockf = nthrf = 0.f;
-        uint32_t* wout = (p.words && live) ? p.words + ((int64_t)chain_idx(p, q, j) * p.n_blocks + i) * 2 : nullptr;
-        if (n == kWideTC) fold_full_block(ss, wcmd, (uint32_t)st.evh, fstart, p.dkeys[i], wout);
-        else fold_block(ss, wcmd, (uint32_t)st.evh, fstart, n, i, wout);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            ss[c].lock += (uint32_t)lockf[c];
+            ss[c].nthr += (uint32_t)nthrf[c];
+            lockf[c] = nthrf[c] = 0.f;
+            uint32_t* wout =
+                (p.words && live[c]) ? p.words + ((int64_t)chain_idx(p, q[c], j) * p.n_blocks + i) * 2 : nullptr;
+            if (n == kWideTC) fold_full_block(ss[c], wcmd[c], (uint32_t)st[c].evh, fstart[c], p.dkeys[i], wout);
+            else fold_block(ss[c], wcmd[c], (uint32_t)st[c].evh, fstart[c], n, i, wout);
+        }
     }
-    if (live) {
-        add_to_chain(p, q, j, ss.nhi, ss.nthr, ss.trans, ss.ev, ss.lock, ss.sexc, ss.digest());
-        atomicMax(p.c_vmax + chain_idx(p, q, j), vmax);
-    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+        if (live[c]) {
+            add_to_chain(p, q[c], j, ss[c].nhi, ss[c].nthr, ss[c].trans, ss[c].ev, ss[c].lock, ss[c].sexc,
+                         ss[c].digest());
+            atomicMax(p.c_vmax + chain_idx(p, q[c], j), vmax);
+        }
 }
 
 }  // namespace magus

@@ -584,6 +584,74 @@ def build_stage_wl(K, TC=8):
     return out
 
 
+def build_stage_w2(K, TC=8):
+    """MAGUS_WSTAGE2P_K<K>: TC ticks of TWO MAGUS chains of one trace under two different policy points of the same
+    chain kind (the wide kernel, replay_wide.cuh), samples passed in registers: the fp32 -> fp64 conversion is
+    shared, every threshold (d*_inc, d*_dec, the scaled Alg. 2 threshold and leaving-flag bit) is per chain.
+    Per chain-tick the operations and their order are MAGUS_WSTAGE1F_K<K>'s (decisions identical)."""
+    C = 2
+    names = [(f"f{c}", "+r") for c in range(C)] + \
+            [(f"r{c}_{i}", "+d") for c in range(C) for i in range(K)] + \
+            [(f"evh{c}", "+r") for c in range(C)] + [(f"cnt{c}", "+r") for c in range(C)] + \
+            [(f"exc{c}", "+d") for c in range(C)] + [(f"lock{c}", "+f") for c in range(C)] + \
+            [(f"nthr{c}", "+f") for c in range(C)] + [(f"wcmd{c}", "+r") for c in range(C)]
+    inames = [(f"S{tt}", "r") for tt in range(TC)] + [("Blo", "f"), ("Blod", "d")] + \
+             [(f"dinc{c}", "d") for c in range(C)] + [(f"ddec{c}", "d") for c in range(C)] + \
+             [(f"bitc{c}", "r") for c in range(C)] + [(f"smin{c}", "r") for c in range(C)] + [("one", "r"), ("mone", "r")]
+    idx = {n: f"%{i}" for i, (n, _) in enumerate(names + inames)}
+    R = idx.__getitem__
+    body = ["{", ".reg .pred phi<2>, pthr<2>, pinc<2>, pev<2>, phf<2>, pq<2>, pk<2>;",
+            f".reg .f64 dd, dv<2>, dx<2>, ad<{TC * C}>;", ".reg .b32 tb<2>;"]
+    for c in range(C):
+        body.append(f"setp.ne.u32 phi{c}, {R(f'f{c}')}, 0;")
+    for tt in range(TC):
+        body.append(f"cvt.f64.f32 dd, {R(f'S{tt}')};")                # shared by the two chains
+        per_chain = [
+            "setp.gt.and.f32 pthr{c}, {D}, {Blo}, !phi{c};",             # throttled: f_min and D > B_lo (A14)
+            "selp.f64 {ad}, {Blod}, dd, pthr{c};",                       # A = min(D, B[f]) as fp64 (exact)
+            "sub.f64 dv{c}, {ad}, {old};",                               # Alg. 1 numerator A_t - A_{t-k} (P:207)
+            "setp.gt.f64 pinc{c}, dv{c}, {dinc};",                       # +1 (P:209)
+            "setp.lt.or.f64 pev{c}, dv{c}, {ddec}, pinc{c};",            # tune flag (P:213, P:243)
+            "and.b32 tb{c}, {evh}, {bitc};",                             # the flag leaving the C-window (scaled)
+            "shl.b32 {evh}, {evh}, 1;",
+            "@pev{c} mad.lo.u32 {evh}, {one}, {one}, {evh};",
+            "mad.lo.u32 {cnt}, tb{c}, {mone}, {cnt};",                   # window count: - leaving + entering
+            "@pev{c} mad.lo.u32 {cnt}, {bitc}, {one}, {cnt};",
+            "setp.ge.u32 phf{c}, {cnt}, {smin};",                        # Alg. 2 (P:230)
+            "not.pred pk{c}, pev{c};",
+            "and.pred pk{c}, pk{c}, phi{c};",
+            "or.pred pq{c}, pk{c}, pinc{c};",                            # +1 || (f_max && !flag)
+            "or.pred phi{c}, pq{c}, phf{c};",                            # || lock: the new level
+            "shl.b32 {wcmd}, {wcmd}, 1;",
+            "@phi{c} mad.lo.u32 {wcmd}, {one}, {one}, {wcmd};",
+            "sub.f64 dx{c}, dd, {ad};",                                  # throttling excess D - A (0 unless thr)
+            "add.f64 {exc}, {exc}, dx{c};",
+            "@phf{c} add.f32 {lock}, {lock}, 0f3F800000;",
+            "@pthr{c} add.f32 {nthr}, {nthr}, 0f3F800000;",
+        ]
+        for tmpl in per_chain:
+            for c in range(C):
+                t = tt * C + c
+                old = f"ad{(tt - K) * C + c}" if tt >= K else R(f"r{c}_{K - 1 - tt}")
+                body.append(tmpl.format(c=c, D=R(f"S{tt}"), ad=f"ad{t}", old=old, Blod=R("Blod"), Blo=R("Blo"),
+                                        dinc=R(f"dinc{c}"), ddec=R(f"ddec{c}"), evh=R(f"evh{c}"), one=R("one"),
+                                        bitc=R(f"bitc{c}"), mone=R("mone"), cnt=R(f"cnt{c}"), smin=R(f"smin{c}"),
+                                        wcmd=R(f"wcmd{c}"), exc=R(f"exc{c}"), lock=R(f"lock{c}"), nthr=R(f"nthr{c}")))
+    for c in range(C):
+        body.append(f"selp.u32 {R(f'f{c}')}, 1, 0, phi{c};")
+        for i in range(K):   # ring newest first: r_i = A_{t0 + TC - 1 - i}
+            body.append(f"mov.f64 {R(f'r{c}_{i}')}, ad{(TC - 1 - i) * C + c};")
+    body.append("}")
+    params = ", ".join(n for n, _ in names + inames)
+    name = f"MAGUS_WSTAGE2P_K{K}"
+    out = [f"#define {name}(...) {name}_(__VA_ARGS__)", f"#define {name}_({params}) \\", "    asm volatile( \\"]
+    out += [f'        "{l}\\n\\t" \\' for l in body]
+    out.append("        : " + ", ".join(f'"{c}"({n})' for n, c in names) + " \\")
+    out.append("        : " + ", ".join(f'"{c}"({n})' for n, c in inames) + " \\")
+    out.append('        : "memory")')
+    return out
+
+
 out = ["// GENERATED by scripts/gen_tick4.py -- do not edit.  One MAGUS tick for the 4 chains of a lane, the",
        "// four chains' instructions interleaved (DESIGN.md section 7); semantics = magus_tick<K, false, SLOW>.",
        "// cnt is the window count scaled by 2^(C-1).",
@@ -609,6 +677,8 @@ for NP in (1, 2):
     out += [""] + build_stage_t(NP)
 for K in range(1, 9):
     out += [""] + build_stage_wl(K)
+for K in range(1, 9):
+    out += [""] + build_stage_w2(K)
 path = os.path.join(os.path.dirname(__file__), "..", "paper_2502_03796_b200", "csrc", "tick4_asm.cuh")
 open(path, "w").write("\n".join(out) + "\n")
 print("wrote", os.path.normpath(path))
