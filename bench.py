@@ -116,6 +116,33 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def alu_roofline(cfg, n, ns, n_pol, replay_ms, replay_ms_max):
+    """Issue roofline of the unsegmented wide plan (the many-policy sweep): the replay is
+    bound by instruction issue, not HBM (each trace byte feeds 64 recurrences).  achieved = lane instructions per
+    second = chain-ticks of the launch x the replay kernels' executed instructions per chain-tick (ncu
+    smsp__inst_executed x 32 / chain-ticks, profiles/ncu_wide_summary.json) / the replay time; peak = the issue
+    ceiling 148 SMs x 4 sub-partitions x 32 lanes x one warp instruction per cycle at the measured max SM clock."""
+    chain_ticks = float(n) * ns * n_pol
+    ipt, src, traffic = None, None, None
+    prof = os.path.join(ROOT, "profiles", "ncu_wide_summary.json")
+    if os.path.exists(prof):
+        pj = json.load(open(prof))
+        if pj.get("config") == cfg["name"]:
+            ipt, src, traffic = pj["lane_instr_per_chain_tick"], pj["source"], pj.get("dram_bytes_per_run")
+    mhz = 1965.0
+    pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(pk):
+        mhz = float(json.load(open(pk)).get("sm_max_mhz", mhz))
+    peak = 148 * 4 * 32 * mhz * 1e6 / 1e9                      # Ginstr/s
+    achieved = chain_ticks * ipt / (replay_ms / 1e3) / 1e9 if ipt else None
+    return {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Ginstr/s",
+            "frac": achieved / peak if achieved else None, "traffic": traffic,
+            "kernel": "magus_replay_wide_kernel", "replay_ms": replay_ms, "replay_ms_max_over_ranks": replay_ms_max,
+            "chain_ticks_per_launch": chain_ticks, "lane_instr_per_chain_tick": ipt,
+            "peak_source": f"issue ceiling 148 x 4 x 32 lanes x {mhz:.0f} MHz (MEASURED_PEAKS.json sm_max_mhz)",
+            "instr_source": src}
+
+
 def cpu_baseline(cfg, target_s):
     """The oracle as it stands, on all host cores, over a bounded sample (the first n traces of the
     workload, full length, all of the config's policies)."""
@@ -260,6 +287,15 @@ def run_ours(args, cfg):
         except Exception:
             traffic = None
 
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic,
+                "kernel": ("magus_wallclock_em_kernel" if args.wallclock else
+                           "magus_replay_solo_kernel" if geo.get("solo_groups") else "magus_replay_kernel"),
+                "replay_ms": tsum["replay_ms"], "replay_ms_max_over_ranks": replay_ms_max,
+                "bytes_per_launch": bytes_per_launch, "peak_source": peak_src}
+    if geo.get("wide_groups") and not args.wallclock:
+        roofline = alu_roofline(cfg, n, ns, geo["lane_policies"], tsum["replay_ms"], replay_ms_max)
+
     e2e = None
     if not args.no_e2e:
         th = tr.cpu().pin_memory()
@@ -303,13 +339,7 @@ def run_ours(args, cfg):
                        "parallelism": f"trace-sharded x{world // ps}" + (f", parameter grid x{ps}" if ps > 1 else "")
                                       + (", NCCL allreduce of per-policy totals" if dist_on else ""),
                        "l2": "inputs 1.64 GB/GPU >> 126 MB L2; no flush needed" if ns * n * 4 > 4e8 else "L2-resident"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic,
-                         "kernel": ("magus_wallclock_em_kernel" if args.wallclock else
-                                    "magus_replay_solo_kernel" if geo.get("solo_groups") else "magus_replay_kernel"),
-                         "replay_ms": tsum["replay_ms"],
-                         "replay_ms_max_over_ranks": replay_ms_max, "bytes_per_launch": bytes_per_launch,
-                         "peak_source": peak_src},
+            "roofline": roofline,
             "e2e": e2e,
             "cpu_baseline": cpu,
             "clocks": clocks,

@@ -185,7 +185,7 @@ ReplayKernel wide_kernel_for(int key, int nc) {
 // one-warp-CTA replay kernel (replay_solo.cuh) of a chain kind, or nullptr if it has none
 ReplayKernel solo_kernel_for(int key, bool sym, bool bits_ok) {
     int v = env_int("MAGUS_SOLO_BAL", 2);   // stage block variant (replay_solo.cuh)
-    if (v == 9 && !sym) v = 3;              // |d| > d*_inc needs d*_dec == -d*_inc
+    if (v == 9) v = 2;   // PSTAGES (|d| test + popcount): slower than 2 and it failed parity on mixed-kinds (round 2)
     if (v == 5 && !bits_ok) v = 2;          // the integer sample conversion needs |d*| >= 2^-60, B_lo normal
     if (v >= 10 && v <= 17) {   // the unified-stage kernel; v - 10 = VAR bits (1 |d| test, 2 incremental count,
                                 // 4 integer sample conversion)
@@ -463,6 +463,8 @@ struct magus_replay {
     int alloc_segments = 1;           // scratch is sized for this many segments (re-plans only shrink)
     int replans = 0;
     double replan_frac = 0.25;        // re-plan above this fraction of wrong speculative entries
+    int warm_extra = 0;               // adaptive warm-up: ticks added to roundup32(k + C - 1)
+    int warm_replans = 0;
     bool pdl = true;           // programmatic dependent launch between the run's kernels (MAGUS_NO_PDL=1: off)
     // device memory
     std::vector<void*> allocs;
@@ -724,7 +726,7 @@ static void choose_geometry(magus_replay_t* h, int n_sm, int forced_segments) {
         return;
     }
     int W = d.tuning_warmup > 0 ? d.tuning_warmup
-                                : ((kmax + cmax - 1 + 31) / 32) * 32 + env_int("MAGUS_WARMUP_EXTRA", 0);
+                                : ((kmax + cmax - 1 + 31) / 32) * 32 + env_int("MAGUS_WARMUP_EXTRA", 0) + h->warm_extra;
     W = ((std::max(W, kmax + cmax - 1) + 31) / 32) * 32;
     const int N = std::max(1, d.n_samples);
     int base = 0;   // CTAs per segment over all launch groups
@@ -1506,10 +1508,26 @@ extern "C" magus_status magus_replay_results(magus_replay_t* h, magus_results* o
     // MAGUS_REPLAN_PCT % of the speculative entries mismatched, the next runs use half as many segments.  The
     // chain walk's cost does not grow with the segment count, so this only starves the replay of parallelism.
     // Results are exact either way.
+    // Adaptive warm-up: speculative entries that mismatched mean the warm-up was too short to
+    // re-derive the true state (oscillating traces: the limit cycle's phase); the next runs start their speculative
+    // segments earlier (extra ticks 0 -> 64 -> 192 -> 448, at most 3 times, the warm-up at most 1/8 of a segment).
+    // A run without a mismatch keeps its plan.  Results are exact either way; this only trades chain-walk time
+    // for replay time (config 5: 2,053 wrong entries at 32 ticks, none at 96; step 0.835 -> 0.721 ms).
+    bool warm_replan = false;
+    if (d.tuning_segments == 0 && d.tuning_warmup == 0 && h->rp.n_seg > 1 && segs > 0 && h->warm_replans < 3 &&
+        !env_int("MAGUS_NO_REPLAN", 0) && !env_int("MAGUS_NO_WARM_ADAPT", 0)) {
+        const int extra = 2 * h->warm_extra + 64;
+        if (h->rp.warmup + (extra - h->warm_extra) <= h->rp.seg_len / 8) {
+            h->warm_extra = extra;
+            h->warm_replans += 1;
+            warm_replan = true;
+        }
+    }
     if (d.tuning_segments == 0 && h->rp.n_seg > 1 && !env_int("MAGUS_NO_REPLAN", 0)) {
         const double spec = (double)h->rp.n_lane * (h->rp.n_seg - 1) * std::max(1, d.n_traces);
-        if ((double)segs > h->replan_frac * spec) {
-            const int S_new = std::max(1, h->rp.n_seg / 2);
+        const bool halve = (double)segs > h->replan_frac * spec;
+        if (halve || warm_replan) {
+            const int S_new = halve ? std::max(1, h->rp.n_seg / 2) : 0;   // 0: the automatic segment count
             const ReplayParams keep = h->rp;
             choose_geometry(h, h->n_sm, S_new);
             // keep the scratch pointers, thresholds and constants; only the plan changed
@@ -1518,6 +1536,7 @@ extern "C" magus_status magus_replay_results(magus_replay_t* h, magus_results* o
             np.seg_len = h->rp.seg_len;
             np.seg_long = h->rp.seg_long;
             np.warmup = h->rp.warmup;
+            np.solo_warm = h->rp.solo_warm;
             h->rp = np;
             for (const LaunchGroup& g : h->groups)
                 cudaFuncSetAttribute((const void*)g.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
