@@ -43,6 +43,7 @@ struct ReplayParams {
     int32_t n_traces, n_samples;
     int32_t n_lane;        // Q lane policies (state / statistics arrays are indexed by lane 0..Q-1)
     int32_t q_base, nq;    // lanes covered by the current replay launch (all of one chain kind)
+    int32_t q_base2, nq2;  // magus_replay_combo_kernel: the TDP group replayed next to the MAGUS group q_base / nq
     int32_t n_seg, seg_len, warmup;
     int32_t seg_long;      // the first seg_long segments are seg_len + 32 ticks long (CTA balance), the rest seg_len
     int32_t n_groups;      // ceil(n_traces / 128)

@@ -182,6 +182,19 @@ ReplayKernel wide_kernel_for(int key, int nc) {
 #undef WIDE_K
 }
 
+// the two-warp MAGUS + TDP kernel (replay_solo.cuh) for a MAGUS chain kind with a solo stage block and np TDP policies
+ReplayKernel combo_kernel_for(int key, int np) {
+#define COMBO_K(KK) (np == 1 ? (ReplayKernel)magus_replay_combo_kernel<MagusTicker<KK, false>, 1, kTC, kNStage>    \
+                             : (ReplayKernel)magus_replay_combo_kernel<MagusTicker<KK, false>, 2, kTC, kNStage>)
+    switch (key) {
+        case 1: return COMBO_K(1);
+        case 2: return COMBO_K(2);
+        case 3: return COMBO_K(3);
+        default: return nullptr;
+    }
+#undef COMBO_K
+}
+
 // one-warp-CTA replay kernel (replay_solo.cuh) of a chain kind, or nullptr if it has none
 ReplayKernel solo_kernel_for(int key, bool sym, bool bits_ok) {
     int v = env_int("MAGUS_SOLO_BAL", 2);   // stage block variant (replay_solo.cuh)
@@ -219,7 +232,6 @@ ReplayKernel solo_kernel_for(int key, bool sym, bool bits_ok) {
      : v == 3 ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 3>                    \
      : v == 4 ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 4>                    \
      : v == 5 ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 5>                    \
-     : v == 9 ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 9>                    \
               : (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 1>)
     switch (key) {
         case 1: return SOLO_K(1);
@@ -236,7 +248,8 @@ struct LaunchGroup {
     int key, q_base, nq, ng, npw, n_tblocks, n_pblocks, n_ctas, threads;
     size_t smem;
     bool solo;   // one-warp CTAs (npw == 1 and the kind has a solo kernel)
-    bool wide;   // the unsegmented one-chain-per-lane kernel (replay_wide.cuh), fed by the 4-trace tensor map
+    bool wide;   // the unsegmented one-chain-per-lane kernel (replay_wide.cuh), fed by the 16-trace tensor map
+    bool fused;  // replayed by the previous group's launch (magus_replay_combo_kernel): no launch of its own
 };
 
 // Kernel launch with programmatic stream serialization (PDL) when `pdl`: the kernel may be scheduled
@@ -725,6 +738,14 @@ static void choose_geometry(magus_replay_t* h, int n_sm, int forced_segments) {
         }
         return;
     }
+    // One MAGUS solo policy next to one or two TDP_DEFAULT baselines (config 5): MAGUS_COMBO=1 runs both launch groups
+    // in one two-warp kernel sharing the TMA tiles (magus_replay_combo_kernel), so each trace byte is read once.  Off
+    // by default: measured slower (config 5 replay 0.84 vs 0.69 ms) -- the replay is bound by
+    // instruction issue and latency, not HBM, and at 128 registers a two-warp CTA leaves MAGUS 8 warps per SM.
+    const bool combo = h->groups.size() == 2 && h->groups[0].key >= 1 && h->groups[0].key <= 3 &&
+                       h->groups[0].nq == 1 && h->groups[1].key == 1000 + LANE_TDP && h->groups[1].nq <= 2 &&
+                       kTC == 8 && env_int("MAGUS_COMBO", 0) != 0 && env_int("MAGUS_SOLO", 1) != 0 &&
+                       env_int("MAGUS_SOLO_BAL", 2) == 2 && env_int("MAGUS_TDP_SOLO", 2) == 2;
     int W = d.tuning_warmup > 0 ? d.tuning_warmup
                                 : ((kmax + cmax - 1 + 31) / 32) * 32 + env_int("MAGUS_WARMUP_EXTRA", 0) + h->warm_extra;
     W = ((std::max(W, kmax + cmax - 1) + 31) / 32) * 32;
@@ -751,6 +772,8 @@ static void choose_geometry(magus_replay_t* h, int n_sm, int forced_segments) {
             const int target = env_int("MAGUS_TARGET_WARPS_PER_SM", 8 * minb_for(g.key));
             S = (int)std::max<int64_t>(S, ((int64_t)n_sm * target) / wps);
         }
+        // the combined kernel: 8 two-warp CTAs per SM (16 warps: 8 MAGUS, 8 TDP)
+        if (combo) S = std::max(1, (int)(((int64_t)n_sm * env_int("MAGUS_COMBO_CTAS_PER_SM", 8)) / std::max(1, p.n_groups)));
         const int L0 = (((N + S - 1) / S) + 31) / 32 * 32;
         if (S > 1 && L0 < 4 * W) S = std::max(1, N / (4 * W));   // segments must dwarf their warm-up
         S_auto = S;
@@ -840,6 +863,14 @@ static void choose_geometry(magus_replay_t* h, int n_sm, int forced_segments) {
             g.smem = SoloSmem<kTC, kNStage>::kBytes;
             g.n_ctas = p.n_seg * p.n_groups * g.n_pblocks;
         }
+    }
+    if (combo && h->groups[0].solo && h->groups[1].solo) {
+        LaunchGroup& gm = h->groups[0];
+        gm.kernel = combo_kernel_for(gm.key, h->groups[1].nq);
+        gm.threads = 64;
+        gm.smem = SoloSmem<kTC, kNStage>::kBytes + kNStage * sizeof(uint64_t);   // + the empty barriers
+        gm.n_ctas = p.n_seg * p.n_groups;
+        h->groups[1].fused = true;
     }
 }
 
@@ -1312,9 +1343,14 @@ static magus_status enqueue_run(magus_replay_t* h, const float* d_trace, const f
         for (int gi = 0; gi < G; ++gi) {
             const LaunchGroup& g = h->groups[gi];
             cudaStream_t gs = gi == 0 ? s : h->aux[gi - 1];
+            if (g.fused) continue;   // replayed by the previous group's combined launch
             ReplayParams pg = p;
             pg.q_base = g.q_base;
             pg.nq = g.nq;
+            if (gi + 1 < G && h->groups[gi + 1].fused) {
+                pg.q_base2 = h->groups[gi + 1].q_base;
+                pg.nq2 = h->groups[gi + 1].nq;
+            }
             pg.ng = g.ng;
             pg.npw = g.npw;
             pg.n_tblocks = g.n_tblocks;
@@ -1630,7 +1666,9 @@ extern "C" magus_status magus_replay_geometry(const magus_replay_t* h, int32_t o
     // kernel launches of one run, as enqueue_run issues them
     const bool has_work = d.n_traces > 0 && d.n_samples > 0;
     const int nwall = env_int("MAGUS_WALL_ROUNDMAJOR", 0) ? 1 : (int)h->groups.size();
-    int nk = 1 + (has_work ? (h->wall ? nwall : (int)h->groups.size()) : 0);   // pre-pass, replay per launch group
+    int nlaunch = 0;
+    for (const LaunchGroup& g : h->groups) nlaunch += g.fused ? 0 : 1;
+    int nk = 1 + (has_work ? (h->wall ? nwall : nlaunch) : 0);   // pre-pass, replay per launch (group or combined pair)
     if (has_work && p.n_seg > 1 && !h->wall) {
         int nw = 0;
         for (const LaunchGroup& g : h->groups) nw += walk_kernel_for(g.key) ? 1 : 0;

@@ -69,6 +69,25 @@ __device__ __forceinline__ void solo_issue(uint32_t tile, const CUtensorMap* tma
 }
 
 
+// Release a consumed ring slot.  Solo (COMBO = false): the warp owns the ring, so its elected lane refills the slot
+// at once (its lanes' shared-memory reads are complete after the caller's __syncwarp).  COMBO: arrive on
+// empty[slot]; the producer warp (the MAGUS warp of magus_replay_combo_kernel) waits until both consumer warps have
+// arrived, then refills.  `refill` is false for the producer past the last stage and always for the other warp.
+template <int TC, bool COMBO>
+__device__ __forceinline__ void solo_release(uint32_t tile, const CUtensorMap* tmap, uint32_t bar0, uint32_t empty0,
+                                             int slot, uint32_t phase, bool refill, int x, int t0, uint64_t cpol,
+                                             int lane) {
+    if constexpr (COMBO) {
+        if (lane == 0) ptx::mbar_arrive_u32(empty0 + 8 * slot);
+        if (refill) {
+            mbar_wait_loop(empty0 + 8 * slot, phase);
+            solo_issue<TC>(tile, tmap, bar0 + 8 * slot, x, t0, cpol);
+        }
+    } else {
+        if (refill) solo_issue<TC>(tile, tmap, bar0 + 8 * slot, x, t0, cpol);
+    }
+}
+
 // run constants of the pipe-balanced stage block (MAGUS_SSTAGE_K<K>, tick4_asm.cuh)
 struct SoloConst {
     double Blo_d;   // B_lo as fp64
@@ -187,45 +206,22 @@ __device__ __forceinline__ void solo_stage(MagusState<K, false>* s, float* lock,
     s[3].evh = e3;
 }
 
-// BAL: 0 = the integer stage block (MAGUS_STAGE8_K<K>), 1 = the pipe-balanced one (MAGUS_SSTAGE_K<K>),
-// 2 = balanced with the throttle test on the ALU pipe (MAGUS_SSTAGEF_K<K>), 3 / 4 = the 3-DSETP level logic with
-// Alg. 2 by popcount / by the incremental count (MAGUS_PSTAGE_K<K> / MAGUS_QSTAGE_K<K>)
-template <class T, int TC, int NSTAGE, int BAL>
-__global__ void __launch_bounds__(32, kSoloCtasPerSm)
-    magus_replay_solo_kernel(const __grid_constant__ CUtensorMap tmap, const ReplayParams p) {
+// The MAGUS solo replay of one (lane policy q, tile group, segment) by one warp, on a TMA ring that the caller has
+// initialised and primed with the first NSTAGE stages.  COMBO = false: the warp owns the ring and refills a slot
+// right after its own __syncwarp.  COMBO = true (magus_replay_combo_kernel): a second warp (the TDP baselines)
+// consumes the same tiles; both release a slot on empty[slot] and this warp, the producer, refills it once both
+// have released it.
+template <class T, int TC, int NSTAGE, int BAL, bool COMBO>
+__device__ __forceinline__ void solo_magus_body(const CUtensorMap* tmap, const ReplayParams& p, const uint8_t* smem,
+                                                uint32_t tile0, uint32_t bar0, uint32_t empty0, int q, int tgroup,
+                                                int seg, int lane) {
     static_assert(T::kHasStage8 && TC == 8, "solo kernel: whole-stage PTX block of 8 ticks");
     using State = typename T::State;
     using SM = SoloSmem<TC, NSTAGE>;
     constexpr uint32_t kTileBytes = SM::kTileBytes;
-    extern __shared__ __align__(1024) uint8_t smem[];
-    const int lane = threadIdx.x;
-
-    // blockIdx -> (lane policy, tile group, segment); policies fastest so the CTAs of one (group,
-    // segment) read the same tiles close together in time (L2 reuse when nq > 1)
-    int b = blockIdx.x;
-    const int qi = b % p.nq;
-    b /= p.nq;
-    const int tgroup = b % p.n_groups;
-    const int seg = b / p.n_groups;
-    const int q = p.q_base + qi;
-
-    const uint32_t tile0 = ptx::smem_u32(smem);
-    const uint32_t bar0 = tile0 + NSTAGE * kTileBytes;
-    if (lane == 0) {
-        ptx::prefetch_tmap(&tmap);
-        for (int i = 0; i < NSTAGE; ++i)
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8 * i) : "memory");
-        ptx::fence_mbar_init();
-    }
-    __syncwarp();
-
     const SegGeom G = seg_geom<TC>(p, seg);
     const int x = tgroup * kTracesPerWarp;
     const uint64_t cpol = ptx::policy_evict_first();
-    for (int i = 0; i < NSTAGE && i < G.n_stages; ++i)
-        solo_issue<TC>(tile0 + i * kTileBytes, &tmap, bar0 + 8 * i, x, G.tau_w + i * TC, cpol);
-    ptx::pdl_wait();   // first_low and the scratch words come from the pre-pass (launched just before)
-
     const DevPolicy pol = p.pol[q];
     const int j0 = x + lane * kChains;
     const float B_lo = p.B_lo, B_hi = p.B_hi;
@@ -315,8 +311,8 @@ __global__ void __launch_bounds__(32, kSoloCtasPerSm)
                     solo_stage_pq<T::kRingK, BAL>(st, lockf, nthrf, wcmd, ss, vmax, tile + lane_off, sc, pol);
                 else T::stage8(st, tile + lane_off, pol, B_lo, Blo_d, wcmd, ss, vmax);
                 __syncwarp();   // every lane's tile reads are complete before the slot is refilled
-                if (i + NSTAGE < G.n_stages)
-                    solo_issue<TC>(tile, &tmap, bar0 + 8 * slot, x, G.tau_w + (i + NSTAGE) * TC, cpol);
+                solo_release<TC, COMBO>(tile, tmap, bar0, empty0, slot, phase, i + NSTAGE < G.n_stages, x,
+                                        G.tau_w + (i + NSTAGE) * TC, cpol, lane);
                 ++i;
                 if (++slot == NSTAGE) {
                     slot = 0;
@@ -356,8 +352,8 @@ __global__ void __launch_bounds__(32, kSoloCtasPerSm)
                     }
                 }
                 __syncwarp();
-                if (i + NSTAGE < G.n_stages)
-                    solo_issue<TC>(tile, &tmap, bar0 + 8 * slot, x, G.tau_w + (i + NSTAGE) * TC, cpol);
+                solo_release<TC, COMBO>(tile, tmap, bar0, empty0, slot, phase, i + NSTAGE < G.n_stages, x,
+                                        G.tau_w + (i + NSTAGE) * TC, cpol, lane);
                 ++i;
                 if (++slot == NSTAGE) {
                     slot = 0;
@@ -397,6 +393,40 @@ __global__ void __launch_bounds__(32, kSoloCtasPerSm)
                      ss[c].lock + (uint32_t)lockf[c], ss[c].sexc, ss[c].digest());
     }
     if (j0 < p.n_traces) atomicMax(p.c_vmax + chain_idx(p, q, j0), vmax);   // lane-level validation maximum
+}
+
+// BAL: 0 = the integer stage block (MAGUS_STAGE8_K<K>), 1 = the pipe-balanced one (MAGUS_SSTAGE_K<K>),
+// 2 = balanced with the throttle test on the ALU pipe (MAGUS_SSTAGEF_K<K>), 3 / 4 = the 3-DSETP level logic with
+// Alg. 2 by popcount / by the incremental count (MAGUS_PSTAGE_K<K> / MAGUS_QSTAGE_K<K>)
+template <class T, int TC, int NSTAGE, int BAL>
+__global__ void __launch_bounds__(32, kSoloCtasPerSm)
+    magus_replay_solo_kernel(const __grid_constant__ CUtensorMap tmap, const ReplayParams p) {
+    using SM = SoloSmem<TC, NSTAGE>;
+    constexpr uint32_t kTileBytes = SM::kTileBytes;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int lane = threadIdx.x;
+    // blockIdx -> (lane policy, tile group, segment); policies fastest so the CTAs of one (group,
+    // segment) read the same tiles close together in time (L2 reuse when nq > 1)
+    int b = blockIdx.x;
+    const int qi = b % p.nq;
+    b /= p.nq;
+    const int tgroup = b % p.n_groups;
+    const int seg = b / p.n_groups;
+    const uint32_t tile0 = ptx::smem_u32(smem);
+    const uint32_t bar0 = tile0 + NSTAGE * kTileBytes;
+    if (lane == 0) {
+        ptx::prefetch_tmap(&tmap);
+        for (int i = 0; i < NSTAGE; ++i)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8 * i) : "memory");
+        ptx::fence_mbar_init();
+    }
+    __syncwarp();
+    const SegGeom G = seg_geom<TC>(p, seg);
+    const uint64_t cpol = ptx::policy_evict_first();
+    for (int i = 0; i < NSTAGE && i < G.n_stages; ++i)
+        solo_issue<TC>(tile0 + i * kTileBytes, &tmap, bar0 + 8 * i, tgroup * kTracesPerWarp, G.tau_w + i * TC, cpol);
+    ptx::pdl_wait();   // first_low and the scratch words come from the pre-pass (launched just before)
+    solo_magus_body<T, TC, NSTAGE, BAL, false>(&tmap, p, smem, tile0, bar0, 0u, p.q_base + qi, tgroup, seg, lane);
 }
 
 // ===================================================================================================================
@@ -641,21 +671,16 @@ __global__ void __launch_bounds__(32, kSoloCtasPerSm)
 // summed in fp64 as sum(D) (a 0/1 DFMA, exact) and turned into the excess sum(D - B_lo) = sum(D) - n_thr B_lo once
 // per segment (exact: DESIGN.md section 8).  Speculative segments start p.warmup ticks early at the guessed
 // level (f_max); the exact fix-up is the TDP lockstep walk.
-template <int NP, int TC, int NSTAGE>
-__global__ void __launch_bounds__(32, kSoloCtasPerSm)
-    magus_replay_tsolo_kernel(const __grid_constant__ CUtensorMap tmap, const ReplayParams p) {
+// The TDP solo replay of one (policy pair pi, tile group, segment) by one warp on a primed TMA ring.  COMBO: the ring
+// is shared with the MAGUS warp of magus_replay_combo_kernel, which refills it; this warp only releases its slots.
+template <int NP, int TC, int NSTAGE, bool COMBO>
+__device__ __forceinline__ void tsolo_body(const CUtensorMap* tmap, const ReplayParams& p, const uint8_t* smem,
+                                           uint32_t tile0, uint32_t bar0, uint32_t empty0, int pi, int tgroup, int seg,
+                                           int lane) {
     static_assert(TC == 8, "TDP solo kernel: whole-stage PTX block of 8 ticks");
     constexpr int NC = 4 * NP;   // chains per lane
     using SM = SoloSmem<TC, NSTAGE>;
     constexpr uint32_t kTileBytes = SM::kTileBytes;
-    extern __shared__ __align__(1024) uint8_t smem[];
-    const int lane = threadIdx.x;
-    const int npairs = (p.nq + NP - 1) / NP;
-    int b = blockIdx.x;
-    const int pi = b % npairs;
-    b /= npairs;
-    const int tgroup = b % p.n_groups;
-    const int seg = b / p.n_groups;
     int qs[NP];
     bool live[NP];
 #pragma unroll
@@ -664,23 +689,9 @@ __global__ void __launch_bounds__(32, kSoloCtasPerSm)
         live[u] = qi < p.nq;
         qs[u] = p.q_base + (live[u] ? qi : pi * NP);   // a missing second policy repeats the first, unrecorded
     }
-
-    const uint32_t tile0 = ptx::smem_u32(smem);
-    const uint32_t bar0 = tile0 + NSTAGE * kTileBytes;
-    if (lane == 0) {
-        ptx::prefetch_tmap(&tmap);
-        for (int i = 0; i < NSTAGE; ++i)
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8 * i) : "memory");
-        ptx::fence_mbar_init();
-    }
-    __syncwarp();
     const SegGeom G = seg_geom<TC>(p, seg);
     const int x = tgroup * kTracesPerWarp;
     const uint64_t cpol = ptx::policy_evict_first();
-    for (int i = 0; i < NSTAGE && i < G.n_stages; ++i)
-        solo_issue<TC>(tile0 + i * kTileBytes, &tmap, bar0 + 8 * i, x, G.tau_w + i * TC, cpol);
-    ptx::pdl_wait();
-
     const int j0 = x + lane * kChains;
     const float B_lo = p.B_lo;
     const double Blo_d = (double)B_lo;
@@ -766,7 +777,8 @@ __global__ void __launch_bounds__(32, kSoloCtasPerSm)
                 }
             }
             __syncwarp();
-            if (i + NSTAGE < G.n_stages) solo_issue<TC>(tile, &tmap, bar0 + 8 * slot, x, G.tau_w + (i + NSTAGE) * TC, cpol);
+            solo_release<TC, COMBO>(tile, tmap, bar0, empty0, slot, phase, !COMBO && i + NSTAGE < G.n_stages, x,
+                                    G.tau_w + (i + NSTAGE) * TC, cpol, lane);
             ++i;
             if (++slot == NSTAGE) {
                 slot = 0;
@@ -815,6 +827,81 @@ __global__ void __launch_bounds__(32, kSoloCtasPerSm)
             add_to_chain(p, qs[u], j, nhi[cc], nthr, trans[cc], 0u, 0u, sexc, digest_pack(dc[cc], 0u));
         }
     if (j0 < p.n_traces) atomicMax(p.c_vmax + chain_idx(p, qs[0], j0), vmax);
+}
+
+template <int NP, int TC, int NSTAGE>
+__global__ void __launch_bounds__(32, kSoloCtasPerSm)
+    magus_replay_tsolo_kernel(const __grid_constant__ CUtensorMap tmap, const ReplayParams p) {
+    using SM = SoloSmem<TC, NSTAGE>;
+    constexpr uint32_t kTileBytes = SM::kTileBytes;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int lane = threadIdx.x;
+    const int npairs = (p.nq + NP - 1) / NP;
+    int b = blockIdx.x;
+    const int pi = b % npairs;
+    b /= npairs;
+    const int tgroup = b % p.n_groups;
+    const int seg = b / p.n_groups;
+    const uint32_t tile0 = ptx::smem_u32(smem);
+    const uint32_t bar0 = tile0 + NSTAGE * kTileBytes;
+    if (lane == 0) {
+        ptx::prefetch_tmap(&tmap);
+        for (int i = 0; i < NSTAGE; ++i)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8 * i) : "memory");
+        ptx::fence_mbar_init();
+    }
+    __syncwarp();
+    const SegGeom G = seg_geom<TC>(p, seg);
+    const uint64_t cpol = ptx::policy_evict_first();
+    for (int i = 0; i < NSTAGE && i < G.n_stages; ++i)
+        solo_issue<TC>(tile0 + i * kTileBytes, &tmap, bar0 + 8 * i, tgroup * kTracesPerWarp, G.tau_w + i * TC, cpol);
+    ptx::pdl_wait();
+    tsolo_body<NP, TC, NSTAGE, false>(&tmap, p, smem, tile0, bar0, 0u, pi, tgroup, seg, lane);
+}
+
+// ===================================================================================================================
+// The combined kernel for a run of one MAGUS solo policy and NP TDP_DEFAULT baselines (config 5): a CTA of two warps
+// shares one TMA ring, so every trace tile is read from HBM once for all of the run's replayed policies.  Warp 0
+// replays MAGUS (solo_magus_body) and refills the ring; warp 1 replays the TDP pair (tsolo_body).  A slot is refilled
+// once both warps released it (empty mbarrier, count 2).  p.q_base / p.nq: the MAGUS group; p.q_base2 / p.nq2: the
+// TDP group.  The per-chain states, statistics and fix-up are those of the two separate kernels.
+template <class T, int NP, int TC, int NSTAGE>
+__global__ void __launch_bounds__(64, kSoloCtasPerSm / 2)
+    magus_replay_combo_kernel(const __grid_constant__ CUtensorMap tmap, const ReplayParams p) {
+    using SM = SoloSmem<TC, NSTAGE>;
+    constexpr uint32_t kTileBytes = SM::kTileBytes;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tgroup = blockIdx.x % p.n_groups;
+    const int seg = blockIdx.x / p.n_groups;
+    const uint32_t tile0 = ptx::smem_u32(smem);
+    const uint32_t bar0 = tile0 + NSTAGE * kTileBytes, empty0 = bar0 + 8 * NSTAGE;
+    if (warp == 0) {
+        if (lane == 0) {
+            ptx::prefetch_tmap(&tmap);
+            for (int i = 0; i < NSTAGE; ++i) {
+                asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8 * i) : "memory");
+                asm volatile("mbarrier.init.shared::cta.b64 [%0], 2;" ::"r"(empty0 + 8 * i) : "memory");
+            }
+            ptx::fence_mbar_init();
+        }
+        __syncwarp();
+        const SegGeom G = seg_geom<TC>(p, seg);
+        const uint64_t cpol = ptx::policy_evict_first();
+        for (int i = 0; i < NSTAGE && i < G.n_stages; ++i)
+            solo_issue<TC>(tile0 + i * kTileBytes, &tmap, bar0 + 8 * i, tgroup * kTracesPerWarp, G.tau_w + i * TC,
+                           cpol);
+    }
+    __syncthreads();   // the barriers are initialised before warp 1 waits on them
+    ptx::pdl_wait();
+    if (warp == 0) {
+        solo_magus_body<T, TC, NSTAGE, 2, true>(&tmap, p, smem, tile0, bar0, empty0, p.q_base, tgroup, seg, lane);
+    } else {
+        ReplayParams pt = p;
+        pt.q_base = p.q_base2;
+        pt.nq = p.nq2;
+        tsolo_body<NP, TC, NSTAGE, true>(&tmap, pt, smem, tile0, bar0, empty0, 0, tgroup, seg, lane);
+    }
 }
 
 }  // namespace magus

@@ -2,6 +2,7 @@
 initcheck).  GPU box only.  usage: compute-sanitizer --tool <t> python scripts/sanitize_run.py
 
 Covers: the generator, the pre-pass, the one-warp solo replay kernel (MAGUS k <= 3, TMA/mbarrier ring), the
+two-warp combined MAGUS + TDP kernel (shared ring, empty barriers), the unsegmented wide kernel (8-warp CTAs), the
 multi-warp replay kernel (shared tiles: several policy warps, TDP / STATIC_MIN / k >= 4 / 64-bit logs), the
 fix-up mark + split / lockstep / per-thread walks, the totals and chunk-sum kernels, the decision re-simulation,
 the wall-clock kernels, the counter ingest -- direct launches and the captured CUDA graph.  Each run is checked
@@ -53,6 +54,13 @@ def main():
     case("cfg2-small graph", 2, 260, 6000, 0, cfg2, 6, stream=True)
     case("cfg5-small solo+tdp, walks", 5, 257, 6000, 2, cfg5 + sweep64()[40:42], 7)
     case("cfg3-small shared tiles", 3, 64, 3000, 1, sweep64()[::5] + [pol(kind=STATIC_MAX)], 5)
+    case("cfg5 combined MAGUS + TDP kernel, walks", 5, 257, 6000, 2, cfg5, 7)
+    os.environ["MAGUS_WIDE"] = "1"
+    case("cfg3-small unsegmented wide plan", 3, 40, 3000, 1, sweep64() + [pol(kind=STATIC_MAX)], 0)
+    os.environ["MAGUS_WIDE_NC"] = "2"
+    case("wide plan, two chains per thread", 3, 40, 3000, 1, sweep64(), 0)
+    os.environ.pop("MAGUS_WIDE_NC")
+    os.environ.pop("MAGUS_WIDE")
     case("k>=4, 64-bit logs, static min", 9, 131, 3000, 1,
          [pol(deriv_ticks=9, tune_log_capacity=10), pol(deriv_ticks=4, tune_log_capacity=40),
           pol(kind=STATIC_MIN), pol(kind=TDP_DEFAULT, tdp_w=217.0)], 5)

@@ -208,6 +208,29 @@ def test_wide_plan_choice(M, monkeypatch):
         assert R.geometry()["wide_groups"] == 0
 
 
+@pytest.mark.parametrize("combo", ["1", "0"])
+@pytest.mark.parametrize("n_tdp", [1, 2])
+def test_combo_kernel_reads_each_tile_once(M, combo, n_tdp, monkeypatch):
+    """Config 5's policy mix (MAGUS + static max + TDP_DEFAULT baselines) runs as ONE two-warp kernel sharing the
+    TMA tiles (magus_replay_combo_kernel: MAGUS warp + TDP warp) -- and, with MAGUS_COMBO=0, as two launches; both
+    equal the oracle (records, every word, a decision dump, totals), with forced segmentation so the fix-up walks
+    run after the combined replay."""
+    monkeypatch.setenv("MAGUS_COMBO", combo)
+    s = SMALL["cfg5-small"]
+    pols = s["policies"][:2 + n_tdp]
+    stride = (s["n"] + 3) // 4 * 4
+    tr, w = gpu_gen(M, s["seed"], s["n"], s["ns"], s["mix"], stride)
+    res = run_gpu(M, tr, w, pols, s["n"], s["ns"], stride, segments=9, dump=(s["n"] - 4, 4))
+    geo = res.geometry
+    assert geo["launch_groups"] == 2
+    assert (geo["threads_per_cta"] == 64) == (combo == "1"), geo
+    rec, codes = oracle_run(tr.cpu().numpy(), w.cpu().numpy(), pols, s["n"])
+    PA.compare_records(res.per_trace, rec, f"combo={combo} tdp={n_tdp}")
+    assert np.array_equal(res.words, PA.pack_words(codes))
+    assert np.array_equal(res.decisions, codes[:, s["n"] - 4:, :])
+    PA.compare_totals(res.totals, rec)
+
+
 @pytest.mark.parametrize("n,ns", [(1, 1), (1, 31), (3, 33), (5, 32), (128, 64), (129, 95), (4, 1000)])
 def test_tiny_and_ragged(M, n, ns):
     stride = (n + 3) // 4 * 4
