@@ -94,7 +94,8 @@ typedef struct {
 /* desc.flags */
 #define MAGUS_F_PER_TRACE_STATS 0x1u  /* fill magus_results.per_trace */
 #define MAGUS_F_DUMP_WORDS      0x2u  /* per-(trace,policy) 32-tick cmd/tune-flag words from the replay kernel */
-#define MAGUS_F_DUMP_DECISIONS  0x4u  /* per-tick code bytes (DESIGN A27) for a window of traces */
+#define MAGUS_F_DUMP_DECISIONS  0x4u  /* per-tick code bytes (DESIGN A27) for a window of traces, decoded from the
+                                         replay kernels' own cmd / tune-flag words (magus_decode_kernel) */
 #define MAGUS_F_TIMING          0x8u  /* record CUDA events around the replay kernel(s) (magus_replay_kernel_times) */
 #define MAGUS_F_TIMING_DETAIL   0x10u /* with MAGUS_F_TIMING: also around the pre-pass, fix-up and totals (each
                                          event node costs a few microseconds of the run) */

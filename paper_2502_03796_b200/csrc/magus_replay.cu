@@ -1100,7 +1100,9 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
         }
         p.dkeys = dk;
     }
-    if (d.flags & MAGUS_F_DUMP_WORDS) {
+    // the replay kernels' words: returned with MAGUS_F_DUMP_WORDS, and the source of the decision dump's codes
+    // (magus_decode_kernel) with MAGUS_F_DUMP_DECISIONS
+    if ((d.flags & MAGUS_F_DUMP_WORDS) || ((d.flags & MAGUS_F_DUMP_DECISIONS) && !h->wall)) {
         ALLOC(p.words, (size_t)Q * std::max(1, d.n_traces) * std::max(1, p.n_blocks) * 2);
     } else {
         p.words = nullptr;
@@ -1470,8 +1472,12 @@ extern "C" magus_status magus_replay_run(magus_replay_t* h, const float* d_trace
     if (h->d_codes && has_work) {
         const int P = d.n_policies;
         dim3 grid((unsigned)((d.dump_n_traces + 63) / 64), (unsigned)p.n_lane);
-        if (!h->wall)   // (the wall-clock kernel writes its rounds' codes itself)
+        // the codes decoded from the replay kernels' own words (MAGUS_DUMP_RESIM=1: re-simulated from t = 0
+        // instead, a cross-check); the wall-clock kernel writes its rounds' codes itself
+        if (!h->wall && env_int("MAGUS_DUMP_RESIM", 0))
             magus_resim_kernel<<<grid, 64, 0, s>>>(p, d_trace, d.dump_first_trace, d.dump_n_traces, P, h->d_codes);
+        else if (!h->wall)
+            magus_decode_kernel<<<grid, 64, 0, s>>>(p, d_trace, d.dump_first_trace, d.dump_n_traces, P, h->d_codes);
         CU(h, cudaGetLastError());
         const int64_t rows = (int64_t)d.n_samples * d.dump_n_traces;
         for (int pi : h->smax) {

@@ -829,6 +829,55 @@ __global__ void magus_resim_kernel(const ReplayParams p, const float* __restrict
 #undef MAGUS_RESIM
 }
 
+// Per-tick codes (DESIGN A27) for traces [first, first + n) of every lane policy, DECODED from the replay kernels' own
+// 32-tick words (p.words: written by the replay kernel for every counted block and rewritten by the fix-up walk for
+// the blocks it re-ran): the cmd and tune-flag bits are the hot kernel's; the rest follows from them and the
+// samples without re-running the recurrence -- level in effect = the previous tick's cmd (f0 at t = 0); A = min(D,
+// B[level]) and throttled = D > B[level] (A14); ready = t >= k (A7); signal = Alg. 1's comparison of the fp64
+// difference A_t - A_{t-k} with the host thresholds; lock = Alg. 2 on the last C logged flags once the log
+// is full (A8).  codes: [n_samples][n][P].  One thread per (trace, lane policy); k <= 64 (fp32 ring of A).
+__global__ void magus_decode_kernel(const ReplayParams p, const float* __restrict__ trace, int first, int n_win, int P,
+                                    uint8_t* codes) {
+    const int jd = blockIdx.x * blockDim.x + threadIdx.x;
+    const int q = blockIdx.y;
+    if (jd >= n_win) return;
+    const DevPolicy pol = p.pol[q];
+    if (pol.policy_index < 0) return;
+    const int j = first + jd;
+    const uint32_t* wq = p.words + ((int64_t)q * p.n_traces + j) * p.n_blocks * 2;
+    const bool magus = pol.kind == LANE_MAGUS;
+    const int k = pol.k, C = pol.C;
+    float ring[KMAX_GENERIC];   // A_{t-k} .. A_{t-1}, circular by t % k
+    uint64_t log = 0;
+    uint32_t lvl = (uint32_t)pol.f0;
+    for (int b = 0; b < p.n_blocks; ++b) {
+        const uint32_t wc = wq[2 * b], we = wq[2 * b + 1];
+        const int n = min(32, p.n_samples - 32 * b);
+        for (int i = 0; i < n; ++i) {
+            const int t = 32 * b + i;
+            const uint32_t cmd = (wc >> (31 - i)) & 1u, ev = (we >> (31 - i)) & 1u;
+            const float D = trace[(int64_t)t * p.trace_stride + j];
+            const float B = lvl ? p.B_hi : p.B_lo;
+            const float A = fminf(D, B);
+            const uint32_t thr = D > B ? 1u : 0u;
+            uint32_t c = cmd | (ev << 2) | (thr << 6) | (lvl << 7);
+            if (magus) {
+                const bool ready = t >= k;
+                if (ready) {
+                    const double d = (double)A - (double)ring[t % k];
+                    c |= 2u | ((d > pol.dinc ? 1u : (d < pol.ddec ? 2u : 0u)) << 4);
+                }
+                ring[t % k] = A;
+                log = (log << 1) | ev;
+                const uint64_t w = log & pol.logmask;
+                if (t >= k + C - 1 && (uint32_t)__popcll(w) >= (uint32_t)pol.s_min) c |= 8u;
+            }
+            codes[((int64_t)t * n_win + jd) * P + pol.policy_index] = (uint8_t)c;
+            lvl = cmd;
+        }
+    }
+}
+
 __global__ void magus_fill_codes_kernel(uint8_t* codes, int64_t n_rows, int P, int pi, uint8_t value) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n_rows) codes[i * P + pi] = value;

@@ -1,0 +1,7 @@
+#!/bin/bash
+# decision dump decoded from the replay words: the full GPU suite
+TAG=${1:-r02s12}
+OUT=gpurun_out; mkdir -p $OUT
+timeout 1500 python -m pytest tests -m gpu -q -s -p no:cacheprovider --durations=5 > $OUT/${TAG}_pytest_gpu.log 2>&1
+echo "pytest rc=$?" >> $OUT/${TAG}_pytest_gpu.log
+grep -E "walked|passed|failed|rc=" $OUT/${TAG}_pytest_gpu.log | tail -8

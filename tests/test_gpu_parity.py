@@ -231,6 +231,28 @@ def test_combo_kernel_reads_each_tile_once(M, combo, n_tdp, monkeypatch):
     PA.compare_totals(res.totals, rec)
 
 
+@pytest.mark.parametrize("name,segments", [("cfg5-small", 7), ("mixed-kinds", 5), ("cfg3-small", 0)])
+def test_decision_dump_decoded_from_replay_words(M, name, segments, monkeypatch):
+    """The decision dump (magus_decode_kernel: codes decoded from the replay kernels' own cmd / tune-flag words, the
+    fix-up walk's rewritten blocks included) equals the independent re-simulation from t = 0 (magus_resim_kernel,
+    MAGUS_DUMP_RESIM=1) and the oracle's codes byte for byte, for every dumped trace, policy and tick."""
+    s = dict(SMALL[name])
+    if name == "cfg5-small":
+        s["policies"] = s["policies"] + sweep64()[40:42]   # lock-sticky points: speculative entries do mismatch
+    stride = (s["n"] + 3) // 4 * 4
+    tr, w = gpu_gen(M, s["seed"], s["n"], s["ns"], s["mix"], stride)
+    dump = (0, s["n"])
+    dec = run_gpu(M, tr, w, s["policies"], s["n"], s["ns"], stride, flags=M.F_PER_TRACE_STATS, segments=segments,
+                  dump=dump)
+    monkeypatch.setenv("MAGUS_DUMP_RESIM", "1")
+    rsm = run_gpu(M, tr, w, s["policies"], s["n"], s["ns"], stride, flags=M.F_PER_TRACE_STATS, segments=segments,
+                  dump=dump)
+    _, codes = oracle_run(tr.cpu().numpy(), w.cpu().numpy(), s["policies"], s["n"])
+    assert np.array_equal(dec.decisions, rsm.decisions)
+    assert np.array_equal(dec.decisions, codes)
+    print(f"{name}: {dec.n_mismatched_segments} wrong speculative entries walked (their blocks' words rewritten)")
+
+
 @pytest.mark.parametrize("n,ns", [(1, 1), (1, 31), (3, 33), (5, 32), (128, 64), (129, 95), (4, 1000)])
 def test_tiny_and_ragged(M, n, ns):
     stride = (n + 3) // 4 * 4
@@ -497,8 +519,8 @@ def test_full_size_every_trace(M, cfg):
     Bit-exact: every (trace, policy) record's counts and digest, and every tick's cmd and tune-flag bit from
     the replay kernel's 32-tick words (MAGUS_F_DUMP_WORDS; cfg 3: the words of 256 traces x 65 policies, the
     records of all 1,024); 1e-9: T, E, E_pkg, EDP, the savings and the per-policy totals against the oracle's
-    (math.fsum) totals.  A 64-trace decision dump (magus_resim_kernel) is checked against the replay kernel's
-    own words and, byte for byte, against the oracle's codes."""
+    (math.fsum) totals.  A 64-trace decision dump (decoded from the replay kernel's words, magus_decode_kernel) is
+    checked against those words and, byte for byte, against the oracle's codes."""
     c = CONFIGS[cfg]
     n, ns = c["n_traces"], c["n_samples"]
     tr, w = gpu_gen(M, c["seed"], n, ns, c["class_mix"], c["stride"])
