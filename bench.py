@@ -336,6 +336,10 @@ def run_ours(args, cfg):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg["name"] + ("+wallclock" if args.wallclock else ""), "n_traces_per_gpu": n, "n_samples": ns, "policies": len(pols),
                        "policies_global": n_pol_glob,
+                       # STATIC_MAX (and a TDP_DEFAULT policy that can never leave f_max) have a closed-form record:
+                       # replayed = the policies whose recurrence the kernels step
+                       "replayed_policies": geo["lane_policies"] if not args.wallclock else None,
+                       "closed_form_policies": "STATIC_MAX (+ TDP never reaching its budget at f_max)",
                        "parallelism": f"trace-sharded x{world // ps}" + (f", parameter grid x{ps}" if ps > 1 else "")
                                       + (", NCCL allreduce of per-policy totals" if dist_on else ""),
                        "l2": "inputs 1.64 GB/GPU >> 126 MB L2; no flush needed" if ns * n * 4 > 4e8 else "L2-resident"},

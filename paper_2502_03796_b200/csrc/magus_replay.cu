@@ -463,7 +463,7 @@ struct magus_replay {
     magus_replay_desc desc{};
     std::vector<magus_policy> pols;
     std::vector<DevPolicy> lane;        // lane policies (everything but STATIC_MAX; or one validate pseudo)
-    std::vector<int> smax;              // indices of STATIC_MAX policies
+    std::vector<int> smax;              // policies in the closed form of STATIC_MAX (and TDP never leaving f_max)
     float B_lo = 0, B_hi = 0;
     uint32_t bwbits = 0;
     double P_lo = 0, P_hi = 0;
@@ -850,8 +850,9 @@ static void choose_geometry(magus_replay_t* h, int n_sm, int forced_segments) {
         }
         // TDP_DEFAULT groups: the TDP solo kernel, NP policies per warp sharing the samples (MAGUS_TDP_SOLO = NP in
         // {1, 2}; 0: the multi-warp kernel)
-        const int tnp = env_int("MAGUS_TDP_SOLO", 2);
-        if (g.key == 1000 + LANE_TDP && kTC == 8 && (tnp == 1 || tnp == 2)) {
+        const int tnp_env = env_int("MAGUS_TDP_SOLO", 2);
+        const int tnp = std::min(tnp_env, g.nq);   // one TDP policy: no idle second chain set per lane
+        if (g.key == 1000 + LANE_TDP && kTC == 8 && (tnp_env == 1 || tnp_env == 2)) {
             g.solo = true;
             g.kernel = tnp == 1 ? (ReplayKernel)magus_replay_tsolo_kernel<1, kTC, kNStage>
                                 : (ReplayKernel)magus_replay_tsolo_kernel<2, kTC, kNStage>;
@@ -1023,6 +1024,14 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
             q.astar_hi = derive_astar(h->P_hi, m, p);
             q.f0 = 1;        // the default sits at max
             q.guess_f = 1;
+            // A TDP_DEFAULT policy whose budget is never reached at f_max -- a*_hi above every observable A (A =
+            // min(D, B_hi) with valid D <= bw_max, A17) -- starts at f_max and never leaves it: its record
+            // is STATIC_MAX's, in closed form (config 5's 270 W: 200 + 0.5 x 20 W < 256.5 W).
+            // MAGUS_NO_TDP_CLOSED=1 replays it anyway.
+            if (q.astar_hi > std::min(bwf, h->B_hi) && !env_int("MAGUS_NO_TDP_CLOSED", 0)) {
+                h->smax.push_back(i);
+                continue;
+            }
         }
         h->lane.push_back(q);
     }

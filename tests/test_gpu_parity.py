@@ -216,6 +216,7 @@ def test_combo_kernel_reads_each_tile_once(M, combo, n_tdp, monkeypatch):
     equal the oracle (records, every word, a decision dump, totals), with forced segmentation so the fix-up walks
     run after the combined replay."""
     monkeypatch.setenv("MAGUS_COMBO", combo)
+    monkeypatch.setenv("MAGUS_NO_TDP_CLOSED", "1")   # replay the 270 W policy too (it never leaves f_max)
     s = SMALL["cfg5-small"]
     pols = s["policies"][:2 + n_tdp]
     stride = (s["n"] + 3) // 4 * 4
@@ -228,6 +229,26 @@ def test_combo_kernel_reads_each_tile_once(M, combo, n_tdp, monkeypatch):
     PA.compare_records(res.per_trace, rec, f"combo={combo} tdp={n_tdp}")
     assert np.array_equal(res.words, PA.pack_words(codes))
     assert np.array_equal(res.decisions, codes[:, s["n"] - 4:, :])
+    PA.compare_totals(res.totals, rec)
+
+
+@pytest.mark.parametrize("closed", ["0", "1"])
+def test_tdp_never_low_closed_form(M, closed, monkeypatch):
+    """A TDP_DEFAULT policy whose budget is never reached at f_max (config 5's 270 W: a*_hi = 113 GB/s > bw_max) is
+    STATIC_MAX in closed form; replayed (MAGUS_NO_TDP_CLOSED=1) or not, every record, word, code and total equals
+    the oracle's replay of the TDP policy, and the 217 W policy (which does reach its budget) is replayed."""
+    monkeypatch.setenv("MAGUS_NO_TDP_CLOSED", "0" if closed == "1" else "1")
+    s = SMALL["cfg5-small"]
+    stride = (s["n"] + 3) // 4 * 4
+    tr, w = gpu_gen(M, s["seed"], s["n"], s["ns"], s["mix"], stride)
+    th = M.derive_thresholds(M.Policy(kind=TDP_DEFAULT, tdp_w=270.0), M.Model())
+    assert th["astar_hi"] > 20.0
+    res = run_gpu(M, tr, w, s["policies"], s["n"], s["ns"], stride, dump=(0, 5))
+    assert res.geometry["lane_policies"] == (2 if closed == "1" else 3), res.geometry
+    rec, codes = oracle_run(tr.cpu().numpy(), w.cpu().numpy(), s["policies"], s["n"])
+    PA.compare_records(res.per_trace, rec, f"tdp closed={closed}")
+    assert np.array_equal(res.words, PA.pack_words(codes))
+    assert np.array_equal(res.decisions, codes[:, :5, :])
     PA.compare_totals(res.totals, rec)
 
 
