@@ -232,6 +232,61 @@ def test_combo_kernel_reads_each_tile_once(M, combo, n_tdp, monkeypatch):
     PA.compare_totals(res.totals, rec)
 
 
+def _random_case(seed):
+    """A seeded random run: sizes (ragged, sometimes tiny), policies of every kind with random parameters (MAGUS k, C
+    up to 64, thresholds; TDP budgets around the model's power range), a random model (Linear / Saturating, closed or
+    open loop, sample period) and edge samples injected into generated traces (0, -0.0, B_lo and its neighbours,
+    bw_max, the largest fp32 below it, the smallest subnormal, 1e-30)."""
+    rng = np.random.default_rng(seed)
+    n = int(rng.choice([1, 3, 17, 64, 131, 257]))
+    ns = int(rng.choice([1, 31, 33, 640, 2049, 5003]))
+    pols = []
+    for _ in range(int(rng.integers(1, 7))):
+        kind = int(rng.choice([0, 0, 0, 1, 2, 3]))
+        if kind == 0:
+            pols.append(pol(deriv_ticks=int(rng.choice([1, 2, 3, 4, 5, 8, 9, 16, 33, 64])),
+                            tune_log_capacity=int(rng.choice([1, 2, 4, 10, 20, 28, 29, 40, 64])),
+                            high_freq_threshold=float(rng.choice([0.05, 0.3, 0.5, 0.6, 0.75, 1.0])),
+                            inc_threshold=float(rng.uniform(0.05, 5.0)), dec_threshold=-float(rng.uniform(0.05, 5.0))))
+        elif kind == 3:
+            pols.append(pol(kind=TDP_DEFAULT, tdp_w=float(rng.uniform(150.0, 300.0)),
+                            tdp_margin=float(rng.uniform(0.01, 0.2))))
+        else:
+            pols.append(pol(kind=STATIC_MAX if kind == 1 else STATIC_MIN))
+    mk = dict(sample_period_s=float(rng.choice([0.05, 0.1, 0.25])), observe=int(rng.integers(0, 2)))
+    if rng.integers(0, 2):
+        mk.update(bw_shape=1, bw_knee=float(rng.choice([0.3, 0.5, 1.0])))
+    segments = int(rng.choice([0, 0, 1, 3, 9]))
+    wide = bool(rng.integers(0, 2))
+    return n, ns, int(rng.integers(0, 4)), pols, mk, segments, wide, rng
+
+
+@pytest.mark.parametrize("seed", list(range(24)))
+def test_randomized_runs_with_edge_samples(M, seed, monkeypatch):
+    """Seeded random runs (_random_case) against the oracle: every record, every tick's cmd / tune-flag word and the
+    totals.  Sizes, policies, models, plans (segmented / unsegmented / forced segment counts) all vary."""
+    n, ns, mix, pols, mk, segments, wide, rng = _random_case(seed)
+    if wide:
+        monkeypatch.setenv("MAGUS_WIDE", "1")
+    stride = (n + 3) // 4 * 4
+    tr, w = gpu_gen(M, 500 + seed, n, ns, mix, stride)
+    h = tr.cpu().numpy()
+    B_lo = np.float32(M.derive_thresholds(M.Policy(), M.Model(**mk))["B_lo"])
+    edges = np.array([0.0, -0.0, B_lo, np.nextafter(B_lo, np.float32(0)), np.nextafter(B_lo, np.float32(30)), 20.0,
+                      np.nextafter(np.float32(20.0), np.float32(0)), np.float32(1.4e-45), 1e-30], dtype=np.float32)
+    edges = edges[edges <= np.float32(20.0)]   # valid samples only (A17): B_lo's upper neighbour may exceed bw_max
+    n_edge = max(1, (ns * n) // 50)
+    rows, cols = rng.integers(0, ns, n_edge), rng.integers(0, n, n_edge)
+    h[rows, cols] = edges[rng.integers(0, len(edges), n_edge)]
+    tr.copy_(torch.from_numpy(h))
+    res = run_gpu(M, tr, w, pols, n, ns, stride, segments=segments, model=M.Model(**mk))
+    rec, codes = oracle_run(h, w.cpu().numpy(), pols, n, model=O.Model(**mk))
+    label = f"seed {seed}: n={n} ns={ns} segments={segments} wide={wide} model={mk} policies={pols}"
+    PA.compare_records(res.per_trace, rec, label)
+    assert np.array_equal(res.words, PA.pack_words(codes)), label
+    PA.compare_totals(res.totals, rec)
+
+
 @pytest.mark.parametrize("closed", ["0", "1"])
 def test_tdp_never_low_closed_form(M, closed, monkeypatch):
     """A TDP_DEFAULT policy whose budget is never reached at f_max (config 5's 270 W: a*_hi = 113 GB/s > bw_max) is
