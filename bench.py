@@ -331,6 +331,8 @@ def run_ours(args, cfg):
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            # sweeps also report trace-sample-policy ticks/s (the replayed recurrences' ticks)
+            "policy_ticks_per_s": value * geo["lane_policies"] if not args.wallclock else None,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
             "scaling": "weak" if ps == 1 else "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
