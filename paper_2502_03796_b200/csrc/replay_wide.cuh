@@ -33,7 +33,11 @@ constexpr int kWideNStage = 6;
 
 struct WideSmem {
     static constexpr int kTileBytes = kWideTC * kWideTpc * 4;   // 2 KB
-    static constexpr size_t kBytes = (size_t)kWideNStage * kTileBytes + 2 * kWideNStage * sizeof(uint64_t);
+    // + one fp64 scratch per warp: its 2 traces x 32 ticks, converted once per stage (one chain per thread)
+    static constexpr int kWarpBufBytes = 2 * kWideTC * 8;       // 512 B
+    static constexpr size_t kBarOff = (size_t)kWideNStage * kTileBytes;
+    static constexpr size_t kBufOff = kBarOff + 2 * kWideNStage * sizeof(uint64_t);
+    static constexpr size_t kBytes = kBufOff + (size_t)kWideWarps * kWarpBufBytes;
 };
 
 // the elected lane arms `bar` for one tile and issues the 2-D TMA box {16 traces, 32 ticks} at (x, t0); no L2
@@ -70,6 +74,29 @@ __device__ __forceinline__ void wide_stage(MagusState<K, false>& st, float& lock
     else MAGUS_WSTAGE1F_K8(st.f, R(0), R(1), R(2), R(3), R(4), R(5), R(6), R(7), WD_TAIL);
 #undef R
 #undef WD_TAIL
+    st.evh = e0;
+}
+
+// 8 ticks of one chain with the samples as fp64 values (MAGUS_WSTAGE1D_K<K>: no conversion, fp64 throttle test)
+template <int K>
+__device__ __forceinline__ void wide_stage_d(MagusState<K, false>& st, float& lock, float& nthr, uint32_t& wcmd,
+                                             double& sexc, const double* d8, const DevPolicy& pol, double Blo_d,
+                                             uint32_t bitc, uint32_t mone) {
+    uint32_t e0 = st.evh;
+#define WDD_TAIL                                                                                                 \
+    e0, st.cnt, sexc, lock, nthr, wcmd, d8[0], d8[1], d8[2], d8[3], d8[4], d8[5], d8[6], d8[7], Blo_d, pol.dinc,    \
+        pol.ddec, bitc, pol.smin_sc, pol.one, mone
+#define R(i) st.ring.v[i]
+    if constexpr (K == 1) MAGUS_WSTAGE1D_K1(st.f, R(0), WDD_TAIL);
+    else if constexpr (K == 2) MAGUS_WSTAGE1D_K2(st.f, R(0), R(1), WDD_TAIL);
+    else if constexpr (K == 3) MAGUS_WSTAGE1D_K3(st.f, R(0), R(1), R(2), WDD_TAIL);
+    else if constexpr (K == 4) MAGUS_WSTAGE1D_K4(st.f, R(0), R(1), R(2), R(3), WDD_TAIL);
+    else if constexpr (K == 5) MAGUS_WSTAGE1D_K5(st.f, R(0), R(1), R(2), R(3), R(4), WDD_TAIL);
+    else if constexpr (K == 6) MAGUS_WSTAGE1D_K6(st.f, R(0), R(1), R(2), R(3), R(4), R(5), WDD_TAIL);
+    else if constexpr (K == 7) MAGUS_WSTAGE1D_K7(st.f, R(0), R(1), R(2), R(3), R(4), R(5), R(6), WDD_TAIL);
+    else MAGUS_WSTAGE1D_K8(st.f, R(0), R(1), R(2), R(3), R(4), R(5), R(6), R(7), WDD_TAIL);
+#undef R
+#undef WDD_TAIL
     st.evh = e0;
 }
 
@@ -139,7 +166,8 @@ __global__ void __launch_bounds__(kWideThreads / NC, 2)
     }
 
     const uint32_t tile0 = ptx::smem_u32(smem);
-    const uint32_t full0 = tile0 + kWideNStage * kTileBytes, empty0 = full0 + 8 * kWideNStage;
+    const uint32_t full0 = tile0 + (uint32_t)WideSmem::kBarOff, empty0 = full0 + 8 * kWideNStage;
+    double* wbuf = reinterpret_cast<double*>(smem + WideSmem::kBufOff) + warp * (2 * kWideTC);   // this warp's
     const int N = p.n_samples;
     const int n_st = (N + kWideTC - 1) / kWideTC;
     if (warp == 0) {
@@ -173,6 +201,9 @@ __global__ void __launch_bounds__(kWideThreads / NC, 2)
         ss[c].zero();
         lockf[c] = nthrf[c] = 0.f;
     }
+    // warp-uniform: the steady branch converts the warp's tile columns with all 32 lanes (and __syncwarp()s), so a
+    // warp whose lanes' policies differ in k + C - 1 takes the per-tick path until the longest warm-up is over
+    warm = __reduce_max_sync(0xffffffffu, warm);
     const float B_lo = p.B_lo, B_hi = p.B_hi;
     const double Blo_d = (double)B_lo;
     const uint32_t mone = 0xFFFFFFFFu * pol[0].one;
@@ -191,7 +222,34 @@ __global__ void __launch_bounds__(kWideThreads / NC, 2)
             fstart[c] = T::level(st[c]);
             wcmd[c] = 0;
         }
-        if (n == kWideTC && bt0 >= warm) {
+        // release the stage; warp 0 refills it with stage i + NSTAGE once all warps have released it
+        auto release = [&]() {
+            if (lane == 0) ptx::mbar_arrive_u32(empty0 + 8 * slot);
+            if (warp == 0 && i + kWideNStage < n_st) {
+                ptx::mbar_wait_u32(empty0 + 8 * slot, phase);
+                wide_issue(tile0 + slot * kTileBytes, &tmap, full0 + 8 * slot, x, (i + kWideNStage) * kWideTC);
+            }
+        };
+        if (NC == 1 && n == kWideTC && bt0 >= warm) {
+            // the warp converts its 2 traces' 32 samples to fp64 once (lane = tick) and validates them (A17), then
+            // releases the fp32 slot; each thread reads its trace's values from the warp's scratch
+            const float2 v = *reinterpret_cast<const float2*>(smem + slot * kTileBytes + lane * (kWideTpc * 4) +
+                                                             (tid >> 4 & ~1) * 4);
+            vmax = max(vmax, max(__float_as_uint(v.x), __float_as_uint(v.y)));
+            wbuf[lane] = (double)v.x;
+            wbuf[kWideTC + lane] = (double)v.y;
+            __syncwarp();
+            release();
+            const double* my = wbuf + ((tid >> 4) & 1) * kWideTC;
+#pragma unroll
+            for (int g = 0; g < kWideTC / 8; ++g) {
+                double d8[8];
+#pragma unroll
+                for (int t = 0; t < 8; ++t) d8[t] = my[8 * g + t];
+                wide_stage_d<K>(st[0], lockf[0], nthrf[0], wcmd[0], ss[0].sexc, d8, pol[0], Blo_d, bitc[0], mone);
+            }
+            __syncwarp();   // every lane has read the scratch before the next stage overwrites it
+        } else if (n == kWideTC && bt0 >= warm) {
 #pragma unroll
             for (int g = 0; g < kWideTC / 8; ++g) {
                 float d8[8];
@@ -210,6 +268,8 @@ __global__ void __launch_bounds__(kWideThreads / NC, 2)
                     ss[1].sexc = sx[1];
                 }
             }
+            __syncwarp();
+            release();
         } else {
             // warm-up block (Alg. 1 / Alg. 2 gated per tick) or the ragged last block of the trace
 #pragma unroll 1
@@ -224,13 +284,8 @@ __global__ void __launch_bounds__(kWideThreads / NC, 2)
                     acc_tick(ss[c], vmax, o, D, B_lo);
                 }
             }
-        }
-        // release the stage; warp 0 refills it with stage i + NSTAGE once all warps have released it
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive_u32(empty0 + 8 * slot);
-        if (warp == 0 && i + kWideNStage < n_st) {
-            ptx::mbar_wait_u32(empty0 + 8 * slot, phase);
-            wide_issue(tile0 + slot * kTileBytes, &tmap, full0 + 8 * slot, x, (i + kWideNStage) * kWideTC);
+            __syncwarp();
+            release();
         }
         if (++slot == kWideNStage) {
             slot = 0;
@@ -247,6 +302,9 @@ __global__ void __launch_bounds__(kWideThreads / NC, 2)
             else fold_block(ss[c], wcmd[c], (uint32_t)st[c].evh, fstart[c], n, i, wout);
         }
     }
+    // the validation maximum covers the warp's traces (the converting lanes saw both of its traces' samples); the
+    // precise first invalid (trace, tick) comes from magus_scan_invalid_kernel when any maximum is out of range
+    vmax = __reduce_max_sync(0xffffffffu, vmax);
 #pragma unroll
     for (int c = 0; c < NC; ++c)
         if (live[c]) {

@@ -652,6 +652,58 @@ def build_stage_w2(K, TC=8):
     return out
 
 
+def build_stage_w1d(K, TC=8):
+    """MAGUS_WSTAGE1D_K<K>: TC ticks of ONE MAGUS chain with the samples passed as fp64 registers (the wide kernel's
+    per-warp converted tile, replay_wide.cuh): MAGUS_WSTAGE1F_K<K> without the fp32 -> fp64 conversion, the throttle
+    test as the fp64 compare of the same exact values (D > B_lo at f_min, A14).  Decisions identical."""
+    names = [("f0", "+r")] + [(f"r0_{i}", "+d") for i in range(K)] + \
+            [("evh0", "+r"), ("cnt0", "+r"), ("exc0", "+d"), ("lock0", "+f"), ("nthr0", "+f"), ("wcmd0", "+r")]
+    inames = [(f"S{tt}", "d") for tt in range(TC)] + [("Blod", "d"), ("dinc", "d"), ("ddec", "d"), ("bitc", "r"),
+                                                     ("smin", "r"), ("one", "r"), ("mone", "r")]
+    idx = {n: f"%{i}" for i, (n, _) in enumerate(names + inames)}
+    R = idx.__getitem__
+    body = ["{", ".reg .pred phi, pthr, pinc, pev, phf, pq, pk;", f".reg .f64 dv, dx, ad<{TC}>;", ".reg .b32 tb;",
+            f"setp.ne.u32 phi, {R('f0')}, 0;"]
+    for tt in range(TC):
+        dd = R(f"S{tt}")
+        old = f"ad{tt - K}" if tt >= K else R(f"r0_{K - 1 - tt}")
+        body += [
+            f"setp.gt.and.f64 pthr, {dd}, {R('Blod')}, !phi;",             # throttled: f_min and D > B_lo (A14)
+            f"selp.f64 ad{tt}, {R('Blod')}, {dd}, pthr;",                   # A = min(D, B[f]) (exact)
+            f"sub.f64 dv, ad{tt}, {old};",                                  # Alg. 1 numerator A_t - A_{t-k} (P:207)
+            f"setp.gt.f64 pinc, dv, {R('dinc')};",                          # +1 (P:209)
+            f"setp.lt.or.f64 pev, dv, {R('ddec')}, pinc;",                  # tune flag (P:213, P:243)
+            f"and.b32 tb, {R('evh0')}, {R('bitc')};",                       # the flag leaving the C-window (scaled)
+            f"shl.b32 {R('evh0')}, {R('evh0')}, 1;",
+            f"@pev mad.lo.u32 {R('evh0')}, {R('one')}, {R('one')}, {R('evh0')};",
+            f"mad.lo.u32 {R('cnt0')}, tb, {R('mone')}, {R('cnt0')};",        # window count: - leaving + entering
+            f"@pev mad.lo.u32 {R('cnt0')}, {R('bitc')}, {R('one')}, {R('cnt0')};",
+            f"setp.ge.u32 phf, {R('cnt0')}, {R('smin')};",                  # Alg. 2 (P:230)
+            "not.pred pk, pev;",
+            "and.pred pk, pk, phi;",
+            "or.pred pq, pk, pinc;",                                       # +1 || (f_max && !flag)
+            "or.pred phi, pq, phf;",                                       # || lock: the new level
+            f"shl.b32 {R('wcmd0')}, {R('wcmd0')}, 1;",
+            f"@phi mad.lo.u32 {R('wcmd0')}, {R('one')}, {R('one')}, {R('wcmd0')};",
+            f"sub.f64 dx, {dd}, ad{tt};",                                   # throttling excess D - A (0 unless thr)
+            f"add.f64 {R('exc0')}, {R('exc0')}, dx;",
+            f"@phf add.f32 {R('lock0')}, {R('lock0')}, 0f3F800000;",
+            f"@pthr add.f32 {R('nthr0')}, {R('nthr0')}, 0f3F800000;",
+        ]
+    body.append(f"selp.u32 {R('f0')}, 1, 0, phi;")
+    for i in range(K):
+        body.append(f"mov.f64 {R(f'r0_{i}')}, ad{TC - 1 - i};")
+    body.append("}")
+    params = ", ".join(n for n, _ in names + inames)
+    name = f"MAGUS_WSTAGE1D_K{K}"
+    out = [f"#define {name}(...) {name}_(__VA_ARGS__)", f"#define {name}_({params}) \\", "    asm volatile( \\"]
+    out += [f'        "{l}\\n\\t" \\' for l in body]
+    out.append("        : " + ", ".join(f'"{c}"({n})' for n, c in names) + " \\")
+    out.append("        : " + ", ".join(f'"{c}"({n})' for n, c in inames) + " \\")
+    out.append('        : "memory")')
+    return out
+
+
 out = ["// GENERATED by scripts/gen_tick4.py -- do not edit.  One MAGUS tick for the 4 chains of a lane, the",
        "// four chains' instructions interleaved (DESIGN.md section 7); semantics = magus_tick<K, false, SLOW>.",
        "// cnt is the window count scaled by 2^(C-1).",
@@ -679,6 +731,8 @@ for K in range(1, 9):
     out += [""] + build_stage_wl(K)
 for K in range(1, 9):
     out += [""] + build_stage_w2(K)
+for K in range(1, 9):
+    out += [""] + build_stage_w1d(K)
 path = os.path.join(os.path.dirname(__file__), "..", "paper_2502_03796_b200", "csrc", "tick4_asm.cuh")
 open(path, "w").write("\n".join(out) + "\n")
 print("wrote", os.path.normpath(path))
