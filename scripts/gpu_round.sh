@@ -6,7 +6,7 @@ OUT=gpurun_out
 mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total,driver_version --format=csv > $OUT/${TAG}_smi.txt
 (nproc; lscpu | grep "Model name") > $OUT/${TAG}_host.txt
-timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > $OUT/${TAG}_pytest_gpu.log 2>&1
+timeout 1500 python -m pytest tests -m gpu -q -s -p no:cacheprovider --timeout 600 > $OUT/${TAG}_pytest_gpu.log 2>&1
 echo "pytest rc=$?" >> $OUT/${TAG}_pytest_gpu.log
 timeout 900 python bench.py > $OUT/${TAG}_bench.json 2> $OUT/${TAG}_bench.err
 echo "bench rc=$?" >> $OUT/${TAG}_bench.err
