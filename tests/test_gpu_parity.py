@@ -329,6 +329,34 @@ def test_decision_dump_decoded_from_replay_words(M, name, segments, monkeypatch)
     print(f"{name}: {dec.n_mismatched_segments} wrong speculative entries walked (their blocks' words rewritten)")
 
 
+@pytest.mark.parametrize("case", ["long-trace", "long-trace-wide", "many-traces"])
+def test_large_shapes(M, case, monkeypatch):
+    """Maximum-size edges: traces longer than 2^24 ticks (the solo kernel's fp32 per-segment counters force a second
+    segment even when one is requested; the wide kernel flushes its counters per 32-tick block) and a very wide
+    trace set (300,000 traces: grid sizes, the per-trace records).  Records, totals (and the words of the long
+    traces) against the oracle."""
+    if case.startswith("long-trace"):
+        n, ns, segments = 4, (1 << 24) + 101, (1 if case == "long-trace" else 0)
+        pols = CONFIGS[2]["policies"] if case == "long-trace" else [pol(deriv_ticks=k) for k in (1, 2, 4, 8)]
+        if case == "long-trace-wide":
+            monkeypatch.setenv("MAGUS_WIDE", "1")
+        flags = M.F_PER_TRACE_STATS | M.F_DUMP_WORDS
+    else:
+        n, ns, segments, pols, flags = 300_000, 64, 0, CONFIGS[5]["policies"], M.F_PER_TRACE_STATS
+    stride = (n + 3) // 4 * 4
+    tr, w = gpu_gen(M, 77, n, ns, 1, stride)
+    res = run_gpu(M, tr, w, pols, n, ns, stride, flags=flags, segments=segments)
+    if case == "long-trace":
+        assert res.n_segments == 2, res.geometry    # the 2^24-tick cap
+    if case == "long-trace-wide":
+        assert res.geometry["wide_groups"] > 0 and res.n_segments == 1, res.geometry
+    rec, codes = oracle_run(tr.cpu().numpy(), w.cpu().numpy(), pols, n)
+    PA.compare_records(res.per_trace, rec, case)
+    PA.compare_totals(res.totals, rec)
+    if flags & M.F_DUMP_WORDS:
+        assert np.array_equal(res.words, PA.pack_words(codes))
+
+
 @pytest.mark.parametrize("n,ns", [(1, 1), (1, 31), (3, 33), (5, 32), (128, 64), (129, 95), (4, 1000)])
 def test_tiny_and_ragged(M, n, ns):
     stride = (n + 3) // 4 * 4
