@@ -854,8 +854,11 @@ static void choose_geometry(magus_replay_t* h, int n_sm, int forced_segments) {
         const int tnp = std::min(tnp_env, g.nq);   // one TDP policy: no idle second chain set per lane
         if (g.key == 1000 + LANE_TDP && kTC == 8 && (tnp_env == 1 || tnp_env == 2)) {
             g.solo = true;
-            g.kernel = tnp == 1 ? (ReplayKernel)magus_replay_tsolo_kernel<1, kTC, kNStage>
-                                : (ReplayKernel)magus_replay_tsolo_kernel<2, kTC, kNStage>;
+            // the first launch group validates the samples (A17); a later TDP group skips the maximum
+            const bool first = &g == &h->groups.front();
+            g.kernel = tnp == 2 ? (ReplayKernel)magus_replay_tsolo_kernel<2, kTC, kNStage>
+                       : first  ? (ReplayKernel)magus_replay_tsolo_kernel<1, kTC, kNStage, true>
+                                : (ReplayKernel)magus_replay_tsolo_kernel<1, kTC, kNStage, false>;
             g.ng = 1;
             g.npw = 1;
             g.n_tblocks = p.n_groups;

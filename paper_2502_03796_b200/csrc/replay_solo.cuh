@@ -673,7 +673,13 @@ __global__ void __launch_bounds__(32, kSoloCtasPerSm)
 // level (f_max); the exact fix-up is the TDP lockstep walk.
 // The TDP solo replay of one (policy pair pi, tile group, segment) by one warp on a primed TMA ring.  COMBO: the ring
 // is shared with the MAGUS warp of magus_replay_combo_kernel, which refills it; this warp only releases its slots.
-template <int NP, int TC, int NSTAGE, bool COMBO>
+#ifndef MAGUS_TDP_LEAN
+#define MAGUS_TDP_LEAN 0   // build switch: 1 = MAGUS_TSTAGE1L{V} (two-compare level, no select, validation only in
+                           // the first group): measured slower on config 5 (0.624 vs 0.607 ms, profiles/r02_tdp_lean_ab.txt)
+#endif
+// VALIDATE: this launch group takes the validation maximum (A17); the other groups of a run skip it, since every
+// group replays the same samples and the check is over the union of all lanes' maxima (one TDP policy per warp).
+template <int NP, int TC, int NSTAGE, bool COMBO, bool VALIDATE = true>
 __device__ __forceinline__ void tsolo_body(const CUtensorMap* tmap, const ReplayParams& p, const uint8_t* smem,
                                            uint32_t tile0, uint32_t bar0, uint32_t empty0, int pi, int tgroup, int seg,
                                            int lane) {
@@ -698,6 +704,7 @@ __device__ __forceinline__ void tsolo_body(const CUtensorMap* tmap, const Replay
     float ahi[NP], alo[NP];
     uint32_t f[NC], wcmd[NC], fstart[NC];
     double exc[NC];
+    double sfac[4] = {0.0, 0.0, 0.0, 0.0};   // MAGUS_TSTAGE1L: the throttled 0/1 factors (low words stay 0)
     float nthrf[NC];
     uint32_t nhi[NC], trans[NC], dc[NC];
     uint32_t one = 1, vmax = 0;
@@ -746,10 +753,18 @@ __device__ __forceinline__ void tsolo_body(const CUtensorMap* tmap, const Replay
             const uint32_t tile = tile0 + slot * kTileBytes;
             mbar_wait_loop(bar0 + 8 * slot, phase);
             if (t0 + TC <= G.seg_end) {
-                if constexpr (NP == 1)
+                if constexpr (NP == 1 && !MAGUS_TDP_LEAN)
                     MAGUS_TSTAGE1(f[0], f[1], f[2], f[3], exc[0], exc[1], exc[2], exc[3], nthrf[0], nthrf[1], nthrf[2],
                                   nthrf[3], wcmd[0], wcmd[1], wcmd[2], wcmd[3], vmax, tile + lane_off, B_lo, ahi[0],
                                   alo[0], one);
+                else if constexpr (NP == 1 && VALIDATE)
+                    MAGUS_TSTAGE1LV(f[0], f[1], f[2], f[3], exc[0], exc[1], exc[2], exc[3], nthrf[0], nthrf[1],
+                                    nthrf[2], nthrf[3], wcmd[0], wcmd[1], wcmd[2], wcmd[3], sfac[0], sfac[1], sfac[2],
+                                    sfac[3], vmax, tile + lane_off, B_lo, ahi[0], alo[0], one);
+                else if constexpr (NP == 1)
+                    MAGUS_TSTAGE1L(f[0], f[1], f[2], f[3], exc[0], exc[1], exc[2], exc[3], nthrf[0], nthrf[1],
+                                   nthrf[2], nthrf[3], wcmd[0], wcmd[1], wcmd[2], wcmd[3], sfac[0], sfac[1], sfac[2],
+                                   sfac[3], tile + lane_off, B_lo, ahi[0], alo[0], one);
                 else
                     MAGUS_TSTAGE2(f[0], f[1], f[2], f[3], f[4], f[5], f[6], f[7], exc[0], exc[1], exc[2], exc[3],
                                   exc[4], exc[5], exc[6], exc[7], nthrf[0], nthrf[1], nthrf[2], nthrf[3], nthrf[4],
@@ -829,7 +844,7 @@ __device__ __forceinline__ void tsolo_body(const CUtensorMap* tmap, const Replay
     if (j0 < p.n_traces) atomicMax(p.c_vmax + chain_idx(p, qs[0], j0), vmax);
 }
 
-template <int NP, int TC, int NSTAGE>
+template <int NP, int TC, int NSTAGE, bool VALIDATE = true>
 __global__ void __launch_bounds__(32, kSoloCtasPerSm)
     magus_replay_tsolo_kernel(const __grid_constant__ CUtensorMap tmap, const ReplayParams p) {
     using SM = SoloSmem<TC, NSTAGE>;
@@ -856,7 +871,7 @@ __global__ void __launch_bounds__(32, kSoloCtasPerSm)
     for (int i = 0; i < NSTAGE && i < G.n_stages; ++i)
         solo_issue<TC>(tile0 + i * kTileBytes, &tmap, bar0 + 8 * i, tgroup * kTracesPerWarp, G.tau_w + i * TC, cpol);
     ptx::pdl_wait();
-    tsolo_body<NP, TC, NSTAGE, false>(&tmap, p, smem, tile0, bar0, 0u, pi, tgroup, seg, lane);
+    tsolo_body<NP, TC, NSTAGE, false, VALIDATE>(&tmap, p, smem, tile0, bar0, 0u, pi, tgroup, seg, lane);
 }
 
 // ===================================================================================================================
@@ -900,7 +915,7 @@ __global__ void __launch_bounds__(64, kSoloCtasPerSm / 2)
         ReplayParams pt = p;
         pt.q_base = p.q_base2;
         pt.nq = p.nq2;
-        tsolo_body<NP, TC, NSTAGE, true>(&tmap, pt, smem, tile0, bar0, empty0, 0, tgroup, seg, lane);
+        tsolo_body<NP, TC, NSTAGE, true, false>(&tmap, pt, smem, tile0, bar0, empty0, 0, tgroup, seg, lane);
     }
 }
 

@@ -704,6 +704,64 @@ def build_stage_w1d(K, TC=8):
     return out
 
 
+def build_stage_t1(validate):
+    """MAGUS_TSTAGE1L{V}: one steady stage (8 ticks x 4 traces) of ONE TDP_DEFAULT policy (the TDP solo kernel, NP = 1)
+    with fewer instructions than MAGUS_TSTAGE1: the next level as two fp32 compares without a select,
+        f' = (D < a_hi) | (!f & D < a_lo)   (= D < a[f], because a_lo >= a_hi: a*[f] is monotone in P[f], P_lo <= P_hi,
+                                             and a_lo is a*_lo or +inf),
+    the 0/1 factor of the throttled-demand DFMA kept in a persistent register pair whose low word stays 0 (only the
+    high word is rewritten per tick: no zeroing move), and the validation maximum only when V (the first launch
+    group validates every sample; the union of all lanes' maxima is what is checked, A17)."""
+    C, TC = 4, 8
+    names = [(f"f{c}", "+r") for c in range(C)] + [(f"exc{c}", "+d") for c in range(C)] + \
+            [(f"nthr{c}", "+f") for c in range(C)] + [(f"wcmd{c}", "+r") for c in range(C)] + \
+            [(f"s{c}", "+d") for c in range(C)] + ([("vmax", "+r")] if validate else [])
+    inames = [("tile", "r"), ("Blo", "f"), ("ahi", "f"), ("alo", "f"), ("one", "r")]
+    idx = {n: f"%{i}" for i, (n, _) in enumerate(names + inames)}
+    R = idx.__getitem__
+    body = ["{", f".reg .pred phi<{C}>, pthr<{C}>, pt<{C}>;", f".reg .b32 D<{TC * 4}>, slo<{C}>, shi<{C}>;",
+            ".reg .f64 dd<4>;"]
+    for c in range(C):
+        body.append(f"setp.ne.u32 phi{c}, {R(f'f{c}')}, 0;")
+        body.append(f"mov.b64 {{slo{c}, shi{c}}}, {R(f's{c}')};")
+    for tt in range(TC):
+        body.append(f"ld.shared.v4.f32 {{D{tt * 4}, D{tt * 4 + 1}, D{tt * 4 + 2}, D{tt * 4 + 3}}}, [{R('tile')}+{tt * 512}];")
+        for u in range(4):
+            body.append(f"cvt.f64.f32 dd{u}, D{tt * 4 + u};")
+        if validate:
+            body.append(f"max.u32 {R('vmax')}, {R('vmax')}, D{tt * 4};")
+            body.append(f"max.u32 {R('vmax')}, {R('vmax')}, D{tt * 4 + 1};")
+            body.append(f"max.u32 {R('vmax')}, {R('vmax')}, D{tt * 4 + 2};")
+            body.append(f"max.u32 {R('vmax')}, {R('vmax')}, D{tt * 4 + 3};")
+        per_chain = [
+            "setp.gt.and.f32 pthr{c}, {D}, {Blo}, !phi{c};",             # throttled (A14)
+            "setp.lt.and.f32 pt{c}, {D}, {alo}, !phi{c};",               # at f_min: A < a*_lo (A24)
+            "setp.lt.or.f32 phi{c}, {D}, {ahi}, pt{c};",                 # next level f_max iff A < a*[f]
+            "selp.b32 shi{c}, 0x3FF00000, 0, pthr{c};",                  # 1.0 if throttled, else 0.0 (low word 0)
+            "mov.b64 {s}, {{slo{c}, shi{c}}};",
+            "fma.rn.f64 {exc}, {s}, dd{u}, {exc};",                      # sum of D over throttled ticks (exact)
+            "@pthr{c} add.f32 {nthr}, {nthr}, 0f3F800000;",
+            "shl.b32 {wcmd}, {wcmd}, 1;",
+            "@phi{c} mad.lo.u32 {wcmd}, {one}, {one}, {wcmd};",
+        ]
+        for tmpl in per_chain:
+            for c in range(C):
+                body.append(tmpl.format(c=c, u=c, D=f"D{tt * 4 + c}", Blo=R("Blo"), ahi=R("ahi"), alo=R("alo"),
+                                        s=R(f"s{c}"), exc=R(f"exc{c}"), nthr=R(f"nthr{c}"), wcmd=R(f"wcmd{c}"),
+                                        one=R("one")))
+    for c in range(C):
+        body.append(f"selp.u32 {R(f'f{c}')}, 1, 0, phi{c};")
+    body.append("}")
+    params = ", ".join(n for n, _ in names + inames)
+    name = f"MAGUS_TSTAGE1L{'V' if validate else ''}"
+    out = [f"#define {name}(...) {name}_(__VA_ARGS__)", f"#define {name}_({params}) \\", "    asm volatile( \\"]
+    out += [f'        "{l}\\n\\t" \\' for l in body]
+    out.append("        : " + ", ".join(f'"{c}"({n})' for n, c in names) + " \\")
+    out.append("        : " + ", ".join(f'"{c}"({n})' for n, c in inames) + " \\")
+    out.append('        : "memory")')
+    return out
+
+
 out = ["// GENERATED by scripts/gen_tick4.py -- do not edit.  One MAGUS tick for the 4 chains of a lane, the",
        "// four chains' instructions interleaved (DESIGN.md section 7); semantics = magus_tick<K, false, SLOW>.",
        "// cnt is the window count scaled by 2^(C-1).",
@@ -733,6 +791,8 @@ for K in range(1, 9):
     out += [""] + build_stage_w2(K)
 for K in range(1, 9):
     out += [""] + build_stage_w1d(K)
+for v in (True, False):
+    out += [""] + build_stage_t1(v)
 path = os.path.join(os.path.dirname(__file__), "..", "paper_2502_03796_b200", "csrc", "tick4_asm.cuh")
 open(path, "w").write("\n".join(out) + "\n")
 print("wrote", os.path.normpath(path))
