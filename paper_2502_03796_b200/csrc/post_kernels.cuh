@@ -700,7 +700,10 @@ __global__ void __launch_bounds__(128) magus_fix_walk_kernel(const ReplayParams 
 // One thread per (trace, policy): the chain's totals -> the closed-form record (section 8), STATIC_MAX
 // records from their closed form (at f_max A = D <= bw_max: never throttled, never a transition or a
 // tune flag, digest of an all-f_max command stream, A17 / A21); then fixed-order per-policy sums.
-constexpr int kTotThreads = 256;       // = traces per chunk
+#ifndef MAGUS_TOT_THREADS
+#define MAGUS_TOT_THREADS 256
+#endif
+constexpr int kTotThreads = MAGUS_TOT_THREADS;   // = traces per chunk
 constexpr int kNTot = 13;              // MAGUS_N_TOTALS
 
 // Block (p, c): the closed-form records of policy p for traces [256 c, 256 c + 256), one per thread (written
@@ -888,7 +891,10 @@ __global__ void magus_fill_codes_kernel(uint8_t* codes, int64_t n_rows, int P, i
 // first_low[n + j] = the first subsampled tick (stride `sub`) with D <= B_lo / D > B_lo, or INT_MAX.
 // Block = 32 traces x 32 row slices; each thread scans its slice in increasing t, the slices are
 // reduced in shared memory.  Pure performance hint: a wrong guess only costs a re-run.
-constexpr int kPrepassTraces = 32, kPrepassSlices = 32;
+#ifndef MAGUS_PREPASS_TRACES
+#define MAGUS_PREPASS_TRACES 32
+#endif
+constexpr int kPrepassTraces = MAGUS_PREPASS_TRACES, kPrepassSlices = 1024 / MAGUS_PREPASS_TRACES;
 __global__ void __launch_bounds__(kPrepassTraces * kPrepassSlices)
     magus_prepass_kernel(const float* __restrict__ trace, int n_traces, int n_samples, int64_t stride, float B_lo,
                          int sub, int* __restrict__ first_low, uint32_t* __restrict__ zero_a, int n_zero_a) {
