@@ -61,7 +61,8 @@ _lib = None
 def lib():
     global _lib
     if _lib is None:
-        path = _build.build()
+        # MAGUS_ORACLE_LIB: another build of the oracle (scripts/oracle_sanitize.sh: ASan + UBSan)
+        path = os.environ.get("MAGUS_ORACLE_LIB") or _build.build()
         L = C.CDLL(path)
         L.oracle_alg1.restype = C.c_int
         L.oracle_alg1.argtypes = [C.c_double, C.c_double, C.POINTER(C.c_double), C.c_int32, C.c_double]
