@@ -292,7 +292,11 @@ def run_ours(args, cfg):
                 "kernel": ("magus_wallclock_em_kernel" if args.wallclock else
                            "magus_replay_solo_kernel" if geo.get("solo_groups") else "magus_replay_kernel"),
                 "replay_ms": tsum["replay_ms"], "replay_ms_max_over_ranks": replay_ms_max,
-                "bytes_per_launch": bytes_per_launch, "peak_source": peak_src}
+                "bytes_per_launch": bytes_per_launch, "peak_source": peak_src,
+                # the algorithmic bytes count each sample once; every replay launch group (one per chain kind,
+                # concurrent) streams the trace itself, so DRAM reads ~ launch_groups x bytes_per_launch (config 5:
+                # MAGUS + TDP = 2; MAGUS_COMBO=1 reads it once, slower -- DESIGN.md section 14)
+                "launch_groups_streaming_trace": geo.get("launch_groups")}
     if geo.get("wide_groups") and not args.wallclock:
         roofline = alu_roofline(cfg, n, ns, geo["lane_policies"], tsum["replay_ms"], replay_ms_max)
 
