@@ -196,8 +196,12 @@ ReplayKernel combo_kernel_for(int key, int np) {
 }
 
 // one-warp-CTA replay kernel (replay_solo.cuh) of a chain kind, or nullptr if it has none
-ReplayKernel solo_kernel_for(int key, bool sym, bool bits_ok) {
-    int v = env_int("MAGUS_SOLO_BAL", 2);   // stage block variant (replay_solo.cuh)
+ReplayKernel solo_kernel_for(int key, bool sym, bool bits_ok, bool lsign_ok) {
+    int v = env_int("MAGUS_SOLO_BAL", 20);   // stage block variant (replay_solo.cuh)
+    // 20: the L stage (level in the cmd word, lock = sign of the biased window count; needs C <= 27), with the
+    // |d| tune-flag test (21) when every lane policy has d*_dec == -d*_inc; 22 forces the two-compare L stage
+    if (v == 20 || v == 22) v = !lsign_ok ? 2 : (v == 20 && sym) ? 21 : 20;
+    else if (v == 21 && !(sym && lsign_ok)) v = 2;
     if (v == 9) v = 2;   // PSTAGES (|d| test + popcount): slower than 2 and it failed parity on mixed-kinds (round 2)
     if (v == 5 && !bits_ok) v = 2;          // the integer sample conversion needs |d*| >= 2^-60, B_lo normal
     if (v >= 10 && v <= 17) {   // the unified-stage kernel; v - 10 = VAR bits (1 |d| test, 2 incremental count,
@@ -232,6 +236,8 @@ ReplayKernel solo_kernel_for(int key, bool sym, bool bits_ok) {
      : v == 3 ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 3>                    \
      : v == 4 ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 4>                    \
      : v == 5 ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 5>                    \
+     : v == 20 ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 20>                  \
+     : v == 21 ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 21>                  \
               : (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 1>)
     switch (key) {
         case 1: return SOLO_K(1);
@@ -745,7 +751,7 @@ static void choose_geometry(magus_replay_t* h, int n_sm, int forced_segments) {
     const bool combo = h->groups.size() == 2 && h->groups[0].key >= 1 && h->groups[0].key <= 3 &&
                        h->groups[0].nq == 1 && h->groups[1].key == 1000 + LANE_TDP && h->groups[1].nq <= 2 &&
                        kTC == 8 && env_int("MAGUS_COMBO", 0) != 0 && env_int("MAGUS_SOLO", 1) != 0 &&
-                       env_int("MAGUS_SOLO_BAL", 2) == 2 && env_int("MAGUS_TDP_SOLO", 2) == 2;
+                       env_int("MAGUS_SOLO_BAL", 20) == 20 && env_int("MAGUS_TDP_SOLO", 2) == 2;
     int W = d.tuning_warmup > 0 ? d.tuning_warmup
                                 : ((kmax + cmax - 1 + 31) / 32) * 32 + env_int("MAGUS_WARMUP_EXTRA", 0) + h->warm_extra;
     W = ((std::max(W, kmax + cmax - 1) + 31) / 32) * 32;
@@ -832,12 +838,14 @@ static void choose_geometry(magus_replay_t* h, int n_sm, int forced_segments) {
         // the integer fp32 -> fp64 sample conversion changes no decision when both thresholds are >= 2^-60 in
         // magnitude and B_lo is a normal fp32
         bool bits_ok = h->B_lo >= 0x1p-126f;
+        bool lsign_ok = true;   // the L stage's biased scaled count stays within int32: C <= 27
         for (int q = g.q_base; q < g.q_base + g.nq; ++q) {
             const DevPolicy& lp = h->lane[q];
             sym = sym && lp.ddec == -lp.dinc;
             bits_ok = bits_ok && lp.dinc >= 0x1p-60 && lp.ddec <= -0x1p-60;
+            lsign_ok = lsign_ok && lp.C <= 27;
         }
-        ReplayKernel sk = solo_kernel_for(g.key, sym, bits_ok);
+        ReplayKernel sk = solo_kernel_for(g.key, sym, bits_ok, lsign_ok);
         g.solo = sk && g.npw == 1 && kTC == 8 && env_int("MAGUS_SOLO", 1) != 0;
         if (g.solo) {
             g.kernel = sk;

@@ -206,6 +206,43 @@ __device__ __forceinline__ void solo_stage(MagusState<K, false>* s, float* lock,
     s[3].evh = e3;
 }
 
+// One whole steady-state stage (8 ticks x 4 chains) with the level carried in the cmd word and the lock as the sign
+// of the biased window count (MAGUS_LSTAGE_K<K>, BAL = 20).  The caller keeps s[c].cnt biased by -smin_sc and
+// wcmd[c]'s bit 0 = the level across the steady stages; nlk[c] counts the ticks not locked.
+template <int K, bool SYM>
+__device__ __forceinline__ void solo_stage_l(MagusState<K, false>* s, uint32_t* nlk, float* nthr, uint32_t* wcmd,
+                                             SegStats* ss, uint32_t& vmax, uint32_t tile, const SoloConst& sc,
+                                             const DevPolicy& pol) {
+    uint32_t e0 = s[0].evh, e1 = s[1].evh, e2 = s[2].evh, e3 = s[3].evh;
+    const uint32_t bitc = 1u << (pol.C - 1), mone = 0xFFFFFFFFu * pol.one;
+#define LS_TAIL                                                                                                \
+    e0, e1, e2, e3, s[0].cnt, s[1].cnt, s[2].cnt, s[3].cnt, ss[0].sexc, ss[1].sexc, ss[2].sexc, ss[3].sexc, nlk[0],  \
+        nlk[1], nlk[2], nlk[3], nthr[0], nthr[1], nthr[2], nthr[3], wcmd[0], wcmd[1], wcmd[2], wcmd[3], vmax, tile,  \
+        sc.B_lo, sc.Blo_d, pol.dinc, pol.ddec, bitc, pol.one, mone
+#define LS_R2                                                                                                  \
+    s[0].ring.v[0], s[0].ring.v[1], s[1].ring.v[0], s[1].ring.v[1], s[2].ring.v[0], s[2].ring.v[1], s[3].ring.v[0], \
+        s[3].ring.v[1]
+#define LS_R3                                                                                                  \
+    s[0].ring.v[0], s[0].ring.v[1], s[0].ring.v[2], s[1].ring.v[0], s[1].ring.v[1], s[1].ring.v[2], s[2].ring.v[0], \
+        s[2].ring.v[1], s[2].ring.v[2], s[3].ring.v[0], s[3].ring.v[1], s[3].ring.v[2]
+    if constexpr (SYM) {   // d*_dec == -d*_inc: the |d| tune-flag test
+        if constexpr (K == 1) MAGUS_LSTAGES_K1(s[0].ring.v[0], s[1].ring.v[0], s[2].ring.v[0], s[3].ring.v[0], LS_TAIL);
+        else if constexpr (K == 2) MAGUS_LSTAGES_K2(LS_R2, LS_TAIL);
+        else MAGUS_LSTAGES_K3(LS_R3, LS_TAIL);
+    } else {
+        if constexpr (K == 1) MAGUS_LSTAGE_K1(s[0].ring.v[0], s[1].ring.v[0], s[2].ring.v[0], s[3].ring.v[0], LS_TAIL);
+        else if constexpr (K == 2) MAGUS_LSTAGE_K2(LS_R2, LS_TAIL);
+        else MAGUS_LSTAGE_K3(LS_R3, LS_TAIL);
+    }
+#undef LS_R2
+#undef LS_R3
+#undef LS_TAIL
+    s[0].evh = e0;
+    s[1].evh = e1;
+    s[2].evh = e2;
+    s[3].evh = e3;
+}
+
 // The MAGUS solo replay of one (lane policy q, tile group, segment) by one warp, on a TMA ring that the caller has
 // initialised and primed with the first NSTAGE stages.  COMBO = false: the warp owns the ring and refills a slot
 // right after its own __syncwarp.  COMBO = true (magus_replay_combo_kernel): a second warp (the TDP baselines)
@@ -242,6 +279,8 @@ __device__ __forceinline__ void solo_magus_body(const CUtensorMap* tmap, const R
     SegStats ss[kChains];
     uint32_t wcmd[kChains], fstart[kChains];
     float lockf[kChains], nthrf[kChains];   // counts as exact fp32 integers (segment length <= 2^24)
+    uint32_t nlk[kChains];   // BAL 20: ticks not locked in the counted steady blocks (lock = lockf + 32 nsb - nlk)
+    uint32_t nsb = 0;        // BAL 20: counted steady blocks
     uint32_t vmax = 0;
 #pragma unroll
     for (int c = 0; c < kChains; ++c) {
@@ -249,6 +288,7 @@ __device__ __forceinline__ void solo_magus_body(const CUtensorMap* tmap, const R
         ss[c].zero();
         wcmd[c] = 0;
         lockf[c] = nthrf[c] = 0.f;
+        nlk[c] = 0;
     }
 
     int i = 0;           // stage index (CTA-uniform)
@@ -261,7 +301,9 @@ __device__ __forceinline__ void solo_magus_body(const CUtensorMap* tmap, const R
                 if (j0 + c < p.n_traces) T::save(st[c], p, pol, 0, q, seg, j0 + c);
                 ss[c].zero();
                 lockf[c] = nthrf[c] = 0.f;
+                nlk[c] = 0;
             }
+            nsb = 0;
         }
         if (bt0 == G.tau_w && seg > 0) {
             // speculative level at the warm-up start: f_max iff the trace is above B_lo
@@ -294,6 +336,14 @@ __device__ __forceinline__ void solo_magus_body(const CUtensorMap* tmap, const R
         const bool counting = bt0 >= G.seg_start;
         if (bt0 + 32 <= G.seg_end && bt0 - G.tau_w >= warm_ticks) {
             // steady state: four whole-stage PTX blocks
+            if constexpr (BAL == 20 || BAL == 21) {   // the count biased by -s_min << (C-1); the level in the cmd word's bit 0
+#pragma unroll
+                for (int c = 0; c < kChains; ++c) {
+                    st[c].cnt -= pol.smin_sc;
+                    wcmd[c] = T::level(st[c]);
+                }
+                if (counting) ++nsb;
+            }
 #if MAGUS_SOLO_UNROLL == 2
 #pragma unroll 2
 #else
@@ -307,8 +357,10 @@ __device__ __forceinline__ void solo_magus_body(const CUtensorMap* tmap, const R
                     solo_stage<T::kRingK, true>(st, lockf, nthrf, wcmd, ss, vmax, tile + lane_off, sc, pol);
                 else if constexpr (BAL == 5)
                     solo_stage<T::kRingK, true, true>(st, lockf, nthrf, wcmd, ss, vmax, tile + lane_off, sc, pol);
-                else if constexpr (BAL == 3 || BAL == 4 || BAL >= 9)
+                else if constexpr (BAL == 3 || BAL == 4 || (BAL >= 9 && BAL < 20))
                     solo_stage_pq<T::kRingK, BAL>(st, lockf, nthrf, wcmd, ss, vmax, tile + lane_off, sc, pol);
+                else if constexpr (BAL == 20 || BAL == 21)
+                    solo_stage_l<T::kRingK, BAL == 21>(st, nlk, nthrf, wcmd, ss, vmax, tile + lane_off, sc, pol);
                 else T::stage8(st, tile + lane_off, pol, B_lo, Blo_d, wcmd, ss, vmax);
                 __syncwarp();   // every lane's tile reads are complete before the slot is refilled
                 solo_release<TC, COMBO>(tile, tmap, bar0, empty0, slot, phase, i + NSTAGE < G.n_stages, x,
@@ -317,6 +369,13 @@ __device__ __forceinline__ void solo_magus_body(const CUtensorMap* tmap, const R
                 if (++slot == NSTAGE) {
                     slot = 0;
                     phase ^= 1u;
+                }
+            }
+            if constexpr (BAL == 20 || BAL == 21) {
+#pragma unroll
+                for (int c = 0; c < kChains; ++c) {
+                    st[c].cnt += pol.smin_sc;
+                    T::set_level(st[c], wcmd[c] & 1u);
                 }
             }
         } else {
@@ -390,7 +449,8 @@ __device__ __forceinline__ void solo_magus_body(const CUtensorMap* tmap, const R
         const int j = j0 + c;
         if (j >= p.n_traces) continue;
         add_to_chain(p, q, j, ss[c].nhi, ss[c].nthr + (uint32_t)nthrf[c], ss[c].trans, ss[c].ev,
-                     ss[c].lock + (uint32_t)lockf[c], ss[c].sexc, ss[c].digest());
+                     ss[c].lock + (uint32_t)lockf[c] + (BAL == 20 || BAL == 21 ? 32u * nsb - nlk[c] : 0u), ss[c].sexc,
+                     ss[c].digest());
     }
     if (j0 < p.n_traces) atomicMax(p.c_vmax + chain_idx(p, q, j0), vmax);   // lane-level validation maximum
 }
