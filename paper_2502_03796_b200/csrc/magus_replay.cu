@@ -166,8 +166,13 @@ WallKernel wall_kernel_for(int key, int64_t n_chains, int n_sm) {
 }
 
 // unsegmented one-chain-per-lane replay kernel (replay_wide.cuh) of a chain kind, or nullptr if it has none
-ReplayKernel wide_kernel_for(int key, int nc) {
-#define WIDE_K(KK) (nc == 1 ? (ReplayKernel)magus_replay_wide_kernel<KK, 1> : (ReplayKernel)magus_replay_wide_kernel<KK, 2>)
+// lv: 0 = the MAGUS_WSTAGE1D block, 1 = its L form, 2 = the L form with the |d| test (replay_wide.cuh; nc = 1 only)
+ReplayKernel wide_kernel_for(int key, int nc, int lv = 0) {
+#define WIDE_K(KK)                                                                                                  \
+    (nc == 2    ? (ReplayKernel)magus_replay_wide_kernel<KK, 2, 0>                                                  \
+     : lv == 1 ? (ReplayKernel)magus_replay_wide_kernel<KK, 1, 1>                                                   \
+     : lv == 2 ? (ReplayKernel)magus_replay_wide_kernel<KK, 1, 2>                                                   \
+               : (ReplayKernel)magus_replay_wide_kernel<KK, 1, 0>)
     switch (key) {
         case 1: return WIDE_K(1);
         case 2: return WIDE_K(2);
@@ -193,6 +198,23 @@ ReplayKernel combo_kernel_for(int key, int np) {
         default: return nullptr;
     }
 #undef COMBO_K
+}
+
+// the fused one-warp MAGUS + TDP kernel (replay_solo.cuh) for a MAGUS chain kind with an L stage block: `sym` = the
+// |d| tune-flag test (d*_dec == -d*_inc), `ctas` = resident CTAs per SM it is built for (12: 168 registers, 16: 128)
+ReplayKernel fused_kernel_for(int key, bool sym, int ctas) {
+#define FUSED_K(KK)                                                                                                 \
+    (ctas == 16 ? (sym ? (ReplayKernel)magus_replay_fused_kernel<MagusTicker<KK, false>, kTC, kNStage, true, 16>       \
+                       : (ReplayKernel)magus_replay_fused_kernel<MagusTicker<KK, false>, kTC, kNStage, false, 16>)     \
+                : (sym ? (ReplayKernel)magus_replay_fused_kernel<MagusTicker<KK, false>, kTC, kNStage, true, 12>       \
+                       : (ReplayKernel)magus_replay_fused_kernel<MagusTicker<KK, false>, kTC, kNStage, false, 12>))
+    switch (key) {
+        case 1: return FUSED_K(1);
+        case 2: return FUSED_K(2);
+        case 3: return FUSED_K(3);
+        default: return nullptr;
+    }
+#undef FUSED_K
 }
 
 // one-warp-CTA replay kernel (replay_solo.cuh) of a chain kind, or nullptr if it has none
@@ -733,7 +755,15 @@ static void choose_geometry(magus_replay_t* h, int n_sm, int forced_segments) {
             // chains per thread: 1; MAGUS_WIDE_NC=2: two policy points sharing the samples (7% fewer instructions,
             // but measured slower: cfg 3 10.7 vs 7.0 ms, profiles/r02_cfg3_wide.txt)
             const int nc = env_int("MAGUS_WIDE_NC", 1) == 2 ? 2 : 1;
-            g.kernel = wide_kernel_for(g.key, nc);
+            // the L stage (MAGUS_WIDE_L, default 1) when every lane policy has C <= 27, with
+            // the |d| tune-flag test when every one has d*_dec == -d*_inc
+            bool sym = true, lsign_ok = true;
+            for (int q = g.q_base; q < g.q_base + g.nq; ++q) {
+                sym = sym && h->lane[q].ddec == -h->lane[q].dinc;
+                lsign_ok = lsign_ok && h->lane[q].C <= 27;
+            }
+            const int lv = (env_int("MAGUS_WIDE_L", 1) != 0 && lsign_ok) ? (sym ? 2 : 1) : 0;
+            g.kernel = wide_kernel_for(g.key, nc, lv);
             g.ng = 1;
             g.npw = 1;
             g.n_pblocks = (g.nq + kWidePpc - 1) / kWidePpc;
@@ -752,6 +782,15 @@ static void choose_geometry(magus_replay_t* h, int n_sm, int forced_segments) {
                        h->groups[0].nq == 1 && h->groups[1].key == 1000 + LANE_TDP && h->groups[1].nq <= 2 &&
                        kTC == 8 && env_int("MAGUS_COMBO", 0) != 0 && env_int("MAGUS_SOLO", 1) != 0 &&
                        env_int("MAGUS_SOLO_BAL", 20) == 20 && env_int("MAGUS_TDP_SOLO", 2) == 2;
+    // One MAGUS solo policy (k <= 3, C <= 27) next to ONE TDP_DEFAULT baseline (config 5): the fused kernel
+    // (magus_replay_fused_kernel, MAGUS_FUSE default 1) replays both in one warp per (tile group, segment) on the same
+    // samples, so each trace byte is read once and loaded / converted / validated once for both chain kinds.
+    const bool fuse = !combo && h->groups.size() == 2 && h->groups[0].key >= 1 && h->groups[0].key <= 3 &&
+                      h->groups[0].nq == 1 && h->lane[h->groups[0].q_base].C <= 27 &&
+                      h->groups[1].key == 1000 + LANE_TDP && h->groups[1].nq == 1 && kTC == 8 &&
+                      env_int("MAGUS_FUSE", 1) != 0 && env_int("MAGUS_SOLO", 1) != 0 &&
+                      env_int("MAGUS_SOLO_BAL", 20) == 20 && env_int("MAGUS_TDP_SOLO", 2) != 0;
+    const int fused_ctas = env_int("MAGUS_FUSED_CTAS", 12) == 16 ? 16 : 12;   // per SM (the kernel's launch bound)
     int W = d.tuning_warmup > 0 ? d.tuning_warmup
                                 : ((kmax + cmax - 1 + 31) / 32) * 32 + env_int("MAGUS_WARMUP_EXTRA", 0) + h->warm_extra;
     W = ((std::max(W, kmax + cmax - 1) + 31) / 32) * 32;
@@ -780,6 +819,7 @@ static void choose_geometry(magus_replay_t* h, int n_sm, int forced_segments) {
         }
         // the combined kernel: 8 two-warp CTAs per SM (16 warps: 8 MAGUS, 8 TDP)
         if (combo) S = std::max(1, (int)(((int64_t)n_sm * env_int("MAGUS_COMBO_CTAS_PER_SM", 8)) / std::max(1, p.n_groups)));
+        if (fuse) S = std::max(1, (int)(((int64_t)n_sm * fused_ctas) / std::max(1, p.n_groups)));
         const int L0 = (((N + S - 1) / S) + 31) / 32 * 32;
         if (S > 1 && L0 < 4 * W) S = std::max(1, N / (4 * W));   // segments must dwarf their warm-up
         S_auto = S;
@@ -875,6 +915,14 @@ static void choose_geometry(magus_replay_t* h, int n_sm, int forced_segments) {
             g.smem = SoloSmem<kTC, kNStage>::kBytes;
             g.n_ctas = p.n_seg * p.n_groups * g.n_pblocks;
         }
+    }
+    if (fuse && h->groups[0].solo && h->groups[1].solo) {
+        LaunchGroup& gm = h->groups[0];
+        gm.kernel = fused_kernel_for(gm.key, h->lane[gm.q_base].ddec == -h->lane[gm.q_base].dinc, fused_ctas);
+        gm.threads = 32;
+        gm.smem = SoloSmem<kTC, kNStage>::kBytes;
+        gm.n_ctas = p.n_seg * p.n_groups;
+        h->groups[1].fused = true;
     }
     if (combo && h->groups[0].solo && h->groups[1].solo) {
         LaunchGroup& gm = h->groups[0];
@@ -1358,14 +1406,17 @@ static magus_status enqueue_run(magus_replay_t* h, const float* d_trace, const f
         // launch groups (one chain kind each) run concurrently: fork onto auxiliary streams and join
         // (parallel branches when the run is captured as a graph)
         const int G = (int)h->groups.size();
-        if (G > 1) {
+        int GL = 0;   // launches: a fused group is replayed by the previous group's launch
+        for (const LaunchGroup& g : h->groups) GL += g.fused ? 0 : 1;
+        if (GL > 1) {
             CU(h, cudaEventRecord(h->fork_ev, s));
-            for (int g = 1; g < G; ++g) CU(h, cudaStreamWaitEvent(h->aux[g - 1], h->fork_ev, 0));
+            for (int g = 1; g < GL; ++g) CU(h, cudaStreamWaitEvent(h->aux[g - 1], h->fork_ev, 0));
         }
-        for (int gi = 0; gi < G; ++gi) {
+        for (int gi = 0, li = 0; gi < G; ++gi) {
             const LaunchGroup& g = h->groups[gi];
-            cudaStream_t gs = gi == 0 ? s : h->aux[gi - 1];
             if (g.fused) continue;   // replayed by the previous group's combined launch
+            cudaStream_t gs = li == 0 ? s : h->aux[li - 1];
+            ++li;
             ReplayParams pg = p;
             pg.q_base = g.q_base;
             pg.nq = g.nq;
@@ -1378,9 +1429,9 @@ static magus_status enqueue_run(magus_replay_t* h, const float* d_trace, const f
             pg.n_tblocks = g.n_tblocks;
             pg.n_pblocks = g.n_pblocks;
             CU(h, launch_k(g.kernel, dim3((unsigned)g.n_ctas), dim3((unsigned)g.threads), g.smem, gs,
-                           h->pdl && G == 1 && !timing, g.wide ? h->tmap_w : h->tmap, pg));
+                           h->pdl && GL == 1 && !timing, g.wide ? h->tmap_w : h->tmap, pg));
         }
-        for (int g = 1; g < G; ++g) {
+        for (int g = 1; g < GL; ++g) {
             CU(h, cudaEventRecord(h->join_ev[g - 1], h->aux[g - 1]));
             CU(h, cudaStreamWaitEvent(s, h->join_ev[g - 1], 0));
         }
@@ -1687,7 +1738,7 @@ extern "C" magus_status magus_replay_geometry(const magus_replay_t* h, int32_t o
     const ReplayParams& p = h->rp;
     const magus_replay_desc& d = h->desc;
     int ctas = 0;
-    for (const LaunchGroup& g : h->groups) ctas += g.n_ctas;
+    for (const LaunchGroup& g : h->groups) ctas += g.fused ? 0 : g.n_ctas;
     const LaunchGroup& g0 = h->groups.front();
     // kernel launches of one run, as enqueue_run issues them
     const bool has_work = d.n_traces > 0 && d.n_samples > 0;

@@ -979,4 +979,302 @@ __global__ void __launch_bounds__(64, kSoloCtasPerSm / 2)
     }
 }
 
+// ===================================================================================================================
+// The fused MAGUS + TDP kernel (config 5: one MAGUS policy next to one replayed TDP_DEFAULT baseline): ONE warp per
+// (tile group, segment) replays both on its own TMA ring, every lane stepping its 4 traces' MAGUS chains and TDP chains
+// over the same samples (MAGUS_LTSTAGE[S]_K<K>: one tile load, one fp64 conversion and one validation maximum per
+// sample for both), so every trace byte is read from HBM once.  p.q_base / p.q_base2: the MAGUS
+// and the TDP policy.  MAGUS as solo_magus_body's L stage (BAL 20 / 21); TDP as tsolo_body with its level carried in
+// its cmd word's bit 0.  The per-chain states, statistics and fix-up are those of the two separate kernels.
+#ifndef MAGUS_FUSED_CTAS_PER_SM
+#define MAGUS_FUSED_CTAS_PER_SM 12
+#endif
+constexpr int kFusedCtasPerSm = MAGUS_FUSED_CTAS_PER_SM;
+
+template <int K, bool SYM>
+__device__ __forceinline__ void fused_stage_lt(MagusState<K, false>* s, uint32_t* nlk, float* nthr, uint32_t* wcmd,
+                                               SegStats* ss, uint32_t& vmax, uint32_t* wcmdT, double* excT,
+                                               float* nthrT, double* sT, uint32_t tile, const SoloConst& sc,
+                                               const DevPolicy& pol, float ahi, float alo) {
+    uint32_t e0 = s[0].evh, e1 = s[1].evh, e2 = s[2].evh, e3 = s[3].evh;
+    const uint32_t bitc = 1u << (pol.C - 1), mone = 0xFFFFFFFFu * pol.one;
+#define LT_TAIL                                                                                                \
+    e0, e1, e2, e3, s[0].cnt, s[1].cnt, s[2].cnt, s[3].cnt, ss[0].sexc, ss[1].sexc, ss[2].sexc, ss[3].sexc, nlk[0],  \
+        nlk[1], nlk[2], nlk[3], nthr[0], nthr[1], nthr[2], nthr[3], wcmd[0], wcmd[1], wcmd[2], wcmd[3], vmax,        \
+        wcmdT[0], wcmdT[1], wcmdT[2], wcmdT[3], excT[0], excT[1], excT[2], excT[3], nthrT[0], nthrT[1], nthrT[2],     \
+        nthrT[3], sT[0], sT[1], sT[2], sT[3], tile, sc.B_lo, sc.Blo_d, pol.dinc, pol.ddec, bitc, pol.one, mone, ahi, alo
+#define LT_R2                                                                                                  \
+    s[0].ring.v[0], s[0].ring.v[1], s[1].ring.v[0], s[1].ring.v[1], s[2].ring.v[0], s[2].ring.v[1], s[3].ring.v[0], \
+        s[3].ring.v[1]
+#define LT_R3                                                                                                  \
+    s[0].ring.v[0], s[0].ring.v[1], s[0].ring.v[2], s[1].ring.v[0], s[1].ring.v[1], s[1].ring.v[2], s[2].ring.v[0], \
+        s[2].ring.v[1], s[2].ring.v[2], s[3].ring.v[0], s[3].ring.v[1], s[3].ring.v[2]
+    if constexpr (SYM) {
+        if constexpr (K == 1) MAGUS_LTSTAGES_K1(s[0].ring.v[0], s[1].ring.v[0], s[2].ring.v[0], s[3].ring.v[0], LT_TAIL);
+        else if constexpr (K == 2) MAGUS_LTSTAGES_K2(LT_R2, LT_TAIL);
+        else MAGUS_LTSTAGES_K3(LT_R3, LT_TAIL);
+    } else {
+        if constexpr (K == 1) MAGUS_LTSTAGE_K1(s[0].ring.v[0], s[1].ring.v[0], s[2].ring.v[0], s[3].ring.v[0], LT_TAIL);
+        else if constexpr (K == 2) MAGUS_LTSTAGE_K2(LT_R2, LT_TAIL);
+        else MAGUS_LTSTAGE_K3(LT_R3, LT_TAIL);
+    }
+#undef LT_R2
+#undef LT_R3
+#undef LT_TAIL
+    s[0].evh = e0;
+    s[1].evh = e1;
+    s[2].evh = e2;
+    s[3].evh = e3;
+}
+
+template <class T, int TC, int NSTAGE, bool SYM, int MINB = kFusedCtasPerSm>
+__global__ void __launch_bounds__(32, MINB)
+    magus_replay_fused_kernel(const __grid_constant__ CUtensorMap tmap, const ReplayParams p) {
+    static_assert(T::kHasStage8 && TC == 8, "fused kernel: whole-stage PTX blocks of 8 ticks");
+    using State = typename T::State;
+    using SM = SoloSmem<TC, NSTAGE>;
+    constexpr uint32_t kTileBytes = SM::kTileBytes;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int lane = threadIdx.x;
+    const int tgroup = blockIdx.x % p.n_groups;
+    const int seg = blockIdx.x / p.n_groups;
+    const uint32_t tile0 = ptx::smem_u32(smem);
+    const uint32_t bar0 = tile0 + NSTAGE * kTileBytes;
+    if (lane == 0) {
+        ptx::prefetch_tmap(&tmap);
+        for (int i = 0; i < NSTAGE; ++i)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8 * i) : "memory");
+        ptx::fence_mbar_init();
+    }
+    __syncwarp();
+    const SegGeom G = seg_geom<TC>(p, seg);
+    const uint64_t cpol = ptx::policy_evict_first();
+    const int x = tgroup * kTracesPerWarp;
+    for (int i = 0; i < NSTAGE && i < G.n_stages; ++i) solo_issue<TC>(tile0 + i * kTileBytes, &tmap, bar0 + 8 * i, x, G.tau_w + i * TC, cpol);
+    ptx::pdl_wait();   // first_low and the scratch words come from the pre-pass (launched just before)
+
+    const int q = p.q_base, qT = p.q_base2;
+    const DevPolicy pol = p.pol[q];
+    const int j0 = x + lane * kChains;
+    const float B_lo = p.B_lo, B_hi = p.B_hi;
+    SoloConst sc;
+    sc.Blo_d = (double)B_lo;
+    sc.B_lo = B_lo;
+    const double Blo_d = sc.Blo_d;
+    const int k = pol.k, C = pol.C;
+    const bool synth = seg > 0 && (p.solo_flags & 1u);
+    const int warm_ticks = synth ? 0 : k + C - 1;
+    const uint32_t lane_off = (uint32_t)lane * 16u;
+    // TDP (tsolo_body, NP = 1): next level f_max iff A < a*[f]; a_lo = +inf when B_lo < a*_lo (A = min(D, B_lo))
+    float ahi, alo;
+    uint32_t fT0;
+    {
+        const DevPolicy polT = p.pol[qT];
+        ahi = polT.astar_hi;
+        alo = B_lo >= polT.astar_lo ? polT.astar_lo : __int_as_float(0x7F800000);
+        fT0 = seg == 0 ? (uint32_t)polT.f0 : (uint32_t)polT.guess_f;
+    }
+
+    State st[kChains];
+    SegStats ss[kChains];
+    uint32_t wcmd[kChains], fstart[kChains];
+    float lockf[kChains], nthrf[kChains];
+    uint32_t nlk[kChains];
+    uint32_t nsb = 0;
+    uint32_t vmax = 0;
+    uint32_t wcmdT[kChains], fstartT[kChains], nhiT[kChains], transT[kChains], dcT[kChains];
+    double excT[kChains], sT[kChains];
+    float nthrT[kChains];
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) {
+        T::init(st[c], pol, seg == 0);
+        ss[c].zero();
+        wcmd[c] = 0;
+        lockf[c] = nthrf[c] = 0.f;
+        nlk[c] = 0;
+        wcmdT[c] = fT0;   // bit 0 = the TDP level
+        excT[c] = sT[c] = 0.0;
+        nthrT[c] = 0.f;
+        nhiT[c] = transT[c] = dcT[c] = 0;
+    }
+
+    int i = 0, slot = 0;
+    uint32_t phase = 0;
+#pragma unroll 1
+    for (int bt0 = G.tau_w; bt0 < G.seg_end; bt0 += 32) {
+        if (bt0 == G.seg_start) {   // the segment's own ticks start: record the entries, reset the statistics
+#pragma unroll
+            for (int c = 0; c < kChains; ++c) {
+                const int j = j0 + c;
+                if (j < p.n_traces) {
+                    T::save(st[c], p, pol, 0, q, seg, j);
+                    const int64_t si = st_idx(p, 0, qT, seg, j);
+                    p.st_f[si] = (uint8_t)(wcmdT[c] & 1u);
+                    p.st_log[si] = 0;
+                }
+                ss[c].zero();
+                lockf[c] = nthrf[c] = 0.f;
+                nlk[c] = 0;
+                excT[c] = 0.0;
+                nthrT[c] = 0.f;
+                nhiT[c] = transT[c] = dcT[c] = 0;
+            }
+            nsb = 0;
+        }
+        if (bt0 == G.tau_w && seg > 0) {   // MAGUS's speculative level at the warm-up start (solo_magus_body)
+            mbar_wait_loop(bar0 + 8 * slot, phase);
+            float4 d0;
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(d0.x), "=f"(d0.y), "=f"(d0.z), "=f"(d0.w)
+                         : "r"(tile0 + slot * kTileBytes + lane_off)
+                         : "memory");
+            const float dd[4] = {d0.x, d0.y, d0.z, d0.w};
+#pragma unroll
+            for (int c = 0; c < kChains; ++c) {
+                const int j = j0 + c;
+                const int fl = j < p.n_traces ? __ldg(p.first_low + j) : 0x7FFFFFFF;
+                const int fh = j < p.n_traces ? __ldg(p.first_low + p.n_traces + j) : 0x7FFFFFFF;
+                const bool hi = (dd[c] > B_lo && fl < G.tau_w) || (pol.sticky && fl < G.tau_w && fh < G.tau_w);
+                T::set_level(st[c], hi ? 1u : 0u);
+                if (synth) {
+                    const double a0 = (double)(hi ? dd[c] : fminf(dd[c], B_lo));
+#pragma unroll
+                    for (int r = 0; r < (int)(sizeof(st[c].ring.v) / sizeof(double)); ++r) st[c].ring.v[r] = a0;
+                }
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < kChains; ++c) {
+            fstart[c] = T::level(st[c]);
+            fstartT[c] = wcmdT[c] & 1u;
+        }
+        const bool counting = bt0 >= G.seg_start;
+        if (bt0 + 32 <= G.seg_end && bt0 - G.tau_w >= warm_ticks) {
+            // steady state: four fused whole-stage PTX blocks
+#pragma unroll
+            for (int c = 0; c < kChains; ++c) {
+                st[c].cnt -= pol.smin_sc;
+                wcmd[c] = fstart[c];
+            }
+            if (counting) ++nsb;
+#pragma unroll 1
+            for (int sub = 0; sub < 32 / TC; ++sub) {
+                const uint32_t tile = tile0 + slot * kTileBytes;
+                mbar_wait_loop(bar0 + 8 * slot, phase);
+                fused_stage_lt<T::kRingK, SYM>(st, nlk, nthrf, wcmd, ss, vmax, wcmdT, excT, nthrT, sT, tile + lane_off,
+                                               sc, pol, ahi, alo);
+                __syncwarp();   // every lane's tile reads are complete before the slot is refilled
+                solo_release<TC, false>(tile, &tmap, bar0, 0u, slot, phase, i + NSTAGE < G.n_stages, x,
+                                        G.tau_w + (i + NSTAGE) * TC, cpol, lane);
+                ++i;
+                if (++slot == NSTAGE) {
+                    slot = 0;
+                    phase ^= 1u;
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < kChains; ++c) {
+                st[c].cnt += pol.smin_sc;
+                T::set_level(st[c], wcmd[c] & 1u);
+            }
+        } else {
+            // warm-up block (MAGUS's Alg. 1 / Alg. 2 gated per tick) or the ragged last block of a trace
+#pragma unroll 1
+            for (int sub = 0; sub < 32 / TC && i < G.n_stages; ++sub) {
+                const int t0 = bt0 + sub * TC;
+                const uint32_t tile = tile0 + slot * kTileBytes;
+                mbar_wait_loop(bar0 + 8 * slot, phase);
+                const float4* rows = reinterpret_cast<const float4*>(smem + slot * kTileBytes) + lane;
+                if (t0 + TC <= G.seg_end) {
+#pragma unroll 1
+                    for (int tt = 0; tt < TC; ++tt) {
+                        const int r = t0 + tt - G.tau_w;
+                        const float4 d4 = rows[tt * (kTracesPerWarp / 4)];
+                        const float d[4] = {d4.x, d4.y, d4.z, d4.w};
+                        T::warm4(st, d, pol, B_lo, Blo_d, wcmd, ss, vmax, r >= k ? 1u : 0u, r >= k + C - 1 ? 1u : 0u);
+                    }
+                    MAGUS_TLSTAGE(wcmdT[0], wcmdT[1], wcmdT[2], wcmdT[3], excT[0], excT[1], excT[2], excT[3], nthrT[0],
+                                  nthrT[1], nthrT[2], nthrT[3], sT[0], sT[1], sT[2], sT[3], tile + lane_off, B_lo, ahi,
+                                  alo, pol.one);
+                } else {
+                    for (int tt = 0; tt < TC; ++tt) {
+                        const int t = t0 + tt;
+                        if (t >= G.seg_end) break;
+                        const float4 d4 = rows[tt * (kTracesPerWarp / 4)];
+                        const float d[4] = {d4.x, d4.y, d4.z, d4.w};
+                        const bool ready = (t - G.tau_w) >= k;
+                        const bool lfull = (t - G.tau_w) >= k + C - 1;
+#pragma unroll
+                        for (int c = 0; c < kChains; ++c) {
+                            const TickOut o = T::template tick<true>(st[c], d[c], pol, B_lo, B_hi, ready, lfull);
+                            wcmd[c] = (wcmd[c] << 1) | o.cmd;
+                            acc_tick(ss[c], vmax, o, d[c], B_lo);
+                            const uint32_t fT = wcmdT[c] & 1u;   // TDP tick (tsolo_body's ragged path)
+                            const bool thr = fT == 0u && d[c] > B_lo;
+                            wcmdT[c] = (wcmdT[c] << 1) | ((d[c] < ahi || (fT == 0u && d[c] < alo)) ? 1u : 0u);
+                            excT[c] = __fma_rn(thr ? 1.0 : 0.0, (double)d[c], excT[c]);
+                            nthrT[c] += thr ? 1.f : 0.f;
+                        }
+                    }
+                }
+                __syncwarp();
+                solo_release<TC, false>(tile, &tmap, bar0, 0u, slot, phase, i + NSTAGE < G.n_stages, x,
+                                        G.tau_w + (i + NSTAGE) * TC, cpol, lane);
+                ++i;
+                if (++slot == NSTAGE) {
+                    slot = 0;
+                    phase ^= 1u;
+                }
+            }
+        }
+        if (counting) {
+            const int64_t bi = bt0 >> 5;
+            const uint2 bkey = p.dkeys[bi];
+            const int n = min(32, G.seg_end - bt0);
+            uint32_t* wbase = p.words ? p.words + ((int64_t)q * p.n_traces * p.n_blocks + bi) * 2 : nullptr;
+            uint32_t* wbaseT = p.words ? p.words + ((int64_t)qT * p.n_traces * p.n_blocks + bi) * 2 : nullptr;
+#pragma unroll
+            for (int c = 0; c < kChains; ++c) {
+                const bool live = j0 + c < p.n_traces;
+                uint32_t* wout = (wbase && live) ? wbase + (int64_t)(j0 + c) * p.n_blocks * 2 : nullptr;
+                if (n == 32) fold_full_block(ss[c], wcmd[c], (uint32_t)st[c].evh, fstart[c], bkey, wout);
+                else fold_block(ss[c], wcmd[c], (uint32_t)st[c].evh, fstart[c], n, bi, wout);
+                // TDP: level / transition counts and the cmd digest (no tune flags)
+                const uint32_t mask = n >= 32 ? 0xFFFFFFFFu : ((1u << n) - 1u);
+                const uint32_t cw = wcmdT[c] & mask;
+                const uint32_t lw = ((wcmdT[c] >> 1) & (mask >> 1)) | (fstartT[c] << (n - 1));
+                transT[c] += __popc(cw ^ lw);
+                nhiT[c] += __popc(lw);
+                const uint32_t wc = cw << (32 - n);
+                dcT[c] += wc * (n == 32 ? bkey.x : digest_key((uint64_t)bi).x);
+                if (wbaseT && live) {
+                    uint32_t* wo = wbaseT + (int64_t)(j0 + c) * p.n_blocks * 2;
+                    wo[0] = wc;
+                    wo[1] = 0u;
+                }
+            }
+        }
+    }
+
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) {
+        const int j = j0 + c;
+        if (j >= p.n_traces) continue;
+        T::save(st[c], p, pol, 1, q, seg, j);
+        add_to_chain(p, q, j, ss[c].nhi, ss[c].nthr + (uint32_t)nthrf[c], ss[c].trans, ss[c].ev,
+                     ss[c].lock + (uint32_t)lockf[c] + 32u * nsb - nlk[c], ss[c].sexc, ss[c].digest());
+        const int64_t si = st_idx(p, 1, qT, seg, j);
+        p.st_f[si] = (uint8_t)(wcmdT[c] & 1u);
+        p.st_log[si] = 0;
+        const uint32_t nthr = (uint32_t)nthrT[c];
+        // sum(D - B_lo) over throttled ticks, exact; no throttled tick: 0 (the open-loop mode's B_lo is +inf)
+        const double sexc = nthr ? excT[c] - (double)nthr * Blo_d : 0.0;
+        add_to_chain(p, qT, j, nhiT[c], nthr, transT[c], 0u, 0u, sexc, digest_pack(dcT[c], 0u));
+    }
+    if (j0 < p.n_traces) {
+        atomicMax(p.c_vmax + chain_idx(p, q, j0), vmax);   // lane-level validation maximum
+        atomicMax(p.c_vmax + chain_idx(p, qT, j0), vmax);
+    }
+}
+
 }  // namespace magus

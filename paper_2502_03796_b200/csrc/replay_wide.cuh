@@ -77,6 +77,37 @@ __device__ __forceinline__ void wide_stage(MagusState<K, false>& st, float& lock
     st.evh = e0;
 }
 
+// 8 ticks of one chain with the samples as fp64 values and the L-stage bookkeeping (MAGUS_WLSTAGE[S]_K<K>): the
+// level in wcmd's bit 0, st.cnt biased by -smin_sc (the caller converts around the block), nlk = ticks not locked
+template <int K, bool SYM>
+__device__ __forceinline__ void wide_stage_l(MagusState<K, false>& st, uint32_t& nlk, float& nthr, uint32_t& wcmd,
+                                             double& sexc, const double* d8, const DevPolicy& pol, double Blo_d,
+                                             uint32_t bitc, uint32_t mone) {
+    uint32_t e0 = st.evh;
+#define WDL_TAIL                                                                                                 \
+    e0, st.cnt, sexc, nlk, nthr, wcmd, d8[0], d8[1], d8[2], d8[3], d8[4], d8[5], d8[6], d8[7], Blo_d, pol.dinc,     \
+        pol.ddec, bitc, pol.one, mone
+#define R(i) st.ring.v[i]
+#define WDL(NAME)                                                                                                \
+    if constexpr (K == 1) NAME##_K1(R(0), WDL_TAIL);                                                               \
+    else if constexpr (K == 2) NAME##_K2(R(0), R(1), WDL_TAIL);                                                    \
+    else if constexpr (K == 3) NAME##_K3(R(0), R(1), R(2), WDL_TAIL);                                              \
+    else if constexpr (K == 4) NAME##_K4(R(0), R(1), R(2), R(3), WDL_TAIL);                                        \
+    else if constexpr (K == 5) NAME##_K5(R(0), R(1), R(2), R(3), R(4), WDL_TAIL);                                  \
+    else if constexpr (K == 6) NAME##_K6(R(0), R(1), R(2), R(3), R(4), R(5), WDL_TAIL);                            \
+    else if constexpr (K == 7) NAME##_K7(R(0), R(1), R(2), R(3), R(4), R(5), R(6), WDL_TAIL);                      \
+    else NAME##_K8(R(0), R(1), R(2), R(3), R(4), R(5), R(6), R(7), WDL_TAIL);
+    if constexpr (SYM) {
+        WDL(MAGUS_WLSTAGES)
+    } else {
+        WDL(MAGUS_WLSTAGE)
+    }
+#undef WDL
+#undef R
+#undef WDL_TAIL
+    st.evh = e0;
+}
+
 // 8 ticks of one chain with the samples as fp64 values (MAGUS_WSTAGE1D_K<K>: no conversion, fp64 throttle test)
 template <int K>
 __device__ __forceinline__ void wide_stage_d(MagusState<K, false>& st, float& lock, float& nthr, uint32_t& wcmd,
@@ -141,11 +172,14 @@ __device__ __forceinline__ void wide_stage2(MagusState<K, false>* st, float* loc
 // MAGUS chains with a register ring of K <= 8 values and a 32-bit tune log (C <= 28).  NC = chains per thread: 1, or
 // 2 = two policy points of the same trace sharing the samples (one shared-memory load, fp32 -> fp64 conversion and
 // validation maximum per tick for both).  Launch: one (256 / NC)-thread CTA per (16-trace column, block of 16 policy
-// points), policy blocks fastest; p.n_pblocks = ceil(nq / 16).
-template <int K, int NC>
+// points), policy blocks fastest; p.n_pblocks = ceil(nq / 16).  LV (NC = 1 only): 0 = the one-chain stage block
+// MAGUS_WSTAGE1D_K<K>, 1 = its L form (MAGUS_WLSTAGE_K<K>: C <= 27), 2 = the L form with the |d| tune-flag test
+// (every lane policy has d*_dec == -d*_inc).
+template <int K, int NC, int LV>
 __global__ void __launch_bounds__(kWideThreads / NC, 2)
     magus_replay_wide_kernel(const __grid_constant__ CUtensorMap tmap, const ReplayParams p) {
     static_assert(NC == 1 || NC == 2, "wide kernel: one or two chains per thread");
+    static_assert(LV == 0 || NC == 1, "wide kernel: the L stage runs one chain per thread");
     using T = MagusTicker<K, false>;
     constexpr uint32_t kTileBytes = WideSmem::kTileBytes;
     constexpr int kWarps = kWideWarps / NC;
@@ -241,12 +275,29 @@ __global__ void __launch_bounds__(kWideThreads / NC, 2)
             __syncwarp();
             release();
             const double* my = wbuf + ((tid >> 4) & 1) * kWideTC;
+            if constexpr (LV != 0) {
+                uint32_t nlk = 0;
+                st[0].cnt -= pol[0].smin_sc;   // biased: lock iff cnt >= 0
+                wcmd[0] = fstart[0];           // bit 0 = the level
 #pragma unroll
-            for (int g = 0; g < kWideTC / 8; ++g) {
-                double d8[8];
+                for (int g = 0; g < kWideTC / 8; ++g) {
+                    double d8[8];
 #pragma unroll
-                for (int t = 0; t < 8; ++t) d8[t] = my[8 * g + t];
-                wide_stage_d<K>(st[0], lockf[0], nthrf[0], wcmd[0], ss[0].sexc, d8, pol[0], Blo_d, bitc[0], mone);
+                    for (int t = 0; t < 8; ++t) d8[t] = my[8 * g + t];
+                    wide_stage_l<K, LV == 2>(st[0], nlk, nthrf[0], wcmd[0], ss[0].sexc, d8, pol[0], Blo_d, bitc[0],
+                                             mone);
+                }
+                st[0].cnt += pol[0].smin_sc;
+                T::set_level(st[0], wcmd[0] & 1u);
+                lockf[0] = (float)(kWideTC - nlk);
+            } else {
+#pragma unroll
+                for (int g = 0; g < kWideTC / 8; ++g) {
+                    double d8[8];
+#pragma unroll
+                    for (int t = 0; t < 8; ++t) d8[t] = my[8 * g + t];
+                    wide_stage_d<K>(st[0], lockf[0], nthrf[0], wcmd[0], ss[0].sexc, d8, pol[0], Blo_d, bitc[0], mone);
+                }
             }
             __syncwarp();   // every lane has read the scratch before the next stage overwrites it
         } else if (n == kWideTC && bt0 >= warm) {

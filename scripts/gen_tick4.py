@@ -344,7 +344,7 @@ def build_stage_p(K, TC=8, popc=True, group=4, sym=False):
 
 
 
-def build_stage_l(K, TC=8, sym=False):
+def build_stage_l(K, TC=8, sym=False, tdp=False):
     """MAGUS_LSTAGE_K<K>: the solo kernel's steady-state stage with the level and the lock counter folded into
     words and signs, fewer instructions per chain-tick than MAGUS_SSTAGEF_K<K> (same decisions):
     - the cmd word is shifted once per stage (by TC) and tick tt sets bit TC-1-tt with a predicated IMAD of an
@@ -355,23 +355,35 @@ def build_stage_l(K, TC=8, sym=False):
       C <= 27), folded into the new-level compare (ISETP.GE.OR); the ticks NOT locked are counted with the sign
       bit (nlk += cnt >> 31, unsigned), so there is no separate lock predicate or predicated lock counter.
     sym=True (MAGUS_LSTAGES_K<K>, only for d*_dec == -d*_inc): the tune flag is |d| > d*_inc and the kept-or-raised
-      level +1 | (f_max & !-1) is two DSETPs ((d >= d*_dec) & level, then (d > d*_inc) | that)."""
+      level +1 | (f_max & !-1) is two DSETPs ((d >= d*_dec) & level, then (d > d*_inc) | that).
+    tdp=True (MAGUS_LTSTAGE[S]_K<K>, the fused MAGUS + TDP kernel): the same 4 traces also step one TDP_DEFAULT chain
+      each (the tick of MAGUS_TLSTAGE: level in its own cmd word, next level f_max iff D < a_hi | (f_min & D < a_lo),
+      throttled demand summed by a 0/1 DFMA), sharing the tile loads, the fp64 conversion and the validation."""
     C = 4
     names = [(f"r{c}_{i}", "+d") for c in range(C) for i in range(K)] + \
             [(f"evh{c}", "+r") for c in range(C)] + [(f"cnt{c}", "+r") for c in range(C)] + \
             [(f"exc{c}", "+d") for c in range(C)] + [(f"nlk{c}", "+r") for c in range(C)] + \
             [(f"nthr{c}", "+f") for c in range(C)] + [(f"wcmd{c}", "+r") for c in range(C)] + [("vmax", "+r")]
+    if tdp:
+        names += [(f"wcmdT{c}", "+r") for c in range(C)] + [(f"excT{c}", "+d") for c in range(C)] + \
+                 [(f"nthrT{c}", "+f") for c in range(C)] + [(f"sT{c}", "+d") for c in range(C)]
     inames = [("tile", "r"), ("Blo", "f"), ("Blod", "d"), ("dinc", "d"), ("ddec", "d"), ("bitc", "r"),
-              ("one", "r"), ("mone", "r")]
+              ("one", "r"), ("mone", "r")] + ([("ahi", "f"), ("alo", "f")] if tdp else [])
     idx = {n: f"%{i}" for i, (n, _) in enumerate(names + inames)}
     R = idx.__getitem__
     body = ["{", ".reg .pred phi<4>, pthr<4>, pinc<4>, pev<4>, pk<4>, pq<4>;",
             f".reg .b32 D<{TC * C}>;", f".reg .f64 dd<4>, dv<4>, da<4>, dx<4>, ad<{TC * C}>;",
             ".reg .b32 tb<4>, tl<4>, lv<4>;"]
+    if tdp:
+        body += [".reg .pred phT<4>, pthT<4>, ptT<4>, pnT<4>;", ".reg .b32 sloT<4>, shiT<4>, lvT<4>;"]
     for c in range(C):
         body.append(f"and.b32 lv{c}, {R(f'wcmd{c}')}, 1;")
         body.append(f"setp.ne.u32 phi{c}, lv{c}, 0;")                   # level = the previous tick's cmd
         body.append(f"shl.b32 {R(f'wcmd{c}')}, {R(f'wcmd{c}')}, {TC};")
+        if tdp:   # the TDP level is re-read from its cmd word every tick (bit TC - tt: the previous tick's cmd), so
+                  # no TDP predicate lives across ticks (8 level predicates would exceed the 7 predicate registers)
+            body.append(f"shl.b32 {R(f'wcmdT{c}')}, {R(f'wcmdT{c}')}, {TC};")
+            body.append(f"mov.b64 {{sloT{c}, shiT{c}}}, {R(f'sT{c}')};")
     for tt in range(TC):
         body.append(f"ld.shared.v4.f32 {{D{tt * C}, D{tt * C + 1}, D{tt * C + 2}, D{tt * C + 3}}}, [{R('tile')}+{tt * 512}];")
         per_chain = [
@@ -404,7 +416,18 @@ def build_stage_l(K, TC=8, sym=False):
             "add.f64 {exc}, {exc}, dx{c};",
             "@pthr{c} add.f32 {nthr}, {nthr}, 0f3F800000;",
             "max.u32 {vmax}, {vmax}, {D};",                               # validation (A17)
-        ]
+        ] + ([
+            "and.b32 lvT{c}, {wcmdT}, {pbit};",                           # TDP: the level (previous tick's cmd)
+            "setp.ne.u32 phT{c}, lvT{c}, 0;",
+            "setp.gt.and.f32 pthT{c}, {D}, {Blo}, !phT{c};",              # throttled (A14)
+            "setp.lt.and.f32 ptT{c}, {D}, {alo}, !phT{c};",               # at f_min: A < a*_lo (A24)
+            "setp.lt.or.f32 pnT{c}, {D}, {ahi}, ptT{c};",                 # next level f_max iff A < a*[f]
+            "selp.b32 shiT{c}, 0x3FF00000, 0, pthT{c};",                  # 1.0 if throttled, else 0.0 (low word 0)
+            "mov.b64 {sT}, {{sloT{c}, shiT{c}}};",
+            "fma.rn.f64 {excT}, {sT}, dd{c}, {excT};",                    # sum of D over throttled ticks (exact)
+            "@pthT{c} add.f32 {nthrT}, {nthrT}, 0f3F800000;",
+            "@pnT{c} mad.lo.u32 {wcmdT}, {one}, {bit}, {wcmdT};",
+        ] if tdp else [])
         for tmpl in per_chain:
             for c in range(C):
                 t = tt * C + c
@@ -413,13 +436,63 @@ def build_stage_l(K, TC=8, sym=False):
                                         dinc=R("dinc"), ddec=R("ddec"), evh=R(f"evh{c}"), one=R("one"),
                                         bitc=R("bitc"), mone=R("mone"), cnt=R(f"cnt{c}"), nlk=R(f"nlk{c}"),
                                         wcmd=R(f"wcmd{c}"), exc=R(f"exc{c}"), nthr=R(f"nthr{c}"), vmax=R("vmax"),
-                                        bit=1 << (TC - 1 - tt)))
+                                        bit=1 << (TC - 1 - tt), pbit=1 << (TC - tt),
+                                        **({"ahi": R("ahi"), "alo": R("alo"), "sT": R(f"sT{c}"),
+                                            "excT": R(f"excT{c}"), "nthrT": R(f"nthrT{c}"),
+                                            "wcmdT": R(f"wcmdT{c}")} if tdp else {})))
     for c in range(C):
         for i in range(K):   # ring newest first: r_i = A_{t0 + TC - 1 - i}
             body.append(f"mov.f64 {R(f'r{c}_{i}')}, ad{(TC - 1 - i) * C + c};")
     body.append("}")
     params = ", ".join(n for n, _ in names + inames)
-    name = f"MAGUS_LSTAGE{'S' if sym else ''}_K{K}"
+    name = f"MAGUS_L{'T' if tdp else ''}STAGE{'S' if sym else ''}_K{K}"
+    out = [f"#define {name}(...) {name}_(__VA_ARGS__)", f"#define {name}_({params}) \\", "    asm volatile( \\"]
+    out += [f'        "{l}\\n\\t" \\' for l in body]
+    out.append("        : " + ", ".join(f'"{c}"({n})' for n, c in names) + " \\")
+    out.append("        : " + ", ".join(f'"{c}"({n})' for n, c in inames) + " \\")
+    out.append('        : "memory")')
+    return out
+
+
+def build_stage_tl(TC=8):
+    """MAGUS_TLSTAGE: one stage (TC ticks x 4 traces) of ONE TDP_DEFAULT policy with the level carried in its cmd word
+    (shifted once per stage, bit 0 = the previous tick's cmd): the fused MAGUS + TDP kernel's TDP step in the blocks
+    where MAGUS runs its per-tick warm-up path.  Tick as in MAGUS_TSTAGE1L; no validation (the MAGUS path takes it)."""
+    C = 4
+    names = [(f"wcmd{c}", "+r") for c in range(C)] + [(f"exc{c}", "+d") for c in range(C)] + \
+            [(f"nthr{c}", "+f") for c in range(C)] + [(f"s{c}", "+d") for c in range(C)]
+    inames = [("tile", "r"), ("Blo", "f"), ("ahi", "f"), ("alo", "f"), ("one", "r")]
+    idx = {n: f"%{i}" for i, (n, _) in enumerate(names + inames)}
+    R = idx.__getitem__
+    body = ["{", f".reg .pred phi<{C}>, pthr<{C}>, pt<{C}>;", f".reg .b32 D<{TC * 4}>, slo<{C}>, shi<{C}>, lv<{C}>;",
+            ".reg .f64 dd<4>;"]
+    for c in range(C):
+        body.append(f"and.b32 lv{c}, {R(f'wcmd{c}')}, 1;")
+        body.append(f"setp.ne.u32 phi{c}, lv{c}, 0;")
+        body.append(f"shl.b32 {R(f'wcmd{c}')}, {R(f'wcmd{c}')}, {TC};")
+        body.append(f"mov.b64 {{slo{c}, shi{c}}}, {R(f's{c}')};")
+    for tt in range(TC):
+        body.append(f"ld.shared.v4.f32 {{D{tt * 4}, D{tt * 4 + 1}, D{tt * 4 + 2}, D{tt * 4 + 3}}}, [{R('tile')}+{tt * 512}];")
+        for u in range(4):
+            body.append(f"cvt.f64.f32 dd{u}, D{tt * 4 + u};")
+        per_chain = [
+            "setp.gt.and.f32 pthr{c}, {D}, {Blo}, !phi{c};",             # throttled (A14)
+            "setp.lt.and.f32 pt{c}, {D}, {alo}, !phi{c};",               # at f_min: A < a*_lo (A24)
+            "setp.lt.or.f32 phi{c}, {D}, {ahi}, pt{c};",                 # next level f_max iff A < a*[f]
+            "selp.b32 shi{c}, 0x3FF00000, 0, pthr{c};",                  # 1.0 if throttled, else 0.0 (low word 0)
+            "mov.b64 {s}, {{slo{c}, shi{c}}};",
+            "fma.rn.f64 {exc}, {s}, dd{c}, {exc};",                      # sum of D over throttled ticks (exact)
+            "@pthr{c} add.f32 {nthr}, {nthr}, 0f3F800000;",
+            "@phi{c} mad.lo.u32 {wcmd}, {one}, {bit}, {wcmd};",
+        ]
+        for tmpl in per_chain:
+            for c in range(C):
+                body.append(tmpl.format(c=c, D=f"D{tt * 4 + c}", Blo=R("Blo"), ahi=R("ahi"), alo=R("alo"),
+                                        s=R(f"s{c}"), exc=R(f"exc{c}"), nthr=R(f"nthr{c}"), wcmd=R(f"wcmd{c}"),
+                                        one=R("one"), bit=1 << (TC - 1 - tt)))
+    body.append("}")
+    params = ", ".join(n for n, _ in names + inames)
+    name = "MAGUS_TLSTAGE"
     out = [f"#define {name}(...) {name}_(__VA_ARGS__)", f"#define {name}_({params}) \\", "    asm volatile( \\"]
     out += [f'        "{l}\\n\\t" \\' for l in body]
     out.append("        : " + ", ".join(f'"{c}"({n})' for n, c in names) + " \\")
@@ -788,6 +861,65 @@ def build_stage_w1d(K, TC=8):
     return out
 
 
+def build_stage_w1l(K, TC=8, sym=False):
+    """MAGUS_WLSTAGE[S]_K<K>: MAGUS_WSTAGE1D_K<K> (one chain, fp64 samples; the wide kernel) with the L-stage
+    transformations of MAGUS_LSTAGE_K<K> (build_stage_l): the level carried in the cmd word (shifted once per
+    TC ticks, bit 0 = the previous tick's cmd), Alg. 2's lock as the sign of the window count biased by
+    -s_min << (C-1) with the not-locked ticks counted by the sign bit, and (sym) the |d| tune-flag test."""
+    names = [(f"r0_{i}", "+d") for i in range(K)] + \
+            [("evh0", "+r"), ("cnt0", "+r"), ("exc0", "+d"), ("nlk0", "+r"), ("nthr0", "+f"), ("wcmd0", "+r")]
+    inames = [(f"S{tt}", "d") for tt in range(TC)] + [("Blod", "d"), ("dinc", "d"), ("ddec", "d"), ("bitc", "r"),
+                                                     ("one", "r"), ("mone", "r")]
+    idx = {n: f"%{i}" for i, (n, _) in enumerate(names + inames)}
+    R = idx.__getitem__
+    body = ["{", ".reg .pred phi, pthr, pinc, pev, pq, pk;", f".reg .f64 dv, da, dx, ad<{TC}>;", ".reg .b32 tb, tl, lv;",
+            f"and.b32 lv, {R('wcmd0')}, 1;", "setp.ne.u32 phi, lv, 0;",      # level = the previous tick's cmd
+            f"shl.b32 {R('wcmd0')}, {R('wcmd0')}, {TC};"]
+    for tt in range(TC):
+        dd = R(f"S{tt}")
+        old = f"ad{tt - K}" if tt >= K else R(f"r0_{K - 1 - tt}")
+        body += [
+            f"setp.gt.and.f64 pthr, {dd}, {R('Blod')}, !phi;",             # throttled: f_min and D > B_lo (A14)
+            f"selp.f64 ad{tt}, {R('Blod')}, {dd}, pthr;",                   # A = min(D, B[f]) (exact)
+            f"sub.f64 dv, ad{tt}, {old};",                                  # Alg. 1 numerator A_t - A_{t-k} (P:207)
+        ] + ([
+            "abs.f64 da, dv;",                                             # symmetric thresholds (d*_dec = -d*_inc):
+            f"setp.gt.f64 pev, da, {R('dinc')};",                           # tune flag iff |d| > d*_inc (P:213, P:243)
+            f"setp.ge.and.f64 pk, dv, {R('ddec')}, phi;",                   # f_max and not -1
+            f"setp.gt.or.f64 pq, dv, {R('dinc')}, pk;",                     # +1 || (f_max && !-1)
+        ] if sym else [
+            f"setp.gt.f64 pinc, dv, {R('dinc')};",                          # +1 (P:209)
+            f"setp.lt.or.f64 pev, dv, {R('ddec')}, pinc;",                  # tune flag (P:213, P:243)
+            "not.pred pk, pev;",
+            "and.pred pk, pk, phi;",
+            "or.pred pq, pk, pinc;",                                       # +1 || (f_max && !flag)
+        ]) + [
+            f"and.b32 tb, {R('evh0')}, {R('bitc')};",                       # the flag leaving the C-window (scaled)
+            f"shl.b32 {R('evh0')}, {R('evh0')}, 1;",
+            f"@pev mad.lo.u32 {R('evh0')}, {R('one')}, {R('one')}, {R('evh0')};",
+            f"mad.lo.u32 {R('cnt0')}, tb, {R('mone')}, {R('cnt0')};",        # window count: - leaving + entering
+            f"@pev mad.lo.u32 {R('cnt0')}, {R('bitc')}, {R('one')}, {R('cnt0')};",
+            f"setp.ge.or.s32 phi, {R('cnt0')}, 0, pq;",                     # || lock (Alg. 2, P:230): the new level
+            f"shr.u32 tl, {R('cnt0')}, 31;",                                # not locked
+            f"add.u32 {R('nlk0')}, {R('nlk0')}, tl;",
+            f"@phi mad.lo.u32 {R('wcmd0')}, {R('one')}, {1 << (TC - 1 - tt)}, {R('wcmd0')};",
+            f"sub.f64 dx, {dd}, ad{tt};",                                   # throttling excess D - A (0 unless thr)
+            f"add.f64 {R('exc0')}, {R('exc0')}, dx;",
+            f"@pthr add.f32 {R('nthr0')}, {R('nthr0')}, 0f3F800000;",
+        ]
+    for i in range(K):
+        body.append(f"mov.f64 {R(f'r0_{i}')}, ad{TC - 1 - i};")
+    body.append("}")
+    params = ", ".join(n for n, _ in names + inames)
+    name = f"MAGUS_WLSTAGE{'S' if sym else ''}_K{K}"
+    out = [f"#define {name}(...) {name}_(__VA_ARGS__)", f"#define {name}_({params}) \\", "    asm volatile( \\"]
+    out += [f'        "{l}\\n\\t" \\' for l in body]
+    out.append("        : " + ", ".join(f'"{c}"({n})' for n, c in names) + " \\")
+    out.append("        : " + ", ".join(f'"{c}"({n})' for n, c in inames) + " \\")
+    out.append('        : "memory")')
+    return out
+
+
 def build_stage_t1(validate):
     """MAGUS_TSTAGE1L{V}: one steady stage (8 ticks x 4 traces) of ONE TDP_DEFAULT policy (the TDP solo kernel, NP = 1)
     with fewer instructions than MAGUS_TSTAGE1: the next level as two fp32 compares without a select,
@@ -858,6 +990,8 @@ for K in (1, 2, 3):
     out += [""] + build_stage_f(K, thr64=False, bits=True)
     out += [""] + build_stage_l(K)
     out += [""] + build_stage_l(K, sym=True)
+    out += [""] + build_stage_l(K, tdp=True)
+    out += [""] + build_stage_l(K, sym=True, tdp=True)
     for sym in (False, True):
         for popc in (True, False):
             for bits in (False, True):
@@ -877,8 +1011,12 @@ for K in range(1, 9):
     out += [""] + build_stage_w2(K)
 for K in range(1, 9):
     out += [""] + build_stage_w1d(K)
+for K in range(1, 9):
+    out += [""] + build_stage_w1l(K)
+    out += [""] + build_stage_w1l(K, sym=True)
 for v in (True, False):
     out += [""] + build_stage_t1(v)
+out += [""] + build_stage_tl()
 path = os.path.join(os.path.dirname(__file__), "..", "paper_2502_03796_b200", "csrc", "tick4_asm.cuh")
 open(path, "w").write("\n".join(out) + "\n")
 print("wrote", os.path.normpath(path))

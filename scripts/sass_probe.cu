@@ -16,3 +16,12 @@ template __global__ void magus::magus_replay_usolo_kernel<magus::MagusTicker<PRO
 template __global__ void magus::magus_replay_tsolo_kernel<PROBE_T, 8, 3>(const __grid_constant__ CUtensorMap,
                                                                          const magus::ReplayParams);
 #endif
+#ifdef PROBE_W
+#include "../paper_2502_03796_b200/csrc/replay_wide.cuh"
+template __global__ void magus::magus_replay_wide_kernel<PROBE_K, 1, PROBE_W>(const __grid_constant__ CUtensorMap,
+                                                                              const magus::ReplayParams);
+#endif
+#ifdef PROBE_F
+template __global__ void magus::magus_replay_fused_kernel<magus::MagusTicker<PROBE_K, false>, 8, 3, (PROBE_F == 2)>(
+    const __grid_constant__ CUtensorMap, const magus::ReplayParams);
+#endif

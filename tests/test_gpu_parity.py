@@ -232,6 +232,37 @@ def test_combo_kernel_reads_each_tile_once(M, combo, n_tdp, monkeypatch):
     PA.compare_totals(res.totals, rec)
 
 
+@pytest.mark.parametrize("fuse,ctas", [("1", "12"), ("1", "16"), ("0", "12")])
+@pytest.mark.parametrize("k", [1, 3])
+@pytest.mark.parametrize("sym", [True, False])
+@pytest.mark.parametrize("segments", [9, 1])
+def test_fused_magus_tdp_kernel(M, fuse, ctas, k, sym, segments, monkeypatch):
+    """One MAGUS policy next to one replayed TDP_DEFAULT baseline (config 5's replayed pair) runs as ONE warp per (tile
+    group, segment) stepping both chain kinds over the same samples (magus_replay_fused_kernel, MAGUS_FUSE=1, built
+    for 12 or 16 CTAs per SM) -- one replay launch instead of two; with MAGUS_FUSE=0 as two launches.  Both equal the
+    oracle (records, every word, a decision dump, totals), with k in {1, 3}, symmetric (the |d| test) and asymmetric
+    thresholds, and forced segmentation (speculative entries, fix-up walks after the fused replay) or none."""
+    monkeypatch.setenv("MAGUS_FUSE", fuse)
+    monkeypatch.setenv("MAGUS_FUSED_CTAS", ctas)
+    s = SMALL["cfg5-small"]
+    th = dict(inc_threshold=1.0, dec_threshold=-1.0) if sym else dict(inc_threshold=0.7, dec_threshold=-1.3)
+    pols = [pol(deriv_ticks=k, **th), pol(kind=TDP_DEFAULT, tdp_w=217.0)]
+    stride = (s["n"] + 3) // 4 * 4
+    tr, w = gpu_gen(M, s["seed"], s["n"], s["ns"], s["mix"], stride)
+    res = run_gpu(M, tr, w, pols, s["n"], s["ns"], stride, segments=segments, dump=(s["n"] - 4, 4))
+    geo = res.geometry
+    assert geo["launch_groups"] == 2
+    monkeypatch.setenv("MAGUS_FUSE", "0")
+    with M.Replay(s["n"], s["ns"], PA.gpu_policies(pols), trace_stride=stride, tuning_segments=segments) as R2:
+        unfused = R2.geometry()
+    assert geo["kernels_per_run"] == unfused["kernels_per_run"] - (1 if fuse == "1" else 0), (geo, unfused)
+    rec, codes = oracle_run(tr.cpu().numpy(), w.cpu().numpy(), pols, s["n"])
+    PA.compare_records(res.per_trace, rec, f"fuse={fuse} ctas={ctas} k={k} sym={sym} S={segments}")
+    assert np.array_equal(res.words, PA.pack_words(codes))
+    assert np.array_equal(res.decisions, codes[:, s["n"] - 4:, :])
+    PA.compare_totals(res.totals, rec)
+
+
 def _random_case(seed):
     """A seeded random run: sizes (ragged, sometimes tiny), policies of every kind with random parameters (MAGUS k, C
     up to 64, thresholds; TDP budgets around the model's power range), a random model (Linear / Saturating, closed or
@@ -645,8 +676,13 @@ def test_full_size_every_trace(M, cfg):
     _, codes, _, _ = O.gen_replay_codes(desc, np.arange(dump0, n), PA.oracle_policies(c["policies"]))
     assert np.array_equal(res.decisions, np.transpose(codes, (2, 0, 1)))
     if cfg in (2, 5) and os.environ.get("MAGUS_SEG_BALANCE", "1") != "0":
-        # the two-length segment plan (17 x 1376 + 57 x 1344 ticks) is what these runs exercise
-        assert res.geometry["n_segments"] == 74 and res.geometry["seg_long"] == 17
+        # the two-length segment plan is what these runs exercise: cfg 2, 17 x 1376 + 57 x 1344 ticks (16 one-warp
+        # CTAs per SM); cfg 5, the fused MAGUS + TDP kernel at 12 CTAs per SM: 55 segments
+        geo = res.geometry
+        if cfg == 2 or os.environ.get("MAGUS_FUSE", "1") == "0":
+            assert geo["n_segments"] == 74 and geo["seg_long"] == 17, geo
+        else:
+            assert geo["n_segments"] == 55 and 0 < geo["seg_long"] < 55, geo
     P = len(c["policies"])
     print(f"cfg{cfg}: compared records of {n} x {P} (trace, policy) chains, per-tick words of {n_words} x {P} "
           f"chains ({n_words * P * ns:,} ticks), codes of 64 x {P}; geometry {res.geometry}, "
