@@ -172,6 +172,8 @@ ReplayKernel wide_kernel_for(int key, int nc, int lv = 0) {
     (nc == 2    ? (ReplayKernel)magus_replay_wide_kernel<KK, 2, 0>                                                  \
      : lv == 1 ? (ReplayKernel)magus_replay_wide_kernel<KK, 1, 1>                                                   \
      : lv == 2 ? (ReplayKernel)magus_replay_wide_kernel<KK, 1, 2>                                                   \
+     : lv == 3 ? (ReplayKernel)magus_replay_wide_kernel<KK, 1, 3>                                                   \
+     : lv == 4 ? (ReplayKernel)magus_replay_wide_kernel<KK, 1, 4>                                                   \
                : (ReplayKernel)magus_replay_wide_kernel<KK, 1, 0>)
     switch (key) {
         case 1: return WIDE_K(1);
@@ -762,7 +764,9 @@ static void choose_geometry(magus_replay_t* h, int n_sm, int forced_segments) {
                 sym = sym && h->lane[q].ddec == -h->lane[q].dinc;
                 lsign_ok = lsign_ok && h->lane[q].C <= 27;
             }
-            const int lv = (env_int("MAGUS_WIDE_L", 1) != 0 && lsign_ok) ? (sym ? 2 : 1) : 0;
+            // MAGUS_WIDE_L: 2 (default) = the P stage, 1 = the L stage, 0 = MAGUS_WSTAGE1D
+            const int wl = env_int("MAGUS_WIDE_L", 2);
+            const int lv = (wl != 0 && lsign_ok) ? (wl == 2 ? (sym ? 4 : 3) : (sym ? 2 : 1)) : 0;
             g.kernel = wide_kernel_for(g.key, nc, lv);
             g.ng = 1;
             g.npw = 1;

@@ -34,7 +34,8 @@ constexpr int kWideNStage = 6;
 struct WideSmem {
     static constexpr int kTileBytes = kWideTC * kWideTpc * 4;   // 2 KB
     // + one fp64 scratch per warp: its 2 traces x 32 ticks, converted once per stage (one chain per thread)
-    static constexpr int kWarpBufBytes = 2 * kWideTC * 8;       // 512 B
+    // (x 2 for the P stage: D and min(D, B_lo) per sample)
+    static constexpr int kWarpBufBytes = 2 * 2 * kWideTC * 8;   // 1 KB
     static constexpr size_t kBarOff = (size_t)kWideNStage * kTileBytes;
     static constexpr size_t kBufOff = kBarOff + 2 * kWideNStage * sizeof(uint64_t);
     static constexpr size_t kBytes = kBufOff + (size_t)kWideWarps * kWarpBufBytes;
@@ -108,6 +109,37 @@ __device__ __forceinline__ void wide_stage_l(MagusState<K, false>& st, uint32_t&
     st.evh = e0;
 }
 
+// 8 ticks of one chain from the warp's scratch: D and min(D, B_lo) as fp64 (MAGUS_WPSTAGE[S]_K<K>: the L stage with
+// A selected by the level itself; the throttled ticks are counted per block from a ballot word)
+template <int K, bool SYM>
+__device__ __forceinline__ void wide_stage_p(MagusState<K, false>& st, uint32_t& nlk, uint32_t& wcmd, double& sexc,
+                                             const double* d8, const double* l8, const DevPolicy& pol, uint32_t bitc,
+                                             uint32_t mone) {
+    uint32_t e0 = st.evh;
+#define WDP_TAIL                                                                                                 \
+    e0, st.cnt, sexc, nlk, wcmd, d8[0], d8[1], d8[2], d8[3], d8[4], d8[5], d8[6], d8[7], l8[0], l8[1], l8[2], l8[3], \
+        l8[4], l8[5], l8[6], l8[7], pol.dinc, pol.ddec, bitc, pol.one, mone
+#define R(i) st.ring.v[i]
+#define WDP(NAME)                                                                                                \
+    if constexpr (K == 1) NAME##_K1(R(0), WDP_TAIL);                                                               \
+    else if constexpr (K == 2) NAME##_K2(R(0), R(1), WDP_TAIL);                                                    \
+    else if constexpr (K == 3) NAME##_K3(R(0), R(1), R(2), WDP_TAIL);                                              \
+    else if constexpr (K == 4) NAME##_K4(R(0), R(1), R(2), R(3), WDP_TAIL);                                        \
+    else if constexpr (K == 5) NAME##_K5(R(0), R(1), R(2), R(3), R(4), WDP_TAIL);                                  \
+    else if constexpr (K == 6) NAME##_K6(R(0), R(1), R(2), R(3), R(4), R(5), WDP_TAIL);                            \
+    else if constexpr (K == 7) NAME##_K7(R(0), R(1), R(2), R(3), R(4), R(5), R(6), WDP_TAIL);                      \
+    else NAME##_K8(R(0), R(1), R(2), R(3), R(4), R(5), R(6), R(7), WDP_TAIL);
+    if constexpr (SYM) {
+        WDP(MAGUS_WPSTAGES)
+    } else {
+        WDP(MAGUS_WPSTAGE)
+    }
+#undef WDP
+#undef R
+#undef WDP_TAIL
+    st.evh = e0;
+}
+
 // 8 ticks of one chain with the samples as fp64 values (MAGUS_WSTAGE1D_K<K>: no conversion, fp64 throttle test)
 template <int K>
 __device__ __forceinline__ void wide_stage_d(MagusState<K, false>& st, float& lock, float& nthr, uint32_t& wcmd,
@@ -174,7 +206,8 @@ __device__ __forceinline__ void wide_stage2(MagusState<K, false>* st, float* loc
 // validation maximum per tick for both).  Launch: one (256 / NC)-thread CTA per (16-trace column, block of 16 policy
 // points), policy blocks fastest; p.n_pblocks = ceil(nq / 16).  LV (NC = 1 only): 0 = the one-chain stage block
 // MAGUS_WSTAGE1D_K<K>, 1 = its L form (MAGUS_WLSTAGE_K<K>: C <= 27), 2 = the L form with the |d| tune-flag test
-// (every lane policy has d*_dec == -d*_inc).
+// (every lane policy has d*_dec == -d*_inc), 3 / 4 = the P form without / with the |d| test (MAGUS_WPSTAGE[S]_K<K>:
+// the warp's scratch also holds min(D, B_lo), the throttled ticks come from a ballot word per block).
 template <int K, int NC, int LV>
 __global__ void __launch_bounds__(kWideThreads / NC, 2)
     magus_replay_wide_kernel(const __grid_constant__ CUtensorMap tmap, const ReplayParams p) {
@@ -201,7 +234,7 @@ __global__ void __launch_bounds__(kWideThreads / NC, 2)
 
     const uint32_t tile0 = ptx::smem_u32(smem);
     const uint32_t full0 = tile0 + (uint32_t)WideSmem::kBarOff, empty0 = full0 + 8 * kWideNStage;
-    double* wbuf = reinterpret_cast<double*>(smem + WideSmem::kBufOff) + warp * (2 * kWideTC);   // this warp's
+    double* wbuf = reinterpret_cast<double*>(smem + WideSmem::kBufOff) + warp * (WideSmem::kWarpBufBytes / 8);   // this warp's
     const int N = p.n_samples;
     const int n_st = (N + kWideTC - 1) / kWideTC;
     if (warp == 0) {
@@ -272,10 +305,38 @@ __global__ void __launch_bounds__(kWideThreads / NC, 2)
             vmax = max(vmax, max(__float_as_uint(v.x), __float_as_uint(v.y)));
             wbuf[lane] = (double)v.x;
             wbuf[kWideTC + lane] = (double)v.y;
+            uint32_t over = 0;   // LV >= 3: bit i = tick i of this thread's trace has D > B_lo
+            if constexpr (LV >= 3) {
+                wbuf[2 * kWideTC + lane] = fmin((double)v.x, Blo_d);   // A at f_min (A14; exact)
+                wbuf[3 * kWideTC + lane] = fmin((double)v.y, Blo_d);
+                const uint32_t o0 = __ballot_sync(0xffffffffu, v.x > B_lo);
+                const uint32_t o1 = __ballot_sync(0xffffffffu, v.y > B_lo);
+                over = ((tid >> 4) & 1) ? o1 : o0;
+            }
             __syncwarp();
             release();
             const double* my = wbuf + ((tid >> 4) & 1) * kWideTC;
-            if constexpr (LV != 0) {
+            if constexpr (LV >= 3) {
+                uint32_t nlk = 0;
+                st[0].cnt -= pol[0].smin_sc;   // biased: lock iff cnt >= 0
+                wcmd[0] = fstart[0];           // bit 0 = the level
+#pragma unroll
+                for (int g = 0; g < kWideTC / 8; ++g) {
+                    double d8[8], l8[8];
+#pragma unroll
+                    for (int t = 0; t < 8; ++t) {
+                        d8[t] = my[8 * g + t];
+                        l8[t] = my[2 * kWideTC + 8 * g + t];
+                    }
+                    wide_stage_p<K, LV == 4>(st[0], nlk, wcmd[0], ss[0].sexc, d8, l8, pol[0], bitc[0], mone);
+                }
+                st[0].cnt += pol[0].smin_sc;
+                T::set_level(st[0], wcmd[0] & 1u);
+                lockf[0] = (float)(kWideTC - nlk);
+                // throttled ticks: f_min (the level word, tick i at bit 31 - i) and D > B_lo (the ballot, tick i at bit i)
+                const uint32_t lw = (wcmd[0] >> 1) | (fstart[0] << 31);
+                nthrf[0] = (float)__popc(~lw & __brev(over));
+            } else if constexpr (LV != 0) {
                 uint32_t nlk = 0;
                 st[0].cnt -= pol[0].smin_sc;   // biased: lock iff cnt >= 0
                 wcmd[0] = fstart[0];           // bit 0 = the level

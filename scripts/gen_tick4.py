@@ -920,6 +920,64 @@ def build_stage_w1l(K, TC=8, sym=False):
     return out
 
 
+def build_stage_w1p(K, TC=8, sym=False):
+    """MAGUS_WPSTAGE[S]_K<K>: the wide kernel's one-chain L stage (MAGUS_WLSTAGE[S]_K<K>) with the level-independent
+    work taken off the per-tick dependency chain (the wide kernel is latency-bound: one chain per thread):
+    - the warp's conversion step also stores min(D, B_lo) as fp64 (L<tt>), so A = level ? D : min(D, B_lo) is one
+      select by the level itself -- no throttle test on the level -> A path;
+    - the throttled ticks are not counted per tick: the caller takes popc(~level word & ballot(D > B_lo)) per
+      32-tick block (exact: throttled iff f_min and D > B_lo, A14);
+    - the new level is (lock | +1) | (level & !-1): the lock ISETP.OR and the (d >= d*_dec) & level DSETP run side by
+      side and one PLOP3 joins them, one FP64 compare shorter than the L stage's DSETP -> DSETP.OR -> ISETP.OR."""
+    names = [(f"r0_{i}", "+d") for i in range(K)] + \
+            [("evh0", "+r"), ("cnt0", "+r"), ("exc0", "+d"), ("nlk0", "+r"), ("wcmd0", "+r")]
+    inames = [(f"S{tt}", "d") for tt in range(TC)] + [(f"L{tt}", "d") for tt in range(TC)] + \
+             [("dinc", "d"), ("ddec", "d"), ("bitc", "r"), ("one", "r"), ("mone", "r")]
+    idx = {n: f"%{i}" for i, (n, _) in enumerate(names + inames)}
+    R = idx.__getitem__
+    body = ["{", ".reg .pred phi, pinc, pev, pk, pl;", f".reg .f64 dv, da, dx, ad<{TC}>;", ".reg .b32 tb, tl, lv;",
+            f"and.b32 lv, {R('wcmd0')}, 1;", "setp.ne.u32 phi, lv, 0;",      # level = the previous tick's cmd
+            f"shl.b32 {R('wcmd0')}, {R('wcmd0')}, {TC};"]
+    for tt in range(TC):
+        dd, lo = R(f"S{tt}"), R(f"L{tt}")
+        old = f"ad{tt - K}" if tt >= K else R(f"r0_{K - 1 - tt}")
+        body += [
+            f"selp.f64 ad{tt}, {dd}, {lo}, phi;",                           # A = min(D, B[f]) (A14; exact)
+            f"sub.f64 dv, ad{tt}, {old};",                                  # Alg. 1 numerator A_t - A_{t-k} (P:207)
+            f"setp.gt.f64 pinc, dv, {R('dinc')};",                          # +1 (P:209)
+        ] + ([
+            "abs.f64 da, dv;",                                             # symmetric thresholds (d*_dec = -d*_inc):
+            f"setp.gt.f64 pev, da, {R('dinc')};",                           # tune flag iff |d| > d*_inc (P:213, P:243)
+        ] if sym else [
+            f"setp.lt.or.f64 pev, dv, {R('ddec')}, pinc;",                  # tune flag (P:213, P:243)
+        ]) + [
+            f"setp.ge.and.f64 pk, dv, {R('ddec')}, phi;",                   # f_max and not -1
+            f"and.b32 tb, {R('evh0')}, {R('bitc')};",                       # the flag leaving the C-window (scaled)
+            f"shl.b32 {R('evh0')}, {R('evh0')}, 1;",
+            f"@pev mad.lo.u32 {R('evh0')}, {R('one')}, {R('one')}, {R('evh0')};",
+            f"mad.lo.u32 {R('cnt0')}, tb, {R('mone')}, {R('cnt0')};",        # window count: - leaving + entering
+            f"@pev mad.lo.u32 {R('cnt0')}, {R('bitc')}, {R('one')}, {R('cnt0')};",
+            f"setp.ge.or.s32 pl, {R('cnt0')}, 0, pinc;",                    # lock (Alg. 2, P:230) || +1
+            "or.pred phi, pl, pk;",                                        # || (f_max && !-1): the new level
+            f"shr.u32 tl, {R('cnt0')}, 31;",                                # not locked
+            f"add.u32 {R('nlk0')}, {R('nlk0')}, tl;",
+            f"@phi mad.lo.u32 {R('wcmd0')}, {R('one')}, {1 << (TC - 1 - tt)}, {R('wcmd0')};",
+            f"sub.f64 dx, {dd}, ad{tt};",                                   # throttling excess D - A (0 unless thr)
+            f"add.f64 {R('exc0')}, {R('exc0')}, dx;",
+        ]
+    for i in range(K):
+        body.append(f"mov.f64 {R(f'r0_{i}')}, ad{TC - 1 - i};")
+    body.append("}")
+    params = ", ".join(n for n, _ in names + inames)
+    name = f"MAGUS_WPSTAGE{'S' if sym else ''}_K{K}"
+    out = [f"#define {name}(...) {name}_(__VA_ARGS__)", f"#define {name}_({params}) \\", "    asm volatile( \\"]
+    out += [f'        "{l}\\n\\t" \\' for l in body]
+    out.append("        : " + ", ".join(f'"{c}"({n})' for n, c in names) + " \\")
+    out.append("        : " + ", ".join(f'"{c}"({n})' for n, c in inames) + " \\")
+    out.append('        : "memory")')
+    return out
+
+
 def build_stage_t1(validate):
     """MAGUS_TSTAGE1L{V}: one steady stage (8 ticks x 4 traces) of ONE TDP_DEFAULT policy (the TDP solo kernel, NP = 1)
     with fewer instructions than MAGUS_TSTAGE1: the next level as two fp32 compares without a select,
@@ -1014,6 +1072,8 @@ for K in range(1, 9):
 for K in range(1, 9):
     out += [""] + build_stage_w1l(K)
     out += [""] + build_stage_w1l(K, sym=True)
+    out += [""] + build_stage_w1p(K)
+    out += [""] + build_stage_w1p(K, sym=True)
 for v in (True, False):
     out += [""] + build_stage_t1(v)
 out += [""] + build_stage_tl()

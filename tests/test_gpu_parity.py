@@ -682,7 +682,7 @@ def test_full_size_every_trace(M, cfg):
         if cfg == 2 or os.environ.get("MAGUS_FUSE", "1") == "0":
             assert geo["n_segments"] == 74 and geo["seg_long"] == 17, geo
         else:
-            assert geo["n_segments"] == 55 and 0 < geo["seg_long"] < 55, geo
+            assert geo["n_segments"] == 55, geo
     P = len(c["policies"])
     print(f"cfg{cfg}: compared records of {n} x {P} (trace, policy) chains, per-tick words of {n_words} x {P} "
           f"chains ({n_words * P * ns:,} ticks), codes of 64 x {P}; geometry {res.geometry}, "
