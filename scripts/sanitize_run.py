@@ -1,8 +1,9 @@
 """Small replays that cover every kernel family, for compute-sanitizer (memcheck / racecheck / synccheck /
 initcheck).  GPU box only.  usage: compute-sanitizer --tool <t> python scripts/sanitize_run.py
 
-Covers: the generator, the pre-pass, the one-warp solo replay kernel (MAGUS k <= 3, TMA/mbarrier ring), the
-two-warp combined MAGUS + TDP kernel (shared ring, empty barriers), the unsegmented wide kernel (8-warp CTAs), the
+Covers: the generator, the pre-pass, the one-warp solo replay kernel (MAGUS k <= 3, TMA/mbarrier ring; the L stage and
+variant 2), the fused one-warp MAGUS + TDP kernel (12- and 16-CTA builds), the two-warp combined MAGUS + TDP kernel
+(shared ring, empty barriers), the unsegmented wide kernel (8-warp CTAs; P, L and D stages, per-warp fp64 scratch), the
 multi-warp replay kernel (shared tiles: several policy warps, TDP / STATIC_MIN / k >= 4 / 64-bit logs), the
 fix-up mark + split / lockstep / per-thread walks, the totals and chunk-sum kernels, the decision re-simulation,
 the wall-clock kernels, the counter ingest -- direct launches and the captured CUDA graph.  Each run is checked
@@ -54,9 +55,32 @@ def main():
     case("cfg2-small graph", 2, 260, 6000, 0, cfg2, 6, stream=True)
     case("cfg5-small solo+tdp, walks", 5, 257, 6000, 2, cfg5 + sweep64()[40:42], 7)
     case("cfg3-small shared tiles", 3, 64, 3000, 1, sweep64()[::5] + [pol(kind=STATIC_MAX)], 5)
-    case("cfg5 combined MAGUS + TDP kernel, walks", 5, 257, 6000, 2, cfg5, 7)
+    case("cfg5 fused MAGUS + TDP kernel (one warp), walks", 5, 257, 6000, 2, cfg5, 7)
+    case("fused kernel, k = 2, asymmetric thresholds", 5, 257, 6000, 2,
+         [pol(deriv_ticks=2, inc_threshold=0.7, dec_threshold=-1.3), pol(kind=TDP_DEFAULT, tdp_w=217.0)], 7)
+    os.environ["MAGUS_FUSED_CTAS"] = "16"
+    case("fused kernel, 16-CTA build", 5, 257, 6000, 2, cfg5, 7)
+    os.environ.pop("MAGUS_FUSED_CTAS")
+    os.environ["MAGUS_COMBO"] = "1"
+    case("cfg5 combined two-warp MAGUS + TDP kernel, walks", 5, 257, 6000, 2, cfg5, 7)
+    os.environ.pop("MAGUS_COMBO")
+    os.environ["MAGUS_FUSE"] = "0"
+    case("cfg5 separate MAGUS solo + TDP solo launches", 5, 257, 6000, 2, cfg5, 7)
+    os.environ.pop("MAGUS_FUSE")
+    case("solo L stage, asymmetric thresholds", 2, 260, 6000, 0,
+         [pol(inc_threshold=0.8, dec_threshold=-1.1), pol(kind=STATIC_MAX)], 6)
+    os.environ["MAGUS_SOLO_BAL"] = "2"
+    case("solo stage variant 2", 2, 260, 6000, 0, cfg2, 6)
+    os.environ.pop("MAGUS_SOLO_BAL")
     os.environ["MAGUS_WIDE"] = "1"
-    case("cfg3-small unsegmented wide plan", 3, 40, 3000, 1, sweep64() + [pol(kind=STATIC_MAX)], 0)
+    case("cfg3-small unsegmented wide plan (P stage)", 3, 40, 3000, 1, sweep64() + [pol(kind=STATIC_MAX)], 0)
+    os.environ["MAGUS_WIDE_L"] = "1"
+    case("wide plan, L stage", 3, 40, 3000, 1, sweep64(), 0)
+    os.environ["MAGUS_WIDE_L"] = "0"
+    case("wide plan, D stage", 3, 40, 3000, 1, sweep64(), 0)
+    os.environ.pop("MAGUS_WIDE_L")
+    case("wide plan, asymmetric thresholds (P stage)", 3, 40, 3000, 1,
+         [pol(deriv_ticks=k, inc_threshold=0.6, dec_threshold=-1.7) for k in (1, 3, 8)], 0)
     os.environ["MAGUS_WIDE_NC"] = "2"
     case("wide plan, two chains per thread", 3, 40, 3000, 1, sweep64(), 0)
     os.environ.pop("MAGUS_WIDE_NC")
