@@ -293,6 +293,12 @@ int32_t magus_abi_version(void);
  * many-policy sweeps, DESIGN.md section 9a -- then n_segments = 1 and there is no fix-up). */
 magus_status magus_replay_geometry(const magus_replay_t* h, int32_t out[16]);
 
+/* Diagnostics (test infrastructure for the debug-check build): returns -1 when the library was
+ * built without device-side bounds checks (the release build), else launches one thread that checks `violate == 0`
+ * with the library's MAGUS_CHECK and returns 1 if the check trapped the kernel (the CUDA context is then unusable:
+ * call it in a separate process), 0 if it passed.  Needs a GPU only in the debug build. */
+int32_t magus_debug_check_probe(int32_t violate);
+
 #ifdef __cplusplus
 }
 #endif

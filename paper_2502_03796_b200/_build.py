@@ -16,6 +16,9 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libmagus_replay.so")
+# the debug-check build (device-side bounds checks that trap, MAGUS_DEBUG_CHECKS=1; device_common.cuh), loaded only by
+# tests/test_debug_checks.py through MAGUS_LIB_PATH
+LIB_DEBUG = os.path.join(LIBDIR, "libmagus_replay_debug.so")
 SOURCES = ["magus_replay.cu", "gen_traces.cu", "ingest.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -42,17 +45,27 @@ def _deps():
                                                                __file__]
 
 
-def build(force: bool = False, verbose: bool = False, out: str | None = None) -> str:
-    """Compile the library; `out` (or MAGUS_LIB_OUT) = another output path, for build-variant experiments."""
+def build(force: bool = False, verbose: bool = False, out: str | None = None, debug: bool = False) -> str:
+    """Compile the library; `out` (or MAGUS_LIB_OUT) = another output path, for build-variant experiments;
+    debug = the debug-check build (LIB_DEBUG)."""
     out = out or os.environ.get("MAGUS_LIB_OUT")
     if out:
         return _compile(out, verbose)
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(d) for d in _deps()):
-        return LIB
-    return _compile(LIB, verbose)
+    lib = LIB_DEBUG if debug else LIB
+    if not force and os.path.exists(lib) and os.path.getmtime(lib) >= max(os.path.getmtime(d) for d in _deps()):
+        return lib
+    return _compile(lib, verbose, ["-DMAGUS_DEBUG_CHECKS=1"] if debug else [])
 
 
-def _compile(LIB: str, verbose: bool) -> str:
+def build_all(force: bool = False) -> None:
+    """The release and the debug-check library, compiled concurrently."""
+    import concurrent.futures as cf
+    with cf.ThreadPoolExecutor(2) as ex:
+        for f in [ex.submit(build, force, False, None, False), ex.submit(build, force, False, None, True)]:
+            f.result()
+
+
+def _compile(LIB: str, verbose: bool, extra: list | None = None) -> str:
     LIBDIR = os.path.dirname(os.path.abspath(LIB))
     os.makedirs(LIBDIR, exist_ok=True)
     nvcc = _nvcc()
@@ -63,6 +76,7 @@ def _compile(LIB: str, verbose: bool) -> str:
         if os.environ.get(key):
             flags += [f"-D{key}={int(os.environ[key])}"]
     flags += os.environ.get("MAGUS_DEFS", "").split()   # build-variant experiments, e.g. "-DMAGUS_SOLO_UNROLL=2"
+    flags += extra or []
     if os.environ.get("MAGUS_PTXAS_VERBOSE"):
         flags += ["-Xptxas", "-v"]
     for src in SOURCES:
@@ -81,4 +95,9 @@ def _compile(LIB: str, verbose: bool) -> str:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    if "--debug" in sys.argv:
+        print(build(force="--force" in sys.argv, verbose=True, debug=True))
+    elif "--all" in sys.argv:
+        build_all(force="--force" in sys.argv)
+    else:
+        print(build(force="--force" in sys.argv, verbose=True))

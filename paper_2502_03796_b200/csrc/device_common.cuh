@@ -38,6 +38,34 @@ struct DevPolicy {
     uint32_t smin_sc;      // 32-bit-log kinds: s_min << (C-1), the lock threshold on the scaled window count
 };
 
+// Debug-check build (MAGUS_DEBUG_CHECKS=1, the library libmagus_replay_debug.so built next to the release one):
+// every state / ring / chain index and every shared-memory tile or scratch access of the replay kernels is checked
+// against its allocation, and a violation traps the kernel (cudaErrorLaunchFailure), so a GPU test running the
+// debug build over every kernel family stands in for compute-sanitizer's memcheck where that tool is unavailable.
+#ifndef MAGUS_DEBUG_CHECKS
+#define MAGUS_DEBUG_CHECKS 0
+#endif
+#if MAGUS_DEBUG_CHECKS
+#ifdef __CUDA_ARCH__
+#define MAGUS_CHECK(cond)    \
+    do {                     \
+        if (!(cond)) __trap(); \
+    } while (0)
+#else
+#define MAGUS_CHECK(cond) ((void)0)
+#endif
+#else
+#define MAGUS_CHECK(cond) ((void)0)
+#endif
+// a shared-memory byte range [addr, addr + bytes) lies inside the CTA's dynamic shared memory
+__device__ __forceinline__ bool smem_range_ok(uint32_t addr, uint32_t bytes) {
+    uint32_t size;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(size));
+    extern __shared__ __align__(16) uint8_t magus_dyn_smem_probe[];
+    const uint32_t base = (uint32_t)__cvta_generic_to_shared(magus_dyn_smem_probe);
+    return addr >= base && addr + bytes <= base + size;
+}
+
 // run-wide constants and scratch pointers
 struct ReplayParams {
     int32_t n_traces, n_samples;
@@ -93,9 +121,12 @@ __device__ __forceinline__ void wl_append(uint64_t* wl, uint32_t* count, bool wa
 }
 
 __host__ __device__ __forceinline__ int64_t st_idx(const ReplayParams& p, int e, int q, int s, int j) {
+    MAGUS_CHECK(e >= 0 && e < 2 && q >= 0 && q < p.n_lane && s >= 0 && s < p.n_seg && j >= 0 && j < p.n_traces);
     return ((int64_t)(e * p.n_lane + q) * p.n_seg + s) * p.n_traces + j;
 }
 __host__ __device__ __forceinline__ int64_t ring_idx(const ReplayParams& p, int e, int q, int s, int r, int j) {
+    MAGUS_CHECK(e >= 0 && e < 2 && q >= 0 && q < p.n_lane && s >= 0 && s < p.n_seg && r >= 0 && r < p.kr && j >= 0 &&
+                j < p.n_traces);
     return (((int64_t)(e * p.n_lane + q) * p.n_seg + s) * p.kr + r) * p.n_traces + j;
 }
 // Time segment s covers ticks [seg_begin(s), seg_finish(s)): every boundary is a
@@ -108,6 +139,7 @@ __host__ __device__ __forceinline__ int seg_finish(const ReplayParams& p, int s)
     return e < p.n_samples ? e : p.n_samples;
 }
 __host__ __device__ __forceinline__ int64_t chain_idx(const ReplayParams& p, int q, int j) {
+    MAGUS_CHECK(q >= 0 && q < p.n_lane && j >= 0 && j < p.n_traces);
     return (int64_t)q * p.n_traces + j;
 }
 

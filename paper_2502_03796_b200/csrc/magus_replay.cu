@@ -590,6 +590,19 @@ extern "C" const char* magus_set_global_error(const char* msg) {
 }
 
 extern "C" int32_t magus_abi_version(void) { return MAGUS_ABI_VERSION; }
+
+__global__ void magus_debug_probe_kernel(int32_t violate) { MAGUS_CHECK(violate == 0); }
+
+extern "C" int32_t magus_debug_check_probe(int32_t violate) {
+#if MAGUS_DEBUG_CHECKS
+    magus_debug_probe_kernel<<<1, 1>>>(violate);
+    const cudaError_t e = cudaDeviceSynchronize();
+    return e == cudaSuccess ? 0 : 1;
+#else
+    (void)violate;
+    return -1;
+#endif
+}
 extern "C" const char* magus_last_error(void) { return g_error.c_str(); }
 extern "C" const char* magus_replay_last_error(const magus_replay_t* h) {
     return h ? h->err.c_str() : g_error.c_str();

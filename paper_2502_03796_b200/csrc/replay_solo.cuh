@@ -57,6 +57,7 @@ __device__ __forceinline__ void mbar_wait_loop(uint32_t bar, uint32_t parity) {
 template <int TC>
 __device__ __forceinline__ void solo_issue(uint32_t tile, const CUtensorMap* tmap, uint32_t bar, int x, int t0,
                                            uint64_t cpol) {
+    MAGUS_CHECK(smem_range_ok(tile, TC * kTracesPerWarp * 4) && smem_range_ok(bar, 8) && x >= 0 && t0 >= 0);
     asm volatile(
         "{\n\t.reg .pred e;\n\t"
         "elect.sync _|e, 0xffffffff;\n\t"
@@ -351,6 +352,7 @@ __device__ __forceinline__ void solo_magus_body(const CUtensorMap* tmap, const R
 #endif
             for (int sub = 0; sub < 32 / TC; ++sub) {
                 const uint32_t tile = tile0 + slot * kTileBytes;
+                MAGUS_CHECK(slot >= 0 && slot < NSTAGE && smem_range_ok(tile + lane_off, (TC - 1) * 512 + 16));
                 mbar_wait_loop(bar0 + 8 * slot, phase);
                 if constexpr (BAL == 1) solo_stage(st, lockf, nthrf, wcmd, ss, vmax, tile + lane_off, sc, pol);
                 else if constexpr (BAL == 2)
@@ -384,6 +386,7 @@ __device__ __forceinline__ void solo_magus_body(const CUtensorMap* tmap, const R
             for (int sub = 0; sub < 32 / TC && i < G.n_stages; ++sub) {
                 const int t0 = bt0 + sub * TC;
                 const uint32_t tile = tile0 + slot * kTileBytes;
+                MAGUS_CHECK(slot >= 0 && slot < NSTAGE && smem_range_ok(tile + lane_off, (TC - 1) * 512 + 16));
                 mbar_wait_loop(bar0 + 8 * slot, phase);
                 const float4* rows = reinterpret_cast<const float4*>(smem + slot * kTileBytes) + lane;
                 if (t0 + TC <= G.seg_end) {
@@ -1160,6 +1163,7 @@ __global__ void __launch_bounds__(32, MINB)
 #pragma unroll 1
             for (int sub = 0; sub < 32 / TC; ++sub) {
                 const uint32_t tile = tile0 + slot * kTileBytes;
+                MAGUS_CHECK(slot >= 0 && slot < NSTAGE && smem_range_ok(tile + lane_off, (TC - 1) * 512 + 16));
                 mbar_wait_loop(bar0 + 8 * slot, phase);
                 fused_stage_lt<T::kRingK, SYM>(st, nlk, nthrf, wcmd, ss, vmax, wcmdT, excT, nthrT, sT, tile + lane_off,
                                                sc, pol, ahi, alo);
@@ -1183,6 +1187,7 @@ __global__ void __launch_bounds__(32, MINB)
             for (int sub = 0; sub < 32 / TC && i < G.n_stages; ++sub) {
                 const int t0 = bt0 + sub * TC;
                 const uint32_t tile = tile0 + slot * kTileBytes;
+                MAGUS_CHECK(slot >= 0 && slot < NSTAGE && smem_range_ok(tile + lane_off, (TC - 1) * 512 + 16));
                 mbar_wait_loop(bar0 + 8 * slot, phase);
                 const float4* rows = reinterpret_cast<const float4*>(smem + slot * kTileBytes) + lane;
                 if (t0 + TC <= G.seg_end) {

@@ -44,6 +44,7 @@ struct WideSmem {
 // the elected lane arms `bar` for one tile and issues the 2-D TMA box {16 traces, 32 ticks} at (x, t0); no L2
 // eviction hint: the tile is read again by the other policy blocks of the column
 __device__ __forceinline__ void wide_issue(uint32_t tile, const CUtensorMap* tmap, uint32_t bar, int x, int t0) {
+    MAGUS_CHECK(smem_range_ok(tile, WideSmem::kTileBytes) && smem_range_ok(bar, 8) && x >= 0 && t0 >= 0);
     asm volatile(
         "{\n\t.reg .pred e;\n\t"
         "elect.sync _|e, 0xffffffff;\n\t"
@@ -303,6 +304,8 @@ __global__ void __launch_bounds__(kWideThreads / NC, 2)
             const float2 v = *reinterpret_cast<const float2*>(smem + slot * kTileBytes + lane * (kWideTpc * 4) +
                                                              (tid >> 4 & ~1) * 4);
             vmax = max(vmax, max(__float_as_uint(v.x), __float_as_uint(v.y)));
+            MAGUS_CHECK(smem_range_ok(ptx::smem_u32(wbuf), WideSmem::kWarpBufBytes) &&
+                        smem_range_ok(ptx::smem_u32(smem + slot * kTileBytes + lane * (kWideTpc * 4) + (tid >> 4 & ~1) * 4), 8));
             wbuf[lane] = (double)v.x;
             wbuf[kWideTC + lane] = (double)v.y;
             uint32_t over = 0;   // LV >= 3: bit i = tick i of this thread's trace has D > B_lo

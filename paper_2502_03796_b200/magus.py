@@ -91,6 +91,8 @@ if not os.path.exists(LIB_PATH):
 lib = C.CDLL(LIB_PATH)
 _S = C.c_int
 lib.magus_abi_version.restype = C.c_int32
+lib.magus_debug_check_probe.restype = C.c_int32
+lib.magus_debug_check_probe.argtypes = [C.c_int32]
 lib.magus_last_error.restype = C.c_char_p
 lib.magus_replay_last_error.restype = C.c_char_p
 lib.magus_replay_last_error.argtypes = [C.c_void_p]
