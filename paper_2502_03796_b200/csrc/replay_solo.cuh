@@ -663,6 +663,7 @@ __global__ void __launch_bounds__(32, kSoloCtasPerSm)
             for (int c = 0; c < kChains; ++c) fstart[c] = T::level(st[c]);
         }
         const uint32_t tile = tile0 + slot * kTileBytes;
+        MAGUS_CHECK(slot >= 0 && slot < NSTAGE && smem_range_ok(tile + lane_off, (TC - 1) * 512 + 16));
         mbar_wait_loop(bar0 + 8 * slot, phase);
         if (t0 + TC <= seg_end) {
             solo_ustage<K_OF(T), VAR>(st, lockf, nthrf, wcmd, ss, vmax, tile + lane_off, sc, pol, m, smin, bitc, mone);
@@ -814,6 +815,7 @@ __device__ __forceinline__ void tsolo_body(const CUtensorMap* tmap, const Replay
         for (int sub = 0; sub < 32 / TC && i < G.n_stages; ++sub) {
             const int t0 = bt0 + sub * TC;
             const uint32_t tile = tile0 + slot * kTileBytes;
+            MAGUS_CHECK(slot >= 0 && slot < NSTAGE && smem_range_ok(tile + lane_off, (TC - 1) * 512 + 16));
             mbar_wait_loop(bar0 + 8 * slot, phase);
             if (t0 + TC <= G.seg_end) {
                 if constexpr (NP == 1 && !MAGUS_TDP_LEAN)
