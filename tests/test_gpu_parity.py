@@ -263,6 +263,25 @@ def test_fused_magus_tdp_kernel(M, fuse, ctas, k, sym, segments, monkeypatch):
     PA.compare_totals(res.totals, rec)
 
 
+@pytest.mark.parametrize("model", ["saturating", "open-loop", "short-period"])
+def test_fused_kernel_models(M, model, monkeypatch):
+    """The fused MAGUS + TDP kernel under the other observation / bandwidth models: Saturating bandwidth (B_lo from the
+    knee), open loop (A = D, no tick throttled: the throttle bound is +inf) and a shorter sample period -- records,
+    every word and totals equal the oracle's, with forced segmentation."""
+    monkeypatch.setenv("MAGUS_FUSE", "1")
+    s = SMALL["cfg5-small"]
+    mk = dict(saturating=dict(bw_shape=1, bw_knee=0.5), **{"open-loop": dict(observe=1)},
+              **{"short-period": dict(sample_period_s=0.05)})[model]
+    pols = [pol(), pol(kind=TDP_DEFAULT, tdp_w=217.0)]
+    stride = (s["n"] + 3) // 4 * 4
+    tr, w = gpu_gen(M, s["seed"], s["n"], s["ns"], s["mix"], stride)
+    res = run_gpu(M, tr, w, pols, s["n"], s["ns"], stride, segments=7, model=M.Model(**mk))
+    rec, codes = oracle_run(tr.cpu().numpy(), w.cpu().numpy(), pols, s["n"], model=O.Model(**mk))
+    PA.compare_records(res.per_trace, rec, f"fused {model}")
+    assert np.array_equal(res.words, PA.pack_words(codes))
+    PA.compare_totals(res.totals, rec)
+
+
 def _random_case(seed):
     """A seeded random run: sizes (ragged, sometimes tiny), policies of every kind with random parameters (MAGUS k, C
     up to 64, thresholds; TDP budgets around the model's power range), a random model (Linear / Saturating, closed or
