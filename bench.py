@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--ref-budget-s", type=float, default=150.0,
                     help="--impl reference: wall-time budget of warmup + steps (sizes each step's sample)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--open-loop", action="store_true", help="NEXT-3 observation model: the trace is a recorded "
+                    "throughput observed as is (magus_model.observe = 1, DESIGN.md A30); not the headline")
     ap.add_argument("--wallclock", action="store_true", help="NEXT-1 time model: wall-clock governor rounds "
                     "(MAGUS_F_WALLCLOCK, DESIGN.md A32); not the headline configuration")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -237,7 +239,7 @@ def run_ours(args, cfg):
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
     pols = [M.Policy(**d) for d in cfg["policies"][p_off:p_off + n_pol]]
-    R = M.Replay(n, ns, pols, M.Model(), trace_stride=stride, global_trace_offset=offset, rank=rank, world=world,
+    R = M.Replay(n, ns, pols, M.Model(observe=1 if args.open_loop else 0), trace_stride=stride, global_trace_offset=offset, rank=rank, world=world,
                  nccl_id=nccl_id, n_policies_global=n_pol_glob, policy_offset=p_off,
                  flags=M.F_TIMING | (M.F_WALLCLOCK if args.wallclock else 0) | (M.F_NCCL if args.nccl else 0))
     geo = R.geometry()
@@ -327,7 +329,7 @@ def run_ours(args, cfg):
         del th, wh
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.wallclock:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.wallclock and not args.open_loop:
         cpu = cpu_baseline(cfg, args.cpu_seconds)
 
     geo = R.geometry()                            # the plan actually timed (after any adaptive re-plan)
@@ -340,7 +342,7 @@ def run_ours(args, cfg):
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
             "scaling": "weak" if ps == 1 else "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg["name"] + ("+wallclock" if args.wallclock else ""), "n_traces_per_gpu": n, "n_samples": ns, "policies": len(pols),
+            "config": {"workload": cfg["name"] + ("+wallclock" if args.wallclock else "") + ("+open-loop" if args.open_loop else ""), "n_traces_per_gpu": n, "n_samples": ns, "policies": len(pols),
                        "policies_global": n_pol_glob,
                        # STATIC_MAX (and a TDP_DEFAULT policy that can never leave f_max) have a closed-form record:
                        # replayed = the policies whose recurrence the kernels step

@@ -89,6 +89,8 @@ struct ReplayParams {
     // chain states, SoA: [e (0 entry, 1 exit)][q][s][j]
     uint8_t* st_f;
     uint64_t* st_log;
+    int32_t* st_first;     // open-loop solo kernel (A30): [q][s][j] first event (lock | flag) of segment s from its start,
+                           // | (the event's cmd) << 30; -1: no event in the segment
     float* st_ring;        // [e][q][s][r < kr][j]
     // per-chain totals [q][j], accumulated with atomics by every segment (and by the fix-up deltas):
     // integers add modulo 2^32 / 2^64 and the throttling excess is an exact fp64 sum, so the result

@@ -220,8 +220,9 @@ ReplayKernel fused_kernel_for(int key, bool sym, int ctas) {
 }
 
 // one-warp-CTA replay kernel (replay_solo.cuh) of a chain kind, or nullptr if it has none
-ReplayKernel solo_kernel_for(int key, bool sym, bool bits_ok, bool lsign_ok) {
+ReplayKernel solo_kernel_for(int key, bool sym, bool bits_ok, bool lsign_ok, bool open = false) {
     int v = env_int("MAGUS_SOLO_BAL", 20);   // stage block variant (replay_solo.cuh)
+    if (open) v = sym ? 31 : 30;             // the open-loop O stage (the caller checked lsign_ok)
     // 20: the L stage (level in the cmd word, lock = sign of the biased window count; needs C <= 27), with the
     // |d| tune-flag test (21) when every lane policy has d*_dec == -d*_inc; 22 forces the two-compare L stage
     if (v == 20 || v == 22) v = !lsign_ok ? 2 : (v == 20 && sym) ? 21 : 20;
@@ -262,6 +263,8 @@ ReplayKernel solo_kernel_for(int key, bool sym, bool bits_ok, bool lsign_ok) {
      : v == 5 ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 5>                    \
      : v == 20 ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 20>                  \
      : v == 21 ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 21>                  \
+     : v == 30 ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 30>                  \
+     : v == 31 ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 31>                  \
               : (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 1>)
     switch (key) {
         case 1: return SOLO_K(1);
@@ -524,6 +527,8 @@ struct magus_replay {
     double* d_fin_local = nullptr;    // exchange on: [P_glob][13], this rank's slice rows (the rest stays 0)
     int P_glob = 1, p_off = 0;        // parameter-grid split: global policy count, global index of local policy 0
     bool xchg = false;                // the cross-rank exchange runs (world > 1 or MAGUS_F_NCCL)
+    bool open_fast = false;           // open loop, every group a MAGUS solo group: the O stage + the closed-form
+                                      // open-loop fix-up instead of the chain walk
     int n_chunks = 1;                 // trace chunks of the totals kernel
     int32_t* d_first_low = nullptr;   // [n_traces] speculation aid
     uint8_t* d_chain = nullptr;       // per-chain totals (ReplayParams::c_*)
@@ -737,6 +742,11 @@ static void choose_geometry(magus_replay_t* h, int n_sm, int forced_segments) {
             p.kr = std::max(p.kr, q.k);
         }
     }
+    // Open loop (A30) with every launch group a MAGUS kind with a solo stage block (k <= 3, C <= 27): the O stage and
+    // the closed-form open-loop fix-up (MAGUS_OPEN_FAST default 1)
+    h->open_fast = d.model.observe == 1 && env_int("MAGUS_OPEN_FAST", 1) != 0 && !h->groups.empty();
+    for (const LaunchGroup& g : h->groups) h->open_fast = h->open_fast && g.key >= 1 && g.key <= 3;
+    for (const DevPolicy& q : h->lane) h->open_fast = h->open_fast && (q.kind != LANE_MAGUS || q.C <= 27);
     // Unsegmented plan: when every launch group is a MAGUS kind with a wide kernel and one
     // chain per lane already gives enough warps (>= MAGUS_WIDE_WARPS_PER_SM per SM, default 12; the lanes at least
     // 3/4 used), replay each chain whole -- no speculation, no fix-up.  MAGUS_WIDE = 0 never, 1 whenever possible.
@@ -902,7 +912,7 @@ static void choose_geometry(magus_replay_t* h, int n_sm, int forced_segments) {
             bits_ok = bits_ok && lp.dinc >= 0x1p-60 && lp.ddec <= -0x1p-60;
             lsign_ok = lsign_ok && lp.C <= 27;
         }
-        ReplayKernel sk = solo_kernel_for(g.key, sym, bits_ok, lsign_ok);
+        ReplayKernel sk = solo_kernel_for(g.key, sym, bits_ok, lsign_ok, h->open_fast);
         g.solo = sk && g.npw == 1 && kTC == 8 && env_int("MAGUS_SOLO", 1) != 0;
         if (g.solo) {
             g.kernel = sk;
@@ -1162,6 +1172,7 @@ extern "C" magus_status magus_replay_create(const magus_replay_desc* desc, magus
     h->d_pol = dpol;
     ALLOC(p.st_f, nst);
     ALLOC(p.st_log, nst);
+    ALLOC(p.st_first, nst);
     ALLOC(p.st_ring, nst * p.kr);
     ALLOC(h->d_chain, nchain * kChainBytes);   // per-chain totals, zeroed by every run
     p.c_sexc = (double*)h->d_chain;
@@ -1455,7 +1466,14 @@ static magus_status enqueue_run(magus_replay_t* h, const float* d_trace, const f
     }
     if (timing) CU(h, rec(2));
     if (d.n_traces > 0) {
-        if (has_work && p.n_seg > 1) {
+        bool open_fix = h->open_fast;
+        for (const LaunchGroup& g : h->groups) open_fix = open_fix && g.solo;
+        if (has_work && p.n_seg > 1 && open_fix) {
+            // open loop: wrong entry levels corrected in closed form from each segment's first event (section 9b)
+            for (const LaunchGroup& g : h->groups)
+                CU(h, launch_k(magus_fix_openloop_kernel, dim3((unsigned)((d.n_traces + 3) / 4), (unsigned)g.nq),
+                               dim3(128), 0, s, h->pdl && !timing, p, ep, g.q_base));
+        } else if (has_work && p.n_seg > 1) {
             // exact fix-up: the first wrong entry of every chain, then one walk per
             // chain in time order from there (magus_fix_lockstep_kernel; magus_fix_walk_kernel for the rest)
             dim3 gc((unsigned)((d.n_traces + 255) / 256), (unsigned)(p.n_seg - 1), (unsigned)p.n_lane);
@@ -1645,6 +1663,7 @@ extern "C" magus_status magus_replay_results(magus_replay_t* h, magus_results* o
     // for replay time (config 5: 2,053 wrong entries at 32 ticks, none at 96; step 0.835 -> 0.721 ms).
     bool warm_replan = false;
     if (d.tuning_segments == 0 && d.tuning_warmup == 0 && h->rp.n_seg > 1 && segs > 0 && h->warm_replans < 3 &&
+        !h->open_fast &&
         !env_int("MAGUS_NO_REPLAN", 0) && !env_int("MAGUS_NO_WARM_ADAPT", 0)) {
         const int extra = 2 * h->warm_extra + 64;
         if (h->rp.warmup + (extra - h->warm_extra) <= h->rp.seg_len / 8) {
@@ -1653,7 +1672,7 @@ extern "C" magus_status magus_replay_results(magus_replay_t* h, magus_results* o
             warm_replan = true;
         }
     }
-    if (d.tuning_segments == 0 && h->rp.n_seg > 1 && !env_int("MAGUS_NO_REPLAN", 0)) {
+    if (d.tuning_segments == 0 && h->rp.n_seg > 1 && !env_int("MAGUS_NO_REPLAN", 0) && !h->open_fast) {
         const double spec = (double)h->rp.n_lane * (h->rp.n_seg - 1) * std::max(1, d.n_traces);
         const bool halve = (double)segs > h->replan_frac * spec;
         if (halve || warm_replan) {
@@ -1763,7 +1782,11 @@ extern "C" magus_status magus_replay_geometry(const magus_replay_t* h, int32_t o
     int nlaunch = 0;
     for (const LaunchGroup& g : h->groups) nlaunch += g.fused ? 0 : 1;
     int nk = 1 + (has_work ? (h->wall ? nwall : nlaunch) : 0);   // pre-pass, replay per launch (group or combined pair)
-    if (has_work && p.n_seg > 1 && !h->wall) {
+    bool open_fix = h->open_fast;
+    for (const LaunchGroup& g : h->groups) open_fix = open_fix && g.solo;
+    if (has_work && p.n_seg > 1 && !h->wall && open_fix) {
+        nk += (int)h->groups.size();                              // one open-loop fix-up kernel per launch group
+    } else if (has_work && p.n_seg > 1 && !h->wall) {
         int nw = 0;
         for (const LaunchGroup& g : h->groups) nw += walk_kernel_for(g.key) ? 1 : 0;
         nk += 1 + nw;                                             // mark + one chain-walk kernel per launch group

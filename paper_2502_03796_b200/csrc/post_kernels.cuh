@@ -99,6 +99,74 @@ __global__ void __launch_bounds__(256) magus_fix_mark_kernel(const ReplayParams 
     if (entry_mismatch_any(p, pol, q, s, j)) atomicMin(f.first_bad + (int64_t)q * p.n_traces + j, s);
 }
 
+// ------------------------------------------------------------------ the open-loop fix-up (A30)
+// Open loop (magus_model.observe = 1): A = D, so Alg. 1's derivatives, the tune flags, the window count and Alg. 2's
+// lock depend on the trace only, and after the warm-up (>= k + C - 1 ticks) a speculative segment's ring, log and count
+// equal the true ones.  Only its entry LEVEL can be wrong, and the level is a last-writer scan of the events (lock |
+// flag: cmd = lock | +1 ? f_max : -1 ? f_min : level).  So a segment replayed from the wrong entry level g (true X)
+// differs only up to its first event e (recorded by the replay in st_first): the level in effect at ticks [0, e] and
+// the cmd at ticks [0, e) are X instead of g, and the transition at e is [cmd_e != X] instead of [cmd_e != g]; with no
+// event the whole segment is at X and so is its exit.  One thread per chain resolves the entries in segment order and
+// adds these closed-form deltas (n_hi, transitions, the cmd half of the digest, the dumped cmd words) -- no chain walk.
+// One warp per chain, one lane per segment (32 segments per pass): the true entry level of segment s is the
+// (speculative, hence true) exit of the last earlier segment with an event, or the carried level -- a ballot and a
+// shuffle, not a serial walk over the segments.
+__global__ void __launch_bounds__(128) magus_fix_openloop_kernel(const ReplayParams p, const EpiParams e, int q_base) {
+    ptx::pdl_wait();
+    const int lane = threadIdx.x & 31;
+    const int j = blockIdx.x * 4 + (threadIdx.x >> 5);
+    const int q = q_base + blockIdx.y;
+    if (j >= p.n_traces) return;   // warp-uniform
+    uint32_t carry = p.st_f[st_idx(p, 1, q, 0, j)];   // segment 0 starts from the exact initial state: its exit is true
+    uint32_t fixed = 0;
+    for (int base = 1; base < p.n_seg; base += 32) {
+        const int s = base + lane;
+        const bool valid = s < p.n_seg;
+        uint32_t g = 0, spec_exit = 0;
+        int32_t code = -1;
+        if (valid) {
+            const int64_t si = st_idx(p, 0, q, s, j);
+            g = p.st_f[si];                      // the speculative entry level
+            code = p.st_first[si];
+            spec_exit = p.st_f[st_idx(p, 1, q, s, j)];
+        }
+        const bool has_ev = valid && code >= 0;
+        const uint32_t m = __ballot_sync(0xffffffffu, has_ev);
+        const uint32_t below = m & ((1u << lane) - 1u);
+        const int src = below ? 31 - __clz(below) : 0;
+        const uint32_t ev_exit = __shfl_sync(0xffffffffu, spec_exit, src);
+        const uint32_t x = below ? ev_exit : carry;     // the true entry level
+        const uint32_t true_exit = has_ev ? spec_exit : x;
+        if (valid && x != g) {
+            const int seg_start = seg_begin(p, s), L = seg_finish(p, s) - seg_start;
+            const int ev = has_ev ? (code & 0x3FFFFFFF) : L;   // first event (or the segment's end)
+            const uint32_t tgt = ((uint32_t)code >> 30) & 1u;   // cmd at the event
+            const int n_lv = has_ev ? ev + 1 : L;               // ticks whose level in effect is the entry level
+            const int n_cmd = ev;                               // ticks whose cmd is the entry level
+            const int32_t sg = x ? 1 : -1;
+            const int32_t dtr = has_ev ? (int32_t)(tgt != x) - (int32_t)(tgt != g) : 0;
+            uint32_t ddc = 0;   // cmd half of the digest: bits of ticks [seg_start, seg_start + n_cmd) flip g -> x
+            for (int t0 = 0; t0 < n_cmd; t0 += 32) {
+                const int r = min(32, n_cmd - t0);
+                const uint32_t mask = r >= 32 ? 0xFFFFFFFFu : ~(0xFFFFFFFFu >> r);   // ticks t0.. at bits 31..
+                const int64_t b = (seg_start + t0) >> 5;
+                ddc += (uint32_t)sg * (mask * p.dkeys[b].x);
+                if (p.words) p.words[(chain_idx(p, q, j) * p.n_blocks + b) * 2] ^= mask;
+            }
+            add_to_chain(p, q, j, (uint32_t)(sg * n_lv), 0u, (uint32_t)dtr, 0u, 0u, 0.0, digest_pack(ddc, 0u));
+            if (!has_ev) p.st_f[st_idx(p, 1, q, s, j)] = (uint8_t)x;   // no event: it ends at the true entry level
+            ++fixed;
+        }
+        const int last = min(31, p.n_seg - 1 - base);
+        carry = __shfl_sync(0xffffffffu, true_exit, last);
+    }
+    fixed = __reduce_add_sync(0xffffffffu, fixed);
+    if (lane == 0 && fixed) {
+        atomicAdd(e.fix_segments, (unsigned long long)fixed);
+        atomicMax(e.fix_rounds, 1);
+    }
+}
+
 // ------------------------------------------------------------------ one segment re-run (generic kinds)
 template <class T>
 __device__ bool rerun_segment(const ReplayParams& p, const DevPolicy& pol, int q, int s, int j, const float* trace,

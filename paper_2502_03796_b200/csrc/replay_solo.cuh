@@ -244,6 +244,40 @@ __device__ __forceinline__ void solo_stage_l(MagusState<K, false>* s, uint32_t* 
     s[3].evh = e3;
 }
 
+// One whole steady-state stage (8 ticks x 4 chains) of the open-loop observation model (A30; MAGUS_OSTAGE[S]_K<K>,
+// BAL 30 / 31): the L stage without throttling (A = D) plus the event word ewd (lock | flag per tick).
+template <int K, bool SYM>
+__device__ __forceinline__ void solo_stage_o(MagusState<K, false>* s, uint32_t* nlk, uint32_t* wcmd, uint32_t* ewd,
+                                             uint32_t& vmax, uint32_t tile, const DevPolicy& pol) {
+    uint32_t e0 = s[0].evh, e1 = s[1].evh, e2 = s[2].evh, e3 = s[3].evh;
+    const uint32_t bitc = 1u << (pol.C - 1), mone = 0xFFFFFFFFu * pol.one;
+#define OS_TAIL                                                                                                \
+    e0, e1, e2, e3, s[0].cnt, s[1].cnt, s[2].cnt, s[3].cnt, nlk[0], nlk[1], nlk[2], nlk[3], wcmd[0], wcmd[1],       \
+        wcmd[2], wcmd[3], ewd[0], ewd[1], ewd[2], ewd[3], vmax, tile, pol.dinc, pol.ddec, bitc, pol.one, mone
+#define OS_R2                                                                                                  \
+    s[0].ring.v[0], s[0].ring.v[1], s[1].ring.v[0], s[1].ring.v[1], s[2].ring.v[0], s[2].ring.v[1], s[3].ring.v[0], \
+        s[3].ring.v[1]
+#define OS_R3                                                                                                  \
+    s[0].ring.v[0], s[0].ring.v[1], s[0].ring.v[2], s[1].ring.v[0], s[1].ring.v[1], s[1].ring.v[2], s[2].ring.v[0], \
+        s[2].ring.v[1], s[2].ring.v[2], s[3].ring.v[0], s[3].ring.v[1], s[3].ring.v[2]
+    if constexpr (SYM) {
+        if constexpr (K == 1) MAGUS_OSTAGES_K1(s[0].ring.v[0], s[1].ring.v[0], s[2].ring.v[0], s[3].ring.v[0], OS_TAIL);
+        else if constexpr (K == 2) MAGUS_OSTAGES_K2(OS_R2, OS_TAIL);
+        else MAGUS_OSTAGES_K3(OS_R3, OS_TAIL);
+    } else {
+        if constexpr (K == 1) MAGUS_OSTAGE_K1(s[0].ring.v[0], s[1].ring.v[0], s[2].ring.v[0], s[3].ring.v[0], OS_TAIL);
+        else if constexpr (K == 2) MAGUS_OSTAGE_K2(OS_R2, OS_TAIL);
+        else MAGUS_OSTAGE_K3(OS_R3, OS_TAIL);
+    }
+#undef OS_R2
+#undef OS_R3
+#undef OS_TAIL
+    s[0].evh = e0;
+    s[1].evh = e1;
+    s[2].evh = e2;
+    s[3].evh = e3;
+}
+
 // The MAGUS solo replay of one (lane policy q, tile group, segment) by one warp, on a TMA ring that the caller has
 // initialised and primed with the first NSTAGE stages.  COMBO = false: the warp owns the ring and refills a slot
 // right after its own __syncwarp.  COMBO = true (magus_replay_combo_kernel): a second warp (the TDP baselines)
@@ -282,6 +316,9 @@ __device__ __forceinline__ void solo_magus_body(const CUtensorMap* tmap, const R
     float lockf[kChains], nthrf[kChains];   // counts as exact fp32 integers (segment length <= 2^24)
     uint32_t nlk[kChains];   // BAL 20: ticks not locked in the counted steady blocks (lock = lockf + 32 nsb - nlk)
     uint32_t nsb = 0;        // BAL 20: counted steady blocks
+    constexpr bool kOpen = BAL == 30 || BAL == 31;   // the open-loop stage (A30)
+    uint32_t ewd[kChains];   // open loop: event word (lock | flag per tick, the cmd word's layout)
+    int32_t fev[kChains];    // open loop: first event of the segment (ticks from its start) | its cmd << 30, -1: none
     uint32_t vmax = 0;
 #pragma unroll
     for (int c = 0; c < kChains; ++c) {
@@ -290,6 +327,8 @@ __device__ __forceinline__ void solo_magus_body(const CUtensorMap* tmap, const R
         wcmd[c] = 0;
         lockf[c] = nthrf[c] = 0.f;
         nlk[c] = 0;
+        ewd[c] = 0;
+        fev[c] = -1;
     }
 
     int i = 0;           // stage index (CTA-uniform)
@@ -303,6 +342,7 @@ __device__ __forceinline__ void solo_magus_body(const CUtensorMap* tmap, const R
                 ss[c].zero();
                 lockf[c] = nthrf[c] = 0.f;
                 nlk[c] = 0;
+                fev[c] = -1;
             }
             nsb = 0;
         }
@@ -337,7 +377,7 @@ __device__ __forceinline__ void solo_magus_body(const CUtensorMap* tmap, const R
         const bool counting = bt0 >= G.seg_start;
         if (bt0 + 32 <= G.seg_end && bt0 - G.tau_w >= warm_ticks) {
             // steady state: four whole-stage PTX blocks
-            if constexpr (BAL == 20 || BAL == 21) {   // the count biased by -s_min << (C-1); the level in the cmd word's bit 0
+            if constexpr (BAL == 20 || BAL == 21 || kOpen) {   // the count biased by -s_min << (C-1); the level in the cmd word's bit 0
 #pragma unroll
                 for (int c = 0; c < kChains; ++c) {
                     st[c].cnt -= pol.smin_sc;
@@ -363,6 +403,8 @@ __device__ __forceinline__ void solo_magus_body(const CUtensorMap* tmap, const R
                     solo_stage_pq<T::kRingK, BAL>(st, lockf, nthrf, wcmd, ss, vmax, tile + lane_off, sc, pol);
                 else if constexpr (BAL == 20 || BAL == 21)
                     solo_stage_l<T::kRingK, BAL == 21>(st, nlk, nthrf, wcmd, ss, vmax, tile + lane_off, sc, pol);
+                else if constexpr (kOpen)
+                    solo_stage_o<T::kRingK, BAL == 31>(st, nlk, wcmd, ewd, vmax, tile + lane_off, pol);
                 else T::stage8(st, tile + lane_off, pol, B_lo, Blo_d, wcmd, ss, vmax);
                 __syncwarp();   // every lane's tile reads are complete before the slot is refilled
                 solo_release<TC, COMBO>(tile, tmap, bar0, empty0, slot, phase, i + NSTAGE < G.n_stages, x,
@@ -373,7 +415,7 @@ __device__ __forceinline__ void solo_magus_body(const CUtensorMap* tmap, const R
                     phase ^= 1u;
                 }
             }
-            if constexpr (BAL == 20 || BAL == 21) {
+            if constexpr (BAL == 20 || BAL == 21 || kOpen) {
 #pragma unroll
                 for (int c = 0; c < kChains; ++c) {
                     st[c].cnt += pol.smin_sc;
@@ -389,7 +431,7 @@ __device__ __forceinline__ void solo_magus_body(const CUtensorMap* tmap, const R
                 MAGUS_CHECK(slot >= 0 && slot < NSTAGE && smem_range_ok(tile + lane_off, (TC - 1) * 512 + 16));
                 mbar_wait_loop(bar0 + 8 * slot, phase);
                 const float4* rows = reinterpret_cast<const float4*>(smem + slot * kTileBytes) + lane;
-                if (t0 + TC <= G.seg_end) {
+                if (t0 + TC <= G.seg_end && !kOpen) {
 #pragma unroll 1   // rolled: the warm-up path runs on ~2% of the stages; its code stays small
                     for (int tt = 0; tt < TC; ++tt) {
                         const int r = t0 + tt - G.tau_w;
@@ -409,6 +451,7 @@ __device__ __forceinline__ void solo_magus_body(const CUtensorMap* tmap, const R
                         for (int c = 0; c < kChains; ++c) {
                             const TickOut o = T::template tick<true>(st[c], d[c], pol, B_lo, B_hi, ready, lfull);
                             wcmd[c] = (wcmd[c] << 1) | o.cmd;
+                            if constexpr (kOpen) ewd[c] = (ewd[c] << 1) | o.ev | o.hf;   // lock | flag
                             acc_tick(ss[c], vmax, o, d[c], B_lo);
                         }
                     }
@@ -426,6 +469,16 @@ __device__ __forceinline__ void solo_magus_body(const CUtensorMap* tmap, const R
         if (counting) {
             const uint2 bkey = p.dkeys[bt0 >> 5];
             const int n = min(32, G.seg_end - bt0);
+            if constexpr (kOpen) {   // the segment's first event (tick i of the block at bit n - 1 - i)
+#pragma unroll
+                for (int c = 0; c < kChains; ++c) {
+                    const uint32_t em = n >= 32 ? ewd[c] : (ewd[c] & ((1u << n) - 1u));
+                    if (fev[c] < 0 && em != 0u) {
+                        const int h = 31 - __clz(em);
+                        fev[c] = (bt0 - G.seg_start + (n - 1 - h)) | (int32_t)(((wcmd[c] >> h) & 1u) << 30);
+                    }
+                }
+            }
             if (n == 32 && p.words == nullptr) {   // the common case: a whole block, no word dump
 #pragma unroll
                 for (int c = 0; c < kChains; ++c)
@@ -446,14 +499,17 @@ __device__ __forceinline__ void solo_magus_body(const CUtensorMap* tmap, const R
 
 #pragma unroll
     for (int c = 0; c < kChains; ++c)
-        if (j0 + c < p.n_traces) T::save(st[c], p, pol, 1, q, seg, j0 + c);
+        if (j0 + c < p.n_traces) {
+            T::save(st[c], p, pol, 1, q, seg, j0 + c);
+            if constexpr (kOpen) p.st_first[st_idx(p, 0, q, seg, j0 + c)] = fev[c];
+        }
 #pragma unroll
     for (int c = 0; c < kChains; ++c) {
         const int j = j0 + c;
         if (j >= p.n_traces) continue;
         add_to_chain(p, q, j, ss[c].nhi, ss[c].nthr + (uint32_t)nthrf[c], ss[c].trans, ss[c].ev,
-                     ss[c].lock + (uint32_t)lockf[c] + (BAL == 20 || BAL == 21 ? 32u * nsb - nlk[c] : 0u), ss[c].sexc,
-                     ss[c].digest());
+                     ss[c].lock + (uint32_t)lockf[c] + (BAL == 20 || BAL == 21 || kOpen ? 32u * nsb - nlk[c] : 0u),
+                     ss[c].sexc, ss[c].digest());
     }
     if (j0 < p.n_traces) atomicMax(p.c_vmax + chain_idx(p, q, j0), vmax);   // lane-level validation maximum
 }

@@ -501,6 +501,82 @@ def build_stage_tl(TC=8):
     return out
 
 
+def build_stage_o(K, TC=8, sym=False):
+    """MAGUS_OSTAGE[S]_K<K>: the solo kernel's steady stage for the open-loop observation model (A30, NEXT-3): the
+    observation is the recorded sample itself (A = D, never throttled), so Alg. 1's derivative, the tune flags and Alg.
+    2's lock depend on the trace only and the level is a last-writer scan of the events (lock | flag).  The L stage
+    (build_stage_l) without the throttle test, the select of A and the excess / throttle accounting, plus an event word
+    (shifted once per stage like the cmd word, bit TC-1-tt = tick tt had lock | flag) from which the kernel takes a
+    segment's first event -- the exact open-loop fix-up (post_kernels.cuh) corrects a wrong speculative entry level in
+    closed form from it, without a chain walk."""
+    C = 4
+    names = [(f"r{c}_{i}", "+d") for c in range(C) for i in range(K)] + \
+            [(f"evh{c}", "+r") for c in range(C)] + [(f"cnt{c}", "+r") for c in range(C)] + \
+            [(f"nlk{c}", "+r") for c in range(C)] + [(f"wcmd{c}", "+r") for c in range(C)] + \
+            [(f"ewd{c}", "+r") for c in range(C)] + [("vmax", "+r")]
+    inames = [("tile", "r"), ("dinc", "d"), ("ddec", "d"), ("bitc", "r"), ("one", "r"), ("mone", "r")]
+    idx = {n: f"%{i}" for i, (n, _) in enumerate(names + inames)}
+    R = idx.__getitem__
+    body = ["{", ".reg .pred phi<4>, pinc<4>, pev<4>, pk<4>, pq<4>, pe<4>;",
+            f".reg .b32 D<{TC * C}>;", f".reg .f64 dv<4>, da<4>, ad<{TC * C}>;",
+            ".reg .b32 tb<4>, tl<4>, lv<4>;"]
+    for c in range(C):
+        body.append(f"and.b32 lv{c}, {R(f'wcmd{c}')}, 1;")
+        body.append(f"setp.ne.u32 phi{c}, lv{c}, 0;")                   # level = the previous tick's cmd
+        body.append(f"shl.b32 {R(f'wcmd{c}')}, {R(f'wcmd{c}')}, {TC};")
+        body.append(f"shl.b32 {R(f'ewd{c}')}, {R(f'ewd{c}')}, {TC};")
+    for tt in range(TC):
+        body.append(f"ld.shared.v4.f32 {{D{tt * C}, D{tt * C + 1}, D{tt * C + 2}, D{tt * C + 3}}}, [{R('tile')}+{tt * 512}];")
+        per_chain = [
+            "cvt.f64.f32 {ad}, {D};",                                     # A = D (open loop, A30)
+            "sub.f64 dv{c}, {ad}, {old};",                                # Alg. 1 numerator A_t - A_{t-k} (P:207)
+        ] + ([
+            "abs.f64 da{c}, dv{c};",                                      # symmetric thresholds (d*_dec = -d*_inc):
+            "setp.gt.f64 pev{c}, da{c}, {dinc};",                         # tune flag iff |d| > d*_inc (P:213, P:243)
+            "setp.ge.and.f64 pk{c}, dv{c}, {ddec}, phi{c};",              # f_max and not -1
+            "setp.gt.or.f64 pq{c}, dv{c}, {dinc}, pk{c};",                # +1 || (f_max && !-1)
+        ] if sym else [
+            "setp.gt.f64 pinc{c}, dv{c}, {dinc};",                        # +1 (P:209)
+            "setp.lt.or.f64 pev{c}, dv{c}, {ddec}, pinc{c};",             # tune flag: +1 or -1 (P:213, P:243)
+            "not.pred pk{c}, pev{c};",
+            "and.pred pk{c}, pk{c}, phi{c};",
+            "or.pred pq{c}, pk{c}, pinc{c};",                             # +1 || (f_max && !flag)
+        ]) + [
+            "and.b32 tb{c}, {evh}, {bitc};",                              # the flag leaving the C-window (scaled)
+            "shl.b32 {evh}, {evh}, 1;",
+            "@pev{c} mad.lo.u32 {evh}, {one}, {one}, {evh};",
+            "mad.lo.u32 {cnt}, tb{c}, {mone}, {cnt};",                    # window count: - leaving + entering
+            "@pev{c} mad.lo.u32 {cnt}, {bitc}, {one}, {cnt};",
+            "setp.ge.or.s32 phi{c}, {cnt}, 0, pq{c};",                    # || lock (Alg. 2, P:230): the new level
+            "setp.ge.or.s32 pe{c}, {cnt}, 0, pev{c};",                    # event: lock || flag (the level is set)
+            "shr.u32 tl{c}, {cnt}, 31;",                                  # not locked
+            "add.u32 {nlk}, {nlk}, tl{c};",
+            "@phi{c} mad.lo.u32 {wcmd}, {one}, {bit}, {wcmd};",
+            "@pe{c} mad.lo.u32 {ewd}, {one}, {bit}, {ewd};",
+            "max.u32 {vmax}, {vmax}, {D};",                               # validation (A17)
+        ]
+        for tmpl in per_chain:
+            for c in range(C):
+                t = tt * C + c
+                old = f"ad{(tt - K) * C + c}" if tt >= K else R(f"r{c}_{K - 1 - tt}")
+                body.append(tmpl.format(c=c, D=f"D{t}", ad=f"ad{t}", old=old, dinc=R("dinc"), ddec=R("ddec"),
+                                        evh=R(f"evh{c}"), one=R("one"), bitc=R("bitc"), mone=R("mone"),
+                                        cnt=R(f"cnt{c}"), nlk=R(f"nlk{c}"), wcmd=R(f"wcmd{c}"), ewd=R(f"ewd{c}"),
+                                        vmax=R("vmax"), bit=1 << (TC - 1 - tt)))
+    for c in range(C):
+        for i in range(K):   # ring newest first: r_i = A_{t0 + TC - 1 - i}
+            body.append(f"mov.f64 {R(f'r{c}_{i}')}, ad{(TC - 1 - i) * C + c};")
+    body.append("}")
+    params = ", ".join(n for n, _ in names + inames)
+    name = f"MAGUS_OSTAGE{'S' if sym else ''}_K{K}"
+    out = [f"#define {name}(...) {name}_(__VA_ARGS__)", f"#define {name}_({params}) \\", "    asm volatile( \\"]
+    out += [f'        "{l}\\n\\t" \\' for l in body]
+    out.append("        : " + ", ".join(f'"{c}"({n})' for n, c in names) + " \\")
+    out.append("        : " + ", ".join(f'"{c}"({n})' for n, c in inames) + " \\")
+    out.append('        : "memory")')
+    return out
+
+
 def build_stage_u(K, TC=8, sym=False, popc=True, bits=False):
     """MAGUS_USTAGE{S}{I}{B}_K<K>: the solo kernel's one stage block for warm-up AND steady state (TC ticks x 4
     chains, tile loads included), with the 3-DSETP level logic (the new level is lock | +1 | (level & !-1)).
@@ -1050,6 +1126,8 @@ for K in (1, 2, 3):
     out += [""] + build_stage_l(K, sym=True)
     out += [""] + build_stage_l(K, tdp=True)
     out += [""] + build_stage_l(K, sym=True, tdp=True)
+    out += [""] + build_stage_o(K)
+    out += [""] + build_stage_o(K, sym=True)
     for sym in (False, True):
         for popc in (True, False):
             for bits in (False, True):

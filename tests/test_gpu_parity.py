@@ -773,6 +773,33 @@ def test_open_loop_mode(M, segments):
     PA.compare_totals(res.totals, rec)
 
 
+@pytest.mark.parametrize("fast", ["1", "0"])
+@pytest.mark.parametrize("case", ["cfg2", "cfg5-k2", "cfg3-k3-asym"])
+@pytest.mark.parametrize("segments", [37, 5])
+def test_open_loop_fast_fixup(M, fast, case, segments, monkeypatch):
+    """Open loop with MAGUS solo groups only: the O stage records each segment's first event and the closed-form
+    open-loop fix-up (magus_fix_openloop_kernel) corrects wrong speculative entry levels without a chain walk
+    (MAGUS_OPEN_FAST=1); with MAGUS_OPEN_FAST=0 the L stage and the chain walk.  Many short segments so that many
+    entries are wrong and many segments have no event at all (flat compute- / memory-bound traces) -- records, every
+    word, a decision dump and totals equal the oracle's open-loop replay."""
+    monkeypatch.setenv("MAGUS_OPEN_FAST", fast)
+    name, pols = dict(cfg2=("cfg2-small", CONFIGS[2]["policies"]),
+                      **{"cfg5-k2": ("cfg5-small", [pol(deriv_ticks=2), pol(kind=STATIC_MAX)]),
+                         "cfg3-k3-asym": ("cfg3-small", [pol(deriv_ticks=3, inc_threshold=0.6, dec_threshold=-1.4),
+                                                         pol(deriv_ticks=1, tune_log_capacity=20)])})[case]
+    s = SMALL[name]
+    stride = (s["n"] + 3) // 4 * 4
+    tr, w = gpu_gen(M, s["seed"], s["n"], s["ns"], s["mix"], stride)
+    res = run_gpu(M, tr, w, pols, s["n"], s["ns"], stride, segments=segments, dump=(s["n"] - 4, 4),
+                  model=M.Model(observe=1))
+    rec, codes = oracle_run(tr.cpu().numpy(), w.cpu().numpy(), pols, s["n"], model=O.Model(observe=1))
+    PA.compare_records(res.per_trace, rec, f"open-loop fast={fast} {case} S={segments}")
+    assert np.array_equal(res.words, PA.pack_words(codes))
+    assert np.array_equal(res.decisions, codes[:, s["n"] - 4:, :])
+    PA.compare_totals(res.totals, rec)
+    print(f"open loop {case} S={segments} fast={fast}: {res.n_mismatched_segments} wrong entries corrected")
+
+
 @pytest.mark.parametrize("with_times", [False, True])
 def test_counters_to_trace_and_open_loop_replay(M, with_times):
     """NEXT-3 front end: recorded byte counters (with wraps / resets, some at the start of a trace or at a
