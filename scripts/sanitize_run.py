@@ -42,7 +42,8 @@ def case(name, seed, n, ns, mix, pols, segments, flags=0, stream=False, model=No
     if flags & M.F_WALLCLOCK:
         rec, _ = PA.oracle_wallclock(tr.cpu().numpy(), w.cpu().numpy(), pols, n, O.Model())
     else:
-        rec, _, _ = O.replay_batch(tr.cpu().numpy()[:, :n], w.cpu().numpy(), PA.oracle_policies(pols))
+        om = O.Model(observe=model.observe) if model is not None else O.Model()
+        rec, _, _ = O.replay_batch(tr.cpu().numpy()[:, :n], w.cpu().numpy(), PA.oracle_policies(pols), om)
     PA.compare_records(res.per_trace, rec, name)
     print(f"{name}: ok  segments={res.n_segments} mismatched={res.n_mismatched_segments} geometry={geo}", flush=True)
 
@@ -94,6 +95,10 @@ def main():
     case("per-thread walk", 5, 200, 6000, 2, cfg5 + sweep64()[40:42], 7)
     os.environ.pop("MAGUS_WALK_SPLIT")
     os.environ.pop("MAGUS_WALK_LOCKSTEP")
+    case("open loop: O stage + closed-form fix-up", 2, 260, 6000, 0, cfg2, 9, model=M.Model(observe=1))
+    case("open loop: two MAGUS groups, asymmetric thresholds", 3, 131, 3000, 1,
+         [pol(deriv_ticks=3, inc_threshold=0.6, dec_threshold=-1.4), pol(deriv_ticks=1, tune_log_capacity=20)], 7,
+         model=M.Model(observe=1))
     case("wall-clock rounds", 5, 96, 1500, 2, cfg5, 0, flags=M.F_WALLCLOCK)
     case("nccl exchange (world 1)", 2, 130, 3000, 0, cfg2, 4, flags=M.F_NCCL, stream=True)
     # NEXT-3 counter ingest
