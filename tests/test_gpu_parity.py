@@ -263,6 +263,28 @@ def test_fused_magus_tdp_kernel(M, fuse, ctas, k, sym, segments, monkeypatch):
     PA.compare_totals(res.totals, rec)
 
 
+@pytest.mark.parametrize("ns", [8011, 97])
+@pytest.mark.parametrize("kind", ["fused", "open-fast"])
+def test_ragged_lengths_new_paths(M, ns, kind, monkeypatch):
+    """The fused MAGUS + TDP kernel and the open-loop fast path on a trace length that is not a multiple of 32 (the
+    ragged last block runs the per-tick paths: the TDP tick from the level bit of its cmd word, the event word of the
+    O stage) and on a trace shorter than the warm-up, with forced segmentation where the length allows."""
+    monkeypatch.setenv("MAGUS_FUSE", "1")
+    monkeypatch.setenv("MAGUS_OPEN_FAST", "1")
+    s = SMALL["cfg5-small"]
+    pols = [pol(), pol(kind=TDP_DEFAULT, tdp_w=217.0)] if kind == "fused" else [pol(deriv_ticks=2), pol(kind=STATIC_MAX)]
+    mk = dict(observe=1) if kind == "open-fast" else {}
+    stride = (s["n"] + 3) // 4 * 4
+    tr, w = gpu_gen(M, s["seed"], s["n"], ns, s["mix"], stride)
+    res = run_gpu(M, tr, w, pols, s["n"], ns, stride, segments=7 if ns > 2000 else 0, dump=(s["n"] - 4, 4),
+                  model=M.Model(**mk))
+    rec, codes = oracle_run(tr.cpu().numpy(), w.cpu().numpy(), pols, s["n"], model=O.Model(**mk))
+    PA.compare_records(res.per_trace, rec, f"{kind} ns={ns}")
+    assert np.array_equal(res.words, PA.pack_words(codes))
+    assert np.array_equal(res.decisions, codes[:, s["n"] - 4:, :])
+    PA.compare_totals(res.totals, rec)
+
+
 @pytest.mark.parametrize("model", ["saturating", "open-loop", "short-period"])
 def test_fused_kernel_models(M, model, monkeypatch):
     """The fused MAGUS + TDP kernel under the other observation / bandwidth models: Saturating bandwidth (B_lo from the
