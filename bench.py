@@ -267,6 +267,7 @@ def run_ours(args, cfg):
     clocks = sampler.stop()
     ms = e0.elapsed_time(e1) / args.steps
     tsum = R.timing_summary(args.steps)          # per-kernel CUDA events of the same K runs, same stream
+    plan = R.plan_info()
     res = R.results()
     ms_t = torch.tensor([ms, tsum["replay_ms"]], dtype=torch.float64, device=dev)
     if dist_on:
@@ -292,13 +293,14 @@ def run_ours(args, cfg):
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic,
                 "kernel": ("magus_wallclock_em_kernel" if args.wallclock else
+                           "magus_replay_fused_kernel" if plan["fused_magus_tdp"] else
                            "magus_replay_solo_kernel" if geo.get("solo_groups") else "magus_replay_kernel"),
                 "replay_ms": tsum["replay_ms"], "replay_ms_max_over_ranks": replay_ms_max,
                 "bytes_per_launch": bytes_per_launch, "peak_source": peak_src,
-                # the algorithmic bytes count each sample once; every replay launch group (one per chain kind,
-                # concurrent) streams the trace itself, so DRAM reads ~ launch_groups x bytes_per_launch (config 5:
-                # MAGUS + TDP = 2; MAGUS_COMBO=1 reads it once, slower -- DESIGN.md section 14)
-                "launch_groups_streaming_trace": geo.get("launch_groups")}
+                # the algorithmic bytes count each sample once; every replay launch (one per chain kind, concurrent,
+                # unless groups are combined) streams the trace itself, so DRAM reads ~ launches x bytes_per_launch
+                # (config 5: MAGUS + TDP in the fused kernel = 1 -- DESIGN.md section 7)
+                "launch_groups_streaming_trace": plan["replay_launches"]}
     if geo.get("wide_groups") and not args.wallclock:
         roofline = alu_roofline(cfg, n, ns, geo["lane_policies"], tsum["replay_ms"], replay_ms_max)
 
@@ -358,6 +360,7 @@ def run_ours(args, cfg):
             "gpu_launches": launches_per_step * args.steps,
             "kernel_ms": {"replay_ms": round(tsum["replay_ms"], 5),
                           "rest_of_step_ms": round(ms - tsum["replay_ms"], 5)},
+            "plan": plan,
             "segmentation": {"n_segments": res.n_segments, "warmup_ticks": res.warmup_ticks,
                              "mismatched_segments": res.n_mismatched_segments, "fixup_rounds": res.fixup_rounds,
                              "geometry": geo},

@@ -293,6 +293,12 @@ int32_t magus_abi_version(void);
  * many-policy sweeps, DESIGN.md section 9a -- then n_segments = 1 and there is no fix-up). */
 magus_status magus_replay_geometry(const magus_replay_t* h, int32_t out[16]);
 
+/* Diagnostics: which replay kernels the current plan launches: out = {replay launches per run (launch groups not
+ * replayed by a combined launch), fused MAGUS + TDP kernel (1/0, magus_replay_fused_kernel: one launch reads each
+ * sample once for both chain kinds), open-loop fast path (1/0: the O stage and the closed-form open-loop fix-up,
+ * DESIGN.md section 9b), unsegmented wide plan groups}.  MAGUS_ERR_INVALID_ARG for a NULL handle or out. */
+magus_status magus_replay_plan_info(const magus_replay_t* h, int32_t out[4]);
+
 /* Diagnostics (test infrastructure for the debug-check build): returns -1 when the library was
  * built without device-side bounds checks (the release build), else launches one thread that checks `violate == 0`
  * with the library's MAGUS_CHECK and returns 1 if the check trapped the kernel (the CUDA context is then unusable:

@@ -596,6 +596,21 @@ extern "C" const char* magus_set_global_error(const char* msg) {
 
 extern "C" int32_t magus_abi_version(void) { return MAGUS_ABI_VERSION; }
 
+extern "C" magus_status magus_replay_plan_info(const magus_replay_t* h, int32_t out[4]) {
+    if (!h || !out) return MAGUS_ERR_INVALID_ARG;
+    int32_t launches = 0, fused = 0, wide = 0;
+    for (const LaunchGroup& g : h->groups) {
+        launches += g.fused ? 0 : 1;
+        fused = fused || g.fused;
+        wide += g.wide ? 1 : 0;
+    }
+    out[0] = launches;
+    out[1] = fused && h->groups.front().threads == 32 ? 1 : 0;   // the one-warp fused kernel (not the 2-warp combo)
+    out[2] = h->open_fast ? 1 : 0;
+    out[3] = wide;
+    return MAGUS_OK;
+}
+
 __global__ void magus_debug_probe_kernel(int32_t violate) { MAGUS_CHECK(violate == 0); }
 
 extern "C" int32_t magus_debug_check_probe(int32_t violate) {

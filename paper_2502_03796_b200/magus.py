@@ -350,6 +350,11 @@ class Replay:
         wp = w.data_ptr() if hasattr(w, "data_ptr") else w.ctypes.data
         _check(lib.magus_replay_run_host(self._h, C.c_void_p(tp), C.c_void_p(wp), _stream_ptr(stream)), self._h)
 
+    def plan_info(self) -> dict:
+        g = (C.c_int32 * 4)()
+        _check(lib.magus_replay_plan_info(self._h, g), self._h)
+        return dict(replay_launches=g[0], fused_magus_tdp=g[1], open_loop_fast=g[2], wide_groups=g[3])
+
     def kernel_times(self):
         out = (C.c_float * 5)()
         _check(lib.magus_replay_kernel_times(self._h, out), self._h)
