@@ -1,5 +1,5 @@
 """Diagnostic (GPU box only): config 3's traces under a one-k sweep (64 points, all k = KK) -- one launch group, one
-kernel image per SM -- timed with the 256-thread wide kernel and the one-warp wide kernel (MAGUS_WIDE1=0/1).
+kernel image per SM -- timed with 16 / 8 / 4 traces per wide-kernel CTA (MAGUS_WIDE_TPC).
 usage: python scripts/wide1_probe.py KK"""
 import os
 import sys
@@ -16,8 +16,8 @@ w = torch.empty(n, dtype=torch.float32, device="cuda")
 M.gen_traces(cfg["seed"], n, ns, cfg["class_mix"], tr, w, trace_stride=n)
 pols = [M.Policy(**pol(deriv_ticks=kk, high_freq_threshold=hf, inc_threshold=th, dec_threshold=-th))
         for hf in (0.4, 0.5, 0.6, 0.7) for th in (0.25, 0.5, 0.75, 1.0, 1.5, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12)]
-for w1 in ("0", "1"):
-    os.environ["MAGUS_WIDE1"] = w1
+for w1 in ("16", "8", "4"):
+    os.environ["MAGUS_WIDE_TPC"] = w1
     R = M.Replay(n, ns, pols, M.Model(), trace_stride=n)
     for _ in range(2):
         R.run(tr, w)
@@ -29,5 +29,5 @@ for w1 in ("0", "1"):
         R.run(tr, w)
     e1.record()
     torch.cuda.synchronize()
-    print(f"k={kk} MAGUS_WIDE1={w1}: {e0.elapsed_time(e1) / 5:.3f} ms per run, geometry {R.geometry()}", flush=True)
+    print(f"k={kk} MAGUS_WIDE_TPC={w1}: {e0.elapsed_time(e1) / 5:.3f} ms per run, geometry {R.geometry()}", flush=True)
     del R
