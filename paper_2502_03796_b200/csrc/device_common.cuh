@@ -83,6 +83,7 @@ struct ReplayParams {
     uint32_t bwbits;       // bit pattern of the largest fp32 <= bw_max
     uint32_t solo_flags;   // solo replay kernel: bit 0 = speculative segments start from a synthetic full state
     int32_t solo_warm;     // warm-up ticks of the unified-stage solo kernel (multiple of 8, >= k + C - 1)
+    int32_t wide_tpcu;     // wide kernel: traces per CTA (even, <= 16; the 16-trace TMA box starts at the CTA's first)
     int64_t trace_stride;
     const DevPolicy* pol;  // [n_lane]
     const int32_t* first_low;   // [2][n_traces] first subsampled tick with D <= B_lo / D > B_lo (INT32_MAX: none)

@@ -789,6 +789,26 @@ static void choose_geometry(magus_replay_t* h, int n_sm, int forced_segments) {
         p.kr = 1;
         for (const DevPolicy& q : h->lane) p.kr = std::max(p.kr, q.k);
         p.n_blocks = (d.n_samples + 31) / 32;
+        // traces per CTA: the even count <= 16 that minimises the chains on the busiest SM,
+        // ceil(CTAs / SMs) x traces x 16, with every CTA resident at once (2 per SM); MAGUS_WIDE_TPC overrides
+        {
+            int64_t pbs_all = 0;
+            for (const LaunchGroup& g : h->groups) pbs_all += (g.nq + kWidePpc - 1) / kWidePpc;
+            int best = kWideTpc;
+            int64_t best_load = INT64_MAX;
+            for (int t = kWideTpc; t >= 8; t -= 2) {
+                if (t != kWideTpc && t > kWideTpc - 2) continue;   // a box starts at a 4-trace boundary: <= 14 fit
+                const int64_t ctas = pbs_all * ((d.n_traces + t - 1) / t);
+                if (ctas > 2 * (int64_t)n_sm && t != kWideTpc) continue;
+                const int64_t load = ((ctas + n_sm - 1) / n_sm) * t;
+                if (load < best_load) {
+                    best_load = load;
+                    best = t;
+                }
+            }
+            const int te = env_int("MAGUS_WIDE_TPC", 0);
+            p.wide_tpcu = (te >= 2 && te <= kWideTpc - 2 && te % 2 == 0) || te == kWideTpc ? te : best;
+        }
         for (LaunchGroup& g : h->groups) {
             g.wide = true;
             g.solo = false;
@@ -809,8 +829,8 @@ static void choose_geometry(magus_replay_t* h, int n_sm, int forced_segments) {
             g.ng = 1;
             g.npw = 1;
             g.n_pblocks = (g.nq + kWidePpc - 1) / kWidePpc;
-            g.n_tblocks = (d.n_traces + kWideTpc - 1) / kWideTpc;
-            g.threads = kWideThreads / nc;
+            g.n_tblocks = (d.n_traces + p.wide_tpcu - 1) / p.wide_tpcu;
+            g.threads = p.wide_tpcu * kWidePpc / nc;
             g.smem = WideSmem::kBytes;
             g.n_ctas = g.n_pblocks * g.n_tblocks;
         }

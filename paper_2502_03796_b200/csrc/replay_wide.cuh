@@ -216,12 +216,16 @@ __global__ void __launch_bounds__(kWideThreads / NC, 2)
     static_assert(LV == 0 || NC == 1, "wide kernel: the L stage runs one chain per thread");
     using T = MagusTicker<K, false>;
     constexpr uint32_t kTileBytes = WideSmem::kTileBytes;
-    constexpr int kWarps = kWideWarps / NC;
     constexpr int kPerTrace = kWidePpc / NC;   // threads per trace
+    const int kWarps = (int)(blockDim.x >> 5);   // (p.wide_tpcu traces x 16 points) / NC threads
     extern __shared__ __align__(1024) uint8_t smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int pb = blockIdx.x % p.n_pblocks;
-    const int x = (blockIdx.x / p.n_pblocks) * kWideTpc;
+    // the CTA's p.wide_tpcu traces start at x; its 16-trace TMA box at xbox = x rounded down to 4 traces (16-byte
+    // aligned rows), the CTA's traces at columns [xoff, xoff + tpcu) of it (tpcu <= 14 when xoff = 2; the other
+    // columns are read and not replayed -- the chains per SM then balance)
+    const int x = (blockIdx.x / p.n_pblocks) * p.wide_tpcu;
+    const int xbox = x & ~3, xoff = x - xbox;
     const int jl = tid / kPerTrace;
     const int j = x + jl;
     int q[NC];
@@ -249,7 +253,7 @@ __global__ void __launch_bounds__(kWideThreads / NC, 2)
         }
         __syncwarp();
         for (int i = 0; i < kWideNStage && i < n_st; ++i)
-            wide_issue(tile0 + i * kTileBytes, &tmap, full0 + 8 * i, x, i * kWideTC);
+            wide_issue(tile0 + i * kTileBytes, &tmap, full0 + 8 * i, xbox, i * kWideTC);
     }
     __syncthreads();   // the barriers are initialised before any warp waits on them
     ptx::pdl_wait();   // the pre-pass zeroes the run's flag words (launched just before)
@@ -283,7 +287,7 @@ __global__ void __launch_bounds__(kWideThreads / NC, 2)
         const int bt0 = i * kWideTC;
         const int n = min(kWideTC, N - bt0);
         mbar_wait_loop(full0 + 8 * slot, phase);
-        const float* colp = reinterpret_cast<const float*>(smem + slot * kTileBytes) + jl;   // stride 16 floats
+        const float* colp = reinterpret_cast<const float*>(smem + slot * kTileBytes) + xoff + jl;   // stride 16
         uint32_t fstart[NC], wcmd[NC];
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
@@ -295,17 +299,18 @@ __global__ void __launch_bounds__(kWideThreads / NC, 2)
             if (lane == 0) ptx::mbar_arrive_u32(empty0 + 8 * slot);
             if (warp == 0 && i + kWideNStage < n_st) {
                 ptx::mbar_wait_u32(empty0 + 8 * slot, phase);
-                wide_issue(tile0 + slot * kTileBytes, &tmap, full0 + 8 * slot, x, (i + kWideNStage) * kWideTC);
+                wide_issue(tile0 + slot * kTileBytes, &tmap, full0 + 8 * slot, xbox, (i + kWideNStage) * kWideTC);
             }
         };
         if (NC == 1 && n == kWideTC && bt0 >= warm) {
             // the warp converts its 2 traces' 32 samples to fp64 once (lane = tick) and validates them (A17), then
             // releases the fp32 slot; each thread reads its trace's values from the warp's scratch
             const float2 v = *reinterpret_cast<const float2*>(smem + slot * kTileBytes + lane * (kWideTpc * 4) +
-                                                             (tid >> 4 & ~1) * 4);
+                                                             (xoff + (tid >> 4 & ~1)) * 4);
             vmax = max(vmax, max(__float_as_uint(v.x), __float_as_uint(v.y)));
-            MAGUS_CHECK(smem_range_ok(ptx::smem_u32(wbuf), WideSmem::kWarpBufBytes) &&
-                        smem_range_ok(ptx::smem_u32(smem + slot * kTileBytes + lane * (kWideTpc * 4) + (tid >> 4 & ~1) * 4), 8));
+            MAGUS_CHECK(smem_range_ok(ptx::smem_u32(wbuf), WideSmem::kWarpBufBytes) && xoff + p.wide_tpcu <= kWideTpc &&
+                        smem_range_ok(ptx::smem_u32(smem + slot * kTileBytes + lane * (kWideTpc * 4) +
+                                                    (xoff + (tid >> 4 & ~1)) * 4), 8));
             wbuf[lane] = (double)v.x;
             wbuf[kWideTC + lane] = (double)v.y;
             uint32_t over = 0;   // LV >= 3: bit i = tick i of this thread's trace has D > B_lo

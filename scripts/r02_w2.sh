@@ -1,12 +1,12 @@
 #!/bin/bash
-# two-chain wide kernel (MAGUS_WIDE2=1, 32-trace CTAs) vs one chain per thread: wide-plan GPU tests + config 3 A/B
+# wide kernel traces per CTA: 16 vs the balanced 14 (MAGUS_WIDE_TPC): wide-plan GPU tests + config 3 A/B
 TAG=${1:-r02w2}
 OUT=gpurun_out; mkdir -p $OUT
 timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider -k "wide or full_size_every_trace or randomized" > $OUT/${TAG}_pytest.log 2>&1 <<< ""
 echo "rc=$?" >> $OUT/${TAG}_pytest.log; tail -3 $OUT/${TAG}_pytest.log; grep -E "^E  " $OUT/${TAG}_pytest.log | head -3
 for rep in 1 2; do
-  for w in 0 1; do
-    MAGUS_WIDE2=$w timeout 300 python bench.py --config 3 --no-e2e --no-cpu-baseline --steps 10 --warmup 3 --preroll-ms 300 \
+  for w in 16 14; do
+    MAGUS_WIDE_TPC=$w timeout 300 python bench.py --config 3 --no-e2e --no-cpu-baseline --steps 10 --warmup 3 --preroll-ms 300 \
         > $OUT/${TAG}_c3_w${w}_$rep.json 2>> $OUT/${TAG}.err
   done
 done
