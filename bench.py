@@ -267,6 +267,7 @@ def run_ours(args, cfg):
     clocks = sampler.stop()
     ms = e0.elapsed_time(e1) / args.steps
     tsum = R.timing_summary(args.steps)          # per-kernel CUDA events of the same K runs, same stream
+    per_run = R.run_times(args.steps)            # the replay kernel of each of those K runs (median / min)
     plan = R.plan_info()
     res = R.results()
     ms_t = torch.tensor([ms, tsum["replay_ms"]], dtype=torch.float64, device=dev)
@@ -296,6 +297,8 @@ def run_ours(args, cfg):
                            "magus_replay_fused_kernel" if plan["fused_magus_tdp"] else
                            "magus_replay_solo_kernel" if geo.get("solo_groups") else "magus_replay_kernel"),
                 "replay_ms": tsum["replay_ms"], "replay_ms_max_over_ranks": replay_ms_max,
+                "replay_ms_median": statistics.median(per_run) if per_run else None,
+                "replay_ms_min": min(per_run) if per_run else None,
                 "bytes_per_launch": bytes_per_launch, "peak_source": peak_src,
                 # the algorithmic bytes count each sample once; every replay launch (one per chain kind, concurrent,
                 # unless groups are combined) streams the trace itself, so DRAM reads ~ launches x bytes_per_launch

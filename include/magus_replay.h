@@ -293,6 +293,11 @@ int32_t magus_abi_version(void);
  * many-policy sweeps, DESIGN.md section 9a -- then n_segments = 1 and there is no fix-up). */
 magus_status magus_replay_geometry(const magus_replay_t* h, int32_t out[16]);
 
+/* Measurement: the replay kernel's CUDA-event time of each of the last n_last runs (MAGUS_F_TIMING), oldest first,
+ * into out_ms[0 .. *n_out); *n_out = min(n_last, runs so far, the timing ring's 256 slots).  Synchronises with the
+ * last run.  MAGUS_ERR_STATE without a timed run; MAGUS_ERR_INVALID_ARG for NULL pointers. */
+magus_status magus_replay_run_times(magus_replay_t* h, int32_t n_last, float* out_ms, int32_t* n_out);
+
 /* Diagnostics: which replay kernels the current plan launches: out = {replay launches per run (launch groups not
  * replayed by a combined launch), fused MAGUS + TDP kernel (1/0, magus_replay_fused_kernel: one launch reads each
  * sample once for both chain kinds), open-loop fast path (1/0: the O stage and the closed-form open-loop fix-up,

@@ -1795,6 +1795,20 @@ static magus_status timing_avg(magus_replay_t* h, int n_last, float out_ms[5]) {
     return MAGUS_OK;
 }
 
+extern "C" magus_status magus_replay_run_times(magus_replay_t* h, int32_t n_last, float* out_ms, int32_t* n_out) {
+    if (!h || !out_ms || !n_out) return fail(h, MAGUS_ERR_INVALID_ARG, "NULL argument");
+    if (!h->ran || h->tev.empty()) return fail(h, MAGUS_ERR_STATE, "no timed run (MAGUS_F_TIMING)");
+    CU(h, cudaEventSynchronize(h->ev[4]));
+    const int64_t n = std::min<int64_t>({(int64_t)std::max(1, n_last), h->n_runs, (int64_t)magus_replay::kTimingRing});
+    int32_t i = 0;
+    for (int64_t r = h->n_runs - n; r < h->n_runs; ++r, ++i) {
+        cudaEvent_t* tv = &h->tev[5 * (r % magus_replay::kTimingRing)];
+        CU(h, cudaEventElapsedTime(out_ms + i, tv[1], tv[2]));
+    }
+    *n_out = i;
+    return MAGUS_OK;
+}
+
 extern "C" magus_status magus_replay_kernel_times(magus_replay_t* h, float out_ms[5]) {
     return timing_avg(h, 1, out_ms);
 }

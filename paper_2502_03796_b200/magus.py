@@ -112,6 +112,10 @@ lib.magus_replay_kernel_times.restype = _S
 lib.magus_replay_kernel_times.argtypes = [C.c_void_p, C.POINTER(C.c_float)]
 lib.magus_replay_timing_summary.restype = _S
 lib.magus_replay_timing_summary.argtypes = [C.c_void_p, C.c_int32, C.POINTER(C.c_float)]
+lib.magus_replay_run_times.restype = _S
+lib.magus_replay_run_times.argtypes = [C.c_void_p, C.c_int32, C.POINTER(C.c_float), C.POINTER(C.c_int32)]
+lib.magus_replay_plan_info.restype = _S
+lib.magus_replay_plan_info.argtypes = [C.c_void_p, C.POINTER(C.c_int32)]
 lib.magus_replay_destroy.restype = None
 lib.magus_replay_destroy.argtypes = [C.c_void_p]
 lib.magus_counters_to_trace.restype = _S
@@ -349,6 +353,13 @@ class Replay:
         tp = trace.data_ptr() if hasattr(trace, "data_ptr") else trace.ctypes.data
         wp = w.data_ptr() if hasattr(w, "data_ptr") else w.ctypes.data
         _check(lib.magus_replay_run_host(self._h, C.c_void_p(tp), C.c_void_p(wp), _stream_ptr(stream)), self._h)
+
+    def run_times(self, n_last: int) -> list:
+        """The replay kernel's CUDA-event time (ms) of each of the last n_last runs, oldest first."""
+        buf = (C.c_float * max(1, n_last))()
+        n = C.c_int32(0)
+        _check(lib.magus_replay_run_times(self._h, n_last, buf, C.byref(n)), self._h)
+        return [buf[i] for i in range(n.value)]
 
     def plan_info(self) -> dict:
         g = (C.c_int32 * 4)()
