@@ -333,7 +333,10 @@ def _random_case(seed):
     return n, ns, int(rng.integers(0, 4)), pols, mk, segments, wide, rng
 
 
-@pytest.mark.parametrize("seed", list(range(24)))
+N_RANDOM = int(os.environ.get("MAGUS_RANDOM_SEEDS", "24"))   # more seeds for a longer sweep (evidence runs)
+
+
+@pytest.mark.parametrize("seed", list(range(N_RANDOM)))
 def test_randomized_runs_with_edge_samples(M, seed, monkeypatch):
     """Seeded random runs (_random_case) against the oracle: every record, every tick's cmd / tune-flag word and the
     totals.  Sizes, policies, models, plans (segmented / unsegmented / forced segment counts) all vary."""
@@ -354,6 +357,53 @@ def test_randomized_runs_with_edge_samples(M, seed, monkeypatch):
     res = run_gpu(M, tr, w, pols, n, ns, stride, segments=segments, model=M.Model(**mk))
     rec, codes = oracle_run(h, w.cpu().numpy(), pols, n, model=O.Model(**mk))
     label = f"seed {seed}: n={n} ns={ns} segments={segments} wide={wide} model={mk} policies={pols}"
+    PA.compare_records(res.per_trace, rec, label)
+    assert np.array_equal(res.words, PA.pack_words(codes)), label
+    PA.compare_totals(res.totals, rec)
+
+
+@pytest.mark.parametrize("seed", list(range(max(8, N_RANDOM // 2))))
+def test_randomized_round2_paths(M, seed, monkeypatch):
+    """Seeded random runs aimed at the round-2 paths, with edge samples: one MAGUS policy next to one TDP_DEFAULT
+    policy (the fused kernel), open-loop MAGUS-only runs (the O stage and the closed-form fix-up), and MAGUS sweeps
+    in the unsegmented plan (the wide P stage with balanced CTAs) -- random k <= 8, C <= 27, thresholds (symmetric
+    or not), TDP budgets, sizes and segment counts; records, every word and the totals against the oracle."""
+    rng = np.random.default_rng(1000 + seed)
+    path = ["fused", "open", "wide"][seed % 3]
+    n = int(rng.choice([37, 129, 300, 517]))
+    ns = int(rng.choice([700, 2049, 4096, 5003]))
+    def mpol(kmax):
+        th = float(rng.uniform(0.05, 4.0))
+        sym = bool(rng.integers(0, 2))
+        return pol(deriv_ticks=int(rng.integers(1, kmax + 1)), tune_log_capacity=int(rng.choice([2, 5, 10, 16, 27])),
+                   high_freq_threshold=float(rng.choice([0.3, 0.5, 0.6, 0.8])), inc_threshold=th,
+                   dec_threshold=-th if sym else -float(rng.uniform(0.05, 4.0)))
+    mk = {}
+    segments = int(rng.choice([1, 3, 9, 17]))
+    if path == "fused":
+        pols = [mpol(3), pol(kind=TDP_DEFAULT, tdp_w=float(rng.uniform(205.0, 260.0)))]
+        monkeypatch.setenv("MAGUS_FUSE", "1")
+    elif path == "open":
+        pols = [mpol(3)] + ([mpol(3)] if rng.integers(0, 2) else []) + [pol(kind=STATIC_MAX)]
+        mk = dict(observe=1)
+    else:
+        pols = [mpol(8) for _ in range(int(rng.integers(4, 20)))]
+        monkeypatch.setenv("MAGUS_WIDE", "1")
+        segments = 0
+    stride = (n + 3) // 4 * 4
+    tr, w = gpu_gen(M, 900 + seed, n, ns, int(rng.integers(0, 4)), stride)
+    h = tr.cpu().numpy()
+    B_lo = np.float32(M.derive_thresholds(M.Policy(), M.Model(**mk))["B_lo"])
+    edges = np.array([0.0, -0.0, B_lo, np.nextafter(B_lo, np.float32(0)), np.nextafter(B_lo, np.float32(30)), 20.0,
+                      np.nextafter(np.float32(20.0), np.float32(0)), np.float32(1.4e-45), 1e-30], dtype=np.float32)
+    edges = edges[edges <= np.float32(20.0)]
+    n_edge = max(1, (ns * n) // 60)
+    rows, cols = rng.integers(0, ns, n_edge), rng.integers(0, n, n_edge)
+    h[rows, cols] = edges[rng.integers(0, len(edges), n_edge)]
+    tr.copy_(torch.from_numpy(h))
+    res = run_gpu(M, tr, w, pols, n, ns, stride, segments=segments, model=M.Model(**mk))
+    rec, codes = oracle_run(h, w.cpu().numpy(), pols, n, model=O.Model(**mk))
+    label = f"seed {seed} ({path}): n={n} ns={ns} segments={segments} model={mk} policies={pols}"
     PA.compare_records(res.per_trace, rec, label)
     assert np.array_equal(res.words, PA.pack_words(codes)), label
     PA.compare_totals(res.totals, rec)
