@@ -204,12 +204,13 @@ ReplayKernel combo_kernel_for(int key, int np) {
 
 // the fused one-warp MAGUS + TDP kernel (replay_solo.cuh) for a MAGUS chain kind with an L stage block: `sym` = the
 // |d| tune-flag test (d*_dec == -d*_inc), `ctas` = resident CTAs per SM it is built for (12: 168 registers, 16: 128)
-ReplayKernel fused_kernel_for(int key, bool sym, int ctas) {
+// up = the TDP policy's f_min threshold is +inf (f_min always rises: one compare fewer per TDP tick)
+ReplayKernel fused_kernel_for(int key, bool sym, int ctas, bool up) {
+#define FUSED_KK(KK, S, C, U) (ReplayKernel)magus_replay_fused_kernel<MagusTicker<KK, false>, kTC, kNStage, S, C, U>
 #define FUSED_K(KK)                                                                                                 \
-    (ctas == 16 ? (sym ? (ReplayKernel)magus_replay_fused_kernel<MagusTicker<KK, false>, kTC, kNStage, true, 16>       \
-                       : (ReplayKernel)magus_replay_fused_kernel<MagusTicker<KK, false>, kTC, kNStage, false, 16>)     \
-                : (sym ? (ReplayKernel)magus_replay_fused_kernel<MagusTicker<KK, false>, kTC, kNStage, true, 12>       \
-                       : (ReplayKernel)magus_replay_fused_kernel<MagusTicker<KK, false>, kTC, kNStage, false, 12>))
+    (ctas == 16 ? (sym ? FUSED_KK(KK, true, 16, false) : FUSED_KK(KK, false, 16, false))                           \
+     : up       ? (sym ? FUSED_KK(KK, true, 12, true) : FUSED_KK(KK, false, 12, true))                             \
+                : (sym ? FUSED_KK(KK, true, 12, false) : FUSED_KK(KK, false, 12, false)))
     switch (key) {
         case 1: return FUSED_K(1);
         case 2: return FUSED_K(2);
@@ -217,6 +218,7 @@ ReplayKernel fused_kernel_for(int key, bool sym, int ctas) {
         default: return nullptr;
     }
 #undef FUSED_K
+#undef FUSED_KK
 }
 
 // one-warp-CTA replay kernel (replay_solo.cuh) of a chain kind, or nullptr if it has none
@@ -980,7 +982,10 @@ static void choose_geometry(magus_replay_t* h, int n_sm, int forced_segments) {
     }
     if (fuse && h->groups[0].solo && h->groups[1].solo) {
         LaunchGroup& gm = h->groups[0];
-        gm.kernel = fused_kernel_for(gm.key, h->lane[gm.q_base].ddec == -h->lane[gm.q_base].dinc, fused_ctas);
+        const DevPolicy& pt = h->lane[h->groups[1].q_base];
+        const float kB_lo = d.model.observe == 1 ? __builtin_inff() : h->B_lo;   // the kernels' throttle bound
+        const bool up = !(kB_lo >= pt.astar_lo) && env_int("MAGUS_FUSED_UP", 1) != 0;   // their a_lo is +inf
+        gm.kernel = fused_kernel_for(gm.key, h->lane[gm.q_base].ddec == -h->lane[gm.q_base].dinc, fused_ctas, up);
         gm.threads = 32;
         gm.smem = SoloSmem<kTC, kNStage>::kBytes;
         gm.n_ctas = p.n_seg * p.n_groups;

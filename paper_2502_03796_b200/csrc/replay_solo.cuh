@@ -1052,7 +1052,7 @@ __global__ void __launch_bounds__(64, kSoloCtasPerSm / 2)
 #endif
 constexpr int kFusedCtasPerSm = MAGUS_FUSED_CTAS_PER_SM;
 
-template <int K, bool SYM>
+template <int K, bool SYM, bool UP>
 __device__ __forceinline__ void fused_stage_lt(MagusState<K, false>* s, uint32_t* nlk, float* nthr, uint32_t* wcmd,
                                                SegStats* ss, uint32_t& vmax, uint32_t* wcmdT, double* excT,
                                                float* nthrT, double* sT, uint32_t tile, const SoloConst& sc,
@@ -1070,7 +1070,15 @@ __device__ __forceinline__ void fused_stage_lt(MagusState<K, false>* s, uint32_t
 #define LT_R3                                                                                                  \
     s[0].ring.v[0], s[0].ring.v[1], s[0].ring.v[2], s[1].ring.v[0], s[1].ring.v[1], s[1].ring.v[2], s[2].ring.v[0], \
         s[2].ring.v[1], s[2].ring.v[2], s[3].ring.v[0], s[3].ring.v[1], s[3].ring.v[2]
-    if constexpr (SYM) {
+    if constexpr (UP && SYM) {   // the TDP policy's f_min threshold is +inf: f_min always rises
+        if constexpr (K == 1) MAGUS_LTUSTAGES_K1(s[0].ring.v[0], s[1].ring.v[0], s[2].ring.v[0], s[3].ring.v[0], LT_TAIL);
+        else if constexpr (K == 2) MAGUS_LTUSTAGES_K2(LT_R2, LT_TAIL);
+        else MAGUS_LTUSTAGES_K3(LT_R3, LT_TAIL);
+    } else if constexpr (UP) {
+        if constexpr (K == 1) MAGUS_LTUSTAGE_K1(s[0].ring.v[0], s[1].ring.v[0], s[2].ring.v[0], s[3].ring.v[0], LT_TAIL);
+        else if constexpr (K == 2) MAGUS_LTUSTAGE_K2(LT_R2, LT_TAIL);
+        else MAGUS_LTUSTAGE_K3(LT_R3, LT_TAIL);
+    } else if constexpr (SYM) {
         if constexpr (K == 1) MAGUS_LTSTAGES_K1(s[0].ring.v[0], s[1].ring.v[0], s[2].ring.v[0], s[3].ring.v[0], LT_TAIL);
         else if constexpr (K == 2) MAGUS_LTSTAGES_K2(LT_R2, LT_TAIL);
         else MAGUS_LTSTAGES_K3(LT_R3, LT_TAIL);
@@ -1088,7 +1096,7 @@ __device__ __forceinline__ void fused_stage_lt(MagusState<K, false>* s, uint32_t
     s[3].evh = e3;
 }
 
-template <class T, int TC, int NSTAGE, bool SYM, int MINB = kFusedCtasPerSm>
+template <class T, int TC, int NSTAGE, bool SYM, int MINB = kFusedCtasPerSm, bool UP = false>
 __global__ void __launch_bounds__(32, MINB)
     magus_replay_fused_kernel(const __grid_constant__ CUtensorMap tmap, const ReplayParams p) {
     static_assert(T::kHasStage8 && TC == 8, "fused kernel: whole-stage PTX blocks of 8 ticks");
@@ -1223,7 +1231,7 @@ __global__ void __launch_bounds__(32, MINB)
                 const uint32_t tile = tile0 + slot * kTileBytes;
                 MAGUS_CHECK(slot >= 0 && slot < NSTAGE && smem_range_ok(tile + lane_off, (TC - 1) * 512 + 16));
                 mbar_wait_loop(bar0 + 8 * slot, phase);
-                fused_stage_lt<T::kRingK, SYM>(st, nlk, nthrf, wcmd, ss, vmax, wcmdT, excT, nthrT, sT, tile + lane_off,
+                fused_stage_lt<T::kRingK, SYM, UP>(st, nlk, nthrf, wcmd, ss, vmax, wcmdT, excT, nthrT, sT, tile + lane_off,
                                                sc, pol, ahi, alo);
                 __syncwarp();   // every lane's tile reads are complete before the slot is refilled
                 solo_release<TC, false>(tile, &tmap, bar0, 0u, slot, phase, i + NSTAGE < G.n_stages, x,

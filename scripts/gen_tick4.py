@@ -344,7 +344,7 @@ def build_stage_p(K, TC=8, popc=True, group=4, sym=False):
 
 
 
-def build_stage_l(K, TC=8, sym=False, tdp=False):
+def build_stage_l(K, TC=8, sym=False, tdp=False, tdp_up=False):
     """MAGUS_LSTAGE_K<K>: the solo kernel's steady-state stage with the level and the lock counter folded into
     words and signs, fewer instructions per chain-tick than MAGUS_SSTAGEF_K<K> (same decisions):
     - the cmd word is shifted once per stage (by TC) and tick tt sets bit TC-1-tt with a predicated IMAD of an
@@ -356,6 +356,8 @@ def build_stage_l(K, TC=8, sym=False, tdp=False):
       bit (nlk += cnt >> 31, unsigned), so there is no separate lock predicate or predicated lock counter.
     sym=True (MAGUS_LSTAGES_K<K>, only for d*_dec == -d*_inc): the tune flag is |d| > d*_inc and the kept-or-raised
       level +1 | (f_max & !-1) is two DSETPs ((d >= d*_dec) & level, then (d > d*_inc) | that).
+    tdp_up=True (MAGUS_LTUSTAGE[S]_K<K>): the same for a TDP policy whose f_min threshold is +inf (B_lo < a*_lo: at
+      f_min the budget is never reached, so f_min always rises), one compare fewer per TDP tick.
     tdp=True (MAGUS_LTSTAGE[S]_K<K>, the fused MAGUS + TDP kernel): the same 4 traces also step one TDP_DEFAULT chain
       each (the tick of MAGUS_TLSTAGE: level in its own cmd word, next level f_max iff D < a_hi | (f_min & D < a_lo),
       throttled demand summed by a 0/1 DFMA), sharing the tile loads, the fp64 conversion and the validation."""
@@ -420,8 +422,12 @@ def build_stage_l(K, TC=8, sym=False, tdp=False):
             "and.b32 lvT{c}, {wcmdT}, {pbit};",                           # TDP: the level (previous tick's cmd)
             "setp.ne.u32 phT{c}, lvT{c}, 0;",
             "setp.gt.and.f32 pthT{c}, {D}, {Blo}, !phT{c};",              # throttled (A14)
+        ] + ([
+            "setp.lt.or.f32 pnT{c}, {D}, {ahi}, !phT{c};",                # f_min always rises (a_lo = +inf), f_max iff A < a*_hi
+        ] if tdp_up else [
             "setp.lt.and.f32 ptT{c}, {D}, {alo}, !phT{c};",               # at f_min: A < a*_lo (A24)
             "setp.lt.or.f32 pnT{c}, {D}, {ahi}, ptT{c};",                 # next level f_max iff A < a*[f]
+        ]) + [
             "selp.b32 shiT{c}, 0x3FF00000, 0, pthT{c};",                  # 1.0 if throttled, else 0.0 (low word 0)
             "mov.b64 {sT}, {{sloT{c}, shiT{c}}};",
             "fma.rn.f64 {excT}, {sT}, dd{c}, {excT};",                    # sum of D over throttled ticks (exact)
@@ -445,7 +451,7 @@ def build_stage_l(K, TC=8, sym=False, tdp=False):
             body.append(f"mov.f64 {R(f'r{c}_{i}')}, ad{(TC - 1 - i) * C + c};")
     body.append("}")
     params = ", ".join(n for n, _ in names + inames)
-    name = f"MAGUS_L{'T' if tdp else ''}STAGE{'S' if sym else ''}_K{K}"
+    name = f"MAGUS_L{'TU' if tdp_up else 'T' if tdp else ''}STAGE{'S' if sym else ''}_K{K}"
     out = [f"#define {name}(...) {name}_(__VA_ARGS__)", f"#define {name}_({params}) \\", "    asm volatile( \\"]
     out += [f'        "{l}\\n\\t" \\' for l in body]
     out.append("        : " + ", ".join(f'"{c}"({n})' for n, c in names) + " \\")
@@ -1126,6 +1132,8 @@ for K in (1, 2, 3):
     out += [""] + build_stage_l(K, sym=True)
     out += [""] + build_stage_l(K, tdp=True)
     out += [""] + build_stage_l(K, sym=True, tdp=True)
+    out += [""] + build_stage_l(K, tdp=True, tdp_up=True)
+    out += [""] + build_stage_l(K, sym=True, tdp=True, tdp_up=True)
     out += [""] + build_stage_o(K)
     out += [""] + build_stage_o(K, sym=True)
     for sym in (False, True):
