@@ -222,9 +222,13 @@ ReplayKernel fused_kernel_for(int key, bool sym, int ctas, bool up) {
 }
 
 // one-warp-CTA replay kernel (replay_solo.cuh) of a chain kind, or nullptr if it has none
-ReplayKernel solo_kernel_for(int key, bool sym, bool bits_ok, bool lsign_ok, bool open = false) {
-    int v = env_int("MAGUS_SOLO_BAL", 20);   // stage block variant (replay_solo.cuh)
+ReplayKernel solo_kernel_for(int key, bool sym, bool bits_ok, bool lsign_ok, bool open = false,
+                             bool lbatch_ok = false) {
+    int v = env_int("MAGUS_SOLO_BAL", 24);   // stage block variant (replay_solo.cuh)
     if (open) v = sym ? 31 : 30;             // the open-loop O stage (the caller checked lsign_ok)
+    // 24: the L stage with the tune-flag log shifted once per stage (8 <= C <= 24, 8-tick stages), |d| test 25 when every
+    // lane policy has d*_dec == -d*_inc; else as 20
+    if (v == 24) v = (lsign_ok && lbatch_ok && kTC == 8) ? (sym ? 25 : 24) : 20;
     // 20: the L stage (level in the cmd word, lock = sign of the biased window count; needs C <= 27), with the
     // |d| tune-flag test (21) when every lane policy has d*_dec == -d*_inc; 22 forces the two-compare L stage
     if (v == 20 || v == 22) v = !lsign_ok ? 2 : (v == 20 && sym) ? 21 : 20;
@@ -265,6 +269,8 @@ ReplayKernel solo_kernel_for(int key, bool sym, bool bits_ok, bool lsign_ok, boo
      : v == 5 ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 5>                    \
      : v == 20 ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 20>                  \
      : v == 21 ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 21>                  \
+     : v == 24 ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 24>                  \
+     : v == 25 ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 25>                  \
      : v == 30 ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 30>                  \
      : v == 31 ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 31>                  \
               : (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 1>)
@@ -943,13 +949,16 @@ static void choose_geometry(magus_replay_t* h, int n_sm, int forced_segments) {
         // magnitude and B_lo is a normal fp32
         bool bits_ok = h->B_lo >= 0x1p-126f;
         bool lsign_ok = true;   // the L stage's biased scaled count stays within int32: C <= 27
+        bool lbatch_ok = true;  // the batched flag log: every flag leaving during a stage logged before it, the
+                                // leaving flag (bit C - 1 + 8 after the stage shift) inside the word: 8 <= C <= 24
         for (int q = g.q_base; q < g.q_base + g.nq; ++q) {
             const DevPolicy& lp = h->lane[q];
             sym = sym && lp.ddec == -lp.dinc;
             bits_ok = bits_ok && lp.dinc >= 0x1p-60 && lp.ddec <= -0x1p-60;
             lsign_ok = lsign_ok && lp.C <= 27;
+            lbatch_ok = lbatch_ok && lp.C >= 8 && lp.C <= 24;
         }
-        ReplayKernel sk = solo_kernel_for(g.key, sym, bits_ok, lsign_ok, h->open_fast);
+        ReplayKernel sk = solo_kernel_for(g.key, sym, bits_ok, lsign_ok, h->open_fast, lbatch_ok);
         g.solo = sk && g.npw == 1 && kTC == 8 && env_int("MAGUS_SOLO", 1) != 0;
         if (g.solo) {
             g.kernel = sk;

@@ -209,8 +209,10 @@ __device__ __forceinline__ void solo_stage(MagusState<K, false>* s, float* lock,
 
 // One whole steady-state stage (8 ticks x 4 chains) with the level carried in the cmd word and the lock as the sign
 // of the biased window count (MAGUS_LSTAGE_K<K>, BAL = 20).  The caller keeps s[c].cnt biased by -smin_sc and
-// wcmd[c]'s bit 0 = the level across the steady stages; nlk[c] counts the ticks not locked.
-template <int K, bool SYM>
+// wcmd[c]'s bit 0 = the level across the steady stages; nlk[c] counts the ticks not locked.  BATCH
+// (MAGUS_LB[S]STAGE_K<K>, BAL = 24 / 25, 8 <= C <= 24): the tune-flag log shifted once per stage too, the
+// count scaled by 2^8 instead of 2^(C-1) (the caller converts it around the steady block).
+template <int K, bool SYM, bool BATCH = false>
 __device__ __forceinline__ void solo_stage_l(MagusState<K, false>* s, uint32_t* nlk, float* nthr, uint32_t* wcmd,
                                              SegStats* ss, uint32_t& vmax, uint32_t tile, const SoloConst& sc,
                                              const DevPolicy& pol) {
@@ -220,13 +222,22 @@ __device__ __forceinline__ void solo_stage_l(MagusState<K, false>* s, uint32_t* 
     e0, e1, e2, e3, s[0].cnt, s[1].cnt, s[2].cnt, s[3].cnt, ss[0].sexc, ss[1].sexc, ss[2].sexc, ss[3].sexc, nlk[0],  \
         nlk[1], nlk[2], nlk[3], nthr[0], nthr[1], nthr[2], nthr[3], wcmd[0], wcmd[1], wcmd[2], wcmd[3], vmax, tile,  \
         sc.B_lo, sc.Blo_d, pol.dinc, pol.ddec, bitc, pol.one, mone
+#define LS_BTAIL LS_TAIL, (uint32_t)(pol.C - 1)
 #define LS_R2                                                                                                  \
     s[0].ring.v[0], s[0].ring.v[1], s[1].ring.v[0], s[1].ring.v[1], s[2].ring.v[0], s[2].ring.v[1], s[3].ring.v[0], \
         s[3].ring.v[1]
 #define LS_R3                                                                                                  \
     s[0].ring.v[0], s[0].ring.v[1], s[0].ring.v[2], s[1].ring.v[0], s[1].ring.v[1], s[1].ring.v[2], s[2].ring.v[0], \
         s[2].ring.v[1], s[2].ring.v[2], s[3].ring.v[0], s[3].ring.v[1], s[3].ring.v[2]
-    if constexpr (SYM) {   // d*_dec == -d*_inc: the |d| tune-flag test
+    if constexpr (BATCH && SYM) {
+        if constexpr (K == 1) MAGUS_LBSTAGES_K1(s[0].ring.v[0], s[1].ring.v[0], s[2].ring.v[0], s[3].ring.v[0], LS_BTAIL);
+        else if constexpr (K == 2) MAGUS_LBSTAGES_K2(LS_R2, LS_BTAIL);
+        else MAGUS_LBSTAGES_K3(LS_R3, LS_BTAIL);
+    } else if constexpr (BATCH) {
+        if constexpr (K == 1) MAGUS_LBSTAGE_K1(s[0].ring.v[0], s[1].ring.v[0], s[2].ring.v[0], s[3].ring.v[0], LS_BTAIL);
+        else if constexpr (K == 2) MAGUS_LBSTAGE_K2(LS_R2, LS_BTAIL);
+        else MAGUS_LBSTAGE_K3(LS_R3, LS_BTAIL);
+    } else if constexpr (SYM) {   // d*_dec == -d*_inc: the |d| tune-flag test
         if constexpr (K == 1) MAGUS_LSTAGES_K1(s[0].ring.v[0], s[1].ring.v[0], s[2].ring.v[0], s[3].ring.v[0], LS_TAIL);
         else if constexpr (K == 2) MAGUS_LSTAGES_K2(LS_R2, LS_TAIL);
         else MAGUS_LSTAGES_K3(LS_R3, LS_TAIL);
@@ -237,6 +248,7 @@ __device__ __forceinline__ void solo_stage_l(MagusState<K, false>* s, uint32_t* 
     }
 #undef LS_R2
 #undef LS_R3
+#undef LS_BTAIL
 #undef LS_TAIL
     s[0].evh = e0;
     s[1].evh = e1;
@@ -317,6 +329,7 @@ __device__ __forceinline__ void solo_magus_body(const CUtensorMap* tmap, const R
     uint32_t nlk[kChains];   // BAL 20: ticks not locked in the counted steady blocks (lock = lockf + 32 nsb - nlk)
     uint32_t nsb = 0;        // BAL 20: counted steady blocks
     constexpr bool kOpen = BAL == 30 || BAL == 31;   // the open-loop stage (A30)
+    constexpr bool kL = BAL == 20 || BAL == 21 || BAL == 24 || BAL == 25;   // the L stage (24/25: batched flag log)
     uint32_t ewd[kChains];   // open loop: event word (lock | flag per tick, the cmd word's layout)
     int32_t fev[kChains];    // open loop: first event of the segment (ticks from its start) | its cmd << 30, -1: none
     uint32_t vmax = 0;
@@ -377,10 +390,12 @@ __device__ __forceinline__ void solo_magus_body(const CUtensorMap* tmap, const R
         const bool counting = bt0 >= G.seg_start;
         if (bt0 + 32 <= G.seg_end && bt0 - G.tau_w >= warm_ticks) {
             // steady state: four whole-stage PTX blocks
-            if constexpr (BAL == 20 || BAL == 21 || kOpen) {   // the count biased by -s_min << (C-1); the level in the cmd word's bit 0
+            if constexpr (kL || kOpen) {   // the count biased by -s_min << (C-1); the level in the cmd word's bit 0
 #pragma unroll
                 for (int c = 0; c < kChains; ++c) {
                     st[c].cnt -= pol.smin_sc;
+                    if constexpr (BAL >= 24 && BAL < 30)   // the batched log's count scale 2^TC (exact: C - 1 >= TC - 1)
+                        st[c].cnt = (uint32_t)((int32_t)st[c].cnt >> (pol.C - 1)) << TC;
                     wcmd[c] = T::level(st[c]);
                 }
                 if (counting) ++nsb;
@@ -401,8 +416,9 @@ __device__ __forceinline__ void solo_magus_body(const CUtensorMap* tmap, const R
                     solo_stage<T::kRingK, true, true>(st, lockf, nthrf, wcmd, ss, vmax, tile + lane_off, sc, pol);
                 else if constexpr (BAL == 3 || BAL == 4 || (BAL >= 9 && BAL < 20))
                     solo_stage_pq<T::kRingK, BAL>(st, lockf, nthrf, wcmd, ss, vmax, tile + lane_off, sc, pol);
-                else if constexpr (BAL == 20 || BAL == 21)
-                    solo_stage_l<T::kRingK, BAL == 21>(st, nlk, nthrf, wcmd, ss, vmax, tile + lane_off, sc, pol);
+                else if constexpr (kL)
+                    solo_stage_l<T::kRingK, BAL == 21 || BAL == 25, (BAL >= 24)>(st, nlk, nthrf, wcmd, ss, vmax,
+                                                                               tile + lane_off, sc, pol);
                 else if constexpr (kOpen)
                     solo_stage_o<T::kRingK, BAL == 31>(st, nlk, wcmd, ewd, vmax, tile + lane_off, pol);
                 else T::stage8(st, tile + lane_off, pol, B_lo, Blo_d, wcmd, ss, vmax);
@@ -415,9 +431,10 @@ __device__ __forceinline__ void solo_magus_body(const CUtensorMap* tmap, const R
                     phase ^= 1u;
                 }
             }
-            if constexpr (BAL == 20 || BAL == 21 || kOpen) {
+            if constexpr (kL || kOpen) {
 #pragma unroll
                 for (int c = 0; c < kChains; ++c) {
+                    if constexpr (BAL >= 24 && BAL < 30) st[c].cnt = (uint32_t)((int32_t)st[c].cnt >> TC) << (pol.C - 1);
                     st[c].cnt += pol.smin_sc;
                     T::set_level(st[c], wcmd[c] & 1u);
                 }
@@ -508,7 +525,7 @@ __device__ __forceinline__ void solo_magus_body(const CUtensorMap* tmap, const R
         const int j = j0 + c;
         if (j >= p.n_traces) continue;
         add_to_chain(p, q, j, ss[c].nhi, ss[c].nthr + (uint32_t)nthrf[c], ss[c].trans, ss[c].ev,
-                     ss[c].lock + (uint32_t)lockf[c] + (BAL == 20 || BAL == 21 || kOpen ? 32u * nsb - nlk[c] : 0u),
+                     ss[c].lock + (uint32_t)lockf[c] + (kL || kOpen ? 32u * nsb - nlk[c] : 0u),
                      ss[c].sexc, ss[c].digest());
     }
     if (j0 < p.n_traces) atomicMax(p.c_vmax + chain_idx(p, q, j0), vmax);   // lane-level validation maximum

@@ -344,7 +344,7 @@ def build_stage_p(K, TC=8, popc=True, group=4, sym=False):
 
 
 
-def build_stage_l(K, TC=8, sym=False, tdp=False, tdp_up=False):
+def build_stage_l(K, TC=8, sym=False, tdp=False, tdp_up=False, batch=False):
     """MAGUS_LSTAGE_K<K>: the solo kernel's steady-state stage with the level and the lock counter folded into
     words and signs, fewer instructions per chain-tick than MAGUS_SSTAGEF_K<K> (same decisions):
     - the cmd word is shifted once per stage (by TC) and tick tt sets bit TC-1-tt with a predicated IMAD of an
@@ -360,7 +360,14 @@ def build_stage_l(K, TC=8, sym=False, tdp=False, tdp_up=False):
       f_min the budget is never reached, so f_min always rises), one compare fewer per TDP tick.
     tdp=True (MAGUS_LTSTAGE[S]_K<K>, the fused MAGUS + TDP kernel): the same 4 traces also step one TDP_DEFAULT chain
       each (the tick of MAGUS_TLSTAGE: level in its own cmd word, next level f_max iff D < a_hi | (f_min & D < a_lo),
-      throttled demand summed by a 0/1 DFMA), sharing the tile loads, the fp64 conversion and the validation."""
+      throttled demand summed by a 0/1 DFMA), sharing the tile loads, the fp64 conversion and the validation.
+    batch=True (MAGUS_LB[T[U]]STAGE[S]_K<K>): the tune-flag log is also shifted once per stage (by TC) and tick tt
+      sets its bit TC-1-tt, like the cmd word, so the per-tick shift goes.  With C >= TC every flag leaving the
+      window during the stage was logged before it: after the stage-start shift the one leaving at tick tt (bit C-1
+      before a per-tick shift) is bit C-1+TC-tt, i.e. bit TC-tt of ev2 = log >> (C-1) (one shift per stage, cm1 =
+      C-1 an input), tested with an immediate mask.  The count is scaled by 2^TC instead of 2^(C-1) (the caller
+      converts it), so the leaving flag is (ev2 & 2^(TC-tt)) * -2^tt and an entering one +2^TC: immediates only.
+      Needs TC <= C <= 32-TC."""
     C = 4
     names = [(f"r{c}_{i}", "+d") for c in range(C) for i in range(K)] + \
             [(f"evh{c}", "+r") for c in range(C)] + [(f"cnt{c}", "+r") for c in range(C)] + \
@@ -370,18 +377,22 @@ def build_stage_l(K, TC=8, sym=False, tdp=False, tdp_up=False):
         names += [(f"wcmdT{c}", "+r") for c in range(C)] + [(f"excT{c}", "+d") for c in range(C)] + \
                  [(f"nthrT{c}", "+f") for c in range(C)] + [(f"sT{c}", "+d") for c in range(C)]
     inames = [("tile", "r"), ("Blo", "f"), ("Blod", "d"), ("dinc", "d"), ("ddec", "d"), ("bitc", "r"),
-              ("one", "r"), ("mone", "r")] + ([("ahi", "f"), ("alo", "f")] if tdp else [])
+              ("one", "r"), ("mone", "r")] + ([("ahi", "f"), ("alo", "f")] if tdp else []) + \
+             ([("cm1", "r")] if batch else [])
     idx = {n: f"%{i}" for i, (n, _) in enumerate(names + inames)}
     R = idx.__getitem__
     body = ["{", ".reg .pred phi<4>, pthr<4>, pinc<4>, pev<4>, pk<4>, pq<4>;",
             f".reg .b32 D<{TC * C}>;", f".reg .f64 dd<4>, dv<4>, da<4>, dx<4>, ad<{TC * C}>;",
-            ".reg .b32 tb<4>, tl<4>, lv<4>;"]
+            ".reg .b32 tb<4>, tl<4>, lv<4>, eo<4>;"]
     if tdp:
         body += [".reg .pred phT<4>, pthT<4>, ptT<4>, pnT<4>;", ".reg .b32 sloT<4>, shiT<4>, lvT<4>;"]
     for c in range(C):
         body.append(f"and.b32 lv{c}, {R(f'wcmd{c}')}, 1;")
         body.append(f"setp.ne.u32 phi{c}, lv{c}, 0;")                   # level = the previous tick's cmd
         body.append(f"shl.b32 {R(f'wcmd{c}')}, {R(f'wcmd{c}')}, {TC};")
+        if batch:
+            body.append(f"shl.b32 {R(f'evh{c}')}, {R(f'evh{c}')}, {TC};")
+            body.append(f"shr.u32 eo{c}, {R(f'evh{c}')}, {R('cm1')};")
         if tdp:   # the TDP level is re-read from its cmd word every tick (bit TC - tt: the previous tick's cmd), so
                   # no TDP predicate lives across ticks (8 level predicates would exceed the 7 predicate registers)
             body.append(f"shl.b32 {R(f'wcmdT{c}')}, {R(f'wcmdT{c}')}, {TC};")
@@ -405,11 +416,17 @@ def build_stage_l(K, TC=8, sym=False, tdp=False, tdp_up=False):
             "and.pred pk{c}, pk{c}, phi{c};",
             "or.pred pq{c}, pk{c}, pinc{c};",                             # +1 || (f_max && !flag)
         ]) + [
+        ] + ([
+            "and.b32 tb{c}, eo{c}, {bmt};",                              # the flag leaving the C-window (<< TC-tt)
+            "@pev{c} mad.lo.u32 {evh}, {one}, {bit}, {evh};",            # the tune-flag log, bit TC-1-tt
+            "mad.lo.u32 {cnt}, tb{c}, {nk}, {cnt};",                      # window count: - leaving (x 2^tt)
+        ] if batch else [
             "and.b32 tb{c}, {evh}, {bitc};",                              # the flag leaving the C-window (scaled)
             "shl.b32 {evh}, {evh}, 1;",
             "@pev{c} mad.lo.u32 {evh}, {one}, {one}, {evh};",
             "mad.lo.u32 {cnt}, tb{c}, {mone}, {cnt};",                    # window count: - leaving + entering
-            "@pev{c} mad.lo.u32 {cnt}, {bitc}, {one}, {cnt};",
+        ]) + [
+            "@pev{c} mad.lo.u32 {cnt}, {one}, {bitin}, {cnt};",           # + entering
             "setp.ge.or.s32 phi{c}, {cnt}, 0, pq{c};",                    # || lock (Alg. 2): the new level
             "shr.u32 tl{c}, {cnt}, 31;",                                  # not locked
             "add.u32 {nlk}, {nlk}, tl{c};",
@@ -443,6 +460,7 @@ def build_stage_l(K, TC=8, sym=False, tdp=False, tdp_up=False):
                                         bitc=R("bitc"), mone=R("mone"), cnt=R(f"cnt{c}"), nlk=R(f"nlk{c}"),
                                         wcmd=R(f"wcmd{c}"), exc=R(f"exc{c}"), nthr=R(f"nthr{c}"), vmax=R("vmax"),
                                         bit=1 << (TC - 1 - tt), pbit=1 << (TC - tt),
+                                        bmt=1 << (TC - tt), nk=-(1 << tt), bitin=(1 << TC) if batch else R("bitc"),
                                         **({"ahi": R("ahi"), "alo": R("alo"), "sT": R(f"sT{c}"),
                                             "excT": R(f"excT{c}"), "nthrT": R(f"nthrT{c}"),
                                             "wcmdT": R(f"wcmdT{c}")} if tdp else {})))
@@ -451,7 +469,7 @@ def build_stage_l(K, TC=8, sym=False, tdp=False, tdp_up=False):
             body.append(f"mov.f64 {R(f'r{c}_{i}')}, ad{(TC - 1 - i) * C + c};")
     body.append("}")
     params = ", ".join(n for n, _ in names + inames)
-    name = f"MAGUS_L{'TU' if tdp_up else 'T' if tdp else ''}STAGE{'S' if sym else ''}_K{K}"
+    name = f"MAGUS_L{'B' if batch else ''}{'TU' if tdp_up else 'T' if tdp else ''}STAGE{'S' if sym else ''}_K{K}"
     out = [f"#define {name}(...) {name}_(__VA_ARGS__)", f"#define {name}_({params}) \\", "    asm volatile( \\"]
     out += [f'        "{l}\\n\\t" \\' for l in body]
     out.append("        : " + ", ".join(f'"{c}"({n})' for n, c in names) + " \\")
@@ -1134,6 +1152,8 @@ for K in (1, 2, 3):
     out += [""] + build_stage_l(K, sym=True, tdp=True)
     out += [""] + build_stage_l(K, tdp=True, tdp_up=True)
     out += [""] + build_stage_l(K, sym=True, tdp=True, tdp_up=True)
+    out += [""] + build_stage_l(K, batch=True)
+    out += [""] + build_stage_l(K, sym=True, batch=True)
     out += [""] + build_stage_o(K)
     out += [""] + build_stage_o(K, sym=True)
     for sym in (False, True):
