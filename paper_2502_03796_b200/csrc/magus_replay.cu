@@ -205,12 +205,15 @@ ReplayKernel combo_kernel_for(int key, int np) {
 // the fused one-warp MAGUS + TDP kernel (replay_solo.cuh) for a MAGUS chain kind with an L stage block: `sym` = the
 // |d| tune-flag test (d*_dec == -d*_inc), `ctas` = resident CTAs per SM it is built for (12: 168 registers, 16: 128)
 // up = the TDP policy's f_min threshold is +inf (f_min always rises: one compare fewer per TDP tick)
-ReplayKernel fused_kernel_for(int key, bool sym, int ctas, bool up) {
-#define FUSED_KK(KK, S, C, U) (ReplayKernel)magus_replay_fused_kernel<MagusTicker<KK, false>, kTC, kNStage, S, C, U>
+ReplayKernel fused_kernel_for(int key, bool sym, int ctas, bool up, bool lb) {
+#define FUSED_KK(KK, S, C, U, L) (ReplayKernel)magus_replay_fused_kernel<MagusTicker<KK, false>, kTC, kNStage, S, C, U, L>
+#define FUSED_K12(KK, L)                                                                                            \
+    (up ? (sym ? FUSED_KK(KK, true, 12, true, L) : FUSED_KK(KK, false, 12, true, L))                               \
+        : (sym ? FUSED_KK(KK, true, 12, false, L) : FUSED_KK(KK, false, 12, false, L)))
 #define FUSED_K(KK)                                                                                                 \
-    (ctas == 16 ? (sym ? FUSED_KK(KK, true, 16, false) : FUSED_KK(KK, false, 16, false))                           \
-     : up       ? (sym ? FUSED_KK(KK, true, 12, true) : FUSED_KK(KK, false, 12, true))                             \
-                : (sym ? FUSED_KK(KK, true, 12, false) : FUSED_KK(KK, false, 12, false)))
+    (ctas == 16 ? (sym ? FUSED_KK(KK, true, 16, false, false) : FUSED_KK(KK, false, 16, false, false))             \
+     : lb       ? FUSED_K12(KK, true)                                                                               \
+                : FUSED_K12(KK, false))
     switch (key) {
         case 1: return FUSED_K(1);
         case 2: return FUSED_K(2);
@@ -218,6 +221,7 @@ ReplayKernel fused_kernel_for(int key, bool sym, int ctas, bool up) {
         default: return nullptr;
     }
 #undef FUSED_K
+#undef FUSED_K12
 #undef FUSED_KK
 }
 
@@ -859,7 +863,8 @@ static void choose_geometry(magus_replay_t* h, int n_sm, int forced_segments) {
                       h->groups[0].nq == 1 && h->lane[h->groups[0].q_base].C <= 27 &&
                       h->groups[1].key == 1000 + LANE_TDP && h->groups[1].nq == 1 && kTC == 8 &&
                       env_int("MAGUS_FUSE", 1) != 0 && env_int("MAGUS_SOLO", 1) != 0 &&
-                      env_int("MAGUS_SOLO_BAL", 20) == 20 && env_int("MAGUS_TDP_SOLO", 2) != 0;
+                      (env_int("MAGUS_SOLO_BAL", 24) == 24 || env_int("MAGUS_SOLO_BAL", 24) == 20) &&
+                      env_int("MAGUS_TDP_SOLO", 2) != 0;
     const int fused_ctas = env_int("MAGUS_FUSED_CTAS", 12) == 16 ? 16 : 12;   // per SM (the kernel's launch bound)
     int W = d.tuning_warmup > 0 ? d.tuning_warmup
                                 : ((kmax + cmax - 1 + 31) / 32) * 32 + env_int("MAGUS_WARMUP_EXTRA", 0) + h->warm_extra;
@@ -994,7 +999,10 @@ static void choose_geometry(magus_replay_t* h, int n_sm, int forced_segments) {
         const DevPolicy& pt = h->lane[h->groups[1].q_base];
         const float kB_lo = d.model.observe == 1 ? __builtin_inff() : h->B_lo;   // the kernels' throttle bound
         const bool up = !(kB_lo >= pt.astar_lo) && env_int("MAGUS_FUSED_UP", 1) != 0;   // their a_lo is +inf
-        gm.kernel = fused_kernel_for(gm.key, h->lane[gm.q_base].ddec == -h->lane[gm.q_base].dinc, fused_ctas, up);
+        // the batched tune-flag log (solo BAL 24 / 25) when 8 <= C <= 24 and MAGUS_SOLO_BAL keeps its default
+        const int mc = h->lane[gm.q_base].C;
+        const bool lb = mc >= 8 && mc <= 24 && env_int("MAGUS_SOLO_BAL", 24) == 24;
+        gm.kernel = fused_kernel_for(gm.key, h->lane[gm.q_base].ddec == -h->lane[gm.q_base].dinc, fused_ctas, up, lb);
         gm.threads = 32;
         gm.smem = SoloSmem<kTC, kNStage>::kBytes;
         gm.n_ctas = p.n_seg * p.n_groups;

@@ -1069,7 +1069,7 @@ __global__ void __launch_bounds__(64, kSoloCtasPerSm / 2)
 #endif
 constexpr int kFusedCtasPerSm = MAGUS_FUSED_CTAS_PER_SM;
 
-template <int K, bool SYM, bool UP>
+template <int K, bool SYM, bool UP, bool LB>
 __device__ __forceinline__ void fused_stage_lt(MagusState<K, false>* s, uint32_t* nlk, float* nthr, uint32_t* wcmd,
                                                SegStats* ss, uint32_t& vmax, uint32_t* wcmdT, double* excT,
                                                float* nthrT, double* sT, uint32_t tile, const SoloConst& sc,
@@ -1081,13 +1081,30 @@ __device__ __forceinline__ void fused_stage_lt(MagusState<K, false>* s, uint32_t
         nlk[1], nlk[2], nlk[3], nthr[0], nthr[1], nthr[2], nthr[3], wcmd[0], wcmd[1], wcmd[2], wcmd[3], vmax,        \
         wcmdT[0], wcmdT[1], wcmdT[2], wcmdT[3], excT[0], excT[1], excT[2], excT[3], nthrT[0], nthrT[1], nthrT[2],     \
         nthrT[3], sT[0], sT[1], sT[2], sT[3], tile, sc.B_lo, sc.Blo_d, pol.dinc, pol.ddec, bitc, pol.one, mone, ahi, alo
+#define LT_BTAIL LT_TAIL, (uint32_t)(pol.C - 1)
 #define LT_R2                                                                                                  \
     s[0].ring.v[0], s[0].ring.v[1], s[1].ring.v[0], s[1].ring.v[1], s[2].ring.v[0], s[2].ring.v[1], s[3].ring.v[0], \
         s[3].ring.v[1]
 #define LT_R3                                                                                                  \
     s[0].ring.v[0], s[0].ring.v[1], s[0].ring.v[2], s[1].ring.v[0], s[1].ring.v[1], s[1].ring.v[2], s[2].ring.v[0], \
         s[2].ring.v[1], s[2].ring.v[2], s[3].ring.v[0], s[3].ring.v[1], s[3].ring.v[2]
-    if constexpr (UP && SYM) {   // the TDP policy's f_min threshold is +inf: f_min always rises
+    if constexpr (LB && UP && SYM) {   // LB: the batched tune-flag log (solo_stage_l's BATCH)
+        if constexpr (K == 1) MAGUS_LBTUSTAGES_K1(s[0].ring.v[0], s[1].ring.v[0], s[2].ring.v[0], s[3].ring.v[0], LT_BTAIL);
+        else if constexpr (K == 2) MAGUS_LBTUSTAGES_K2(LT_R2, LT_BTAIL);
+        else MAGUS_LBTUSTAGES_K3(LT_R3, LT_BTAIL);
+    } else if constexpr (LB && UP) {
+        if constexpr (K == 1) MAGUS_LBTUSTAGE_K1(s[0].ring.v[0], s[1].ring.v[0], s[2].ring.v[0], s[3].ring.v[0], LT_BTAIL);
+        else if constexpr (K == 2) MAGUS_LBTUSTAGE_K2(LT_R2, LT_BTAIL);
+        else MAGUS_LBTUSTAGE_K3(LT_R3, LT_BTAIL);
+    } else if constexpr (LB && SYM) {
+        if constexpr (K == 1) MAGUS_LBTSTAGES_K1(s[0].ring.v[0], s[1].ring.v[0], s[2].ring.v[0], s[3].ring.v[0], LT_BTAIL);
+        else if constexpr (K == 2) MAGUS_LBTSTAGES_K2(LT_R2, LT_BTAIL);
+        else MAGUS_LBTSTAGES_K3(LT_R3, LT_BTAIL);
+    } else if constexpr (LB) {
+        if constexpr (K == 1) MAGUS_LBTSTAGE_K1(s[0].ring.v[0], s[1].ring.v[0], s[2].ring.v[0], s[3].ring.v[0], LT_BTAIL);
+        else if constexpr (K == 2) MAGUS_LBTSTAGE_K2(LT_R2, LT_BTAIL);
+        else MAGUS_LBTSTAGE_K3(LT_R3, LT_BTAIL);
+    } else if constexpr (UP && SYM) {   // the TDP policy's f_min threshold is +inf: f_min always rises
         if constexpr (K == 1) MAGUS_LTUSTAGES_K1(s[0].ring.v[0], s[1].ring.v[0], s[2].ring.v[0], s[3].ring.v[0], LT_TAIL);
         else if constexpr (K == 2) MAGUS_LTUSTAGES_K2(LT_R2, LT_TAIL);
         else MAGUS_LTUSTAGES_K3(LT_R3, LT_TAIL);
@@ -1106,6 +1123,7 @@ __device__ __forceinline__ void fused_stage_lt(MagusState<K, false>* s, uint32_t
     }
 #undef LT_R2
 #undef LT_R3
+#undef LT_BTAIL
 #undef LT_TAIL
     s[0].evh = e0;
     s[1].evh = e1;
@@ -1113,7 +1131,7 @@ __device__ __forceinline__ void fused_stage_lt(MagusState<K, false>* s, uint32_t
     s[3].evh = e3;
 }
 
-template <class T, int TC, int NSTAGE, bool SYM, int MINB = kFusedCtasPerSm, bool UP = false>
+template <class T, int TC, int NSTAGE, bool SYM, int MINB = kFusedCtasPerSm, bool UP = false, bool LB = false>
 __global__ void __launch_bounds__(32, MINB)
     magus_replay_fused_kernel(const __grid_constant__ CUtensorMap tmap, const ReplayParams p) {
     static_assert(T::kHasStage8 && TC == 8, "fused kernel: whole-stage PTX blocks of 8 ticks");
@@ -1240,6 +1258,7 @@ __global__ void __launch_bounds__(32, MINB)
 #pragma unroll
             for (int c = 0; c < kChains; ++c) {
                 st[c].cnt -= pol.smin_sc;
+                if constexpr (LB) st[c].cnt = (uint32_t)((int32_t)st[c].cnt >> (pol.C - 1)) << TC;   // 2^TC scale
                 wcmd[c] = fstart[c];
             }
             if (counting) ++nsb;
@@ -1248,7 +1267,7 @@ __global__ void __launch_bounds__(32, MINB)
                 const uint32_t tile = tile0 + slot * kTileBytes;
                 MAGUS_CHECK(slot >= 0 && slot < NSTAGE && smem_range_ok(tile + lane_off, (TC - 1) * 512 + 16));
                 mbar_wait_loop(bar0 + 8 * slot, phase);
-                fused_stage_lt<T::kRingK, SYM, UP>(st, nlk, nthrf, wcmd, ss, vmax, wcmdT, excT, nthrT, sT, tile + lane_off,
+                fused_stage_lt<T::kRingK, SYM, UP, LB>(st, nlk, nthrf, wcmd, ss, vmax, wcmdT, excT, nthrT, sT, tile + lane_off,
                                                sc, pol, ahi, alo);
                 __syncwarp();   // every lane's tile reads are complete before the slot is refilled
                 solo_release<TC, false>(tile, &tmap, bar0, 0u, slot, phase, i + NSTAGE < G.n_stages, x,
@@ -1261,6 +1280,7 @@ __global__ void __launch_bounds__(32, MINB)
             }
 #pragma unroll
             for (int c = 0; c < kChains; ++c) {
+                if constexpr (LB) st[c].cnt = (uint32_t)((int32_t)st[c].cnt >> TC) << (pol.C - 1);
                 st[c].cnt += pol.smin_sc;
                 T::set_level(st[c], wcmd[c] & 1u);
             }

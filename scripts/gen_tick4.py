@@ -1154,6 +1154,10 @@ for K in (1, 2, 3):
     out += [""] + build_stage_l(K, sym=True, tdp=True, tdp_up=True)
     out += [""] + build_stage_l(K, batch=True)
     out += [""] + build_stage_l(K, sym=True, batch=True)
+    out += [""] + build_stage_l(K, tdp=True, batch=True)
+    out += [""] + build_stage_l(K, sym=True, tdp=True, batch=True)
+    out += [""] + build_stage_l(K, tdp=True, tdp_up=True, batch=True)
+    out += [""] + build_stage_l(K, sym=True, tdp=True, tdp_up=True, batch=True)
     out += [""] + build_stage_o(K)
     out += [""] + build_stage_o(K, sym=True)
     for sym in (False, True):

@@ -250,16 +250,18 @@ def test_combo_kernel_reads_each_tile_once(M, combo, n_tdp, monkeypatch):
     PA.compare_totals(res.totals, rec)
 
 
-@pytest.mark.parametrize("fuse,ctas", [("1", "12"), ("1", "16"), ("0", "12")])
+@pytest.mark.parametrize("fuse,ctas,bal", [("1", "12", "24"), ("1", "12", "20"), ("1", "16", "24"), ("0", "12", "24")])
 @pytest.mark.parametrize("k", [1, 3])
 @pytest.mark.parametrize("sym", [True, False])
 @pytest.mark.parametrize("segments", [9, 1])
-def test_fused_magus_tdp_kernel(M, fuse, ctas, k, sym, segments, monkeypatch):
+def test_fused_magus_tdp_kernel(M, fuse, ctas, bal, k, sym, segments, monkeypatch):
     """One MAGUS policy next to one replayed TDP_DEFAULT baseline (config 5's replayed pair) runs as ONE warp per (tile
     group, segment) stepping both chain kinds over the same samples (magus_replay_fused_kernel, MAGUS_FUSE=1, built
     for 12 or 16 CTAs per SM) -- one replay launch instead of two; with MAGUS_FUSE=0 as two launches.  Both equal the
     oracle (records, every word, a decision dump, totals), with k in {1, 3}, symmetric (the |d| test) and asymmetric
-    thresholds, and forced segmentation (speculative entries, fix-up walks after the fused replay) or none."""
+    thresholds, and forced segmentation (speculative entries, fix-up walks after the fused replay) or none; bal 24 =
+    the batched tune-flag log (C = 10), 20 = the per-tick shift."""
+    monkeypatch.setenv("MAGUS_SOLO_BAL", bal)
     monkeypatch.setenv("MAGUS_FUSE", fuse)
     monkeypatch.setenv("MAGUS_FUSED_CTAS", ctas)
     s = SMALL["cfg5-small"]
@@ -275,7 +277,7 @@ def test_fused_magus_tdp_kernel(M, fuse, ctas, k, sym, segments, monkeypatch):
         unfused = R2.geometry()
     assert geo["kernels_per_run"] == unfused["kernels_per_run"] - (1 if fuse == "1" else 0), (geo, unfused)
     rec, codes = oracle_run(tr.cpu().numpy(), w.cpu().numpy(), pols, s["n"])
-    PA.compare_records(res.per_trace, rec, f"fuse={fuse} ctas={ctas} k={k} sym={sym} S={segments}")
+    PA.compare_records(res.per_trace, rec, f"fuse={fuse} ctas={ctas} bal={bal} k={k} sym={sym} S={segments}")
     assert np.array_equal(res.words, PA.pack_words(codes))
     assert np.array_equal(res.decisions, codes[:, s["n"] - 4:, :])
     PA.compare_totals(res.totals, rec)
