@@ -229,7 +229,8 @@ ReplayKernel fused_kernel_for(int key, bool sym, int ctas, bool up, bool lb) {
 ReplayKernel solo_kernel_for(int key, bool sym, bool bits_ok, bool lsign_ok, bool open = false,
                              bool lbatch_ok = false) {
     int v = env_int("MAGUS_SOLO_BAL", 24);   // stage block variant (replay_solo.cuh)
-    if (open) v = sym ? 31 : 30;             // the open-loop O stage (the caller checked lsign_ok)
+    // the open-loop O stage (the caller checked lsign_ok); 34 / 35 with the batched tune-flag log (8 <= C <= 24)
+    if (open) v = (lbatch_ok && kTC == 8 && env_int("MAGUS_SOLO_BAL", 24) == 24 ? 34 : 30) + (sym ? 1 : 0);
     // 24: the L stage with the tune-flag log shifted once per stage (8 <= C <= 24, 8-tick stages), |d| test 25 when every
     // lane policy has d*_dec == -d*_inc; else as 20
     if (v == 24) v = (lsign_ok && lbatch_ok && kTC == 8) ? (sym ? 25 : 24) : 20;
@@ -277,6 +278,8 @@ ReplayKernel solo_kernel_for(int key, bool sym, bool bits_ok, bool lsign_ok, boo
      : v == 25 ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 25>                  \
      : v == 30 ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 30>                  \
      : v == 31 ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 31>                  \
+     : v == 34 ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 34>                  \
+     : v == 35 ? (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 35>                  \
               : (ReplayKernel)magus_replay_solo_kernel<MagusTicker<KK, false>, kTC, kNStage, 1>)
     switch (key) {
         case 1: return SOLO_K(1);

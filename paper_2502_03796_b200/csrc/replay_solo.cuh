@@ -257,8 +257,9 @@ __device__ __forceinline__ void solo_stage_l(MagusState<K, false>* s, uint32_t* 
 }
 
 // One whole steady-state stage (8 ticks x 4 chains) of the open-loop observation model (A30; MAGUS_OSTAGE[S]_K<K>,
-// BAL 30 / 31): the L stage without throttling (A = D) plus the event word ewd (lock | flag per tick).
-template <int K, bool SYM>
+// BAL 30 / 31): the L stage without throttling (A = D) plus the event word ewd (lock | flag per tick).  BATCH
+// (MAGUS_OBSTAGE[S]_K<K>, BAL 34 / 35, 8 <= C <= 24): solo_stage_l's batched tune-flag log.
+template <int K, bool SYM, bool BATCH = false>
 __device__ __forceinline__ void solo_stage_o(MagusState<K, false>* s, uint32_t* nlk, uint32_t* wcmd, uint32_t* ewd,
                                              uint32_t& vmax, uint32_t tile, const DevPolicy& pol) {
     uint32_t e0 = s[0].evh, e1 = s[1].evh, e2 = s[2].evh, e3 = s[3].evh;
@@ -266,13 +267,22 @@ __device__ __forceinline__ void solo_stage_o(MagusState<K, false>* s, uint32_t* 
 #define OS_TAIL                                                                                                \
     e0, e1, e2, e3, s[0].cnt, s[1].cnt, s[2].cnt, s[3].cnt, nlk[0], nlk[1], nlk[2], nlk[3], wcmd[0], wcmd[1],       \
         wcmd[2], wcmd[3], ewd[0], ewd[1], ewd[2], ewd[3], vmax, tile, pol.dinc, pol.ddec, bitc, pol.one, mone
+#define OS_BTAIL OS_TAIL, (uint32_t)(pol.C - 1)
 #define OS_R2                                                                                                  \
     s[0].ring.v[0], s[0].ring.v[1], s[1].ring.v[0], s[1].ring.v[1], s[2].ring.v[0], s[2].ring.v[1], s[3].ring.v[0], \
         s[3].ring.v[1]
 #define OS_R3                                                                                                  \
     s[0].ring.v[0], s[0].ring.v[1], s[0].ring.v[2], s[1].ring.v[0], s[1].ring.v[1], s[1].ring.v[2], s[2].ring.v[0], \
         s[2].ring.v[1], s[2].ring.v[2], s[3].ring.v[0], s[3].ring.v[1], s[3].ring.v[2]
-    if constexpr (SYM) {
+    if constexpr (BATCH && SYM) {
+        if constexpr (K == 1) MAGUS_OBSTAGES_K1(s[0].ring.v[0], s[1].ring.v[0], s[2].ring.v[0], s[3].ring.v[0], OS_BTAIL);
+        else if constexpr (K == 2) MAGUS_OBSTAGES_K2(OS_R2, OS_BTAIL);
+        else MAGUS_OBSTAGES_K3(OS_R3, OS_BTAIL);
+    } else if constexpr (BATCH) {
+        if constexpr (K == 1) MAGUS_OBSTAGE_K1(s[0].ring.v[0], s[1].ring.v[0], s[2].ring.v[0], s[3].ring.v[0], OS_BTAIL);
+        else if constexpr (K == 2) MAGUS_OBSTAGE_K2(OS_R2, OS_BTAIL);
+        else MAGUS_OBSTAGE_K3(OS_R3, OS_BTAIL);
+    } else if constexpr (SYM) {
         if constexpr (K == 1) MAGUS_OSTAGES_K1(s[0].ring.v[0], s[1].ring.v[0], s[2].ring.v[0], s[3].ring.v[0], OS_TAIL);
         else if constexpr (K == 2) MAGUS_OSTAGES_K2(OS_R2, OS_TAIL);
         else MAGUS_OSTAGES_K3(OS_R3, OS_TAIL);
@@ -283,6 +293,7 @@ __device__ __forceinline__ void solo_stage_o(MagusState<K, false>* s, uint32_t* 
     }
 #undef OS_R2
 #undef OS_R3
+#undef OS_BTAIL
 #undef OS_TAIL
     s[0].evh = e0;
     s[1].evh = e1;
@@ -328,7 +339,8 @@ __device__ __forceinline__ void solo_magus_body(const CUtensorMap* tmap, const R
     float lockf[kChains], nthrf[kChains];   // counts as exact fp32 integers (segment length <= 2^24)
     uint32_t nlk[kChains];   // BAL 20: ticks not locked in the counted steady blocks (lock = lockf + 32 nsb - nlk)
     uint32_t nsb = 0;        // BAL 20: counted steady blocks
-    constexpr bool kOpen = BAL == 30 || BAL == 31;   // the open-loop stage (A30)
+    constexpr bool kOpen = BAL == 30 || BAL == 31 || BAL == 34 || BAL == 35;   // the open-loop stage (A30)
+    constexpr bool kBatchLog = (BAL >= 24 && BAL < 30) || BAL == 34 || BAL == 35;   // the batched tune-flag log
     constexpr bool kL = BAL == 20 || BAL == 21 || BAL == 24 || BAL == 25;   // the L stage (24/25: batched flag log)
     uint32_t ewd[kChains];   // open loop: event word (lock | flag per tick, the cmd word's layout)
     int32_t fev[kChains];    // open loop: first event of the segment (ticks from its start) | its cmd << 30, -1: none
@@ -394,7 +406,7 @@ __device__ __forceinline__ void solo_magus_body(const CUtensorMap* tmap, const R
 #pragma unroll
                 for (int c = 0; c < kChains; ++c) {
                     st[c].cnt -= pol.smin_sc;
-                    if constexpr (BAL >= 24 && BAL < 30)   // the batched log's count scale 2^TC (exact: C - 1 >= TC - 1)
+                    if constexpr (kBatchLog)   // the batched log's count scale 2^TC (exact: C - 1 >= TC - 1)
                         st[c].cnt = (uint32_t)((int32_t)st[c].cnt >> (pol.C - 1)) << TC;
                     wcmd[c] = T::level(st[c]);
                 }
@@ -420,7 +432,8 @@ __device__ __forceinline__ void solo_magus_body(const CUtensorMap* tmap, const R
                     solo_stage_l<T::kRingK, BAL == 21 || BAL == 25, (BAL >= 24)>(st, nlk, nthrf, wcmd, ss, vmax,
                                                                                tile + lane_off, sc, pol);
                 else if constexpr (kOpen)
-                    solo_stage_o<T::kRingK, BAL == 31>(st, nlk, wcmd, ewd, vmax, tile + lane_off, pol);
+                    solo_stage_o<T::kRingK, BAL == 31 || BAL == 35, (BAL >= 34)>(st, nlk, wcmd, ewd, vmax,
+                                                                                 tile + lane_off, pol);
                 else T::stage8(st, tile + lane_off, pol, B_lo, Blo_d, wcmd, ss, vmax);
                 __syncwarp();   // every lane's tile reads are complete before the slot is refilled
                 solo_release<TC, COMBO>(tile, tmap, bar0, empty0, slot, phase, i + NSTAGE < G.n_stages, x,
@@ -434,7 +447,7 @@ __device__ __forceinline__ void solo_magus_body(const CUtensorMap* tmap, const R
             if constexpr (kL || kOpen) {
 #pragma unroll
                 for (int c = 0; c < kChains; ++c) {
-                    if constexpr (BAL >= 24 && BAL < 30) st[c].cnt = (uint32_t)((int32_t)st[c].cnt >> TC) << (pol.C - 1);
+                    if constexpr (kBatchLog) st[c].cnt = (uint32_t)((int32_t)st[c].cnt >> TC) << (pol.C - 1);
                     st[c].cnt += pol.smin_sc;
                     T::set_level(st[c], wcmd[c] & 1u);
                 }

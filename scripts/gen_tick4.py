@@ -525,30 +525,35 @@ def build_stage_tl(TC=8):
     return out
 
 
-def build_stage_o(K, TC=8, sym=False):
+def build_stage_o(K, TC=8, sym=False, batch=False):
     """MAGUS_OSTAGE[S]_K<K>: the solo kernel's steady stage for the open-loop observation model (A30, NEXT-3): the
     observation is the recorded sample itself (A = D, never throttled), so Alg. 1's derivative, the tune flags and Alg.
     2's lock depend on the trace only and the level is a last-writer scan of the events (lock | flag).  The L stage
     (build_stage_l) without the throttle test, the select of A and the excess / throttle accounting, plus an event word
     (shifted once per stage like the cmd word, bit TC-1-tt = tick tt had lock | flag) from which the kernel takes a
     segment's first event -- the exact open-loop fix-up (post_kernels.cuh) corrects a wrong speculative entry level in
-    closed form from it, without a chain walk."""
+    closed form from it, without a chain walk.  batch=True (MAGUS_OBSTAGE[S]_K<K>): the tune-flag log of
+    build_stage_l(batch=True) (once-per-stage shift, immediate leaving-flag masks, count scaled by 2^TC)."""
     C = 4
     names = [(f"r{c}_{i}", "+d") for c in range(C) for i in range(K)] + \
             [(f"evh{c}", "+r") for c in range(C)] + [(f"cnt{c}", "+r") for c in range(C)] + \
             [(f"nlk{c}", "+r") for c in range(C)] + [(f"wcmd{c}", "+r") for c in range(C)] + \
             [(f"ewd{c}", "+r") for c in range(C)] + [("vmax", "+r")]
-    inames = [("tile", "r"), ("dinc", "d"), ("ddec", "d"), ("bitc", "r"), ("one", "r"), ("mone", "r")]
+    inames = [("tile", "r"), ("dinc", "d"), ("ddec", "d"), ("bitc", "r"), ("one", "r"), ("mone", "r")] + \
+             ([("cm1", "r")] if batch else [])
     idx = {n: f"%{i}" for i, (n, _) in enumerate(names + inames)}
     R = idx.__getitem__
     body = ["{", ".reg .pred phi<4>, pinc<4>, pev<4>, pk<4>, pq<4>, pe<4>;",
             f".reg .b32 D<{TC * C}>;", f".reg .f64 dv<4>, da<4>, ad<{TC * C}>;",
-            ".reg .b32 tb<4>, tl<4>, lv<4>;"]
+            ".reg .b32 tb<4>, tl<4>, lv<4>, eo<4>;"]
     for c in range(C):
         body.append(f"and.b32 lv{c}, {R(f'wcmd{c}')}, 1;")
         body.append(f"setp.ne.u32 phi{c}, lv{c}, 0;")                   # level = the previous tick's cmd
         body.append(f"shl.b32 {R(f'wcmd{c}')}, {R(f'wcmd{c}')}, {TC};")
         body.append(f"shl.b32 {R(f'ewd{c}')}, {R(f'ewd{c}')}, {TC};")
+        if batch:
+            body.append(f"shl.b32 {R(f'evh{c}')}, {R(f'evh{c}')}, {TC};")
+            body.append(f"shr.u32 eo{c}, {R(f'evh{c}')}, {R('cm1')};")
     for tt in range(TC):
         body.append(f"ld.shared.v4.f32 {{D{tt * C}, D{tt * C + 1}, D{tt * C + 2}, D{tt * C + 3}}}, [{R('tile')}+{tt * 512}];")
         per_chain = [
@@ -566,11 +571,18 @@ def build_stage_o(K, TC=8, sym=False):
             "and.pred pk{c}, pk{c}, phi{c};",
             "or.pred pq{c}, pk{c}, pinc{c};",                             # +1 || (f_max && !flag)
         ]) + [
+        ] + ([
+            "and.b32 tb{c}, eo{c}, {bmt};",                               # the flag leaving the C-window (<< TC-tt)
+            "@pev{c} mad.lo.u32 {evh}, {one}, {bit}, {evh};",            # the tune-flag log, bit TC-1-tt
+            "mad.lo.u32 {cnt}, tb{c}, {nk}, {cnt};",                      # window count: - leaving (x 2^tt)
+            "@pev{c} mad.lo.u32 {cnt}, {one}, {bitin}, {cnt};",           # + entering
+        ] if batch else [
             "and.b32 tb{c}, {evh}, {bitc};",                              # the flag leaving the C-window (scaled)
             "shl.b32 {evh}, {evh}, 1;",
             "@pev{c} mad.lo.u32 {evh}, {one}, {one}, {evh};",
             "mad.lo.u32 {cnt}, tb{c}, {mone}, {cnt};",                    # window count: - leaving + entering
             "@pev{c} mad.lo.u32 {cnt}, {bitc}, {one}, {cnt};",
+        ]) + [
             "setp.ge.or.s32 phi{c}, {cnt}, 0, pq{c};",                    # || lock (Alg. 2): the new level
             "setp.ge.or.s32 pe{c}, {cnt}, 0, pev{c};",                    # event: lock || flag (the level is set)
             "shr.u32 tl{c}, {cnt}, 31;",                                  # not locked
@@ -586,13 +598,14 @@ def build_stage_o(K, TC=8, sym=False):
                 body.append(tmpl.format(c=c, D=f"D{t}", ad=f"ad{t}", old=old, dinc=R("dinc"), ddec=R("ddec"),
                                         evh=R(f"evh{c}"), one=R("one"), bitc=R("bitc"), mone=R("mone"),
                                         cnt=R(f"cnt{c}"), nlk=R(f"nlk{c}"), wcmd=R(f"wcmd{c}"), ewd=R(f"ewd{c}"),
-                                        vmax=R("vmax"), bit=1 << (TC - 1 - tt)))
+                                        vmax=R("vmax"), bit=1 << (TC - 1 - tt), bmt=1 << (TC - tt), nk=-(1 << tt),
+                                        bitin=1 << TC))
     for c in range(C):
         for i in range(K):   # ring newest first: r_i = A_{t0 + TC - 1 - i}
             body.append(f"mov.f64 {R(f'r{c}_{i}')}, ad{(TC - 1 - i) * C + c};")
     body.append("}")
     params = ", ".join(n for n, _ in names + inames)
-    name = f"MAGUS_OSTAGE{'S' if sym else ''}_K{K}"
+    name = f"MAGUS_O{'B' if batch else ''}STAGE{'S' if sym else ''}_K{K}"
     out = [f"#define {name}(...) {name}_(__VA_ARGS__)", f"#define {name}_({params}) \\", "    asm volatile( \\"]
     out += [f'        "{l}\\n\\t" \\' for l in body]
     out.append("        : " + ", ".join(f'"{c}"({n})' for n, c in names) + " \\")
@@ -1160,6 +1173,8 @@ for K in (1, 2, 3):
     out += [""] + build_stage_l(K, sym=True, tdp=True, tdp_up=True, batch=True)
     out += [""] + build_stage_o(K)
     out += [""] + build_stage_o(K, sym=True)
+    out += [""] + build_stage_o(K, batch=True)
+    out += [""] + build_stage_o(K, sym=True, batch=True)
     for sym in (False, True):
         for popc in (True, False):
             for bits in (False, True):

@@ -156,21 +156,24 @@ def test_window_and_log_sizes(M, k, C, hf):
     assert np.array_equal(res.words, PA.pack_words(codes))
 
 
+@pytest.mark.parametrize("model", ["closed", "open"])
 @pytest.mark.parametrize("bal", ["24", "20"])
 @pytest.mark.parametrize("C,k,th", [(7, 1, 0.5), (8, 1, 0.5), (8, 3, 1.0), (9, 2, 0.5), (10, 1, 1.0), (16, 3, 0.5),
                                     (23, 2, 1.0), (24, 1, 0.5), (24, 3, 1.0), (25, 1, 0.5)])
-def test_batched_flag_log(M, C, k, th, bal, monkeypatch):
-    """The solo L stage with the tune-flag log shifted once per stage (BAL 24 / 25, 8 <= C <= 24, DESIGN.md
-    section 7) at both ends of its C range and just outside it (C = 7, 25: the per-tick-shift L stage), with the
-    |d| (symmetric) and the two-compare tests, against the oracle; MAGUS_SOLO_BAL=20 forces the per-tick shift."""
+def test_batched_flag_log(M, C, k, th, bal, model, monkeypatch):
+    """The solo L stage (closed loop) and O stage (open loop, A30) with the tune-flag log shifted once per stage
+    (BAL 24 / 25 and 34 / 35, 8 <= C <= 24) at both ends of its C range and just outside it
+    (C = 7, 25: the per-tick shift), with the |d| (symmetric) and the two-compare tests, against the oracle;
+    MAGUS_SOLO_BAL=20 forces the per-tick shift."""
     monkeypatch.setenv("MAGUS_SOLO_BAL", bal)
     n, ns = 140, 6000
     tr, w = gpu_gen(M, 300 + C + k, n, ns, 1, 140)
     pols = [pol(deriv_ticks=k, tune_log_capacity=C, high_freq_threshold=0.6, inc_threshold=th,
                 dec_threshold=-th if k != 2 else -0.75 * th)]
-    res = run_gpu(M, tr, w, pols, n, ns, 140, segments=5)
-    rec, codes = oracle_run(tr.cpu().numpy(), w.cpu().numpy(), pols, n)
-    PA.compare_records(res.per_trace, rec, f"batched log C={C} k={k} BAL {bal}")
+    gm = (M.Model(observe=1), O.Model(observe=1)) if model == "open" else (M.Model(), O.Model())
+    res = run_gpu(M, tr, w, pols, n, ns, 140, segments=5, model=gm[0])
+    rec, codes = oracle_run(tr.cpu().numpy(), w.cpu().numpy(), pols, n, model=gm[1])
+    PA.compare_records(res.per_trace, rec, f"batched log C={C} k={k} BAL {bal} {model}")
     assert np.array_equal(res.words, PA.pack_words(codes))
 
 
