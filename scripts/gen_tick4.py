@@ -1202,6 +1202,7 @@ for K in range(1, 9):
 for v in (True, False):
     out += [""] + build_stage_t1(v)
 out += [""] + build_stage_tl()
-path = os.path.join(os.path.dirname(__file__), "..", "paper_2502_03796_b200", "csrc", "tick4_asm.cuh")
+path = os.environ.get("MAGUS_GEN_OUT") or \
+    os.path.join(os.path.dirname(__file__), "..", "paper_2502_03796_b200", "csrc", "tick4_asm.cuh")
 open(path, "w").write("\n".join(out) + "\n")
 print("wrote", os.path.normpath(path))

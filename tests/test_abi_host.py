@@ -49,6 +49,25 @@ def test_sass_has_tma_and_no_fp64_division():
         assert "MUFU.RCP64H" not in f and "DMUL" not in f
 
 
+def test_generated_stage_macros_in_sync(tmp_path):
+    """csrc/tick4_asm.cuh (the generated PTX stage blocks) is exactly what scripts/gen_tick4.py writes now."""
+    out = tmp_path / "tick4_asm.cuh"
+    subprocess.run(["python", os.path.join(ROOT, "scripts", "gen_tick4.py")], check=True, capture_output=True,
+                   env={**os.environ, "MAGUS_GEN_OUT": str(out)})
+    committed = open(os.path.join(ROOT, "paper_2502_03796_b200", "csrc", "tick4_asm.cuh")).read()
+    assert out.read_text() == committed, "run python scripts/gen_tick4.py and rebuild"
+
+
+def test_solo_batched_log_variants_in_library():
+    """The default solo stage variants (BAL 24 / 25: the batched tune-flag log; 34 / 35 in open loop) and the fused
+    kernel's batched-log build (LB) are compiled into the library for every register ring k <= 3."""
+    sass = subprocess.run(["cuobjdump", "-res-usage", M.LIB_PATH], capture_output=True, text=True).stdout
+    for k in (1, 2, 3):
+        for bal in (24, 25, 34, 35):
+            assert f"magus_replay_solo_kernelINS_11MagusTickerILi{k}ELb0EEELi8ELi3ELi{bal}EEE" in sass, (k, bal)
+        assert f"magus_replay_fused_kernelINS_11MagusTickerILi{k}ELb0EEELi8ELi3ELb1ELi12ELb1ELb1EEE" in sass, k
+
+
 def test_no_cuda_device_means_error_not_fallback():
     try:
         import torch
